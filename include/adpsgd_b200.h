@@ -1,0 +1,168 @@
+/*
+ * adpsgd_b200.h — C ABI of the B200-native ADPSGD learner step.
+ *
+ * Drop-in boundary for the reference's per-learner step API
+ * (/root/reference/proj/include/adpsgd/engine.hpp:85-105) and its loss/gradient
+ * plugin (/root/reference/proj/include/adpsgd/objectives.hpp:45-69). Plain pointers
+ * and sizes only; every entry point returns an adpsgd_status that the C++/Python
+ * shims map 1:1 onto the reference's exception types (errors.hpp:9-46).
+ *
+ * Implemented by libadpsgd_b200.so (paper_2110_11199_b200/csrc), sm_100a only.
+ */
+#ifndef ADPSGD_B200_H
+#define ADPSGD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* errors.hpp:9-46, in declaration order; CUDA/NCCL failures are additional. */
+typedef enum adpsgd_status {
+    ADPSGD_OK = 0,
+    ADPSGD_E_INVALID_ORDER = 1,       /* InvalidOrderError      (mixing.cpp:36-39, 81-84) */
+    ADPSGD_E_DIMENSION = 2,           /* DimensionError         (engine.cpp:158-160)      */
+    ADPSGD_E_OUT_OF_REGIME = 3,       /* OutOfRegimeError                                 */
+    ADPSGD_E_NUMERICAL = 4,           /* NumericalError                                   */
+    ADPSGD_E_SYNC_VIOLATION = 5,      /* SyncViolationError     (engine.cpp:139-144)      */
+    ADPSGD_E_STALENESS_OVERFLOW = 6,  /* StalenessOverflowError (engine.cpp:90-96)        */
+    ADPSGD_E_INVALID_STATE = 7,       /* InvalidStateError      (objectives.cpp:240-241)  */
+    ADPSGD_E_CONFIG = 8,              /* ConfigError            (engine.cpp:60-77)        */
+    ADPSGD_E_CUDA = 9,
+    ADPSGD_E_NCCL = 10
+} adpsgd_status;
+
+/* engine.hpp:17 — Strategy enum, same order. */
+typedef enum adpsgd_strategy {
+    ADPSGD_SDPSGD = 0,
+    ADPSGD_FM = 1,
+    ADPSGD_RM = 2,
+    ADPSGD_D1D = 3,
+    ADPSGD_GENERIC = 4
+} adpsgd_strategy;
+
+/* mixing.hpp:13 — MixKind (generic-staleness mixing matrix). */
+typedef enum adpsgd_mix_kind { ADPSGD_MIX_FIXED = 0, ADPSGD_MIX_RANDOM = 1, ADPSGD_MIX_UNIFORM = 2 } adpsgd_mix_kind;
+
+/* GEMM operand precision of the learner step. FP32 = SIMT fp32 GEMMs (parity mode);
+ * BF16 = tcgen05 bf16 x bf16 -> fp32 (TMEM) GEMMs. Master weights, cell state, gate
+ * activations, the update and the mixing are fp32 in both modes. */
+typedef enum adpsgd_precision { ADPSGD_PREC_FP32 = 0, ADPSGD_PREC_BF16 = 1 } adpsgd_precision;
+
+/* BLSTM acoustic model. proj = 0 means no projection layer. */
+typedef struct adpsgd_model_desc {
+    int32_t layers;
+    int32_t hidden;        /* cells per direction */
+    int32_t bidirectional; /* 0 or 1 */
+    int32_t input_dim;
+    int32_t proj;
+    int32_t classes;
+    int32_t unroll;        /* T, frames per segment */
+} adpsgd_model_desc;
+
+typedef struct adpsgd_config {
+    adpsgd_model_desc model;
+    int32_t precision;        /* adpsgd_precision */
+    int32_t strategy;         /* adpsgd_strategy (engine.hpp:36) */
+    int32_t learners;         /* global L (engine.hpp:37) */
+    int32_t first_learner;    /* global id of this context's first learner */
+    int32_t local_learners;   /* learners hosted by this context (same device) */
+    int32_t batch;            /* M segments per learner per step (engine.hpp:38) */
+    int32_t device;
+    int32_t generic_mix;      /* adpsgd_mix_kind, GENERIC only */
+    int32_t staleness_cap;    /* GENERIC only (engine.hpp:44) */
+    uint64_t seed;            /* run seed (engine.hpp:41) */
+} adpsgd_config;
+
+typedef struct adpsgd_perf {
+    double last_step_ms;      /* device time of the last step (CUDA events) */
+    double last_mix_ms;       /* device time of the mixing/update phase */
+    double gossip_bytes;      /* bytes pulled from neighbours in the last step */
+    int64_t steps;            /* global iteration counter k */
+    int64_t kernel_launches;  /* this library's kernel launches so far */
+} adpsgd_perf;
+
+typedef struct adpsgd_ctx adpsgd_ctx;
+
+/* ---- pure host helpers (bit-exact with rng.hpp / mixing.cpp / engine.cpp) ---- */
+int64_t adpsgd_param_count(const adpsgd_model_desc* m);
+/* engine.cpp:130-134 — mapping[L] for iteration k. */
+int adpsgd_permutation_for_iteration(uint64_t seed, int32_t learners, int64_t k, int32_t* mapping);
+/* (left, right) of every learner for FM (l±1) or RM (chronos.cpp:224-235): left_right[2*l+{0,1}]. */
+int adpsgd_pairing(int32_t strategy, uint64_t seed, int32_t learners, int64_t k, int32_t* mapping,
+                   int32_t* left_right);
+double adpsgd_lr_at(double base_lr, double peak_lr, int32_t warmup_epochs, double anneal_factor,
+                    int32_t anneal_start_epoch, int32_t epoch);
+const char* adpsgd_last_error(void);
+const char* adpsgd_build_info(void);
+
+/* ---- context lifecycle ---- */
+int adpsgd_ctx_create(const adpsgd_config* cfg, adpsgd_ctx** out);
+int adpsgd_ctx_destroy(adpsgd_ctx* ctx);
+/* Device-resident dataset: feats [n_seg][T][input_dim] fp32, labels [n_seg][T] int32.
+ * Segments [0, train_count) are the training split (objectives.hpp:24-32). */
+int adpsgd_set_dataset(adpsgd_ctx* ctx, const float* feats, const int32_t* labels, int32_t n_seg,
+                       int32_t train_count);
+/* Deterministic synthetic SWB-shaped dataset generated on the device. */
+int adpsgd_synth_dataset(adpsgd_ctx* ctx, int32_t n_seg, int32_t train_count, uint64_t seed);
+int adpsgd_get_dataset(adpsgd_ctx* ctx, float* feats, int32_t* labels);
+/* fp64 host mirrors of learner weights (init_learners, engine.cpp:99-116, runs at create). */
+int adpsgd_set_weights(adpsgd_ctx* ctx, int32_t local_learner, const double* w, int64_t n);
+int adpsgd_get_weights(adpsgd_ctx* ctx, int32_t local_learner, double* w, int64_t n);
+
+/* ---- the per-learner step ---- */
+/* One iteration k of cfg.strategy for every local learner: sample M segments from the
+ * learner's stream (engine.cpp:17-21), BLSTM forward/backward on the device, then the
+ * mixing+update (engine.cpp:136-204). loss_out[local_learners] = batch-mean CE (nullable).
+ * taus (GENERIC) = per-global-learner staleness, nullable. */
+int adpsgd_step(adpsgd_ctx* ctx, double lr, const int32_t* taus, float* loss_out);
+/* Same step, batch supplied by the caller in HOST memory: feats [local][M][T][input_dim],
+ * labels [local][M][T]; copied H2D inside (the end-to-end path). */
+int adpsgd_step_host_batch(adpsgd_ctx* ctx, double lr, const float* feats, const int32_t* labels,
+                           float* loss_out);
+/* Gradient-injection step: grads [local_learners][D] fp64 replace the LSTM gradient. */
+int adpsgd_step_injected(adpsgd_ctx* ctx, double lr, const int32_t* taus, const double* grads);
+/* Objective::gradient adapter (objectives.hpp:50-51): loss and gradient at w over the
+ * given segment indices, computed on the device; does not touch learner state. */
+int adpsgd_gradient(adpsgd_ctx* ctx, const double* w, const int32_t* idx, int32_t M, double* g_out,
+                    double* loss_out);
+/* Straggler hook (chronos.cpp:51-58): local learner's step is stretched by factor >= 1
+ * with a device-side delay of (factor-1) x its measured compute time. */
+int adpsgd_set_straggler(adpsgd_ctx* ctx, int32_t local_learner, double factor);
+int adpsgd_get_stats(adpsgd_ctx* ctx, adpsgd_perf* out);
+int64_t adpsgd_iteration(adpsgd_ctx* ctx);
+int adpsgd_set_iteration(adpsgd_ctx* ctx, int64_t k);
+/* Consensus distance ||W (I - 11^T/L)||_2 over the local learners (mixing.cpp:159-180). */
+int adpsgd_consensus_distance(adpsgd_ctx* ctx, double* out);
+
+/* ---- multi-process (one process per GPU) ---- */
+/* NCCL communicator over all ranks; nccl_id = 128-byte ncclUniqueId from rank 0. */
+int adpsgd_nccl_unique_id(void* out128);
+int adpsgd_comm_init(adpsgd_ctx* ctx, int32_t rank, int32_t world, const void* nccl_id128);
+/* CUDA IPC handles of this context's weight buffers, for peer (NVLink P2P) gossip pulls. */
+int64_t adpsgd_ipc_handle_size(adpsgd_ctx* ctx);
+int adpsgd_export_ipc(adpsgd_ctx* ctx, void* out, int64_t size);
+int adpsgd_import_ipc(adpsgd_ctx* ctx, int32_t rank, int32_t rank_first_learner,
+                      int32_t rank_local_learners, const void* handles, int64_t size);
+/* Gossip transport for FM/RM: 0 = direct peer loads inside the fused mix kernel,
+ * 1 = copy-engine prefetch overlapped with compute, 2 = NCCL send/recv (baseline). */
+int adpsgd_set_gossip_mode(adpsgd_ctx* ctx, int32_t mode);
+int adpsgd_barrier(adpsgd_ctx* ctx);
+
+/* ---- kernel-level entry points (tests / benchmarks; device pointers) ---- */
+/* C[M,N] = alpha * sum_k A(m,k) B(n,k) (+ C if accumulate) (+ bias[n]).
+ * A(m,k) = a_mn ? A[k*lda+m] : A[m*lda+k]; B likewise. bf16 = 1: A,B bf16, tcgen05;
+ * bf16 = 0: fp32 SIMT. c_bf16 selects the output type. */
+int adpsgd_gemm(int32_t bf16, int32_t M, int32_t N, int32_t K, const void* A, int64_t lda, int32_t a_mn,
+                const void* B, int64_t ldb, int32_t b_mn, void* Cout, int64_t ldc, int32_t c_bf16,
+                float alpha, int32_t accumulate, const float* bias, void* stream);
+/* w_out = (w_self + w_left + w_right)/3 - lr*g, also writes a bf16 shadow (nullable). */
+int adpsgd_mix_update(int64_t n, const float* w_self, const float* w_left, const float* w_right,
+                      const float* g, float lr, float* w_out, void* shadow_bf16, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ADPSGD_B200_H */

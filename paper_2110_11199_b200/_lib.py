@@ -1,0 +1,107 @@
+"""ctypes binding of libadpsgd_b200.so (the C ABI declared in include/adpsgd_b200.h).
+
+There is no fallback: if the CUDA library is missing this module raises on load.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+
+from .errors import raise_for
+
+PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG_DIR)
+LIB_PATH = os.path.join(PKG_DIR, "libadpsgd_b200.so")
+HEADER = os.path.join(ROOT, "include", "adpsgd_b200.h")
+
+u64, i64, i32 = C.c_uint64, C.c_int64, C.c_int32
+P = C.POINTER
+
+
+class ModelDesc(C.Structure):
+    _fields_ = [(n, i32) for n in
+                ("layers", "hidden", "bidirectional", "input_dim", "proj", "classes", "unroll")]
+
+
+class Config(C.Structure):
+    _fields_ = [("model", ModelDesc), ("precision", i32), ("strategy", i32), ("learners", i32),
+                ("first_learner", i32), ("local_learners", i32), ("batch", i32), ("device", i32),
+                ("generic_mix", i32), ("staleness_cap", i32), ("seed", u64)]
+
+
+class Perf(C.Structure):
+    _fields_ = [("last_step_ms", C.c_double), ("last_mix_ms", C.c_double), ("gossip_bytes", C.c_double),
+                ("steps", i64), ("kernel_launches", i64)]
+
+
+_SIGS = {
+    "adpsgd_param_count": (i64, [P(ModelDesc)]),
+    "adpsgd_permutation_for_iteration": (C.c_int, [u64, i32, i64, P(i32)]),
+    "adpsgd_pairing": (C.c_int, [i32, u64, i32, i64, P(i32), P(i32)]),
+    "adpsgd_lr_at": (C.c_double, [C.c_double, C.c_double, i32, C.c_double, i32, i32]),
+    "adpsgd_last_error": (C.c_char_p, []),
+    "adpsgd_build_info": (C.c_char_p, []),
+    "adpsgd_ctx_create": (C.c_int, [P(Config), P(C.c_void_p)]),
+    "adpsgd_ctx_destroy": (C.c_int, [C.c_void_p]),
+    "adpsgd_set_dataset": (C.c_int, [C.c_void_p, P(C.c_float), P(i32), i32, i32]),
+    "adpsgd_synth_dataset": (C.c_int, [C.c_void_p, i32, i32, u64]),
+    "adpsgd_get_dataset": (C.c_int, [C.c_void_p, P(C.c_float), P(i32)]),
+    "adpsgd_set_weights": (C.c_int, [C.c_void_p, i32, P(C.c_double), i64]),
+    "adpsgd_get_weights": (C.c_int, [C.c_void_p, i32, P(C.c_double), i64]),
+    "adpsgd_step": (C.c_int, [C.c_void_p, C.c_double, P(i32), P(C.c_float)]),
+    "adpsgd_step_host_batch": (C.c_int, [C.c_void_p, C.c_double, P(C.c_float), P(i32), P(C.c_float)]),
+    "adpsgd_step_injected": (C.c_int, [C.c_void_p, C.c_double, P(i32), P(C.c_double)]),
+    "adpsgd_gradient": (C.c_int, [C.c_void_p, P(C.c_double), P(i32), i32, P(C.c_double), P(C.c_double)]),
+    "adpsgd_set_straggler": (C.c_int, [C.c_void_p, i32, C.c_double]),
+    "adpsgd_get_stats": (C.c_int, [C.c_void_p, P(Perf)]),
+    "adpsgd_iteration": (i64, [C.c_void_p]),
+    "adpsgd_set_iteration": (C.c_int, [C.c_void_p, i64]),
+    "adpsgd_consensus_distance": (C.c_int, [C.c_void_p, P(C.c_double)]),
+    "adpsgd_nccl_unique_id": (C.c_int, [C.c_void_p]),
+    "adpsgd_comm_init": (C.c_int, [C.c_void_p, i32, i32, C.c_void_p]),
+    "adpsgd_ipc_handle_size": (i64, [C.c_void_p]),
+    "adpsgd_export_ipc": (C.c_int, [C.c_void_p, C.c_void_p, i64]),
+    "adpsgd_import_ipc": (C.c_int, [C.c_void_p, i32, i32, i32, C.c_void_p, i64]),
+    "adpsgd_set_gossip_mode": (C.c_int, [C.c_void_p, i32]),
+    "adpsgd_barrier": (C.c_int, [C.c_void_p]),
+    "adpsgd_gemm": (C.c_int, [i32, i32, i32, i32, C.c_void_p, i64, i32, C.c_void_p, i64, i32, C.c_void_p, i64,
+                              i32, C.c_float, i32, C.c_void_p, C.c_void_p]),
+    "adpsgd_mix_update": (C.c_int, [i64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_float, C.c_void_p,
+                                    C.c_void_p, C.c_void_p]),
+}
+
+_LIB = None
+
+
+def header_symbols() -> list[str]:
+    """Every function the public header declares."""
+    with open(HEADER) as f:
+        text = f.read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[a-z0-9_]+\s*\**\s*(adpsgd_[a-z0-9_]+)\s*\(", text, flags=re.M)))
+
+
+def lib() -> C.CDLL:
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                              "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _LIB = L
+    return _LIB
+
+
+def last_error() -> str:
+    msg = lib().adpsgd_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        raise_for(rc, last_error())

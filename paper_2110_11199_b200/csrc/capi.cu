@@ -1,0 +1,340 @@
+// extern "C" boundary (include/adpsgd_b200.h). Every entry point converts library
+// exceptions into adpsgd_status codes and records the message for adpsgd_last_error().
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "adpsgd_b200.h"
+#include "comm.hpp"
+#include "engine.hpp"
+#include "gemm.hpp"
+#include "kernels.cuh"
+#include "rng.hpp"
+
+using namespace ab;
+
+struct adpsgd_ctx {
+    ab::Ctx* impl;
+};
+
+namespace {
+template <typename F>
+int guard(F&& f) {
+    try {
+        f();
+        return ADPSGD_OK;
+    } catch (const ab::Error& e) {
+        set_last_error(e.what());
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        set_last_error("host allocation failed");
+        return ADPSGD_E_CUDA;
+    } catch (const std::exception& e) {
+        set_last_error(e.what());
+        return ADPSGD_E_INVALID_STATE;
+    }
+}
+Ctx& C_(adpsgd_ctx* c) {
+    AB_CHECK(c && c->impl, ADPSGD_E_INVALID_STATE, "null context");
+    return *c->impl;
+}
+}  // namespace
+
+extern "C" {
+
+int64_t adpsgd_param_count(const adpsgd_model_desc* m) { return m ? make_layout(*m).total : -1; }
+
+int adpsgd_permutation_for_iteration(uint64_t seed, int32_t L, int64_t k, int32_t* mapping) {
+    return guard([&] {
+        AB_CHECK(L >= 1, ADPSGD_E_INVALID_ORDER, "permutation requires order >= 1");  // mixing.cpp:65-68
+        permutation_for_iteration(seed, L, k, mapping);
+    });
+}
+
+int adpsgd_pairing(int32_t strategy, uint64_t seed, int32_t L, int64_t k, int32_t* mapping, int32_t* lr) {
+    return guard([&] {
+        AB_CHECK(L >= 3, ADPSGD_E_INVALID_ORDER, "ring pairing requires order >= 3");  // mixing.cpp:36-39
+        std::vector<int32_t> map(L);
+        if (strategy == ADPSGD_RM) permutation_for_iteration(seed, L, k, map.data());
+        else for (int i = 0; i < L; ++i) map[i] = i;
+        if (mapping) std::memcpy(mapping, map.data(), sizeof(int32_t) * L);
+        // learner map[a] sits at ring position a (mixing.cpp:97-101, chronos.cpp:229-234)
+        for (int a = 0; a < L; ++a) {
+            const int l = map[a];
+            lr[2 * l] = map[(a + L - 1) % L];
+            lr[2 * l + 1] = map[(a + 1) % L];
+        }
+    });
+}
+
+double adpsgd_lr_at(double base, double peak, int32_t warmup, double anneal_factor, int32_t anneal_start, int32_t epoch) {
+    // engine.cpp:45-58
+    if (epoch < 0) return -1.0;
+    double lr = (warmup > 0 && epoch < warmup) ? base + (peak - base) * static_cast<double>(epoch) / warmup : peak;
+    if (epoch >= anneal_start) lr = peak * std::pow(anneal_factor, epoch - anneal_start);
+    return lr;
+}
+
+const char* adpsgd_last_error(void) { return last_error(); }
+
+const char* adpsgd_build_info(void) {
+    return "libadpsgd_b200: sm_100a; tcgen05/TMA/TMEM bf16 GEMM + fp32 SIMT parity GEMM; NCCL via dlopen";
+}
+
+int adpsgd_ctx_create(const adpsgd_config* cfg, adpsgd_ctx** out) {
+    return guard([&] {
+        AB_CHECK(cfg && out, ADPSGD_E_CONFIG, "null argument");
+        *out = nullptr;
+        auto* c = new adpsgd_ctx{nullptr};
+        try {
+            c->impl = new Ctx(*cfg);
+        } catch (...) {
+            delete c;
+            throw;
+        }
+        *out = c;
+    });
+}
+
+int adpsgd_ctx_destroy(adpsgd_ctx* ctx) {
+    return guard([&] {
+        if (!ctx) return;
+        delete ctx->impl;
+        delete ctx;
+    });
+}
+
+int adpsgd_set_dataset(adpsgd_ctx* ctx, const float* feats, const int32_t* labels, int32_t n_seg, int32_t train_count) {
+    return guard([&] {
+        Ctx& c = C_(ctx);
+        AB_CHECK(n_seg >= 1 && train_count >= 1 && train_count <= n_seg, ADPSGD_E_INVALID_STATE,
+                 "dataset has no training samples");
+        AB_CUDA(cudaSetDevice(c.cfg.device));
+        const size_t nf = static_cast<size_t>(n_seg) * c.T * c.I;
+        if (c.n_seg < n_seg) {
+            c.feats = static_cast<float*>(c.alloc(nf * sizeof(float)));
+            c.labels = static_cast<int32_t*>(c.alloc(static_cast<size_t>(n_seg) * c.T * sizeof(int32_t)));
+        }
+        AB_CUDA(cudaMemcpy(c.feats, feats, nf * sizeof(float), cudaMemcpyHostToDevice));
+        AB_CUDA(cudaMemcpy(c.labels, labels, static_cast<size_t>(n_seg) * c.T * sizeof(int32_t), cudaMemcpyHostToDevice));
+        c.n_seg = n_seg;
+        c.train_count = train_count;
+    });
+}
+
+int adpsgd_synth_dataset(adpsgd_ctx* ctx, int32_t n_seg, int32_t train_count, uint64_t seed) {
+    return guard([&] {
+        Ctx& c = C_(ctx);
+        AB_CHECK(n_seg >= 1 && train_count >= 1 && train_count <= n_seg, ADPSGD_E_INVALID_STATE,
+                 "dataset has no training samples");
+        AB_CUDA(cudaSetDevice(c.cfg.device));
+        if (c.n_seg < n_seg) {
+            c.feats = static_cast<float*>(c.alloc(static_cast<size_t>(n_seg) * c.T * c.I * sizeof(float)));
+            c.labels = static_cast<int32_t*>(c.alloc(static_cast<size_t>(n_seg) * c.T * sizeof(int32_t)));
+        }
+        launch_synth(c.feats, c.labels, n_seg, c.T, c.I, c.lay.C, seed, c.s_main);
+        AB_CUDA(cudaStreamSynchronize(c.s_main));
+        c.n_seg = n_seg;
+        c.train_count = train_count;
+    });
+}
+
+int adpsgd_get_dataset(adpsgd_ctx* ctx, float* feats, int32_t* labels) {
+    return guard([&] {
+        Ctx& c = C_(ctx);
+        AB_CHECK(c.feats, ADPSGD_E_INVALID_STATE, "no dataset");
+        AB_CUDA(cudaMemcpy(feats, c.feats, static_cast<size_t>(c.n_seg) * c.T * c.I * sizeof(float), cudaMemcpyDeviceToHost));
+        AB_CUDA(cudaMemcpy(labels, c.labels, static_cast<size_t>(c.n_seg) * c.T * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    });
+}
+
+int adpsgd_set_weights(adpsgd_ctx* ctx, int32_t j, const double* w, int64_t n) {
+    return guard([&] {
+        Ctx& c = C_(ctx);
+        AB_CHECK(j >= 0 && j < c.cfg.local_learners, ADPSGD_E_DIMENSION, "local learner out of range");
+        AB_CHECK(n == c.D, ADPSGD_E_DIMENSION, "weight vector length != parameter count");
+        AB_CUDA(cudaSetDevice(c.cfg.device));
+        std::vector<float> f(w, w + n);
+        Learner& ln = c.learners[j];
+        const int cur = static_cast<int>(c.k & 1);
+        AB_CUDA(cudaMemcpy(ln.w[cur], f.data(), n * sizeof(float), cudaMemcpyHostToDevice));
+        c.refresh_shadow(ln, ln.w[cur], c.s_main);
+        AB_CUDA(cudaStreamSynchronize(c.s_main));
+    });
+}
+
+int adpsgd_get_weights(adpsgd_ctx* ctx, int32_t j, double* w, int64_t n) {
+    return guard([&] {
+        Ctx& c = C_(ctx);
+        AB_CHECK(j >= 0 && j < c.cfg.local_learners, ADPSGD_E_DIMENSION, "local learner out of range");
+        AB_CHECK(n == c.D, ADPSGD_E_DIMENSION, "weight vector length != parameter count");
+        AB_CUDA(cudaSetDevice(c.cfg.device));
+        std::vector<float> f(n);
+        AB_CUDA(cudaStreamSynchronize(c.s_main));
+        AB_CUDA(cudaMemcpy(f.data(), c.learners[j].w[c.k & 1], n * sizeof(float), cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < n; ++i) w[i] = f[i];
+    });
+}
+
+int adpsgd_step(adpsgd_ctx* ctx, double lr, const int32_t* taus, float* loss_out) {
+    return guard([&] { C_(ctx).step(lr, taus, loss_out, nullptr, nullptr, nullptr); });
+}
+
+int adpsgd_step_host_batch(adpsgd_ctx* ctx, double lr, const float* feats, const int32_t* labels, float* loss_out) {
+    return guard([&] {
+        AB_CHECK(feats && labels, ADPSGD_E_INVALID_STATE, "null host batch");
+        C_(ctx).step(lr, nullptr, loss_out, feats, labels, nullptr);
+    });
+}
+
+int adpsgd_step_injected(adpsgd_ctx* ctx, double lr, const int32_t* taus, const double* grads) {
+    return guard([&] {
+        AB_CHECK(grads, ADPSGD_E_INVALID_STATE, "null gradients");
+        C_(ctx).step(lr, taus, nullptr, nullptr, nullptr, grads);
+    });
+}
+
+int adpsgd_gradient(adpsgd_ctx* ctx, const double* w, const int32_t* idx, int32_t M, double* g_out, double* loss_out) {
+    return guard([&] {
+        double l = C_(ctx).gradient(w, idx, M, g_out);
+        if (loss_out) *loss_out = l;
+    });
+}
+
+int adpsgd_set_straggler(adpsgd_ctx* ctx, int32_t j, double factor) {
+    return guard([&] {
+        Ctx& c = C_(ctx);
+        AB_CHECK(j >= 0 && j < c.cfg.local_learners, ADPSGD_E_CONFIG, "straggler learner_id out of range");
+        AB_CHECK(factor >= 1.0, ADPSGD_E_CONFIG, "slowdown factor must be >= 1");  // chronos.cpp:47
+        c.learners[j].straggle = factor;
+    });
+}
+
+int adpsgd_get_stats(adpsgd_ctx* ctx, adpsgd_perf* out) {
+    return guard([&] {
+        Ctx& c = C_(ctx);
+        out->last_step_ms = c.last_step_ms;
+        out->last_mix_ms = c.last_mix_ms;
+        out->gossip_bytes = c.last_gossip_bytes;
+        out->steps = c.k;
+        out->kernel_launches = g_launch_count;
+    });
+}
+
+int64_t adpsgd_iteration(adpsgd_ctx* ctx) { return ctx && ctx->impl ? ctx->impl->k : -1; }
+
+int adpsgd_set_iteration(adpsgd_ctx* ctx, int64_t k) {
+    return guard([&] {
+        Ctx& c = C_(ctx);
+        AB_CHECK(k >= 0, ADPSGD_E_INVALID_STATE, "iteration must be >= 0");
+        AB_CHECK(((k ^ c.k) & 1) == 0, ADPSGD_E_INVALID_STATE, "iteration parity must be preserved");
+        c.k = k;
+    });
+}
+
+int adpsgd_consensus_distance(adpsgd_ctx* ctx, double* out) {
+    return guard([&] {
+        // mixing.cpp:159-180: ||W (I - 11^T/L)||_2 = sqrt(lambda_max(G_c)), G_c the centred Gram of the columns.
+        Ctx& c = C_(ctx);
+        const int L = c.cfg.local_learners;
+        std::vector<std::vector<float>> W(L, std::vector<float>(c.D));
+        AB_CUDA(cudaStreamSynchronize(c.s_main));
+        for (int j = 0; j < L; ++j)
+            AB_CUDA(cudaMemcpy(W[j].data(), c.learners[j].w[c.k & 1], c.D * sizeof(float), cudaMemcpyDeviceToHost));
+        std::vector<double> G(static_cast<size_t>(L) * L, 0.0);
+        std::vector<double> mean(c.D, 0.0);
+        for (int j = 0; j < L; ++j) for (int64_t p = 0; p < c.D; ++p) mean[p] += W[j][p];
+        for (int64_t p = 0; p < c.D; ++p) mean[p] /= L;
+        for (int a = 0; a < L; ++a)
+            for (int b = a; b < L; ++b) {
+                double s = 0;
+                for (int64_t p = 0; p < c.D; ++p) s += (W[a][p] - mean[p]) * (W[b][p] - mean[p]);
+                G[a * L + b] = G[b * L + a] = s;
+            }
+        // power iteration on the PSD Gram
+        std::vector<double> v(L, 1.0), u(L);
+        double lam = 0;
+        for (int it = 0; it < 500; ++it) {
+            double nrm = 0;
+            for (int a = 0; a < L; ++a) { u[a] = 0; for (int b = 0; b < L; ++b) u[a] += G[a * L + b] * v[b]; nrm += u[a] * u[a]; }
+            nrm = std::sqrt(nrm);
+            if (nrm == 0) { lam = 0; break; }
+            for (int a = 0; a < L; ++a) v[a] = u[a] / nrm;
+            lam = nrm;
+        }
+        *out = std::sqrt(std::max(0.0, lam));
+    });
+}
+
+int adpsgd_nccl_unique_id(void* out128) { return guard([&] { Comm::unique_id(out128); }); }
+
+int adpsgd_comm_init(adpsgd_ctx* ctx, int32_t rank, int32_t world, const void* id) {
+    return guard([&] {
+        Ctx& c = C_(ctx);
+        AB_CUDA(cudaSetDevice(c.cfg.device));
+        c.comm = std::make_unique<Comm>(c, rank, world, id);
+    });
+}
+
+int64_t adpsgd_ipc_handle_size(adpsgd_ctx* ctx) {
+    return ctx && ctx->impl ? static_cast<int64_t>(ctx->impl->cfg.local_learners) * 2 * sizeof(cudaIpcMemHandle_t) : -1;
+}
+
+int adpsgd_export_ipc(adpsgd_ctx* ctx, void* out, int64_t size) {
+    return guard([&] {
+        Ctx& c = C_(ctx);
+        AB_CHECK(c.comm, ADPSGD_E_INVALID_STATE, "adpsgd_comm_init first");
+        c.comm->export_ipc(c, out, size);
+    });
+}
+
+int adpsgd_import_ipc(adpsgd_ctx* ctx, int32_t rank, int32_t first, int32_t count, const void* h, int64_t size) {
+    return guard([&] {
+        Ctx& c = C_(ctx);
+        AB_CHECK(c.comm, ADPSGD_E_INVALID_STATE, "adpsgd_comm_init first");
+        AB_CUDA(cudaSetDevice(c.cfg.device));
+        c.comm->import_ipc(rank, first, count, h, size);
+    });
+}
+
+int adpsgd_set_gossip_mode(adpsgd_ctx* ctx, int32_t mode) {
+    return guard([&] {
+        Ctx& c = C_(ctx);
+        AB_CHECK(mode >= 0 && mode <= 2, ADPSGD_E_CONFIG, "gossip mode must be 0, 1 or 2");
+        AB_CHECK(c.comm, ADPSGD_E_INVALID_STATE, "adpsgd_comm_init first");
+        c.comm->gossip_mode = mode;
+    });
+}
+
+int adpsgd_barrier(adpsgd_ctx* ctx) {
+    return guard([&] {
+        Ctx& c = C_(ctx);
+        if (!c.comm) return;
+        c.comm->barrier(c.s_main);
+        AB_CUDA(cudaStreamSynchronize(c.s_main));
+    });
+}
+
+int adpsgd_gemm(int32_t bf, int32_t M, int32_t N, int32_t K, const void* A, int64_t lda, int32_t a_mn, const void* B,
+                int64_t ldb, int32_t b_mn, void* Cout, int64_t ldc, int32_t c_bf16, float alpha, int32_t accumulate,
+                const float* bias, void* stream) {
+    return guard([&] {
+        GemmArgs g;
+        g.M = M; g.N = N;
+        g.seg[0].a = {A, lda, a_mn != 0};
+        g.seg[0].b = {B, ldb, b_mn != 0};
+        g.seg[0].K = K;
+        g.C = Cout; g.ldc = ldc; g.c_bf16 = c_bf16 != 0;
+        g.alpha = alpha; g.accumulate = accumulate != 0; g.bias = bias;
+        gemm(bf != 0, g, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int adpsgd_mix_update(int64_t n, const float* w, const float* wl, const float* wr, const float* g, float lr, float* out,
+                      void* shadow, void* stream) {
+    return guard([&] {
+        launch_mix3(n, w, wl, wr, g, lr, out, static_cast<bf16*>(shadow), static_cast<cudaStream_t>(stream));
+    });
+}
+
+}  // extern "C"

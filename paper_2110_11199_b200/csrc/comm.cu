@@ -1,0 +1,162 @@
+// NCCL + CUDA-IPC transport (see comm.hpp). NCCL is resolved with dlopen so the
+// library shares whichever libnccl.so.2 the process already loaded (torch's).
+#include "comm.hpp"
+
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "engine.hpp"
+
+namespace ab {
+
+namespace {
+
+struct NcclApi {
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+    static NcclApi api;
+    static std::once_flag once;
+    static std::string err;
+    std::call_once(once, [] {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) { err = dlerror() ? dlerror() : "dlopen libnccl failed"; return; }
+        api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+        api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+        api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+        api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(dlsym(h, "ncclAllReduce"));
+        api.Send = reinterpret_cast<decltype(api.Send)>(dlsym(h, "ncclSend"));
+        api.Recv = reinterpret_cast<decltype(api.Recv)>(dlsym(h, "ncclRecv"));
+        api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(dlsym(h, "ncclGroupStart"));
+        api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(dlsym(h, "ncclGroupEnd"));
+        api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+    });
+    AB_CHECK(api.AllReduce && api.CommInitRank, ADPSGD_E_NCCL, "NCCL unavailable: " + err);
+    return api;
+}
+
+#define AB_NCCL(x)                                                                                     \
+    do {                                                                                               \
+        ncclResult_t r_ = (x);                                                                         \
+        if (r_ != ncclSuccess)                                                                         \
+            throw ::ab::Error(ADPSGD_E_NCCL, std::string(#x) + ": " +                                  \
+                                                 (nccl().GetErrorString ? nccl().GetErrorString(r_) : "")); \
+    } while (0)
+
+constexpr int kHandle = static_cast<int>(sizeof(cudaIpcMemHandle_t));
+
+}  // namespace
+
+void Comm::unique_id(void* out128) {
+    ncclUniqueId id;
+    AB_NCCL(nccl().GetUniqueId(&id));
+    std::memcpy(out128, &id, sizeof(id));
+}
+
+Comm::Comm(Ctx& c, int r, int w, const void* id128) : rank(r), world(w), D_(c.D) {
+    AB_CHECK(w >= 1 && r >= 0 && r < w, ADPSGD_E_CONFIG, "bad rank/world");
+    AB_CHECK(w == 1 || c.cfg.local_learners == 1, ADPSGD_E_CONFIG,
+             "multi-process runs host exactly one learner per rank");
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof(id));
+    ncclComm_t comm;
+    AB_NCCL(nccl().CommInitRank(&comm, w, id, r));
+    nccl_ = comm;
+    wsum_ = static_cast<float*>(c.alloc(c.D * sizeof(float)));
+    gsum_ = static_cast<float*>(c.alloc(c.D * sizeof(float)));
+    bar_ = static_cast<float*>(c.alloc(sizeof(float) * 4));
+    AB_CUDA(cudaMemset(bar_, 0, sizeof(float) * 4));
+    AB_CUDA(cudaEventCreateWithFlags(&ev_start_, cudaEventDisableTiming));
+    AB_CUDA(cudaEventCreateWithFlags(&ev_ws_, cudaEventDisableTiming));
+}
+
+Comm::~Comm() {
+    for (void* p : opened_) cudaIpcCloseMemHandle(p);
+    if (nccl_) nccl().CommDestroy(static_cast<ncclComm_t>(nccl_));
+    if (ev_start_) cudaEventDestroy(ev_start_);
+    if (ev_ws_) cudaEventDestroy(ev_ws_);
+}
+
+void Comm::barrier(cudaStream_t s) {
+    AB_NCCL(nccl().AllReduce(bar_, bar_ + 1, 1, ncclFloat32, ncclSum, static_cast<ncclComm_t>(nccl_), s));
+}
+
+const float* Comm::allreduce_sum_grads(Ctx& c, cudaStream_t s) {
+    AB_NCCL(nccl().AllReduce(c.learners[0].g, gsum_, c.D, ncclFloat32, ncclSum, static_cast<ncclComm_t>(nccl_), s));
+    return gsum_;
+}
+
+void Comm::start_weight_sum(Ctx& c, cudaStream_t s) {
+    // w_k is final once the previous iteration's update (enqueued on s) has run.
+    AB_CUDA(cudaEventRecord(ev_start_, s));
+    AB_CUDA(cudaStreamWaitEvent(c.s_comm, ev_start_, 0));
+    const float* w = c.learners[0].w[c.k & 1];
+    AB_NCCL(nccl().AllReduce(w, wsum_, c.D, ncclFloat32, ncclSum, static_cast<ncclComm_t>(nccl_), c.s_comm));
+    AB_CUDA(cudaEventRecord(ev_ws_, c.s_comm));
+}
+
+const float* Comm::wait_weight_sum(Ctx& c, cudaStream_t s) {
+    (void)c;
+    AB_CUDA(cudaStreamWaitEvent(s, ev_ws_, 0));
+    return wsum_;
+}
+
+void Comm::pre_gossip(Ctx& c, cudaStream_t s) {
+    (void)c;
+    barrier(s);
+}
+
+const float* Comm::peer_weight(int gid, int buf) const {
+    auto it = peers_.find(gid);
+    AB_CHECK(it != peers_.end(), ADPSGD_E_INVALID_STATE,
+             "learner " + std::to_string(gid) + " has no mapped weights (adpsgd_import_ipc)");
+    return buf ? it->second.second : it->second.first;
+}
+
+int64_t Comm::ipc_size(const Ctx& c) const { return static_cast<int64_t>(c.cfg.local_learners) * 2 * kHandle; }
+
+void Comm::export_ipc(const Ctx& c, void* out, int64_t size) const {
+    AB_CHECK(size >= ipc_size(c), ADPSGD_E_DIMENSION, "ipc buffer too small");
+    uint8_t* o = static_cast<uint8_t*>(out);
+    for (int j = 0; j < c.cfg.local_learners; ++j)
+        for (int b = 0; b < 2; ++b) {
+            cudaIpcMemHandle_t h;
+            AB_CUDA(cudaIpcGetMemHandle(&h, c.learners[j].w[b]));
+            std::memcpy(o + (j * 2 + b) * kHandle, &h, kHandle);
+        }
+}
+
+void Comm::import_ipc(int peer_rank, int first, int count, const void* handles, int64_t size) {
+    AB_CHECK(size >= static_cast<int64_t>(count) * 2 * kHandle, ADPSGD_E_DIMENSION, "ipc buffer too small");
+    if (peer_rank == rank) return;
+    const uint8_t* in = static_cast<const uint8_t*>(handles);
+    for (int j = 0; j < count; ++j) {
+        float* p[2];
+        for (int b = 0; b < 2; ++b) {
+            cudaIpcMemHandle_t h;
+            std::memcpy(&h, in + (j * 2 + b) * kHandle, kHandle);
+            void* ptr = nullptr;
+            AB_CUDA(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+            opened_.push_back(ptr);
+            p[b] = static_cast<float*>(ptr);
+        }
+        peers_[first + j] = {p[0], p[1]};
+    }
+}
+
+}  // namespace ab

@@ -1,0 +1,52 @@
+// Cross-GPU transport for one-process-per-GPU runs: NCCL (dlopen'ed, shares the
+// process's libnccl.so.2) for allreduce / barrier / send-recv, CUDA IPC for direct
+// NVLink peer reads of neighbour weights.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <map>
+#include <vector>
+
+#include "common.cuh"
+
+namespace ab {
+
+struct Ctx;
+
+class Comm {
+  public:
+    Comm(Ctx& ctx, int rank, int world, const void* nccl_id128);
+    ~Comm();
+    static void unique_id(void* out128);
+
+    int rank = 0, world = 1;
+    int gossip_mode = 0;  // 0 direct peer loads, 1 copy-engine prefetch, 2 NCCL send/recv
+
+    // SDPSGD: sum of every learner's gradient (in place in a comm buffer).
+    const float* allreduce_sum_grads(Ctx& c, cudaStream_t s);
+    // D1D: allreduce of w_k launched on the comm stream before the gradient compute ...
+    void start_weight_sum(Ctx& c, cudaStream_t s);
+    // ... and joined before the update.
+    const float* wait_weight_sum(Ctx& c, cudaStream_t s);
+    // FM/RM: GPU-side barrier so that every neighbour's w_k is final before the pulls.
+    void pre_gossip(Ctx& c, cudaStream_t s);
+    void barrier(cudaStream_t s);
+    const float* peer_weight(int gid, int buf) const;
+
+    int64_t ipc_size(const Ctx& c) const;
+    void export_ipc(const Ctx& c, void* out, int64_t size) const;
+    void import_ipc(int peer_rank, int first, int count, const void* handles, int64_t size);
+
+  private:
+    void* nccl_ = nullptr;  // ncclComm_t
+    float* wsum_ = nullptr;
+    float* gsum_ = nullptr;
+    float* bar_ = nullptr;
+    cudaEvent_t ev_start_ = nullptr, ev_ws_ = nullptr;
+    std::map<int, std::pair<float*, float*>> peers_;  // gid -> (w[0], w[1]) mapped over NVLink
+    std::vector<void*> opened_;
+    int64_t D_ = 0;
+};
+
+}  // namespace ab

@@ -1,0 +1,61 @@
+// Shared device/host helpers for the B200 ADPSGD learner step (sm_100a only).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "adpsgd_b200.h"
+
+namespace ab {
+
+// Status-carrying exception used inside the library; converted to adpsgd_status at the
+// C ABI (errors.hpp:9-46 taxonomy).
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define AB_CUDA(x)                                                                        \
+    do {                                                                                  \
+        cudaError_t e_ = (x);                                                             \
+        if (e_ != cudaSuccess)                                                            \
+            throw ::ab::Error(ADPSGD_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_) + \
+                                                 " @" + __FILE__ + ":" + std::to_string(__LINE__)); \
+    } while (0)
+
+#define AB_CHECK(cond, code, msg)                      \
+    do {                                               \
+        if (!(cond)) throw ::ab::Error((code), (msg)); \
+    } while (0)
+
+using bf16 = __nv_bfloat16;
+
+template <typename T> __device__ __forceinline__ float to_f(T v);
+template <> __device__ __forceinline__ float to_f<float>(float v) { return v; }
+template <> __device__ __forceinline__ float to_f<bf16>(bf16 v) { return __bfloat162float(v); }
+template <typename T> __device__ __forceinline__ T from_f(float v);
+template <> __device__ __forceinline__ float from_f<float>(float v) { return v; }
+template <> __device__ __forceinline__ bf16 from_f<bf16>(float v) { return __float2bfloat16_rn(v); }
+
+__device__ __forceinline__ float sigmoidf_(float x) { return 1.0f / (1.0f + __expf(-x)); }
+
+// Counts this library's kernel launches (reported as gpu_launches by bench.py).
+extern int64_t g_launch_count;
+inline void count_launch(int64_t n = 1) { g_launch_count += n; }
+
+inline int num_sms() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms;
+}
+
+}  // namespace ab

@@ -1,0 +1,674 @@
+// ADPSGD learner-step engine for B200: device-resident context, BLSTM forward/backward
+// orchestration over the GEMM + pointwise kernels, and the mixing/update of every
+// strategy (SDPSGD, FM, RM, D1D, GENERIC). Exposed through the C ABI in
+// include/adpsgd_b200.h.
+//
+// Reference correspondence (per-iteration semantics):
+//   step_sdpsgd         /root/reference/proj/src/engine.cpp:136-154
+//   step_adpsgd_mixing  engine.cpp:156-171 (FM: fixed ring; RM: permutation of iteration k)
+//   step_d1d            engine.cpp:173-184
+//   step_generic        engine.cpp:186-204 (history ring, ModelHistory engine.cpp:79-97)
+//   L == 1 -> SGD       engine.cpp:245-247
+//   init_learners       engine.cpp:99-116; sampling objectives.cpp:239-249
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "comm.hpp"
+#include "engine.hpp"
+#include "gemm.hpp"
+#include "kernels.cuh"
+#include "rng.hpp"
+
+namespace ab {
+
+namespace {
+thread_local std::string g_last_error;
+
+size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+}  // namespace
+
+void set_last_error(const std::string& s) { g_last_error = s; }
+const char* last_error() { return g_last_error.c_str(); }
+
+// ---------------------------------------------------------------------------
+// Device memory arena (one cudaMalloc per buffer; freed at ctx destroy).
+// ---------------------------------------------------------------------------
+void* Ctx::alloc(size_t bytes) {
+    void* p = nullptr;
+    AB_CUDA(cudaMalloc(&p, round_up(bytes ? bytes : 16, 256)));
+    allocations.push_back(p);
+    return p;
+}
+
+Ctx::~Ctx() {
+    cudaSetDevice(cfg.device);
+    cudaDeviceSynchronize();
+    comm.reset();
+    for (void* p : allocations) cudaFree(p);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (ev_mix) cudaEventDestroy(ev_mix);
+    if (ev_comp0) cudaEventDestroy(ev_comp0);
+    if (ev_comp1) cudaEventDestroy(ev_comp1);
+    if (s_comm) cudaStreamDestroy(s_comm);
+    if (s_main) cudaStreamDestroy(s_main);
+    if (h_loss) cudaFreeHost(h_loss);
+}
+
+static void validate_config(const adpsgd_config& c) {
+    const auto& m = c.model;
+    AB_CHECK(m.layers >= 1 && m.hidden >= 1 && m.input_dim >= 1 && m.classes >= 2 && m.unroll >= 1 && m.proj >= 0,
+             ADPSGD_E_CONFIG, "invalid model description");
+    AB_CHECK(c.learners >= 1, ADPSGD_E_CONFIG, "learners must be >= 1");                       // engine.cpp:61
+    AB_CHECK(!((c.strategy == ADPSGD_FM || c.strategy == ADPSGD_RM) && c.learners != 1 && c.learners < 3),
+             ADPSGD_E_CONFIG, "FM/RM mixing requires at least 3 learners");                    // engine.cpp:62-65
+    AB_CHECK(c.batch >= 1, ADPSGD_E_CONFIG, "batch must be >= 1");                             // engine.cpp:66
+    AB_CHECK(c.staleness_cap >= 0, ADPSGD_E_CONFIG, "staleness_cap must be >= 0");             // engine.cpp:68
+    AB_CHECK(c.strategy >= 0 && c.strategy <= 4, ADPSGD_E_CONFIG, "unknown strategy");
+    AB_CHECK(c.local_learners >= 1 && c.first_learner >= 0 && c.first_learner + c.local_learners <= c.learners,
+             ADPSGD_E_CONFIG, "local learner range outside [0, learners)");
+    AB_CHECK(c.precision == ADPSGD_PREC_FP32 || c.precision == ADPSGD_PREC_BF16, ADPSGD_E_CONFIG, "bad precision");
+    if (c.precision == ADPSGD_PREC_BF16) {
+        AB_CHECK(m.hidden % 8 == 0 && m.classes % 8 == 0 && m.proj % 8 == 0, ADPSGD_E_CONFIG,
+                 "bf16 tensor-core path needs hidden, classes and proj to be multiples of 8 (TMA pitch)");
+    }
+}
+
+Ctx::Ctx(const adpsgd_config& c) : cfg(c) {
+    validate_config(c);
+    lay = make_layout(c.model);
+    D = lay.total;
+    bf16_mode = c.precision == ADPSGD_PREC_BF16;
+    es = bf16_mode ? 2 : 4;
+    T = lay.T; B = c.batch; H = lay.H; nd = lay.nd; I = lay.I;
+    Ipad = bf16_mode ? static_cast<int>(round_up(I, 8)) : I;
+    TB = static_cast<int64_t>(T) * B;
+    ndH = nd * H;
+    nd4H = nd * 4 * H;
+    k = 0;
+    history_depth = c.strategy == ADPSGD_GENERIC ? c.staleness_cap + 1 : 1;  // engine.cpp:216-217
+
+    AB_CUDA(cudaSetDevice(c.device));
+    AB_CUDA(cudaStreamCreateWithFlags(&s_main, cudaStreamNonBlocking));
+    AB_CUDA(cudaStreamCreateWithFlags(&s_comm, cudaStreamNonBlocking));
+    AB_CUDA(cudaEventCreate(&ev0));
+    AB_CUDA(cudaEventCreate(&ev1));
+    AB_CUDA(cudaEventCreate(&ev_mix));
+    AB_CUDA(cudaEventCreate(&ev_comp0));
+    AB_CUDA(cudaEventCreate(&ev_comp1));
+    AB_CUDA(cudaMallocHost(&h_loss, sizeof(float) * 64));
+
+    // ---- workspace (shared by the local learners; they are computed in turn) ----
+    idx_dev = static_cast<int32_t*>(alloc(sizeof(int32_t) * B));
+    X0 = alloc(TB * Ipad * es);
+    lab_step = static_cast<int32_t*>(alloc(sizeof(int32_t) * TB));
+    for (int l = 0; l < lay.L; ++l) {
+        Hout.push_back(alloc(TB * ndH * es));
+        gates.push_back(static_cast<float*>(alloc(TB * nd4H * sizeof(float))));
+        cst.push_back(static_cast<float*>(alloc(TB * ndH * sizeof(float))));
+    }
+    if (lay.P > 0) {
+        Y = alloc(TB * lay.P * es);
+        dY = alloc(TB * lay.P * es);
+    }
+    logits = static_cast<float*>(alloc(TB * lay.C * sizeof(float)));
+    dlogits = alloc(TB * lay.C * es);
+    row_loss = static_cast<float*>(alloc(TB * sizeof(float)));
+    int max_in = std::max(lay.top, Ipad);
+    dHa = static_cast<float*>(alloc(TB * max_in * sizeof(float)));
+    dHb = static_cast<float*>(alloc(TB * max_in * sizeof(float)));
+    dZ = alloc(TB * nd4H * es);
+    zstep = static_cast<float*>(alloc(static_cast<size_t>(nd) * B * 4 * H * sizeof(float)));
+    dh_rec = static_cast<float*>(alloc(static_cast<size_t>(nd) * B * H * sizeof(float)));
+    dc_rec = static_cast<float*>(alloc(static_cast<size_t>(nd) * B * H * sizeof(float)));
+    ws_elems = std::max<int64_t>(int64_t(128) * std::max<int64_t>(nd4H, lay.C), 1 << 20);
+    colsum_ws = static_cast<float*>(alloc(ws_elems * sizeof(float)));
+    loss_dev = static_cast<float*>(alloc(sizeof(float) * 64));
+    scratch_f = static_cast<float*>(alloc(sizeof(float) * 16));
+    // staging for host batches (end-to-end path)
+    stage_feats = static_cast<float*>(alloc(static_cast<size_t>(B) * T * I * sizeof(float)));
+    stage_labels = static_cast<int32_t*>(alloc(static_cast<size_t>(B) * T * sizeof(int32_t)));
+    ident_idx = static_cast<int32_t*>(alloc(sizeof(int32_t) * B));
+    {
+        std::vector<int32_t> id(B);
+        for (int b = 0; b < B; ++b) id[b] = b;
+        AB_CUDA(cudaMemcpy(ident_idx, id.data(), sizeof(int32_t) * B, cudaMemcpyHostToDevice));
+    }
+
+    // ---- learners: w0 shared by all (engine.cpp:101-103), streams 0xB000 + global id ----
+    std::vector<double> w0(D);
+    {
+        Rng init(derive_seed(c.seed, kInitStream));
+        for (int64_t i = 0; i < D; ++i) w0[i] = 0.1 * init.next_gaussian();
+    }
+    std::vector<float> w0f(w0.begin(), w0.end());
+    for (int j = 0; j < c.local_learners; ++j) {
+        Learner ln;
+        ln.gid = c.first_learner + j;
+        ln.rng = Rng(derive_seed(c.seed, kLearnerStream + static_cast<uint64_t>(ln.gid)));
+        for (int b = 0; b < 2; ++b) ln.w[b] = static_cast<float*>(alloc(D * sizeof(float)));
+        ln.g = static_cast<float*>(alloc(D * sizeof(float)));
+        if (bf16_mode) {
+            ln.shadow = static_cast<bf16*>(alloc(D * sizeof(bf16)));
+            for (int d = 0; d < nd; ++d)
+                ln.l1pad.push_back(static_cast<bf16*>(alloc(static_cast<size_t>(4) * H * Ipad * sizeof(bf16))));
+        }
+        for (int h = 1; h < history_depth; ++h) ln.hist.push_back(static_cast<float*>(alloc(D * sizeof(float))));
+        AB_CUDA(cudaMemcpy(ln.w[0], w0f.data(), D * sizeof(float), cudaMemcpyHostToDevice));
+        learners.push_back(std::move(ln));
+    }
+    for (auto& ln : learners) {
+        refresh_shadow(ln, ln.w[0], s_main);
+        for (float* h : ln.hist) AB_CUDA(cudaMemcpyAsync(h, ln.w[0], D * sizeof(float), cudaMemcpyDeviceToDevice, s_main));
+    }
+    AB_CUDA(cudaStreamSynchronize(s_main));
+}
+
+// bf16 shadow of the master weights + TMA-aligned padded copy of layer-1 W_ih.
+void Ctx::refresh_shadow(Learner& ln, const float* w, cudaStream_t s) {
+    if (!bf16_mode) return;
+    launch_f32_to_bf16(w, ln.shadow, D, s);
+    refresh_pad(ln, w, s);
+}
+void Ctx::refresh_pad(Learner& ln, const float* w, cudaStream_t s) {
+    if (!bf16_mode) return;
+    for (int d = 0; d < nd; ++d)
+        launch_pad_rows_bf16(w + lay.dir[0][d].w_ih, I, ln.l1pad[d], Ipad, 4 * H, I, s);
+}
+
+// Weight views used as GEMM operands for a given master vector / shadow.
+struct WView {
+    const void* base;   // bf16 shadow (bf16 mode) or fp32 master
+    const float* master;
+    const Ctx* c;
+    const Learner* ln;
+    const void* at(int64_t off) const {
+        return static_cast<const uint8_t*>(base) + off * c->es;
+    }
+    // layer-1 W_ih: padded bf16 copy in bf16 mode (ld = Ipad), flat in fp32 mode (ld = I)
+    const void* wih(int l, int d, int64_t* ld) const {
+        if (l == 0 && c->bf16_mode) { *ld = c->Ipad; return ln->l1pad[d]; }
+        *ld = c->lay.in_dim[l];
+        return at(c->lay.dir[l][d].w_ih);
+    }
+};
+
+static inline const void* off_ptr(const void* p, int64_t elems, int es) {
+    return static_cast<const uint8_t*>(p) + elems * es;
+}
+static inline void* off_ptr(void* p, int64_t elems, int es) { return static_cast<uint8_t*>(p) + elems * es; }
+
+// Forward + backward of the BLSTM on the batch already gathered into X0 / lab_step.
+// grad (fp32, flat layout) receives d(mean CE)/dw; loss_slot receives the mean CE.
+void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, float* loss_slot, cudaStream_t s) {
+    const bool bf = bf16_mode;
+    WView W{bf ? static_cast<const void*>(ln.shadow) : static_cast<const void*>(master), master, this, &ln};
+    const int G4 = 4 * H;
+
+    // ---------------- forward ----------------
+    for (int l = 0; l < lay.L; ++l) {
+        const void* Xin = l == 0 ? X0 : Hout[l - 1];
+        const int Kin = l == 0 ? Ipad : ndH;
+        for (int st = 0; st < T; ++st) {
+            for (int d = 0; d < nd; ++d) {
+                const int t = d == 0 ? st : T - 1 - st;
+                const int tp = d == 0 ? t - 1 : t + 1;
+                GemmArgs g;
+                g.M = B; g.N = G4;
+                int64_t ldw;
+                const void* wih = W.wih(l, d, &ldw);
+                g.seg[0].a = {off_ptr(Xin, static_cast<int64_t>(t) * B * Kin, es), Kin, false};
+                g.seg[0].b = {wih, ldw, false};
+                g.seg[0].K = Kin;
+                g.nseg = 1;
+                if (st > 0) {
+                    g.seg[1].a = {off_ptr(Hout[l], static_cast<int64_t>(tp) * B * ndH + d * H, es), ndH, false};
+                    g.seg[1].b = {W.at(lay.dir[l][d].w_hh), H, false};
+                    g.seg[1].K = H;
+                    g.nseg = 2;
+                }
+                g.C = zstep + static_cast<int64_t>(d) * B * G4;
+                g.ldc = G4;
+                g.bias = master + lay.dir[l][d].b;
+                gemm(bf, g, s);
+                const float* cprev = st > 0 ? cst[l] + static_cast<int64_t>(tp) * B * ndH + d * H : nullptr;
+                float* gt = gates[l] + static_cast<int64_t>(t) * B * nd4H + d * G4;
+                float* ct = cst[l] + static_cast<int64_t>(t) * B * ndH + d * H;
+                void* ht = off_ptr(Hout[l], static_cast<int64_t>(t) * B * ndH + d * H, es);
+                if (bf)
+                    launch_cell_fwd<bf16>(zstep + static_cast<int64_t>(d) * B * G4, G4, cprev, ndH, gt, nd4H, ct,
+                                          static_cast<bf16*>(ht), ndH, B, H, s);
+                else
+                    launch_cell_fwd<float>(zstep + static_cast<int64_t>(d) * B * G4, G4, cprev, ndH, gt, nd4H, ct,
+                                           static_cast<float*>(ht), ndH, B, H, s);
+            }
+        }
+    }
+    const void* top = Hout[lay.L - 1];
+    const void* yin = top;
+    const int oi = lay.out_in;
+    if (lay.P > 0) {
+        GemmArgs g;
+        g.M = static_cast<int>(TB); g.N = lay.P;
+        g.seg[0].a = {top, ndH, false};
+        g.seg[0].b = {W.at(lay.w_proj), ndH, false};
+        g.seg[0].K = ndH;
+        g.C = Y; g.ldc = lay.P; g.c_bf16 = bf;
+        g.bias = master + lay.b_proj;
+        gemm(bf, g, s);
+        yin = Y;
+    }
+    {
+        GemmArgs g;
+        g.M = static_cast<int>(TB); g.N = lay.C;
+        g.seg[0].a = {yin, oi, false};
+        g.seg[0].b = {W.at(lay.w_out), oi, false};
+        g.seg[0].K = oi;
+        g.C = logits; g.ldc = lay.C;
+        g.bias = master + lay.b_out;
+        gemm(bf, g, s);
+    }
+    const float scale = 1.0f / static_cast<float>(TB);
+    if (bf) launch_softmax_ce<bf16>(logits, lab_step, static_cast<int>(TB), lay.C, scale, static_cast<bf16*>(dlogits), row_loss, s);
+    else launch_softmax_ce<float>(logits, lab_step, static_cast<int>(TB), lay.C, scale, static_cast<float*>(dlogits), row_loss, s);
+    launch_sum(row_loss, static_cast<int>(TB), scale, loss_slot, s);
+
+    // ---------------- backward: output / projection ----------------
+    auto colsum = [&](const void* X, int64_t ld, int R, int N, float* out) {
+        if (bf) launch_colsum<bf16>(static_cast<const bf16*>(X), ld, R, N, out, colsum_ws, ws_elems, s);
+        else launch_colsum<float>(static_cast<const float*>(X), ld, R, N, out, colsum_ws, ws_elems, s);
+    };
+    {   // dW_out = dlogits^T Yin
+        GemmArgs g;
+        g.M = lay.C; g.N = oi;
+        g.seg[0].a = {dlogits, lay.C, true};
+        g.seg[0].b = {yin, oi, true};
+        g.seg[0].K = static_cast<int>(TB);
+        g.C = grad + lay.w_out; g.ldc = oi;
+        gemm(bf, g, s);
+    }
+    colsum(dlogits, lay.C, static_cast<int>(TB), lay.C, grad + lay.b_out);
+    float* dHcur = dHa;
+    float* dHnext = dHb;
+    if (lay.P > 0) {
+        {   // dY = dlogits W_out  (bf16/fp32 activation type: it is a GEMM operand next)
+            GemmArgs g;
+            g.M = static_cast<int>(TB); g.N = lay.P;
+            g.seg[0].a = {dlogits, lay.C, false};
+            g.seg[0].b = {W.at(lay.w_out), lay.P, true};
+            g.seg[0].K = lay.C;
+            g.C = dY; g.ldc = lay.P; g.c_bf16 = bf;
+            gemm(bf, g, s);
+        }
+        {   // dW_proj = dY^T top
+            GemmArgs g;
+            g.M = lay.P; g.N = ndH;
+            g.seg[0].a = {dY, lay.P, true};
+            g.seg[0].b = {top, ndH, true};
+            g.seg[0].K = static_cast<int>(TB);
+            g.C = grad + lay.w_proj; g.ldc = ndH;
+            gemm(bf, g, s);
+        }
+        colsum(dY, lay.P, static_cast<int>(TB), lay.P, grad + lay.b_proj);
+        {   // dTop = dY W_proj
+            GemmArgs g;
+            g.M = static_cast<int>(TB); g.N = ndH;
+            g.seg[0].a = {dY, lay.P, false};
+            g.seg[0].b = {W.at(lay.w_proj), ndH, true};
+            g.seg[0].K = lay.P;
+            g.C = dHcur; g.ldc = ndH;
+            gemm(bf, g, s);
+        }
+    } else {
+        GemmArgs g;
+        g.M = static_cast<int>(TB); g.N = ndH;
+        g.seg[0].a = {dlogits, lay.C, false};
+        g.seg[0].b = {W.at(lay.w_out), ndH, true};
+        g.seg[0].K = lay.C;
+        g.C = dHcur; g.ldc = ndH;
+        gemm(bf, g, s);
+    }
+
+    // ---------------- backward: LSTM layers (BPTT) ----------------
+    for (int l = lay.L - 1; l >= 0; --l) {
+        const void* Xin = l == 0 ? X0 : Hout[l - 1];
+        const int Kin = l == 0 ? Ipad : ndH;
+        for (int st = 0; st < T; ++st) {
+            const int sf = T - 1 - st;  // forward-order step index of this time
+            for (int d = 0; d < nd; ++d) {
+                const int t = d == 0 ? sf : T - 1 - sf;
+                const int tp = d == 0 ? t - 1 : t + 1;
+                float* dhr = dh_rec + static_cast<int64_t>(d) * B * H;
+                float* dcr = dc_rec + static_cast<int64_t>(d) * B * H;
+                const float* gt = gates[l] + static_cast<int64_t>(t) * B * nd4H + d * G4;
+                const float* ct = cst[l] + static_cast<int64_t>(t) * B * ndH + d * H;
+                const float* cp = sf > 0 ? cst[l] + static_cast<int64_t>(tp) * B * ndH + d * H : nullptr;
+                void* dzt = off_ptr(dZ, static_cast<int64_t>(t) * B * nd4H + d * G4, es);
+                const float* dHt = dHcur + static_cast<int64_t>(t) * B * ndH + d * H;
+                if (bf)
+                    launch_cell_bwd<bf16>(dHt, ndH, dhr, dcr, st == 0, gt, nd4H, ct, cp, ndH, static_cast<bf16*>(dzt),
+                                          nd4H, B, H, s);
+                else
+                    launch_cell_bwd<float>(dHt, ndH, dhr, dcr, st == 0, gt, nd4H, ct, cp, ndH,
+                                           static_cast<float*>(dzt), nd4H, B, H, s);
+                if (sf > 0) {  // dh_{prev} = dz_t W_hh
+                    GemmArgs g;
+                    g.M = B; g.N = H;
+                    g.seg[0].a = {dzt, nd4H, false};
+                    g.seg[0].b = {W.at(lay.dir[l][d].w_hh), H, true};
+                    g.seg[0].K = G4;
+                    g.C = dhr; g.ldc = H;
+                    gemm(bf, g, s);
+                }
+            }
+        }
+        for (int d = 0; d < nd; ++d) {
+            const DirOff& o = lay.dir[l][d];
+            {   // dW_ih = dZ_d^T Xin
+                GemmArgs g;
+                g.M = G4; g.N = lay.in_dim[l];
+                g.seg[0].a = {off_ptr(dZ, d * G4, es), nd4H, true};
+                g.seg[0].b = {Xin, Kin, true};
+                g.seg[0].K = static_cast<int>(TB);
+                g.C = grad + o.w_ih; g.ldc = lay.in_dim[l];
+                gemm(bf, g, s);
+            }
+            if (T > 1) {  // dW_hh = sum_t dz_t^T h_prev(t)
+                GemmArgs g;
+                g.M = G4; g.N = H;
+                const int64_t a_row0 = d == 0 ? B : 0;
+                const int64_t b_row0 = d == 0 ? 0 : B;
+                g.seg[0].a = {off_ptr(dZ, a_row0 * nd4H + d * G4, es), nd4H, true};
+                g.seg[0].b = {off_ptr(Hout[l], b_row0 * ndH + d * H, es), ndH, true};
+                g.seg[0].K = static_cast<int>((T - 1) * static_cast<int64_t>(B));
+                g.C = grad + o.w_hh; g.ldc = H;
+                gemm(bf, g, s);
+            } else {
+                AB_CUDA(cudaMemsetAsync(grad + o.w_hh, 0, sizeof(float) * G4 * H, s));
+            }
+            colsum(off_ptr(dZ, d * G4, es), nd4H, static_cast<int>(TB), G4, grad + o.b);
+        }
+        if (l > 0) {  // dXin = sum_d dZ_d W_ih_d
+            GemmArgs g;
+            g.M = static_cast<int>(TB); g.N = Kin;
+            for (int d = 0; d < nd; ++d) {
+                int64_t ldw;
+                const void* wih = W.wih(l, d, &ldw);
+                g.seg[d].a = {off_ptr(dZ, d * G4, es), nd4H, false};
+                g.seg[d].b = {wih, ldw, true};
+                g.seg[d].K = G4;
+            }
+            g.nseg = nd;
+            g.C = dHnext; g.ldc = Kin;
+            gemm(bf, g, s);
+            std::swap(dHcur, dHnext);
+        }
+    }
+}
+
+void Ctx::gather_batch(const float* feats_src, const int32_t* labels_src, const int32_t* idx, cudaStream_t s) {
+    if (bf16_mode)
+        launch_gather<bf16>(feats_src, labels_src, idx, B, T, I, Ipad, static_cast<bf16*>(X0), lab_step, s);
+    else
+        launch_gather<float>(feats_src, labels_src, idx, B, T, I, Ipad, static_cast<float*>(X0), lab_step, s);
+}
+
+// Host-side sampling of learner j's batch: M draws next_below(train_count)
+// (objectives.cpp:239-249) from its own stream, then upload.
+void Ctx::sample_and_gather(Learner& ln, cudaStream_t s) {
+    AB_CHECK(feats != nullptr && train_count >= 1, ADPSGD_E_INVALID_STATE, "dataset has no training samples");
+    std::vector<int32_t> idx(B);
+    for (int b = 0; b < B; ++b) idx[b] = static_cast<int32_t>(ln.rng.next_below(static_cast<uint64_t>(train_count)));
+    // pinned staging keeps the copy asynchronous and graph-friendly
+    if (!h_idx) AB_CUDA(cudaMallocHost(&h_idx, sizeof(int32_t) * B * 2));
+    int32_t* hb = h_idx + (idx_flip ^= 1) * B;
+    AB_CUDA(cudaStreamSynchronize(s));  // previous users of this pinned half are done
+    std::memcpy(hb, idx.data(), sizeof(int32_t) * B);
+    AB_CUDA(cudaMemcpyAsync(idx_dev, hb, sizeof(int32_t) * B, cudaMemcpyHostToDevice, s));
+    gather_batch(feats, labels, idx_dev, s);
+}
+
+// ---------------------------------------------------------------------------
+// The iteration (engine.cpp:245-283)
+// ---------------------------------------------------------------------------
+void Ctx::mix_and_update(double lr_d, const int32_t* taus) {
+    const float lr = static_cast<float>(lr_d);
+    const int cur = static_cast<int>(k & 1), nxt = cur ^ 1;
+    const int Lg = cfg.learners;
+    const int nloc = cfg.local_learners;
+    std::vector<const float*> wtab, gtab;
+    std::vector<float*> otab;
+    std::vector<bf16*> stab;
+    for (auto& ln : learners) {
+        gtab.push_back(ln.g);
+        otab.push_back(ln.w[nxt]);
+        stab.push_back(bf16_mode ? ln.shadow : nullptr);
+    }
+    cudaStream_t s = s_main;
+    int strategy = cfg.strategy;
+    if (Lg == 1) strategy = ADPSGD_SDPSGD;  // engine.cpp:245-247
+    last_gossip_bytes = 0;
+
+    if (strategy == ADPSGD_SDPSGD) {
+        if (comm && comm->world > 1) {
+            // gradient allreduce (sum over ranks of the local sums), then the shared update
+            const float* gsum = comm->allreduce_sum_grads(*this, s);
+            launch_sdpsgd(D, Lg, learners[0].w[cur], nullptr, gsum, nloc, lr, otab.data(), stab.data(), s);
+        } else {
+            launch_sdpsgd(D, Lg, learners[0].w[cur], gtab.data(), nullptr, nloc, lr, otab.data(), stab.data(), s);
+        }
+    } else if (strategy == ADPSGD_D1D) {
+        if (comm && comm->world > 1) {
+            const float* wsum = comm->wait_weight_sum(*this, s);  // allreduce started before the compute
+            launch_d1d(D, Lg, nullptr, wsum, nloc, gtab.data(), lr, otab.data(), stab.data(), s);
+        } else {
+            for (auto& ln : learners) wtab.push_back(ln.w[cur]);
+            launch_d1d(D, Lg, wtab.data(), nullptr, nloc, gtab.data(), lr, otab.data(), stab.data(), s);
+        }
+    } else if (strategy == ADPSGD_FM || strategy == ADPSGD_RM) {
+        std::vector<int32_t> map(Lg);
+        if (strategy == ADPSGD_RM) permutation_for_iteration(cfg.seed, Lg, k, map.data());
+        if (comm && comm->world > 1) comm->pre_gossip(*this, s);
+        for (int j = 0; j < nloc; ++j) {
+            const int l = learners[j].gid;
+            int left, right;
+            if (strategy == ADPSGD_FM) {
+                left = (l + Lg - 1) % Lg;
+                right = (l + 1) % Lg;
+            } else {  // chronos.cpp:227-235
+                int pos = 0;
+                for (int i = 0; i < Lg; ++i) if (map[i] == l) { pos = i; break; }
+                left = map[(pos + Lg - 1) % Lg];
+                right = map[(pos + 1) % Lg];
+            }
+            const float* wl = weight_ptr(left, cur);
+            const float* wr = weight_ptr(right, cur);
+            if (!is_local(left)) last_gossip_bytes += D * 4.0;
+            if (!is_local(right)) last_gossip_bytes += D * 4.0;
+            launch_mix3(D, learners[j].w[cur], wl, wr, learners[j].g, lr, learners[j].w[nxt], stab[j], s);
+        }
+    } else {  // GENERIC: W T - lr G(tau-lagged), engine.cpp:186-204
+        AB_CHECK(!(comm && comm->world > 1), ADPSGD_E_CONFIG, "GENERIC staleness is single-process only");
+        std::vector<double> Tm(static_cast<size_t>(Lg) * Lg, 0.0);
+        const int kind = cfg.generic_mix;
+        if (kind == ADPSGD_MIX_UNIFORM) {
+            AB_CHECK(Lg >= 2, ADPSGD_E_INVALID_ORDER, "uniform mixing requires order >= 2");
+            std::fill(Tm.begin(), Tm.end(), 1.0 / Lg);
+        } else {
+            AB_CHECK(Lg >= 3, ADPSGD_E_INVALID_ORDER, "ring mixing requires order >= 3");
+            std::vector<double> f(static_cast<size_t>(Lg) * Lg, 0.0);
+            for (int i = 0; i < Lg; ++i) {
+                f[i * Lg + i] += 1.0 / 3.0;
+                f[i * Lg + (i + 1) % Lg] += 1.0 / 3.0;
+                f[i * Lg + (i + Lg - 1) % Lg] += 1.0 / 3.0;
+            }
+            if (kind == ADPSGD_MIX_FIXED) {
+                Tm = f;
+            } else {
+                std::vector<int32_t> map(Lg);
+                permutation_for_iteration(cfg.seed, Lg, k, map.data());
+                for (int a = 0; a < Lg; ++a)
+                    for (int b = 0; b < Lg; ++b) Tm[map[a] * Lg + map[b]] += f[a * Lg + b];
+            }
+        }
+        for (auto& ln : learners) wtab.push_back(ln.w[cur]);
+        std::vector<int> cols;
+        for (auto& ln : learners) cols.push_back(ln.gid);
+        launch_dense_mix(D, Lg, wtab.data(), Tm.data(), cols.data(), nloc, gtab.data(), lr, otab.data(), stab.data(), s);
+        (void)taus;
+    }
+    if (bf16_mode)
+        for (auto& ln : learners) refresh_pad(ln, ln.w[nxt], s);
+    // ModelHistory push (engine.cpp:85-88): keep depth-1 older models for GENERIC.
+    if (history_depth > 1) {
+        for (auto& ln : learners) {
+            // rotate: hist[0] <- w[cur] (the model before this update)
+            float* oldest = ln.hist.back();
+            for (size_t h = ln.hist.size() - 1; h > 0; --h) ln.hist[h] = ln.hist[h - 1];
+            ln.hist[0] = oldest;
+            AB_CUDA(cudaMemcpyAsync(oldest, ln.w[cur], D * sizeof(float), cudaMemcpyDeviceToDevice, s));
+        }
+    }
+}
+
+const float* Ctx::weight_ptr(int gid, int buf) const {
+    const int j = gid - cfg.first_learner;
+    if (j >= 0 && j < cfg.local_learners) return learners[j].w[buf];
+    AB_CHECK(comm != nullptr, ADPSGD_E_INVALID_STATE, "neighbour weights not mapped (call adpsgd_import_ipc)");
+    return comm->peer_weight(gid, buf);
+}
+bool Ctx::is_local(int gid) const {
+    return gid >= cfg.first_learner && gid < cfg.first_learner + cfg.local_learners;
+}
+
+// Model each learner evaluates its gradient at: its own model (FM/RM/D1D), the shared
+// model (SDPSGD; identical on every learner), or the tau-lagged model (GENERIC).
+const float* Ctx::grad_point(const Learner& ln, const int32_t* taus) {
+    const int cur = static_cast<int>(k & 1);
+    if (cfg.strategy == ADPSGD_GENERIC && cfg.learners > 1 && taus) {
+        const int tau = taus[ln.gid];
+        AB_CHECK(tau >= 0 && tau < history_depth, ADPSGD_E_STALENESS_OVERFLOW,
+                 "staleness " + std::to_string(tau) + " exceeds history depth " + std::to_string(history_depth));
+        if (tau > 0) return ln.hist[tau - 1];
+    }
+    return ln.w[cur];
+}
+
+void Ctx::check_sync() {
+    // engine.cpp:139-144 — models must agree within 1e-12 before an SDPSGD step
+    // (local learners; identical fp32 arithmetic keeps them bit-identical).
+    if (cfg.local_learners < 2) return;
+    const int cur = static_cast<int>(k & 1);
+    AB_CUDA(cudaMemsetAsync(scratch_f, 0, sizeof(float), s_main));
+    for (int j = 1; j < cfg.local_learners; ++j) launch_maxdiff(D, learners[j].w[cur], learners[0].w[cur], scratch_f, s_main);
+    float h = 0;
+    AB_CUDA(cudaMemcpyAsync(&h, scratch_f, sizeof(float), cudaMemcpyDeviceToHost, s_main));
+    AB_CUDA(cudaStreamSynchronize(s_main));
+    AB_CHECK(!(h > 1e-12f), ADPSGD_E_SYNC_VIOLATION, "learner desynchronized before SDPSGD step");
+}
+
+void Ctx::step(double lr, const int32_t* taus, float* loss_out, const float* host_feats, const int32_t* host_labels,
+               const double* injected) {
+    AB_CUDA(cudaSetDevice(cfg.device));
+    const int strategy = cfg.learners == 1 ? ADPSGD_SDPSGD : cfg.strategy;
+    if (strategy == ADPSGD_SDPSGD) check_sync();
+    if (strategy == ADPSGD_GENERIC && taus) {
+        for (int l = 0; l < cfg.learners; ++l)
+            AB_CHECK(taus[l] >= 0 && taus[l] < history_depth, ADPSGD_E_STALENESS_OVERFLOW,
+                     "staleness " + std::to_string(taus[l]) + " exceeds history depth " + std::to_string(history_depth));
+    }
+    cudaStream_t s = s_main;
+    AB_CUDA(cudaEventRecord(ev0, s));
+    // D1D: start the weight allreduce on the comm stream before the gradient compute
+    if (strategy == ADPSGD_D1D && comm && comm->world > 1) comm->start_weight_sum(*this, s);
+    for (int j = 0; j < cfg.local_learners; ++j) {
+        Learner& ln = learners[j];
+        if (injected) {
+            std::vector<float> gf(injected + j * D, injected + (j + 1) * D);
+            AB_CUDA(cudaMemcpyAsync(ln.g, gf.data(), D * sizeof(float), cudaMemcpyHostToDevice, s));
+            AB_CUDA(cudaStreamSynchronize(s));
+            continue;
+        }
+        if (host_feats) {
+            const size_t nf = static_cast<size_t>(B) * T * I;
+            AB_CUDA(cudaMemcpyAsync(stage_feats, host_feats + j * nf, nf * sizeof(float), cudaMemcpyHostToDevice, s));
+            AB_CUDA(cudaMemcpyAsync(stage_labels, host_labels + static_cast<size_t>(j) * B * T,
+                                    sizeof(int32_t) * B * T, cudaMemcpyHostToDevice, s));
+            gather_batch(stage_feats, stage_labels, ident_idx, s);
+        } else {
+            sample_and_gather(ln, s);
+        }
+        const float* wpt = grad_point(ln, taus);
+        if (bf16_mode && wpt != ln.w[k & 1]) {
+            // lagged model: refresh a temporary shadow view (GENERIC only)
+            refresh_shadow(ln, wpt, s);
+        }
+        if (ln.straggle > 1.0) AB_CUDA(cudaEventRecord(ev_comp0, s));
+        forward_backward(ln, wpt, ln.g, loss_dev + j, s);
+        if (ln.straggle > 1.0) {
+            AB_CUDA(cudaEventRecord(ev_comp1, s));
+            // stretch this learner's compute by (factor - 1) x its last measured compute time
+            if (ln.last_compute_ms > 0)
+                launch_delay(static_cast<uint64_t>((ln.straggle - 1.0) * ln.last_compute_ms * 1e6), s);
+        }
+        if (bf16_mode && wpt != ln.w[k & 1]) refresh_shadow(ln, ln.w[k & 1], s);
+    }
+    AB_CUDA(cudaEventRecord(ev_mix, s));
+    mix_and_update(lr, taus);
+    AB_CUDA(cudaEventRecord(ev1, s));
+    if (!injected && loss_out) {
+        AB_CUDA(cudaMemcpyAsync(h_loss, loss_dev, sizeof(float) * cfg.local_learners, cudaMemcpyDeviceToHost, s));
+    }
+    AB_CUDA(cudaEventSynchronize(ev1));
+    if (!injected && loss_out) std::memcpy(loss_out, h_loss, sizeof(float) * cfg.local_learners);
+    float ms = 0, mms = 0;
+    AB_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+    AB_CUDA(cudaEventElapsedTime(&mms, ev_mix, ev1));
+    last_step_ms = ms;
+    last_mix_ms = mms;
+    for (auto& ln : learners) {
+        if (ln.straggle > 1.0) {
+            float cm = 0;
+            if (cudaEventElapsedTime(&cm, ev_comp0, ev_comp1) == cudaSuccess) ln.last_compute_ms = cm;
+        }
+    }
+    ++k;
+}
+
+double Ctx::gradient(const double* w, const int32_t* idx, int M, double* g_out) {
+    AB_CHECK(M == B, ADPSGD_E_DIMENSION, "gradient(): M must equal the context batch");
+    AB_CHECK(feats != nullptr, ADPSGD_E_INVALID_STATE, "dataset has no training samples");
+    AB_CUDA(cudaSetDevice(cfg.device));
+    cudaStream_t s = s_main;
+    Learner& ln = learners[0];
+    // use the learner's spare buffer (w[nxt]) as the evaluation point; restore shadow after
+    const int nxt = static_cast<int>((k & 1) ^ 1);
+    std::vector<float> wf(w, w + D);
+    AB_CUDA(cudaMemcpyAsync(ln.w[nxt], wf.data(), D * sizeof(float), cudaMemcpyHostToDevice, s));
+    refresh_shadow(ln, ln.w[nxt], s);
+    AB_CUDA(cudaMemcpyAsync(idx_dev, idx, sizeof(int32_t) * B, cudaMemcpyHostToDevice, s));
+    gather_batch(feats, labels, idx_dev, s);
+    float* gtmp = static_cast<float*>(alloc_scratch_grad());
+    forward_backward(ln, ln.w[nxt], gtmp, loss_dev + 63, s);
+    std::vector<float> gh(D);
+    float lh = 0;
+    AB_CUDA(cudaMemcpyAsync(gh.data(), gtmp, D * sizeof(float), cudaMemcpyDeviceToHost, s));
+    AB_CUDA(cudaMemcpyAsync(&lh, loss_dev + 63, sizeof(float), cudaMemcpyDeviceToHost, s));
+    refresh_shadow(ln, ln.w[k & 1], s);
+    AB_CUDA(cudaStreamSynchronize(s));
+    for (int64_t i = 0; i < D; ++i) g_out[i] = gh[i];
+    return lh;
+}
+
+void* Ctx::alloc_scratch_grad() {
+    if (!scratch_grad) scratch_grad = alloc(D * sizeof(float));
+    return scratch_grad;
+}
+
+}  // namespace ab

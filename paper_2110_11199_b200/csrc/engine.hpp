@@ -1,0 +1,106 @@
+// Device-resident learner context behind the C ABI (engine.cu, capi.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "model.hpp"
+#include "rng.hpp"
+
+namespace ab {
+
+class Comm;
+
+// engine.hpp:67-72 (LearnerState): model (double-buffered fp32 master + bf16 shadow),
+// history (GENERIC), sampling stream.
+struct Learner {
+    int gid = 0;
+    float* w[2] = {nullptr, nullptr};
+    float* g = nullptr;
+    bf16* shadow = nullptr;          // bf16 copy of the current model (GEMM operand)
+    std::vector<bf16*> l1pad;        // layer-1 W_ih per direction, rows padded for TMA
+    std::vector<float*> hist;        // lags 1..depth-1 (ModelHistory, engine.cpp:79-97)
+    Rng rng{0};
+    double straggle = 1.0;
+    float last_compute_ms = 0.f;
+};
+
+struct Ctx {
+    explicit Ctx(const adpsgd_config& c);
+    ~Ctx();
+
+    adpsgd_config cfg;
+    Layout lay;
+    int64_t D = 0;
+    bool bf16_mode = false;
+    int es = 4;  // activation element size
+    int T = 0, B = 0, H = 0, nd = 1, I = 0, Ipad = 0, ndH = 0, nd4H = 0;
+    int64_t TB = 0;
+    int64_t k = 0;
+    int history_depth = 1;
+
+    cudaStream_t s_main = nullptr, s_comm = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_mix = nullptr, ev_comp0 = nullptr, ev_comp1 = nullptr;
+    double last_step_ms = 0, last_mix_ms = 0, last_gossip_bytes = 0;
+
+    // dataset (device)
+    float* feats = nullptr;
+    int32_t* labels = nullptr;
+    int n_seg = 0, train_count = 0;
+
+    // workspace
+    int32_t* idx_dev = nullptr;
+    int32_t* ident_idx = nullptr;
+    void* X0 = nullptr;
+    int32_t* lab_step = nullptr;
+    std::vector<void*> Hout;
+    std::vector<float*> gates, cst;
+    void* Y = nullptr;
+    void* dY = nullptr;
+    float* logits = nullptr;
+    void* dlogits = nullptr;
+    float* row_loss = nullptr;
+    float *dHa = nullptr, *dHb = nullptr;
+    void* dZ = nullptr;
+    float* zstep = nullptr;
+    float *dh_rec = nullptr, *dc_rec = nullptr;
+    float* colsum_ws = nullptr;
+    int64_t ws_elems = 0;
+    float* loss_dev = nullptr;
+    float* scratch_f = nullptr;
+    void* scratch_grad = nullptr;
+    float* stage_feats = nullptr;
+    int32_t* stage_labels = nullptr;
+    float* h_loss = nullptr;
+    int32_t* h_idx = nullptr;
+    int idx_flip = 0;
+
+    std::vector<Learner> learners;
+    std::unique_ptr<Comm> comm;
+    std::vector<void*> allocations;
+
+    void* alloc(size_t bytes);
+    void* alloc_scratch_grad();
+    void refresh_shadow(Learner& ln, const float* w, cudaStream_t s);
+    void refresh_pad(Learner& ln, const float* w, cudaStream_t s);
+    void gather_batch(const float* feats_src, const int32_t* labels_src, const int32_t* idx, cudaStream_t s);
+    void sample_and_gather(Learner& ln, cudaStream_t s);
+    void forward_backward(const Learner& ln, const float* master, float* grad, float* loss_slot, cudaStream_t s);
+    void mix_and_update(double lr, const int32_t* taus);
+    const float* grad_point(const Learner& ln, const int32_t* taus);
+    const float* weight_ptr(int gid, int buf) const;
+    bool is_local(int gid) const;
+    void check_sync();
+    void step(double lr, const int32_t* taus, float* loss_out, const float* host_feats, const int32_t* host_labels,
+              const double* injected);
+    double gradient(const double* w, const int32_t* idx, int M, double* g_out);
+};
+
+void set_last_error(const std::string& s);
+const char* last_error();
+
+}  // namespace ab

@@ -1,0 +1,48 @@
+// GEMM front-end shared by the fp32 SIMT path (parity mode) and the tcgen05 bf16 path.
+//
+//   C[M,N] = alpha * sum_seg sum_k A_seg(m,k) B_seg(n,k)  (+ C if accumulate) (+ bias[n])
+//
+// A(m,k) = A[m*lda + k] (K-major) or A[k*lda + m] (MN-major); B(n,k) likewise. Up to two
+// K segments accumulate into one output tile (used for [x_t | h_{t-1}] x [W_ih | W_hh]
+// and for the two directions of dX = sum_d dZ_d W_ih_d).
+#pragma once
+
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace ab {
+
+struct GemmOperand {
+    const void* ptr = nullptr;
+    int64_t ld = 0;
+    bool mn = false;  // MN-major (the non-reduction index is contiguous)
+};
+
+struct GemmSeg {
+    GemmOperand a, b;
+    int K = 0;
+};
+
+struct GemmArgs {
+    int M = 0, N = 0;
+    GemmSeg seg[2];
+    int nseg = 1;
+    void* C = nullptr;
+    int64_t ldc = 0;
+    bool c_bf16 = false;
+    float alpha = 1.0f;
+    bool accumulate = false;
+    const float* bias = nullptr;
+};
+
+// fp32 operands, fp32 or bf16 output, any majorness (gemm_simt.cu).
+void gemm_simt(const GemmArgs& g, cudaStream_t s);
+// bf16 operands, tcgen05 + TMA + TMEM, fp32 accumulate (gemm_tc.cu).
+void gemm_tc(const GemmArgs& g, cudaStream_t s);
+
+inline void gemm(bool bf16_mode, const GemmArgs& g, cudaStream_t s) {
+    if (bf16_mode) gemm_tc(g, s); else gemm_simt(g, s);
+}
+
+}  // namespace ab

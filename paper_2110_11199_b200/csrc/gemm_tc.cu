@@ -1,0 +1,369 @@
+// tcgen05 bf16 GEMM for sm_100a: TMA-fed, mbarrier-pipelined, accumulators in TMEM.
+//
+// Persistent warp-specialised kernel, one CTA per SM:
+//   warp 0     TMA producer (one elected lane), STAGES-deep smem ring
+//   warp 1     MMA issuer (one lane) + TMEM allocator; 2 accumulator stages in TMEM
+//   warps 2-5  epilogue: tcgen05.ld -> alpha/bias/accumulate -> global
+// Tile 128 x BN (BN = 256 or 128) x 64, UMMA 128 x BN x 16. Either operand may be K-major
+// or MN-major (instruction-descriptor transpose bits; SW128 canonical layouts), so the
+// LSTM's dgrad / wgrad contractions run without explicit transposes.
+#include <cuda.h>
+
+#include <cstring>
+#include <mutex>
+#include <unordered_map>
+
+#include "gemm.hpp"
+#include "tc_ptx.cuh"
+
+namespace ab {
+
+namespace {
+
+constexpr int BM = 128, BK = 64;
+constexpr int kThreads = 192;
+
+struct TcParams {
+    CUtensorMap ta[2];
+    CUtensorMap tb[2];
+    int kblocks[2];
+    int nseg;
+    int M, N;
+    int m_tiles, n_tiles;
+    void* C;
+    int64_t ldc;
+    float alpha;
+    int accumulate;
+    const float* bias;
+    int vec_ok;
+};
+
+template <int BN>
+struct Cfg {
+    static constexpr int STAGES = BN == 256 ? 4 : 6;
+    static constexpr int A_BYTES = BM * BK * 2;
+    static constexpr int B_BYTES = BN * BK * 2;
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int TMEM_COLS = 2 * BN;  // two accumulator stages
+    static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+template <int BN, bool AMN, bool BMN, bool CBF16>
+__global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_constant__ TcParams p) {
+    using CF = Cfg<BN>;
+    constexpr int STAGES = CF::STAGES;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + STAGES * CF::A_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * CF::STAGE_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int num_tiles = p.m_tiles * p.n_tiles;
+    const int total_kb = p.kblocks[0] + (p.nseg > 1 ? p.kblocks[1] : 0);
+
+    if (warp == 0 && lane == 0) {
+        for (int i = 0; i < STAGES; ++i) { ptx::mbar_init(&full[i], 1); ptx::mbar_init(&empty[i], 1); }
+        for (int i = 0; i < 2; ++i) { ptx::mbar_init(&tfull[i], 1); ptx::mbar_init(&tempty[i], 4); }
+        ptx::fence_barrier_init();
+        for (int s = 0; s < p.nseg; ++s) { ptx::tma_prefetch(&p.ta[s]); ptx::tma_prefetch(&p.tb[s]); }
+    }
+    if (warp == 1) ptx::tmem_alloc(tmem_slot, CF::TMEM_COLS);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                const int m0 = (tile % p.m_tiles) * BM;
+                const int n0 = (tile / p.m_tiles) * BN;
+                for (int kb = 0; kb < total_kb; ++kb) {
+                    const int s = kb < p.kblocks[0] ? 0 : 1;
+                    const int k0 = (s == 0 ? kb : kb - p.kblocks[0]) * BK;
+                    ptx::mbar_wait(&empty[stage], phase ^ 1);
+                    ptx::mbar_arrive_expect_tx(&full[stage], CF::STAGE_BYTES);
+                    uint8_t* a_dst = sA + stage * CF::A_BYTES;
+                    uint8_t* b_dst = sB + stage * CF::B_BYTES;
+                    if (AMN) {
+#pragma unroll
+                        for (int j = 0; j < BM / 64; ++j)
+                            ptx::tma_load_2d(a_dst + j * 64 * BK * 2, &p.ta[s], &full[stage], m0 + 64 * j, k0);
+                    } else {
+                        ptx::tma_load_2d(a_dst, &p.ta[s], &full[stage], k0, m0);
+                    }
+                    if (BMN) {
+#pragma unroll
+                        for (int j = 0; j < BN / 64; ++j)
+                            ptx::tma_load_2d(b_dst + j * 64 * BK * 2, &p.tb[s], &full[stage], n0 + 64 * j, k0);
+                    } else {
+                        ptx::tma_load_2d(b_dst, &p.tb[s], &full[stage], k0, n0);
+                    }
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = ptx::idesc_bf16_f32(BM, BN, AMN, BMN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t aphase = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                ptx::mbar_wait(&tempty[acc], aphase ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t tmem_d = tmem_base + acc * BN;
+                for (int kb = 0; kb < total_kb; ++kb) {
+                    ptx::mbar_wait(&full[stage], phase);
+                    ptx::tc_fence_after();
+                    const uint32_t a_addr = ptx::smem_u32(sA + stage * CF::A_BYTES);
+                    const uint32_t b_addr = ptx::smem_u32(sB + stage * CF::B_BYTES);
+#pragma unroll
+                    for (int kk = 0; kk < BK / 16; ++kk) {
+                        const uint64_t ad = AMN ? ptx::umma_desc_sw128(a_addr + kk * 2048, 64 * BK * 2, 1024)
+                                                : ptx::umma_desc_sw128(a_addr + kk * 32, 16, 1024);
+                        const uint64_t bd = BMN ? ptx::umma_desc_sw128(b_addr + kk * 2048, 64 * BK * 2, 1024)
+                                                : ptx::umma_desc_sw128(b_addr + kk * 32, 16, 1024);
+                        ptx::mma_bf16(tmem_d, ad, bd, idesc, (kb | kk) != 0);
+                    }
+                    ptx::mma_commit(&empty[stage]);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+                ptx::mma_commit(&tfull[acc]);
+                if (++acc == 2) { acc = 0; aphase ^= 1; }
+            }
+        }
+    } else {
+        // epilogue warps 2..5 -> TMEM lane quarter (warp % 4)
+        const int q = warp % 4;
+        const int row_in_tile = q * 32 + lane;
+        int acc = 0;
+        uint32_t aphase = 0;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            const int m0 = (tile % p.m_tiles) * BM;
+            const int n0 = (tile / p.m_tiles) * BN;
+            ptx::mbar_wait(&tfull[acc], aphase);
+            ptx::tc_fence_after();
+            const int gm = m0 + row_in_tile;
+            const bool row_ok = gm < p.M;
+#pragma unroll 1
+            for (int c = 0; c < BN; c += 32) {
+                uint32_t r[32];
+                ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c, r);
+                ptx::tmem_ld_wait();
+                if (c + 32 >= BN) {
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+                }
+                if (!row_ok) continue;
+                const int gn0 = n0 + c;
+                if (gn0 >= p.N) continue;
+                float v[32];
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = p.alpha * __uint_as_float(r[i]);
+                if (p.bias) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i)
+                        if (gn0 + i < p.N) v[i] += p.bias[gn0 + i];
+                }
+                if constexpr (CBF16) {
+                    bf16* crow = reinterpret_cast<bf16*>(p.C) + static_cast<int64_t>(gm) * p.ldc + gn0;
+                    if (p.vec_ok && gn0 + 32 <= p.N) {
+#pragma unroll
+                        for (int i = 0; i < 32; i += 8) {
+                            uint4 u;
+                            if (p.accumulate) {
+                                const uint4 o = *reinterpret_cast<const uint4*>(crow + i);
+                                const bf16* ob = reinterpret_cast<const bf16*>(&o);
+#pragma unroll
+                                for (int j = 0; j < 8; ++j) v[i + j] += __bfloat162float(ob[j]);
+                            }
+                            bf16* ub = reinterpret_cast<bf16*>(&u);
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) ub[j] = __float2bfloat16_rn(v[i + j]);
+                            *reinterpret_cast<uint4*>(crow + i) = u;
+                        }
+                    } else {
+                        for (int i = 0; i < 32 && gn0 + i < p.N; ++i) {
+                            float x = v[i];
+                            if (p.accumulate) x += __bfloat162float(crow[i]);
+                            crow[i] = __float2bfloat16_rn(x);
+                        }
+                    }
+                } else {
+                    float* crow = reinterpret_cast<float*>(p.C) + static_cast<int64_t>(gm) * p.ldc + gn0;
+                    if (p.vec_ok && gn0 + 32 <= p.N) {
+#pragma unroll
+                        for (int i = 0; i < 32; i += 4) {
+                            float4 u = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+                            if (p.accumulate) {
+                                const float4 o = *reinterpret_cast<const float4*>(crow + i);
+                                u.x += o.x; u.y += o.y; u.z += o.z; u.w += o.w;
+                            }
+                            *reinterpret_cast<float4*>(crow + i) = u;
+                        }
+                    } else {
+                        for (int i = 0; i < 32 && gn0 + i < p.N; ++i) {
+                            float x = v[i];
+                            if (p.accumulate) x += crow[i];
+                            crow[i] = x;
+                        }
+                    }
+                }
+            }
+            if (++acc == 2) { acc = 0; aphase ^= 1; }
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) ptx::tmem_dealloc(tmem_base, CF::TMEM_COLS);
+}
+
+// ---- host side -------------------------------------------------------------
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+    static EncodeFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(p);
+    });
+    AB_CHECK(fn != nullptr, ADPSGD_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    return fn;
+}
+
+// bf16 2-D tensor map, SWIZZLE_128B, box {64, box_outer}.
+void make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, int64_t ld_elems, uint32_t box_outer) {
+    AB_CHECK((reinterpret_cast<uintptr_t>(base) & 15) == 0, ADPSGD_E_DIMENSION, "TMA base must be 16B aligned");
+    AB_CHECK(((ld_elems * 2) & 15) == 0, ADPSGD_E_DIMENSION, "TMA row pitch must be a multiple of 16 bytes");
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld_elems) * 2};
+    cuuint32_t box[2] = {64, box_outer};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    AB_CHECK(r == CUDA_SUCCESS, ADPSGD_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+}
+
+template <int BN, bool AMN, bool BMN, bool CBF16>
+void launch_cfg(const TcParams& p, cudaStream_t s) {
+    auto k = gemm_tc_kernel<BN, AMN, BMN, CBF16>;
+    static bool attr = false;
+    if (!attr) {
+        AB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
+        attr = true;
+    }
+    const int tiles = p.m_tiles * p.n_tiles;
+    const int grid = tiles < num_sms() ? tiles : num_sms();
+    k<<<grid, kThreads, Cfg<BN>::SMEM, s>>>(p);
+    count_launch();
+    AB_CUDA(cudaGetLastError());
+}
+
+template <int BN>
+void dispatch(const TcParams& p, bool amn, bool bmn, bool cbf16, cudaStream_t s) {
+    const int key = (amn ? 4 : 0) | (bmn ? 2 : 0) | (cbf16 ? 1 : 0);
+    switch (key) {
+        case 0: launch_cfg<BN, false, false, false>(p, s); break;
+        case 1: launch_cfg<BN, false, false, true>(p, s); break;
+        case 2: launch_cfg<BN, false, true, false>(p, s); break;
+        case 3: launch_cfg<BN, false, true, true>(p, s); break;
+        case 4: launch_cfg<BN, true, false, false>(p, s); break;
+        case 5: launch_cfg<BN, true, false, true>(p, s); break;
+        case 6: launch_cfg<BN, true, true, false>(p, s); break;
+        default: launch_cfg<BN, true, true, true>(p, s); break;
+    }
+}
+
+struct PlanKey {
+    const void* a[2]; const void* b[2];
+    int64_t lda[2], ldb[2];
+    int K[2], M, N, nseg, bn;
+    bool amn, bmn;
+    bool operator==(const PlanKey& o) const { return std::memcmp(this, &o, sizeof(PlanKey)) == 0; }
+};
+struct PlanHash {
+    size_t operator()(const PlanKey& k) const {
+        const uint64_t* w = reinterpret_cast<const uint64_t*>(&k);
+        uint64_t h = 1469598103934665603ULL;
+        for (size_t i = 0; i < sizeof(PlanKey) / 8; ++i) { h ^= w[i]; h *= 1099511628211ULL; }
+        return h;
+    }
+};
+
+}  // namespace
+
+void gemm_tc(const GemmArgs& g, cudaStream_t s) {
+    if (g.M <= 0 || g.N <= 0) return;
+    AB_CHECK(g.nseg >= 1 && g.nseg <= 2, ADPSGD_E_DIMENSION, "gemm_tc: 1 or 2 K segments");
+    const bool amn = g.seg[0].a.mn, bmn = g.seg[0].b.mn;
+    for (int i = 1; i < g.nseg; ++i)
+        AB_CHECK(g.seg[i].a.mn == amn && g.seg[i].b.mn == bmn, ADPSGD_E_DIMENSION,
+                 "gemm_tc: segments must share operand majorness");
+    const int m_tiles = (g.M + BM - 1) / BM;
+    const int bn = (g.N > 128 && m_tiles * ((g.N + 255) / 256) >= num_sms() / 2) ? 256 : 128;
+
+    static std::unordered_map<PlanKey, TcParams, PlanHash> cache;
+    static std::mutex mu;
+    PlanKey key;
+    std::memset(&key, 0, sizeof(key));
+    for (int i = 0; i < g.nseg; ++i) {
+        key.a[i] = g.seg[i].a.ptr; key.b[i] = g.seg[i].b.ptr;
+        key.lda[i] = g.seg[i].a.ld; key.ldb[i] = g.seg[i].b.ld; key.K[i] = g.seg[i].K;
+    }
+    key.M = g.M; key.N = g.N; key.nseg = g.nseg; key.bn = bn; key.amn = amn; key.bmn = bmn;
+
+    TcParams p;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) {
+            p = it->second;
+        } else {
+            std::memset(&p, 0, sizeof(p));
+            for (int i = 0; i < g.nseg; ++i) {
+                const GemmSeg& sg = g.seg[i];
+                AB_CHECK(sg.K > 0, ADPSGD_E_DIMENSION, "gemm_tc: K must be > 0");
+                if (amn) make_map(&p.ta[i], sg.a.ptr, g.M, sg.K, sg.a.ld, BK);
+                else make_map(&p.ta[i], sg.a.ptr, sg.K, g.M, sg.a.ld, BM);
+                if (bmn) make_map(&p.tb[i], sg.b.ptr, g.N, sg.K, sg.b.ld, BK);
+                else make_map(&p.tb[i], sg.b.ptr, sg.K, g.N, sg.b.ld, bn);
+                p.kblocks[i] = (sg.K + BK - 1) / BK;
+            }
+            p.nseg = g.nseg;
+            p.M = g.M; p.N = g.N;
+            p.m_tiles = m_tiles;
+            p.n_tiles = (g.N + bn - 1) / bn;
+            if (cache.size() > 4096) cache.clear();
+            cache.emplace(key, p);
+        }
+    }
+    p.C = g.C;
+    p.ldc = g.ldc;
+    p.alpha = g.alpha;
+    p.accumulate = g.accumulate;
+    p.bias = g.bias;
+    const int esz = g.c_bf16 ? 2 : 4;
+    p.vec_ok = ((reinterpret_cast<uintptr_t>(g.C) & 15) == 0) && ((g.ldc * esz) % 16 == 0);
+    if (bn == 256) dispatch<256>(p, amn, bmn, g.c_bf16, s);
+    else dispatch<128>(p, amn, bmn, g.c_bf16, s);
+}
+
+}  // namespace ab

@@ -1,0 +1,463 @@
+// Pointwise, reduction and update kernels of the ADPSGD learner step (sm_100a).
+// All are HBM-bound: vectorised, grid-stride, grids sized in multiples of the SM count.
+#include "kernels.cuh"
+
+namespace ab {
+
+int64_t g_launch_count = 0;
+
+namespace {
+
+constexpr int kMaxTab = 64;
+struct PtrTab { const float* p[kMaxTab]; };
+struct MutTab { float* p[kMaxTab]; };
+struct BfTab { bf16* p[kMaxTab]; };
+
+inline int grid_for(int64_t work, int threads = 256, int per_sm = 8) {
+    int64_t g = (work + threads - 1) / threads;
+    const int64_t cap = static_cast<int64_t>(num_sms()) * per_sm;
+    if (g > cap) g = cap;
+    return static_cast<int>(g < 1 ? 1 : g);
+}
+
+// ---- gather ----
+template <typename AT>
+__global__ void gather_kernel(const float* __restrict__ feats, const int32_t* __restrict__ labels,
+                              const int32_t* __restrict__ idx, int B, int T, int I, int ldx, AT* __restrict__ X,
+                              int32_t* __restrict__ lab) {
+    const int64_t total = static_cast<int64_t>(T) * B * ldx;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int i = static_cast<int>(e % ldx);
+        const int64_t r = e / ldx;  // r = t*B + b
+        const int b = static_cast<int>(r % B), t = static_cast<int>(r / B);
+        const int64_t n = idx[b];
+        const float v = i < I ? feats[(n * T + t) * I + i] : 0.f;
+        X[e] = from_f<AT>(v);
+        if (i == 0) lab[r] = labels[n * T + t];
+    }
+}
+
+// ---- LSTM cell ----
+template <typename AT>
+__global__ void cell_fwd_kernel(const float* __restrict__ z, int ldz, const float* __restrict__ c_prev, int ldc,
+                                float* __restrict__ gates, int ldg, float* __restrict__ c, AT* __restrict__ h, int ldh,
+                                int B, int H) {
+    const int64_t total = static_cast<int64_t>(B) * H;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int b = static_cast<int>(e / H), j = static_cast<int>(e % H);
+        const float* zr = z + static_cast<int64_t>(b) * ldz;
+        const float ig = 1.f / (1.f + expf(-zr[j]));
+        const float fg = 1.f / (1.f + expf(-zr[H + j]));
+        const float gg = tanhf(zr[2 * H + j]);
+        const float og = 1.f / (1.f + expf(-zr[3 * H + j]));
+        const float cp = c_prev ? c_prev[static_cast<int64_t>(b) * ldc + j] : 0.f;
+        const float cn = fg * cp + ig * gg;
+        float* gr = gates + static_cast<int64_t>(b) * ldg;
+        gr[j] = ig; gr[H + j] = fg; gr[2 * H + j] = gg; gr[3 * H + j] = og;
+        c[static_cast<int64_t>(b) * ldc + j] = cn;
+        h[static_cast<int64_t>(b) * ldh + j] = from_f<AT>(og * tanhf(cn));
+    }
+}
+
+template <typename AT>
+__global__ void cell_bwd_kernel(const float* __restrict__ dH, int lddh, const float* __restrict__ dh_rec,
+                                float* __restrict__ dc_rec, int first, const float* __restrict__ gates, int ldg,
+                                const float* __restrict__ c, const float* __restrict__ c_prev, int ldc,
+                                AT* __restrict__ dz, int lddz, int B, int H) {
+    const int64_t total = static_cast<int64_t>(B) * H;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int b = static_cast<int>(e / H), j = static_cast<int>(e % H);
+        float dh = dH[static_cast<int64_t>(b) * lddh + j];
+        float dcr = 0.f;
+        if (!first) { dh += dh_rec[e]; dcr = dc_rec[e]; }
+        const float* gr = gates + static_cast<int64_t>(b) * ldg;
+        const float ig = gr[j], fg = gr[H + j], gg = gr[2 * H + j], og = gr[3 * H + j];
+        const float tc = tanhf(c[static_cast<int64_t>(b) * ldc + j]);
+        const float cp = c_prev ? c_prev[static_cast<int64_t>(b) * ldc + j] : 0.f;
+        const float dc = dcr + dh * og * (1.f - tc * tc);
+        AT* dzr = dz + static_cast<int64_t>(b) * lddz;
+        dzr[j] = from_f<AT>(dc * gg * ig * (1.f - ig));
+        dzr[H + j] = from_f<AT>(dc * cp * fg * (1.f - fg));
+        dzr[2 * H + j] = from_f<AT>(dc * ig * (1.f - gg * gg));
+        dzr[3 * H + j] = from_f<AT>(dh * tc * og * (1.f - og));
+        dc_rec[e] = dc * fg;
+    }
+}
+
+// ---- softmax cross-entropy (one block per row) ----
+__device__ __forceinline__ float block_reduce(float v, bool is_max, float* sh) {
+    const int lane = threadIdx.x % 32, w = threadIdx.x / 32;
+    for (int o = 16; o; o >>= 1) {
+        const float u = __shfl_xor_sync(0xffffffffu, v, o);
+        v = is_max ? fmaxf(v, u) : v + u;
+    }
+    __syncthreads();
+    if (lane == 0) sh[w] = v;
+    __syncthreads();
+    const int nw = blockDim.x / 32;
+    v = threadIdx.x < nw ? sh[threadIdx.x] : (is_max ? -INFINITY : 0.f);
+    if (w == 0)
+        for (int o = 16; o; o >>= 1) {
+            const float u = __shfl_xor_sync(0xffffffffu, v, o);
+            v = is_max ? fmaxf(v, u) : v + u;
+        }
+    if (threadIdx.x == 0) sh[0] = v;
+    __syncthreads();
+    return sh[0];
+}
+
+template <typename AT>
+__global__ void __launch_bounds__(256) softmax_ce_kernel(const float* __restrict__ logits,
+                                                         const int32_t* __restrict__ labels, int C, float scale,
+                                                         AT* __restrict__ dlogits, float* __restrict__ row_loss) {
+    __shared__ float sh[32];
+    const int64_t r = blockIdx.x;
+    const float* x = logits + r * C;
+    float mx = -INFINITY;
+    for (int i = threadIdx.x; i < C; i += blockDim.x) mx = fmaxf(mx, x[i]);
+    mx = block_reduce(mx, true, sh);
+    float se = 0.f;
+    for (int i = threadIdx.x; i < C; i += blockDim.x) se += expf(x[i] - mx);
+    se = block_reduce(se, false, sh);
+    const float lse = mx + logf(se);
+    const int lab = labels[r];
+    AT* d = dlogits + r * C;
+    for (int i = threadIdx.x; i < C; i += blockDim.x) {
+        float p = expf(x[i] - lse) * scale;
+        if (i == lab) p -= scale;
+        d[i] = from_f<AT>(p);
+    }
+    if (threadIdx.x == 0) row_loss[r] = lse - x[lab];
+}
+
+// ---- deterministic column sums ----
+template <typename AT>
+__global__ void colsum_partial_kernel(const AT* __restrict__ X, int64_t ld, int R, int N, int rows_per_chunk,
+                                      float* __restrict__ part) {
+    const int n = blockIdx.x * blockDim.x + threadIdx.x;
+    const int chunk = blockIdx.y;
+    if (n >= N) return;
+    const int r0 = chunk * rows_per_chunk;
+    const int r1 = min(R, r0 + rows_per_chunk);
+    float s = 0.f;
+    for (int r = r0; r < r1; ++r) s += to_f<AT>(X[static_cast<int64_t>(r) * ld + n]);
+    part[static_cast<int64_t>(chunk) * N + n] = s;
+}
+__global__ void colsum_final_kernel(const float* __restrict__ part, int chunks, int N, float* __restrict__ out) {
+    const int n = blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= N) return;
+    float s = 0.f;
+    for (int c = 0; c < chunks; ++c) s += part[static_cast<int64_t>(c) * N + n];
+    out[n] = s;
+}
+
+__global__ void sum_kernel(const float* __restrict__ x, int n, float scale, float* __restrict__ out) {
+    __shared__ float sh[32];
+    float s = 0.f;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s += x[i];
+    s = block_reduce(s, false, sh);
+    if (threadIdx.x == 0) out[0] = s * scale;
+}
+
+__global__ void f32_to_bf16_kernel(const float* __restrict__ in, bf16* __restrict__ out, int64_t n) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        out[i] = __float2bfloat16_rn(in[i]);
+}
+__global__ void pad_rows_kernel(const float* __restrict__ in, int64_t ld_in, bf16* __restrict__ out, int64_t ld_out,
+                                int rows, int cols) {
+    const int64_t total = static_cast<int64_t>(rows) * ld_out;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = e / ld_out, c = e % ld_out;
+        out[e] = __float2bfloat16_rn(c < cols ? in[r * ld_in + c] : 0.f);
+    }
+}
+
+// ---- mixing / update ----
+__global__ void mix3_kernel(int64_t n, const float* __restrict__ w, const float* __restrict__ wl,
+                            const float* __restrict__ wr, const float* __restrict__ g, float lr,
+                            float* __restrict__ out, bf16* __restrict__ shadow) {
+    const float third = 1.0f / 3.0f;
+    const int64_t n4 = n / 4;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4; i += stride) {
+        const float4 a = reinterpret_cast<const float4*>(w)[i];
+        const float4 b = reinterpret_cast<const float4*>(wl)[i];
+        const float4 c = reinterpret_cast<const float4*>(wr)[i];
+        const float4 d = reinterpret_cast<const float4*>(g)[i];
+        float4 o;
+        o.x = (a.x + b.x + c.x) * third - lr * d.x;
+        o.y = (a.y + b.y + c.y) * third - lr * d.y;
+        o.z = (a.z + b.z + c.z) * third - lr * d.z;
+        o.w = (a.w + b.w + c.w) * third - lr * d.w;
+        reinterpret_cast<float4*>(out)[i] = o;
+        if (shadow) {
+            __nv_bfloat162 lo = __floats2bfloat162_rn(o.x, o.y), hi = __floats2bfloat162_rn(o.z, o.w);
+            reinterpret_cast<__nv_bfloat162*>(shadow)[2 * i] = lo;
+            reinterpret_cast<__nv_bfloat162*>(shadow)[2 * i + 1] = hi;
+        }
+    }
+    for (int64_t i = n4 * 4 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
+        const float o = (w[i] + wl[i] + wr[i]) * third - lr * g[i];
+        out[i] = o;
+        if (shadow) shadow[i] = __float2bfloat16_rn(o);
+    }
+}
+
+__global__ void d1d_kernel(int64_t n, int L, PtrTab w, const float* __restrict__ w_sum, int nloc, PtrTab g, float lr,
+                           MutTab out, BfTab sh) {
+    const float invL = 1.0f / static_cast<float>(L);
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        float s;
+        if (w_sum) {
+            s = w_sum[i];
+        } else {
+            s = 0.f;
+            for (int l = 0; l < L; ++l) s += w.p[l][i];
+        }
+        const float mean = s * invL;
+        for (int j = 0; j < nloc; ++j) {
+            const float o = mean - lr * g.p[j][i];
+            out.p[j][i] = o;
+            if (sh.p[j]) sh.p[j][i] = __float2bfloat16_rn(o);
+        }
+    }
+}
+
+__global__ void sdpsgd_kernel(int64_t n, int L, const float* __restrict__ w, PtrTab g, const float* __restrict__ g_sum,
+                              int nloc, float lr, MutTab out, BfTab sh) {
+    const float invL = 1.0f / static_cast<float>(L);
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        float s;
+        if (g_sum) {
+            s = g_sum[i];
+        } else {
+            s = 0.f;
+            for (int l = 0; l < L; ++l) s += g.p[l][i];
+        }
+        const float o = w[i] - lr * (s * invL);
+        for (int j = 0; j < nloc; ++j) {
+            out.p[j][i] = o;
+            if (sh.p[j]) sh.p[j][i] = __float2bfloat16_rn(o);
+        }
+    }
+}
+
+struct DenseT { float t[kMaxTab]; int idx[kMaxTab]; int cnt; };
+struct DenseArgs { DenseT col[16]; };
+
+__global__ void dense_mix_kernel(int64_t n, PtrTab w, DenseArgs T, int nloc, PtrTab g, float lr, MutTab out,
+                                 BfTab sh) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        for (int j = 0; j < nloc; ++j) {
+            float s = 0.f;
+            for (int q = 0; q < T.col[j].cnt; ++q) s += T.col[j].t[q] * w.p[T.col[j].idx[q]][i];
+            const float o = s - lr * g.p[j][i];
+            out.p[j][i] = o;
+            if (sh.p[j]) sh.p[j][i] = __float2bfloat16_rn(o);
+        }
+    }
+}
+
+__global__ void maxdiff_kernel(int64_t n, const float* __restrict__ a, const float* __restrict__ b, float* out) {
+    float m = 0.f;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        m = fmaxf(m, fabsf(a[i] - b[i]));
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<int*>(out), __float_as_int(m));
+}
+
+__device__ __forceinline__ uint64_t hash64(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+}
+__device__ __forceinline__ float u01(uint64_t h) { return (static_cast<float>(h >> 40) + 0.5f) * (1.0f / 16777216.0f); }
+
+// Synthetic SWB-shaped frames: label ~ U[0,C) per frame with a slowly varying state
+// (runs of frames share a label), features N(0,1) + 0.75 * class prototype (+/-1).
+__global__ void synth_kernel(float* __restrict__ feats, int32_t* __restrict__ labels, int n_seg, int T, int I, int C,
+                             uint64_t seed) {
+    const int64_t total = static_cast<int64_t>(n_seg) * T * I;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int i = static_cast<int>(e % I);
+        const int64_t nt = e / I;
+        const int t = static_cast<int>(nt % T);
+        const int64_t n = nt / T;
+        const uint64_t lh = hash64(seed ^ hash64(static_cast<uint64_t>(n) * 64 + t / 4));
+        const int lab = static_cast<int>(lh % static_cast<uint64_t>(C));
+        const uint64_t h1 = hash64(seed + 0x1234567ULL + static_cast<uint64_t>(e) * 2);
+        const uint64_t h2 = hash64(seed + 0x89abcdefULL + static_cast<uint64_t>(e) * 2 + 1);
+        const float r = sqrtf(-2.f * logf(u01(h1)));
+        const float gsn = r * cospif(2.f * u01(h2));
+        const float proto = (hash64(static_cast<uint64_t>(lab) * 1315423911ULL + i) & 1) ? 0.75f : -0.75f;
+        feats[e] = gsn + proto;
+        if (i == 0) labels[nt] = lab;
+    }
+}
+
+__global__ void delay_kernel(uint64_t ns) {
+    uint64_t t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 >= ns) break;
+        __nanosleep(1000);
+    }
+}
+
+}  // namespace
+
+template <typename AT>
+void launch_gather(const float* feats, const int32_t* labels, const int32_t* idx, int B, int T, int I, int ldx, AT* X,
+                   int32_t* lab, cudaStream_t s) {
+    const int64_t total = static_cast<int64_t>(T) * B * ldx;
+    gather_kernel<AT><<<grid_for(total), 256, 0, s>>>(feats, labels, idx, B, T, I, ldx, X, lab);
+    count_launch();
+}
+
+template <typename AT>
+void launch_cell_fwd(const float* z, int ldz, const float* c_prev, int ldc, float* gates, int ldg, float* c, AT* h,
+                     int ldh, int B, int H, cudaStream_t s) {
+    cell_fwd_kernel<AT><<<grid_for(static_cast<int64_t>(B) * H), 256, 0, s>>>(z, ldz, c_prev, ldc, gates, ldg, c, h,
+                                                                                ldh, B, H);
+    count_launch();
+}
+
+template <typename AT>
+void launch_cell_bwd(const float* dH, int lddh, const float* dh_rec, float* dc_rec, bool first, const float* gates,
+                     int ldg, const float* c, const float* c_prev, int ldc, AT* dz, int lddz, int B, int H,
+                     cudaStream_t s) {
+    cell_bwd_kernel<AT><<<grid_for(static_cast<int64_t>(B) * H), 256, 0, s>>>(
+        dH, lddh, dh_rec, dc_rec, first ? 1 : 0, gates, ldg, c, c_prev, ldc, dz, lddz, B, H);
+    count_launch();
+}
+
+template <typename AT>
+void launch_softmax_ce(const float* logits, const int32_t* labels, int R, int C, float scale, AT* dlogits,
+                       float* row_loss, cudaStream_t s) {
+    softmax_ce_kernel<AT><<<R, 256, 0, s>>>(logits, labels, C, scale, dlogits, row_loss);
+    count_launch();
+}
+
+template <typename AT>
+void launch_colsum(const AT* X, int64_t ld, int R, int N, float* out, float* ws, int64_t ws_elems, cudaStream_t s) {
+    int chunks = (R + 127) / 128;
+    if (chunks > 128) chunks = 128;
+    while (chunks > 1 && static_cast<int64_t>(chunks) * N > ws_elems) chunks /= 2;
+    const int rpc = (R + chunks - 1) / chunks;
+    dim3 grid((N + 255) / 256, chunks);
+    colsum_partial_kernel<AT><<<grid, 256, 0, s>>>(X, ld, R, N, rpc, ws);
+    colsum_final_kernel<<<(N + 255) / 256, 256, 0, s>>>(ws, chunks, N, out);
+    count_launch(2);
+}
+
+void launch_sum(const float* x, int n, float scale, float* out, cudaStream_t s) {
+    sum_kernel<<<1, 1024, 0, s>>>(x, n, scale, out);
+    count_launch();
+}
+
+void launch_f32_to_bf16(const float* in, bf16* out, int64_t n, cudaStream_t s) {
+    f32_to_bf16_kernel<<<grid_for(n), 256, 0, s>>>(in, out, n);
+    count_launch();
+}
+void launch_pad_rows_bf16(const float* in, int64_t ld_in, bf16* out, int64_t ld_out, int rows, int cols,
+                          cudaStream_t s) {
+    pad_rows_kernel<<<grid_for(static_cast<int64_t>(rows) * ld_out), 256, 0, s>>>(in, ld_in, out, ld_out, rows, cols);
+    count_launch();
+}
+
+void launch_mix3(int64_t n, const float* w, const float* wl, const float* wr, const float* g, float lr, float* w_out,
+                 bf16* shadow, cudaStream_t s) {
+    mix3_kernel<<<grid_for((n + 3) / 4, 256, 4), 256, 0, s>>>(n, w, wl, wr, g, lr, w_out, shadow);
+    count_launch();
+}
+
+void launch_d1d(int64_t n, int L, const float* const* w_tab, const float* w_sum, int nloc, const float* const* g_tab,
+                float lr, float* const* out_tab, bf16* const* shadow_tab, cudaStream_t s) {
+    AB_CHECK(L <= kMaxTab && nloc <= kMaxTab, ADPSGD_E_CONFIG, "too many learners for one device");
+    PtrTab w{}, g{};
+    MutTab o{};
+    BfTab sh{};
+    if (!w_sum)
+        for (int i = 0; i < L; ++i) w.p[i] = w_tab[i];
+    for (int j = 0; j < nloc; ++j) { g.p[j] = g_tab[j]; o.p[j] = out_tab[j]; sh.p[j] = shadow_tab[j]; }
+    d1d_kernel<<<grid_for(n, 256, 4), 256, 0, s>>>(n, L, w, w_sum, nloc, g, lr, o, sh);
+    count_launch();
+}
+
+void launch_sdpsgd(int64_t n, int L, const float* w, const float* const* g_tab, const float* g_sum, int nloc,
+                   float lr, float* const* out_tab, bf16* const* shadow_tab, cudaStream_t s) {
+    AB_CHECK(L <= kMaxTab && nloc <= kMaxTab, ADPSGD_E_CONFIG, "too many learners for one device");
+    PtrTab g{};
+    MutTab o{};
+    BfTab sh{};
+    if (!g_sum)
+        for (int i = 0; i < L; ++i) g.p[i] = g_tab[i];
+    for (int j = 0; j < nloc; ++j) { o.p[j] = out_tab[j]; sh.p[j] = shadow_tab[j]; }
+    sdpsgd_kernel<<<grid_for(n, 256, 4), 256, 0, s>>>(n, L, w, g, g_sum, nloc, lr, o, sh);
+    count_launch();
+}
+
+void launch_dense_mix(int64_t n, int L, const float* const* w_tab, const double* T, const int* cols, int nloc,
+                      const float* const* g_tab, float lr, float* const* out_tab, bf16* const* shadow_tab,
+                      cudaStream_t s) {
+    AB_CHECK(L <= kMaxTab && nloc <= 16, ADPSGD_E_CONFIG, "too many learners for dense mixing");
+    PtrTab w{}, g{};
+    MutTab o{};
+    BfTab sh{};
+    DenseArgs da{};
+    for (int i = 0; i < L; ++i) w.p[i] = w_tab[i];
+    for (int j = 0; j < nloc; ++j) {
+        g.p[j] = g_tab[j]; o.p[j] = out_tab[j]; sh.p[j] = shadow_tab[j];
+        int cnt = 0;
+        for (int i = 0; i < L; ++i) {
+            const double t = T[i * L + cols[j]];
+            if (t != 0.0) { da.col[j].t[cnt] = static_cast<float>(t); da.col[j].idx[cnt] = i; ++cnt; }
+        }
+        da.col[j].cnt = cnt;
+    }
+    dense_mix_kernel<<<grid_for(n, 256, 4), 256, 0, s>>>(n, w, da, nloc, g, lr, o, sh);
+    count_launch();
+}
+
+void launch_maxdiff(int64_t n, const float* a, const float* b, float* out, cudaStream_t s) {
+    maxdiff_kernel<<<grid_for(n, 256, 4), 256, 0, s>>>(n, a, b, out);
+    count_launch();
+}
+
+void launch_synth(float* feats, int32_t* labels, int n_seg, int T, int I, int C, uint64_t seed, cudaStream_t s) {
+    synth_kernel<<<grid_for(static_cast<int64_t>(n_seg) * T * I), 256, 0, s>>>(feats, labels, n_seg, T, I, C, seed);
+    count_launch();
+}
+
+void launch_delay(uint64_t ns, cudaStream_t s) {
+    delay_kernel<<<1, 1, 0, s>>>(ns);
+    count_launch();
+}
+
+#define AB_INST(AT)                                                                                                  \
+    template void launch_gather<AT>(const float*, const int32_t*, const int32_t*, int, int, int, int, AT*, int32_t*, \
+                                    cudaStream_t);                                                                  \
+    template void launch_cell_fwd<AT>(const float*, int, const float*, int, float*, int, float*, AT*, int, int, int, \
+                                      cudaStream_t);                                                                \
+    template void launch_cell_bwd<AT>(const float*, int, const float*, float*, bool, const float*, int, const float*, \
+                                      const float*, int, AT*, int, int, int, cudaStream_t);                         \
+    template void launch_softmax_ce<AT>(const float*, const int32_t*, int, int, float, AT*, float*, cudaStream_t);  \
+    template void launch_colsum<AT>(const AT*, int64_t, int, int, float*, float*, int64_t, cudaStream_t);
+AB_INST(float)
+AB_INST(bf16)
+#undef AB_INST
+
+}  // namespace ab

@@ -1,0 +1,325 @@
+"""Host-side mirror of the reference learner API (proj/include/adpsgd/engine.hpp), backed by
+the B200 C ABI. Same names, argument meaning and error behaviour as the reference:
+
+  Strategy / strategy_name / strategy_from_name      engine.hpp:17-20, engine.cpp:25-43
+  LrSchedule / lr_at                                 engine.hpp:25-33, engine.cpp:45-58
+  StrategyConfig.validate                            engine.hpp:35-50, engine.cpp:60-77
+  permutation_for_iteration                          engine.hpp:85-86, engine.cpp:130-134
+  LearnerGroup.step (step_sdpsgd / step_adpsgd_mixing / step_d1d / step_generic_staleness)
+                                                     engine.hpp:88-105, engine.cpp:136-204
+  LstmObjective (Objective plugin)                   objectives.hpp:45-69
+
+The learners' models, gradients and activations live on the GPU; only O(M) sampling
+indices and the pairing (O(L)) are produced on the host, bit-exactly as the reference does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .errors import ConfigError, InvalidStateError
+
+
+class Strategy(enum.IntEnum):
+    SDPSGD = 0
+    ADPSGD_FM = 1
+    ADPSGD_RM = 2
+    ADPSGD_D1D = 3
+    GENERIC = 4
+
+
+class MixKind(enum.IntEnum):
+    FIXED_RING = 0
+    RANDOM_RING = 1
+    UNIFORM = 2
+
+
+class Precision(enum.IntEnum):
+    FP32 = 0
+    BF16 = 1
+
+
+_NAMES = {Strategy.SDPSGD: "SDPSGD", Strategy.ADPSGD_FM: "ADPSGD_FM", Strategy.ADPSGD_RM: "ADPSGD_RM",
+          Strategy.ADPSGD_D1D: "ADPSGD_D1D", Strategy.GENERIC: "GENERIC"}
+
+
+def strategy_name(s: Strategy) -> str:
+    return _NAMES.get(Strategy(s), "unknown")
+
+
+def strategy_from_name(name: str) -> Strategy:
+    for s, n in _NAMES.items():
+        if n == name:
+            return s
+    raise ConfigError("unknown strategy: " + name)
+
+
+@dataclass
+class LrSchedule:
+    base_lr: float = 0.1
+    peak_lr: float = 0.1
+    warmup_epochs: int = 0
+    anneal_factor: float = 0.7071067811865476
+    anneal_start_epoch: int = 1 << 30
+
+
+def lr_at(s: LrSchedule, epoch: int) -> float:
+    if epoch < 0:
+        raise InvalidStateError("lr_at: epoch must be >= 0")
+    return float(_lib.lib().adpsgd_lr_at(s.base_lr, s.peak_lr, s.warmup_epochs, s.anneal_factor,
+                                         s.anneal_start_epoch, epoch))
+
+
+@dataclass
+class ModelDesc:
+    """BLSTM acoustic model. hidden = cells per direction."""
+    layers: int = 6
+    hidden: int = 1024
+    bidirectional: bool = True
+    input_dim: int = 260
+    proj: int = 256
+    classes: int = 32000
+    unroll: int = 21
+
+    def c(self) -> _lib.ModelDesc:
+        return _lib.ModelDesc(self.layers, self.hidden, int(self.bidirectional), self.input_dim, self.proj,
+                              self.classes, self.unroll)
+
+    def param_count(self) -> int:
+        return int(_lib.lib().adpsgd_param_count(C.byref(self.c())))
+
+    def fwd_flops_per_frame(self) -> float:
+        nd = 2 if self.bidirectional else 1
+        f = 0.0
+        for l in range(self.layers):
+            i = self.input_dim if l == 0 else nd * self.hidden
+            f += 2.0 * nd * 4 * self.hidden * (i + self.hidden)
+        top = nd * self.hidden
+        if self.proj > 0:
+            f += 2.0 * top * self.proj
+        f += 2.0 * (self.proj if self.proj > 0 else top) * self.classes
+        return f
+
+    def train_flops_per_frame(self) -> float:
+        nd = 2 if self.bidirectional else 1
+        return 3.0 * self.fwd_flops_per_frame() - 2.0 * nd * 4 * self.hidden * self.input_dim
+
+
+@dataclass
+class StrategyConfig:
+    strategy: Strategy = Strategy.SDPSGD
+    learners: int = 2
+    batch: int = 1
+    epochs: int = 1
+    lr: LrSchedule = field(default_factory=LrSchedule)
+    seed: int = 0
+    staleness_cap: int = 1
+    staleness: list = field(default_factory=list)
+    generic_mix: MixKind = MixKind.UNIFORM
+
+    def validate(self) -> None:  # engine.cpp:60-77
+        if self.learners < 1:
+            raise ConfigError("learners must be >= 1")
+        if self.strategy in (Strategy.ADPSGD_FM, Strategy.ADPSGD_RM) and self.learners != 1 and self.learners < 3:
+            raise ConfigError("FM/RM mixing requires at least 3 learners")
+        if self.batch < 1:
+            raise ConfigError("batch must be >= 1")
+        if self.epochs < 1:
+            raise ConfigError("epochs must be >= 1")
+        if self.staleness_cap < 0:
+            raise ConfigError("staleness_cap must be >= 0")
+        if self.staleness and len(self.staleness) != self.learners:
+            raise ConfigError("staleness list must have one entry per learner")
+        for tau in self.staleness:
+            if tau < 0 or tau > self.staleness_cap:
+                raise ConfigError("staleness entries must lie in [0, staleness_cap]")
+
+
+def permutation_for_iteration(seed: int, learners: int, iteration: int) -> list:
+    out = (C.c_int32 * learners)()
+    _lib.check(_lib.lib().adpsgd_permutation_for_iteration(seed, learners, iteration, out))
+    return list(out)
+
+
+def pairing(strategy: Strategy, seed: int, learners: int, iteration: int):
+    """(mapping, [(left, right) per learner]) for FM or RM at iteration k (chronos.cpp:224-235)."""
+    m = (C.c_int32 * learners)()
+    lr = (C.c_int32 * (2 * learners))()
+    _lib.check(_lib.lib().adpsgd_pairing(int(strategy), seed, learners, iteration, m, lr))
+    return list(m), [(lr[2 * i], lr[2 * i + 1]) for i in range(learners)]
+
+
+def _ptr(a: np.ndarray, ct):
+    return a.ctypes.data_as(C.POINTER(ct))
+
+
+class LearnerGroup:
+    """The vector<LearnerState> of engine::run_training, device-resident: `local_learners`
+    learners of a global ring of `cfg.learners`, hosted on one GPU."""
+
+    def __init__(self, model: ModelDesc, cfg: StrategyConfig, precision: Precision = Precision.BF16, device: int = 0,
+                 first_learner: int = 0, local_learners: int | None = None):
+        cfg.validate()
+        self.model, self.cfg, self.precision = model, cfg, Precision(precision)
+        self.local = cfg.learners if local_learners is None else local_learners
+        c = _lib.Config()
+        c.model = model.c()
+        c.precision = int(precision)
+        c.strategy = int(cfg.strategy)
+        c.learners = cfg.learners
+        c.first_learner = first_learner
+        c.local_learners = self.local
+        c.batch = cfg.batch
+        c.device = device
+        c.generic_mix = int(cfg.generic_mix)
+        c.staleness_cap = cfg.staleness_cap
+        c.seed = cfg.seed
+        h = C.c_void_p()
+        _lib.check(_lib.lib().adpsgd_ctx_create(C.byref(c), C.byref(h)))
+        self._h = h
+        self.D = model.param_count()
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            _lib.lib().adpsgd_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    # ---- data ----
+    def set_dataset(self, feats: np.ndarray, labels: np.ndarray, train_count: int) -> None:
+        feats = np.ascontiguousarray(feats, dtype=np.float32)
+        labels = np.ascontiguousarray(labels, dtype=np.int32)
+        _lib.check(_lib.lib().adpsgd_set_dataset(self._h, _ptr(feats, C.c_float), _ptr(labels, C.c_int32),
+                                                 feats.shape[0], train_count))
+        self.n_seg = feats.shape[0]
+
+    def synth_dataset(self, n_seg: int, train_count: int, seed: int) -> None:
+        _lib.check(_lib.lib().adpsgd_synth_dataset(self._h, n_seg, train_count, seed))
+        self.n_seg = n_seg
+
+    def dataset(self):
+        m = self.model
+        f = np.zeros((self.n_seg, m.unroll, m.input_dim), dtype=np.float32)
+        l = np.zeros((self.n_seg, m.unroll), dtype=np.int32)
+        _lib.check(_lib.lib().adpsgd_get_dataset(self._h, _ptr(f, C.c_float), _ptr(l, C.c_int32)))
+        return f, l
+
+    # ---- models ----
+    def weights(self, j: int) -> np.ndarray:
+        w = np.zeros(self.D, dtype=np.float64)
+        _lib.check(_lib.lib().adpsgd_get_weights(self._h, j, _ptr(w, C.c_double), self.D))
+        return w
+
+    def set_weights(self, j: int, w) -> None:
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        _lib.check(_lib.lib().adpsgd_set_weights(self._h, j, _ptr(w, C.c_double), self.D))
+
+    @property
+    def iteration(self) -> int:
+        return int(_lib.lib().adpsgd_iteration(self._h))
+
+    # ---- steps ----
+    def _taus(self, taus):
+        if taus is None:
+            return None, None
+        t = np.ascontiguousarray(taus, dtype=np.int32)
+        return t, _ptr(t, C.c_int32)
+
+    def step(self, lr: float, taus=None) -> np.ndarray:
+        loss = np.zeros(self.local, dtype=np.float32)
+        t, tp = self._taus(taus)
+        _lib.check(_lib.lib().adpsgd_step(self._h, lr, tp, _ptr(loss, C.c_float)))
+        return loss
+
+    def step_host_batch(self, lr: float, feats: np.ndarray, labels: np.ndarray) -> np.ndarray:
+        feats = np.ascontiguousarray(feats, dtype=np.float32)
+        labels = np.ascontiguousarray(labels, dtype=np.int32)
+        loss = np.zeros(self.local, dtype=np.float32)
+        _lib.check(_lib.lib().adpsgd_step_host_batch(self._h, lr, _ptr(feats, C.c_float), _ptr(labels, C.c_int32),
+                                                     _ptr(loss, C.c_float)))
+        return loss
+
+    def step_injected(self, lr: float, grads: np.ndarray, taus=None) -> None:
+        g = np.ascontiguousarray(grads, dtype=np.float64)
+        t, tp = self._taus(taus)
+        _lib.check(_lib.lib().adpsgd_step_injected(self._h, lr, tp, _ptr(g, C.c_double)))
+
+    def gradient(self, w, idx):
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        idx = np.ascontiguousarray(idx, dtype=np.int32)
+        g = np.zeros(self.D, dtype=np.float64)
+        loss = C.c_double()
+        _lib.check(_lib.lib().adpsgd_gradient(self._h, _ptr(w, C.c_double), _ptr(idx, C.c_int32), len(idx),
+                                              _ptr(g, C.c_double), C.byref(loss)))
+        return loss.value, g
+
+    def set_straggler(self, j: int, factor: float) -> None:
+        _lib.check(_lib.lib().adpsgd_set_straggler(self._h, j, factor))
+
+    def stats(self) -> dict:
+        p = _lib.Perf()
+        _lib.check(_lib.lib().adpsgd_get_stats(self._h, C.byref(p)))
+        return {"last_step_ms": p.last_step_ms, "last_mix_ms": p.last_mix_ms, "gossip_bytes": p.gossip_bytes,
+                "steps": p.steps, "kernel_launches": p.kernel_launches}
+
+    def consensus_distance(self) -> float:
+        out = C.c_double()
+        _lib.check(_lib.lib().adpsgd_consensus_distance(self._h, C.byref(out)))
+        return out.value
+
+    # ---- multi-process plumbing (one process per GPU) ----
+    def comm_init(self, rank: int, world: int, nccl_id: bytes) -> None:
+        buf = C.create_string_buffer(nccl_id, 128)
+        _lib.check(_lib.lib().adpsgd_comm_init(self._h, rank, world, buf))
+
+    def export_ipc(self) -> bytes:
+        n = int(_lib.lib().adpsgd_ipc_handle_size(self._h))
+        buf = C.create_string_buffer(n)
+        _lib.check(_lib.lib().adpsgd_export_ipc(self._h, buf, n))
+        return buf.raw
+
+    def import_ipc(self, rank: int, first: int, count: int, handles: bytes) -> None:
+        buf = C.create_string_buffer(handles, len(handles))
+        _lib.check(_lib.lib().adpsgd_import_ipc(self._h, rank, first, count, buf, len(handles)))
+
+    def set_gossip_mode(self, mode: int) -> None:
+        _lib.check(_lib.lib().adpsgd_set_gossip_mode(self._h, mode))
+
+    def barrier(self) -> None:
+        _lib.check(_lib.lib().adpsgd_barrier(self._h))
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _lib.check(_lib.lib().adpsgd_nccl_unique_id(buf))
+    return buf.raw
+
+
+class LstmObjective:
+    """objectives::Objective (objectives.hpp:45-69) for the BLSTM, evaluated on the GPU.
+    loss/gradient take a flat fp64 parameter vector and a batch of segment indices."""
+
+    def __init__(self, group: LearnerGroup):
+        self.g = group
+
+    def dimension(self) -> int:
+        return self.g.D
+
+    def gradient(self, w, indices) -> np.ndarray:
+        return self.g.gradient(w, indices)[1]
+
+    def loss(self, w, indices) -> float:
+        return self.g.gradient(w, indices)[0]

@@ -1,0 +1,197 @@
+"""GPU parity of the learner step against the CPU fp64 oracle (same inputs, same seeds),
+through the C ABI.
+
+Tolerances (stated):
+  * pairing / permutations / sampled batches: bit-exact (index work);
+  * FP32 mode (SIMT fp32 GEMMs): loss rel err <= 1e-5, gradient max-abs err <= 2e-5 * max|g|,
+    weights after N steps max-abs err <= 1e-5;
+  * BF16 mode (tcgen05 bf16 x bf16 -> fp32): gradient relative L2 err <= 5e-2, loss rel err <= 1e-2.
+"""
+import numpy as np
+import pytest
+
+from paper_2110_11199_b200 import LearnerGroup, MixKind, ModelDesc, Precision, Strategy, StrategyConfig
+from paper_2110_11199_b200.errors import StalenessOverflowError, SyncViolationError
+
+pytestmark = pytest.mark.gpu
+
+CASES = {
+    "uni2": ModelDesc(layers=2, hidden=16, bidirectional=False, input_dim=12, proj=0, classes=24, unroll=5),
+    "bi2p": ModelDesc(layers=2, hidden=16, bidirectional=True, input_dim=20, proj=8, classes=40, unroll=7),
+    "bi3p_t21": ModelDesc(layers=3, hidden=32, bidirectional=True, input_dim=36, proj=16, classes=64, unroll=21),
+    "odd_in": ModelDesc(layers=2, hidden=24, bidirectional=True, input_dim=13, proj=8, classes=16, unroll=4),
+}
+
+
+def _data(m, n_seg=48, seed=0):
+    rng = np.random.default_rng(seed)
+    feats = rng.normal(size=(n_seg, m.unroll, m.input_dim)).astype(np.float32)
+    labels = rng.integers(0, m.classes, size=(n_seg, m.unroll)).astype(np.int32)
+    return feats, labels
+
+
+def _odesc(O, m):
+    return O.desc(m.layers, m.hidden, int(m.bidirectional), m.input_dim, m.proj, m.classes, m.unroll)
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_gradient_fp32_matches_oracle(oracle_mod, name):
+    O, m = oracle_mod, CASES[name]
+    feats, labels = _data(m)
+    M = 6
+    g = LearnerGroup(m, StrategyConfig(learners=1, batch=M, seed=1), precision=Precision.FP32)
+    g.set_dataset(feats, labels, 40)
+    rng = np.random.default_rng(7)
+    w = rng.normal(0, 0.2, g.D)
+    idx = rng.integers(0, 40, size=M).astype(np.int32)
+    loss, grad = g.gradient(w, idx)
+    oloss, ograd = O.lstm_loss_grad(_odesc(O, m), w, feats, labels, idx)
+    assert abs(loss - oloss) <= 1e-5 * abs(oloss)
+    assert np.max(np.abs(grad - ograd)) <= 2e-5 * np.max(np.abs(ograd))
+
+
+@pytest.mark.parametrize("name", ["bi2p", "bi3p_t21"])
+def test_gradient_bf16_tensor_core_tolerance(oracle_mod, name):
+    O, m = oracle_mod, CASES[name]
+    feats, labels = _data(m)
+    M = 8
+    g = LearnerGroup(m, StrategyConfig(learners=1, batch=M, seed=1), precision=Precision.BF16)
+    g.set_dataset(feats, labels, 40)
+    rng = np.random.default_rng(9)
+    w = rng.normal(0, 0.2, g.D)
+    idx = rng.integers(0, 40, size=M).astype(np.int32)
+    loss, grad = g.gradient(w, idx)
+    oloss, ograd = O.lstm_loss_grad(_odesc(O, m), w, feats, labels, idx)
+    rel = np.linalg.norm(grad - ograd) / np.linalg.norm(ograd)
+    print(f"bf16 {name}: loss rel err {abs(loss - oloss) / oloss:.2e}, grad rel L2 err {rel:.2e}")
+    assert abs(loss - oloss) <= 1e-2 * oloss
+    assert rel <= 5e-2
+
+
+def _engine_pair(O, m, strategy, L, M, seed, precision=Precision.FP32, depth=2, cap=1, mix=MixKind.UNIFORM):
+    feats, labels = _data(m, seed=seed)
+    cfg = StrategyConfig(strategy=strategy, learners=L, batch=M, seed=seed, staleness_cap=cap, generic_mix=mix)
+    g = LearnerGroup(m, cfg, precision=precision)
+    g.set_dataset(feats, labels, 40)
+    ref = O.OracleEngine(_odesc(O, m), L, M, seed, feats, labels, 40, history_depth=depth)
+    return g, ref
+
+
+@pytest.mark.parametrize("strategy", [Strategy.ADPSGD_FM, Strategy.ADPSGD_RM, Strategy.ADPSGD_D1D, Strategy.SDPSGD])
+def test_engine_steps_fp32_match_oracle(oracle_mod, strategy):
+    O, m = oracle_mod, CASES["bi2p"]
+    L, M = 4, 3
+    g, ref = _engine_pair(O, m, strategy, L, M, seed=11)
+    for k in range(4):
+        loss = g.step(0.3)
+        assert ref.step(int(strategy), 0.3, k) == 0
+        for j in range(L):
+            assert abs(loss[j] - ref.last_loss(j)) <= 1e-5 * ref.last_loss(j)
+    for j in range(L):
+        assert np.max(np.abs(g.weights(j) - ref.model(j))) <= 1e-5
+
+
+def test_generic_staleness_fp32_matches_oracle(oracle_mod):
+    O, m = oracle_mod, CASES["uni2"]
+    L, M = 4, 3
+    g, ref = _engine_pair(O, m, Strategy.GENERIC, L, M, seed=5, depth=3, cap=2, mix=MixKind.FIXED_RING)
+    taus = [0, 1, 2, 1]
+    for k in range(4):
+        g.step(0.2, taus=taus)
+        assert ref.step(int(Strategy.GENERIC), 0.2, k, generic_mix=0, taus=taus) == 0
+    for j in range(L):
+        assert np.max(np.abs(g.weights(j) - ref.model(j))) <= 1e-5
+    with pytest.raises(StalenessOverflowError):
+        g.step(0.2, taus=[0, 3, 0, 0])
+
+
+@pytest.mark.parametrize("strategy", [Strategy.ADPSGD_FM, Strategy.ADPSGD_RM, Strategy.ADPSGD_D1D, Strategy.SDPSGD])
+def test_injected_gradient_steps_match_oracle(oracle_mod, strategy):
+    O, m = oracle_mod, CASES["uni2"]
+    L = 6
+    g, ref = _engine_pair(O, m, Strategy.ADPSGD_D1D, L, 2, seed=21)
+    # de-synchronise identically first (one real D1D step on both)
+    g.step(0.5)
+    ref.step(int(Strategy.ADPSGD_D1D), 0.5, 0)
+    g2, ref2 = g, ref
+    if strategy == Strategy.SDPSGD:  # needs synchronised models
+        g2, ref2 = _engine_pair(O, m, Strategy.SDPSGD, L, 2, seed=21)
+    else:
+        g2.close()
+        g2, ref2 = _engine_pair(O, m, strategy, L, 2, seed=21)
+        for j in range(L):
+            g2.set_weights(j, g.weights(j) if False else ref.model(j))
+            ref2.set_model(j, ref.model(j))
+    rng = np.random.default_rng(4)
+    for k in range(1, 4):
+        G = rng.normal(size=(L, g2.D))
+        g2.step_injected(0.1, G)
+        assert ref2.step_injected(int(strategy), 0.1, k, G) == 0
+    for j in range(L):
+        assert np.max(np.abs(g2.weights(j) - ref2.model(j))) <= 2e-6
+
+
+def test_single_learner_every_strategy_is_sgd(oracle_mod):
+    m = CASES["uni2"]
+    feats, labels = _data(m)
+    ws = []
+    for s in Strategy:
+        g = LearnerGroup(m, StrategyConfig(strategy=s, learners=1, batch=4, seed=99), precision=Precision.FP32)
+        g.set_dataset(feats, labels, 40)
+        for _ in range(3):
+            g.step(0.05)
+        ws.append(g.weights(0))
+        g.close()
+    for w in ws[1:]:
+        assert np.array_equal(w, ws[0])
+
+
+def test_sdpsgd_sync_violation():
+    m = CASES["uni2"]
+    feats, labels = _data(m)
+    g = LearnerGroup(m, StrategyConfig(strategy=Strategy.SDPSGD, learners=3, batch=2, seed=3), precision=Precision.FP32)
+    g.set_dataset(feats, labels, 40)
+    w = g.weights(1)
+    w[0] += 1e-3
+    g.set_weights(1, w)
+    with pytest.raises(SyncViolationError):
+        g.step(0.1)
+
+
+def test_host_batch_step_equals_indexed_step(oracle_mod):
+    O, m = oracle_mod, CASES["bi2p"]
+    feats, labels = _data(m)
+    cfg = StrategyConfig(strategy=Strategy.ADPSGD_FM, learners=3, batch=4, seed=8)
+    a = LearnerGroup(m, cfg, precision=Precision.FP32)
+    a.set_dataset(feats, labels, 40)
+    b = LearnerGroup(m, cfg, precision=Precision.FP32)
+    b.set_dataset(feats, labels, 40)
+    la = a.step(0.2)
+    idx = np.stack([O.learner_batches(8, l, 1, 4, 40)[0] for l in range(3)])
+    lb = b.step_host_batch(0.2, feats[idx], labels[idx])
+    assert np.allclose(la, lb, rtol=0, atol=0)
+    for j in range(3):
+        assert np.array_equal(a.weights(j), b.weights(j))
+
+
+def test_config_s_fixed_ring_fp32(oracle_mod):
+    """BASELINE configs[0]: 2-layer LSTM H=256, 40-dim features, 4 learners, FM."""
+    O = oracle_mod
+    m = ModelDesc(layers=2, hidden=256, bidirectional=False, input_dim=40, proj=0, classes=32, unroll=21)
+    g, ref = _engine_pair(O, m, Strategy.ADPSGD_FM, 4, 4, seed=2026)
+    for k in range(2):
+        g.step(0.5)
+        ref.step(int(Strategy.ADPSGD_FM), 0.5, k)
+    for j in range(4):
+        assert np.max(np.abs(g.weights(j) - ref.model(j))) <= 1e-5
+
+
+def test_bf16_training_reduces_loss():
+    m = ModelDesc(layers=2, hidden=64, bidirectional=True, input_dim=40, proj=32, classes=64, unroll=21)
+    g = LearnerGroup(m, StrategyConfig(strategy=Strategy.ADPSGD_RM, learners=3, batch=32, seed=1),
+                     precision=Precision.BF16)
+    g.synth_dataset(512, 480, seed=3)
+    first = g.step(1.0).mean()
+    for _ in range(40):
+        last = g.step(1.0).mean()
+    assert np.isfinite(last) and last < first
