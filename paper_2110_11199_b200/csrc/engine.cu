@@ -625,7 +625,7 @@ void Ctx::step(double lr, const int32_t* taus, float* loss_out, const float* hos
     if (!injected && loss_out) {
         AB_CUDA(cudaMemcpyAsync(h_loss, loss_dev, sizeof(float) * cfg.local_learners, cudaMemcpyDeviceToHost, s));
     }
-    AB_CUDA(cudaEventSynchronize(ev1));
+    AB_CUDA(cudaStreamSynchronize(s));
     if (!injected && loss_out) std::memcpy(loss_out, h_loss, sizeof(float) * cfg.local_learners);
     float ms = 0, mms = 0;
     AB_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));

@@ -120,10 +120,10 @@ def test_injected_gradient_steps_match_oracle(oracle_mod, strategy):
         g2.close()
         g2, ref2 = _engine_pair(O, m, strategy, L, 2, seed=21)
         for j in range(L):
-            g2.set_weights(j, g.weights(j) if False else ref.model(j))
+            g2.set_weights(j, ref.model(j))
             ref2.set_model(j, ref.model(j))
     rng = np.random.default_rng(4)
-    for k in range(1, 4):
+    for k in range(3):  # g2 is a fresh context: its iteration counter starts at 0
         G = rng.normal(size=(L, g2.D))
         g2.step_injected(0.1, G)
         assert ref2.step_injected(int(strategy), 0.1, k, G) == 0
