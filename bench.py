@@ -1,0 +1,335 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 ADPSGD learner step (BASELINE.json metric: frames/sec of the
+6-layer BLSTM 1024/dir acoustic model under ADPSGD at 1/2/4/8 B200).
+
+One process per GPU (torchrun for N > 1). A "step" is one ADPSGD iteration of every
+learner: sample M = 1024 segments x 21 frames, BLSTM forward/backward on tcgen05 tensor
+cores, then the mixing + SGD update of the chosen strategy (default D1D, configs[3]; it is
+valid at every N, while FM/RM need >= 3 learners and degenerate to SGD at N = 1,
+engine.cpp:245-247).
+
+  value  = frames/s over all ranks, device time (CUDA events on the library stream), inputs
+           resident in HBM (device dataset, device-side gather of each step's batch)
+  e2e    = same metric through the public API with the batch in pinned HOST memory,
+           H2D copy and loss D2H inside every step (wall clock)
+  roofline = live CUDA-event timing of every tcgen05 GEMM launch in the timed region
+  cpu_baseline = the fp64 CPU oracle (oracle/, a port of the reference engine + LSTM) on a
+           bounded sample, rank 0, N = 1
+
+`--impl reference` times the reference-side CPU path (the oracle port; the reference itself
+cannot be built: no Eigen) with all usable host threads on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+T_UNROLL = 21
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--strategy", default="ADPSGD_D1D")
+    ap.add_argument("--layers", type=int, default=6)
+    ap.add_argument("--hidden", type=int, default=1024, help="cells per direction (paper-faithful: 512)")
+    ap.add_argument("--batch", type=int, default=1024, help="segments per learner per step")
+    ap.add_argument("--n-seg", type=int, default=65536)
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    return ap.parse_args()
+
+
+def model_desc(a):
+    from paper_2110_11199_b200 import ModelDesc
+    return ModelDesc(layers=a.layers, hidden=a.hidden, bidirectional=True, input_dim=260, proj=256, classes=32000,
+                     unroll=T_UNROLL)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "sm_max_mhz": 1965.0}, \
+            "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    def __init__(self, device: int):
+        self.device, self.proc, self.lines = device, None, []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return world, rank, local
+
+
+def cpu_oracle_sample(a, threads: int, segments: int):
+    """Time the fp64 CPU oracle (learner gradient + update) on `segments` segments of the
+    same model; returns (frames/s, seconds)."""
+    import numpy as np
+    from oracle import oracle as O
+    m = model_desc(a)
+    d = O.desc(m.layers, m.hidden, 1, m.input_dim, m.proj, m.classes, m.unroll)
+    D = O.param_count(d)
+    rng = np.random.default_rng(0)
+    w = O.init_w0(0, D)
+    feats = rng.normal(size=(segments, T_UNROLL, m.input_dim)).astype(np.float32)
+    labels = rng.integers(0, m.classes, size=(segments, T_UNROLL)).astype(np.int32)
+    idx = np.arange(segments, dtype=np.int32)
+    t0 = time.perf_counter()
+    _, g = O.lstm_loss_grad(d, w, feats, labels, idx, threads=threads)
+    w -= 0.1 * g  # the SGD update of the step
+    dt = time.perf_counter() - t0
+    return segments * T_UNROLL / dt, dt
+
+
+def run_reference(a):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    ncpu = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    threads = max(1, min(ncpu, 8))  # per-thread fp64 gradient partials are 1.16 GB each
+    segs = threads
+    times = []
+    budget = 150.0
+    for i in range(a.warmup + a.steps):
+        fps, dt = cpu_oracle_sample(a, threads, segs)
+        if i >= a.warmup:
+            times.append(dt)
+        if sum(times) + (0 if not times else times[-1]) > budget and len(times) >= 1:
+            break
+    tot = sum(times)
+    frames = segs * T_UNROLL * len(times)
+    val = frames / tot
+    m = model_desc(a)
+    line = {
+        "impl": "reference", "metric": "frames/sec (6x1024 BLSTM ADPSGD learner step)", "value": val,
+        "unit": "frames/s", "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": 1000.0 * tot / len(times), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "configs[1]/[3] BLSTM learner step", "model": f"{m.layers}x{m.hidden}/dir BLSTM",
+                   "seq_len": T_UNROLL, "strategy": a.strategy},
+        "cpu_baseline": {"value": val, "unit": "frames/s", "cores": threads, "kind": "port",
+                         "sample": f"{segs} segments x 21 frames per step (one per thread), fp64 oracle "
+                                   f"(reference cannot build: Eigen absent); {len(times)} timed steps "
+                                   f"of {a.steps} requested (150 s budget)"},
+        "e2e": {"value": val, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(a):
+    import numpy as np
+    import torch
+    from paper_2110_11199_b200 import LearnerGroup, Precision, StrategyConfig, _lib, nccl_unique_id, \
+        strategy_from_name
+
+    world, rank, local = dist_env()
+    assert world == a.gpus, f"--gpus {a.gpus} but WORLD_SIZE={world}"
+    torch.cuda.set_device(local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        pg = dist
+    m = model_desc(a)
+    strategy = strategy_from_name(a.strategy)
+    cfg = StrategyConfig(strategy=strategy, learners=world, batch=a.batch, seed=2110_11199)
+    prec = Precision.BF16 if a.precision == "bf16" else Precision.FP32
+    g = LearnerGroup(m, cfg, precision=prec, device=local, first_learner=rank, local_learners=1)
+    if world > 1:
+        obj = [nccl_unique_id() if rank == 0 else None]
+        pg.broadcast_object_list(obj, src=0)
+        g.comm_init(rank, world, obj[0])
+        handles = [None] * world
+        pg.all_gather_object(handles, g.export_ipc())
+        for r in range(world):
+            g.import_ipc(r, r, 1, handles[r])
+    g.synth_dataset(a.n_seg, a.n_seg, seed=7)
+    lr = 0.1
+
+    def barrier():
+        if pg:
+            pg.barrier()
+        g.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(a.warmup):
+        g.step(lr)
+    barrier()
+    dev = local
+    with ClockSampler(dev) as clk:
+        _lib.profile_enable(True)
+        ms = []
+        for _ in range(a.steps):
+            g.step(lr)
+            ms.append(g.stats()["last_step_ms"])
+        _lib.profile_enable(False)
+        prof = _lib.profile_read()
+    barrier()
+    tot_ms = sum(ms)
+    if pg:
+        t = torch.tensor([tot_ms], dtype=torch.float64)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        tot_ms = float(t[0])
+    frames = world * a.batch * T_UNROLL * a.steps
+    value = frames / (tot_ms / 1000.0)
+
+    # ---- end-to-end through the public API with host (pinned) batches ----
+    e2e_steps = a.e2e_steps or max(3, a.steps // 2)
+    nf = a.batch * T_UNROLL * m.input_dim
+    hf = torch.empty(nf, dtype=torch.float32, pin_memory=True)
+    hl = torch.empty(a.batch * T_UNROLL, dtype=torch.int32, pin_memory=True)
+    feats, labels = g.dataset() if a.n_seg <= 8192 else (None, None)
+    rng = np.random.default_rng(rank)
+    if feats is None:
+        hf.copy_(torch.randn(nf))
+        hl.copy_(torch.randint(0, m.classes, (a.batch * T_UNROLL,), dtype=torch.int32))
+    else:
+        idx = rng.integers(0, a.n_seg, a.batch)
+        hf.copy_(torch.from_numpy(feats[idx].reshape(-1)))
+        hl.copy_(torch.from_numpy(labels[idx].reshape(-1)))
+    import ctypes as C
+    fptr = C.cast(hf.data_ptr(), C.POINTER(C.c_float))
+    lptr = C.cast(hl.data_ptr(), C.POINTER(C.c_int32))
+    loss = (C.c_float * 1)()
+    _lib.check(_lib.lib().adpsgd_step_host_batch(g.handle, lr, fptr, lptr, loss))  # warm
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        _lib.check(_lib.lib().adpsgd_step_host_batch(g.handle, lr, fptr, lptr, loss))
+    e2e_s = time.perf_counter() - t0
+    if pg:
+        t = torch.tensor([e2e_s], dtype=torch.float64)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        e2e_s = float(t[0])
+    barrier()
+    e2e_val = world * a.batch * T_UNROLL * e2e_steps / e2e_s
+
+    if rank != 0:
+        return
+    pk, pk_kind = peaks()
+    gt = prof["gemm_tc"] if prec == Precision.BF16 else prof["gemm_simt"]
+    achieved = gt["flops"] / (gt["ms"] / 1000.0) / 1e12 if gt["ms"] > 0 else 0.0
+    peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "gemm_tc_traffic.json")
+    if os.path.exists(tp):
+        try:
+            with open(tp) as f:
+                traffic = json.load(f).get("dram_bytes_per_launch_mean")
+        except Exception:
+            traffic = None
+    launches = int(sum(v["launches"] for v in prof.values()))
+    kernel_ms = {k: round(v["ms"] / a.steps, 4) for k, v in prof.items() if v["launches"]}
+    mix = prof["mix_update"]
+    mix_gbs = mix["bytes"] / (mix["ms"] / 1000.0) / 1e9 if mix["ms"] > 0 else None
+    cpu = None
+    if world == 1 and not a.no_cpu_baseline:
+        fps, dt = cpu_oracle_sample(a, 1, 1)
+        cpu = {"value": fps, "unit": "frames/s", "cores": 1, "kind": "port",
+               "sample": f"1 segment x 21 frames of the same model, fp64 oracle gradient + SGD update, "
+                         f"single thread ({dt:.1f} s)"}
+    line = {
+        "metric": "frames/sec (6x1024 BLSTM ADPSGD learner step)",
+        "value": value, "unit": "frames/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": tot_ms / a.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": a.precision, "data": "synthetic (device-generated SWB-shaped frames, 260-dim, 32k labels)",
+        "config": {"workload": "configs[1]/[3]: 6-layer BLSTM, per-learner step on one B200",
+                   "model": f"{m.layers}x{m.hidden}/dir BLSTM, proj {m.proj}, {m.classes} out, I=260",
+                   "params": g.D, "global_batch": a.batch * world, "per_gpu_batch": a.batch, "seq_len": T_UNROLL,
+                   "strategy": a.strategy if world > 1 else f"{a.strategy} (L=1 => SGD, engine.cpp:245-247)",
+                   "parallelism": f"dp{world} (one learner per GPU)",
+                   "l2": "per-step working set (~12 GB) >> 126 MB L2; no flush needed",
+                   "train_flops_per_frame": m.train_flops_per_frame()},
+        "e2e": {"value": e2e_val, "unit": "frames/s", "h2d_bytes_per_step": nf * 4 + a.batch * T_UNROLL * 4,
+                "d2h_bytes_per_step": 4, "steps": e2e_steps},
+        "roofline": {"bound": "tensor", "kernel": "gemm_tc_kernel (tcgen05 bf16, all GEMM launches)",
+                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
+                     "peak_kind": f"bf16_tflops_sustained ({pk_kind})", "traffic": traffic,
+                     "gemm_share_of_step": gt["ms"] / tot_ms if tot_ms else None,
+                     "step_tflops": frames * m.train_flops_per_frame() / (tot_ms / 1000.0) / 1e12 / world},
+        "mix_update": {"ms_per_step": mix["ms"] / a.steps, "achieved_gbs": mix_gbs, "peak_hbm_gbs": pk.get("hbm_gbs")},
+        "kernel_ms_per_step": kernel_ms,
+        "gpu_launches": launches,
+        "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    g.close()
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

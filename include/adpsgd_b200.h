@@ -151,6 +151,15 @@ int adpsgd_import_ipc(adpsgd_ctx* ctx, int32_t rank, int32_t rank_first_learner,
 int adpsgd_set_gossip_mode(adpsgd_ctx* ctx, int32_t mode);
 int adpsgd_barrier(adpsgd_ctx* ctx);
 
+/* ---- live kernel profiling (CUDA events around every library launch) ---- */
+/* Kernel classes: 0 tcgen05 GEMM, 1 SIMT GEMM, 2 LSTM cell, 3 softmax-CE, 4 reductions,
+ * 5 batch gather, 6 mixing/update/shadow, 7 other. */
+#define ADPSGD_PROF_NCAT 8
+int adpsgd_profile_enable(int32_t on);
+/* Synchronises the device; returns per-class device ms, algorithmic FLOPs, algorithmic
+ * bytes and launch counts accumulated since the last read, then clears them. */
+int adpsgd_profile_read(double* ms, double* flops, double* bytes, int64_t* launches, int32_t ncat);
+
 /* ---- kernel-level entry points (tests / benchmarks; device pointers) ---- */
 /* C[M,N] = alpha * sum_k A(m,k) B(n,k) (+ C if accumulate) (+ bias[n]).
  * A(m,k) = a_mn ? A[k*lda+m] : A[m*lda+k]; B likewise. bf16 = 1: A,B bf16, tcgen05;

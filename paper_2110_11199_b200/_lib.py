@@ -65,11 +65,15 @@ _SIGS = {
     "adpsgd_import_ipc": (C.c_int, [C.c_void_p, i32, i32, i32, C.c_void_p, i64]),
     "adpsgd_set_gossip_mode": (C.c_int, [C.c_void_p, i32]),
     "adpsgd_barrier": (C.c_int, [C.c_void_p]),
+    "adpsgd_profile_enable": (C.c_int, [i32]),
+    "adpsgd_profile_read": (C.c_int, [P(C.c_double), P(C.c_double), P(C.c_double), P(i64), i32]),
     "adpsgd_gemm": (C.c_int, [i32, i32, i32, i32, C.c_void_p, i64, i32, C.c_void_p, i64, i32, C.c_void_p, i64,
                               i32, C.c_float, i32, C.c_void_p, C.c_void_p]),
     "adpsgd_mix_update": (C.c_int, [i64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_float, C.c_void_p,
                                     C.c_void_p, C.c_void_p]),
 }
+
+PROF_CATS = ["gemm_tc", "gemm_simt", "lstm_cell", "softmax_ce", "reduce", "gather", "mix_update", "other"]
 
 _LIB = None
 
@@ -105,3 +109,15 @@ def last_error() -> str:
 def check(rc: int) -> None:
     if rc != 0:
         raise_for(rc, last_error())
+
+
+def profile_enable(on: bool) -> None:
+    check(lib().adpsgd_profile_enable(int(on)))
+
+
+def profile_read() -> dict:
+    n = len(PROF_CATS)
+    ms, fl, by = (C.c_double * n)(), (C.c_double * n)(), (C.c_double * n)()
+    la = (C.c_int64 * n)()
+    check(lib().adpsgd_profile_read(ms, fl, by, la, n))
+    return {c: {"ms": ms[i], "flops": fl[i], "bytes": by[i], "launches": la[i]} for i, c in enumerate(PROF_CATS)}

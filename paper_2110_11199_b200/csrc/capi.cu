@@ -9,6 +9,7 @@
 #include "engine.hpp"
 #include "gemm.hpp"
 #include "kernels.cuh"
+#include "prof.hpp"
 #include "rng.hpp"
 
 using namespace ab;
@@ -313,6 +314,14 @@ int adpsgd_barrier(adpsgd_ctx* ctx) {
         c.comm->barrier(c.s_main);
         AB_CUDA(cudaStreamSynchronize(c.s_main));
     });
+}
+
+int adpsgd_profile_enable(int32_t on) {
+    return guard([&] { g_prof_enabled = on != 0; });
+}
+
+int adpsgd_profile_read(double* ms, double* flops, double* bytes, int64_t* launches, int32_t ncat) {
+    return guard([&] { prof_read(ms, flops, bytes, launches, ncat < PROF_NCAT ? ncat : PROF_NCAT); });
 }
 
 int adpsgd_gemm(int32_t bf, int32_t M, int32_t N, int32_t K, const void* A, int64_t lda, int32_t a_mn, const void* B,

@@ -2,6 +2,7 @@
 // Tiled 64x64x16, 256 threads, 4x4 register micro-tile, any operand majorness.
 // Not the performance path: the bf16 tcgen05 kernel (gemm_tc.cu) is.
 #include "gemm.hpp"
+#include "prof.hpp"
 
 namespace ab {
 
@@ -103,6 +104,10 @@ void gemm_simt(const GemmArgs& g, cudaStream_t s) {
     }
     p.C = g.C; p.ldc = g.ldc; p.cbf16 = g.c_bf16;
     p.alpha = g.alpha; p.accumulate = g.accumulate; p.bias = g.bias;
+    double ksum = 0;
+    for (int i = 0; i < g.nseg; ++i) ksum += g.seg[i].K;
+    ProfScope ps_(s, PROF_GEMM_SIMT, 2.0 * g.M * g.N * ksum,
+                  4.0 * (static_cast<double>(g.M) + g.N) * ksum + static_cast<double>(g.M) * g.N * 4.0);
     dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM);
     gemm_simt_kernel<<<grid, 256, 0, s>>>(p);
     count_launch();

@@ -15,6 +15,7 @@
 
 #include "gemm.hpp"
 #include "tc_ptx.cuh"
+#include "prof.hpp"
 
 namespace ab {
 
@@ -361,6 +362,10 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
     p.accumulate = g.accumulate;
     p.bias = g.bias;
     const int esz = g.c_bf16 ? 2 : 4;
+    double ksum = 0;
+    for (int i = 0; i < g.nseg; ++i) ksum += g.seg[i].K;
+    ProfScope ps_(s, PROF_GEMM_TC, 2.0 * g.M * g.N * ksum,
+                  2.0 * (static_cast<double>(g.M) + g.N) * ksum + static_cast<double>(g.M) * g.N * esz * (g.accumulate ? 2 : 1));
     p.vec_ok = ((reinterpret_cast<uintptr_t>(g.C) & 15) == 0) && ((g.ldc * esz) % 16 == 0);
     if (bn == 256) dispatch<256>(p, amn, bmn, g.c_bf16, s);
     else dispatch<128>(p, amn, bmn, g.c_bf16, s);

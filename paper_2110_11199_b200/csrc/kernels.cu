@@ -1,6 +1,7 @@
 // Pointwise, reduction and update kernels of the ADPSGD learner step (sm_100a).
 // All are HBM-bound: vectorised, grid-stride, grids sized in multiples of the SM count.
 #include "kernels.cuh"
+#include "prof.hpp"
 
 namespace ab {
 
@@ -322,6 +323,7 @@ __global__ void delay_kernel(uint64_t ns) {
 template <typename AT>
 void launch_gather(const float* feats, const int32_t* labels, const int32_t* idx, int B, int T, int I, int ldx, AT* X,
                    int32_t* lab, cudaStream_t s) {
+    ProfScope ps_(s, PROF_GATHER, 0, (double)T * B * ldx * (sizeof(AT) + 4.0) + (double)T * B * 8);
     const int64_t total = static_cast<int64_t>(T) * B * ldx;
     gather_kernel<AT><<<grid_for(total), 256, 0, s>>>(feats, labels, idx, B, T, I, ldx, X, lab);
     count_launch();
@@ -330,6 +332,7 @@ void launch_gather(const float* feats, const int32_t* labels, const int32_t* idx
 template <typename AT>
 void launch_cell_fwd(const float* z, int ldz, const float* c_prev, int ldc, float* gates, int ldg, float* c, AT* h,
                      int ldh, int B, int H, cudaStream_t s) {
+    ProfScope ps_(s, PROF_CELL, 0, (double)B * H * (16 + 4 + 16 + 4 + sizeof(AT) + (c_prev ? 4 : 0)));
     cell_fwd_kernel<AT><<<grid_for(static_cast<int64_t>(B) * H), 256, 0, s>>>(z, ldz, c_prev, ldc, gates, ldg, c, h,
                                                                                 ldh, B, H);
     count_launch();
@@ -339,6 +342,7 @@ template <typename AT>
 void launch_cell_bwd(const float* dH, int lddh, const float* dh_rec, float* dc_rec, bool first, const float* gates,
                      int ldg, const float* c, const float* c_prev, int ldc, AT* dz, int lddz, int B, int H,
                      cudaStream_t s) {
+    ProfScope ps_(s, PROF_CELL, 0, (double)B * H * (4 + 16 + 4 + 4 + 4 * sizeof(AT) + (first ? 0 : 8) + (c_prev ? 4 : 0)));
     cell_bwd_kernel<AT><<<grid_for(static_cast<int64_t>(B) * H), 256, 0, s>>>(
         dH, lddh, dh_rec, dc_rec, first ? 1 : 0, gates, ldg, c, c_prev, ldc, dz, lddz, B, H);
     count_launch();
@@ -347,12 +351,14 @@ void launch_cell_bwd(const float* dH, int lddh, const float* dh_rec, float* dc_r
 template <typename AT>
 void launch_softmax_ce(const float* logits, const int32_t* labels, int R, int C, float scale, AT* dlogits,
                        float* row_loss, cudaStream_t s) {
+    ProfScope ps_(s, PROF_CE, 0, (double)R * C * (4 + sizeof(AT)) + (double)R * 8);
     softmax_ce_kernel<AT><<<R, 256, 0, s>>>(logits, labels, C, scale, dlogits, row_loss);
     count_launch();
 }
 
 template <typename AT>
 void launch_colsum(const AT* X, int64_t ld, int R, int N, float* out, float* ws, int64_t ws_elems, cudaStream_t s) {
+    ProfScope ps_(s, PROF_REDUCE, 0, (double)R * N * sizeof(AT) + (double)N * 4);
     int chunks = (R + 127) / 128;
     if (chunks > 128) chunks = 128;
     while (chunks > 1 && static_cast<int64_t>(chunks) * N > ws_elems) chunks /= 2;
@@ -364,28 +370,33 @@ void launch_colsum(const AT* X, int64_t ld, int R, int N, float* out, float* ws,
 }
 
 void launch_sum(const float* x, int n, float scale, float* out, cudaStream_t s) {
+    ProfScope ps_(s, PROF_REDUCE, 0, (double)n * 4);
     sum_kernel<<<1, 1024, 0, s>>>(x, n, scale, out);
     count_launch();
 }
 
 void launch_f32_to_bf16(const float* in, bf16* out, int64_t n, cudaStream_t s) {
+    ProfScope ps_(s, PROF_MIX, 0, (double)n * 6);
     f32_to_bf16_kernel<<<grid_for(n), 256, 0, s>>>(in, out, n);
     count_launch();
 }
 void launch_pad_rows_bf16(const float* in, int64_t ld_in, bf16* out, int64_t ld_out, int rows, int cols,
                           cudaStream_t s) {
+    ProfScope ps_(s, PROF_MIX, 0, (double)rows * (cols * 4.0 + ld_out * 2.0));
     pad_rows_kernel<<<grid_for(static_cast<int64_t>(rows) * ld_out), 256, 0, s>>>(in, ld_in, out, ld_out, rows, cols);
     count_launch();
 }
 
 void launch_mix3(int64_t n, const float* w, const float* wl, const float* wr, const float* g, float lr, float* w_out,
                  bf16* shadow, cudaStream_t s) {
+    ProfScope ps_(s, PROF_MIX, 0, (double)n * (20 + (shadow ? 2 : 0)));
     mix3_kernel<<<grid_for((n + 3) / 4, 256, 4), 256, 0, s>>>(n, w, wl, wr, g, lr, w_out, shadow);
     count_launch();
 }
 
 void launch_d1d(int64_t n, int L, const float* const* w_tab, const float* w_sum, int nloc, const float* const* g_tab,
                 float lr, float* const* out_tab, bf16* const* shadow_tab, cudaStream_t s) {
+    ProfScope ps_(s, PROF_MIX, 0, (double)n * ((w_sum ? 4 : 4 * L) + nloc * 10.0));
     AB_CHECK(L <= kMaxTab && nloc <= kMaxTab, ADPSGD_E_CONFIG, "too many learners for one device");
     PtrTab w{}, g{};
     MutTab o{};
@@ -399,6 +410,7 @@ void launch_d1d(int64_t n, int L, const float* const* w_tab, const float* w_sum,
 
 void launch_sdpsgd(int64_t n, int L, const float* w, const float* const* g_tab, const float* g_sum, int nloc,
                    float lr, float* const* out_tab, bf16* const* shadow_tab, cudaStream_t s) {
+    ProfScope ps_(s, PROF_MIX, 0, (double)n * ((g_sum ? 4 : 4 * L) + 4 + nloc * 6.0));
     AB_CHECK(L <= kMaxTab && nloc <= kMaxTab, ADPSGD_E_CONFIG, "too many learners for one device");
     PtrTab g{};
     MutTab o{};
@@ -413,6 +425,7 @@ void launch_sdpsgd(int64_t n, int L, const float* w, const float* const* g_tab, 
 void launch_dense_mix(int64_t n, int L, const float* const* w_tab, const double* T, const int* cols, int nloc,
                       const float* const* g_tab, float lr, float* const* out_tab, bf16* const* shadow_tab,
                       cudaStream_t s) {
+    ProfScope ps_(s, PROF_MIX, 0, (double)n * (4 * L + nloc * 10.0));
     AB_CHECK(L <= kMaxTab && nloc <= 16, ADPSGD_E_CONFIG, "too many learners for dense mixing");
     PtrTab w{}, g{};
     MutTab o{};
@@ -433,16 +446,19 @@ void launch_dense_mix(int64_t n, int L, const float* const* w_tab, const double*
 }
 
 void launch_maxdiff(int64_t n, const float* a, const float* b, float* out, cudaStream_t s) {
+    ProfScope ps_(s, PROF_OTHER, 0, (double)n * 8);
     maxdiff_kernel<<<grid_for(n, 256, 4), 256, 0, s>>>(n, a, b, out);
     count_launch();
 }
 
 void launch_synth(float* feats, int32_t* labels, int n_seg, int T, int I, int C, uint64_t seed, cudaStream_t s) {
+    ProfScope ps_(s, PROF_OTHER, 0, (double)n_seg * T * I * 4);
     synth_kernel<<<grid_for(static_cast<int64_t>(n_seg) * T * I), 256, 0, s>>>(feats, labels, n_seg, T, I, C, seed);
     count_launch();
 }
 
 void launch_delay(uint64_t ns, cudaStream_t s) {
+    ProfScope ps_(s, PROF_OTHER, 0, 0);
     delay_kernel<<<1, 1, 0, s>>>(ns);
     count_launch();
 }
