@@ -152,9 +152,10 @@ int adpsgd_set_gossip_mode(adpsgd_ctx* ctx, int32_t mode);
 int adpsgd_barrier(adpsgd_ctx* ctx);
 
 /* ---- live kernel profiling (CUDA events around every library launch) ---- */
-/* Kernel classes: 0 tcgen05 GEMM, 1 SIMT GEMM, 2 LSTM cell, 3 softmax-CE, 4 reductions,
- * 5 batch gather, 6 mixing/update/shadow, 7 other. */
-#define ADPSGD_PROF_NCAT 8
+/* Kernel classes: tcgen05 GEMMs 0 recurrent fwd, 1 BPTT dgrad, 2 weight grads, 3 input dgrad,
+ * 4 output/projection fwd; 5 SIMT GEMM, 6 LSTM cell, 7 softmax-CE, 8 reductions, 9 batch
+ * gather, 10 mixing/update/shadow, 11 other. */
+#define ADPSGD_PROF_NCAT 12
 int adpsgd_profile_enable(int32_t on);
 /* Synchronises the device; returns per-class device ms, algorithmic FLOPs, algorithmic
  * bytes and launch counts accumulated since the last read, then clears them. */

@@ -73,7 +73,9 @@ _SIGS = {
                                     C.c_void_p, C.c_void_p]),
 }
 
-PROF_CATS = ["gemm_tc", "gemm_simt", "lstm_cell", "softmax_ce", "reduce", "gather", "mix_update", "other"]
+PROF_CATS = ["gemm_rec_fwd", "gemm_rec_bwd", "gemm_wgrad", "gemm_dgrad_x", "gemm_out", "gemm_simt", "lstm_cell",
+             "softmax_ce", "reduce", "gather", "mix_update", "other"]
+GEMM_TC_CATS = PROF_CATS[:5]
 
 _LIB = None
 

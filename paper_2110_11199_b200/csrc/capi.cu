@@ -116,6 +116,7 @@ int adpsgd_set_dataset(adpsgd_ctx* ctx, const float* feats, const int32_t* label
             c.feats = static_cast<float*>(c.alloc(nf * sizeof(float)));
             c.labels = static_cast<int32_t*>(c.alloc(static_cast<size_t>(n_seg) * c.T * sizeof(int32_t)));
         }
+        c.clear_graphs();
         AB_CUDA(cudaMemcpy(c.feats, feats, nf * sizeof(float), cudaMemcpyHostToDevice));
         AB_CUDA(cudaMemcpy(c.labels, labels, static_cast<size_t>(n_seg) * c.T * sizeof(int32_t), cudaMemcpyHostToDevice));
         c.n_seg = n_seg;
@@ -133,6 +134,7 @@ int adpsgd_synth_dataset(adpsgd_ctx* ctx, int32_t n_seg, int32_t train_count, ui
             c.feats = static_cast<float*>(c.alloc(static_cast<size_t>(n_seg) * c.T * c.I * sizeof(float)));
             c.labels = static_cast<int32_t*>(c.alloc(static_cast<size_t>(n_seg) * c.T * sizeof(int32_t)));
         }
+        c.clear_graphs();
         launch_synth(c.feats, c.labels, n_seg, c.T, c.I, c.lay.C, seed, c.s_main);
         AB_CUDA(cudaStreamSynchronize(c.s_main));
         c.n_seg = n_seg;

@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -22,7 +23,9 @@
 #include "comm.hpp"
 #include "engine.hpp"
 #include "gemm.hpp"
+#include "gemm_lstm.hpp"
 #include "kernels.cuh"
+#include "prof.hpp"
 #include "rng.hpp"
 
 namespace ab {
@@ -50,6 +53,7 @@ Ctx::~Ctx() {
     cudaSetDevice(cfg.device);
     cudaDeviceSynchronize();
     comm.reset();
+    clear_graphs();
     for (void* p : allocations) cudaFree(p);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
@@ -59,6 +63,7 @@ Ctx::~Ctx() {
     if (s_comm) cudaStreamDestroy(s_comm);
     if (s_main) cudaStreamDestroy(s_main);
     if (h_loss) cudaFreeHost(h_loss);
+    if (h_idx) cudaFreeHost(h_idx);
 }
 
 static void validate_config(const adpsgd_config& c) {
@@ -93,6 +98,8 @@ Ctx::Ctx(const adpsgd_config& c) : cfg(c) {
     nd4H = nd * 4 * H;
     k = 0;
     history_depth = c.strategy == ADPSGD_GENERIC ? c.staleness_cap + 1 : 1;  // engine.cpp:216-217
+    if (const char* e = std::getenv("ADPSGD_NO_GRAPHS")) use_graphs = e[0] == '0';
+    if (const char* e = std::getenv("ADPSGD_NO_FUSED")) use_fused_cell = e[0] == '0';
 
     AB_CUDA(cudaSetDevice(c.device));
     AB_CUDA(cudaStreamCreateWithFlags(&s_main, cudaStreamNonBlocking));
@@ -103,6 +110,7 @@ Ctx::Ctx(const adpsgd_config& c) : cfg(c) {
     AB_CUDA(cudaEventCreate(&ev_comp0));
     AB_CUDA(cudaEventCreate(&ev_comp1));
     AB_CUDA(cudaMallocHost(&h_loss, sizeof(float) * 64));
+    AB_CUDA(cudaMallocHost(&h_idx, sizeof(int32_t) * static_cast<size_t>(B) * c.local_learners));
 
     // ---- workspace (shared by the local learners; they are computed in turn) ----
     idx_dev = static_cast<int32_t*>(alloc(sizeof(int32_t) * B));
@@ -210,11 +218,38 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
     const bool bf = bf16_mode;
     WView W{bf ? static_cast<const void*>(ln.shadow) : static_cast<const void*>(master), master, this, &ln};
     const int G4 = 4 * H;
+    const bool fused = bf && use_fused_cell && H % 64 == 0;
 
     // ---------------- forward ----------------
     for (int l = 0; l < lay.L; ++l) {
         const void* Xin = l == 0 ? X0 : Hout[l - 1];
         const int Kin = l == 0 ? Ipad : ndH;
+        if (fused) {
+            for (int st = 0; st < T; ++st) {
+                LstmFwdDir dirs[2];
+                for (int d = 0; d < nd; ++d) {
+                    const int t = d == 0 ? st : T - 1 - st;
+                    const int tp = d == 0 ? t - 1 : t + 1;
+                    int64_t ldw;
+                    LstmFwdDir& a = dirs[d];
+                    a.x = static_cast<const bf16*>(off_ptr(Xin, static_cast<int64_t>(t) * B * Kin, es));
+                    a.ldx = Kin;
+                    a.Kx = Kin;
+                    a.w_ih = static_cast<const bf16*>(W.wih(l, d, &ldw));
+                    a.ld_wih = ldw;
+                    a.h_prev = st > 0 ? static_cast<const bf16*>(off_ptr(Hout[l], static_cast<int64_t>(tp) * B * ndH + d * H, es)) : nullptr;
+                    a.ld_hprev = ndH;
+                    a.w_hh = static_cast<const bf16*>(W.at(lay.dir[l][d].w_hh));
+                    a.bias = master + lay.dir[l][d].b;
+                    a.c_prev = st > 0 ? cst[l] + static_cast<int64_t>(tp) * B * ndH + d * H : nullptr;
+                    a.gates = gates[l] + static_cast<int64_t>(t) * B * nd4H + d * G4;
+                    a.c = cst[l] + static_cast<int64_t>(t) * B * ndH + d * H;
+                    a.h = static_cast<bf16*>(off_ptr(Hout[l], static_cast<int64_t>(t) * B * ndH + d * H, es));
+                }
+                lstm_fwd_step(dirs, nd, B, H, nd4H, ndH, ndH, s);
+            }
+            continue;
+        }
         for (int st = 0; st < T; ++st) {
             for (int d = 0; d < nd; ++d) {
                 const int t = d == 0 ? st : T - 1 - st;
@@ -234,6 +269,7 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
                     g.nseg = 2;
                 }
                 g.C = zstep + static_cast<int64_t>(d) * B * G4;
+                g.tag = PROF_GEMM_REC_FWD;
                 g.ldc = G4;
                 g.bias = master + lay.dir[l][d].b;
                 gemm(bf, g, s);
@@ -261,6 +297,7 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
         g.seg[0].K = ndH;
         g.C = Y; g.ldc = lay.P; g.c_bf16 = bf;
         g.bias = master + lay.b_proj;
+        g.tag = PROF_GEMM_OUT;
         gemm(bf, g, s);
         yin = Y;
     }
@@ -272,6 +309,7 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
         g.seg[0].K = oi;
         g.C = logits; g.ldc = lay.C;
         g.bias = master + lay.b_out;
+        g.tag = PROF_GEMM_OUT;
         gemm(bf, g, s);
     }
     const float scale = 1.0f / static_cast<float>(TB);
@@ -291,6 +329,7 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
         g.seg[0].b = {yin, oi, true};
         g.seg[0].K = static_cast<int>(TB);
         g.C = grad + lay.w_out; g.ldc = oi;
+        g.tag = PROF_GEMM_WGRAD;
         gemm(bf, g, s);
     }
     colsum(dlogits, lay.C, static_cast<int>(TB), lay.C, grad + lay.b_out);
@@ -304,6 +343,7 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
             g.seg[0].b = {W.at(lay.w_out), lay.P, true};
             g.seg[0].K = lay.C;
             g.C = dY; g.ldc = lay.P; g.c_bf16 = bf;
+            g.tag = PROF_GEMM_DGRAD_X;
             gemm(bf, g, s);
         }
         {   // dW_proj = dY^T top
@@ -313,6 +353,7 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
             g.seg[0].b = {top, ndH, true};
             g.seg[0].K = static_cast<int>(TB);
             g.C = grad + lay.w_proj; g.ldc = ndH;
+            g.tag = PROF_GEMM_WGRAD;
             gemm(bf, g, s);
         }
         colsum(dY, lay.P, static_cast<int>(TB), lay.P, grad + lay.b_proj);
@@ -323,6 +364,7 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
             g.seg[0].b = {W.at(lay.w_proj), ndH, true};
             g.seg[0].K = lay.P;
             g.C = dHcur; g.ldc = ndH;
+            g.tag = PROF_GEMM_DGRAD_X;
             gemm(bf, g, s);
         }
     } else {
@@ -332,6 +374,7 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
         g.seg[0].b = {W.at(lay.w_out), ndH, true};
         g.seg[0].K = lay.C;
         g.C = dHcur; g.ldc = ndH;
+        g.tag = PROF_GEMM_DGRAD_X;
         gemm(bf, g, s);
     }
 
@@ -339,6 +382,41 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
     for (int l = lay.L - 1; l >= 0; --l) {
         const void* Xin = l == 0 ? X0 : Hout[l - 1];
         const int Kin = l == 0 ? Ipad : ndH;
+        if (fused) {
+            // BPTT: first cell backward unfused (no recurrent term), then one launch per step
+            // doing dh_rec = dz_t W_hh for both directions with the next cell backward fused.
+            for (int d = 0; d < nd; ++d) {
+                const int t = d == 0 ? T - 1 : 0;
+                const int tp = d == 0 ? t - 1 : t + 1;
+                const float* cp = T > 1 ? cst[l] + static_cast<int64_t>(tp) * B * ndH + d * H : nullptr;
+                launch_cell_bwd<bf16>(dHcur + static_cast<int64_t>(t) * B * ndH + d * H, ndH, nullptr,
+                                      dc_rec + static_cast<int64_t>(d) * B * H, true,
+                                      gates[l] + static_cast<int64_t>(t) * B * nd4H + d * G4, nd4H,
+                                      cst[l] + static_cast<int64_t>(t) * B * ndH + d * H, cp, ndH,
+                                      static_cast<bf16*>(off_ptr(dZ, static_cast<int64_t>(t) * B * nd4H + d * G4, es)),
+                                      nd4H, B, H, s);
+            }
+            for (int st = 0; st + 1 < T; ++st) {
+                LstmBwdDir dirs[2];
+                for (int d = 0; d < nd; ++d) {
+                    const int sf = T - 1 - st, sn = sf - 1;
+                    const int t = d == 0 ? sf : T - 1 - sf;
+                    const int tn = d == 0 ? sn : T - 1 - sn;
+                    const int tnp = d == 0 ? tn - 1 : tn + 1;
+                    LstmBwdDir& a = dirs[d];
+                    a.dz_src = static_cast<const bf16*>(off_ptr(dZ, static_cast<int64_t>(t) * B * nd4H + d * G4, es));
+                    a.ld_dz_src = nd4H;
+                    a.w_hh = static_cast<const bf16*>(W.at(lay.dir[l][d].w_hh));
+                    a.dH = dHcur + static_cast<int64_t>(tn) * B * ndH + d * H;
+                    a.dc_rec = dc_rec + static_cast<int64_t>(d) * B * H;
+                    a.gates = gates[l] + static_cast<int64_t>(tn) * B * nd4H + d * G4;
+                    a.c = cst[l] + static_cast<int64_t>(tn) * B * ndH + d * H;
+                    a.c_prev = sn > 0 ? cst[l] + static_cast<int64_t>(tnp) * B * ndH + d * H : nullptr;
+                    a.dz_dst = static_cast<bf16*>(off_ptr(dZ, static_cast<int64_t>(tn) * B * nd4H + d * G4, es));
+                }
+                lstm_bwd_step(dirs, nd, B, H, ndH, nd4H, ndH, nd4H, s);
+            }
+        } else
         for (int st = 0; st < T; ++st) {
             const int sf = T - 1 - st;  // forward-order step index of this time
             for (int d = 0; d < nd; ++d) {
@@ -364,6 +442,7 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
                     g.seg[0].b = {W.at(lay.dir[l][d].w_hh), H, true};
                     g.seg[0].K = G4;
                     g.C = dhr; g.ldc = H;
+                    g.tag = PROF_GEMM_REC_BWD;
                     gemm(bf, g, s);
                 }
             }
@@ -377,6 +456,7 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
                 g.seg[0].b = {Xin, Kin, true};
                 g.seg[0].K = static_cast<int>(TB);
                 g.C = grad + o.w_ih; g.ldc = lay.in_dim[l];
+                g.tag = PROF_GEMM_WGRAD;
                 gemm(bf, g, s);
             }
             if (T > 1) {  // dW_hh = sum_t dz_t^T h_prev(t)
@@ -388,6 +468,7 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
                 g.seg[0].b = {off_ptr(Hout[l], b_row0 * ndH + d * H, es), ndH, true};
                 g.seg[0].K = static_cast<int>((T - 1) * static_cast<int64_t>(B));
                 g.C = grad + o.w_hh; g.ldc = H;
+                g.tag = PROF_GEMM_WGRAD;
                 gemm(bf, g, s);
             } else {
                 AB_CUDA(cudaMemsetAsync(grad + o.w_hh, 0, sizeof(float) * G4 * H, s));
@@ -406,6 +487,7 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
             }
             g.nseg = nd;
             g.C = dHnext; g.ldc = Kin;
+            g.tag = PROF_GEMM_DGRAD_X;
             gemm(bf, g, s);
             std::swap(dHcur, dHnext);
         }
@@ -420,18 +502,78 @@ void Ctx::gather_batch(const float* feats_src, const int32_t* labels_src, const 
 }
 
 // Host-side sampling of learner j's batch: M draws next_below(train_count)
-// (objectives.cpp:239-249) from its own stream, then upload.
-void Ctx::sample_and_gather(Learner& ln, cudaStream_t s) {
+// (objectives.cpp:239-249) from its own stream into learner j's pinned slot.
+void Ctx::sample_indices(Learner& ln, int j) {
     AB_CHECK(feats != nullptr && train_count >= 1, ADPSGD_E_INVALID_STATE, "dataset has no training samples");
-    std::vector<int32_t> idx(B);
-    for (int b = 0; b < B; ++b) idx[b] = static_cast<int32_t>(ln.rng.next_below(static_cast<uint64_t>(train_count)));
-    // pinned staging keeps the copy asynchronous and graph-friendly
-    if (!h_idx) AB_CUDA(cudaMallocHost(&h_idx, sizeof(int32_t) * B * 2));
-    int32_t* hb = h_idx + (idx_flip ^= 1) * B;
-    AB_CUDA(cudaStreamSynchronize(s));  // previous users of this pinned half are done
-    std::memcpy(hb, idx.data(), sizeof(int32_t) * B);
-    AB_CUDA(cudaMemcpyAsync(idx_dev, hb, sizeof(int32_t) * B, cudaMemcpyHostToDevice, s));
-    gather_batch(feats, labels, idx_dev, s);
+    int32_t* hb = h_idx + static_cast<int64_t>(j) * B;
+    for (int b = 0; b < B; ++b) hb[b] = static_cast<int32_t>(ln.rng.next_below(static_cast<uint64_t>(train_count)));
+}
+
+// The learner's gradient computation as one replayable unit: batch upload + gather +
+// BLSTM forward/backward. mode 0 = indices from the pinned slot into the device dataset,
+// mode 1 = batch already staged in stage_feats / stage_labels.
+void Ctx::compute_body(int j, int mode, const float* wpt, cudaStream_t s) {
+    Learner& ln = learners[j];
+    if (mode == 0) {
+        AB_CUDA(cudaMemcpyAsync(idx_dev, h_idx + static_cast<int64_t>(j) * B, sizeof(int32_t) * B,
+                                cudaMemcpyHostToDevice, s));
+        gather_batch(feats, labels, idx_dev, s);
+    } else {
+        gather_batch(stage_feats, stage_labels, ident_idx, s);
+    }
+    forward_backward(ln, wpt, ln.g, loss_dev + j, s);
+}
+
+// Runs compute_body through a CUDA graph keyed by (learner, weight parity, mode, profiling):
+// the first encounter runs eagerly (warms plan caches / attributes), the second captures,
+// later ones replay — ~1000 launches per learner step become one graph launch.
+void Ctx::run_compute(int j, int mode, const float* wpt, cudaStream_t s) {
+    Learner& ln = learners[j];
+    const bool lagged = wpt != ln.w[k & 1];
+    if (lagged || !use_graphs) {
+        compute_body(j, mode, wpt, s);
+        return;
+    }
+    const int key = ((j * 2 + static_cast<int>(k & 1)) * 2 + mode) * 2 + (g_prof_enabled ? 1 : 0);
+    auto it = graphs.find(key);
+    if (it == graphs.end()) {
+        StepGraph sg;
+        graphs.emplace(key, std::move(sg));
+        compute_body(j, mode, wpt, s);  // eager warm-up run
+        return;
+    }
+    StepGraph& sg = it->second;
+    if (!sg.exec) {
+        const int64_t launches0 = g_launch_count;
+        std::vector<ProfRec>* prev = g_prof_capture;
+        if (g_prof_enabled) g_prof_capture = &sg.prof;
+        AB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        try {
+            compute_body(j, mode, wpt, s);
+        } catch (...) {
+            cudaGraph_t gtmp;
+            cudaStreamEndCapture(s, &gtmp);
+            if (gtmp) cudaGraphDestroy(gtmp);
+            g_prof_capture = prev;
+            throw;
+        }
+        cudaGraph_t graph;
+        AB_CUDA(cudaStreamEndCapture(s, &graph));
+        g_prof_capture = prev;
+        AB_CUDA(cudaGraphInstantiate(&sg.exec, graph, 0));
+        AB_CUDA(cudaGraphDestroy(graph));
+        sg.launches = g_launch_count - launches0;
+        g_launch_count = launches0;
+    }
+    AB_CUDA(cudaGraphLaunch(sg.exec, s));
+    g_launch_count += sg.launches;
+    if (!sg.prof.empty()) replayed_prof.push_back(&sg.prof);
+}
+
+void Ctx::clear_graphs() {
+    for (auto& kv : graphs)
+        if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    graphs.clear();
 }
 
 // ---------------------------------------------------------------------------
@@ -584,6 +726,8 @@ void Ctx::step(double lr, const int32_t* taus, float* loss_out, const float* hos
                      "staleness " + std::to_string(taus[l]) + " exceeds history depth " + std::to_string(history_depth));
     }
     cudaStream_t s = s_main;
+    if (!injected && !host_feats)
+        for (int j = 0; j < cfg.local_learners; ++j) sample_indices(learners[j], j);
     AB_CUDA(cudaEventRecord(ev0, s));
     // D1D: start the weight allreduce on the comm stream before the gradient compute
     if (strategy == ADPSGD_D1D && comm && comm->world > 1) comm->start_weight_sum(*this, s);
@@ -595,29 +739,26 @@ void Ctx::step(double lr, const int32_t* taus, float* loss_out, const float* hos
             AB_CUDA(cudaStreamSynchronize(s));
             continue;
         }
+        int mode = 0;
         if (host_feats) {
             const size_t nf = static_cast<size_t>(B) * T * I;
             AB_CUDA(cudaMemcpyAsync(stage_feats, host_feats + j * nf, nf * sizeof(float), cudaMemcpyHostToDevice, s));
             AB_CUDA(cudaMemcpyAsync(stage_labels, host_labels + static_cast<size_t>(j) * B * T,
                                     sizeof(int32_t) * B * T, cudaMemcpyHostToDevice, s));
-            gather_batch(stage_feats, stage_labels, ident_idx, s);
-        } else {
-            sample_and_gather(ln, s);
+            mode = 1;
         }
         const float* wpt = grad_point(ln, taus);
-        if (bf16_mode && wpt != ln.w[k & 1]) {
-            // lagged model: refresh a temporary shadow view (GENERIC only)
-            refresh_shadow(ln, wpt, s);
-        }
+        const bool lagged = wpt != ln.w[k & 1];
+        if (bf16_mode && lagged) refresh_shadow(ln, wpt, s);  // GENERIC: shadow of the lagged model
         if (ln.straggle > 1.0) AB_CUDA(cudaEventRecord(ev_comp0, s));
-        forward_backward(ln, wpt, ln.g, loss_dev + j, s);
+        run_compute(j, mode, wpt, s);
         if (ln.straggle > 1.0) {
             AB_CUDA(cudaEventRecord(ev_comp1, s));
             // stretch this learner's compute by (factor - 1) x its last measured compute time
             if (ln.last_compute_ms > 0)
                 launch_delay(static_cast<uint64_t>((ln.straggle - 1.0) * ln.last_compute_ms * 1e6), s);
         }
-        if (bf16_mode && wpt != ln.w[k & 1]) refresh_shadow(ln, ln.w[k & 1], s);
+        if (bf16_mode && lagged) refresh_shadow(ln, ln.w[k & 1], s);
     }
     AB_CUDA(cudaEventRecord(ev_mix, s));
     mix_and_update(lr, taus);
@@ -626,6 +767,8 @@ void Ctx::step(double lr, const int32_t* taus, float* loss_out, const float* hos
         AB_CUDA(cudaMemcpyAsync(h_loss, loss_dev, sizeof(float) * cfg.local_learners, cudaMemcpyDeviceToHost, s));
     }
     AB_CUDA(cudaStreamSynchronize(s));
+    for (auto* recs : replayed_prof) prof_accumulate(*recs);
+    replayed_prof.clear();
     if (!injected && loss_out) std::memcpy(loss_out, h_loss, sizeof(float) * cfg.local_learners);
     float ms = 0, mms = 0;
     AB_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));

@@ -3,12 +3,14 @@
 
 #include <cuda_runtime.h>
 
+#include <map>
 #include <memory>
 #include <string>
 #include <vector>
 
 #include "common.cuh"
 #include "model.hpp"
+#include "prof.hpp"
 #include "rng.hpp"
 
 namespace ab {
@@ -76,8 +78,17 @@ struct Ctx {
     float* stage_feats = nullptr;
     int32_t* stage_labels = nullptr;
     float* h_loss = nullptr;
-    int32_t* h_idx = nullptr;
-    int idx_flip = 0;
+    int32_t* h_idx = nullptr;  // pinned sampling slots, B per local learner
+
+    struct StepGraph {
+        cudaGraphExec_t exec = nullptr;
+        std::vector<ProfRec> prof;
+        int64_t launches = 0;
+    };
+    std::map<int, StepGraph> graphs;
+    std::vector<const std::vector<ProfRec>*> replayed_prof;
+    bool use_graphs = true;
+    bool use_fused_cell = true;
 
     std::vector<Learner> learners;
     std::unique_ptr<Comm> comm;
@@ -88,7 +99,10 @@ struct Ctx {
     void refresh_shadow(Learner& ln, const float* w, cudaStream_t s);
     void refresh_pad(Learner& ln, const float* w, cudaStream_t s);
     void gather_batch(const float* feats_src, const int32_t* labels_src, const int32_t* idx, cudaStream_t s);
-    void sample_and_gather(Learner& ln, cudaStream_t s);
+    void sample_indices(Learner& ln, int j);
+    void compute_body(int j, int mode, const float* wpt, cudaStream_t s);
+    void run_compute(int j, int mode, const float* wpt, cudaStream_t s);
+    void clear_graphs();
     void forward_backward(const Learner& ln, const float* master, float* grad, float* loss_slot, cudaStream_t s);
     void mix_and_update(double lr, const int32_t* taus);
     const float* grad_point(const Learner& ln, const int32_t* taus);

@@ -34,6 +34,7 @@ struct GemmArgs {
     float alpha = 1.0f;
     bool accumulate = false;
     const float* bias = nullptr;
+    int tag = 0;  // ProfCat of the tcgen05 launch (prof.hpp)
 };
 
 // fp32 operands, fp32 or bf16 output, any majorness (gemm_simt.cu).

@@ -1,0 +1,41 @@
+// Fused LSTM step kernels (gemm_lstm.cu): recurrent GEMM + cell forward, and BPTT
+// dgrad + cell backward, both directions of a layer per launch. bf16 mode, H % 64 == 0.
+#pragma once
+
+#include <cuda.h>
+
+#include <cstdint>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace ab {
+
+using EncodeFnT = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+struct LstmFwdDir {
+    const bf16* x; int64_t ldx; int Kx;       // x_t rows [B x Kx]
+    const bf16* w_ih; int64_t ld_wih;         // [4H x Kx]
+    const bf16* h_prev; int64_t ld_hprev;     // h_{t-1} rows [B x H] (nullptr at the first step)
+    const bf16* w_hh;                         // [4H x H]
+    const float* bias;                        // [4H] (fp32 master)
+    const float* c_prev;                      // [B x H] at ldc (nullptr at the first step)
+    float* gates; float* c; bf16* h;          // outputs (row pitch ldg / ldc / ldh)
+};
+
+struct LstmBwdDir {
+    const bf16* dz_src; int64_t ld_dz_src;    // dz_t [B x 4H] (A of the recurrent dgrad)
+    const bf16* w_hh;                         // [4H x H]
+    const float* dH;                          // dHout[t'] (+ d*H), row pitch lddh
+    float* dc_rec;                            // [B x H]
+    const float* gates; const float* c; const float* c_prev;  // at t' (c_prev may be nullptr)
+    bf16* dz_dst;                             // dz_{t'}
+};
+
+void lstm_fwd_step(const LstmFwdDir* dirs, int ndirs, int B, int H, int ldg, int ldc, int ldh, cudaStream_t s);
+void lstm_bwd_step(const LstmBwdDir* dirs, int ndirs, int B, int H, int lddh, int ldg, int ldc, int lddz,
+                   cudaStream_t s);
+
+}  // namespace ab

@@ -14,6 +14,7 @@
 #include <unordered_map>
 
 #include "gemm.hpp"
+#include "gemm_lstm.hpp"
 #include "tc_ptx.cuh"
 #include "prof.hpp"
 
@@ -231,23 +232,24 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
 
 // ---- host side -------------------------------------------------------------
 
-using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-EncodeFn encode_fn() {
-    static EncodeFn fn = nullptr;
+}  // namespace
+
+EncodeFnT get_encode_fn() {
+    static EncodeFnT fn = nullptr;
     static std::once_flag once;
     std::call_once(once, [] {
         void* p = nullptr;
         cudaDriverEntryPointQueryResult q;
         if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
             q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<EncodeFn>(p);
+            fn = reinterpret_cast<EncodeFnT>(p);
     });
     AB_CHECK(fn != nullptr, ADPSGD_E_CUDA, "cuTensorMapEncodeTiled unavailable");
     return fn;
 }
+
+namespace {
 
 // bf16 2-D tensor map, SWIZZLE_128B, box {64, box_outer}.
 void make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, int64_t ld_elems, uint32_t box_outer) {
@@ -257,7 +259,7 @@ void make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, 
     cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld_elems) * 2};
     cuuint32_t box[2] = {64, box_outer};
     cuuint32_t es[2] = {1, 1};
-    CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+    CUresult r = get_encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     AB_CHECK(r == CUDA_SUCCESS, ADPSGD_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
@@ -364,7 +366,7 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
     const int esz = g.c_bf16 ? 2 : 4;
     double ksum = 0;
     for (int i = 0; i < g.nseg; ++i) ksum += g.seg[i].K;
-    ProfScope ps_(s, PROF_GEMM_TC, 2.0 * g.M * g.N * ksum,
+    ProfScope ps_(s, g.tag, 2.0 * g.M * g.N * ksum,
                   2.0 * (static_cast<double>(g.M) + g.N) * ksum + static_cast<double>(g.M) * g.N * esz * (g.accumulate ? 2 : 1));
     p.vec_ok = ((reinterpret_cast<uintptr_t>(g.C) & 15) == 0) && ((g.ldc * esz) % 16 == 0);
     if (bn == 256) dispatch<256>(p, amn, bmn, g.c_bf16, s);

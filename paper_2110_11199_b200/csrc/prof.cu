@@ -1,18 +1,19 @@
 #include "prof.hpp"
 
 #include <mutex>
-#include <vector>
 
 #include "common.cuh"
 
 namespace ab {
 
 bool g_prof_enabled = false;
+std::vector<ProfRec>* g_prof_capture = nullptr;
 
 namespace {
-struct Rec { cudaEvent_t a, b; int cat; double flops, bytes; bool done; };
-std::vector<Rec> g_recs;
+std::vector<ProfRec> g_eager;
 std::vector<cudaEvent_t> g_pool;
+double g_ms[PROF_NCAT], g_flops[PROF_NCAT], g_bytes[PROF_NCAT];
+int64_t g_launches[PROF_NCAT];
 std::mutex g_mu;
 cudaEvent_t get_event() {
     if (!g_pool.empty()) { cudaEvent_t e = g_pool.back(); g_pool.pop_back(); return e; }
@@ -20,37 +21,50 @@ cudaEvent_t get_event() {
     AB_CUDA(cudaEventCreate(&e));
     return e;
 }
+std::vector<ProfRec>& target() { return g_prof_capture ? *g_prof_capture : g_eager; }
+void add(const ProfRec& r) {
+    float t = 0;
+    if (cudaEventElapsedTime(&t, r.a, r.b) != cudaSuccess) { cudaGetLastError(); return; }
+    if (r.cat < 0 || r.cat >= PROF_NCAT) return;
+    g_ms[r.cat] += t; g_flops[r.cat] += r.flops; g_bytes[r.cat] += r.bytes; g_launches[r.cat] += 1;
+}
 }  // namespace
 
 int prof_begin(cudaStream_t s) {
     std::lock_guard<std::mutex> lk(g_mu);
-    Rec r{get_event(), get_event(), 0, 0, 0, false};
-    AB_CUDA(cudaEventRecord(r.a, s));
-    g_recs.push_back(r);
-    return static_cast<int>(g_recs.size()) - 1;
+    ProfRec r{get_event(), get_event(), -1, 0, 0};
+    // inside stream capture a plain record is only a dependency marker; External makes it a
+    // real event-record node that fires on every replay
+    AB_CUDA(cudaEventRecordWithFlags(r.a, s, g_prof_capture ? cudaEventRecordExternal : cudaEventRecordDefault));
+    target().push_back(r);
+    return static_cast<int>(target().size()) - 1;
 }
 
 void prof_end(int id, cudaStream_t s, int cat, double flops, double bytes) {
     std::lock_guard<std::mutex> lk(g_mu);
-    Rec& r = g_recs[id];
-    AB_CUDA(cudaEventRecord(r.b, s));
-    r.cat = cat; r.flops = flops; r.bytes = bytes; r.done = true;
+    ProfRec& r = target()[id];
+    AB_CUDA(cudaEventRecordWithFlags(r.b, s, g_prof_capture ? cudaEventRecordExternal : cudaEventRecordDefault));
+    r.cat = cat; r.flops = flops; r.bytes = bytes;
+}
+
+void prof_accumulate(const std::vector<ProfRec>& recs) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (const auto& r : recs) add(r);
 }
 
 void prof_read(double* ms, double* flops, double* bytes, int64_t* launches, int ncat) {
     std::lock_guard<std::mutex> lk(g_mu);
     AB_CUDA(cudaDeviceSynchronize());
-    for (int c = 0; c < ncat; ++c) { ms[c] = 0; flops[c] = 0; bytes[c] = 0; launches[c] = 0; }
-    for (auto& r : g_recs) {
-        if (r.done && r.cat < ncat) {
-            float t = 0;
-            AB_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
-            ms[r.cat] += t; flops[r.cat] += r.flops; bytes[r.cat] += r.bytes; launches[r.cat] += 1;
-        }
+    for (auto& r : g_eager) {
+        add(r);
         g_pool.push_back(r.a);
         g_pool.push_back(r.b);
     }
-    g_recs.clear();
+    g_eager.clear();
+    for (int c = 0; c < ncat && c < PROF_NCAT; ++c) {
+        ms[c] = g_ms[c]; flops[c] = g_flops[c]; bytes[c] = g_bytes[c]; launches[c] = g_launches[c];
+    }
+    for (int c = 0; c < PROF_NCAT; ++c) { g_ms[c] = 0; g_flops[c] = 0; g_bytes[c] = 0; g_launches[c] = 0; }
 }
 
 }  // namespace ab

@@ -68,6 +68,35 @@ def test_gradient_bf16_tensor_core_tolerance(oracle_mod, name):
     assert rel <= 5e-2
 
 
+@pytest.mark.parametrize("bidir", [True, False])
+def test_fused_lstm_kernels_match_oracle_and_unfused(oracle_mod, monkeypatch, bidir):
+    """H % 64 == 0 selects the fused tcgen05 recurrent kernels (cell fwd / bwd in the GEMM
+    epilogue); they must agree with the oracle (bf16 tolerance) and with the unfused
+    GEMM + pointwise path (same bf16 operands)."""
+    O = oracle_mod
+    m = ModelDesc(layers=2, hidden=64, bidirectional=bidir, input_dim=40, proj=16, classes=48, unroll=9)
+    feats, labels = _data(m)
+    M = 136  # > one 128-row tile: exercises the row mask
+    rng = np.random.default_rng(3)
+    idx = rng.integers(0, 40, size=M).astype(np.int32)
+    grads = {}
+    for fused in ("1", "0"):
+        monkeypatch.setenv("ADPSGD_NO_FUSED", "0" if fused == "1" else "1")
+        g = LearnerGroup(m, StrategyConfig(learners=1, batch=M, seed=1), precision=Precision.BF16)
+        g.set_dataset(feats, labels, 40)
+        w = np.random.default_rng(11).normal(0, 0.2, g.D)
+        grads[fused] = g.gradient(w, idx)
+        g.close()
+    oloss, ograd = O.lstm_loss_grad(_odesc(O, m), w, feats, labels, idx)
+    (lf, gf), (lu, gu) = grads["1"], grads["0"]
+    rel_o = np.linalg.norm(gf - ograd) / np.linalg.norm(ograd)
+    rel_u = np.linalg.norm(gf - gu) / np.linalg.norm(gu)
+    print(f"fused vs oracle {rel_o:.2e}, fused vs unfused {rel_u:.2e}")
+    assert abs(lf - oloss) <= 1e-2 * oloss
+    assert rel_o <= 5e-2
+    assert rel_u <= 1e-2
+
+
 def _engine_pair(O, m, strategy, L, M, seed, precision=Precision.FP32, depth=2, cap=1, mix=MixKind.UNIFORM):
     feats, labels = _data(m, seed=seed)
     cfg = StrategyConfig(strategy=strategy, learners=L, batch=M, seed=seed, staleness_cap=cap, generic_mix=mix)
