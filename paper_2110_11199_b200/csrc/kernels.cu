@@ -209,11 +209,39 @@ __global__ void mix3_kernel(int64_t n, const float* __restrict__ w, const float*
     }
 }
 
+__device__ __forceinline__ float4 f4add(float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
+__device__ __forceinline__ void st_shadow4(bf16* sh, int64_t i4, float4 o) {
+    __nv_bfloat162 lo = __floats2bfloat162_rn(o.x, o.y), hi = __floats2bfloat162_rn(o.z, o.w);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&lo);
+    u.y = *reinterpret_cast<uint32_t*>(&hi);
+    reinterpret_cast<uint2*>(sh)[i4] = u;
+}
+
+// D1D update, float4-vectorised: one pass reads the L models (or their allreduced sum) and
+// the local gradients, writes the new fp32 models and their bf16 shadows.
 __global__ void d1d_kernel(int64_t n, int L, PtrTab w, const float* __restrict__ w_sum, int nloc, PtrTab g, float lr,
                            MutTab out, BfTab sh) {
     const float invL = 1.0f / static_cast<float>(L);
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t n4 = n / 4;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4; i += stride) {
+        float4 s;
+        if (w_sum) {
+            s = reinterpret_cast<const float4*>(w_sum)[i];
+        } else {
+            s = reinterpret_cast<const float4*>(w.p[0])[i];
+            for (int l = 1; l < L; ++l) s = f4add(s, reinterpret_cast<const float4*>(w.p[l])[i]);
+        }
+        for (int j = 0; j < nloc; ++j) {
+            const float4 gg = reinterpret_cast<const float4*>(g.p[j])[i];
+            const float4 o = make_float4(s.x * invL - lr * gg.x, s.y * invL - lr * gg.y, s.z * invL - lr * gg.z,
+                                         s.w * invL - lr * gg.w);
+            reinterpret_cast<float4*>(out.p[j])[i] = o;
+            if (sh.p[j]) st_shadow4(sh.p[j], i, o);
+        }
+    }
+    for (int64_t i = n4 * 4 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
         float s;
         if (w_sum) {
             s = w_sum[i];
@@ -221,20 +249,37 @@ __global__ void d1d_kernel(int64_t n, int L, PtrTab w, const float* __restrict__
             s = 0.f;
             for (int l = 0; l < L; ++l) s += w.p[l][i];
         }
-        const float mean = s * invL;
         for (int j = 0; j < nloc; ++j) {
-            const float o = mean - lr * g.p[j][i];
+            const float o = s * invL - lr * g.p[j][i];
             out.p[j][i] = o;
             if (sh.p[j]) sh.p[j][i] = __float2bfloat16_rn(o);
         }
     }
 }
 
+// SDPSGD update (engine.cpp:145-153), float4-vectorised.
 __global__ void sdpsgd_kernel(int64_t n, int L, const float* __restrict__ w, PtrTab g, const float* __restrict__ g_sum,
                               int nloc, float lr, MutTab out, BfTab sh) {
     const float invL = 1.0f / static_cast<float>(L);
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t n4 = n / 4;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4; i += stride) {
+        float4 s;
+        if (g_sum) {
+            s = reinterpret_cast<const float4*>(g_sum)[i];
+        } else {
+            s = reinterpret_cast<const float4*>(g.p[0])[i];
+            for (int l = 1; l < L; ++l) s = f4add(s, reinterpret_cast<const float4*>(g.p[l])[i]);
+        }
+        const float4 wv = reinterpret_cast<const float4*>(w)[i];
+        const float4 o = make_float4(wv.x - lr * (s.x * invL), wv.y - lr * (s.y * invL), wv.z - lr * (s.z * invL),
+                                     wv.w - lr * (s.w * invL));
+        for (int j = 0; j < nloc; ++j) {
+            reinterpret_cast<float4*>(out.p[j])[i] = o;
+            if (sh.p[j]) st_shadow4(sh.p[j], i, o);
+        }
+    }
+    for (int64_t i = n4 * 4 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
         float s;
         if (g_sum) {
             s = g_sum[i];
@@ -404,7 +449,7 @@ void launch_d1d(int64_t n, int L, const float* const* w_tab, const float* w_sum,
     if (!w_sum)
         for (int i = 0; i < L; ++i) w.p[i] = w_tab[i];
     for (int j = 0; j < nloc; ++j) { g.p[j] = g_tab[j]; o.p[j] = out_tab[j]; sh.p[j] = shadow_tab[j]; }
-    d1d_kernel<<<grid_for(n, 256, 4), 256, 0, s>>>(n, L, w, w_sum, nloc, g, lr, o, sh);
+    d1d_kernel<<<grid_for((n + 3) / 4, 256, 4), 256, 0, s>>>(n, L, w, w_sum, nloc, g, lr, o, sh);
     count_launch();
 }
 
@@ -418,7 +463,7 @@ void launch_sdpsgd(int64_t n, int L, const float* w, const float* const* g_tab, 
     if (!g_sum)
         for (int i = 0; i < L; ++i) g.p[i] = g_tab[i];
     for (int j = 0; j < nloc; ++j) { o.p[j] = out_tab[j]; sh.p[j] = shadow_tab[j]; }
-    sdpsgd_kernel<<<grid_for(n, 256, 4), 256, 0, s>>>(n, L, w, g, g_sum, nloc, lr, o, sh);
+    sdpsgd_kernel<<<grid_for((n + 3) / 4, 256, 4), 256, 0, s>>>(n, L, w, g, g_sum, nloc, lr, o, sh);
     count_launch();
 }
 
