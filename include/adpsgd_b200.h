@@ -161,6 +161,9 @@ int adpsgd_profile_enable(int32_t on);
  * bytes and launch counts accumulated since the last read, then clears them. */
 int adpsgd_profile_read(double* ms, double* flops, double* bytes, int64_t* launches, int32_t ncat);
 
+/* Debug: device timeline of the CTA-pair tensor-core kernels (160 CTAs x 32 globaltimer stamps). */
+int adpsgd_debug_trace(int32_t enable, uint64_t* out, int32_t n);
+
 /* ---- kernel-level entry points (tests / benchmarks; device pointers) ---- */
 /* C[M,N] = alpha * sum_k A(m,k) B(n,k) (+ C if accumulate) (+ bias[n]).
  * A(m,k) = a_mn ? A[k*lda+m] : A[m*lda+k]; B likewise. bf16 = 1: A,B bf16, tcgen05;

@@ -67,6 +67,7 @@ _SIGS = {
     "adpsgd_barrier": (C.c_int, [C.c_void_p]),
     "adpsgd_profile_enable": (C.c_int, [i32]),
     "adpsgd_profile_read": (C.c_int, [P(C.c_double), P(C.c_double), P(C.c_double), P(i64), i32]),
+    "adpsgd_debug_trace": (C.c_int, [i32, C.c_void_p, i32]),
     "adpsgd_gemm": (C.c_int, [i32, i32, i32, i32, C.c_void_p, i64, i32, C.c_void_p, i64, i32, C.c_void_p, i64,
                               i32, C.c_float, i32, C.c_void_p, C.c_void_p]),
     "adpsgd_mix_update": (C.c_int, [i64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_float, C.c_void_p,

@@ -326,6 +326,17 @@ int adpsgd_profile_read(double* ms, double* flops, double* bytes, int64_t* launc
     return guard([&] { prof_read(ms, flops, bytes, launches, ncat < PROF_NCAT ? ncat : PROF_NCAT); });
 }
 
+}  // extern "C"
+namespace ab { void trace_enable(int); void trace_read(unsigned long long*, int); }
+extern "C" {
+// Debug: device timeline of the CTA-pair tcgen05 kernels (160 CTAs x 32 globaltimer stamps).
+int adpsgd_debug_trace(int32_t enable, uint64_t* out, int32_t n) {
+    return guard([&] {
+        if (out) ab::trace_read(reinterpret_cast<unsigned long long*>(out), n);
+        ab::trace_enable(enable);
+    });
+}
+
 int adpsgd_gemm(int32_t bf, int32_t M, int32_t N, int32_t K, const void* A, int64_t lda, int32_t a_mn, const void* B,
                 int64_t ldb, int32_t b_mn, void* Cout, int64_t ldc, int32_t c_bf16, float alpha, int32_t accumulate,
                 const float* bias, void* stream) {

@@ -30,6 +30,8 @@
 
 namespace ab {
 
+extern bool g_use_pair_mma;  // gemm_lstm.cu
+
 namespace {
 thread_local std::string g_last_error;
 
@@ -100,6 +102,7 @@ Ctx::Ctx(const adpsgd_config& c) : cfg(c) {
     history_depth = c.strategy == ADPSGD_GENERIC ? c.staleness_cap + 1 : 1;  // engine.cpp:216-217
     if (const char* e = std::getenv("ADPSGD_NO_GRAPHS")) use_graphs = e[0] == '0';
     if (const char* e = std::getenv("ADPSGD_NO_FUSED")) use_fused_cell = e[0] == '0';
+    if (const char* e = std::getenv("ADPSGD_NO_PAIR")) g_use_pair_mma = e[0] == '0';
 
     AB_CUDA(cudaSetDevice(c.device));
     AB_CUDA(cudaStreamCreateWithFlags(&s_main, cudaStreamNonBlocking));
@@ -118,7 +121,7 @@ Ctx::Ctx(const adpsgd_config& c) : cfg(c) {
     lab_step = static_cast<int32_t*>(alloc(sizeof(int32_t) * TB));
     for (int l = 0; l < lay.L; ++l) {
         Hout.push_back(alloc(TB * ndH * es));
-        gates.push_back(static_cast<float*>(alloc(TB * nd4H * sizeof(float))));
+        gates.push_back(alloc(TB * nd4H * es));  // gate activations in the activation type
         cst.push_back(static_cast<float*>(alloc(TB * ndH * sizeof(float))));
     }
     if (lay.P > 0) {
@@ -242,7 +245,7 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
                     a.w_hh = static_cast<const bf16*>(W.at(lay.dir[l][d].w_hh));
                     a.bias = master + lay.dir[l][d].b;
                     a.c_prev = st > 0 ? cst[l] + static_cast<int64_t>(tp) * B * ndH + d * H : nullptr;
-                    a.gates = gates[l] + static_cast<int64_t>(t) * B * nd4H + d * G4;
+                    a.gates = static_cast<bf16*>(off_ptr(gates[l], static_cast<int64_t>(t) * B * nd4H + d * G4, es));
                     a.c = cst[l] + static_cast<int64_t>(t) * B * ndH + d * H;
                     a.h = static_cast<bf16*>(off_ptr(Hout[l], static_cast<int64_t>(t) * B * ndH + d * H, es));
                 }
@@ -274,14 +277,14 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
                 g.bias = master + lay.dir[l][d].b;
                 gemm(bf, g, s);
                 const float* cprev = st > 0 ? cst[l] + static_cast<int64_t>(tp) * B * ndH + d * H : nullptr;
-                float* gt = gates[l] + static_cast<int64_t>(t) * B * nd4H + d * G4;
+                void* gt = off_ptr(gates[l], static_cast<int64_t>(t) * B * nd4H + d * G4, es);
                 float* ct = cst[l] + static_cast<int64_t>(t) * B * ndH + d * H;
                 void* ht = off_ptr(Hout[l], static_cast<int64_t>(t) * B * ndH + d * H, es);
                 if (bf)
-                    launch_cell_fwd<bf16>(zstep + static_cast<int64_t>(d) * B * G4, G4, cprev, ndH, gt, nd4H, ct,
+                    launch_cell_fwd<bf16>(zstep + static_cast<int64_t>(d) * B * G4, G4, cprev, ndH, static_cast<bf16*>(gt), nd4H, ct,
                                           static_cast<bf16*>(ht), ndH, B, H, s);
                 else
-                    launch_cell_fwd<float>(zstep + static_cast<int64_t>(d) * B * G4, G4, cprev, ndH, gt, nd4H, ct,
+                    launch_cell_fwd<float>(zstep + static_cast<int64_t>(d) * B * G4, G4, cprev, ndH, static_cast<float*>(gt), nd4H, ct,
                                            static_cast<float*>(ht), ndH, B, H, s);
             }
         }
@@ -391,7 +394,7 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
                 const float* cp = T > 1 ? cst[l] + static_cast<int64_t>(tp) * B * ndH + d * H : nullptr;
                 launch_cell_bwd<bf16>(dHcur + static_cast<int64_t>(t) * B * ndH + d * H, ndH, nullptr,
                                       dc_rec + static_cast<int64_t>(d) * B * H, true,
-                                      gates[l] + static_cast<int64_t>(t) * B * nd4H + d * G4, nd4H,
+                                      static_cast<const bf16*>(off_ptr(gates[l], static_cast<int64_t>(t) * B * nd4H + d * G4, es)), nd4H,
                                       cst[l] + static_cast<int64_t>(t) * B * ndH + d * H, cp, ndH,
                                       static_cast<bf16*>(off_ptr(dZ, static_cast<int64_t>(t) * B * nd4H + d * G4, es)),
                                       nd4H, B, H, s);
@@ -409,7 +412,7 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
                     a.w_hh = static_cast<const bf16*>(W.at(lay.dir[l][d].w_hh));
                     a.dH = dHcur + static_cast<int64_t>(tn) * B * ndH + d * H;
                     a.dc_rec = dc_rec + static_cast<int64_t>(d) * B * H;
-                    a.gates = gates[l] + static_cast<int64_t>(tn) * B * nd4H + d * G4;
+                    a.gates = static_cast<const bf16*>(off_ptr(gates[l], static_cast<int64_t>(tn) * B * nd4H + d * G4, es));
                     a.c = cst[l] + static_cast<int64_t>(tn) * B * ndH + d * H;
                     a.c_prev = sn > 0 ? cst[l] + static_cast<int64_t>(tnp) * B * ndH + d * H : nullptr;
                     a.dz_dst = static_cast<bf16*>(off_ptr(dZ, static_cast<int64_t>(tn) * B * nd4H + d * G4, es));
@@ -424,16 +427,16 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
                 const int tp = d == 0 ? t - 1 : t + 1;
                 float* dhr = dh_rec + static_cast<int64_t>(d) * B * H;
                 float* dcr = dc_rec + static_cast<int64_t>(d) * B * H;
-                const float* gt = gates[l] + static_cast<int64_t>(t) * B * nd4H + d * G4;
+                const void* gt = off_ptr(gates[l], static_cast<int64_t>(t) * B * nd4H + d * G4, es);
                 const float* ct = cst[l] + static_cast<int64_t>(t) * B * ndH + d * H;
                 const float* cp = sf > 0 ? cst[l] + static_cast<int64_t>(tp) * B * ndH + d * H : nullptr;
                 void* dzt = off_ptr(dZ, static_cast<int64_t>(t) * B * nd4H + d * G4, es);
                 const float* dHt = dHcur + static_cast<int64_t>(t) * B * ndH + d * H;
                 if (bf)
-                    launch_cell_bwd<bf16>(dHt, ndH, dhr, dcr, st == 0, gt, nd4H, ct, cp, ndH, static_cast<bf16*>(dzt),
+                    launch_cell_bwd<bf16>(dHt, ndH, dhr, dcr, st == 0, static_cast<const bf16*>(gt), nd4H, ct, cp, ndH, static_cast<bf16*>(dzt),
                                           nd4H, B, H, s);
                 else
-                    launch_cell_bwd<float>(dHt, ndH, dhr, dcr, st == 0, gt, nd4H, ct, cp, ndH,
+                    launch_cell_bwd<float>(dHt, ndH, dhr, dcr, st == 0, static_cast<const float*>(gt), nd4H, ct, cp, ndH,
                                            static_cast<float*>(dzt), nd4H, B, H, s);
                 if (sf > 0) {  // dh_{prev} = dz_t W_hh
                     GemmArgs g;

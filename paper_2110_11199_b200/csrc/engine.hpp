@@ -60,7 +60,8 @@ struct Ctx {
     void* X0 = nullptr;
     int32_t* lab_step = nullptr;
     std::vector<void*> Hout;
-    std::vector<float*> gates, cst;
+    std::vector<void*> gates;  // gate activations i,f,g,o (activation type)
+    std::vector<float*> cst;
     void* Y = nullptr;
     void* dY = nullptr;
     float* logits = nullptr;

@@ -12,6 +12,8 @@
 //     dh = dH[t'] + dh_rec; dc = dc_rec + dh o (1 - tanh^2 c); dz_{t'} = ...; dc_rec = dc f
 #include <cuda.h>
 
+#include <cstdlib>
+
 #include "gemm_lstm.hpp"
 #include "prof.hpp"
 #include "tc_core.cuh"
@@ -19,38 +21,47 @@
 namespace ab {
 
 EncodeFnT get_encode_fn();  // gemm_tc.cu
+unsigned long long* trace_take();  // prof.cu
 
 namespace {
 
 using tc::kBK;
 using tc::kBM;
 
-__device__ __forceinline__ float sigf(float x) { return 1.f / (1.f + __expf(-x)); }
+// One MUFU.TANH each (max rel. err ~2^-11, below the bf16 rounding of the stored activations);
+// an IEEE-division sigmoid/tanh compiles to branchy slow paths that serialise the unrolled
+// per-row element chains of the epilogue (measured ~15 us per 32-unit chunk).
 __device__ __forceinline__ float tanhf_fast(float x) {
-    // tanh via exp; accurate to ~1e-6 relative in fp32 for the ranges of an LSTM cell
-    const float e = __expf(-2.f * fabsf(x));
-    const float t = (1.f - e) / (1.f + e);
-    return copysignf(t, x);
+    float y;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
 }
+__device__ __forceinline__ float sigf(float x) { return fmaf(0.5f, tanhf_fast(0.5f * x), 0.5f); }
 
 // ---------------- forward ----------------
 struct FwdGroup {
     CUtensorMap ta[2];
     CUtensorMap tb[2];
+    CUtensorMap m_cprev, m_gates, m_c, m_h;  // epilogue I/O (TMA)
     int kb0, kb1, nseg;
     const float* bias;
     const float* c_prev;
-    float* gates;
+    bf16* gates;
     float* c;
     bf16* h;
 };
 struct FwdParams {
     FwdGroup g[2];
     int ngroups, m_tiles, n_tiles, B, H, ldg, ldc, ldh;
+    int epi_skip;  // debug: timing experiments only
+    unsigned long long* trace;
 };
 
 struct FwdTraits {
     static constexpr int BN = 256;
+    // per warp (20 KB): c_{t-1} box (fp32 32x32, SW128) | c box | 4 gate boxes (bf16 32x32, SW64) | h box
+    static constexpr int EPI_WARP = 20 * 1024;
+    static constexpr int EPI_SMEM = 4 * EPI_WARP;
     static constexpr bool B_MN = false;
     __device__ static int num_tiles(const FwdParams& p) { return p.ngroups * p.m_tiles * p.n_tiles; }
     __device__ static void prefetch(const FwdParams& p) {
@@ -74,66 +85,148 @@ struct FwdTraits {
         const FwdGroup& g = p.g[grp];
         const int s = kb < g.kb0 ? 0 : 1;
         const int k0 = (s == 0 ? kb : kb - g.kb0) * kBK;
-        ptx::tma_load_2d(sA, &g.ta[s], bar, k0, m0);
+        ptx::tma_load_2d_hint(sA, &g.ta[s], bar, k0, m0, ptx::policy_evict_first());
+        const uint64_t keep = ptx::policy_evict_last();
 #pragma unroll
         for (int gate = 0; gate < 4; ++gate)
-            ptx::tma_load_2d(sB + gate * 64 * kBK * 2, &g.tb[s], bar, k0, gate * p.H + u0);
+            ptx::tma_load_2d_hint(sB + gate * 64 * kBK * 2, &g.tb[s], bar, k0, gate * p.H + u0, keep);
     }
-    __device__ static void epilogue(const FwdParams& p, int tile, uint32_t tbase, int q, int lane, uint64_t* tempty) {
+    // CTA pair: rank r loads rows [m0 + 128 r, +128) of A and gates {2r, 2r+1} of B
+    static constexpr bool A_MN = false;
+    __device__ static void coords2(const FwdParams& p, int tile, int& grp, int& m0, int& u0) {
+        const int per = p.m_tiles * p.n_tiles;
+        grp = tile / per;
+        const int r = tile % per;
+        m0 = (r % p.m_tiles) * 2 * kBM;
+        u0 = (r / p.m_tiles) * 64;
+    }
+    __device__ static void load2(const FwdParams& p, int tile, int kb, uint32_t rank, uint8_t* sA, uint8_t* sB,
+                                 uint32_t bar) {
+        int grp, m0, u0;
+        coords2(p, tile, grp, m0, u0);
+        const FwdGroup& g = p.g[grp];
+        const int s = kb < g.kb0 ? 0 : 1;
+        const int k0 = (s == 0 ? kb : kb - g.kb0) * kBK;
+        ptx::tma_load_2d_2sm_hint(sA, &g.ta[s], bar, k0, m0 + kBM * rank, ptx::policy_evict_first());
+        const uint64_t keep = ptx::policy_evict_last();
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+            ptx::tma_load_2d_2sm_hint(sB + j * 64 * kBK * 2, &g.tb[s], bar, k0, (2 * rank + j) * p.H + u0, keep);
+    }
+    __device__ static void epilogue2(const FwdParams& p, int tile, uint32_t rank, uint32_t tbase, int q, int lane,
+                                     uint32_t tempty_leader, uint8_t* st, uint64_t* ebar, uint32_t& ephase) {
+        int grp, m0, u0;
+        coords2(p, tile, grp, m0, u0);
+        body(p, grp, m0 + kBM * rank, u0, tbase, q, lane, [&] { tc::release_acc_2sm(tempty_leader, lane); }, st, ebar,
+             ephase);
+    }
+    __device__ static void epilogue(const FwdParams& p, int tile, uint32_t tbase, int q, int lane, uint64_t* tempty,
+                                    uint8_t* st, uint64_t* ebar, uint32_t& ephase) {
         int grp, m0, u0;
         coords(p, tile, grp, m0, u0);
+        body(p, grp, m0, u0, tbase, q, lane, [&] { tc::release_acc(tempty, lane); }, st, ebar, ephase);
+    }
+    // epilogue (thread = row): per 32-unit chunk, c_{t-1} arrives by TMA into swizzled smem while
+    // the 4 gate columns leave TMEM; the cell runs in registers; gates (bf16), c (fp32) and h
+    // (bf16) are written as swizzled smem boxes and leave by TMA bulk stores (fully coalesced,
+    // asynchronous, rows >= B clipped by the tensor map).
+    template <class Rel>
+    __device__ static void body(const FwdParams& p, int grp, int m0, int u0, uint32_t tbase, int q, int lane,
+                                Rel release, uint8_t* st, uint64_t* ebar, uint32_t& ephase) {
         const FwdGroup& g = p.g[grp];
-        const int r = m0 + q * 32 + lane;
-        const bool ok = r < p.B;
         const int H = p.H;
+        const int rowbase = m0 + q * 32;
+        uint8_t* cin = st;
+        uint8_t* cbox = st + 4096;
+        uint8_t* gbox = st + 8192;  // 4 x 2 KB
+        uint8_t* hbox = st + 16384;
+        const bool has_prev = g.c_prev != nullptr;
 #pragma unroll 1
         for (int uc = 0; uc < 64; uc += 32) {
+            const int j0 = u0 + uc;
+            if (has_prev && lane == 0) {
+                ptx::mbar_arrive_expect_tx(ebar, 32 * 32 * 4);
+                ptx::tma_load_2d(cin, &g.m_cprev, ebar, j0, rowbase);
+            }
             uint32_t zi[32], zf[32], zg[32], zo[32];
             ptx::tmem_ld_32x32b_x32(tbase + 0 * 64 + uc, zi);
             ptx::tmem_ld_32x32b_x32(tbase + 1 * 64 + uc, zf);
             ptx::tmem_ld_32x32b_x32(tbase + 2 * 64 + uc, zg);
             ptx::tmem_ld_32x32b_x32(tbase + 3 * 64 + uc, zo);
             ptx::tmem_ld_wait();
-            if (uc == 32) tc::release_acc(tempty, lane);
-            if (!ok) continue;
-            const int j0 = u0 + uc;
-            const float* bi = g.bias + j0;
-            float* grow = g.gates + static_cast<int64_t>(r) * p.ldg + j0;
-            float* crow = g.c + static_cast<int64_t>(r) * p.ldc + j0;
-            const float* cprow = g.c_prev ? g.c_prev + static_cast<int64_t>(r) * p.ldc + j0 : nullptr;
-            bf16* hrow = g.h + static_cast<int64_t>(r) * p.ldh + j0;
+            const bool tr = q == 2 && lane == 0;
+            if (tr) tc::trace_once(p.trace, 12 + (uc / 32) * 4 + 0);
+            if (uc == 32) release();
+            float cp[32];
+            if (has_prev) {
+                ptx::mbar_wait(ebar, ephase);
+                ephase ^= 1;
+                tc::ld_row_f32_sw128(cin, lane, cp);
+            } else {
 #pragma unroll
-            for (int i0 = 0; i0 < 32; i0 += 4) {
-                const float4 bI = __ldg(reinterpret_cast<const float4*>(bi + i0));
-                const float4 bF = __ldg(reinterpret_cast<const float4*>(bi + H + i0));
-                const float4 bG = __ldg(reinterpret_cast<const float4*>(bi + 2 * H + i0));
-                const float4 bO = __ldg(reinterpret_cast<const float4*>(bi + 3 * H + i0));
-                const float4 cp4 = cprow ? *reinterpret_cast<const float4*>(cprow + i0) : make_float4(0.f, 0.f, 0.f, 0.f);
-                const float bIa[4] = {bI.x, bI.y, bI.z, bI.w}, bFa[4] = {bF.x, bF.y, bF.z, bF.w};
-                const float bGa[4] = {bG.x, bG.y, bG.z, bG.w}, bOa[4] = {bO.x, bO.y, bO.z, bO.w};
-                const float cpa[4] = {cp4.x, cp4.y, cp4.z, cp4.w};
-                float ig[4], fg[4], gg[4], og[4], cn[4], hn[4];
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int i = i0 + e;
-                    ig[e] = sigf(__uint_as_float(zi[i]) + bIa[e]);
-                    fg[e] = sigf(__uint_as_float(zf[i]) + bFa[e]);
-                    gg[e] = tanhf_fast(__uint_as_float(zg[i]) + bGa[e]);
-                    og[e] = sigf(__uint_as_float(zo[i]) + bOa[e]);
-                    cn[e] = fg[e] * cpa[e] + ig[e] * gg[e];
-                    hn[e] = og[e] * tanhf_fast(cn[e]);
-                }
-                *reinterpret_cast<float4*>(grow + i0) = make_float4(ig[0], ig[1], ig[2], ig[3]);
-                *reinterpret_cast<float4*>(grow + H + i0) = make_float4(fg[0], fg[1], fg[2], fg[3]);
-                *reinterpret_cast<float4*>(grow + 2 * H + i0) = make_float4(gg[0], gg[1], gg[2], gg[3]);
-                *reinterpret_cast<float4*>(grow + 3 * H + i0) = make_float4(og[0], og[1], og[2], og[3]);
-                *reinterpret_cast<float4*>(crow + i0) = make_float4(cn[0], cn[1], cn[2], cn[3]);
-                __nv_bfloat162 h01 = __floats2bfloat162_rn(hn[0], hn[1]), h23 = __floats2bfloat162_rn(hn[2], hn[3]);
-                uint2 hv;
-                hv.x = *reinterpret_cast<uint32_t*>(&h01);
-                hv.y = *reinterpret_cast<uint32_t*>(&h23);
-                *reinterpret_cast<uint2*>(hrow + i0) = hv;
+                for (int i = 0; i < 32; ++i) cp[i] = 0.f;
             }
+            if (tr) tc::trace_once(p.trace, 12 + (uc / 32) * 4 + 1);
+            if (p.epi_skip) continue;
+            float a[32];
+            // i
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+                const float4 b4 = __ldg(reinterpret_cast<const float4*>(g.bias + j0 + i));
+                a[i] = sigf(__uint_as_float(zi[i]) + b4.x); a[i + 1] = sigf(__uint_as_float(zi[i + 1]) + b4.y);
+                a[i + 2] = sigf(__uint_as_float(zi[i + 2]) + b4.z); a[i + 3] = sigf(__uint_as_float(zi[i + 3]) + b4.w);
+            }
+            tc::st_row_bf16_sw64(gbox + 0 * 2048, lane, a);
+            // g, and i*g into cp (c_t = f c_{t-1} + i g, accumulated in two parts)
+            float gv[32];
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+                const float4 b4 = __ldg(reinterpret_cast<const float4*>(g.bias + 2 * H + j0 + i));
+                gv[i] = tanhf_fast(__uint_as_float(zg[i]) + b4.x);
+                gv[i + 1] = tanhf_fast(__uint_as_float(zg[i + 1]) + b4.y);
+                gv[i + 2] = tanhf_fast(__uint_as_float(zg[i + 2]) + b4.z);
+                gv[i + 3] = tanhf_fast(__uint_as_float(zg[i + 3]) + b4.w);
+            }
+            tc::st_row_bf16_sw64(gbox + 2 * 2048, lane, gv);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) gv[i] *= a[i];  // i * g
+            // f
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+                const float4 b4 = __ldg(reinterpret_cast<const float4*>(g.bias + H + j0 + i));
+                a[i] = sigf(__uint_as_float(zf[i]) + b4.x); a[i + 1] = sigf(__uint_as_float(zf[i + 1]) + b4.y);
+                a[i + 2] = sigf(__uint_as_float(zf[i + 2]) + b4.z); a[i + 3] = sigf(__uint_as_float(zf[i + 3]) + b4.w);
+            }
+            tc::st_row_bf16_sw64(gbox + 1 * 2048, lane, a);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) cp[i] = a[i] * cp[i] + gv[i];  // c_t
+            tc::st_row_f32_sw128(cbox, lane, cp);
+            // o, h
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+                const float4 b4 = __ldg(reinterpret_cast<const float4*>(g.bias + 3 * H + j0 + i));
+                a[i] = sigf(__uint_as_float(zo[i]) + b4.x); a[i + 1] = sigf(__uint_as_float(zo[i + 1]) + b4.y);
+                a[i + 2] = sigf(__uint_as_float(zo[i + 2]) + b4.z); a[i + 3] = sigf(__uint_as_float(zo[i + 3]) + b4.w);
+            }
+            tc::st_row_bf16_sw64(gbox + 3 * 2048, lane, a);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) a[i] *= tanhf_fast(cp[i]);
+            tc::st_row_bf16_sw64(hbox, lane, a);
+            if (tr) tc::trace_once(p.trace, 12 + (uc / 32) * 4 + 2);
+            ptx::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+#pragma unroll
+                const uint64_t stream = ptx::policy_evict_first();
+                for (int gi = 0; gi < 4; ++gi)
+                    ptx::tma_store_2d_hint(&g.m_gates, gbox + gi * 2048, gi * H + j0, rowbase, stream);
+                ptx::tma_store_2d(&g.m_c, cbox, j0, rowbase);
+                ptx::tma_store_2d(&g.m_h, hbox, j0, rowbase);
+                ptx::bulk_commit();
+                ptx::bulk_wait_read0();  // staging boxes reusable by the next chunk
+            }
+            if (tr) tc::trace_once(p.trace, 12 + (uc / 32) * 4 + 3);
+            __syncwarp();
         }
     }
 };
@@ -142,10 +235,11 @@ struct FwdTraits {
 struct BwdGroup {
     CUtensorMap ta;
     CUtensorMap tb;
+    CUtensorMap m_dH, m_dc, m_gates, m_c, m_cp, m_dz;  // epilogue I/O (TMA), 16-unit x 32-row boxes
     int kb;
     const float* dH;
     float* dc_rec;
-    const float* gates;
+    const bf16* gates;
     const float* c;
     const float* c_prev;
     bf16* dz;
@@ -153,11 +247,16 @@ struct BwdGroup {
 struct BwdParams {
     BwdGroup g[2];
     int ngroups, m_tiles, n_tiles, B, H, lddh, ldg, ldc, lddz;
+    int epi_skip;  // debug: timing experiments only
+    unsigned long long* trace;
 };
 
 template <int BN_>
 struct BwdTraits {
     static constexpr int BN = BN_;
+    // per warp (16 KB): dH | dc | c | c_prev (fp32 16x32, SW64, 2 KB each) | gates 4 x (bf16 16x32, SW32, 1 KB)
+    //                   | dz 4 x (bf16 16x32, SW32, 1 KB)
+    static constexpr int EPI_SMEM = 4 * 16 * 1024;
     static constexpr bool B_MN = true;
     __device__ static int num_tiles(const BwdParams& p) { return p.ngroups * p.m_tiles * p.n_tiles; }
     __device__ static void prefetch(const BwdParams& p) {
@@ -176,85 +275,157 @@ struct BwdTraits {
         coords(p, tile, grp, m0, u0);
         const BwdGroup& g = p.g[grp];
         const int k0 = kb * kBK;
-        ptx::tma_load_2d(sA, &g.ta, bar, k0, m0);
+        ptx::tma_load_2d_hint(sA, &g.ta, bar, k0, m0, ptx::policy_evict_first());
+        const uint64_t keep = ptx::policy_evict_last();
 #pragma unroll
-        for (int j = 0; j < BN / 64; ++j) ptx::tma_load_2d(sB + j * 64 * kBK * 2, &g.tb, bar, u0 + 64 * j, k0);
+        for (int j = 0; j < BN / 64; ++j)
+            ptx::tma_load_2d_hint(sB + j * 64 * kBK * 2, &g.tb, bar, u0 + 64 * j, k0, keep);
     }
-    __device__ static void epilogue(const BwdParams& p, int tile, uint32_t tbase, int q, int lane, uint64_t* tempty) {
+    // CTA pair (BN = pair tile width): rank r loads A rows [m0 + 128 r, +128) and units
+    // [u0 + r BN/2, +BN/2) of W_hh (MN-major)
+    static constexpr bool A_MN = false;
+    __device__ static void coords2(const BwdParams& p, int tile, int& grp, int& m0, int& u0) {
+        const int per = p.m_tiles * p.n_tiles;
+        grp = tile / per;
+        const int r = tile % per;
+        m0 = (r % p.m_tiles) * 2 * kBM;
+        u0 = (r / p.m_tiles) * BN;
+    }
+    __device__ static void load2(const BwdParams& p, int tile, int kb, uint32_t rank, uint8_t* sA, uint8_t* sB,
+                                 uint32_t bar) {
+        int grp, m0, u0;
+        coords2(p, tile, grp, m0, u0);
+        const BwdGroup& g = p.g[grp];
+        const int k0 = kb * kBK;
+        ptx::tma_load_2d_2sm_hint(sA, &g.ta, bar, k0, m0 + kBM * rank, ptx::policy_evict_first());
+        const uint64_t keep = ptx::policy_evict_last();
+#pragma unroll
+        for (int j = 0; j < BN / 128; ++j)
+            ptx::tma_load_2d_2sm_hint(sB + j * 64 * kBK * 2, &g.tb, bar, u0 + rank * (BN / 2) + 64 * j, k0, keep);
+    }
+    __device__ static void epilogue2(const BwdParams& p, int tile, uint32_t rank, uint32_t tbase, int q, int lane,
+                                     uint32_t tempty_leader, uint8_t* st, uint64_t* ebar, uint32_t& ephase) {
+        int grp, m0, u0;
+        coords2(p, tile, grp, m0, u0);
+        body(p, grp, m0 + kBM * rank, u0, tbase, q, lane, [&] { tc::release_acc_2sm(tempty_leader, lane); }, st,
+             ebar, ephase);
+    }
+    __device__ static void epilogue(const BwdParams& p, int tile, uint32_t tbase, int q, int lane, uint64_t* tempty,
+                                    uint8_t* st, uint64_t* ebar, uint32_t& ephase) {
         int grp, m0, u0;
         coords(p, tile, grp, m0, u0);
+        body(p, grp, m0, u0, tbase, q, lane, [&] { tc::release_acc(tempty, lane); }, st, ebar, ephase);
+    }
+    // epilogue (thread = row), per 16-unit chunk: the 8 input streams (dH, dc_rec, gates i,f,g,o,
+    // c, c_{t-1}) of this warp's 32 rows arrive by TMA into swizzled smem while dh_rec leaves
+    // TMEM; the cell backward runs in registers; dz (4 x bf16) and dc_rec leave by TMA stores.
+    template <class Rel>
+    __device__ static void body(const BwdParams& p, int grp, int m0, int u0, uint32_t tbase, int q, int lane,
+                                Rel release, uint8_t* st, uint64_t* ebar, uint32_t& ephase) {
         const BwdGroup& g = p.g[grp];
-        const int r = m0 + q * 32 + lane;
-        const bool ok = r < p.B;
         const int H = p.H;
+        const int rowbase = m0 + q * 32;
+        uint8_t* bdH = st;
+        uint8_t* bdc = st + 2048;
+        uint8_t* bc = st + 4096;
+        uint8_t* bcp = st + 6144;
+        uint8_t* bg = st + 8192;    // 4 x 1 KB
+        uint8_t* bdz = st + 12288;  // 4 x 1 KB
+        const bool has_prev = g.c_prev != nullptr;
+        const uint32_t in_bytes = (has_prev ? 4 : 3) * 2048 + 4 * 1024;
 #pragma unroll 1
-        for (int uc = 0; uc < BN; uc += 32) {
-            uint32_t acc[32];
-            ptx::tmem_ld_32x32b_x32(tbase + uc, acc);
-            ptx::tmem_ld_wait();
-            if (uc + 32 >= BN) tc::release_acc(tempty, lane);
-            if (!ok) continue;
+        for (int uc = 0; uc < BN; uc += 16) {
             const int j0 = u0 + uc;
-            const float* dHr = g.dH + static_cast<int64_t>(r) * p.lddh + j0;
-            float* dcr = g.dc_rec + static_cast<int64_t>(r) * H + j0;
-            const float* gr = g.gates + static_cast<int64_t>(r) * p.ldg + j0;
-            const float* cr = g.c + static_cast<int64_t>(r) * p.ldc + j0;
-            const float* cpr = g.c_prev ? g.c_prev + static_cast<int64_t>(r) * p.ldc + j0 : nullptr;
-            bf16* dzr = g.dz + static_cast<int64_t>(r) * p.lddz + j0;
+            if (lane == 0) {
+                ptx::mbar_arrive_expect_tx(ebar, in_bytes);
+                const uint64_t stream = ptx::policy_evict_first();
+                ptx::tma_load_2d_hint(bdH, &g.m_dH, ebar, j0, rowbase, stream);
+                ptx::tma_load_2d(bdc, &g.m_dc, ebar, j0, rowbase);
+                ptx::tma_load_2d_hint(bc, &g.m_c, ebar, j0, rowbase, stream);
+                if (has_prev) ptx::tma_load_2d_hint(bcp, &g.m_cp, ebar, j0, rowbase, stream);
 #pragma unroll
-            for (int i0 = 0; i0 < 32; i0 += 4) {
-                const float4 dh4 = *reinterpret_cast<const float4*>(dHr + i0);
-                const float4 dc4 = *reinterpret_cast<const float4*>(dcr + i0);
-                const float4 i4 = *reinterpret_cast<const float4*>(gr + i0);
-                const float4 f4 = *reinterpret_cast<const float4*>(gr + H + i0);
-                const float4 g4 = *reinterpret_cast<const float4*>(gr + 2 * H + i0);
-                const float4 o4 = *reinterpret_cast<const float4*>(gr + 3 * H + i0);
-                const float4 c4 = *reinterpret_cast<const float4*>(cr + i0);
-                const float4 cp4 = cpr ? *reinterpret_cast<const float4*>(cpr + i0) : make_float4(0.f, 0.f, 0.f, 0.f);
-                const float dha[4] = {dh4.x, dh4.y, dh4.z, dh4.w}, dca[4] = {dc4.x, dc4.y, dc4.z, dc4.w};
-                const float ia[4] = {i4.x, i4.y, i4.z, i4.w}, fa[4] = {f4.x, f4.y, f4.z, f4.w};
-                const float ga[4] = {g4.x, g4.y, g4.z, g4.w}, oa[4] = {o4.x, o4.y, o4.z, o4.w};
-                const float ca[4] = {c4.x, c4.y, c4.z, c4.w}, cpa[4] = {cp4.x, cp4.y, cp4.z, cp4.w};
-                float zi[4], zf[4], zg[4], zo[4], dco[4];
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const float dh = dha[e] + __uint_as_float(acc[i0 + e]);
-                    const float tc = tanhf_fast(ca[e]);
-                    const float dc = dca[e] + dh * oa[e] * (1.f - tc * tc);
-                    zi[e] = dc * ga[e] * ia[e] * (1.f - ia[e]);
-                    zf[e] = dc * cpa[e] * fa[e] * (1.f - fa[e]);
-                    zg[e] = dc * ia[e] * (1.f - ga[e] * ga[e]);
-                    zo[e] = dh * tc * oa[e] * (1.f - oa[e]);
-                    dco[e] = dc * fa[e];
-                }
-                *reinterpret_cast<float4*>(dcr + i0) = make_float4(dco[0], dco[1], dco[2], dco[3]);
-                auto st4 = [](bf16* dst, const float* v) {
-                    __nv_bfloat162 a = __floats2bfloat162_rn(v[0], v[1]), b = __floats2bfloat162_rn(v[2], v[3]);
-                    uint2 u;
-                    u.x = *reinterpret_cast<uint32_t*>(&a);
-                    u.y = *reinterpret_cast<uint32_t*>(&b);
-                    *reinterpret_cast<uint2*>(dst) = u;
-                };
-                st4(dzr + i0, zi);
-                st4(dzr + H + i0, zf);
-                st4(dzr + 2 * H + i0, zg);
-                st4(dzr + 3 * H + i0, zo);
+                for (int gi = 0; gi < 4; ++gi)
+                    ptx::tma_load_2d_hint(bg + gi * 1024, &g.m_gates, ebar, gi * H + j0, rowbase, stream);
             }
+            uint32_t acc[16];
+            ptx::tmem_ld_32x32b_x16_(tbase + uc, acc);
+            ptx::tmem_ld_wait();
+            if (uc + 16 >= BN) release();
+            ptx::mbar_wait(ebar, ephase);
+            ephase ^= 1;
+            if (p.epi_skip) continue;
+            uint32_t wdh[16], wdc[16], wc[16], wcp[16], wi[8], wf[8], wg[8], wo[8];
+            tc::ld_row_words<64>(bdH, lane, wdh);
+            tc::ld_row_words<64>(bdc, lane, wdc);
+            tc::ld_row_words<64>(bc, lane, wc);
+            if (has_prev) tc::ld_row_words<64>(bcp, lane, wcp);
+            tc::ld_row_words<32>(bg + 0 * 1024, lane, wi);
+            tc::ld_row_words<32>(bg + 1 * 1024, lane, wf);
+            tc::ld_row_words<32>(bg + 2 * 1024, lane, wg);
+            tc::ld_row_words<32>(bg + 3 * 1024, lane, wo);
+            uint32_t zi[8], zf[8], zg[8], zo[8], dco[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+                const int w = e >> 1;
+                const bool hi = e & 1;
+                const float ig = hi ? tc::bf16_hi(wi[w]) : tc::bf16_lo(wi[w]);
+                const float fg = hi ? tc::bf16_hi(wf[w]) : tc::bf16_lo(wf[w]);
+                const float gg = hi ? tc::bf16_hi(wg[w]) : tc::bf16_lo(wg[w]);
+                const float og = hi ? tc::bf16_hi(wo[w]) : tc::bf16_lo(wo[w]);
+                const float dh = __uint_as_float(wdh[e]) + __uint_as_float(acc[e]);
+                const float tc = tanhf_fast(__uint_as_float(wc[e]));
+                const float cp = has_prev ? __uint_as_float(wcp[e]) : 0.f;
+                const float dc = __uint_as_float(wdc[e]) + dh * og * (1.f - tc * tc);
+                const float vi = dc * gg * ig * (1.f - ig);
+                const float vf = dc * cp * fg * (1.f - fg);
+                const float vg = dc * ig * (1.f - gg * gg);
+                const float vo = dh * tc * og * (1.f - og);
+                dco[e] = __float_as_uint(dc * fg);
+                if (hi) {
+                    zi[w] = tc::pack_bf16x2(__uint_as_float(zi[w]), vi);
+                    zf[w] = tc::pack_bf16x2(__uint_as_float(zf[w]), vf);
+                    zg[w] = tc::pack_bf16x2(__uint_as_float(zg[w]), vg);
+                    zo[w] = tc::pack_bf16x2(__uint_as_float(zo[w]), vo);
+                } else {
+                    zi[w] = __float_as_uint(vi); zf[w] = __float_as_uint(vf);
+                    zg[w] = __float_as_uint(vg); zo[w] = __float_as_uint(vo);
+                }
+            }
+            tc::st_row_words<32>(bdz + 0 * 1024, lane, zi);
+            tc::st_row_words<32>(bdz + 1 * 1024, lane, zf);
+            tc::st_row_words<32>(bdz + 2 * 1024, lane, zg);
+            tc::st_row_words<32>(bdz + 3 * 1024, lane, zo);
+            tc::st_row_words<64>(bdc, lane, dco);  // dc_rec updated in place
+            ptx::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+#pragma unroll
+                for (int gi = 0; gi < 4; ++gi) ptx::tma_store_2d(&g.m_dz, bdz + gi * 1024, gi * H + j0, rowbase);
+                ptx::tma_store_2d(&g.m_dc, bdc, j0, rowbase);
+                ptx::bulk_commit();
+                ptx::bulk_wait_read0();
+            }
+            __syncwarp();
         }
     }
 };
 
-void make_map_box(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, int64_t ld, uint32_t box_outer) {
+void make_map_gen(CUtensorMap* m, const void* base, bool f32, uint64_t inner, uint64_t outer, int64_t ld,
+                  uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle sw) {
+    const int esz = f32 ? 4 : 2;
     AB_CHECK((reinterpret_cast<uintptr_t>(base) & 15) == 0, ADPSGD_E_DIMENSION, "TMA base must be 16B aligned");
-    AB_CHECK(((ld * 2) & 15) == 0, ADPSGD_E_DIMENSION, "TMA row pitch must be a multiple of 16 bytes");
+    AB_CHECK(((ld * esz) & 15) == 0, ADPSGD_E_DIMENSION, "TMA row pitch must be a multiple of 16 bytes");
     cuuint64_t dims[2] = {inner, outer};
-    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
-    cuuint32_t box[2] = {64, box_outer};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * esz};
+    cuuint32_t box[2] = {box_inner, box_outer};
     cuuint32_t es[2] = {1, 1};
-    CUresult r = get_encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
-                                 es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+    CUresult r = get_encode_fn()(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                                 const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     AB_CHECK(r == CUDA_SUCCESS, ADPSGD_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+}
+void make_map_box(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, int64_t ld, uint32_t box_outer) {
+    make_map_gen(m, base, false, inner, outer, ld, 64, box_outer, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
 template <class Traits, class Params>
@@ -262,16 +433,44 @@ void launch_persistent(const Params& p, int tiles, cudaStream_t s) {
     auto k = tc::persistent_kernel<Traits, Params>;
     static bool attr = false;
     if (!attr) {
-        AB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::Shape<Traits::BN>::SMEM));
+        AB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::Shape<Traits::BN, Traits::EPI_SMEM>::SMEM));
         attr = true;
     }
     const int grid = tiles < num_sms() ? tiles : num_sms();
-    k<<<grid, tc::kThreads, tc::Shape<Traits::BN>::SMEM, s>>>(p);
+    k<<<grid, tc::kThreads, tc::Shape<Traits::BN, Traits::EPI_SMEM>::SMEM, s>>>(p);
     count_launch();
     AB_CUDA(cudaGetLastError());
 }
 
+template <class Traits, class Params>
+void launch_pair(const Params& p, int pair_tiles, cudaStream_t s) {
+    auto k = tc::persistent_kernel_2cta<Traits, Params>;
+    static bool attr = false;
+    if (!attr) {
+        AB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::Shape2<Traits::BN, Traits::EPI_SMEM>::SMEM));
+        attr = true;
+    }
+    int pairs = num_sms() / 2;
+    if (pair_tiles < pairs) pairs = pair_tiles;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * pairs);
+    cfg.blockDim = dim3(tc::kThreads);
+    cfg.dynamicSmemBytes = tc::Shape2<Traits::BN, Traits::EPI_SMEM>::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute attrs[1];
+    attrs[0].id = cudaLaunchAttributeClusterDimension;
+    attrs[0].val.clusterDim.x = 2;
+    attrs[0].val.clusterDim.y = 1;
+    attrs[0].val.clusterDim.z = 1;
+    cfg.attrs = attrs;
+    cfg.numAttrs = 1;
+    AB_CUDA(cudaLaunchKernelEx(&cfg, k, p));
+    count_launch();
+}
+
 }  // namespace
+
+bool g_use_pair_mma = true;
 
 void lstm_fwd_step(const LstmFwdDir* dirs, int ndirs, int B, int H, int ldg, int ldc, int ldh, cudaStream_t s) {
     AB_CHECK(H % 64 == 0 && ndirs >= 1 && ndirs <= 2, ADPSGD_E_DIMENSION, "fused LSTM step needs H % 64 == 0");
@@ -294,14 +493,26 @@ void lstm_fwd_step(const LstmFwdDir* dirs, int ndirs, int B, int H, int ldg, int
             K += H;
         }
         g.bias = a.bias; g.c_prev = a.c_prev; g.gates = a.gates; g.c = a.c; g.h = a.h;
+        if (a.c_prev) make_map_gen(&g.m_cprev, a.c_prev, true, H, B, ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+        make_map_gen(&g.m_gates, a.gates, false, 4 * H, B, ldg, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+        make_map_gen(&g.m_c, a.c, true, H, B, ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+        make_map_gen(&g.m_h, a.h, false, H, B, ldh, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
         flops += 2.0 * B * 4.0 * H * K;
-        bytes += 2.0 * (B + 4.0 * H) * K + B * H * (16.0 + 4 + 2 + (a.c_prev ? 4 : 0));
+        bytes += 2.0 * (B + 4.0 * H) * K + B * H * (8.0 + 4 + 2 + (a.c_prev ? 4 : 0));
     }
     p.ngroups = ndirs; p.B = B; p.H = H; p.ldg = ldg; p.ldc = ldc; p.ldh = ldh;
-    p.m_tiles = (B + kBM - 1) / kBM;
+    static const int skip = std::getenv("ADPSGD_EPI_SKIP") ? std::atoi(std::getenv("ADPSGD_EPI_SKIP")) : 0;
+    p.epi_skip = skip;
+    p.trace = trace_take();
     p.n_tiles = H / 64;
     ProfScope ps_(s, PROF_GEMM_REC_FWD, flops, bytes);
-    launch_persistent<FwdTraits>(p, ndirs * p.m_tiles * p.n_tiles, s);
+    if (g_use_pair_mma && B > kBM) {
+        p.m_tiles = (B + 2 * kBM - 1) / (2 * kBM);
+        launch_pair<FwdTraits>(p, ndirs * p.m_tiles * p.n_tiles, s);
+    } else {
+        p.m_tiles = (B + kBM - 1) / kBM;
+        launch_persistent<FwdTraits>(p, ndirs * p.m_tiles * p.n_tiles, s);
+    }
 }
 
 void lstm_bwd_step(const LstmBwdDir* dirs, int ndirs, int B, int H, int lddh, int ldg, int ldc, int lddz,
@@ -310,8 +521,9 @@ void lstm_bwd_step(const LstmBwdDir* dirs, int ndirs, int B, int H, int lddh, in
     BwdParams p;
     std::memset(&p, 0, sizeof(p));
     // 128 x 64 tiles: a 1024 x 1024 dgrad per direction is only 64 tiles at BN = 128
-    const int m_tiles = (B + kBM - 1) / kBM;
-    const int bn = (ndirs * m_tiles * (H / 128) >= num_sms()) ? 128 : 64;
+    const bool pair = g_use_pair_mma && B > kBM && H % 128 == 0;
+    const int m_tiles = pair ? (B + 2 * kBM - 1) / (2 * kBM) : (B + kBM - 1) / kBM;
+    const int bn = pair ? 128 : ((ndirs * m_tiles * (H / 128) >= num_sms()) ? 128 : 64);
     double flops = 0, bytes = 0;
     for (int d = 0; d < ndirs; ++d) {
         const LstmBwdDir& a = dirs[d];
@@ -320,14 +532,24 @@ void lstm_bwd_step(const LstmBwdDir* dirs, int ndirs, int B, int H, int lddh, in
         make_map_box(&g.tb, a.w_hh, H, 4 * H, H, 64);
         g.kb = (4 * H + kBK - 1) / kBK;
         g.dH = a.dH; g.dc_rec = a.dc_rec; g.gates = a.gates; g.c = a.c; g.c_prev = a.c_prev; g.dz = a.dz_dst;
+        make_map_gen(&g.m_dH, a.dH, true, H, B, lddh, 16, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+        make_map_gen(&g.m_dc, a.dc_rec, true, H, B, H, 16, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+        make_map_gen(&g.m_c, a.c, true, H, B, ldc, 16, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+        if (a.c_prev) make_map_gen(&g.m_cp, a.c_prev, true, H, B, ldc, 16, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+        make_map_gen(&g.m_gates, a.gates, false, 4 * H, B, ldg, 16, 32, CU_TENSOR_MAP_SWIZZLE_32B);
+        make_map_gen(&g.m_dz, a.dz_dst, false, 4 * H, B, lddz, 16, 32, CU_TENSOR_MAP_SWIZZLE_32B);
         flops += 2.0 * B * H * 4.0 * H;
-        bytes += 2.0 * (B + H) * 4.0 * H + B * H * (4 + 8 + 16 + 4 + (a.c_prev ? 4 : 0) + 8);
+        bytes += 2.0 * (B + H) * 4.0 * H + B * H * (4 + 8 + 8 + 4 + (a.c_prev ? 4 : 0) + 8);
     }
     p.ngroups = ndirs; p.B = B; p.H = H; p.lddh = lddh; p.ldg = ldg; p.ldc = ldc; p.lddz = lddz;
+    static const int skip = std::getenv("ADPSGD_EPI_SKIP") ? std::atoi(std::getenv("ADPSGD_EPI_SKIP")) : 0;
+    p.epi_skip = skip;
+    p.trace = trace_take();
     p.m_tiles = m_tiles;
     p.n_tiles = H / bn;
     ProfScope ps_(s, PROF_GEMM_REC_BWD, flops, bytes);
-    if (bn == 128) launch_persistent<BwdTraits<128>>(p, ndirs * p.m_tiles * p.n_tiles, s);
+    if (pair) launch_pair<BwdTraits<128>>(p, ndirs * p.m_tiles * p.n_tiles, s);
+    else if (bn == 128) launch_persistent<BwdTraits<128>>(p, ndirs * p.m_tiles * p.n_tiles, s);
     else launch_persistent<BwdTraits<64>>(p, ndirs * p.m_tiles * p.n_tiles, s);
 }
 

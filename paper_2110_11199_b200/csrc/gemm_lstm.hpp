@@ -22,7 +22,7 @@ struct LstmFwdDir {
     const bf16* w_hh;                         // [4H x H]
     const float* bias;                        // [4H] (fp32 master)
     const float* c_prev;                      // [B x H] at ldc (nullptr at the first step)
-    float* gates; float* c; bf16* h;          // outputs (row pitch ldg / ldc / ldh)
+    bf16* gates; float* c; bf16* h;           // outputs (row pitch ldg / ldc / ldh); gates i,f,g,o bf16
 };
 
 struct LstmBwdDir {
@@ -30,7 +30,7 @@ struct LstmBwdDir {
     const bf16* w_hh;                         // [4H x H]
     const float* dH;                          // dHout[t'] (+ d*H), row pitch lddh
     float* dc_rec;                            // [B x H]
-    const float* gates; const float* c; const float* c_prev;  // at t' (c_prev may be nullptr)
+    const bf16* gates; const float* c; const float* c_prev;   // at t' (c_prev may be nullptr)
     bf16* dz_dst;                             // dz_{t'}
 };
 

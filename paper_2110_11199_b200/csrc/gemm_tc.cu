@@ -15,6 +15,7 @@
 
 #include "gemm.hpp"
 #include "gemm_lstm.hpp"
+#include "tc_core.cuh"
 #include "tc_ptx.cuh"
 #include "prof.hpp"
 
@@ -23,7 +24,6 @@ namespace ab {
 namespace {
 
 constexpr int BM = 128, BK = 64;
-constexpr int kThreads = 192;
 
 struct TcParams {
     CUtensorMap ta[2];
@@ -38,202 +38,152 @@ struct TcParams {
     int accumulate;
     const float* bias;
     int vec_ok;
+    unsigned long long* trace;
 };
 
-template <int BN>
-struct Cfg {
-    static constexpr int STAGES = BN == 256 ? 4 : 6;
-    static constexpr int A_BYTES = BM * BK * 2;
-    static constexpr int B_BYTES = BN * BK * 2;
-    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int TMEM_COLS = 2 * BN;  // two accumulator stages
-    static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-};
 
-template <int BN, bool AMN, bool BMN, bool CBF16>
-__global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_constant__ TcParams p) {
-    using CF = Cfg<BN>;
-    constexpr int STAGES = CF::STAGES;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sA = smem;
-    uint8_t* sB = smem + STAGES * CF::A_BYTES;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * CF::STAGE_BYTES);
-    uint64_t* empty = full + STAGES;
-    uint64_t* tfull = empty + STAGES;
-    uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-
-    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int num_tiles = p.m_tiles * p.n_tiles;
-    const int total_kb = p.kblocks[0] + (p.nseg > 1 ? p.kblocks[1] : 0);
-
-    if (warp == 0 && lane == 0) {
-        for (int i = 0; i < STAGES; ++i) { ptx::mbar_init(&full[i], 1); ptx::mbar_init(&empty[i], 1); }
-        for (int i = 0; i < 2; ++i) { ptx::mbar_init(&tfull[i], 1); ptx::mbar_init(&tempty[i], 4); }
-        ptx::fence_barrier_init();
+// Generic GEMM traits for the persistent skeletons in tc_core.cuh (single CTA and CTA pair).
+template <int BN_, bool AMN, bool BMN, bool CBF16>
+struct GenTraits {
+    static constexpr int BN = BN_;
+    static constexpr int EPI_SMEM = 0;
+    static constexpr bool A_MN = AMN;
+    static constexpr bool B_MN = BMN;
+    __device__ static int num_tiles(const TcParams& p) { return p.m_tiles * p.n_tiles; }
+    __device__ static void prefetch(const TcParams& p) {
         for (int s = 0; s < p.nseg; ++s) { ptx::tma_prefetch(&p.ta[s]); ptx::tma_prefetch(&p.tb[s]); }
     }
-    if (warp == 1) ptx::tmem_alloc(tmem_slot, CF::TMEM_COLS);
-    ptx::tc_fence_before();
-    __syncthreads();
-    ptx::tc_fence_after();
-    const uint32_t tmem_base = *tmem_slot;
-
-    if (warp == 0) {
-        if (lane == 0) {
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-                const int m0 = (tile % p.m_tiles) * BM;
-                const int n0 = (tile / p.m_tiles) * BN;
-                for (int kb = 0; kb < total_kb; ++kb) {
-                    const int s = kb < p.kblocks[0] ? 0 : 1;
-                    const int k0 = (s == 0 ? kb : kb - p.kblocks[0]) * BK;
-                    ptx::mbar_wait(&empty[stage], phase ^ 1);
-                    ptx::mbar_arrive_expect_tx(&full[stage], CF::STAGE_BYTES);
-                    uint8_t* a_dst = sA + stage * CF::A_BYTES;
-                    uint8_t* b_dst = sB + stage * CF::B_BYTES;
-                    if (AMN) {
+    __device__ static int kblocks(const TcParams& p, int) { return p.kblocks[0] + (p.nseg > 1 ? p.kblocks[1] : 0); }
+    __device__ static void seg_of(const TcParams& p, int kb, int& s, int& k0) {
+        s = kb < p.kblocks[0] ? 0 : 1;
+        k0 = (s == 0 ? kb : kb - p.kblocks[0]) * BK;
+    }
+    // ---- single CTA: 128 x BN tiles ----
+    __device__ static void load(const TcParams& p, int tile, int kb, uint8_t* sA, uint8_t* sB, uint64_t* bar) {
+        const int m0 = (tile % p.m_tiles) * BM, n0 = (tile / p.m_tiles) * BN;
+        int s, k0;
+        seg_of(p, kb, s, k0);
+        if (AMN) {
 #pragma unroll
-                        for (int j = 0; j < BM / 64; ++j)
-                            ptx::tma_load_2d(a_dst + j * 64 * BK * 2, &p.ta[s], &full[stage], m0 + 64 * j, k0);
-                    } else {
-                        ptx::tma_load_2d(a_dst, &p.ta[s], &full[stage], k0, m0);
-                    }
-                    if (BMN) {
-#pragma unroll
-                        for (int j = 0; j < BN / 64; ++j)
-                            ptx::tma_load_2d(b_dst + j * 64 * BK * 2, &p.tb[s], &full[stage], n0 + 64 * j, k0);
-                    } else {
-                        ptx::tma_load_2d(b_dst, &p.tb[s], &full[stage], k0, n0);
-                    }
-                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
-                }
-            }
+            for (int j = 0; j < BM / 64; ++j) ptx::tma_load_2d(sA + j * 64 * BK * 2, &p.ta[s], bar, m0 + 64 * j, k0);
+        } else {
+            ptx::tma_load_2d(sA, &p.ta[s], bar, k0, m0);
         }
-    } else if (warp == 1) {
-        if (lane == 0) {
-            constexpr uint32_t idesc = ptx::idesc_bf16_f32(BM, BN, AMN, BMN);
-            int stage = 0;
-            uint32_t phase = 0;
-            int acc = 0;
-            uint32_t aphase = 0;
-            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-                ptx::mbar_wait(&tempty[acc], aphase ^ 1);
-                ptx::tc_fence_after();
-                const uint32_t tmem_d = tmem_base + acc * BN;
-                for (int kb = 0; kb < total_kb; ++kb) {
-                    ptx::mbar_wait(&full[stage], phase);
-                    ptx::tc_fence_after();
-                    const uint32_t a_addr = ptx::smem_u32(sA + stage * CF::A_BYTES);
-                    const uint32_t b_addr = ptx::smem_u32(sB + stage * CF::B_BYTES);
+        if (BMN) {
 #pragma unroll
-                    for (int kk = 0; kk < BK / 16; ++kk) {
-                        const uint64_t ad = AMN ? ptx::umma_desc_sw128(a_addr + kk * 2048, 64 * BK * 2, 1024)
-                                                : ptx::umma_desc_sw128(a_addr + kk * 32, 16, 1024);
-                        const uint64_t bd = BMN ? ptx::umma_desc_sw128(b_addr + kk * 2048, 64 * BK * 2, 1024)
-                                                : ptx::umma_desc_sw128(b_addr + kk * 32, 16, 1024);
-                        ptx::mma_bf16(tmem_d, ad, bd, idesc, (kb | kk) != 0);
-                    }
-                    ptx::mma_commit(&empty[stage]);
-                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
-                }
-                ptx::mma_commit(&tfull[acc]);
-                if (++acc == 2) { acc = 0; aphase ^= 1; }
-            }
-        }
-    } else {
-        // epilogue warps 2..5 -> TMEM lane quarter (warp % 4)
-        const int q = warp % 4;
-        const int row_in_tile = q * 32 + lane;
-        int acc = 0;
-        uint32_t aphase = 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-            const int m0 = (tile % p.m_tiles) * BM;
-            const int n0 = (tile / p.m_tiles) * BN;
-            ptx::mbar_wait(&tfull[acc], aphase);
-            ptx::tc_fence_after();
-            const int gm = m0 + row_in_tile;
-            const bool row_ok = gm < p.M;
-#pragma unroll 1
-            for (int c = 0; c < BN; c += 32) {
-                uint32_t r[32];
-                ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c, r);
-                ptx::tmem_ld_wait();
-                if (c + 32 >= BN) {
-                    ptx::tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
-                }
-                if (!row_ok) continue;
-                const int gn0 = n0 + c;
-                if (gn0 >= p.N) continue;
-                float v[32];
-#pragma unroll
-                for (int i = 0; i < 32; ++i) v[i] = p.alpha * __uint_as_float(r[i]);
-                if (p.bias) {
-#pragma unroll
-                    for (int i = 0; i < 32; ++i)
-                        if (gn0 + i < p.N) v[i] += p.bias[gn0 + i];
-                }
-                if constexpr (CBF16) {
-                    bf16* crow = reinterpret_cast<bf16*>(p.C) + static_cast<int64_t>(gm) * p.ldc + gn0;
-                    if (p.vec_ok && gn0 + 32 <= p.N) {
-#pragma unroll
-                        for (int i = 0; i < 32; i += 8) {
-                            uint4 u;
-                            if (p.accumulate) {
-                                const uint4 o = *reinterpret_cast<const uint4*>(crow + i);
-                                const bf16* ob = reinterpret_cast<const bf16*>(&o);
-#pragma unroll
-                                for (int j = 0; j < 8; ++j) v[i + j] += __bfloat162float(ob[j]);
-                            }
-                            bf16* ub = reinterpret_cast<bf16*>(&u);
-#pragma unroll
-                            for (int j = 0; j < 8; ++j) ub[j] = __float2bfloat16_rn(v[i + j]);
-                            *reinterpret_cast<uint4*>(crow + i) = u;
-                        }
-                    } else {
-                        for (int i = 0; i < 32 && gn0 + i < p.N; ++i) {
-                            float x = v[i];
-                            if (p.accumulate) x += __bfloat162float(crow[i]);
-                            crow[i] = __float2bfloat16_rn(x);
-                        }
-                    }
-                } else {
-                    float* crow = reinterpret_cast<float*>(p.C) + static_cast<int64_t>(gm) * p.ldc + gn0;
-                    if (p.vec_ok && gn0 + 32 <= p.N) {
-#pragma unroll
-                        for (int i = 0; i < 32; i += 4) {
-                            float4 u = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-                            if (p.accumulate) {
-                                const float4 o = *reinterpret_cast<const float4*>(crow + i);
-                                u.x += o.x; u.y += o.y; u.z += o.z; u.w += o.w;
-                            }
-                            *reinterpret_cast<float4*>(crow + i) = u;
-                        }
-                    } else {
-                        for (int i = 0; i < 32 && gn0 + i < p.N; ++i) {
-                            float x = v[i];
-                            if (p.accumulate) x += crow[i];
-                            crow[i] = x;
-                        }
-                    }
-                }
-            }
-            if (++acc == 2) { acc = 0; aphase ^= 1; }
+            for (int j = 0; j < BN / 64; ++j) ptx::tma_load_2d(sB + j * 64 * BK * 2, &p.tb[s], bar, n0 + 64 * j, k0);
+        } else {
+            ptx::tma_load_2d(sB, &p.tb[s], bar, k0, n0);
         }
     }
-    ptx::tc_fence_before();
-    __syncthreads();
-    if (warp == 1) ptx::tmem_dealloc(tmem_base, CF::TMEM_COLS);
-}
+    __device__ static void epilogue(const TcParams& p, int tile, uint32_t tbase, int q, int lane, uint64_t* tempty,
+                                    uint8_t*, uint64_t*, uint32_t&) {
+        const int m0 = (tile % p.m_tiles) * BM, n0 = (tile / p.m_tiles) * BN;
+        body(p, m0 + q * 32, n0, tbase, lane, [&] { tc::release_acc(tempty, lane); });
+    }
+    // ---- CTA pair: 256 x BN tiles, rank r holds A rows [m0 + 128 r, +128) and B rows [n0 + r BN/2, +BN/2) ----
+    __device__ static void load2(const TcParams& p, int tile, int kb, uint32_t rank, uint8_t* sA, uint8_t* sB,
+                                 uint32_t bar) {
+        const int m0 = (tile % p.m_tiles) * 2 * BM + BM * rank;
+        const int n0 = (tile / p.m_tiles) * BN + (BN / 2) * rank;
+        int s, k0;
+        seg_of(p, kb, s, k0);
+        if (AMN) {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j) ptx::tma_load_2d_2sm(sA + j * 64 * BK * 2, &p.ta[s], bar, m0 + 64 * j, k0);
+        } else {
+            ptx::tma_load_2d_2sm(sA, &p.ta[s], bar, k0, m0);
+        }
+        if (BMN) {
+#pragma unroll
+            for (int j = 0; j < BN / 128; ++j)
+                ptx::tma_load_2d_2sm(sB + j * 64 * BK * 2, &p.tb[s], bar, n0 + 64 * j, k0);
+        } else {
+            ptx::tma_load_2d_2sm(sB, &p.tb[s], bar, k0, n0);
+        }
+    }
+    __device__ static void epilogue2(const TcParams& p, int tile, uint32_t rank, uint32_t tbase, int q, int lane,
+                                     uint32_t tempty_leader, uint8_t*, uint64_t*, uint32_t&) {
+        const int m0 = (tile % p.m_tiles) * 2 * BM + BM * rank, n0 = (tile / p.m_tiles) * BN;
+        body(p, m0 + q * 32, n0, tbase, lane, [&] { tc::release_acc_2sm(tempty_leader, lane); });
+    }
+    // TMEM accumulator (thread = row, 32-column chunks in registers) -> alpha / bias / accumulate
+    // -> vectorised row-segment stores.
+    template <class Rel>
+    __device__ static void body(const TcParams& p, int rowbase, int n0, uint32_t tbase, int lane, Rel release) {
+        const int gm = rowbase + lane;
+        const bool row_ok = gm < p.M;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+            uint32_t r[32];
+            ptx::tmem_ld_32x32b_x32(tbase + c, r);
+            ptx::tmem_ld_wait();
+            if (c + 32 >= BN) release();
+            if (!row_ok) continue;
+            const int gn0 = n0 + c;
+            if (gn0 >= p.N) continue;
+            float v[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = p.alpha * __uint_as_float(r[i]);
+            if (p.bias) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                    if (gn0 + i < p.N) v[i] += p.bias[gn0 + i];
+            }
+            if constexpr (CBF16) {
+                bf16* crow = reinterpret_cast<bf16*>(p.C) + static_cast<int64_t>(gm) * p.ldc + gn0;
+                if (p.vec_ok && gn0 + 32 <= p.N) {
+#pragma unroll
+                    for (int i = 0; i < 32; i += 8) {
+                        uint4 u;
+                        if (p.accumulate) {
+                            const uint4 o = *reinterpret_cast<const uint4*>(crow + i);
+                            const bf16* ob = reinterpret_cast<const bf16*>(&o);
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) v[i + j] += __bfloat162float(ob[j]);
+                        }
+                        bf16* ub = reinterpret_cast<bf16*>(&u);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) ub[j] = __float2bfloat16_rn(v[i + j]);
+                        *reinterpret_cast<uint4*>(crow + i) = u;
+                    }
+                } else {
+                    for (int i = 0; i < 32 && gn0 + i < p.N; ++i) {
+                        float x = v[i];
+                        if (p.accumulate) x += __bfloat162float(crow[i]);
+                        crow[i] = __float2bfloat16_rn(x);
+                    }
+                }
+            } else {
+                float* crow = reinterpret_cast<float*>(p.C) + static_cast<int64_t>(gm) * p.ldc + gn0;
+                if (p.vec_ok && gn0 + 32 <= p.N) {
+#pragma unroll
+                    for (int i = 0; i < 32; i += 4) {
+                        float4 u = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+                        if (p.accumulate) {
+                            const float4 o = *reinterpret_cast<const float4*>(crow + i);
+                            u.x += o.x; u.y += o.y; u.z += o.z; u.w += o.w;
+                        }
+                        *reinterpret_cast<float4*>(crow + i) = u;
+                    }
+                } else {
+                    for (int i = 0; i < 32 && gn0 + i < p.N; ++i) {
+                        float x = v[i];
+                        if (p.accumulate) x += crow[i];
+                        crow[i] = x;
+                    }
+                }
+            }
+        }
+    }
+};
 
 // ---- host side -------------------------------------------------------------
 
 
 }  // namespace
+
+unsigned long long* trace_take();  // prof.cu
 
 EncodeFnT get_encode_fn() {
     static EncodeFnT fn = nullptr;
@@ -265,33 +215,65 @@ void make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, 
     AB_CHECK(r == CUDA_SUCCESS, ADPSGD_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
 }
 
-template <int BN, bool AMN, bool BMN, bool CBF16>
-void launch_cfg(const TcParams& p, cudaStream_t s) {
-    auto k = gemm_tc_kernel<BN, AMN, BMN, CBF16>;
+template <class Traits>
+void launch_single(const TcParams& p, cudaStream_t s) {
+    auto k = tc::persistent_kernel<Traits, TcParams>;
     static bool attr = false;
     if (!attr) {
-        AB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
+        AB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::Shape<Traits::BN, Traits::EPI_SMEM>::SMEM));
         attr = true;
     }
     const int tiles = p.m_tiles * p.n_tiles;
     const int grid = tiles < num_sms() ? tiles : num_sms();
-    k<<<grid, kThreads, Cfg<BN>::SMEM, s>>>(p);
+    k<<<grid, tc::kThreads, tc::Shape<Traits::BN, Traits::EPI_SMEM>::SMEM, s>>>(p);
     count_launch();
     AB_CUDA(cudaGetLastError());
 }
 
+template <class Traits>
+void launch_pair(const TcParams& p, cudaStream_t s) {
+    auto k = tc::persistent_kernel_2cta<Traits, TcParams>;
+    static bool attr = false;
+    if (!attr) {
+        AB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::Shape2<Traits::BN, Traits::EPI_SMEM>::SMEM));
+        attr = true;
+    }
+    const int tiles = p.m_tiles * p.n_tiles;
+    const int pairs = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * pairs);
+    cfg.blockDim = dim3(tc::kThreads);
+    cfg.dynamicSmemBytes = tc::Shape2<Traits::BN, Traits::EPI_SMEM>::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute attrs[1];
+    attrs[0].id = cudaLaunchAttributeClusterDimension;
+    attrs[0].val.clusterDim.x = 2;
+    attrs[0].val.clusterDim.y = 1;
+    attrs[0].val.clusterDim.z = 1;
+    cfg.attrs = attrs;
+    cfg.numAttrs = 1;
+    AB_CUDA(cudaLaunchKernelEx(&cfg, k, p));
+    count_launch();
+}
+
+template <int BN, bool AMN, bool BMN, bool CBF16>
+void launch_cfg(const TcParams& p, bool pair, cudaStream_t s) {
+    if (pair) launch_pair<GenTraits<BN, AMN, BMN, CBF16>>(p, s);
+    else launch_single<GenTraits<BN, AMN, BMN, CBF16>>(p, s);
+}
+
 template <int BN>
-void dispatch(const TcParams& p, bool amn, bool bmn, bool cbf16, cudaStream_t s) {
+void dispatch(const TcParams& p, bool amn, bool bmn, bool cbf16, bool pair, cudaStream_t s) {
     const int key = (amn ? 4 : 0) | (bmn ? 2 : 0) | (cbf16 ? 1 : 0);
     switch (key) {
-        case 0: launch_cfg<BN, false, false, false>(p, s); break;
-        case 1: launch_cfg<BN, false, false, true>(p, s); break;
-        case 2: launch_cfg<BN, false, true, false>(p, s); break;
-        case 3: launch_cfg<BN, false, true, true>(p, s); break;
-        case 4: launch_cfg<BN, true, false, false>(p, s); break;
-        case 5: launch_cfg<BN, true, false, true>(p, s); break;
-        case 6: launch_cfg<BN, true, true, false>(p, s); break;
-        default: launch_cfg<BN, true, true, true>(p, s); break;
+        case 0: launch_cfg<BN, false, false, false>(p, pair, s); break;
+        case 1: launch_cfg<BN, false, false, true>(p, pair, s); break;
+        case 2: launch_cfg<BN, false, true, false>(p, pair, s); break;
+        case 3: launch_cfg<BN, false, true, true>(p, pair, s); break;
+        case 4: launch_cfg<BN, true, false, false>(p, pair, s); break;
+        case 5: launch_cfg<BN, true, false, true>(p, pair, s); break;
+        case 6: launch_cfg<BN, true, true, false>(p, pair, s); break;
+        default: launch_cfg<BN, true, true, true>(p, pair, s); break;
     }
 }
 
@@ -320,8 +302,12 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
     for (int i = 1; i < g.nseg; ++i)
         AB_CHECK(g.seg[i].a.mn == amn && g.seg[i].b.mn == bmn, ADPSGD_E_DIMENSION,
                  "gemm_tc: segments must share operand majorness");
-    const int m_tiles = (g.M + BM - 1) / BM;
-    const int bn = (g.N > 128 && m_tiles * ((g.N + 255) / 256) >= num_sms() / 2) ? 256 : 128;
+    extern bool g_use_pair_mma;
+    // CTA pairs (256-row tiles) whenever there are at least two row blocks
+    const bool pair = g_use_pair_mma && g.M > BM;
+    const int rows = pair ? 2 * BM : BM;
+    const int m_tiles = (g.M + rows - 1) / rows;
+    const int bn = (g.N > 128 && m_tiles * ((g.N + 255) / 256) >= (pair ? num_sms() / 4 : num_sms() / 2)) ? 256 : 128;
 
     static std::unordered_map<PlanKey, TcParams, PlanHash> cache;
     static std::mutex mu;
@@ -331,7 +317,7 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
         key.a[i] = g.seg[i].a.ptr; key.b[i] = g.seg[i].b.ptr;
         key.lda[i] = g.seg[i].a.ld; key.ldb[i] = g.seg[i].b.ld; key.K[i] = g.seg[i].K;
     }
-    key.M = g.M; key.N = g.N; key.nseg = g.nseg; key.bn = bn; key.amn = amn; key.bmn = bmn;
+    key.M = g.M; key.N = g.N; key.nseg = g.nseg; key.bn = bn * (pair ? 2 : 1); key.amn = amn; key.bmn = bmn;
 
     TcParams p;
     {
@@ -347,7 +333,7 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
                 if (amn) make_map(&p.ta[i], sg.a.ptr, g.M, sg.K, sg.a.ld, BK);
                 else make_map(&p.ta[i], sg.a.ptr, sg.K, g.M, sg.a.ld, BM);
                 if (bmn) make_map(&p.tb[i], sg.b.ptr, g.N, sg.K, sg.b.ld, BK);
-                else make_map(&p.tb[i], sg.b.ptr, sg.K, g.N, sg.b.ld, bn);
+                else make_map(&p.tb[i], sg.b.ptr, sg.K, g.N, sg.b.ld, pair ? bn / 2 : bn);
                 p.kblocks[i] = (sg.K + BK - 1) / BK;
             }
             p.nseg = g.nseg;
@@ -368,9 +354,10 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
     for (int i = 0; i < g.nseg; ++i) ksum += g.seg[i].K;
     ProfScope ps_(s, g.tag, 2.0 * g.M * g.N * ksum,
                   2.0 * (static_cast<double>(g.M) + g.N) * ksum + static_cast<double>(g.M) * g.N * esz * (g.accumulate ? 2 : 1));
+    p.trace = trace_take();
     p.vec_ok = ((reinterpret_cast<uintptr_t>(g.C) & 15) == 0) && ((g.ldc * esz) % 16 == 0);
-    if (bn == 256) dispatch<256>(p, amn, bmn, g.c_bf16, s);
-    else dispatch<128>(p, amn, bmn, g.c_bf16, s);
+    if (bn == 256) dispatch<256>(p, amn, bmn, g.c_bf16, pair, s);
+    else dispatch<128>(p, amn, bmn, g.c_bf16, pair, s);
 }
 
 }  // namespace ab

@@ -42,7 +42,7 @@ __global__ void gather_kernel(const float* __restrict__ feats, const int32_t* __
 // ---- LSTM cell ----
 template <typename AT>
 __global__ void cell_fwd_kernel(const float* __restrict__ z, int ldz, const float* __restrict__ c_prev, int ldc,
-                                float* __restrict__ gates, int ldg, float* __restrict__ c, AT* __restrict__ h, int ldh,
+                                AT* __restrict__ gates, int ldg, float* __restrict__ c, AT* __restrict__ h, int ldh,
                                 int B, int H) {
     const int64_t total = static_cast<int64_t>(B) * H;
     for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
@@ -55,8 +55,8 @@ __global__ void cell_fwd_kernel(const float* __restrict__ z, int ldz, const floa
         const float og = 1.f / (1.f + expf(-zr[3 * H + j]));
         const float cp = c_prev ? c_prev[static_cast<int64_t>(b) * ldc + j] : 0.f;
         const float cn = fg * cp + ig * gg;
-        float* gr = gates + static_cast<int64_t>(b) * ldg;
-        gr[j] = ig; gr[H + j] = fg; gr[2 * H + j] = gg; gr[3 * H + j] = og;
+        AT* gr = gates + static_cast<int64_t>(b) * ldg;
+        gr[j] = from_f<AT>(ig); gr[H + j] = from_f<AT>(fg); gr[2 * H + j] = from_f<AT>(gg); gr[3 * H + j] = from_f<AT>(og);
         c[static_cast<int64_t>(b) * ldc + j] = cn;
         h[static_cast<int64_t>(b) * ldh + j] = from_f<AT>(og * tanhf(cn));
     }
@@ -64,7 +64,7 @@ __global__ void cell_fwd_kernel(const float* __restrict__ z, int ldz, const floa
 
 template <typename AT>
 __global__ void cell_bwd_kernel(const float* __restrict__ dH, int lddh, const float* __restrict__ dh_rec,
-                                float* __restrict__ dc_rec, int first, const float* __restrict__ gates, int ldg,
+                                float* __restrict__ dc_rec, int first, const AT* __restrict__ gates, int ldg,
                                 const float* __restrict__ c, const float* __restrict__ c_prev, int ldc,
                                 AT* __restrict__ dz, int lddz, int B, int H) {
     const int64_t total = static_cast<int64_t>(B) * H;
@@ -74,8 +74,8 @@ __global__ void cell_bwd_kernel(const float* __restrict__ dH, int lddh, const fl
         float dh = dH[static_cast<int64_t>(b) * lddh + j];
         float dcr = 0.f;
         if (!first) { dh += dh_rec[e]; dcr = dc_rec[e]; }
-        const float* gr = gates + static_cast<int64_t>(b) * ldg;
-        const float ig = gr[j], fg = gr[H + j], gg = gr[2 * H + j], og = gr[3 * H + j];
+        const AT* gr = gates + static_cast<int64_t>(b) * ldg;
+        const float ig = to_f<AT>(gr[j]), fg = to_f<AT>(gr[H + j]), gg = to_f<AT>(gr[2 * H + j]), og = to_f<AT>(gr[3 * H + j]);
         const float tc = tanhf(c[static_cast<int64_t>(b) * ldc + j]);
         const float cp = c_prev ? c_prev[static_cast<int64_t>(b) * ldc + j] : 0.f;
         const float dc = dcr + dh * og * (1.f - tc * tc);
@@ -375,19 +375,19 @@ void launch_gather(const float* feats, const int32_t* labels, const int32_t* idx
 }
 
 template <typename AT>
-void launch_cell_fwd(const float* z, int ldz, const float* c_prev, int ldc, float* gates, int ldg, float* c, AT* h,
+void launch_cell_fwd(const float* z, int ldz, const float* c_prev, int ldc, AT* gates, int ldg, float* c, AT* h,
                      int ldh, int B, int H, cudaStream_t s) {
-    ProfScope ps_(s, PROF_CELL, 0, (double)B * H * (16 + 4 + 16 + 4 + sizeof(AT) + (c_prev ? 4 : 0)));
+    ProfScope ps_(s, PROF_CELL, 0, (double)B * H * (16 + 4 + 5 * sizeof(AT) + 4 + (c_prev ? 4 : 0)));
     cell_fwd_kernel<AT><<<grid_for(static_cast<int64_t>(B) * H), 256, 0, s>>>(z, ldz, c_prev, ldc, gates, ldg, c, h,
                                                                                 ldh, B, H);
     count_launch();
 }
 
 template <typename AT>
-void launch_cell_bwd(const float* dH, int lddh, const float* dh_rec, float* dc_rec, bool first, const float* gates,
+void launch_cell_bwd(const float* dH, int lddh, const float* dh_rec, float* dc_rec, bool first, const AT* gates,
                      int ldg, const float* c, const float* c_prev, int ldc, AT* dz, int lddz, int B, int H,
                      cudaStream_t s) {
-    ProfScope ps_(s, PROF_CELL, 0, (double)B * H * (4 + 16 + 4 + 4 + 4 * sizeof(AT) + (first ? 0 : 8) + (c_prev ? 4 : 0)));
+    ProfScope ps_(s, PROF_CELL, 0, (double)B * H * (4 + 4 * sizeof(AT) + 4 + 4 + 4 * sizeof(AT) + (first ? 0 : 8) + (c_prev ? 4 : 0)));
     cell_bwd_kernel<AT><<<grid_for(static_cast<int64_t>(B) * H), 256, 0, s>>>(
         dH, lddh, dh_rec, dc_rec, first ? 1 : 0, gates, ldg, c, c_prev, ldc, dz, lddz, B, H);
     count_launch();
@@ -511,9 +511,9 @@ void launch_delay(uint64_t ns, cudaStream_t s) {
 #define AB_INST(AT)                                                                                                  \
     template void launch_gather<AT>(const float*, const int32_t*, const int32_t*, int, int, int, int, AT*, int32_t*, \
                                     cudaStream_t);                                                                  \
-    template void launch_cell_fwd<AT>(const float*, int, const float*, int, float*, int, float*, AT*, int, int, int, \
+    template void launch_cell_fwd<AT>(const float*, int, const float*, int, AT*, int, float*, AT*, int, int, int, \
                                       cudaStream_t);                                                                \
-    template void launch_cell_bwd<AT>(const float*, int, const float*, float*, bool, const float*, int, const float*, \
+    template void launch_cell_bwd<AT>(const float*, int, const float*, float*, bool, const AT*, int, const float*, \
                                       const float*, int, AT*, int, int, int, cudaStream_t);                         \
     template void launch_softmax_ce<AT>(const float*, const int32_t*, int, int, float, AT*, float*, cudaStream_t);  \
     template void launch_colsum<AT>(const AT*, int64_t, int, int, float*, float*, int64_t, cudaStream_t);

@@ -12,12 +12,12 @@ void launch_gather(const float* feats, const int32_t* labels, const int32_t* idx
 
 // LSTM cell forward for one (layer, direction, time step) over B rows (gate order i,f,g,o).
 template <typename AT>
-void launch_cell_fwd(const float* z, int ldz, const float* c_prev, int ldc, float* gates, int ldg, float* c, AT* h,
+void launch_cell_fwd(const float* z, int ldz, const float* c_prev, int ldc, AT* gates, int ldg, float* c, AT* h,
                      int ldh, int B, int H, cudaStream_t s);
 
 // LSTM cell backward (BPTT step): dz = d(loss)/d(pre-activations) at time t; dc_rec updated in place.
 template <typename AT>
-void launch_cell_bwd(const float* dH, int lddh, const float* dh_rec, float* dc_rec, bool first, const float* gates,
+void launch_cell_bwd(const float* dH, int lddh, const float* dh_rec, float* dc_rec, bool first, const AT* gates,
                      int ldg, const float* c, const float* c_prev, int ldc, AT* dz, int lddz, int B, int H,
                      cudaStream_t s);
 

@@ -5,6 +5,35 @@
 #include "common.cuh"
 
 namespace ab {
+unsigned long long* g_trace_buf = nullptr;  // device buffer while tracing is on (tc_core.cuh)
+int g_trace_skip = 0;                       // pair-kernel launches to skip before the traced one
+
+// The buffer for exactly one launch: the (skip+1)-th pair-kernel launch after enabling.
+unsigned long long* trace_take() {
+    if (!g_trace_buf) return nullptr;
+    if (g_trace_skip-- == 0) return g_trace_buf;
+    return nullptr;
+}
+
+// Debug timeline control (see tc_core.cuh): enable, then read and clear.
+void trace_enable(int on) {
+    if (on) g_trace_skip = on - 1;
+    if (on && !g_trace_buf) {
+        AB_CUDA(cudaMalloc(&g_trace_buf, sizeof(unsigned long long) * 160 * 32));
+        AB_CUDA(cudaMemset(g_trace_buf, 0, sizeof(unsigned long long) * 160 * 32));
+    }
+    if (!on && g_trace_buf) {
+        AB_CUDA(cudaDeviceSynchronize());
+        AB_CUDA(cudaFree(g_trace_buf));
+        g_trace_buf = nullptr;
+    }
+}
+void trace_read(unsigned long long* out, int n) {
+    AB_CUDA(cudaDeviceSynchronize());
+    if (!g_trace_buf) return;
+    AB_CUDA(cudaMemcpy(out, g_trace_buf, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost));
+    AB_CUDA(cudaMemset(g_trace_buf, 0, sizeof(unsigned long long) * 160 * 32));
+}
 
 bool g_prof_enabled = false;
 std::vector<ProfRec>* g_prof_capture = nullptr;

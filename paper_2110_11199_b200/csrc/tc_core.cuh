@@ -12,22 +12,37 @@
 
 namespace ab::tc {
 
+// Debug timeline (adpsgd_debug_trace): per-CTA globaltimer stamps written by the MMA and
+// epilogue warps of persistent_kernel_2cta into p.trace (nullptr = off).
+// Slot layout: [cta][event] u64, event = 4 * tile_iter + kind.
+constexpr int kTraceCtas = 160, kTraceEv = 32;
+__device__ __forceinline__ void trace(unsigned long long* buf, int ev) {
+    if (buf && blockIdx.x < kTraceCtas && ev < kTraceEv) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        buf[blockIdx.x * kTraceEv + ev] = t;
+    }
+}
+
 constexpr int kBM = 128, kBK = 64, kThreads = 192;
 
-template <int BN>
+constexpr int kSmemBudget = 225 * 1024;
+
+template <int BN, int EPI = 0>
 struct Shape {
-    static constexpr int STAGES = BN >= 256 ? 4 : (BN >= 128 ? 6 : 8);
     static constexpr int A_BYTES = kBM * kBK * 2;
     static constexpr int B_BYTES = BN * kBK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int FIT = (kSmemBudget - EPI - 2048) / STAGE_BYTES;
+    static constexpr int STAGES = FIT > 8 ? 8 : FIT;
     static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
-    static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+    static constexpr int SMEM = STAGES * STAGE_BYTES + EPI + 2048;
 };
 
 template <class Traits, class Params>
 __global__ void __launch_bounds__(kThreads, 1) persistent_kernel(const __grid_constant__ Params p) {
     constexpr int BN = Traits::BN;
-    using S = Shape<BN>;
+    using S = Shape<BN, Traits::EPI_SMEM>;
     constexpr int STAGES = S::STAGES;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -38,6 +53,8 @@ __global__ void __launch_bounds__(kThreads, 1) persistent_kernel(const __grid_co
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint8_t* epi_smem = smem + STAGES * S::STAGE_BYTES + 1024;  // 1024-aligned (TMA swizzle atoms)
+    uint64_t* epi_bar = reinterpret_cast<uint64_t*>(smem + STAGES * S::STAGE_BYTES + 128);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int num_tiles = Traits::num_tiles(p);
@@ -45,6 +62,7 @@ __global__ void __launch_bounds__(kThreads, 1) persistent_kernel(const __grid_co
     if (warp == 0 && lane == 0) {
         for (int i = 0; i < STAGES; ++i) { ptx::mbar_init(&full[i], 1); ptx::mbar_init(&empty[i], 1); }
         for (int i = 0; i < 2; ++i) { ptx::mbar_init(&tfull[i], 1); ptx::mbar_init(&tempty[i], 4); }
+        for (int i = 0; i < 4; ++i) ptx::mbar_init(&epi_bar[i], 1);
         ptx::fence_barrier_init();
         Traits::prefetch(p);
     }
@@ -70,7 +88,7 @@ __global__ void __launch_bounds__(kThreads, 1) persistent_kernel(const __grid_co
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            constexpr uint32_t idesc = ptx::idesc_bf16_f32(kBM, BN, false, Traits::B_MN);
+            constexpr uint32_t idesc = ptx::idesc_bf16_f32(kBM, BN, Traits::A_MN, Traits::B_MN);
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
@@ -87,7 +105,8 @@ __global__ void __launch_bounds__(kThreads, 1) persistent_kernel(const __grid_co
                     const uint32_t b_addr = ptx::smem_u32(sB + stage * S::B_BYTES);
 #pragma unroll
                     for (int kk = 0; kk < kBK / 16; ++kk) {
-                        const uint64_t ad = ptx::umma_desc_sw128(a_addr + kk * 32, 16, 1024);
+                        const uint64_t ad = Traits::A_MN ? ptx::umma_desc_sw128(a_addr + kk * 2048, 64 * kBK * 2, 1024)
+                                                         : ptx::umma_desc_sw128(a_addr + kk * 32, 16, 1024);
                         const uint64_t bd = Traits::B_MN ? ptx::umma_desc_sw128(b_addr + kk * 2048, 64 * kBK * 2, 1024)
                                                          : ptx::umma_desc_sw128(b_addr + kk * 32, 16, 1024);
                         ptx::mma_bf16(tmem_d, ad, bd, idesc, (kb | kk) != 0);
@@ -102,19 +121,241 @@ __global__ void __launch_bounds__(kThreads, 1) persistent_kernel(const __grid_co
     } else {
         const int q = warp % 4;
         int acc = 0;
-        uint32_t aphase = 0;
+        uint32_t aphase = 0, ephase = 0;
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
             ptx::mbar_wait(&tfull[acc], aphase);
             ptx::tc_fence_after();
             const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
-            Traits::epilogue(p, tile, tbase, q, lane, &tempty[acc]);
+            Traits::epilogue(p, tile, tbase, q, lane, &tempty[acc], epi_smem + q * (Traits::EPI_SMEM / 4), &epi_bar[q],
+                             ephase);
             if (++acc == 2) { acc = 0; aphase ^= 1; }
         }
+        if (lane == 0) ptx::bulk_wait0();
     }
     ptx::tc_fence_before();
     __syncthreads();
     if (warp == 1) ptx::tmem_dealloc(tmem_base, S::TMEM_COLS);
 }
+
+// ---------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2): a cluster of 2 CTAs computes a 256 x BN tile; CTA rank r
+// loads A rows [m0 + 128 r, +128) and B rows [n0 + r BN/2, +BN/2) into its own smem, both
+// TMAs complete on the leader's barrier, the leader alone issues
+// tcgen05.mma.cta_group::2 (M = 256), and each CTA's TMEM holds its 128 rows x BN fp32.
+// Per-SM operand bytes per FLOP drop by a third vs 128 x BN single-CTA tiles.
+// Traits: BN, B_MN, num_tiles (pair tiles), kblocks, prefetch,
+//         load2(p, tile, kb, rank, sA, sB, bar_cluster_addr), epilogue2(p, tile, rank, tbase, q, lane, tempty_leader)
+// ---------------------------------------------------------------------------
+template <int BN, int EPI = 0>
+struct Shape2 {
+    static constexpr int BNH = BN / 2;  // B rows held per CTA
+    static constexpr int A_BYTES = kBM * kBK * 2;
+    static constexpr int B_BYTES = BNH * kBK * 2;
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int FIT = (kSmemBudget - EPI - 2048) / STAGE_BYTES;
+    static constexpr int STAGES = FIT > 8 ? 8 : FIT;
+    static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+    static constexpr int SMEM = STAGES * STAGE_BYTES + EPI + 2048;
+};
+
+template <class Traits, class Params>
+__global__ void __launch_bounds__(kThreads, 1) persistent_kernel_2cta(const __grid_constant__ Params p) {
+    constexpr int BN = Traits::BN;
+    using S = Shape2<BN, Traits::EPI_SMEM>;
+    constexpr int STAGES = S::STAGES;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + STAGES * S::A_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::STAGE_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint8_t* epi_smem = smem + STAGES * S::STAGE_BYTES + 1024;  // 1024-aligned (TMA swizzle atoms)
+    uint64_t* epi_bar = reinterpret_cast<uint64_t*>(smem + STAGES * S::STAGE_BYTES + 128);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t rank = ptx::cluster_ctarank();
+    const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+    const int num_tiles = Traits::num_tiles(p);
+    if (threadIdx.x == 0) trace(p.trace, kTraceEv - 2);
+
+    if (warp == 0 && lane == 0) {
+        for (int i = 0; i < STAGES; ++i) { ptx::mbar_init(&full[i], 1); ptx::mbar_init(&empty[i], 1); }
+        for (int i = 0; i < 2; ++i) { ptx::mbar_init(&tfull[i], 1); ptx::mbar_init(&tempty[i], 8); }
+        for (int i = 0; i < 4; ++i) ptx::mbar_init(&epi_bar[i], 1);
+        ptx::fence_barrier_init();
+        Traits::prefetch(p);
+    }
+    if (warp == 1) ptx::tmem_alloc_2sm(tmem_slot, S::TMEM_COLS);
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = cid; tile < num_tiles; tile += ncl) {
+                const int nkb = Traits::kblocks(p, tile);
+                for (int kb = 0; kb < nkb; ++kb) {
+                    ptx::mbar_wait(&empty[stage], phase ^ 1);
+                    const uint32_t bar0 = ptx::mapa(ptx::smem_u32(&full[stage]), 0);
+                    if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * S::STAGE_BYTES);
+                    Traits::load2(p, tile, kb, rank, sA + stage * S::A_BYTES, sB + stage * S::B_BYTES, bar0);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && rank == 0) {
+            constexpr uint32_t idesc = ptx::idesc_bf16_f32(2 * kBM, BN, Traits::A_MN, Traits::B_MN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t aphase = 0;
+            int it = 0;
+            for (int tile = cid; tile < num_tiles; tile += ncl, ++it) {
+                const int nkb = Traits::kblocks(p, tile);
+                ptx::mbar_wait(&tempty[acc], aphase ^ 1);
+                ptx::tc_fence_after();
+                trace(p.trace, 4 * it + 0);
+                const uint32_t tmem_d = tmem_base + acc * BN;
+                for (int kb = 0; kb < nkb; ++kb) {
+                    ptx::mbar_wait(&full[stage], phase);
+                    if (kb == 0) trace(p.trace, 4 * it + 1);
+                    ptx::tc_fence_after();
+                    const uint32_t a_addr = ptx::smem_u32(sA + stage * S::A_BYTES);
+                    const uint32_t b_addr = ptx::smem_u32(sB + stage * S::B_BYTES);
+#pragma unroll
+                    for (int kk = 0; kk < kBK / 16; ++kk) {
+                        const uint64_t ad = Traits::A_MN ? ptx::umma_desc_sw128(a_addr + kk * 2048, 64 * kBK * 2, 1024)
+                                                         : ptx::umma_desc_sw128(a_addr + kk * 32, 16, 1024);
+                        const uint64_t bd = Traits::B_MN ? ptx::umma_desc_sw128(b_addr + kk * 2048, 64 * kBK * 2, 1024)
+                                                         : ptx::umma_desc_sw128(b_addr + kk * 32, 16, 1024);
+                        ptx::mma_bf16_2sm(tmem_d, ad, bd, idesc, (kb | kk) != 0);
+                    }
+                    ptx::mma_commit_2sm(&empty[stage]);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+                ptx::mma_commit_2sm(&tfull[acc]);
+                trace(p.trace, 4 * it + 2);
+                if (++acc == 2) { acc = 0; aphase ^= 1; }
+            }
+        }
+    } else {
+        const int q = warp % 4;
+        const uint32_t tempty0 = ptx::mapa(ptx::smem_u32(&tempty[0]), 0);
+        int acc = 0;
+        uint32_t aphase = 0, ephase = 0;
+        int it = 0;
+        for (int tile = cid; tile < num_tiles; tile += ncl, ++it) {
+            ptx::mbar_wait(&tfull[acc], aphase);
+            ptx::tc_fence_after();
+            const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
+            Traits::epilogue2(p, tile, rank, tbase, q, lane, tempty0 + acc * 8, epi_smem + q * (Traits::EPI_SMEM / 4),
+                              &epi_bar[q], ephase);
+            if (q == 2 && lane == 0) trace(p.trace, 4 * it + 3);
+            if (++acc == 2) { acc = 0; aphase ^= 1; }
+        }
+        if (lane == 0) ptx::bulk_wait0();
+    }
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    if (threadIdx.x == 0) trace(p.trace, kTraceEv - 1);
+    if (warp == 1) ptx::tmem_dealloc_2sm(tmem_base, S::TMEM_COLS);
+}
+
+// CTA-pair epilogue helper: release the accumulator stage on the leader's tempty barrier.
+__device__ __forceinline__ void release_acc_2sm(uint32_t tempty_leader, int lane) {
+    ptx::tc_fence_before();
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader);
+}
+
+// Per-warp staging of a 32-row x NC-column fp32 accumulator chunk: thread `lane` holds row
+// `lane` (tcgen05.ld 32x32b layout); after stage_rows + __syncwarp, element (row, col) sits at
+// st[row * (NC + 1) + col] (padded: conflict-free both ways), so the warp can sweep rows with
+// lanes along columns (coalesced global access).
+template <int NC>
+__device__ __forceinline__ void stage_rows(float* st, int lane, const uint32_t* v) {
+    // (row-major padded staging; used by epilogues that sweep rows)
+#pragma unroll
+    for (int i = 0; i < NC; ++i) st[lane * (NC + 1) + i] = __uint_as_float(v[i]);
+}
+
+// Swizzled smem tiles for TMA boxes (row = this thread's lane).
+// fp32 row of 32 values (128 B) in a SWIZZLE_128B box: 16-B chunk c at c ^ (row & 7).
+__device__ __forceinline__ void st_row_f32_sw128(uint8_t* box, int row, const float* v) {
+    const uint32_t base = ptx::smem_u32(box) + row * 128;
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+        ptx::st_shared_v4(base + ((c ^ (row & 7)) << 4), __float_as_uint(v[4 * c]), __float_as_uint(v[4 * c + 1]),
+                          __float_as_uint(v[4 * c + 2]), __float_as_uint(v[4 * c + 3]));
+}
+__device__ __forceinline__ void ld_row_f32_sw128(const uint8_t* box, int row, float* v) {
+    const uint32_t base = ptx::smem_u32(box) + row * 128;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        const float4 f = ptx::ld_shared_v4f(base + ((c ^ (row & 7)) << 4));
+        v[4 * c] = f.x; v[4 * c + 1] = f.y; v[4 * c + 2] = f.z; v[4 * c + 3] = f.w;
+    }
+}
+// bf16 row of 32 values (64 B) in a SWIZZLE_64B box: 16-B chunk c at c ^ ((row >> 1) & 3).
+__device__ __forceinline__ void st_row_bf16_sw64(uint8_t* box, int row, const float* v) {
+    const uint32_t base = ptx::smem_u32(box) + row * 64;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        uint32_t w[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            __nv_bfloat162 b2 = __floats2bfloat162_rn(v[8 * c + 2 * k], v[8 * c + 2 * k + 1]);
+            w[k] = *reinterpret_cast<uint32_t*>(&b2);
+        }
+        ptx::st_shared_v4(base + ((c ^ ((row >> 1) & 3)) << 4), w[0], w[1], w[2], w[3]);
+    }
+}
+
+// first-write-wins stamp (sub-phases of the first tile's epilogue)
+__device__ __forceinline__ void trace_once(unsigned long long* buf, int ev) {
+    if (buf && blockIdx.x < kTraceCtas && ev < kTraceEv && buf[blockIdx.x * kTraceEv + ev] == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        buf[blockIdx.x * kTraceEv + ev] = t;
+    }
+}
+
+// Generic swizzled-row access for TMA boxes whose rows are ROWB bytes (32, 64 or 128):
+// 16-B chunk c of row r sits at chunk position c ^ swz(r) (SWIZZLE_32B / 64B / 128B).
+template <int ROWB>
+__device__ __forceinline__ int swz(int r) {
+    return ROWB == 128 ? (r & 7) : (ROWB == 64 ? ((r >> 1) & 3) : ((r >> 2) & 1));
+}
+template <int ROWB>
+__device__ __forceinline__ void st_row_words(uint8_t* box, int row, const uint32_t* w) {
+    const uint32_t base = ptx::smem_u32(box) + row * ROWB;
+#pragma unroll
+    for (int c = 0; c < ROWB / 16; ++c)
+        ptx::st_shared_v4(base + ((c ^ swz<ROWB>(row)) << 4), w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
+}
+template <int ROWB>
+__device__ __forceinline__ void ld_row_words(const uint8_t* box, int row, uint32_t* w) {
+    const uint32_t base = ptx::smem_u32(box) + row * ROWB;
+#pragma unroll
+    for (int c = 0; c < ROWB / 16; ++c) {
+        const float4 f = ptx::ld_shared_v4f(base + ((c ^ swz<ROWB>(row)) << 4));
+        w[4 * c] = __float_as_uint(f.x); w[4 * c + 1] = __float_as_uint(f.y);
+        w[4 * c + 2] = __float_as_uint(f.z); w[4 * c + 3] = __float_as_uint(f.w);
+    }
+}
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&v);
+}
+__device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
 
 // Epilogue helper: after the last tcgen05.ld of an accumulator stage, hand it back to the MMA warp.
 __device__ __forceinline__ void release_acc(uint64_t* tempty, int lane) {
