@@ -23,6 +23,7 @@
 #include "comm.hpp"
 #include "engine.hpp"
 #include "gemm.hpp"
+#include "gemm_ce.hpp"
 #include "gemm_lstm.hpp"
 #include "kernels.cuh"
 #include "prof.hpp"
@@ -128,7 +129,13 @@ Ctx::Ctx(const adpsgd_config& c) : cfg(c) {
         Y = alloc(TB * lay.P * es);
         dY = alloc(TB * lay.P * es);
     }
-    logits = static_cast<float*>(alloc(TB * lay.C * sizeof(float)));
+    if (bf16_mode) {
+        ce_part = static_cast<float2*>(alloc(ce_part_elems(static_cast<int>(TB), lay.C) * sizeof(float2)));
+        ce_zlab = static_cast<float*>(alloc(TB * sizeof(float)));
+        ce_lse = static_cast<float*>(alloc(TB * sizeof(float)));
+    } else {
+        logits = static_cast<float*>(alloc(TB * lay.C * sizeof(float)));
+    }
     dlogits = alloc(TB * lay.C * es);
     row_loss = static_cast<float*>(alloc(TB * sizeof(float)));
     int max_in = std::max(lay.top, Ipad);
@@ -304,7 +311,21 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
         gemm(bf, g, s);
         yin = Y;
     }
-    {
+    const float scale = 1.0f / static_cast<float>(TB);
+    if (bf) {
+        // output GEMM fused with softmax-CE: no logits in HBM (gemm_ce.cu)
+        CeArgs a;
+        a.Y = static_cast<const bf16*>(yin);
+        a.W = static_cast<const bf16*>(W.at(lay.w_out));
+        a.bias = master + lay.b_out;
+        a.labels = lab_step;
+        a.M = static_cast<int>(TB); a.N = lay.C; a.K = oi;
+        a.scale = scale;
+        a.part = ce_part; a.zlab = ce_zlab; a.lse = ce_lse;
+        a.row_loss = row_loss;
+        a.dlogits = static_cast<bf16*>(dlogits);
+        ce_forward_backward(a, s);
+    } else {
         GemmArgs g;
         g.M = static_cast<int>(TB); g.N = lay.C;
         g.seg[0].a = {yin, oi, false};
@@ -314,10 +335,9 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
         g.bias = master + lay.b_out;
         g.tag = PROF_GEMM_OUT;
         gemm(bf, g, s);
+        launch_softmax_ce<float>(logits, lab_step, static_cast<int>(TB), lay.C, scale, static_cast<float*>(dlogits),
+                                 row_loss, s);
     }
-    const float scale = 1.0f / static_cast<float>(TB);
-    if (bf) launch_softmax_ce<bf16>(logits, lab_step, static_cast<int>(TB), lay.C, scale, static_cast<bf16*>(dlogits), row_loss, s);
-    else launch_softmax_ce<float>(logits, lab_step, static_cast<int>(TB), lay.C, scale, static_cast<float*>(dlogits), row_loss, s);
     launch_sum(row_loss, static_cast<int>(TB), scale, loss_slot, s);
 
     // ---------------- backward: output / projection ----------------

@@ -64,7 +64,10 @@ struct Ctx {
     std::vector<float*> cst;
     void* Y = nullptr;
     void* dY = nullptr;
-    float* logits = nullptr;
+    float* logits = nullptr;       // fp32 mode only
+    float2* ce_part = nullptr;      // bf16 mode: fused CE scratch
+    float* ce_zlab = nullptr;
+    float* ce_lse = nullptr;
     void* dlogits = nullptr;
     float* row_loss = nullptr;
     float *dHa = nullptr, *dHb = nullptr;

@@ -23,10 +23,30 @@ namespace ab {
 EncodeFnT get_encode_fn();  // gemm_tc.cu
 unsigned long long* trace_take();  // prof.cu
 
+void make_map_gen(CUtensorMap* m, const void* base, bool f32, uint64_t inner, uint64_t outer, int64_t ld,
+                  uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle sw) {
+    const int esz = f32 ? 4 : 2;
+    AB_CHECK((reinterpret_cast<uintptr_t>(base) & 15) == 0, ADPSGD_E_DIMENSION, "TMA base must be 16B aligned");
+    AB_CHECK(((ld * esz) & 15) == 0, ADPSGD_E_DIMENSION, "TMA row pitch must be a multiple of 16 bytes");
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * esz};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = get_encode_fn()(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                                 const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    AB_CHECK(r == CUDA_SUCCESS, ADPSGD_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+}
+
 namespace {
 
 using tc::kBK;
 using tc::kBM;
+
+void make_map_box(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, int64_t ld, uint32_t box_outer) {
+    make_map_gen(m, base, false, inner, outer, ld, 64, box_outer, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
 
 // One MUFU.TANH each (max rel. err ~2^-11, below the bf16 rounding of the stored activations);
 // an IEEE-division sigmoid/tanh compiles to branchy slow paths that serialise the unrolled
@@ -61,7 +81,8 @@ struct FwdTraits {
     static constexpr int BN = 256;
     // per warp (20 KB): c_{t-1} box (fp32 32x32, SW128) | c box | 4 gate boxes (bf16 32x32, SW64) | h box
     static constexpr int EPI_WARP = 20 * 1024;
-    static constexpr int EPI_SMEM = 4 * EPI_WARP;
+    static constexpr int EPI_WARPS = 4;
+    static constexpr int EPI_SMEM = EPI_WARPS * EPI_WARP;
     static constexpr bool B_MN = false;
     __device__ static int num_tiles(const FwdParams& p) { return p.ngroups * p.m_tiles * p.n_tiles; }
     __device__ static void prefetch(const FwdParams& p) {
@@ -114,17 +135,18 @@ struct FwdTraits {
             ptx::tma_load_2d_2sm_hint(sB + j * 64 * kBK * 2, &g.tb[s], bar, k0, (2 * rank + j) * p.H + u0, keep);
     }
     __device__ static void epilogue2(const FwdParams& p, int tile, uint32_t rank, uint32_t tbase, int q, int lane,
-                                     uint32_t tempty_leader, uint8_t* st, uint64_t* ebar, uint32_t& ephase) {
+                                     uint32_t tempty_leader, uint8_t* st, uint64_t* ebar, uint32_t& ephase,
+                                     tc::EpiSlot sl) {
         int grp, m0, u0;
         coords2(p, tile, grp, m0, u0);
         body(p, grp, m0 + kBM * rank, u0, tbase, q, lane, [&] { tc::release_acc_2sm(tempty_leader, lane); }, st, ebar,
-             ephase);
+             ephase, sl);
     }
     __device__ static void epilogue(const FwdParams& p, int tile, uint32_t tbase, int q, int lane, uint64_t* tempty,
-                                    uint8_t* st, uint64_t* ebar, uint32_t& ephase) {
+                                    uint8_t* st, uint64_t* ebar, uint32_t& ephase, tc::EpiSlot sl) {
         int grp, m0, u0;
         coords(p, tile, grp, m0, u0);
-        body(p, grp, m0, u0, tbase, q, lane, [&] { tc::release_acc(tempty, lane); }, st, ebar, ephase);
+        body(p, grp, m0, u0, tbase, q, lane, [&] { tc::release_acc(tempty, lane); }, st, ebar, ephase, sl);
     }
     // epilogue (thread = row): per 32-unit chunk, c_{t-1} arrives by TMA into swizzled smem while
     // the 4 gate columns leave TMEM; the cell runs in registers; gates (bf16), c (fp32) and h
@@ -132,7 +154,7 @@ struct FwdTraits {
     // asynchronous, rows >= B clipped by the tensor map).
     template <class Rel>
     __device__ static void body(const FwdParams& p, int grp, int m0, int u0, uint32_t tbase, int q, int lane,
-                                Rel release, uint8_t* st, uint64_t* ebar, uint32_t& ephase) {
+                                Rel release, uint8_t* st, uint64_t* ebar, uint32_t& ephase, tc::EpiSlot sl) {
         const FwdGroup& g = p.g[grp];
         const int H = p.H;
         const int rowbase = m0 + q * 32;
@@ -142,7 +164,7 @@ struct FwdTraits {
         uint8_t* hbox = st + 16384;
         const bool has_prev = g.c_prev != nullptr;
 #pragma unroll 1
-        for (int uc = 0; uc < 64; uc += 32) {
+        for (int uc = 32 * sl.sub; uc < 64; uc += 32 * sl.n) {
             const int j0 = u0 + uc;
             if (has_prev && lane == 0) {
                 ptx::mbar_arrive_expect_tx(ebar, 32 * 32 * 4);
@@ -156,7 +178,7 @@ struct FwdTraits {
             ptx::tmem_ld_wait();
             const bool tr = q == 2 && lane == 0;
             if (tr) tc::trace_once(p.trace, 12 + (uc / 32) * 4 + 0);
-            if (uc == 32) release();
+            if (uc + 32 * sl.n >= 64) release();
             float cp[32];
             if (has_prev) {
                 ptx::mbar_wait(ebar, ephase);
@@ -256,7 +278,8 @@ struct BwdTraits {
     static constexpr int BN = BN_;
     // per warp (16 KB): dH | dc | c | c_prev (fp32 16x32, SW64, 2 KB each) | gates 4 x (bf16 16x32, SW32, 1 KB)
     //                   | dz 4 x (bf16 16x32, SW32, 1 KB)
-    static constexpr int EPI_SMEM = 4 * 16 * 1024;
+    static constexpr int EPI_WARPS = 4;
+    static constexpr int EPI_SMEM = EPI_WARPS * 16 * 1024;
     static constexpr bool B_MN = true;
     __device__ static int num_tiles(const BwdParams& p) { return p.ngroups * p.m_tiles * p.n_tiles; }
     __device__ static void prefetch(const BwdParams& p) {
@@ -304,24 +327,25 @@ struct BwdTraits {
             ptx::tma_load_2d_2sm_hint(sB + j * 64 * kBK * 2, &g.tb, bar, u0 + rank * (BN / 2) + 64 * j, k0, keep);
     }
     __device__ static void epilogue2(const BwdParams& p, int tile, uint32_t rank, uint32_t tbase, int q, int lane,
-                                     uint32_t tempty_leader, uint8_t* st, uint64_t* ebar, uint32_t& ephase) {
+                                     uint32_t tempty_leader, uint8_t* st, uint64_t* ebar, uint32_t& ephase,
+                                     tc::EpiSlot sl) {
         int grp, m0, u0;
         coords2(p, tile, grp, m0, u0);
         body(p, grp, m0 + kBM * rank, u0, tbase, q, lane, [&] { tc::release_acc_2sm(tempty_leader, lane); }, st,
-             ebar, ephase);
+             ebar, ephase, sl);
     }
     __device__ static void epilogue(const BwdParams& p, int tile, uint32_t tbase, int q, int lane, uint64_t* tempty,
-                                    uint8_t* st, uint64_t* ebar, uint32_t& ephase) {
+                                    uint8_t* st, uint64_t* ebar, uint32_t& ephase, tc::EpiSlot sl) {
         int grp, m0, u0;
         coords(p, tile, grp, m0, u0);
-        body(p, grp, m0, u0, tbase, q, lane, [&] { tc::release_acc(tempty, lane); }, st, ebar, ephase);
+        body(p, grp, m0, u0, tbase, q, lane, [&] { tc::release_acc(tempty, lane); }, st, ebar, ephase, sl);
     }
     // epilogue (thread = row), per 16-unit chunk: the 8 input streams (dH, dc_rec, gates i,f,g,o,
     // c, c_{t-1}) of this warp's 32 rows arrive by TMA into swizzled smem while dh_rec leaves
     // TMEM; the cell backward runs in registers; dz (4 x bf16) and dc_rec leave by TMA stores.
     template <class Rel>
     __device__ static void body(const BwdParams& p, int grp, int m0, int u0, uint32_t tbase, int q, int lane,
-                                Rel release, uint8_t* st, uint64_t* ebar, uint32_t& ephase) {
+                                Rel release, uint8_t* st, uint64_t* ebar, uint32_t& ephase, tc::EpiSlot sl) {
         const BwdGroup& g = p.g[grp];
         const int H = p.H;
         const int rowbase = m0 + q * 32;
@@ -334,7 +358,7 @@ struct BwdTraits {
         const bool has_prev = g.c_prev != nullptr;
         const uint32_t in_bytes = (has_prev ? 4 : 3) * 2048 + 4 * 1024;
 #pragma unroll 1
-        for (int uc = 0; uc < BN; uc += 16) {
+        for (int uc = 16 * sl.sub; uc < BN; uc += 16 * sl.n) {
             const int j0 = u0 + uc;
             if (lane == 0) {
                 ptx::mbar_arrive_expect_tx(ebar, in_bytes);
@@ -350,7 +374,7 @@ struct BwdTraits {
             uint32_t acc[16];
             ptx::tmem_ld_32x32b_x16_(tbase + uc, acc);
             ptx::tmem_ld_wait();
-            if (uc + 16 >= BN) release();
+            if (uc + 16 * sl.n >= BN) release();
             ptx::mbar_wait(ebar, ephase);
             ephase ^= 1;
             if (p.epi_skip) continue;
@@ -410,23 +434,6 @@ struct BwdTraits {
     }
 };
 
-void make_map_gen(CUtensorMap* m, const void* base, bool f32, uint64_t inner, uint64_t outer, int64_t ld,
-                  uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle sw) {
-    const int esz = f32 ? 4 : 2;
-    AB_CHECK((reinterpret_cast<uintptr_t>(base) & 15) == 0, ADPSGD_E_DIMENSION, "TMA base must be 16B aligned");
-    AB_CHECK(((ld * esz) & 15) == 0, ADPSGD_E_DIMENSION, "TMA row pitch must be a multiple of 16 bytes");
-    cuuint64_t dims[2] = {inner, outer};
-    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * esz};
-    cuuint32_t box[2] = {box_inner, box_outer};
-    cuuint32_t es[2] = {1, 1};
-    CUresult r = get_encode_fn()(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
-                                 const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
-                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    AB_CHECK(r == CUDA_SUCCESS, ADPSGD_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
-}
-void make_map_box(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, int64_t ld, uint32_t box_outer) {
-    make_map_gen(m, base, false, inner, outer, ld, 64, box_outer, CU_TENSOR_MAP_SWIZZLE_128B);
-}
 
 template <class Traits, class Params>
 void launch_persistent(const Params& p, int tiles, cudaStream_t s) {
@@ -437,7 +444,7 @@ void launch_persistent(const Params& p, int tiles, cudaStream_t s) {
         attr = true;
     }
     const int grid = tiles < num_sms() ? tiles : num_sms();
-    k<<<grid, tc::kThreads, tc::Shape<Traits::BN, Traits::EPI_SMEM>::SMEM, s>>>(p);
+    k<<<grid, tc::threads_of<Traits>(), tc::Shape<Traits::BN, Traits::EPI_SMEM>::SMEM, s>>>(p);
     count_launch();
     AB_CUDA(cudaGetLastError());
 }
@@ -454,7 +461,7 @@ void launch_pair(const Params& p, int pair_tiles, cudaStream_t s) {
     if (pair_tiles < pairs) pairs = pair_tiles;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * pairs);
-    cfg.blockDim = dim3(tc::kThreads);
+    cfg.blockDim = dim3(tc::threads_of<Traits>());
     cfg.dynamicSmemBytes = tc::Shape2<Traits::BN, Traits::EPI_SMEM>::SMEM;
     cfg.stream = s;
     cudaLaunchAttribute attrs[1];

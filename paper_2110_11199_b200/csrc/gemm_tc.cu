@@ -47,6 +47,7 @@ template <int BN_, bool AMN, bool BMN, bool CBF16>
 struct GenTraits {
     static constexpr int BN = BN_;
     static constexpr int EPI_SMEM = 0;
+    static constexpr int EPI_WARPS = 8;
     static constexpr bool A_MN = AMN;
     static constexpr bool B_MN = BMN;
     __device__ static int num_tiles(const TcParams& p) { return p.m_tiles * p.n_tiles; }
@@ -77,9 +78,9 @@ struct GenTraits {
         }
     }
     __device__ static void epilogue(const TcParams& p, int tile, uint32_t tbase, int q, int lane, uint64_t* tempty,
-                                    uint8_t*, uint64_t*, uint32_t&) {
+                                    uint8_t*, uint64_t*, uint32_t&, tc::EpiSlot sl) {
         const int m0 = (tile % p.m_tiles) * BM, n0 = (tile / p.m_tiles) * BN;
-        body(p, m0 + q * 32, n0, tbase, lane, [&] { tc::release_acc(tempty, lane); });
+        body(p, m0 + q * 32, n0, tbase, lane, [&] { tc::release_acc(tempty, lane); }, sl);
     }
     // ---- CTA pair: 256 x BN tiles, rank r holds A rows [m0 + 128 r, +128) and B rows [n0 + r BN/2, +BN/2) ----
     __device__ static void load2(const TcParams& p, int tile, int kb, uint32_t rank, uint8_t* sA, uint8_t* sB,
@@ -103,22 +104,23 @@ struct GenTraits {
         }
     }
     __device__ static void epilogue2(const TcParams& p, int tile, uint32_t rank, uint32_t tbase, int q, int lane,
-                                     uint32_t tempty_leader, uint8_t*, uint64_t*, uint32_t&) {
+                                     uint32_t tempty_leader, uint8_t*, uint64_t*, uint32_t&, tc::EpiSlot sl) {
         const int m0 = (tile % p.m_tiles) * 2 * BM + BM * rank, n0 = (tile / p.m_tiles) * BN;
-        body(p, m0 + q * 32, n0, tbase, lane, [&] { tc::release_acc_2sm(tempty_leader, lane); });
+        body(p, m0 + q * 32, n0, tbase, lane, [&] { tc::release_acc_2sm(tempty_leader, lane); }, sl);
     }
     // TMEM accumulator (thread = row, 32-column chunks in registers) -> alpha / bias / accumulate
     // -> vectorised row-segment stores.
     template <class Rel>
-    __device__ static void body(const TcParams& p, int rowbase, int n0, uint32_t tbase, int lane, Rel release) {
+    __device__ static void body(const TcParams& p, int rowbase, int n0, uint32_t tbase, int lane, Rel release,
+                                tc::EpiSlot sl) {
         const int gm = rowbase + lane;
         const bool row_ok = gm < p.M;
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
+        for (int c = 32 * sl.sub; c < BN; c += 32 * sl.n) {
             uint32_t r[32];
             ptx::tmem_ld_32x32b_x32(tbase + c, r);
             ptx::tmem_ld_wait();
-            if (c + 32 >= BN) release();
+            if (c + 32 * sl.n >= BN) release();
             if (!row_ok) continue;
             const int gn0 = n0 + c;
             if (gn0 >= p.N) continue;
@@ -225,7 +227,7 @@ void launch_single(const TcParams& p, cudaStream_t s) {
     }
     const int tiles = p.m_tiles * p.n_tiles;
     const int grid = tiles < num_sms() ? tiles : num_sms();
-    k<<<grid, tc::kThreads, tc::Shape<Traits::BN, Traits::EPI_SMEM>::SMEM, s>>>(p);
+    k<<<grid, tc::threads_of<Traits>(), tc::Shape<Traits::BN, Traits::EPI_SMEM>::SMEM, s>>>(p);
     count_launch();
     AB_CUDA(cudaGetLastError());
 }
@@ -242,7 +244,7 @@ void launch_pair(const TcParams& p, cudaStream_t s) {
     const int pairs = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * pairs);
-    cfg.blockDim = dim3(tc::kThreads);
+    cfg.blockDim = dim3(tc::threads_of<Traits>());
     cfg.dynamicSmemBytes = tc::Shape2<Traits::BN, Traits::EPI_SMEM>::SMEM;
     cfg.stream = s;
     cudaLaunchAttribute attrs[1];

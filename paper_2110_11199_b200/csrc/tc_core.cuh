@@ -26,6 +26,12 @@ __device__ __forceinline__ void trace(unsigned long long* buf, int ev) {
 
 constexpr int kBM = 128, kBK = 64, kThreads = 192;
 
+// Which column chunks of the accumulator an epilogue warp owns: with EPI_WARPS = 8 two warps
+// share each TMEM lane quarter and take alternate chunks (index % n == sub).
+struct EpiSlot {
+    int sub, n;
+};
+
 constexpr int kSmemBudget = 225 * 1024;
 
 template <int BN, int EPI = 0>
@@ -39,8 +45,11 @@ struct Shape {
     static constexpr int SMEM = STAGES * STAGE_BYTES + EPI + 2048;
 };
 
+template <class Traits>
+constexpr int threads_of() { return 64 + 32 * Traits::EPI_WARPS; }
+
 template <class Traits, class Params>
-__global__ void __launch_bounds__(kThreads, 1) persistent_kernel(const __grid_constant__ Params p) {
+__global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_kernel(const __grid_constant__ Params p) {
     constexpr int BN = Traits::BN;
     using S = Shape<BN, Traits::EPI_SMEM>;
     constexpr int STAGES = S::STAGES;
@@ -48,21 +57,25 @@ __global__ void __launch_bounds__(kThreads, 1) persistent_kernel(const __grid_co
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
     uint8_t* sB = smem + STAGES * S::A_BYTES;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::STAGE_BYTES);
-    uint64_t* empty = full + STAGES;
-    uint64_t* tfull = empty + STAGES;
-    uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-    uint8_t* epi_smem = smem + STAGES * S::STAGE_BYTES + 1024;  // 1024-aligned (TMA swizzle atoms)
-    uint64_t* epi_bar = reinterpret_cast<uint64_t*>(smem + STAGES * S::STAGE_BYTES + 128);
+    // 1 KB barrier block: full[<=8] @0, empty[<=8] @64, tfull[2] @128, tempty[2] @144,
+    // TMEM slot @160, per-epilogue-warp barriers[<=8] @256
+    uint8_t* bblk = smem + STAGES * S::STAGE_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(bblk);
+    uint64_t* empty = reinterpret_cast<uint64_t*>(bblk + 64);
+    uint64_t* tfull = reinterpret_cast<uint64_t*>(bblk + 128);
+    uint64_t* tempty = reinterpret_cast<uint64_t*>(bblk + 144);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bblk + 160);
+    uint64_t* epi_bar = reinterpret_cast<uint64_t*>(bblk + 256);
+    uint8_t* epi_smem = bblk + 1024;  // 1024-aligned (TMA swizzle atoms)
+    static_assert(STAGES <= 8 && Traits::EPI_WARPS <= 8, "barrier block layout");
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int num_tiles = Traits::num_tiles(p);
 
     if (warp == 0 && lane == 0) {
         for (int i = 0; i < STAGES; ++i) { ptx::mbar_init(&full[i], 1); ptx::mbar_init(&empty[i], 1); }
-        for (int i = 0; i < 2; ++i) { ptx::mbar_init(&tfull[i], 1); ptx::mbar_init(&tempty[i], 4); }
-        for (int i = 0; i < 4; ++i) ptx::mbar_init(&epi_bar[i], 1);
+        for (int i = 0; i < 2; ++i) { ptx::mbar_init(&tfull[i], 1); ptx::mbar_init(&tempty[i], Traits::EPI_WARPS); }
+        for (int i = 0; i < Traits::EPI_WARPS; ++i) ptx::mbar_init(&epi_bar[i], 1);
         ptx::fence_barrier_init();
         Traits::prefetch(p);
     }
@@ -119,15 +132,18 @@ __global__ void __launch_bounds__(kThreads, 1) persistent_kernel(const __grid_co
             }
         }
     } else {
-        const int q = warp % 4;
+        const int q = warp % 4;          // TMEM lane quarter this warp may access
+        const int e = warp - 2;          // epilogue warp index
+        const EpiSlot slot{(e / 4), Traits::EPI_WARPS / 4};
         int acc = 0;
         uint32_t aphase = 0, ephase = 0;
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
             ptx::mbar_wait(&tfull[acc], aphase);
             ptx::tc_fence_after();
             const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
-            Traits::epilogue(p, tile, tbase, q, lane, &tempty[acc], epi_smem + q * (Traits::EPI_SMEM / 4), &epi_bar[q],
-                             ephase);
+            Traits::epilogue(p, tile, tbase, q, lane, &tempty[acc],
+                             epi_smem + e * (Traits::EPI_WARPS ? Traits::EPI_SMEM / Traits::EPI_WARPS : 0), &epi_bar[e],
+                             ephase, slot);
             if (++acc == 2) { acc = 0; aphase ^= 1; }
         }
         if (lane == 0) ptx::bulk_wait0();
@@ -159,7 +175,7 @@ struct Shape2 {
 };
 
 template <class Traits, class Params>
-__global__ void __launch_bounds__(kThreads, 1) persistent_kernel_2cta(const __grid_constant__ Params p) {
+__global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_kernel_2cta(const __grid_constant__ Params p) {
     constexpr int BN = Traits::BN;
     using S = Shape2<BN, Traits::EPI_SMEM>;
     constexpr int STAGES = S::STAGES;
@@ -167,13 +183,17 @@ __global__ void __launch_bounds__(kThreads, 1) persistent_kernel_2cta(const __gr
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
     uint8_t* sB = smem + STAGES * S::A_BYTES;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::STAGE_BYTES);
-    uint64_t* empty = full + STAGES;
-    uint64_t* tfull = empty + STAGES;
-    uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-    uint8_t* epi_smem = smem + STAGES * S::STAGE_BYTES + 1024;  // 1024-aligned (TMA swizzle atoms)
-    uint64_t* epi_bar = reinterpret_cast<uint64_t*>(smem + STAGES * S::STAGE_BYTES + 128);
+    // 1 KB barrier block: full[<=8] @0, empty[<=8] @64, tfull[2] @128, tempty[2] @144,
+    // TMEM slot @160, per-epilogue-warp barriers[<=8] @256
+    uint8_t* bblk = smem + STAGES * S::STAGE_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(bblk);
+    uint64_t* empty = reinterpret_cast<uint64_t*>(bblk + 64);
+    uint64_t* tfull = reinterpret_cast<uint64_t*>(bblk + 128);
+    uint64_t* tempty = reinterpret_cast<uint64_t*>(bblk + 144);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bblk + 160);
+    uint64_t* epi_bar = reinterpret_cast<uint64_t*>(bblk + 256);
+    uint8_t* epi_smem = bblk + 1024;  // 1024-aligned (TMA swizzle atoms)
+    static_assert(STAGES <= 8 && Traits::EPI_WARPS <= 8, "barrier block layout");
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const uint32_t rank = ptx::cluster_ctarank();
@@ -183,8 +203,8 @@ __global__ void __launch_bounds__(kThreads, 1) persistent_kernel_2cta(const __gr
 
     if (warp == 0 && lane == 0) {
         for (int i = 0; i < STAGES; ++i) { ptx::mbar_init(&full[i], 1); ptx::mbar_init(&empty[i], 1); }
-        for (int i = 0; i < 2; ++i) { ptx::mbar_init(&tfull[i], 1); ptx::mbar_init(&tempty[i], 8); }
-        for (int i = 0; i < 4; ++i) ptx::mbar_init(&epi_bar[i], 1);
+        for (int i = 0; i < 2; ++i) { ptx::mbar_init(&tfull[i], 1); ptx::mbar_init(&tempty[i], 2 * Traits::EPI_WARPS); }
+        for (int i = 0; i < Traits::EPI_WARPS; ++i) ptx::mbar_init(&epi_bar[i], 1);
         ptx::fence_barrier_init();
         Traits::prefetch(p);
     }
@@ -247,6 +267,8 @@ __global__ void __launch_bounds__(kThreads, 1) persistent_kernel_2cta(const __gr
         }
     } else {
         const int q = warp % 4;
+        const int e = warp - 2;
+        const EpiSlot slot{(e / 4), Traits::EPI_WARPS / 4};
         const uint32_t tempty0 = ptx::mapa(ptx::smem_u32(&tempty[0]), 0);
         int acc = 0;
         uint32_t aphase = 0, ephase = 0;
@@ -255,9 +277,10 @@ __global__ void __launch_bounds__(kThreads, 1) persistent_kernel_2cta(const __gr
             ptx::mbar_wait(&tfull[acc], aphase);
             ptx::tc_fence_after();
             const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
-            Traits::epilogue2(p, tile, rank, tbase, q, lane, tempty0 + acc * 8, epi_smem + q * (Traits::EPI_SMEM / 4),
-                              &epi_bar[q], ephase);
-            if (q == 2 && lane == 0) trace(p.trace, 4 * it + 3);
+            Traits::epilogue2(p, tile, rank, tbase, q, lane, tempty0 + acc * 8,
+                              epi_smem + e * (Traits::EPI_WARPS ? Traits::EPI_SMEM / Traits::EPI_WARPS : 0), &epi_bar[e],
+                              ephase, slot);
+            if (e == 0 && lane == 0) trace(p.trace, 4 * it + 3);
             if (++acc == 2) { acc = 0; aphase ^= 1; }
         }
         if (lane == 0) ptx::bulk_wait0();
