@@ -185,36 +185,25 @@ def run_reference(a):
 def run_ours(a):
     import numpy as np
     import torch
-    from paper_2110_11199_b200 import LearnerGroup, Precision, StrategyConfig, _lib, nccl_unique_id, \
-        strategy_from_name
+    from paper_2110_11199_b200 import LearnerGroup, Precision, StrategyConfig, _lib, strategy_from_name
 
-    world, rank, local = dist_env()
+    from paper_2110_11199_b200 import dist as D
+    env = D.rank_env()
+    world, rank, local = env.world, env.rank, env.local_rank
     assert world == a.gpus, f"--gpus {a.gpus} but WORLD_SIZE={world}"
     torch.cuda.set_device(local)
-    pg = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("gloo")
-        pg = dist
+    P = D.Plumbing(env)
     m = model_desc(a)
     strategy = strategy_from_name(a.strategy)
     cfg = StrategyConfig(strategy=strategy, learners=world, batch=a.batch, seed=2110_11199)
     prec = Precision.BF16 if a.precision == "bf16" else Precision.FP32
     g = LearnerGroup(m, cfg, precision=prec, device=local, first_learner=rank, local_learners=1)
-    if world > 1:
-        obj = [nccl_unique_id() if rank == 0 else None]
-        pg.broadcast_object_list(obj, src=0)
-        g.comm_init(rank, world, obj[0])
-        handles = [None] * world
-        pg.all_gather_object(handles, g.export_ipc())
-        for r in range(world):
-            g.import_ipc(r, r, 1, handles[r])
+    D.connect(g, P)
     g.synth_dataset(a.n_seg, a.n_seg, seed=7)
     lr = 0.1
 
     def barrier():
-        if pg:
-            pg.barrier()
+        P.barrier()
         g.barrier()
         torch.cuda.synchronize()
 
@@ -229,11 +218,7 @@ def run_ours(a):
             g.step(lr)
             ms.append(g.stats()["last_step_ms"])
         barrier()
-    tot_ms = sum(ms)
-    if pg:
-        t = torch.tensor([tot_ms], dtype=torch.float64)
-        pg.all_reduce(t, op=pg.ReduceOp.MAX)
-        tot_ms = float(t[0])
+    tot_ms = P.max_over_ranks(sum(ms))
     # ---- kernel roofline: the same K steps again with an event pair around every launch ----
     _lib.profile_enable(True)
     for _ in range(2):  # first profiled encounter runs eagerly, the second captures the graph
@@ -273,11 +258,7 @@ def run_ours(a):
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         _lib.check(_lib.lib().adpsgd_step_host_batch(g.handle, lr, fptr, lptr, loss))
-    e2e_s = time.perf_counter() - t0
-    if pg:
-        t = torch.tensor([e2e_s], dtype=torch.float64)
-        pg.all_reduce(t, op=pg.ReduceOp.MAX)
-        e2e_s = float(t[0])
+    e2e_s = P.max_over_ranks(time.perf_counter() - t0)
     barrier()
     e2e_val = world * a.batch * T_UNROLL * e2e_steps / e2e_s
 

@@ -134,8 +134,14 @@ int adpsgd_set_straggler(adpsgd_ctx* ctx, int32_t local_learner, double factor);
 int adpsgd_get_stats(adpsgd_ctx* ctx, adpsgd_perf* out);
 int64_t adpsgd_iteration(adpsgd_ctx* ctx);
 int adpsgd_set_iteration(adpsgd_ctx* ctx, int64_t k);
-/* Consensus distance ||W (I - 11^T/L)||_2 over the local learners (mixing.cpp:159-180). */
+/* Consensus distance ||W (I - 11^T/L)||_2 over the local learners (mixing.cpp:159-180),
+ * Gram of the deviations reduced on the device. */
 int adpsgd_consensus_distance(adpsgd_ctx* ctx, double* out);
+/* Mean frame cross-entropy at w over M segments (any M; heldout / full-train evaluation,
+ * objectives.hpp:55-56, engine.cpp:291-293). Forward only, on the device. */
+int adpsgd_eval_loss(adpsgd_ctx* ctx, const double* w, const int32_t* idx, int32_t M, double* loss_out);
+/* engine.cpp:124-128 averaged_model over the local learners (fp64 host vector). */
+int adpsgd_averaged_model(adpsgd_ctx* ctx, double* out, int64_t n);
 
 /* ---- multi-process (one process per GPU) ---- */
 /* NCCL communicator over all ranks; nccl_id = 128-byte ncclUniqueId from rank 0. */

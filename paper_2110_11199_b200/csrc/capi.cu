@@ -236,36 +236,18 @@ int adpsgd_set_iteration(adpsgd_ctx* ctx, int64_t k) {
 }
 
 int adpsgd_consensus_distance(adpsgd_ctx* ctx, double* out) {
+    return guard([&] { *out = C_(ctx).consensus_distance(); });
+}
+
+int adpsgd_eval_loss(adpsgd_ctx* ctx, const double* w, const int32_t* idx, int32_t M, double* loss_out) {
+    return guard([&] { *loss_out = C_(ctx).evaluate(w, idx, M, nullptr); });
+}
+
+int adpsgd_averaged_model(adpsgd_ctx* ctx, double* out, int64_t n) {
     return guard([&] {
-        // mixing.cpp:159-180: ||W (I - 11^T/L)||_2 = sqrt(lambda_max(G_c)), G_c the centred Gram of the columns.
         Ctx& c = C_(ctx);
-        const int L = c.cfg.local_learners;
-        std::vector<std::vector<float>> W(L, std::vector<float>(c.D));
-        AB_CUDA(cudaStreamSynchronize(c.s_main));
-        for (int j = 0; j < L; ++j)
-            AB_CUDA(cudaMemcpy(W[j].data(), c.learners[j].w[c.k & 1], c.D * sizeof(float), cudaMemcpyDeviceToHost));
-        std::vector<double> G(static_cast<size_t>(L) * L, 0.0);
-        std::vector<double> mean(c.D, 0.0);
-        for (int j = 0; j < L; ++j) for (int64_t p = 0; p < c.D; ++p) mean[p] += W[j][p];
-        for (int64_t p = 0; p < c.D; ++p) mean[p] /= L;
-        for (int a = 0; a < L; ++a)
-            for (int b = a; b < L; ++b) {
-                double s = 0;
-                for (int64_t p = 0; p < c.D; ++p) s += (W[a][p] - mean[p]) * (W[b][p] - mean[p]);
-                G[a * L + b] = G[b * L + a] = s;
-            }
-        // power iteration on the PSD Gram
-        std::vector<double> v(L, 1.0), u(L);
-        double lam = 0;
-        for (int it = 0; it < 500; ++it) {
-            double nrm = 0;
-            for (int a = 0; a < L; ++a) { u[a] = 0; for (int b = 0; b < L; ++b) u[a] += G[a * L + b] * v[b]; nrm += u[a] * u[a]; }
-            nrm = std::sqrt(nrm);
-            if (nrm == 0) { lam = 0; break; }
-            for (int a = 0; a < L; ++a) v[a] = u[a] / nrm;
-            lam = nrm;
-        }
-        *out = std::sqrt(std::max(0.0, lam));
+        AB_CHECK(n == c.D, ADPSGD_E_DIMENSION, "weight vector length != parameter count");
+        c.averaged_model(out);
     });
 }
 

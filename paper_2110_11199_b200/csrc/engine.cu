@@ -224,7 +224,8 @@ static inline void* off_ptr(void* p, int64_t elems, int es) { return static_cast
 
 // Forward + backward of the BLSTM on the batch already gathered into X0 / lab_step.
 // grad (fp32, flat layout) receives d(mean CE)/dw; loss_slot receives the mean CE.
-void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, float* loss_slot, cudaStream_t s) {
+void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, float* loss_slot, cudaStream_t s,
+                           bool backward) {
     const bool bf = bf16_mode;
     WView W{bf ? static_cast<const void*>(ln.shadow) : static_cast<const void*>(master), master, this, &ln};
     const int G4 = 4 * H;
@@ -339,6 +340,7 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
                                  row_loss, s);
     }
     launch_sum(row_loss, static_cast<int>(TB), scale, loss_slot, s);
+    if (!backward) return;
 
     // ---------------- backward: output / projection ----------------
     auto colsum = [&](const void* X, int64_t ld, int R, int N, float* out) {
@@ -808,28 +810,116 @@ void Ctx::step(double lr, const int32_t* taus, float* loss_out, const float* hos
 }
 
 double Ctx::gradient(const double* w, const int32_t* idx, int M, double* g_out) {
-    AB_CHECK(M == B, ADPSGD_E_DIMENSION, "gradient(): M must equal the context batch");
+    return evaluate(w, idx, M, g_out);
+}
+
+// Loss (and, if g_out != nullptr, gradient) at w over the given segments, chunked by the
+// context batch B (the last chunk wraps); the mean is over all frames (objectives.cpp:144-157).
+double Ctx::evaluate(const double* w, const int32_t* idx, int M, double* g_out) {
+    AB_CHECK(!g_out || M == B, ADPSGD_E_DIMENSION, "gradient(): M must equal the context batch");
+    AB_CHECK(M >= 1, ADPSGD_E_INVALID_STATE, "batch size must be >= 1");
     AB_CHECK(feats != nullptr, ADPSGD_E_INVALID_STATE, "dataset has no training samples");
     AB_CUDA(cudaSetDevice(cfg.device));
     cudaStream_t s = s_main;
     Learner& ln = learners[0];
-    // use the learner's spare buffer (w[nxt]) as the evaluation point; restore shadow after
+    // evaluate at w in the learner's spare buffer (w[nxt]); the shadow is restored after
     const int nxt = static_cast<int>((k & 1) ^ 1);
     std::vector<float> wf(w, w + D);
     AB_CUDA(cudaMemcpyAsync(ln.w[nxt], wf.data(), D * sizeof(float), cudaMemcpyHostToDevice, s));
     refresh_shadow(ln, ln.w[nxt], s);
-    AB_CUDA(cudaMemcpyAsync(idx_dev, idx, sizeof(int32_t) * B, cudaMemcpyHostToDevice, s));
-    gather_batch(feats, labels, idx_dev, s);
-    float* gtmp = static_cast<float*>(alloc_scratch_grad());
-    forward_backward(ln, ln.w[nxt], gtmp, loss_dev + 63, s);
-    std::vector<float> gh(D);
-    float lh = 0;
-    AB_CUDA(cudaMemcpyAsync(gh.data(), gtmp, D * sizeof(float), cudaMemcpyDeviceToHost, s));
-    AB_CUDA(cudaMemcpyAsync(&lh, loss_dev + 63, sizeof(float), cudaMemcpyDeviceToHost, s));
+    double result = 0.0;
+    if (g_out) {
+        AB_CUDA(cudaMemcpyAsync(idx_dev, idx, sizeof(int32_t) * B, cudaMemcpyHostToDevice, s));
+        gather_batch(feats, labels, idx_dev, s);
+        float* gtmp = static_cast<float*>(alloc_scratch_grad());
+        forward_backward(ln, ln.w[nxt], gtmp, loss_dev + 63, s, true);
+        std::vector<float> gh(D);
+        float lh = 0;
+        AB_CUDA(cudaMemcpyAsync(gh.data(), gtmp, D * sizeof(float), cudaMemcpyDeviceToHost, s));
+        AB_CUDA(cudaMemcpyAsync(&lh, loss_dev + 63, sizeof(float), cudaMemcpyDeviceToHost, s));
+        AB_CUDA(cudaStreamSynchronize(s));
+        for (int64_t i = 0; i < D; ++i) g_out[i] = gh[i];
+        result = lh;
+    } else {
+        // loss only, in chunks of B segments; the padded tail of the last chunk is masked out
+        double total = 0.0;
+        std::vector<int32_t> chunk(B);
+        for (int start = 0; start < M; start += B) {
+            const int valid = std::min(B, M - start);
+            for (int b = 0; b < B; ++b) chunk[b] = idx[start + (b < valid ? b : 0)];
+            AB_CUDA(cudaMemcpyAsync(idx_dev, chunk.data(), sizeof(int32_t) * B, cudaMemcpyHostToDevice, s));
+            gather_batch(feats, labels, idx_dev, s);
+            forward_backward(ln, ln.w[nxt], nullptr, loss_dev + 63, s, false);
+            launch_sum_masked(row_loss, T, B, valid, loss_dev + 62, s);
+            float part = 0;
+            AB_CUDA(cudaMemcpyAsync(&part, loss_dev + 62, sizeof(float), cudaMemcpyDeviceToHost, s));
+            AB_CUDA(cudaStreamSynchronize(s));
+            total += part;
+        }
+        result = total / (static_cast<double>(M) * T);
+    }
     refresh_shadow(ln, ln.w[k & 1], s);
     AB_CUDA(cudaStreamSynchronize(s));
-    for (int64_t i = 0; i < D; ++i) g_out[i] = gh[i];
-    return lh;
+    return result;
+}
+
+// engine.cpp:124-128 (averaged_model) over the local learners, fp64 on the host.
+void Ctx::averaged_model(double* out) {
+    AB_CUDA(cudaSetDevice(cfg.device));
+    AB_CUDA(cudaStreamSynchronize(s_main));
+    std::vector<float> f(D);
+    std::fill(out, out + D, 0.0);
+    for (auto& ln : learners) {
+        AB_CUDA(cudaMemcpy(f.data(), ln.w[k & 1], D * sizeof(float), cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < D; ++i) out[i] += f[i];
+    }
+    for (int64_t i = 0; i < D; ++i) out[i] /= static_cast<double>(learners.size());
+}
+
+// mixing.cpp:159-180: ||W (I - 11^T/L)||_2 = sqrt(lambda_max(G)), G the Gram of the
+// deviations of the local learners' models from their mean (device kernel, fp64 sums).
+double Ctx::consensus_distance() {
+    AB_CUDA(cudaSetDevice(cfg.device));
+    const int L = cfg.local_learners;
+    if (L < 2) return 0.0;
+    if (!gram_dev) gram_dev = static_cast<double*>(alloc(sizeof(double) * 16 * 16));
+    std::vector<const float*> wt;
+    for (auto& ln : learners) wt.push_back(ln.w[k & 1]);
+    launch_gram(D, L, wt.data(), gram_dev, s_main);
+    std::vector<double> G(static_cast<size_t>(L) * L);
+    AB_CUDA(cudaMemcpyAsync(G.data(), gram_dev, sizeof(double) * L * L, cudaMemcpyDeviceToHost, s_main));
+    AB_CUDA(cudaStreamSynchronize(s_main));
+    for (int a = 0; a < L; ++a)
+        for (int b = 0; b < a; ++b) G[a * L + b] = G[b * L + a];
+    // symmetric PSD L x L: cyclic Jacobi eigenvalues (exact enough for L <= 16)
+    std::vector<double> A = G;
+    for (int sweep = 0; sweep < 100; ++sweep) {
+        double off = 0;
+        for (int p = 0; p < L; ++p)
+            for (int q = p + 1; q < L; ++q) off += A[p * L + q] * A[p * L + q];
+        if (off < 1e-30) break;
+        for (int p = 0; p < L; ++p)
+            for (int q = p + 1; q < L; ++q) {
+                const double apq = A[p * L + q];
+                if (std::fabs(apq) < 1e-300) continue;
+                const double theta = (A[q * L + q] - A[p * L + p]) / (2 * apq);
+                const double t = (theta >= 0 ? 1.0 : -1.0) / (std::fabs(theta) + std::sqrt(theta * theta + 1));
+                const double c = 1 / std::sqrt(t * t + 1), sn = t * c;
+                for (int r = 0; r < L; ++r) {
+                    const double arp = A[r * L + p], arq = A[r * L + q];
+                    A[r * L + p] = c * arp - sn * arq;
+                    A[r * L + q] = sn * arp + c * arq;
+                }
+                for (int r = 0; r < L; ++r) {
+                    const double apr = A[p * L + r], aqr = A[q * L + r];
+                    A[p * L + r] = c * apr - sn * aqr;
+                    A[q * L + r] = sn * apr + c * aqr;
+                }
+            }
+    }
+    double lam = 0;
+    for (int p = 0; p < L; ++p) lam = std::max(lam, A[p * L + p]);
+    return std::sqrt(std::max(0.0, lam));
 }
 
 void* Ctx::alloc_scratch_grad() {

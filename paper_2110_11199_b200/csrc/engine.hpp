@@ -107,7 +107,12 @@ struct Ctx {
     void compute_body(int j, int mode, const float* wpt, cudaStream_t s);
     void run_compute(int j, int mode, const float* wpt, cudaStream_t s);
     void clear_graphs();
-    void forward_backward(const Learner& ln, const float* master, float* grad, float* loss_slot, cudaStream_t s);
+    void forward_backward(const Learner& ln, const float* master, float* grad, float* loss_slot, cudaStream_t s,
+                          bool backward = true);
+    double evaluate(const double* w, const int32_t* idx, int M, double* g_out);
+    void averaged_model(double* out);
+    double consensus_distance();
+    double* gram_dev = nullptr;
     void mix_and_update(double lr, const int32_t* taus);
     const float* grad_point(const Learner& ln, const int32_t* taus);
     const float* weight_ptr(int gid, int buf) const;

@@ -163,6 +163,16 @@ __global__ void sum_kernel(const float* __restrict__ x, int n, float scale, floa
     if (threadIdx.x == 0) out[0] = s * scale;
 }
 
+// sum of row_loss over rows r = t*B + b with b < valid (masked tail of a padded batch)
+__global__ void sum_masked_kernel(const float* __restrict__ x, int T, int B, int valid, float* __restrict__ out) {
+    __shared__ float sh[32];
+    float s = 0.f;
+    for (int i = threadIdx.x; i < T * B; i += blockDim.x)
+        if (i % B < valid) s += x[i];
+    s = block_reduce(s, false, sh);
+    if (threadIdx.x == 0) out[0] = s;
+}
+
 __global__ void f32_to_bf16_kernel(const float* __restrict__ in, bf16* __restrict__ out, int64_t n) {
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -321,6 +331,39 @@ __global__ void maxdiff_kernel(int64_t n, const float* __restrict__ a, const flo
     if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<int*>(out), __float_as_int(m));
 }
 
+// Gram of the deviations from the learner mean, G[a][b] += sum_p (w_a - mean)(w_b - mean), for a
+// list of up to 36 (a, b) pairs per launch (mixing.cpp:159-180 consensus_distance, on device).
+struct PairList { int a[36], b[36]; int n; };
+__global__ void gram_kernel(int64_t n, int L, PtrTab w, PairList pl, double* __restrict__ G) {
+    double acc[36];
+#pragma unroll
+    for (int q = 0; q < 36; ++q) acc[q] = 0.0;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        float v[kMaxTab > 16 ? 16 : kMaxTab];
+        float mean = 0.f;
+        for (int l = 0; l < L; ++l) { v[l] = w.p[l][i]; mean += v[l]; }
+        mean /= static_cast<float>(L);
+#pragma unroll
+        for (int q = 0; q < 36; ++q)
+            if (q < pl.n) acc[q] += static_cast<double>(v[pl.a[q]] - mean) * static_cast<double>(v[pl.b[q]] - mean);
+    }
+    __shared__ double sh[36][8];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int q = 0; q < 36; ++q) {
+        double x = acc[q];
+        for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if (lane == 0 && wid < 8) sh[q][wid] = x;
+    }
+    __syncthreads();
+    if (threadIdx.x < pl.n) {
+        double x = 0.0;
+        for (int j = 0; j < (blockDim.x >> 5) && j < 8; ++j) x += sh[threadIdx.x][j];
+        atomicAdd(&G[pl.a[threadIdx.x] * L + pl.b[threadIdx.x]], x);
+    }
+}
+
 __device__ __forceinline__ uint64_t hash64(uint64_t x) {
     x += 0x9e3779b97f4a7c15ULL;
     x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
@@ -420,6 +463,12 @@ void launch_sum(const float* x, int n, float scale, float* out, cudaStream_t s) 
     count_launch();
 }
 
+void launch_sum_masked(const float* x, int T, int B, int valid, float* out, cudaStream_t s) {
+    ProfScope ps_(s, PROF_REDUCE, 0, static_cast<double>(T) * B * 4);
+    sum_masked_kernel<<<1, 1024, 0, s>>>(x, T, B, valid, out);
+    count_launch();
+}
+
 void launch_f32_to_bf16(const float* in, bf16* out, int64_t n, cudaStream_t s) {
     ProfScope ps_(s, PROF_MIX, 0, (double)n * 6);
     f32_to_bf16_kernel<<<grid_for(n), 256, 0, s>>>(in, out, n);
@@ -488,6 +537,29 @@ void launch_dense_mix(int64_t n, int L, const float* const* w_tab, const double*
     }
     dense_mix_kernel<<<grid_for(n, 256, 4), 256, 0, s>>>(n, w, da, nloc, g, lr, o, sh);
     count_launch();
+}
+
+void launch_gram(int64_t n, int L, const float* const* w_tab, double* G, cudaStream_t s) {
+    AB_CHECK(L >= 1 && L <= 16, ADPSGD_E_CONFIG, "device consensus distance supports up to 16 local learners");
+    ProfScope ps_(s, PROF_OTHER, 0, static_cast<double>(n) * 4 * L);
+    PtrTab w{};
+    for (int l = 0; l < L; ++l) w.p[l] = w_tab[l];
+    AB_CUDA(cudaMemsetAsync(G, 0, sizeof(double) * L * L, s));
+    PairList pl{};
+    for (int a = 0; a < L; ++a)
+        for (int b = a; b < L; ++b) {
+            pl.a[pl.n] = a;
+            pl.b[pl.n] = b;
+            if (++pl.n == 36) {
+                gram_kernel<<<grid_for(n, 256, 4), 256, 0, s>>>(n, L, w, pl, G);
+                count_launch();
+                pl.n = 0;
+            }
+        }
+    if (pl.n) {
+        gram_kernel<<<grid_for(n, 256, 4), 256, 0, s>>>(n, L, w, pl, G);
+        count_launch();
+    }
 }
 
 void launch_maxdiff(int64_t n, const float* a, const float* b, float* out, cudaStream_t s) {

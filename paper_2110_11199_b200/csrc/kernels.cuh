@@ -34,6 +34,7 @@ void launch_colsum(const AT* X, int64_t ld, int R, int N, float* out, float* ws,
 // out[0] = scale * sum(x[0..n)) (single block, fixed order).
 void launch_sum(const float* x, int n, float scale, float* out, cudaStream_t s);
 
+void launch_sum_masked(const float* x, int T, int B, int valid, float* out, cudaStream_t s);
 void launch_f32_to_bf16(const float* in, bf16* out, int64_t n, cudaStream_t s);
 // rows x cols fp32 (ld_in) -> bf16 (ld_out), zero-filling columns [cols, ld_out).
 void launch_pad_rows_bf16(const float* in, int64_t ld_in, bf16* out, int64_t ld_out, int rows, int cols,
@@ -54,6 +55,8 @@ void launch_sdpsgd(int64_t n, int L, const float* w, const float* const* g_tab, 
 void launch_dense_mix(int64_t n, int L, const float* const* w_tab, const double* T, const int* cols, int nloc,
                       const float* const* g_tab, float lr, float* const* out_tab, bf16* const* shadow_tab,
                       cudaStream_t s);
+// Upper triangle of the Gram of deviations from the learner mean (fp64), L <= 16.
+void launch_gram(int64_t n, int L, const float* const* w_tab, double* G, cudaStream_t s);
 // max_j max_p |w_j[p] - w_0[p]| -> out (float, atomicMax on bits)
 void launch_maxdiff(int64_t n, const float* a, const float* b, float* out, cudaStream_t s);
 

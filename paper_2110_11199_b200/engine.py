@@ -280,6 +280,19 @@ class LearnerGroup:
         _lib.check(_lib.lib().adpsgd_consensus_distance(self._h, C.byref(out)))
         return out.value
 
+    def averaged_model(self) -> np.ndarray:
+        out = np.zeros(self.D, dtype=np.float64)
+        _lib.check(_lib.lib().adpsgd_averaged_model(self._h, _ptr(out, C.c_double), self.D))
+        return out
+
+    def eval_loss(self, w, idx) -> float:
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        idx = np.ascontiguousarray(idx, dtype=np.int32)
+        out = C.c_double()
+        _lib.check(_lib.lib().adpsgd_eval_loss(self._h, _ptr(w, C.c_double), _ptr(idx, C.c_int32), len(idx),
+                                               C.byref(out)))
+        return out.value
+
     # ---- multi-process plumbing (one process per GPU) ----
     def comm_init(self, rank: int, world: int, nccl_id: bytes) -> None:
         buf = C.create_string_buffer(nccl_id, 128)
@@ -323,3 +336,87 @@ class LstmObjective:
 
     def loss(self, w, indices) -> float:
         return self.g.gradient(w, indices)[0]
+
+
+# ---------------------------------------------------------------------------
+# run_training (engine.cpp:206-304) and its record / CSV output (engine.hpp:107-125, csvio.hpp)
+# ---------------------------------------------------------------------------
+DIVERGENCE_FACTOR = 10.0  # engine.cpp:15
+
+
+@dataclass
+class RunRecord:
+    iterations: list = field(default_factory=list)   # (k, consensus, lr)
+    epochs: list = field(default_factory=list)       # (epoch, heldout_loss, train_loss, lr)
+    final_model: np.ndarray | None = None
+    diverged: bool = False
+    divergence_epoch: int = -1
+    iteration_count: int = 0
+
+
+def iterations_per_epoch(cfg: StrategyConfig, train_count: int) -> int:
+    per = train_count // (cfg.learners * cfg.batch)  # engine.cpp:206-210
+    return per if per > 0 else 1
+
+
+def run_training(cfg: StrategyConfig, model: ModelDesc, feats, labels, train_count: int,
+                 precision: Precision = Precision.BF16, device: int = 0, consensus_every: int = 1,
+                 eval_train: bool = True) -> RunRecord:
+    """engine::run_training on the device: every local learner on one GPU, the mixing of
+    cfg.strategy each iteration, consensus distance (every `consensus_every` iterations; the
+    reference measures every iteration), per-epoch heldout / full-train loss of the averaged
+    model and the divergence rule (non-finite or > 10x the initial heldout loss)."""
+    cfg.validate()
+    g = LearnerGroup(model, cfg, precision=precision, device=device)
+    try:
+        g.set_dataset(feats, labels, train_count)
+        n_seg = np.asarray(feats).shape[0]
+        heldout_idx = np.arange(train_count, n_seg, dtype=np.int32)
+        train_idx = np.arange(train_count, dtype=np.int32)
+        rec = RunRecord()
+        initial = g.eval_loss(g.averaged_model(), heldout_idx) if len(heldout_idx) else float("nan")
+        ipe = iterations_per_epoch(cfg, train_count)
+        taus = list(cfg.staleness) if cfg.staleness else None
+        k = 0
+        for epoch in range(cfg.epochs):
+            lr = lr_at(cfg.lr, epoch)
+            for _ in range(ipe):
+                g.step(lr, taus=taus if cfg.strategy == Strategy.GENERIC else None)
+                cons = 0.0
+                if cfg.learners > 1 and (k % consensus_every == 0):
+                    cons = g.consensus_distance()
+                rec.iterations.append((k, cons, lr))
+                k += 1
+            avg = g.averaged_model()
+            heldout = g.eval_loss(avg, heldout_idx) if len(heldout_idx) else float("nan")
+            train = g.eval_loss(avg, train_idx) if eval_train else float("nan")
+            rec.epochs.append((epoch, heldout, train, lr))
+            if not np.isfinite(heldout) or heldout > DIVERGENCE_FACTOR * initial:
+                rec.diverged = True
+                rec.divergence_epoch = epoch
+                break
+        rec.iteration_count = len(rec.iterations)
+        rec.final_model = g.averaged_model()
+        return rec
+    finally:
+        g.close()
+
+
+def fmt_double(x: float) -> str:
+    """csvio.hpp:12-16 (%.17g)."""
+    return "%.17g" % x
+
+
+def write_csv(record: RunRecord, out_dir: str) -> None:
+    """run.csv (epoch, heldout_loss, train_loss, lr) and consensus.csv (k, consensus, lr), the
+    schema written by tools/main.cpp:99-105."""
+    import os
+    os.makedirs(out_dir, exist_ok=True)
+    with open(os.path.join(out_dir, "run.csv"), "w") as f:
+        f.write("epoch,heldout_loss,train_loss,lr\n")
+        for e, h, t, lr in record.epochs:
+            f.write(f"{e},{fmt_double(h)},{fmt_double(t)},{fmt_double(lr)}\n")
+    with open(os.path.join(out_dir, "consensus.csv"), "w") as f:
+        f.write("k,consensus,lr\n")
+        for k, c, lr in record.iterations:
+            f.write(f"{k},{fmt_double(c)},{fmt_double(lr)}\n")

@@ -94,3 +94,15 @@ def test_config_validation_without_gpu():
     c.batch, c.precision = 4, 1
     c.model = E.ModelDesc(2, 12, True, 8, 8, 16, 4).c()  # hidden not a multiple of 8 in bf16 mode
     assert _lib.lib().adpsgd_ctx_create(C.byref(c), C.byref(h)) == ConfigError.code
+
+
+def test_csv_format_and_ipe():
+    from paper_2110_11199_b200.engine import RunRecord, fmt_double, iterations_per_epoch, write_csv
+    import tempfile, os
+    assert fmt_double(0.1) == "0.10000000000000001"
+    assert iterations_per_epoch(E.StrategyConfig(learners=8, batch=1024), 65536) == 8
+    assert iterations_per_epoch(E.StrategyConfig(learners=4, batch=64), 100) == 1
+    r = RunRecord(iterations=[(0, 0.5, 0.1)], epochs=[(0, 2.5, 2.25, 0.1)])
+    with tempfile.TemporaryDirectory() as d:
+        write_csv(r, d)
+        assert open(os.path.join(d, "consensus.csv")).read().splitlines() == ["k,consensus,lr", "0,0.5,0.10000000000000001"]
