@@ -143,6 +143,16 @@ int adpsgd_eval_loss(adpsgd_ctx* ctx, const double* w, const int32_t* idx, int32
 /* engine.cpp:124-128 averaged_model over the local learners (fp64 host vector). */
 int adpsgd_averaged_model(adpsgd_ctx* ctx, double* out, int64_t n);
 
+/* chronos::coupled_async (chronos.cpp:178-299) on the device: FM/RM learners iterate at their
+ * own rates (durations[l] seconds per update = max(compute_l x straggler_l, comm_pairwise),
+ * chronos.cpp:51-58, 207), each update mixing with the neighbours' latest publications strictly
+ * before its time; `target` updates in the reference's event order. lr of update round r is
+ * lr_per_epoch[min(r / ipe, n_epochs - 1)]. event_learner / event_time (nullable, length target)
+ * receive the event log. */
+int adpsgd_async_run(adpsgd_ctx* ctx, int32_t strategy, const double* durations, int64_t target, int32_t ipe,
+                     const double* lr_per_epoch, int32_t n_epochs, int32_t* event_learner, double* event_time,
+                     int64_t* processed);
+
 /* ---- multi-process (one process per GPU) ---- */
 /* NCCL communicator over all ranks; nccl_id = 128-byte ncclUniqueId from rank 0. */
 int adpsgd_nccl_unique_id(void* out128);

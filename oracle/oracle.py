@@ -62,6 +62,9 @@ def lib() -> C.CDLL:
         L.or_engine_last_loss.restype = C.c_double
         L.or_engine_last_loss.argtypes = [C.c_void_p, C.c_int]
         L.or_engine_step.argtypes = [C.c_void_p, C.c_int, C.c_double, i64, C.c_int, P(i32)]
+        L.or_coupled_async.restype = i64
+        L.or_coupled_async.argtypes = [C.c_void_p, C.c_int, P(C.c_double), i64, C.c_int, P(C.c_double), C.c_int,
+                                       P(i32), P(C.c_double)]
         L.or_engine_step_injected.argtypes = [C.c_void_p, C.c_int, C.c_double, i64, C.c_int, P(i32),
                                               P(C.c_double)]
         _LIB = L
@@ -189,6 +192,16 @@ class OracleEngine:
         t = None if taus is None else np.ascontiguousarray(taus, dtype=np.int32)
         return lib().or_engine_step(self._h, strategy, lr, k, generic_mix,
                                     _p(t, C.c_int32) if t is not None else None)
+
+    def coupled_async(self, strategy: int, durations, target: int, ipe: int, lr_per_epoch):
+        """chronos::coupled_async (chronos.cpp:178-299); returns (event learners, event times)."""
+        d = np.ascontiguousarray(durations, dtype=np.float64)
+        lrs = np.ascontiguousarray(lr_per_epoch, dtype=np.float64)
+        ev = np.zeros(target, dtype=np.int32)
+        et = np.zeros(target, dtype=np.float64)
+        n = lib().or_coupled_async(self._h, strategy, _p(d, C.c_double), target, ipe, _p(lrs, C.c_double),
+                                   len(lrs), _p(ev, C.c_int32), _p(et, C.c_double))
+        return ev[:n], et[:n]
 
     def step_injected(self, strategy: int, lr: float, k: int, grads, generic_mix: int = 2,
                       taus=None) -> int:

@@ -60,6 +60,8 @@ _SIGS = {
     "adpsgd_consensus_distance": (C.c_int, [C.c_void_p, P(C.c_double)]),
     "adpsgd_eval_loss": (C.c_int, [C.c_void_p, P(C.c_double), P(i32), i32, P(C.c_double)]),
     "adpsgd_averaged_model": (C.c_int, [C.c_void_p, P(C.c_double), i64]),
+    "adpsgd_async_run": (C.c_int, [C.c_void_p, i32, P(C.c_double), i64, i32, P(C.c_double), i32, P(i32),
+                                   P(C.c_double), P(i64)]),
     "adpsgd_nccl_unique_id": (C.c_int, [C.c_void_p]),
     "adpsgd_comm_init": (C.c_int, [C.c_void_p, i32, i32, C.c_void_p]),
     "adpsgd_ipc_handle_size": (i64, [C.c_void_p]),

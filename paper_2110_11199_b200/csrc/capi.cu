@@ -251,6 +251,19 @@ int adpsgd_averaged_model(adpsgd_ctx* ctx, double* out, int64_t n) {
     });
 }
 
+int adpsgd_async_run(adpsgd_ctx* ctx, int32_t strategy, const double* durations, int64_t target, int32_t ipe,
+                     const double* lr_per_epoch, int32_t n_epochs, int32_t* event_learner, double* event_time,
+                     int64_t* processed) {
+    return guard([&] {
+        AB_CHECK(durations && lr_per_epoch, ADPSGD_E_CONFIG, "null durations / lr table");
+        for (int l = 0; l < C_(ctx).cfg.learners; ++l)
+            AB_CHECK(durations[l] > 0.0, ADPSGD_E_CONFIG, "cluster profile: compute_time must be > 0");
+        const int64_t n = C_(ctx).async_run(strategy, durations, target, ipe, lr_per_epoch, n_epochs, event_learner,
+                                            event_time);
+        if (processed) *processed = n;
+    });
+}
+
 int adpsgd_nccl_unique_id(void* out128) { return guard([&] { Comm::unique_id(out128); }); }
 
 int adpsgd_comm_init(adpsgd_ctx* ctx, int32_t rank, int32_t world, const void* id) {

@@ -17,6 +17,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <queue>
 #include <string>
 #include <vector>
 
@@ -552,14 +553,15 @@ void Ctx::compute_body(int j, int mode, const float* wpt, cudaStream_t s) {
 // Runs compute_body through a CUDA graph keyed by (learner, weight parity, mode, profiling):
 // the first encounter runs eagerly (warms plan caches / attributes), the second captures,
 // later ones replay — ~1000 launches per learner step become one graph launch.
-void Ctx::run_compute(int j, int mode, const float* wpt, cudaStream_t s) {
+void Ctx::run_compute(int j, int mode, const float* wpt, cudaStream_t s, int parity) {
     Learner& ln = learners[j];
-    const bool lagged = wpt != ln.w[k & 1];
+    if (parity < 0) parity = static_cast<int>(k & 1);
+    const bool lagged = wpt != ln.w[parity];
     if (lagged || !use_graphs) {
         compute_body(j, mode, wpt, s);
         return;
     }
-    const int key = ((j * 2 + static_cast<int>(k & 1)) * 2 + mode) * 2 + (g_prof_enabled ? 1 : 0);
+    const int key = ((j * 2 + parity) * 2 + mode) * 2 + (g_prof_enabled ? 1 : 0);
     auto it = graphs.find(key);
     if (it == graphs.end()) {
         StepGraph sg;
@@ -593,6 +595,102 @@ void Ctx::run_compute(int j, int mode, const float* wpt, cudaStream_t s) {
     AB_CUDA(cudaGraphLaunch(sg.exec, s));
     g_launch_count += sg.launches;
     if (!sg.prof.empty()) replayed_prof.push_back(&sg.prof);
+}
+
+// chronos::coupled_async (chronos.cpp:178-299) on the device: learners iterate at their own
+// rates (duration_l), each update averages the learner's model with its neighbours' latest
+// publications strictly before its update time (chronos.cpp:171-176) — w <- (w + pl + pr)/3 -
+// lr g (chronos.cpp:256) — and publishes the result (4 kept per learner, chronos.cpp:258-259).
+// The event order is the reference's min-heap order; gradients, mixing and publication run on
+// the GPU in that order. Returns the number of updates applied.
+int64_t Ctx::async_run(int strategy, const double* durations, int64_t target, int ipe, const double* lr_per_epoch,
+                       int n_epochs, int32_t* ev_learner, double* ev_time) {
+    AB_CHECK(strategy == ADPSGD_FM || strategy == ADPSGD_RM, ADPSGD_E_CONFIG, "coupled async runs FM or RM");
+    AB_CHECK(!(comm && comm->world > 1) && cfg.local_learners == cfg.learners, ADPSGD_E_CONFIG,
+             "coupled async: every learner hosted by this context");
+    const int L = cfg.learners;
+    AB_CHECK(L >= 3, ADPSGD_E_CONFIG, "FM/RM mixing requires at least 3 learners");
+    AB_CHECK(ipe >= 1 && n_epochs >= 1, ADPSGD_E_CONFIG, "ipe and lr table must be non-empty");
+    AB_CHECK(feats != nullptr && train_count >= 1, ADPSGD_E_INVALID_STATE, "dataset has no training samples");
+    AB_CUDA(cudaSetDevice(cfg.device));
+    cudaStream_t s = s_main;
+    constexpr int kPubs = 4;
+    if (pubs.empty())
+        for (int l = 0; l < L; ++l)
+            for (int q = 0; q < kPubs; ++q) pubs.push_back(static_cast<float*>(alloc(D * sizeof(float))));
+    struct Pub { double t; int slot; };
+    std::vector<std::vector<Pub>> pl(L);  // oldest first
+    std::vector<int> par(L, static_cast<int>(k & 1));
+    for (int l = 0; l < L; ++l) {
+        AB_CUDA(cudaMemcpyAsync(pubs[l * kPubs], learners[l].w[par[l]], D * sizeof(float), cudaMemcpyDeviceToDevice, s));
+        pl[l].push_back({0.0, 0});
+    }
+    using Entry = std::pair<double, int>;
+    std::priority_queue<Entry, std::vector<Entry>, std::greater<Entry>> q;
+    std::vector<int64_t> round(L, 0);
+    for (int l = 0; l < L; ++l) q.push({durations[l], l});
+    auto before = [&](int l, double t) -> const float* {  // chronos.cpp:171-176
+        for (auto it = pl[l].rbegin(); it != pl[l].rend(); ++it)
+            if (it->t < t) return pubs[l * kPubs + it->slot];
+        return pubs[l * kPubs + pl[l].front().slot];
+    };
+    int64_t processed = 0;
+    std::vector<int32_t> map(L);
+    while (processed < target) {
+        const auto [t_done, l] = q.top();
+        q.pop();
+        Learner& ln = learners[l];
+        const int64_t r = round[l];
+        const int ep = std::min<int64_t>(r / ipe, n_epochs - 1);
+        const float lr = static_cast<float>(lr_per_epoch[ep]);
+        AB_CUDA(cudaStreamSynchronize(s));  // pinned sampling slot reuse
+        sample_indices(ln, l);
+        run_compute(l, 0, ln.w[par[l]], s, par[l]);
+        int left, right;
+        if (strategy == ADPSGD_FM) {
+            left = (l + L - 1) % L;
+            right = (l + 1) % L;
+        } else {
+            permutation_for_iteration(cfg.seed, L, r, map.data());
+            int pos = 0;
+            for (int i = 0; i < L; ++i) if (map[i] == l) { pos = i; break; }
+            left = map[(pos + L - 1) % L];
+            right = map[(pos + 1) % L];
+        }
+        const int nxt = par[l] ^ 1;
+        launch_mix3(D, ln.w[par[l]], before(left, t_done), before(right, t_done), ln.g, lr, ln.w[nxt],
+                    bf16_mode ? ln.shadow : nullptr, s);
+        refresh_pad(ln, ln.w[nxt], s);
+        par[l] = nxt;
+        // publish (keep 4): reuse the oldest slot
+        int slot;
+        if (static_cast<int>(pl[l].size()) < kPubs) {
+            slot = static_cast<int>(pl[l].size());
+        } else {
+            slot = pl[l].front().slot;
+            pl[l].erase(pl[l].begin());
+        }
+        AB_CUDA(cudaMemcpyAsync(pubs[l * kPubs + slot], ln.w[nxt], D * sizeof(float), cudaMemcpyDeviceToDevice, s));
+        pl[l].push_back({t_done, slot});
+        if (ev_learner) ev_learner[processed] = l;
+        if (ev_time) ev_time[processed] = t_done;
+        ++round[l];
+        ++processed;
+        q.push({t_done + durations[l], l});
+    }
+    // leave every model in the context's current buffer
+    for (int l = 0; l < L; ++l) {
+        Learner& ln = learners[l];
+        const int cur = static_cast<int>(k & 1);
+        if (par[l] != cur) {
+            AB_CUDA(cudaMemcpyAsync(ln.w[cur], ln.w[par[l]], D * sizeof(float), cudaMemcpyDeviceToDevice, s));
+            refresh_shadow(ln, ln.w[cur], s);
+        }
+    }
+    AB_CUDA(cudaStreamSynchronize(s));
+    for (auto* recs : replayed_prof) prof_accumulate(*recs);
+    replayed_prof.clear();
+    return processed;
 }
 
 void Ctx::clear_graphs() {

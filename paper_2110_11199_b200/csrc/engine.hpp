@@ -105,7 +105,10 @@ struct Ctx {
     void gather_batch(const float* feats_src, const int32_t* labels_src, const int32_t* idx, cudaStream_t s);
     void sample_indices(Learner& ln, int j);
     void compute_body(int j, int mode, const float* wpt, cudaStream_t s);
-    void run_compute(int j, int mode, const float* wpt, cudaStream_t s);
+    void run_compute(int j, int mode, const float* wpt, cudaStream_t s, int parity = -1);
+    int64_t async_run(int strategy, const double* durations, int64_t target, int ipe, const double* lr_per_epoch,
+                      int n_epochs, int32_t* ev_learner, double* ev_time);
+    std::vector<float*> pubs;  // coupled-async publications, 4 per learner
     void clear_graphs();
     void forward_backward(const Learner& ln, const float* master, float* grad, float* loss_slot, cudaStream_t s,
                           bool backward = true);

@@ -106,3 +106,21 @@ def test_csv_format_and_ipe():
     with tempfile.TemporaryDirectory() as d:
         write_csv(r, d)
         assert open(os.path.join(d, "consensus.csv")).read().splitlines() == ["k,consensus,lr", "0,0.5,0.10000000000000001"]
+
+
+def test_wallclock_model_matches_reference_known_answers():
+    # test_chronos.cpp:47-76, 110-129
+    from paper_2110_11199_b200 import chronos as CH
+    from paper_2110_11199_b200.engine import Strategy as S
+    h = lambda L, **kw: CH.ClusterProfile(learners=L, compute_time=1.0, comm_pairwise=0.01, comm_allreduce=0.1, **kw)
+    assert CH.simulate_wallclock(S.SDPSGD, h(4), 10) == pytest.approx(11.0, rel=1e-12)
+    assert CH.simulate_wallclock(S.ADPSGD_D1D, h(4), 10) == pytest.approx(10.0, rel=1e-12)
+    assert CH.simulate_wallclock(S.SDPSGD, h(4, sync_overhead=0.05), 10) == pytest.approx(11.5, rel=1e-12)
+    assert CH.simulate_wallclock(S.ADPSGD_FM, h(4), 10) == pytest.approx(10.0, rel=1e-12)
+    slow = CH.simulate_wallclock(S.ADPSGD_FM, h(16, stragglers=[(0, 100.0)]), 20)
+    assert slow / CH.simulate_wallclock(S.ADPSGD_FM, h(16), 20) <= 16.0 / 15.0 + 0.1
+    rep = CH.slowdown_experiment(S.ADPSGD_D1D, h(16), [1.0, 5.0, 10.0, 100.0], 20)
+    assert rep[0]["ratio"] == pytest.approx(1.0) and rep[3]["ratio"] == pytest.approx(100.0, rel=0.05)
+    assert CH.slowdown_experiment(S.ADPSGD_FM, h(16), [100.0], 20)[0]["ratio"] <= 2.0
+    with pytest.raises(ConfigError):
+        CH.slowdown_experiment(S.ADPSGD_FM, h(16), [0.5], 20)
