@@ -96,7 +96,10 @@ Ctx::Ctx(const adpsgd_config& c) : cfg(c) {
     bf16_mode = c.precision == ADPSGD_PREC_BF16;
     es = bf16_mode ? 2 : 4;
     T = lay.T; B = c.batch; H = lay.H; nd = lay.nd; I = lay.I;
-    Ipad = bf16_mode ? static_cast<int>(round_up(I, 8)) : I;
+    fold_bias = bf16_mode;  // bias grads from a ones column of the wgrad B operands (no colsum passes)
+    Ipad = bf16_mode ? static_cast<int>(round_up(I + (fold_bias ? 1 : 0), 8)) : I;
+    ldH = nd * H + (fold_bias ? 8 : 0);
+    ldY = lay.P > 0 ? (fold_bias ? lay.P + 8 : lay.P) : 0;
     TB = static_cast<int64_t>(T) * B;
     ndH = nd * H;
     nd4H = nd * 4 * H;
@@ -122,13 +125,17 @@ Ctx::Ctx(const adpsgd_config& c) : cfg(c) {
     X0 = alloc(TB * Ipad * es);
     lab_step = static_cast<int32_t*>(alloc(sizeof(int32_t) * TB));
     for (int l = 0; l < lay.L; ++l) {
-        Hout.push_back(alloc(TB * ndH * es));
+        Hout.push_back(alloc(TB * ldH * es));
         gates.push_back(alloc(TB * nd4H * es));  // gate activations in the activation type
         cst.push_back(static_cast<float*>(alloc(TB * ndH * sizeof(float))));
     }
     if (lay.P > 0) {
-        Y = alloc(TB * lay.P * es);
+        Y = alloc(TB * ldY * es);
         dY = alloc(TB * lay.P * es);
+    }
+    if (fold_bias) {
+        for (int l = 0; l < lay.L; ++l) launch_fill_col_bf16(static_cast<bf16*>(Hout[l]), TB, ldH, ndH, 1.0f, s_main);
+        if (lay.P > 0) launch_fill_col_bf16(static_cast<bf16*>(Y), TB, ldY, lay.P, 1.0f, s_main);
     }
     if (bf16_mode) {
         ce_part = static_cast<float2*>(alloc(ce_part_elems(static_cast<int>(TB), lay.C) * sizeof(float2)));
@@ -236,6 +243,7 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
     for (int l = 0; l < lay.L; ++l) {
         const void* Xin = l == 0 ? X0 : Hout[l - 1];
         const int Kin = l == 0 ? Ipad : ndH;
+        const int ldx = l == 0 ? Ipad : ldH;
         if (fused) {
             for (int st = 0; st < T; ++st) {
                 LstmFwdDir dirs[2];
@@ -244,21 +252,21 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
                     const int tp = d == 0 ? t - 1 : t + 1;
                     int64_t ldw;
                     LstmFwdDir& a = dirs[d];
-                    a.x = static_cast<const bf16*>(off_ptr(Xin, static_cast<int64_t>(t) * B * Kin, es));
-                    a.ldx = Kin;
+                    a.x = static_cast<const bf16*>(off_ptr(Xin, static_cast<int64_t>(t) * B * ldx, es));
+                    a.ldx = ldx;
                     a.Kx = Kin;
                     a.w_ih = static_cast<const bf16*>(W.wih(l, d, &ldw));
                     a.ld_wih = ldw;
-                    a.h_prev = st > 0 ? static_cast<const bf16*>(off_ptr(Hout[l], static_cast<int64_t>(tp) * B * ndH + d * H, es)) : nullptr;
-                    a.ld_hprev = ndH;
+                    a.h_prev = st > 0 ? static_cast<const bf16*>(off_ptr(Hout[l], static_cast<int64_t>(tp) * B * ldH + d * H, es)) : nullptr;
+                    a.ld_hprev = ldH;
                     a.w_hh = static_cast<const bf16*>(W.at(lay.dir[l][d].w_hh));
                     a.bias = master + lay.dir[l][d].b;
                     a.c_prev = st > 0 ? cst[l] + static_cast<int64_t>(tp) * B * ndH + d * H : nullptr;
                     a.gates = static_cast<bf16*>(off_ptr(gates[l], static_cast<int64_t>(t) * B * nd4H + d * G4, es));
                     a.c = cst[l] + static_cast<int64_t>(t) * B * ndH + d * H;
-                    a.h = static_cast<bf16*>(off_ptr(Hout[l], static_cast<int64_t>(t) * B * ndH + d * H, es));
+                    a.h = static_cast<bf16*>(off_ptr(Hout[l], static_cast<int64_t>(t) * B * ldH + d * H, es));
                 }
-                lstm_fwd_step(dirs, nd, B, H, nd4H, ndH, ndH, s);
+                lstm_fwd_step(dirs, nd, B, H, nd4H, ndH, ldH, s);
             }
             continue;
         }
@@ -270,12 +278,12 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
                 g.M = B; g.N = G4;
                 int64_t ldw;
                 const void* wih = W.wih(l, d, &ldw);
-                g.seg[0].a = {off_ptr(Xin, static_cast<int64_t>(t) * B * Kin, es), Kin, false};
+                g.seg[0].a = {off_ptr(Xin, static_cast<int64_t>(t) * B * ldx, es), ldx, false};
                 g.seg[0].b = {wih, ldw, false};
                 g.seg[0].K = Kin;
                 g.nseg = 1;
                 if (st > 0) {
-                    g.seg[1].a = {off_ptr(Hout[l], static_cast<int64_t>(tp) * B * ndH + d * H, es), ndH, false};
+                    g.seg[1].a = {off_ptr(Hout[l], static_cast<int64_t>(tp) * B * ldH + d * H, es), ldH, false};
                     g.seg[1].b = {W.at(lay.dir[l][d].w_hh), H, false};
                     g.seg[1].K = H;
                     g.nseg = 2;
@@ -288,26 +296,27 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
                 const float* cprev = st > 0 ? cst[l] + static_cast<int64_t>(tp) * B * ndH + d * H : nullptr;
                 void* gt = off_ptr(gates[l], static_cast<int64_t>(t) * B * nd4H + d * G4, es);
                 float* ct = cst[l] + static_cast<int64_t>(t) * B * ndH + d * H;
-                void* ht = off_ptr(Hout[l], static_cast<int64_t>(t) * B * ndH + d * H, es);
+                void* ht = off_ptr(Hout[l], static_cast<int64_t>(t) * B * ldH + d * H, es);
                 if (bf)
                     launch_cell_fwd<bf16>(zstep + static_cast<int64_t>(d) * B * G4, G4, cprev, ndH, static_cast<bf16*>(gt), nd4H, ct,
-                                          static_cast<bf16*>(ht), ndH, B, H, s);
+                                          static_cast<bf16*>(ht), ldH, B, H, s);
                 else
                     launch_cell_fwd<float>(zstep + static_cast<int64_t>(d) * B * G4, G4, cprev, ndH, static_cast<float*>(gt), nd4H, ct,
-                                           static_cast<float*>(ht), ndH, B, H, s);
+                                           static_cast<float*>(ht), ldH, B, H, s);
             }
         }
     }
     const void* top = Hout[lay.L - 1];
     const void* yin = top;
     const int oi = lay.out_in;
+    const int ld_yin = lay.P > 0 ? ldY : ldH;
     if (lay.P > 0) {
         GemmArgs g;
         g.M = static_cast<int>(TB); g.N = lay.P;
-        g.seg[0].a = {top, ndH, false};
+        g.seg[0].a = {top, ldH, false};
         g.seg[0].b = {W.at(lay.w_proj), ndH, false};
         g.seg[0].K = ndH;
-        g.C = Y; g.ldc = lay.P; g.c_bf16 = bf;
+        g.C = Y; g.ldc = ldY; g.c_bf16 = bf;
         g.bias = master + lay.b_proj;
         g.tag = PROF_GEMM_OUT;
         gemm(bf, g, s);
@@ -321,7 +330,7 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
         a.W = static_cast<const bf16*>(W.at(lay.w_out));
         a.bias = master + lay.b_out;
         a.labels = lab_step;
-        a.M = static_cast<int>(TB); a.N = lay.C; a.K = oi;
+        a.M = static_cast<int>(TB); a.N = lay.C; a.K = oi; a.ldY = ld_yin;
         a.scale = scale;
         a.part = ce_part; a.zlab = ce_zlab; a.lse = ce_lse;
         a.row_loss = row_loss;
@@ -330,7 +339,7 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
     } else {
         GemmArgs g;
         g.M = static_cast<int>(TB); g.N = lay.C;
-        g.seg[0].a = {yin, oi, false};
+        g.seg[0].a = {yin, ld_yin, false};
         g.seg[0].b = {W.at(lay.w_out), oi, false};
         g.seg[0].K = oi;
         g.C = logits; g.ldc = lay.C;
@@ -350,15 +359,16 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
     };
     {   // dW_out = dlogits^T Yin
         GemmArgs g;
-        g.M = lay.C; g.N = oi;
+        g.M = lay.C; g.N = oi + (fold_bias ? 1 : 0);
         g.seg[0].a = {dlogits, lay.C, true};
-        g.seg[0].b = {yin, oi, true};
+        g.seg[0].b = {yin, ld_yin, true};
         g.seg[0].K = static_cast<int>(TB);
         g.C = grad + lay.w_out; g.ldc = oi;
+        if (fold_bias) { g.n_main = oi; g.extra = grad + lay.b_out; }  // ones column of Y -> db_out
         g.tag = PROF_GEMM_WGRAD;
         gemm(bf, g, s);
     }
-    colsum(dlogits, lay.C, static_cast<int>(TB), lay.C, grad + lay.b_out);
+    if (!fold_bias) colsum(dlogits, lay.C, static_cast<int>(TB), lay.C, grad + lay.b_out);
     float* dHcur = dHa;
     float* dHnext = dHb;
     if (lay.P > 0) {
@@ -374,15 +384,16 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
         }
         {   // dW_proj = dY^T top
             GemmArgs g;
-            g.M = lay.P; g.N = ndH;
+            g.M = lay.P; g.N = ndH + (fold_bias ? 1 : 0);
             g.seg[0].a = {dY, lay.P, true};
-            g.seg[0].b = {top, ndH, true};
+            g.seg[0].b = {top, ldH, true};
             g.seg[0].K = static_cast<int>(TB);
             g.C = grad + lay.w_proj; g.ldc = ndH;
+            if (fold_bias) { g.n_main = ndH; g.extra = grad + lay.b_proj; }  // ones column of the top layer -> db_proj
             g.tag = PROF_GEMM_WGRAD;
             gemm(bf, g, s);
         }
-        colsum(dY, lay.P, static_cast<int>(TB), lay.P, grad + lay.b_proj);
+        if (!fold_bias) colsum(dY, lay.P, static_cast<int>(TB), lay.P, grad + lay.b_proj);
         {   // dTop = dY W_proj
             GemmArgs g;
             g.M = static_cast<int>(TB); g.N = ndH;
@@ -408,6 +419,7 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
     for (int l = lay.L - 1; l >= 0; --l) {
         const void* Xin = l == 0 ? X0 : Hout[l - 1];
         const int Kin = l == 0 ? Ipad : ndH;
+        const int ldx = l == 0 ? Ipad : ldH;
         if (fused) {
             // BPTT: first cell backward unfused (no recurrent term), then one launch per step
             // doing dh_rec = dz_t W_hh for both directions with the next cell backward fused.
@@ -477,11 +489,12 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
             const DirOff& o = lay.dir[l][d];
             {   // dW_ih = dZ_d^T Xin
                 GemmArgs g;
-                g.M = G4; g.N = lay.in_dim[l];
+                g.M = G4; g.N = lay.in_dim[l] + (fold_bias ? 1 : 0);
                 g.seg[0].a = {off_ptr(dZ, d * G4, es), nd4H, true};
-                g.seg[0].b = {Xin, Kin, true};
+                g.seg[0].b = {Xin, ldx, true};
                 g.seg[0].K = static_cast<int>(TB);
                 g.C = grad + o.w_ih; g.ldc = lay.in_dim[l];
+                if (fold_bias) { g.n_main = lay.in_dim[l]; g.extra = grad + o.b; }  // ones column of the input -> db
                 g.tag = PROF_GEMM_WGRAD;
                 gemm(bf, g, s);
             }
@@ -491,7 +504,7 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
                 const int64_t a_row0 = d == 0 ? B : 0;
                 const int64_t b_row0 = d == 0 ? 0 : B;
                 g.seg[0].a = {off_ptr(dZ, a_row0 * nd4H + d * G4, es), nd4H, true};
-                g.seg[0].b = {off_ptr(Hout[l], b_row0 * ndH + d * H, es), ndH, true};
+                g.seg[0].b = {off_ptr(Hout[l], b_row0 * ldH + d * H, es), ldH, true};
                 g.seg[0].K = static_cast<int>((T - 1) * static_cast<int64_t>(B));
                 g.C = grad + o.w_hh; g.ldc = H;
                 g.tag = PROF_GEMM_WGRAD;
@@ -499,7 +512,7 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
             } else {
                 AB_CUDA(cudaMemsetAsync(grad + o.w_hh, 0, sizeof(float) * G4 * H, s));
             }
-            colsum(off_ptr(dZ, d * G4, es), nd4H, static_cast<int>(TB), G4, grad + o.b);
+            if (!fold_bias) colsum(off_ptr(dZ, d * G4, es), nd4H, static_cast<int>(TB), G4, grad + o.b);
         }
         if (l > 0) {  // dXin = sum_d dZ_d W_ih_d
             GemmArgs g;
@@ -522,9 +535,9 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
 
 void Ctx::gather_batch(const float* feats_src, const int32_t* labels_src, const int32_t* idx, cudaStream_t s) {
     if (bf16_mode)
-        launch_gather<bf16>(feats_src, labels_src, idx, B, T, I, Ipad, static_cast<bf16*>(X0), lab_step, s);
+        launch_gather<bf16>(feats_src, labels_src, idx, B, T, I, Ipad, static_cast<bf16*>(X0), lab_step, s, fold_bias);
     else
-        launch_gather<float>(feats_src, labels_src, idx, B, T, I, Ipad, static_cast<float*>(X0), lab_step, s);
+        launch_gather<float>(feats_src, labels_src, idx, B, T, I, Ipad, static_cast<float*>(X0), lab_step, s, false);
 }
 
 // Host-side sampling of learner j's batch: M draws next_below(train_count)

@@ -35,6 +35,10 @@ struct GemmArgs {
     bool accumulate = false;
     const float* bias = nullptr;
     int tag = 0;  // ProfCat of the tcgen05 launch (prof.hpp)
+    // Column redirect: output columns n >= n_main go to extra[m] (used with a ones column in the
+    // B operand so a weight-gradient GEMM also yields the bias gradient). n_main < 0: off.
+    int n_main = -1;
+    float* extra = nullptr;
 };
 
 // fp32 operands, fp32 or bf16 output, any majorness (gemm_simt.cu).

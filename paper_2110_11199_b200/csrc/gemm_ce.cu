@@ -264,7 +264,7 @@ void ce_forward_backward(const CeArgs& a, cudaStream_t s) {
     CeParams p;
     std::memset(&p, 0, sizeof(p));
     const bool pair = g_use_pair_mma && a.M > kBM;
-    make_map_gen(&p.ta, a.Y, false, a.K, a.M, a.K, 64, kBM, CU_TENSOR_MAP_SWIZZLE_128B);
+    make_map_gen(&p.ta, a.Y, false, a.K, a.M, a.ldY, 64, kBM, CU_TENSOR_MAP_SWIZZLE_128B);
     make_map_gen(&p.tb, a.W, false, a.K, a.N, a.K, 64, pair ? 128 : 256, CU_TENSOR_MAP_SWIZZLE_128B);
     make_map_gen(&p.m_dl, a.dlogits, false, a.N, a.M, a.N, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
     p.kb = (a.K + kBK - 1) / kBK;

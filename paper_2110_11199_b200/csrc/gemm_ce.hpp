@@ -15,6 +15,7 @@ struct CeArgs {
     const float* bias;      // b_out [N] (fp32 master)
     const int32_t* labels;  // [M]
     int M, N, K;
+    int ldY;                // row pitch of Y (>= K)
     float scale;            // 1 / (T * B)
     float2* part;           // [M x ceil(N/256)] scratch
     float* zlab;            // [M] scratch

@@ -93,6 +93,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const SimtParams p) {
 
 void gemm_simt(const GemmArgs& g, cudaStream_t s) {
     if (g.M <= 0 || g.N <= 0) return;
+    AB_CHECK(g.extra == nullptr, ADPSGD_E_DIMENSION, "column redirect is a tcgen05-path feature");
     SimtParams p{};
     p.M = g.M; p.N = g.N; p.nseg = g.nseg;
     for (int i = 0; i < g.nseg; ++i) {

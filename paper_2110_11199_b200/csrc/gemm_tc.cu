@@ -39,6 +39,8 @@ struct TcParams {
     const float* bias;
     int vec_ok;
     unsigned long long* trace;
+    int n_main;    // columns >= n_main are redirected to extra[row]
+    float* extra;
 };
 
 
@@ -124,6 +126,18 @@ struct GenTraits {
             if (!row_ok) continue;
             const int gn0 = n0 + c;
             if (gn0 >= p.N) continue;
+            if (p.extra && gn0 + 32 > p.n_main) {
+                // tail chunk containing redirected columns (fp32 output only)
+                float* crow = reinterpret_cast<float*>(p.C) + static_cast<int64_t>(gm) * p.ldc;
+                for (int i = 0; i < 32; ++i) {
+                    const int gn = gn0 + i;
+                    if (gn >= p.N) break;
+                    const float x = p.alpha * __uint_as_float(r[i]) + (p.bias ? p.bias[gn] : 0.f);
+                    if (gn < p.n_main) crow[gn] = p.accumulate ? crow[gn] + x : x;
+                    else if (gn == p.n_main) p.extra[gm] = p.accumulate ? p.extra[gm] + x : x;
+                }
+                continue;
+            }
             float v[32];
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] = p.alpha * __uint_as_float(r[i]);
@@ -357,6 +371,10 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
     ProfScope ps_(s, g.tag, 2.0 * g.M * g.N * ksum,
                   2.0 * (static_cast<double>(g.M) + g.N) * ksum + static_cast<double>(g.M) * g.N * esz * (g.accumulate ? 2 : 1));
     p.trace = trace_take();
+    p.n_main = g.n_main < 0 ? g.N : g.n_main;
+    p.extra = g.extra;
+    AB_CHECK(!g.extra || (!g.c_bf16 && g.N == p.n_main + 1), ADPSGD_E_DIMENSION,
+             "column redirect: fp32 output, exactly one extra column");
     p.vec_ok = ((reinterpret_cast<uintptr_t>(g.C) & 15) == 0) && ((g.ldc * esz) % 16 == 0);
     if (bn == 256) dispatch<256>(p, amn, bmn, g.c_bf16, pair, s);
     else dispatch<128>(p, amn, bmn, g.c_bf16, pair, s);

@@ -25,7 +25,7 @@ inline int grid_for(int64_t work, int threads = 256, int per_sm = 8) {
 template <typename AT>
 __global__ void gather_kernel(const float* __restrict__ feats, const int32_t* __restrict__ labels,
                               const int32_t* __restrict__ idx, int B, int T, int I, int ldx, AT* __restrict__ X,
-                              int32_t* __restrict__ lab) {
+                              int32_t* __restrict__ lab, int ones_col) {
     const int64_t total = static_cast<int64_t>(T) * B * ldx;
     for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -33,7 +33,7 @@ __global__ void gather_kernel(const float* __restrict__ feats, const int32_t* __
         const int64_t r = e / ldx;  // r = t*B + b
         const int b = static_cast<int>(r % B), t = static_cast<int>(r / B);
         const int64_t n = idx[b];
-        const float v = i < I ? feats[(n * T + t) * I + i] : 0.f;
+        const float v = i < I ? feats[(n * T + t) * I + i] : ((ones_col && i == I) ? 1.f : 0.f);
         X[e] = from_f<AT>(v);
         if (i == 0) lab[r] = labels[n * T + t];
     }
@@ -171,6 +171,12 @@ __global__ void sum_masked_kernel(const float* __restrict__ x, int T, int B, int
         if (i % B < valid) s += x[i];
     s = block_reduce(s, false, sh);
     if (threadIdx.x == 0) out[0] = s;
+}
+
+__global__ void fill_col_kernel(bf16* __restrict__ p, int64_t rows, int64_t ld, int col, float v) {
+    for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < rows;
+         r += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        p[r * ld + col] = __float2bfloat16_rn(v);
 }
 
 __global__ void f32_to_bf16_kernel(const float* __restrict__ in, bf16* __restrict__ out, int64_t n) {
@@ -410,10 +416,10 @@ __global__ void delay_kernel(uint64_t ns) {
 
 template <typename AT>
 void launch_gather(const float* feats, const int32_t* labels, const int32_t* idx, int B, int T, int I, int ldx, AT* X,
-                   int32_t* lab, cudaStream_t s) {
+                   int32_t* lab, cudaStream_t s, bool ones_col) {
     ProfScope ps_(s, PROF_GATHER, 0, (double)T * B * ldx * (sizeof(AT) + 4.0) + (double)T * B * 8);
     const int64_t total = static_cast<int64_t>(T) * B * ldx;
-    gather_kernel<AT><<<grid_for(total), 256, 0, s>>>(feats, labels, idx, B, T, I, ldx, X, lab);
+    gather_kernel<AT><<<grid_for(total), 256, 0, s>>>(feats, labels, idx, B, T, I, ldx, X, lab, ones_col ? 1 : 0);
     count_launch();
 }
 
@@ -466,6 +472,11 @@ void launch_sum(const float* x, int n, float scale, float* out, cudaStream_t s) 
 void launch_sum_masked(const float* x, int T, int B, int valid, float* out, cudaStream_t s) {
     ProfScope ps_(s, PROF_REDUCE, 0, static_cast<double>(T) * B * 4);
     sum_masked_kernel<<<1, 1024, 0, s>>>(x, T, B, valid, out);
+    count_launch();
+}
+
+void launch_fill_col_bf16(bf16* p, int64_t rows, int64_t ld, int col, float v, cudaStream_t s) {
+    fill_col_kernel<<<grid_for(rows), 256, 0, s>>>(p, rows, ld, col, v);
     count_launch();
 }
 
@@ -582,7 +593,7 @@ void launch_delay(uint64_t ns, cudaStream_t s) {
 
 #define AB_INST(AT)                                                                                                  \
     template void launch_gather<AT>(const float*, const int32_t*, const int32_t*, int, int, int, int, AT*, int32_t*, \
-                                    cudaStream_t);                                                                  \
+                                    cudaStream_t, bool);                                                            \
     template void launch_cell_fwd<AT>(const float*, int, const float*, int, AT*, int, float*, AT*, int, int, int, \
                                       cudaStream_t);                                                                \
     template void launch_cell_bwd<AT>(const float*, int, const float*, float*, bool, const AT*, int, const float*, \

@@ -8,7 +8,7 @@ namespace ab {
 // X[(t*B + b)*ldx + i] = feats[idx[b]][t][i] (i < I), 0 for I <= i < ldx; lab[t*B+b] = labels[idx[b]][t]
 template <typename AT>
 void launch_gather(const float* feats, const int32_t* labels, const int32_t* idx, int B, int T, int I, int ldx,
-                   AT* X, int32_t* lab, cudaStream_t s);
+                   AT* X, int32_t* lab, cudaStream_t s, bool ones_col);
 
 // LSTM cell forward for one (layer, direction, time step) over B rows (gate order i,f,g,o).
 template <typename AT>
@@ -35,6 +35,8 @@ void launch_colsum(const AT* X, int64_t ld, int R, int N, float* out, float* ws,
 void launch_sum(const float* x, int n, float scale, float* out, cudaStream_t s);
 
 void launch_sum_masked(const float* x, int T, int B, int valid, float* out, cudaStream_t s);
+// p[r * ld + col] = v for r < rows (the constant ones column of the bias-folding trick)
+void launch_fill_col_bf16(bf16* p, int64_t rows, int64_t ld, int col, float v, cudaStream_t s);
 void launch_f32_to_bf16(const float* in, bf16* out, int64_t n, cudaStream_t s);
 // rows x cols fp32 (ld_in) -> bf16 (ld_out), zero-filling columns [cols, ld_out).
 void launch_pad_rows_bf16(const float* in, int64_t ld_in, bf16* out, int64_t ld_out, int rows, int cols,
