@@ -97,6 +97,7 @@ Ctx::Ctx(const adpsgd_config& c) : cfg(c) {
     es = bf16_mode ? 2 : 4;
     T = lay.T; B = c.batch; H = lay.H; nd = lay.nd; I = lay.I;
     fold_bias = bf16_mode;  // bias grads from a ones column of the wgrad B operands (no colsum passes)
+    if (const char* e = std::getenv("ADPSGD_NO_FOLD_BIAS")) fold_bias = fold_bias && e[0] == '0';
     Ipad = bf16_mode ? static_cast<int>(round_up(I + (fold_bias ? 1 : 0), 8)) : I;
     ldH = nd * H + (fold_bias ? 8 : 0);
     ldY = lay.P > 0 ? (fold_bias ? lay.P + 8 : lay.P) : 0;

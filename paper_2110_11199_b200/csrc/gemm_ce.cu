@@ -2,9 +2,9 @@
 //
 //   logits = Y W_out^T + b_out        [M = T*B frames, N = C classes, K = P]
 //   pass 1: per 256-column tile, each frame's running max / sum-exp (thread = frame row, the
-//           32-column TMEM chunks stay in registers) -> part[r][tile]; the tile holding the
-//           frame's label records its logit.
-//   reduce: per frame, lse = combine(part), loss_r = lse - logit[label].
+//           32-column TMEM chunks stay in registers) -> part[r][tile].
+//   reduce: per frame, lse = combine(part), logit[label] = Y[r] . W_out[label] + b (a warp dot
+//           product), loss_r = lse - logit[label].
 //   pass 2: the logits tile is recomputed and dlogits = (softmax - onehot) / (T*B) leaves as
 //           bf16 through swizzled smem + TMA bulk stores.
 // The 21,504 x 32,000 logits (2.75 GB fp32) never reach HBM; the recompute costs one more
@@ -43,7 +43,7 @@ struct CeParams {
     int epi_skip;  // debug timing experiments (ADPSGD_EPI_SKIP=2): drain TMEM only
 };
 
-struct CeTraits {
+struct CeTraits : tc::TraitsBase {
     static constexpr int BN = 256;
     static constexpr bool A_MN = false;
     static constexpr bool B_MN = false;
@@ -78,32 +78,154 @@ struct CeTraits {
         body(p, m0 + q * 32, nt, tbase, lane, [&] { tc::release_acc_2sm(tempty_leader, lane); }, st, sl);
     }
     // thread = frame row; two warps per TMEM lane quarter take alternate 32-column chunks
-    // (EpiSlot); exponentials are single MUFU.EX2 on log2e-prescaled values; reductions are trees.
+    // (EpiSlot), two chunks per TMEM wait. Per element: pass 1 = FADD2 (bias) + FMNMX3 (max) +
+    // FFMA2 (scale, shift) + MUFU.EX2 + FADD2 (sum); pass 2 = FADD2 + FFMA2 + MUFU.EX2 + pack.
+    // No per-element branches: the label's logit comes from ce_reduce (a dot product), and
+    // pass 2 patches the one label element of a row in the staged smem box.
     __device__ static __forceinline__ float ex2(float x) {
         float y;
         asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
         return y;
     }
-    __device__ static __forceinline__ void bias32(const CeParams& p, int col, bool full, float* b) {
+    __device__ static __forceinline__ float max3(float a, float b, float c) {
+        float d;
+        asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+        return d;
+    }
+    __device__ static __forceinline__ void add2(float& a0, float& a1, float b0, float b1) {
+        uint64_t d;
+        asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pk(a0, a1)), "l"(pk(b0, b1)));
+        a0 = __uint_as_float(static_cast<uint32_t>(d)); a1 = __uint_as_float(static_cast<uint32_t>(d >> 32));
+    }
+    __device__ static __forceinline__ void fma2(float& a0, float& a1, float m, float c) {
+        uint64_t d;
+        asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(pk(a0, a1)), "l"(pk(m, m)), "l"(pk(c, c)));
+        a0 = __uint_as_float(static_cast<uint32_t>(d)); a1 = __uint_as_float(static_cast<uint32_t>(d >> 32));
+    }
+    __device__ static __forceinline__ uint64_t pk(float a, float b) {
+        return static_cast<uint64_t>(__float_as_uint(a)) | (static_cast<uint64_t>(__float_as_uint(b)) << 32);
+    }
+    // z[i] = acc[i] + bias[col + i]; columns >= N -> -inf (non-full tiles only)
+    template <bool FULL>
+    __device__ static __forceinline__ void logits32(const CeParams& p, int col, const uint32_t* v, float* z) {
 #pragma unroll
         for (int i = 0; i < 32; i += 4) {
-            if (full) {
+            float b0, b1, b2, b3;
+            if (FULL) {
                 const float4 b4 = __ldg(reinterpret_cast<const float4*>(p.bias + col + i));
-                b[i] = b4.x; b[i + 1] = b4.y; b[i + 2] = b4.z; b[i + 3] = b4.w;
+                b0 = b4.x; b1 = b4.y; b2 = b4.z; b3 = b4.w;
             } else {
+                b0 = __ldg(p.bias + min(col + i, p.N - 1)); b1 = __ldg(p.bias + min(col + i + 1, p.N - 1));
+                b2 = __ldg(p.bias + min(col + i + 2, p.N - 1)); b3 = __ldg(p.bias + min(col + i + 3, p.N - 1));
+            }
+            z[i] = __uint_as_float(v[i]); z[i + 1] = __uint_as_float(v[i + 1]);
+            z[i + 2] = __uint_as_float(v[i + 2]); z[i + 3] = __uint_as_float(v[i + 3]);
+            add2(z[i], z[i + 1], b0, b1);
+            add2(z[i + 2], z[i + 3], b2, b3);
+        }
+        if (!FULL) {
 #pragma unroll
-                for (int e = 0; e < 4; ++e) b[i + e] = col + i + e < p.N ? p.bias[col + i + e] : 0.f;
+            for (int i = 0; i < 32; ++i) z[i] = col + i < p.N ? z[i] : -INFINITY;
+        }
+    }
+    // online (max, sum-exp) over one 32-column chunk, natural-log units
+    __device__ static __forceinline__ void online32(float* z, float& m, float& s) {
+        constexpr float kLog2e = 1.4426950408889634f;
+        float t[11];
+#pragma unroll
+        for (int i = 0; i < 10; ++i) t[i] = max3(z[3 * i], z[3 * i + 1], z[3 * i + 2]);
+        t[10] = fmaxf(z[30], z[31]);
+        const float c0 = max3(t[0], t[1], t[2]), c1 = max3(t[3], t[4], t[5]), c2 = max3(t[6], t[7], t[8]);
+        const float mn = max3(max3(c0, c1, c2), t[9], fmaxf(t[10], m));
+        // all columns so far past N: keep m = -inf, subtract 0 instead of -inf
+        const float mr = mn == -INFINITY ? 0.f : mn;
+        const float sh = -mr * kLog2e;
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+            fma2(z[i], z[i + 1], kLog2e, sh);
+            z[i] = ex2(z[i]); z[i + 1] = ex2(z[i + 1]);
+        }
+#pragma unroll
+        for (int w = 16; w >= 2; w >>= 1)
+#pragma unroll
+            for (int i = 0; i < w; i += 2) add2(z[i], z[i + 1], z[i + w], z[i + w + 1]);
+        s = s * ex2((m - mr) * kLog2e) + (z[0] + z[1]);
+        m = mn;
+    }
+    template <bool FULL, class Rel>
+    __device__ static void body_t(const CeParams& p, int rowbase, int nt, uint32_t tbase, int lane, Rel release,
+                                  uint8_t* st, tc::EpiSlot sl) {
+        constexpr int PER = BN / 32;  // chunks per tile
+        const int r = rowbase + lane;
+        const bool ok = r < p.M;
+        const int n0 = nt * BN;
+        constexpr float kLog2e = 1.4426950408889634f;
+        if (p.mode == 0) {
+            float m = -INFINITY, s = 0.f;
+#pragma unroll 1
+            for (int j = sl.sub; j < PER; j += 2 * sl.n) {
+                const int ca = 32 * j, cb = 32 * (j + sl.n);
+                uint32_t va[32], vb[32];
+                ptx::tmem_ld_32x32b_x32(tbase + ca, va);
+                ptx::tmem_ld_32x32b_x32(tbase + cb, vb);
+                ptx::tmem_ld_wait();
+                if (j + 2 * sl.n >= PER) release();
+                float za[32], zb[32];
+                logits32<FULL>(p, n0 + ca, va, za);
+                logits32<FULL>(p, n0 + cb, vb, zb);
+                online32(za, m, s);
+                online32(zb, m, s);
+            }
+            // one partial per (tile, epilogue sub-slot)
+            if (ok) p.part[(static_cast<int64_t>(r) * p.n_tiles + nt) * sl.n + sl.sub] = make_float2(m, s);
+        } else {
+            const float lse = ok ? p.lse[r] : 0.f;
+            const float sc = p.scale;
+            const float q = __log2f(sc) - lse * kLog2e;  // dlogit = exp(z - lse) * sc = ex2(z log2e + q)
+            const int lab = ok ? p.labels[r] : -1;
+            const float dlab = ok ? ex2(fmaf(p.zlab[r], kLog2e, q)) - sc : 0.f;
+            int buf = 0;
+#pragma unroll 1
+            for (int j = sl.sub; j < PER; j += 2 * sl.n) {
+                uint32_t v[2][32];
+                ptx::tmem_ld_32x32b_x32(tbase + 32 * j, v[0]);
+                ptx::tmem_ld_32x32b_x32(tbase + 32 * (j + sl.n), v[1]);
+                ptx::tmem_ld_wait();
+                if (j + 2 * sl.n >= PER) release();
+#pragma unroll
+                for (int h = 0; h < 2; ++h, buf ^= 1) {
+                    const int col = n0 + 32 * (j + h * sl.n);
+                    float z[32];
+                    logits32<FULL>(p, col, v[h], z);
+                    uint32_t w[16];
+#pragma unroll
+                    for (int i = 0; i < 32; i += 2) {
+                        fma2(z[i], z[i + 1], kLog2e, q);
+                        w[i / 2] = tc::pack_bf16x2(ex2(z[i]), ex2(z[i + 1]));
+                    }
+                    uint8_t* box = st + buf * 2048;
+                    if (lane == 0) ptx::bulk_wait_read1();  // the store that last used this buffer has read it
+                    __syncwarp();
+                    tc::st_row_words<64>(box, lane, w);
+                    const int ll = lab - col;
+                    if (ll >= 0 && ll < 32) {  // softmax - onehot at the label column
+                        const uint32_t a = ptx::smem_u32(box) + lane * 64 + ((((ll >> 3) ^ ((lane >> 1) & 3))) << 4) + (ll & 7) * 2;
+                        const __nv_bfloat16 hv = __float2bfloat16_rn(dlab);
+                        asm volatile("st.shared.b16 [%0], %1;" ::"r"(a), "h"(*reinterpret_cast<const unsigned short*>(&hv)) : "memory");
+                    }
+                    ptx::fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        ptx::tma_store_2d_hint(&p.m_dl, box, col, rowbase, ptx::policy_evict_first());
+                        ptx::bulk_commit();
+                    }
+                }
             }
         }
     }
     template <class Rel>
     __device__ static void body(const CeParams& p, int rowbase, int nt, uint32_t tbase, int lane, Rel release,
                                 uint8_t* st, tc::EpiSlot sl) {
-        const int r = rowbase + lane;
-        const bool ok = r < p.M;
-        const int n0 = nt * BN;
-        const int lab = ok ? p.labels[r] : -1;
-        constexpr float kLog2e = 1.4426950408889634f;
         if (p.epi_skip == 1) {
 #pragma unroll 1
             for (int c = 32 * sl.sub; c < BN; c += 32 * sl.n) {
@@ -114,88 +236,8 @@ struct CeTraits {
             }
             return;
         }
-        if (p.mode == 0) {
-            float m = -INFINITY, s = 0.f, zl = 0.f;
-            bool has = false;
-#pragma unroll 1
-            for (int c = 32 * sl.sub; c < BN; c += 32 * sl.n) {
-                const int col = n0 + c;
-                const bool full = col + 32 <= p.N;
-                float b[32];
-                bias32(p, col, full, b);  // issued before the TMEM wait
-                uint32_t v[32];
-                ptx::tmem_ld_32x32b_x32(tbase + c, v);
-                ptx::tmem_ld_wait();
-                if (c + 32 * sl.n >= BN) release();
-                float z[32];
-#pragma unroll
-                for (int i = 0; i < 32; ++i)
-                    z[i] = (full || col + i < p.N) ? (__uint_as_float(v[i]) + b[i]) * kLog2e : -INFINITY;
-                const int ll = lab - col;
-                if (ll >= 0 && ll < 32) {
-#pragma unroll
-                    for (int i = 0; i < 32; ++i)
-                        if (i == ll) zl = z[i];
-                    has = true;
-                }
-                float t[16];
-#pragma unroll
-                for (int i = 0; i < 16; ++i) t[i] = fmaxf(z[i], z[i + 16]);
-#pragma unroll
-                for (int w = 8; w >= 1; w >>= 1)
-#pragma unroll
-                    for (int i = 0; i < w; ++i) t[i] = fmaxf(t[i], t[i + w]);
-                const float mn = fmaxf(m, t[0]);
-#pragma unroll
-                for (int i = 0; i < 16; ++i) t[i] = ex2(z[i] - mn) + ex2(z[i + 16] - mn);
-#pragma unroll
-                for (int w = 8; w >= 1; w >>= 1)
-#pragma unroll
-                    for (int i = 0; i < w; ++i) t[i] += t[i + w];
-                s = s * ex2(m - mn) + t[0];
-                m = mn;
-            }
-            if (ok) {
-                // natural-log units; one partial per (tile, epilogue sub-slot)
-                p.part[(static_cast<int64_t>(r) * p.n_tiles + nt) * sl.n + sl.sub] = make_float2(m / kLog2e, s);
-                if (has) p.zlab[r] = zl / kLog2e;
-            }
-        } else {
-            const float lse2 = ok ? p.lse[r] * kLog2e : 0.f;
-            const float sc = p.scale;
-            int buf = 0;
-#pragma unroll 1
-            for (int c = 32 * sl.sub; c < BN; c += 32 * sl.n, buf ^= 1) {
-                const int col = n0 + c;
-                const bool full = col + 32 <= p.N;
-                float b[32];
-                bias32(p, col, full, b);
-                uint32_t v[32];
-                ptx::tmem_ld_32x32b_x32(tbase + c, v);
-                ptx::tmem_ld_wait();
-                if (c + 32 * sl.n >= BN) release();
-                const int ll = lab - col;
-                uint32_t w[16];
-#pragma unroll
-                for (int i = 0; i < 32; i += 2) {
-                    float x0 = ex2(fmaf(__uint_as_float(v[i]) + b[i], kLog2e, -lse2)) * sc;
-                    float x1 = ex2(fmaf(__uint_as_float(v[i + 1]) + b[i + 1], kLog2e, -lse2)) * sc;
-                    if (i == ll) x0 -= sc;
-                    if (i + 1 == ll) x1 -= sc;
-                    w[i / 2] = tc::pack_bf16x2(x0, x1);
-                }
-                uint8_t* box = st + buf * 2048;
-                if (lane == 0) ptx::bulk_wait_read1();  // the store that last used this buffer has read it
-                __syncwarp();
-                tc::st_row_words<64>(box, lane, w);
-                ptx::fence_proxy_async_smem();
-                __syncwarp();
-                if (lane == 0) {
-                    ptx::tma_store_2d_hint(&p.m_dl, box, col, rowbase, ptx::policy_evict_first());
-                    ptx::bulk_commit();
-                }
-            }
-        }
+        if ((nt + 1) * BN <= p.N) body_t<true>(p, rowbase, nt, tbase, lane, release, st, sl);
+        else body_t<false>(p, rowbase, nt, tbase, lane, release, st, sl);
     }
 };
 
@@ -238,8 +280,12 @@ void launch_any(const Params& p, int tiles, bool pair, cudaStream_t s) {
     AB_CUDA(cudaGetLastError());
 }
 
-// one warp per frame: lse = m* + log(sum_t s_t exp(m_t - m*)), loss = lse - z_label
-__global__ void ce_reduce_kernel(const float2* __restrict__ part, int n_tiles, const float* __restrict__ zlab, int M,
+// one warp per frame: lse = m* + log(sum_t s_t exp(m_t - m*)); the label's logit
+// z_label = Y[r] . W_out[label] + b[label] (bf16 operands, fp32 accumulate, like the GEMM);
+// loss = lse - z_label.
+__global__ void ce_reduce_kernel(const float2* __restrict__ part, int n_tiles, const bf16* __restrict__ Y, int ldY,
+                                 const bf16* __restrict__ W, int K, const float* __restrict__ bias,
+                                 const int32_t* __restrict__ labels, int M, float* __restrict__ zlab,
                                  float* __restrict__ lse, float* __restrict__ row_loss) {
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (warp >= M) return;
@@ -250,10 +296,22 @@ __global__ void ce_reduce_kernel(const float2* __restrict__ part, int n_tiles, c
     float s = 0.f;
     for (int t = lane; t < n_tiles; t += 32) s += pr[t].y * __expf(pr[t].x - m);
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const int lab = labels[warp];
+    const bf16* y = Y + static_cast<int64_t>(warp) * ldY;
+    const bf16* w = W + static_cast<int64_t>(lab) * K;
+    float d = 0.f;
+    for (int k = 2 * lane; k < K; k += 64) {
+        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(y + k));
+        const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(w + k));
+        d = fmaf(a.x, b.x, fmaf(a.y, b.y, d));
+    }
+    for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
     if (lane == 0) {
         const float l = m + __logf(s);
+        const float z = d + bias[lab];
         lse[warp] = l;
-        row_loss[warp] = l - zlab[warp];
+        zlab[warp] = z;
+        row_loss[warp] = l - z;
     }
 }
 
@@ -285,8 +343,9 @@ void ce_forward_backward(const CeArgs& a, cudaStream_t s) {
     }
     {
         ProfScope ps_(s, PROF_CE, 0, static_cast<double>(a.M) * (p.n_tiles * 8 + 12));
-        ce_reduce_kernel<<<(a.M * 32 + 255) / 256, 256, 0, s>>>(a.part, p.n_tiles * (CeTraits::EPI_WARPS / 4), a.zlab,
-                                                                a.M, a.lse, a.row_loss);
+        ce_reduce_kernel<<<(a.M * 32 + 255) / 256, 256, 0, s>>>(a.part, p.n_tiles * (CeTraits::EPI_WARPS / 4), a.Y,
+                                                                a.ldY, a.W, a.K, a.bias, a.labels, a.M, a.zlab,
+                                                                a.lse, a.row_loss);
         count_launch();
     }
     {

@@ -77,7 +77,7 @@ struct FwdParams {
     unsigned long long* trace;
 };
 
-struct FwdTraits {
+struct FwdTraits : tc::TraitsBase {
     static constexpr int BN = 256;
     // per warp (20 KB): c_{t-1} box (fp32 32x32, SW128) | c box | 4 gate boxes (bf16 32x32, SW64) | h box
     static constexpr int EPI_WARP = 20 * 1024;
@@ -274,12 +274,12 @@ struct BwdParams {
 };
 
 template <int BN_>
-struct BwdTraits {
+struct BwdTraits : tc::TraitsBase {
     static constexpr int BN = BN_;
-    // per warp (16 KB): dH | dc | c | c_prev (fp32 16x32, SW64, 2 KB each) | gates 4 x (bf16 16x32, SW32, 1 KB)
-    //                   | dz 4 x (bf16 16x32, SW32, 1 KB)
+    // per warp (30 KB): two input sets (12 KB each: dH | dc | c | c_prev fp32 16x32 SW64 2 KB each,
+    // gates 4 x bf16 16x32 SW32 1 KB) | dz out 4 x 1 KB | dc out 2 KB
     static constexpr int EPI_WARPS = 4;
-    static constexpr int EPI_SMEM = EPI_WARPS * 16 * 1024;
+    static constexpr int EPI_SMEM = EPI_WARPS * 30 * 1024;
     static constexpr bool B_MN = true;
     __device__ static int num_tiles(const BwdParams& p) { return p.ngroups * p.m_tiles * p.n_tiles; }
     __device__ static void prefetch(const BwdParams& p) {
@@ -326,6 +326,57 @@ struct BwdTraits {
         for (int j = 0; j < BN / 128; ++j)
             ptx::tma_load_2d_2sm_hint(sB + j * 64 * kBK * 2, &g.tb, bar, u0 + rank * (BN / 2) + 64 * j, k0, keep);
     }
+    // The epilogue inputs (dH, dc_rec, c, c_{t-1}, gates) do not depend on the GEMM: epi_begin
+    // issues the TMA loads of this warp's first two 16-unit chunks into smem and L2-prefetches
+    // the rest while the mainloop runs; body then consumes chunk c from buffer c&1 and refills
+    // that buffer with chunk c+2 (two chunks in flight per warp).
+    static constexpr int IN_BYTES = 12 * 1024;
+    __device__ static void issue(const BwdGroup& g, int H, int j0, int rowbase, uint8_t* in, uint64_t* bar) {
+        const bool has_prev = g.c_prev != nullptr;
+        ptx::mbar_arrive_expect_tx(bar, (has_prev ? 4 : 3) * 2048 + 4 * 1024);
+        const uint64_t stream = ptx::policy_evict_first();
+        ptx::tma_load_2d_hint(in, &g.m_dH, bar, j0, rowbase, stream);
+        ptx::tma_load_2d(in + 2048, &g.m_dc, bar, j0, rowbase);
+        ptx::tma_load_2d_hint(in + 4096, &g.m_c, bar, j0, rowbase, stream);
+        if (has_prev) ptx::tma_load_2d_hint(in + 6144, &g.m_cp, bar, j0, rowbase, stream);
+#pragma unroll
+        for (int gi = 0; gi < 4; ++gi) ptx::tma_load_2d_hint(in + 8192 + gi * 1024, &g.m_gates, bar, gi * H + j0, rowbase, stream);
+    }
+    __device__ static void begin(const BwdParams& p, int grp, int m0, int u0, int q, int lane, uint8_t* st, uint64_t* ebar,
+                                 tc::EpiSlot sl) {
+        const BwdGroup& g = p.g[grp];
+        const int rowbase = m0 + q * 32;
+        const int step = 16 * sl.n;
+        if (lane == 0) {
+            int b = 0;
+            for (int uc = 16 * sl.sub; uc < BN && b < 2; uc += step, ++b) issue(g, p.H, u0 + uc, rowbase, st + b * IN_BYTES, ebar + b);
+        }
+        // L2 prefetch of the chunks after the first two: one box per lane
+        const bool has_prev = g.c_prev != nullptr;
+        for (int uc = 16 * sl.sub + 2 * step, i = 0; uc < BN; uc += step, ++i) {
+            const int j0 = u0 + uc;
+            const int box = lane & 7;
+            if ((lane >> 3) != (i & 3)) continue;
+            if (box == 0) ptx::tma_prefetch_l2_2d(&g.m_dH, j0, rowbase);
+            else if (box == 1) ptx::tma_prefetch_l2_2d(&g.m_dc, j0, rowbase);
+            else if (box == 2) ptx::tma_prefetch_l2_2d(&g.m_c, j0, rowbase);
+            else if (box == 3) { if (has_prev) ptx::tma_prefetch_l2_2d(&g.m_cp, j0, rowbase); }
+            else ptx::tma_prefetch_l2_2d(&g.m_gates, (box - 4) * p.H + j0, rowbase);
+        }
+    }
+    template <class S>
+    __device__ static void epi_begin2(const BwdParams& p, int tile, uint32_t rank, int q, int lane, uint8_t* st,
+                                      uint64_t* ebar, S sl) {
+        int grp, m0, u0;
+        coords2(p, tile, grp, m0, u0);
+        begin(p, grp, m0 + kBM * rank, u0, q, lane, st, ebar, sl);
+    }
+    template <class S>
+    __device__ static void epi_begin(const BwdParams& p, int tile, int q, int lane, uint8_t* st, uint64_t* ebar, S sl) {
+        int grp, m0, u0;
+        coords(p, tile, grp, m0, u0);
+        begin(p, grp, m0, u0, q, lane, st, ebar, sl);
+    }
     __device__ static void epilogue2(const BwdParams& p, int tile, uint32_t rank, uint32_t tbase, int q, int lane,
                                      uint32_t tempty_leader, uint8_t* st, uint64_t* ebar, uint32_t& ephase,
                                      tc::EpiSlot sl) {
@@ -340,53 +391,38 @@ struct BwdTraits {
         coords(p, tile, grp, m0, u0);
         body(p, grp, m0, u0, tbase, q, lane, [&] { tc::release_acc(tempty, lane); }, st, ebar, ephase, sl);
     }
-    // epilogue (thread = row), per 16-unit chunk: the 8 input streams (dH, dc_rec, gates i,f,g,o,
-    // c, c_{t-1}) of this warp's 32 rows arrive by TMA into swizzled smem while dh_rec leaves
-    // TMEM; the cell backward runs in registers; dz (4 x bf16) and dc_rec leave by TMA stores.
+    // epilogue (thread = row), per 16-unit chunk: dh_rec leaves TMEM; the cell backward runs in
+    // registers on the chunk's prefetched inputs; dz (4 x bf16) and dc_rec leave by TMA stores.
     template <class Rel>
     __device__ static void body(const BwdParams& p, int grp, int m0, int u0, uint32_t tbase, int q, int lane,
                                 Rel release, uint8_t* st, uint64_t* ebar, uint32_t& ephase, tc::EpiSlot sl) {
         const BwdGroup& g = p.g[grp];
         const int H = p.H;
         const int rowbase = m0 + q * 32;
-        uint8_t* bdH = st;
-        uint8_t* bdc = st + 2048;
-        uint8_t* bc = st + 4096;
-        uint8_t* bcp = st + 6144;
-        uint8_t* bg = st + 8192;    // 4 x 1 KB
-        uint8_t* bdz = st + 12288;  // 4 x 1 KB
+        uint8_t* bdz = st + 2 * IN_BYTES;         // 4 x 1 KB
+        uint8_t* bdco = st + 2 * IN_BYTES + 4096;  // 2 KB
         const bool has_prev = g.c_prev != nullptr;
-        const uint32_t in_bytes = (has_prev ? 4 : 3) * 2048 + 4 * 1024;
+        const int step = 16 * sl.n;
+        int b = 0;
 #pragma unroll 1
-        for (int uc = 16 * sl.sub; uc < BN; uc += 16 * sl.n) {
+        for (int uc = 16 * sl.sub; uc < BN; uc += step, b ^= 1) {
             const int j0 = u0 + uc;
-            if (lane == 0) {
-                ptx::mbar_arrive_expect_tx(ebar, in_bytes);
-                const uint64_t stream = ptx::policy_evict_first();
-                ptx::tma_load_2d_hint(bdH, &g.m_dH, ebar, j0, rowbase, stream);
-                ptx::tma_load_2d(bdc, &g.m_dc, ebar, j0, rowbase);
-                ptx::tma_load_2d_hint(bc, &g.m_c, ebar, j0, rowbase, stream);
-                if (has_prev) ptx::tma_load_2d_hint(bcp, &g.m_cp, ebar, j0, rowbase, stream);
-#pragma unroll
-                for (int gi = 0; gi < 4; ++gi)
-                    ptx::tma_load_2d_hint(bg + gi * 1024, &g.m_gates, ebar, gi * H + j0, rowbase, stream);
-            }
+            uint8_t* in = st + b * IN_BYTES;
             uint32_t acc[16];
             ptx::tmem_ld_32x32b_x16_(tbase + uc, acc);
             ptx::tmem_ld_wait();
-            if (uc + 16 * sl.n >= BN) release();
-            ptx::mbar_wait(ebar, ephase);
-            ephase ^= 1;
-            if (p.epi_skip) continue;
+            if (uc + step >= BN) release();
+            ptx::mbar_wait(ebar + b, (ephase >> b) & 1u);
+            ephase ^= 1u << b;
             uint32_t wdh[16], wdc[16], wc[16], wcp[16], wi[8], wf[8], wg[8], wo[8];
-            tc::ld_row_words<64>(bdH, lane, wdh);
-            tc::ld_row_words<64>(bdc, lane, wdc);
-            tc::ld_row_words<64>(bc, lane, wc);
-            if (has_prev) tc::ld_row_words<64>(bcp, lane, wcp);
-            tc::ld_row_words<32>(bg + 0 * 1024, lane, wi);
-            tc::ld_row_words<32>(bg + 1 * 1024, lane, wf);
-            tc::ld_row_words<32>(bg + 2 * 1024, lane, wg);
-            tc::ld_row_words<32>(bg + 3 * 1024, lane, wo);
+            tc::ld_row_words<64>(in, lane, wdh);
+            tc::ld_row_words<64>(in + 2048, lane, wdc);
+            tc::ld_row_words<64>(in + 4096, lane, wc);
+            if (has_prev) tc::ld_row_words<64>(in + 6144, lane, wcp);
+            tc::ld_row_words<32>(in + 8192 + 0 * 1024, lane, wi);
+            tc::ld_row_words<32>(in + 8192 + 1 * 1024, lane, wf);
+            tc::ld_row_words<32>(in + 8192 + 2 * 1024, lane, wg);
+            tc::ld_row_words<32>(in + 8192 + 3 * 1024, lane, wo);
             uint32_t zi[8], zf[8], zg[8], zo[8], dco[16];
 #pragma unroll
             for (int e = 0; e < 16; ++e) {
@@ -415,21 +451,24 @@ struct BwdTraits {
                     zg[w] = __float_as_uint(vg); zo[w] = __float_as_uint(vo);
                 }
             }
+            // every lane has consumed its inputs: refill this buffer with chunk c + 2; and the
+            // previous chunk's stores must have read the output boxes before they are rewritten
+            if (lane == 0) ptx::bulk_wait_read0();
+            __syncwarp();
+            if (lane == 0 && uc + 2 * step < BN) issue(g, H, j0 + 2 * step, rowbase, in, ebar + b);
             tc::st_row_words<32>(bdz + 0 * 1024, lane, zi);
             tc::st_row_words<32>(bdz + 1 * 1024, lane, zf);
             tc::st_row_words<32>(bdz + 2 * 1024, lane, zg);
             tc::st_row_words<32>(bdz + 3 * 1024, lane, zo);
-            tc::st_row_words<64>(bdc, lane, dco);  // dc_rec updated in place
+            tc::st_row_words<64>(bdco, lane, dco);
             ptx::fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
 #pragma unroll
                 for (int gi = 0; gi < 4; ++gi) ptx::tma_store_2d(&g.m_dz, bdz + gi * 1024, gi * H + j0, rowbase);
-                ptx::tma_store_2d(&g.m_dc, bdc, j0, rowbase);
+                ptx::tma_store_2d(&g.m_dc, bdco, j0, rowbase);
                 ptx::bulk_commit();
-                ptx::bulk_wait_read0();
             }
-            __syncwarp();
         }
     }
 };

@@ -46,7 +46,7 @@ struct TcParams {
 
 // Generic GEMM traits for the persistent skeletons in tc_core.cuh (single CTA and CTA pair).
 template <int BN_, bool AMN, bool BMN, bool CBF16>
-struct GenTraits {
+struct GenTraits : tc::TraitsBase {
     static constexpr int BN = BN_;
     static constexpr int EPI_SMEM = 0;
     static constexpr int EPI_WARPS = 8;

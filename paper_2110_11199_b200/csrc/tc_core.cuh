@@ -34,6 +34,18 @@ struct EpiSlot {
 
 constexpr int kSmemBudget = 225 * 1024;
 
+// Default hooks: Traits inherit from TraitsBase and may shadow these.
+// epi_begin / epi_begin2 run on every epilogue warp BEFORE it waits for the tile's accumulator:
+// epilogue inputs that do not depend on the GEMM (cell state, upstream gradients) can be
+// loaded or L2-prefetched there, overlapping the mainloop. Each epilogue warp owns two
+// mbarriers (ebar[0], ebar[1]) and the bits of ephase.
+struct TraitsBase {
+    template <class P, class S>
+    __device__ static void epi_begin(const P&, int, int, int, uint8_t*, uint64_t*, S) {}
+    template <class P, class S>
+    __device__ static void epi_begin2(const P&, int, uint32_t, int, int, uint8_t*, uint64_t*, S) {}
+};
+
 template <int BN, int EPI = 0>
 struct Shape {
     static constexpr int A_BYTES = kBM * kBK * 2;
@@ -58,7 +70,7 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
     uint8_t* sA = smem;
     uint8_t* sB = smem + STAGES * S::A_BYTES;
     // 1 KB barrier block: full[<=8] @0, empty[<=8] @64, tfull[2] @128, tempty[2] @144,
-    // TMEM slot @160, per-epilogue-warp barriers[<=8] @256
+    // TMEM slot @160, per-epilogue-warp barrier pairs[<=16] @256
     uint8_t* bblk = smem + STAGES * S::STAGE_BYTES;
     uint64_t* full = reinterpret_cast<uint64_t*>(bblk);
     uint64_t* empty = reinterpret_cast<uint64_t*>(bblk + 64);
@@ -75,7 +87,7 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
     if (warp == 0 && lane == 0) {
         for (int i = 0; i < STAGES; ++i) { ptx::mbar_init(&full[i], 1); ptx::mbar_init(&empty[i], 1); }
         for (int i = 0; i < 2; ++i) { ptx::mbar_init(&tfull[i], 1); ptx::mbar_init(&tempty[i], Traits::EPI_WARPS); }
-        for (int i = 0; i < Traits::EPI_WARPS; ++i) ptx::mbar_init(&epi_bar[i], 1);
+        for (int i = 0; i < 2 * Traits::EPI_WARPS; ++i) ptx::mbar_init(&epi_bar[i], 1);
         ptx::fence_barrier_init();
         Traits::prefetch(p);
     }
@@ -86,19 +98,28 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0) {
-        if (lane == 0) {
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-                const int nkb = Traits::kblocks(p, tile);
-                for (int kb = 0; kb < nkb; ++kb) {
+        // whole warp walks the loop (lane 0 issues); after the first tile's first STAGES loads
+        // it releases the epilogue warps' epi_begin (their TMA traffic queues behind the operands)
+        int stage = 0;
+        uint32_t phase = 0;
+        bool released = false;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            const int nkb = Traits::kblocks(p, tile);
+            for (int kb = 0; kb < nkb; ++kb) {
+                if (lane == 0) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
                     ptx::mbar_arrive_expect_tx(&full[stage], S::STAGE_BYTES);
                     Traits::load(p, tile, kb, sA + stage * S::A_BYTES, sB + stage * S::B_BYTES, &full[stage]);
-                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+                if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                if (!released && (kb + 1 == STAGES || kb + 1 == nkb)) {
+                    __syncwarp();
+                    ptx::named_arrive(1, 32 + 32 * Traits::EPI_WARPS);
+                    released = true;
                 }
             }
         }
+        if (!released) ptx::named_arrive(1, 32 + 32 * Traits::EPI_WARPS);
     } else if (warp == 1) {
         if (lane == 0) {
             constexpr uint32_t idesc = ptx::idesc_bf16_f32(kBM, BN, Traits::A_MN, Traits::B_MN);
@@ -137,13 +158,14 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
         const EpiSlot slot{(e / 4), Traits::EPI_WARPS / 4};
         int acc = 0;
         uint32_t aphase = 0, ephase = 0;
+        uint8_t* est = epi_smem + e * (Traits::EPI_WARPS ? Traits::EPI_SMEM / Traits::EPI_WARPS : 0);
+        ptx::named_sync(1, 32 + 32 * Traits::EPI_WARPS);
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            Traits::epi_begin(p, tile, q, lane, est, &epi_bar[2 * e], slot);
             ptx::mbar_wait(&tfull[acc], aphase);
             ptx::tc_fence_after();
             const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
-            Traits::epilogue(p, tile, tbase, q, lane, &tempty[acc],
-                             epi_smem + e * (Traits::EPI_WARPS ? Traits::EPI_SMEM / Traits::EPI_WARPS : 0), &epi_bar[e],
-                             ephase, slot);
+            Traits::epilogue(p, tile, tbase, q, lane, &tempty[acc], est, &epi_bar[2 * e], ephase, slot);
             if (++acc == 2) { acc = 0; aphase ^= 1; }
         }
         if (lane == 0) ptx::bulk_wait0();
@@ -184,7 +206,7 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
     uint8_t* sA = smem;
     uint8_t* sB = smem + STAGES * S::A_BYTES;
     // 1 KB barrier block: full[<=8] @0, empty[<=8] @64, tfull[2] @128, tempty[2] @144,
-    // TMEM slot @160, per-epilogue-warp barriers[<=8] @256
+    // TMEM slot @160, per-epilogue-warp barrier pairs[<=16] @256
     uint8_t* bblk = smem + STAGES * S::STAGE_BYTES;
     uint64_t* full = reinterpret_cast<uint64_t*>(bblk);
     uint64_t* empty = reinterpret_cast<uint64_t*>(bblk + 64);
@@ -204,7 +226,7 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
     if (warp == 0 && lane == 0) {
         for (int i = 0; i < STAGES; ++i) { ptx::mbar_init(&full[i], 1); ptx::mbar_init(&empty[i], 1); }
         for (int i = 0; i < 2; ++i) { ptx::mbar_init(&tfull[i], 1); ptx::mbar_init(&tempty[i], 2 * Traits::EPI_WARPS); }
-        for (int i = 0; i < Traits::EPI_WARPS; ++i) ptx::mbar_init(&epi_bar[i], 1);
+        for (int i = 0; i < 2 * Traits::EPI_WARPS; ++i) ptx::mbar_init(&epi_bar[i], 1);
         ptx::fence_barrier_init();
         Traits::prefetch(p);
     }
@@ -215,20 +237,27 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0) {
-        if (lane == 0) {
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int tile = cid; tile < num_tiles; tile += ncl) {
-                const int nkb = Traits::kblocks(p, tile);
-                for (int kb = 0; kb < nkb; ++kb) {
+        int stage = 0;
+        uint32_t phase = 0;
+        bool released = false;
+        for (int tile = cid; tile < num_tiles; tile += ncl) {
+            const int nkb = Traits::kblocks(p, tile);
+            for (int kb = 0; kb < nkb; ++kb) {
+                if (lane == 0) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
                     const uint32_t bar0 = ptx::mapa(ptx::smem_u32(&full[stage]), 0);
                     if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * S::STAGE_BYTES);
                     Traits::load2(p, tile, kb, rank, sA + stage * S::A_BYTES, sB + stage * S::B_BYTES, bar0);
-                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+                if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                if (!released && (kb + 1 == STAGES || kb + 1 == nkb)) {
+                    __syncwarp();
+                    ptx::named_arrive(1, 32 + 32 * Traits::EPI_WARPS);
+                    released = true;
                 }
             }
         }
+        if (!released) ptx::named_arrive(1, 32 + 32 * Traits::EPI_WARPS);
     } else if (warp == 1) {
         if (lane == 0 && rank == 0) {
             constexpr uint32_t idesc = ptx::idesc_bf16_f32(2 * kBM, BN, Traits::A_MN, Traits::B_MN);
@@ -273,13 +302,14 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
         int acc = 0;
         uint32_t aphase = 0, ephase = 0;
         int it = 0;
+        uint8_t* est = epi_smem + e * (Traits::EPI_WARPS ? Traits::EPI_SMEM / Traits::EPI_WARPS : 0);
+        ptx::named_sync(1, 32 + 32 * Traits::EPI_WARPS);
         for (int tile = cid; tile < num_tiles; tile += ncl, ++it) {
+            Traits::epi_begin2(p, tile, rank, q, lane, est, &epi_bar[2 * e], slot);
             ptx::mbar_wait(&tfull[acc], aphase);
             ptx::tc_fence_after();
             const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
-            Traits::epilogue2(p, tile, rank, tbase, q, lane, tempty0 + acc * 8,
-                              epi_smem + e * (Traits::EPI_WARPS ? Traits::EPI_SMEM / Traits::EPI_WARPS : 0), &epi_bar[e],
-                              ephase, slot);
+            Traits::epilogue2(p, tile, rank, tbase, q, lane, tempty0 + acc * 8, est, &epi_bar[2 * e], ephase, slot);
             if (e == 0 && lane == 0) trace(p.trace, 4 * it + 3);
             if (++acc == 2) { acc = 0; aphase ^= 1; }
         }

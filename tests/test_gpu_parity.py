@@ -68,15 +68,38 @@ def test_gradient_bf16_tensor_core_tolerance(oracle_mod, name):
     assert rel <= 5e-2
 
 
-@pytest.mark.parametrize("bidir", [True, False])
-def test_fused_lstm_kernels_match_oracle_and_unfused(oracle_mod, monkeypatch, bidir):
+@pytest.mark.parametrize("classes", [24, 264, 296, 512])
+def test_fused_softmax_ce_ragged_class_tiles(oracle_mod, classes):
+    """The fused output-GEMM + softmax-CE splits each 256-class tile into 32-column chunks over
+    two epilogue warps; class counts whose last tile leaves one warp with no valid column
+    (C % 256 <= 32) must not poison the log-sum-exp (bf16 tolerance)."""
+    O = oracle_mod
+    m = ModelDesc(layers=1, hidden=16, bidirectional=True, input_dim=20, proj=16, classes=classes, unroll=6)
+    feats, labels = _data(m)
+    M = 8
+    g = LearnerGroup(m, StrategyConfig(learners=1, batch=M, seed=1), precision=Precision.BF16)
+    g.set_dataset(feats, labels, 40)
+    rng = np.random.default_rng(5)
+    w = rng.normal(0, 0.2, g.D)
+    idx = rng.integers(0, 40, size=M).astype(np.int32)
+    loss, grad = g.gradient(w, idx)
+    g.close()
+    oloss, ograd = O.lstm_loss_grad(_odesc(O, m), w, feats, labels, idx)
+    assert np.isfinite(loss) and np.all(np.isfinite(grad))
+    assert abs(loss - oloss) <= 1e-2 * oloss
+    assert np.linalg.norm(grad - ograd) / np.linalg.norm(ograd) <= 5e-2
+
+
+@pytest.mark.parametrize("bidir,hidden,M,T", [(True, 64, 136, 9), (False, 64, 136, 9), (True, 256, 300, 5),
+                                               (False, 128, 260, 4)])
+def test_fused_lstm_kernels_match_oracle_and_unfused(oracle_mod, monkeypatch, bidir, hidden, M, T):
     """H % 64 == 0 selects the fused tcgen05 recurrent kernels (cell fwd / bwd in the GEMM
     epilogue); they must agree with the oracle (bf16 tolerance) and with the unfused
-    GEMM + pointwise path (same bf16 operands)."""
+    GEMM + pointwise path (same bf16 operands). M > 128 exercises the row mask; H % 128 == 0
+    with M > 128 selects the CTA-pair (cta_group::2) kernels, H = 256 gives several unit tiles."""
     O = oracle_mod
-    m = ModelDesc(layers=2, hidden=64, bidirectional=bidir, input_dim=40, proj=16, classes=48, unroll=9)
+    m = ModelDesc(layers=2, hidden=hidden, bidirectional=bidir, input_dim=40, proj=16, classes=48, unroll=T)
     feats, labels = _data(m)
-    M = 136  # > one 128-row tile: exercises the row mask
     rng = np.random.default_rng(3)
     idx = rng.integers(0, 40, size=M).astype(np.int32)
     grads = {}
