@@ -33,6 +33,7 @@
 namespace ab {
 
 extern bool g_use_pair_mma;  // gemm_lstm.cu
+extern bool g_use_wide_fwd;  // gemm_lstm.cu
 
 namespace {
 thread_local std::string g_last_error;
@@ -109,6 +110,7 @@ Ctx::Ctx(const adpsgd_config& c) : cfg(c) {
     if (const char* e = std::getenv("ADPSGD_NO_GRAPHS")) use_graphs = e[0] == '0';
     if (const char* e = std::getenv("ADPSGD_NO_FUSED")) use_fused_cell = e[0] == '0';
     if (const char* e = std::getenv("ADPSGD_NO_PAIR")) g_use_pair_mma = e[0] == '0';
+    if (const char* e = std::getenv("ADPSGD_NO_WIDE")) g_use_wide_fwd = e[0] == '0';
 
     AB_CUDA(cudaSetDevice(c.device));
     AB_CUDA(cudaStreamCreateWithFlags(&s_main, cudaStreamNonBlocking));

@@ -246,7 +246,7 @@ void launch_any(const Params& p, int tiles, bool pair, cudaStream_t s) {
     if (pair) {
         auto k = tc::persistent_kernel_2cta<Traits, Params>;
         static bool attr = false;
-        constexpr int SM = tc::Shape2<Traits::BN, Traits::EPI_SMEM>::SMEM;
+        constexpr int SM = tc::ShapeOf2<Traits>::SMEM;
         if (!attr) {
             AB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SM));
             attr = true;

@@ -77,12 +77,21 @@ struct FwdParams {
     unsigned long long* trace;
 };
 
-struct FwdTraits : tc::TraitsBase {
-    static constexpr int BN = 256;
-    // per warp (20 KB): c_{t-1} box (fp32 32x32, SW128) | c box | 4 gate boxes (bf16 32x32, SW64) | h box
-    static constexpr int EPI_WARP = 20 * 1024;
-    static constexpr int EPI_WARPS = 4;
+// U = hidden units per tile (x 4 gates = BN accumulator columns).
+//   U = 64:  256-column pair tiles, 2 accumulator stages, 4 epilogue warps (tiles > CTA pairs).
+//   U = 128: 512-column pair tiles (two N = 256 MMAs per k-step), one accumulator stage, 8
+//            epilogue warps whose staging overlays the (then idle) pipeline stages; used when
+//            every CTA pair owns exactly one tile (one wave, ~25% less L2->SM operand traffic).
+template <int U>
+struct FwdT : tc::TraitsBase {
+    static constexpr bool WIDE = U == 128;
+    static constexpr int BN = 4 * U;
+    static constexpr int EPI_WARP = 22 * 1024;  // see body()
+    static constexpr int EPI_WARPS = WIDE ? 8 : 4;
     static constexpr int EPI_SMEM = EPI_WARPS * EPI_WARP;
+    static constexpr int ACC_STAGES = WIDE ? 1 : 2;
+    static constexpr int MMA_N = WIDE ? 256 : 0;
+    static constexpr bool EPI_OVERLAY = WIDE;
     static constexpr bool B_MN = false;
     __device__ static int num_tiles(const FwdParams& p) { return p.ngroups * p.m_tiles * p.n_tiles; }
     __device__ static void prefetch(const FwdParams& p) {
@@ -94,7 +103,7 @@ struct FwdTraits : tc::TraitsBase {
         grp = tile / per;
         const int r = tile % per;
         m0 = (r % p.m_tiles) * kBM;
-        u0 = (r / p.m_tiles) * 64;
+        u0 = (r / p.m_tiles) * U;
     }
     __device__ static int kblocks(const FwdParams& p, int tile) {
         const FwdGroup& g = p.g[tile / (p.m_tiles * p.n_tiles)];
@@ -119,7 +128,7 @@ struct FwdTraits : tc::TraitsBase {
         grp = tile / per;
         const int r = tile % per;
         m0 = (r % p.m_tiles) * 2 * kBM;
-        u0 = (r / p.m_tiles) * 64;
+        u0 = (r / p.m_tiles) * U;
     }
     __device__ static void load2(const FwdParams& p, int tile, int kb, uint32_t rank, uint8_t* sA, uint8_t* sB,
                                  uint32_t bar) {
@@ -130,9 +139,25 @@ struct FwdTraits : tc::TraitsBase {
         const int k0 = (s == 0 ? kb : kb - g.kb0) * kBK;
         ptx::tma_load_2d_2sm_hint(sA, &g.ta[s], bar, k0, m0 + kBM * rank, ptx::policy_evict_first());
         const uint64_t keep = ptx::policy_evict_last();
+        // U = 64: CTA r holds gates {2r, 2r+1} (64 rows each) of the one N = 256 MMA.
+        // U = 128: CTA r holds gate r (sub-MMA 0 -> cols [0,256)) and gate 2+r (sub-MMA 1).
 #pragma unroll
         for (int j = 0; j < 2; ++j)
-            ptx::tma_load_2d_2sm_hint(sB + j * 64 * kBK * 2, &g.tb[s], bar, k0, (2 * rank + j) * p.H + u0, keep);
+            ptx::tma_load_2d_2sm_hint(sB + j * U * kBK * 2, &g.tb[s], bar, k0,
+                                      (WIDE ? 2 * j + static_cast<int>(rank) : 2 * static_cast<int>(rank) + j) * p.H + u0, keep);
+    }
+    // WIDE: the whole tile's c_{t-1} goes to L2 while the mainloop runs (epilogue smem is the
+    // pipeline's, so no early smem loads)
+    template <class S>
+    __device__ static void epi_begin2(const FwdParams& p, int tile, uint32_t rank, int q, int lane, uint8_t*, uint64_t*,
+                                      S sl) {
+        if (!WIDE) return;
+        int grp, m0, u0;
+        coords2(p, tile, grp, m0, u0);
+        const FwdGroup& g = p.g[grp];
+        if (g.c_prev == nullptr) return;
+        const int uc = 32 * sl.sub + 32 * sl.n * (lane & 1);
+        if (lane < 2 && uc < U) ptx::tma_prefetch_l2_2d(&g.m_cprev, u0 + uc, m0 + kBM * static_cast<int>(rank) + q * 32);
     }
     __device__ static void epilogue2(const FwdParams& p, int tile, uint32_t rank, uint32_t tbase, int q, int lane,
                                      uint32_t tempty_leader, uint8_t* st, uint64_t* ebar, uint32_t& ephase,
@@ -148,110 +173,138 @@ struct FwdTraits : tc::TraitsBase {
         coords(p, tile, grp, m0, u0);
         body(p, grp, m0, u0, tbase, q, lane, [&] { tc::release_acc(tempty, lane); }, st, ebar, ephase, sl);
     }
-    // epilogue (thread = row): per 32-unit chunk, c_{t-1} arrives by TMA into swizzled smem while
-    // the 4 gate columns leave TMEM; the cell runs in registers; gates (bf16), c (fp32) and h
-    // (bf16) are written as swizzled smem boxes and leave by TMA bulk stores (fully coalesced,
-    // asynchronous, rows >= B clipped by the tensor map).
+    // epilogue (thread = row): per 32-unit chunk, c_{t-1} arrives by TMA into swizzled smem
+    // (double-buffered: chunk j+1's load is issued when chunk j starts); the 4 gate columns
+    // leave TMEM in two 16-unit halves (bounding register pressure); the cell runs in registers;
+    // each half's gates (bf16), c (fp32) and h (bf16) are staged in one of two swizzled output
+    // sets and leave by TMA bulk stores that overlap the next half's math (rows >= B clipped).
+    // smem per warp (22 KB): c_{t-1} 2 x 4 KB | out 2 x 7 KB (c 2 KB | gates 4 x 1 KB | h 1 KB)
     template <class Rel>
     __device__ static void body(const FwdParams& p, int grp, int m0, int u0, uint32_t tbase, int q, int lane,
                                 Rel release, uint8_t* st, uint64_t* ebar, uint32_t& ephase, tc::EpiSlot sl) {
         const FwdGroup& g = p.g[grp];
         const int H = p.H;
         const int rowbase = m0 + q * 32;
-        uint8_t* cin = st;
-        uint8_t* cbox = st + 4096;
-        uint8_t* gbox = st + 8192;  // 4 x 2 KB
-        uint8_t* hbox = st + 16384;
         const bool has_prev = g.c_prev != nullptr;
+        const bool tr = q == 2 && lane == 0;
+        const int step = 32 * sl.n;
+        auto issue_cprev = [&](int uc, int b) {
+            ptx::mbar_arrive_expect_tx(ebar + b, 32 * 32 * 4);
+            ptx::tma_load_2d(st + b * 4096, &g.m_cprev, ebar + b, u0 + uc, rowbase);
+        };
+        if (has_prev && lane == 0) issue_cprev(32 * sl.sub, 0);
+        int ob = 0;
+        int cb = 0;
 #pragma unroll 1
-        for (int uc = 32 * sl.sub; uc < 64; uc += 32 * sl.n) {
+        for (int uc = 32 * sl.sub; uc < U; uc += step, cb ^= 1) {
             const int j0 = u0 + uc;
-            if (has_prev && lane == 0) {
-                ptx::mbar_arrive_expect_tx(ebar, 32 * 32 * 4);
-                ptx::tma_load_2d(cin, &g.m_cprev, ebar, j0, rowbase);
-            }
-            uint32_t zi[32], zf[32], zg[32], zo[32];
-            ptx::tmem_ld_32x32b_x32(tbase + 0 * 64 + uc, zi);
-            ptx::tmem_ld_32x32b_x32(tbase + 1 * 64 + uc, zf);
-            ptx::tmem_ld_32x32b_x32(tbase + 2 * 64 + uc, zg);
-            ptx::tmem_ld_32x32b_x32(tbase + 3 * 64 + uc, zo);
-            ptx::tmem_ld_wait();
-            const bool tr = q == 2 && lane == 0;
+            if (has_prev && lane == 0 && uc + step < U) issue_cprev(uc + step, cb ^ 1);
             if (tr) tc::trace_once(p.trace, 12 + (uc / 32) * 4 + 0);
-            if (uc + 32 * sl.n >= 64) release();
-            float cp[32];
-            if (has_prev) {
-                ptx::mbar_wait(ebar, ephase);
-                ephase ^= 1;
-                tc::ld_row_f32_sw128(cin, lane, cp);
-            } else {
+            const uint8_t* cin = st + cb * 4096;
 #pragma unroll
-                for (int i = 0; i < 32; ++i) cp[i] = 0.f;
+            for (int h = 0; h < 2; ++h, ob ^= 1) {
+                const int c16 = uc + 16 * h;  // first unit of this half (tile-relative)
+                uint32_t zi[16], zf[16], zg[16], zo[16];
+                ptx::tmem_ld_32x32b_x16_(tbase + 0 * U + c16, zi);
+                ptx::tmem_ld_32x32b_x16_(tbase + 1 * U + c16, zf);
+                ptx::tmem_ld_32x32b_x16_(tbase + 2 * U + c16, zg);
+                ptx::tmem_ld_32x32b_x16_(tbase + 3 * U + c16, zo);
+                ptx::tmem_ld_wait();
+                if (h == 1 && uc + step >= U) release();
+                float cp[16];
+                if (has_prev) {
+                    if (h == 0) {
+                        ptx::mbar_wait(ebar + cb, (ephase >> cb) & 1u);
+                        ephase ^= 1u << cb;
+                    }
+                    tc::ld_half_f32_sw128(cin, lane, h, cp);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) cp[i] = 0.f;
+                }
+                if (tr && h == 0) tc::trace_once(p.trace, 12 + (uc / 32) * 4 + 1);
+                uint8_t* out = st + 8192 + ob * 7168;
+                // the store that last used this output set (two halves ago) has read it
+                if (lane == 0) ptx::bulk_wait_read1();
+                __syncwarp();
+                const int jb = j0 + 16 * h;
+                float a[16], gv[16];
+                uint32_t w[8];
+                // i
+#pragma unroll
+                for (int i = 0; i < 16; i += 4) {
+                    const float4 b4 = __ldg(reinterpret_cast<const float4*>(g.bias + jb + i));
+                    a[i] = sigf(__uint_as_float(zi[i]) + b4.x); a[i + 1] = sigf(__uint_as_float(zi[i + 1]) + b4.y);
+                    a[i + 2] = sigf(__uint_as_float(zi[i + 2]) + b4.z); a[i + 3] = sigf(__uint_as_float(zi[i + 3]) + b4.w);
+                }
+#pragma unroll
+                for (int i = 0; i < 8; ++i) w[i] = tc::pack_bf16x2(a[2 * i], a[2 * i + 1]);
+                tc::st_row_words<32>(out + 2048 + 0 * 1024, lane, w);
+                // g, and i*g (c_t = f c_{t-1} + i g, accumulated in two parts)
+#pragma unroll
+                for (int i = 0; i < 16; i += 4) {
+                    const float4 b4 = __ldg(reinterpret_cast<const float4*>(g.bias + 2 * H + jb + i));
+                    gv[i] = tanhf_fast(__uint_as_float(zg[i]) + b4.x);
+                    gv[i + 1] = tanhf_fast(__uint_as_float(zg[i + 1]) + b4.y);
+                    gv[i + 2] = tanhf_fast(__uint_as_float(zg[i + 2]) + b4.z);
+                    gv[i + 3] = tanhf_fast(__uint_as_float(zg[i + 3]) + b4.w);
+                }
+#pragma unroll
+                for (int i = 0; i < 8; ++i) w[i] = tc::pack_bf16x2(gv[2 * i], gv[2 * i + 1]);
+                tc::st_row_words<32>(out + 2048 + 2 * 1024, lane, w);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) gv[i] *= a[i];  // i * g
+                // f
+#pragma unroll
+                for (int i = 0; i < 16; i += 4) {
+                    const float4 b4 = __ldg(reinterpret_cast<const float4*>(g.bias + H + jb + i));
+                    a[i] = sigf(__uint_as_float(zf[i]) + b4.x); a[i + 1] = sigf(__uint_as_float(zf[i + 1]) + b4.y);
+                    a[i + 2] = sigf(__uint_as_float(zf[i + 2]) + b4.z); a[i + 3] = sigf(__uint_as_float(zf[i + 3]) + b4.w);
+                }
+#pragma unroll
+                for (int i = 0; i < 8; ++i) w[i] = tc::pack_bf16x2(a[2 * i], a[2 * i + 1]);
+                tc::st_row_words<32>(out + 2048 + 1 * 1024, lane, w);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) cp[i] = a[i] * cp[i] + gv[i];  // c_t
+                {
+                    uint32_t cw[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) cw[i] = __float_as_uint(cp[i]);
+                    tc::st_row_words<64>(out, lane, cw);
+                }
+                // o, h
+#pragma unroll
+                for (int i = 0; i < 16; i += 4) {
+                    const float4 b4 = __ldg(reinterpret_cast<const float4*>(g.bias + 3 * H + jb + i));
+                    a[i] = sigf(__uint_as_float(zo[i]) + b4.x); a[i + 1] = sigf(__uint_as_float(zo[i + 1]) + b4.y);
+                    a[i + 2] = sigf(__uint_as_float(zo[i + 2]) + b4.z); a[i + 3] = sigf(__uint_as_float(zo[i + 3]) + b4.w);
+                }
+#pragma unroll
+                for (int i = 0; i < 8; ++i) w[i] = tc::pack_bf16x2(a[2 * i], a[2 * i + 1]);
+                tc::st_row_words<32>(out + 2048 + 3 * 1024, lane, w);
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    w[i] = tc::pack_bf16x2(a[2 * i] * tanhf_fast(cp[2 * i]), a[2 * i + 1] * tanhf_fast(cp[2 * i + 1]));
+                tc::st_row_words<32>(out + 6144, lane, w);
+                ptx::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    const uint64_t stream = ptx::policy_evict_first();
+#pragma unroll
+                    for (int gi = 0; gi < 4; ++gi)
+                        ptx::tma_store_2d_hint(&g.m_gates, out + 2048 + gi * 1024, gi * H + jb, rowbase, stream);
+                    ptx::tma_store_2d(&g.m_c, out, jb, rowbase);
+                    ptx::tma_store_2d(&g.m_h, out + 6144, jb, rowbase);
+                    ptx::bulk_commit();
+                }
             }
-            if (tr) tc::trace_once(p.trace, 12 + (uc / 32) * 4 + 1);
-            if (p.epi_skip) continue;
-            float a[32];
-            // i
-#pragma unroll
-            for (int i = 0; i < 32; i += 4) {
-                const float4 b4 = __ldg(reinterpret_cast<const float4*>(g.bias + j0 + i));
-                a[i] = sigf(__uint_as_float(zi[i]) + b4.x); a[i + 1] = sigf(__uint_as_float(zi[i + 1]) + b4.y);
-                a[i + 2] = sigf(__uint_as_float(zi[i + 2]) + b4.z); a[i + 3] = sigf(__uint_as_float(zi[i + 3]) + b4.w);
-            }
-            tc::st_row_bf16_sw64(gbox + 0 * 2048, lane, a);
-            // g, and i*g into cp (c_t = f c_{t-1} + i g, accumulated in two parts)
-            float gv[32];
-#pragma unroll
-            for (int i = 0; i < 32; i += 4) {
-                const float4 b4 = __ldg(reinterpret_cast<const float4*>(g.bias + 2 * H + j0 + i));
-                gv[i] = tanhf_fast(__uint_as_float(zg[i]) + b4.x);
-                gv[i + 1] = tanhf_fast(__uint_as_float(zg[i + 1]) + b4.y);
-                gv[i + 2] = tanhf_fast(__uint_as_float(zg[i + 2]) + b4.z);
-                gv[i + 3] = tanhf_fast(__uint_as_float(zg[i + 3]) + b4.w);
-            }
-            tc::st_row_bf16_sw64(gbox + 2 * 2048, lane, gv);
-#pragma unroll
-            for (int i = 0; i < 32; ++i) gv[i] *= a[i];  // i * g
-            // f
-#pragma unroll
-            for (int i = 0; i < 32; i += 4) {
-                const float4 b4 = __ldg(reinterpret_cast<const float4*>(g.bias + H + j0 + i));
-                a[i] = sigf(__uint_as_float(zf[i]) + b4.x); a[i + 1] = sigf(__uint_as_float(zf[i + 1]) + b4.y);
-                a[i + 2] = sigf(__uint_as_float(zf[i + 2]) + b4.z); a[i + 3] = sigf(__uint_as_float(zf[i + 3]) + b4.w);
-            }
-            tc::st_row_bf16_sw64(gbox + 1 * 2048, lane, a);
-#pragma unroll
-            for (int i = 0; i < 32; ++i) cp[i] = a[i] * cp[i] + gv[i];  // c_t
-            tc::st_row_f32_sw128(cbox, lane, cp);
-            // o, h
-#pragma unroll
-            for (int i = 0; i < 32; i += 4) {
-                const float4 b4 = __ldg(reinterpret_cast<const float4*>(g.bias + 3 * H + j0 + i));
-                a[i] = sigf(__uint_as_float(zo[i]) + b4.x); a[i + 1] = sigf(__uint_as_float(zo[i + 1]) + b4.y);
-                a[i + 2] = sigf(__uint_as_float(zo[i + 2]) + b4.z); a[i + 3] = sigf(__uint_as_float(zo[i + 3]) + b4.w);
-            }
-            tc::st_row_bf16_sw64(gbox + 3 * 2048, lane, a);
-#pragma unroll
-            for (int i = 0; i < 32; ++i) a[i] *= tanhf_fast(cp[i]);
-            tc::st_row_bf16_sw64(hbox, lane, a);
             if (tr) tc::trace_once(p.trace, 12 + (uc / 32) * 4 + 2);
-            ptx::fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-#pragma unroll
-                const uint64_t stream = ptx::policy_evict_first();
-                for (int gi = 0; gi < 4; ++gi)
-                    ptx::tma_store_2d_hint(&g.m_gates, gbox + gi * 2048, gi * H + j0, rowbase, stream);
-                ptx::tma_store_2d(&g.m_c, cbox, j0, rowbase);
-                ptx::tma_store_2d(&g.m_h, hbox, j0, rowbase);
-                ptx::bulk_commit();
-                ptx::bulk_wait_read0();  // staging boxes reusable by the next chunk
-            }
-            if (tr) tc::trace_once(p.trace, 12 + (uc / 32) * 4 + 3);
-            __syncwarp();
         }
     }
 };
+
+using FwdTraits = FwdT<64>;
+using FwdWideTraits = FwdT<128>;
 
 // ---------------- backward ----------------
 struct BwdGroup {
@@ -493,7 +546,7 @@ void launch_pair(const Params& p, int pair_tiles, cudaStream_t s) {
     auto k = tc::persistent_kernel_2cta<Traits, Params>;
     static bool attr = false;
     if (!attr) {
-        AB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::Shape2<Traits::BN, Traits::EPI_SMEM>::SMEM));
+        AB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::ShapeOf2<Traits>::SMEM));
         attr = true;
     }
     int pairs = num_sms() / 2;
@@ -501,7 +554,7 @@ void launch_pair(const Params& p, int pair_tiles, cudaStream_t s) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * pairs);
     cfg.blockDim = dim3(tc::threads_of<Traits>());
-    cfg.dynamicSmemBytes = tc::Shape2<Traits::BN, Traits::EPI_SMEM>::SMEM;
+    cfg.dynamicSmemBytes = tc::ShapeOf2<Traits>::SMEM;
     cfg.stream = s;
     cudaLaunchAttribute attrs[1];
     attrs[0].id = cudaLaunchAttributeClusterDimension;
@@ -517,32 +570,39 @@ void launch_pair(const Params& p, int pair_tiles, cudaStream_t s) {
 }  // namespace
 
 bool g_use_pair_mma = true;
+bool g_use_wide_fwd = true;
 
 void lstm_fwd_step(const LstmFwdDir* dirs, int ndirs, int B, int H, int ldg, int ldc, int ldh, cudaStream_t s) {
     AB_CHECK(H % 64 == 0 && ndirs >= 1 && ndirs <= 2, ADPSGD_E_DIMENSION, "fused LSTM step needs H % 64 == 0");
     FwdParams p;
     std::memset(&p, 0, sizeof(p));
+    const bool pair = g_use_pair_mma && B > kBM;
+    // one wave of 256 x 512 pair tiles when every CTA pair gets exactly one tile
+    const bool wide = pair && g_use_wide_fwd && H % 128 == 0 &&
+                      ndirs * ((B + 2 * kBM - 1) / (2 * kBM)) * (H / 128) <= num_sms() / 2;
+    const uint32_t wbox = wide ? 128 : 64;
     double flops = 0, bytes = 0;
     for (int d = 0; d < ndirs; ++d) {
         const LstmFwdDir& a = dirs[d];
         FwdGroup& g = p.g[d];
         make_map_box(&g.ta[0], a.x, a.Kx, B, a.ldx, kBM);
-        make_map_box(&g.tb[0], a.w_ih, a.Kx, 4 * H, a.ld_wih, 64);
+        make_map_box(&g.tb[0], a.w_ih, a.Kx, 4 * H, a.ld_wih, wbox);
         g.kb0 = (a.Kx + kBK - 1) / kBK;
         g.nseg = 1;
         double K = a.Kx;
         if (a.h_prev) {
             make_map_box(&g.ta[1], a.h_prev, H, B, a.ld_hprev, kBM);
-            make_map_box(&g.tb[1], a.w_hh, H, 4 * H, H, 64);
+            make_map_box(&g.tb[1], a.w_hh, H, 4 * H, H, wbox);
             g.kb1 = (H + kBK - 1) / kBK;
             g.nseg = 2;
             K += H;
         }
         g.bias = a.bias; g.c_prev = a.c_prev; g.gates = a.gates; g.c = a.c; g.h = a.h;
         if (a.c_prev) make_map_gen(&g.m_cprev, a.c_prev, true, H, B, ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
-        make_map_gen(&g.m_gates, a.gates, false, 4 * H, B, ldg, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
-        make_map_gen(&g.m_c, a.c, true, H, B, ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
-        make_map_gen(&g.m_h, a.h, false, H, B, ldh, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+        // epilogue stores: 16-unit x 32-row half boxes
+        make_map_gen(&g.m_gates, a.gates, false, 4 * H, B, ldg, 16, 32, CU_TENSOR_MAP_SWIZZLE_32B);
+        make_map_gen(&g.m_c, a.c, true, H, B, ldc, 16, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+        make_map_gen(&g.m_h, a.h, false, H, B, ldh, 16, 32, CU_TENSOR_MAP_SWIZZLE_32B);
         flops += 2.0 * B * 4.0 * H * K;
         bytes += 2.0 * (B + 4.0 * H) * K + B * H * (8.0 + 4 + 2 + (a.c_prev ? 4 : 0));
     }
@@ -550,9 +610,12 @@ void lstm_fwd_step(const LstmFwdDir* dirs, int ndirs, int B, int H, int ldg, int
     static const int skip = std::getenv("ADPSGD_EPI_SKIP") ? std::atoi(std::getenv("ADPSGD_EPI_SKIP")) : 0;
     p.epi_skip = skip;
     p.trace = trace_take();
-    p.n_tiles = H / 64;
+    p.n_tiles = H / (wide ? 128 : 64);
     ProfScope ps_(s, PROF_GEMM_REC_FWD, flops, bytes);
-    if (g_use_pair_mma && B > kBM) {
+    if (wide) {
+        p.m_tiles = (B + 2 * kBM - 1) / (2 * kBM);
+        launch_pair<FwdWideTraits>(p, ndirs * p.m_tiles * p.n_tiles, s);
+    } else if (pair) {
         p.m_tiles = (B + 2 * kBM - 1) / (2 * kBM);
         launch_pair<FwdTraits>(p, ndirs * p.m_tiles * p.n_tiles, s);
     } else {

@@ -251,7 +251,7 @@ void launch_pair(const TcParams& p, cudaStream_t s) {
     auto k = tc::persistent_kernel_2cta<Traits, TcParams>;
     static bool attr = false;
     if (!attr) {
-        AB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::Shape2<Traits::BN, Traits::EPI_SMEM>::SMEM));
+        AB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::ShapeOf2<Traits>::SMEM));
         attr = true;
     }
     const int tiles = p.m_tiles * p.n_tiles;
@@ -259,7 +259,7 @@ void launch_pair(const TcParams& p, cudaStream_t s) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * pairs);
     cfg.blockDim = dim3(tc::threads_of<Traits>());
-    cfg.dynamicSmemBytes = tc::Shape2<Traits::BN, Traits::EPI_SMEM>::SMEM;
+    cfg.dynamicSmemBytes = tc::ShapeOf2<Traits>::SMEM;
     cfg.stream = s;
     cudaLaunchAttribute attrs[1];
     attrs[0].id = cudaLaunchAttributeClusterDimension;

@@ -40,6 +40,9 @@ constexpr int kSmemBudget = 225 * 1024;
 // loaded or L2-prefetched there, overlapping the mainloop. Each epilogue warp owns two
 // mbarriers (ebar[0], ebar[1]) and the bits of ephase.
 struct TraitsBase {
+    static constexpr int ACC_STAGES = 2;      // TMEM accumulator stages (ACC_STAGES * BN <= 512 columns)
+    static constexpr int MMA_N = 0;           // N of one MMA instruction (0: = BN); BN / MMA_N MMAs per k-step
+    static constexpr bool EPI_OVERLAY = false; // epilogue smem overlays the pipeline stages (one tile per CTA only)
     template <class P, class S>
     __device__ static void epi_begin(const P&, int, int, int, uint8_t*, uint64_t*, S) {}
     template <class P, class S>
@@ -184,23 +187,31 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
 // Traits: BN, B_MN, num_tiles (pair tiles), kblocks, prefetch,
 //         load2(p, tile, kb, rank, sA, sB, bar_cluster_addr), epilogue2(p, tile, rank, tbase, q, lane, tempty_leader)
 // ---------------------------------------------------------------------------
-template <int BN, int EPI = 0>
+template <int BN, int EPI = 0, bool OVERLAY = false, int ACC = 2>
 struct Shape2 {
     static constexpr int BNH = BN / 2;  // B rows held per CTA
     static constexpr int A_BYTES = kBM * kBK * 2;
     static constexpr int B_BYTES = BNH * kBK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int FIT = (kSmemBudget - EPI - 2048) / STAGE_BYTES;
+    static constexpr int FIT = (kSmemBudget - (OVERLAY ? 0 : EPI) - 2048) / STAGE_BYTES;
     static constexpr int STAGES = FIT > 8 ? 8 : FIT;
-    static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
-    static constexpr int SMEM = STAGES * STAGE_BYTES + EPI + 2048;
+    static constexpr int TMEM_COLS = ACC * BN < 32 ? 32 : ACC * BN;
+    static constexpr int SMEM = STAGES * STAGE_BYTES + (OVERLAY ? 0 : EPI) + 2048;
+    static_assert(!OVERLAY || EPI <= STAGES * STAGE_BYTES, "overlaid epilogue smem must fit in the stages");
+    static_assert(ACC * BN <= 512, "TMEM has 512 columns");
 };
+template <class T>
+using ShapeOf2 = Shape2<T::BN, T::EPI_SMEM, T::EPI_OVERLAY, T::ACC_STAGES>;
 
 template <class Traits, class Params>
 __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_kernel_2cta(const __grid_constant__ Params p) {
     constexpr int BN = Traits::BN;
-    using S = Shape2<BN, Traits::EPI_SMEM>;
+    using S = ShapeOf2<Traits>;
     constexpr int STAGES = S::STAGES;
+    constexpr int ACC = Traits::ACC_STAGES;
+    constexpr int MN = Traits::MMA_N ? Traits::MMA_N : BN;  // N per MMA instruction
+    constexpr int NSUB = BN / MN;                             // MMAs per k-step (B sub-tiles of MN/2 rows per CTA)
+    static_assert(NSUB == 1 || !Traits::B_MN, "split MMA-N needs a K-major B");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
@@ -214,7 +225,7 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
     uint64_t* tempty = reinterpret_cast<uint64_t*>(bblk + 144);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bblk + 160);
     uint64_t* epi_bar = reinterpret_cast<uint64_t*>(bblk + 256);
-    uint8_t* epi_smem = bblk + 1024;  // 1024-aligned (TMA swizzle atoms)
+    uint8_t* epi_smem = Traits::EPI_OVERLAY ? smem : bblk + 1024;  // 1024-aligned (TMA swizzle atoms)
     static_assert(STAGES <= 8 && Traits::EPI_WARPS <= 8, "barrier block layout");
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -260,7 +271,7 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
         if (!released) ptx::named_arrive(1, 32 + 32 * Traits::EPI_WARPS);
     } else if (warp == 1) {
         if (lane == 0 && rank == 0) {
-            constexpr uint32_t idesc = ptx::idesc_bf16_f32(2 * kBM, BN, Traits::A_MN, Traits::B_MN);
+            constexpr uint32_t idesc = ptx::idesc_bf16_f32(2 * kBM, MN, Traits::A_MN, Traits::B_MN);
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
@@ -284,14 +295,19 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
                                                          : ptx::umma_desc_sw128(a_addr + kk * 32, 16, 1024);
                         const uint64_t bd = Traits::B_MN ? ptx::umma_desc_sw128(b_addr + kk * 2048, 64 * kBK * 2, 1024)
                                                          : ptx::umma_desc_sw128(b_addr + kk * 32, 16, 1024);
-                        ptx::mma_bf16_2sm(tmem_d, ad, bd, idesc, (kb | kk) != 0);
+#pragma unroll
+                        for (int sub = 0; sub < NSUB; ++sub) {
+                            // sub-MMA sub: B rows [sub MN/2, +MN/2) of this CTA's stage -> TMEM cols [sub MN, +MN)
+                            const uint64_t bds = bd + static_cast<uint64_t>((sub * (MN / 2) * kBK * 2) >> 4);
+                            ptx::mma_bf16_2sm(tmem_d + sub * MN, ad, bds, idesc, (kb | kk) != 0);
+                        }
                     }
                     ptx::mma_commit_2sm(&empty[stage]);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
                 ptx::mma_commit_2sm(&tfull[acc]);
                 trace(p.trace, 4 * it + 2);
-                if (++acc == 2) { acc = 0; aphase ^= 1; }
+                if (++acc == ACC) { acc = 0; aphase ^= 1; }
             }
         }
     } else {
@@ -311,7 +327,7 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
             const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
             Traits::epilogue2(p, tile, rank, tbase, q, lane, tempty0 + acc * 8, est, &epi_bar[2 * e], ephase, slot);
             if (e == 0 && lane == 0) trace(p.trace, 4 * it + 3);
-            if (++acc == 2) { acc = 0; aphase ^= 1; }
+            if (++acc == ACC) { acc = 0; aphase ^= 1; }
         }
         if (lane == 0) ptx::bulk_wait0();
     }
@@ -368,6 +384,37 @@ __device__ __forceinline__ void st_row_bf16_sw64(uint8_t* box, int row, const fl
             w[k] = *reinterpret_cast<uint32_t*>(&b2);
         }
         ptx::st_shared_v4(base + ((c ^ ((row >> 1) & 3)) << 4), w[0], w[1], w[2], w[3]);
+    }
+}
+
+// Half rows (16 values) of the 32-value swizzled rows above: half h = chunks [h*n, (h+1)*n).
+__device__ __forceinline__ void st_half_bf16_sw64(uint8_t* box, int row, int h, const float* v) {
+    const uint32_t base = ptx::smem_u32(box) + row * 64;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int c = 2 * h + k;
+        uint32_t w[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            __nv_bfloat162 b2 = __floats2bfloat162_rn(v[8 * k + 2 * j], v[8 * k + 2 * j + 1]);
+            w[j] = *reinterpret_cast<uint32_t*>(&b2);
+        }
+        ptx::st_shared_v4(base + ((c ^ ((row >> 1) & 3)) << 4), w[0], w[1], w[2], w[3]);
+    }
+}
+__device__ __forceinline__ void st_half_f32_sw128(uint8_t* box, int row, int h, const float* v) {
+    const uint32_t base = ptx::smem_u32(box) + row * 128;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        ptx::st_shared_v4(base + (((4 * h + k) ^ (row & 7)) << 4), __float_as_uint(v[4 * k]), __float_as_uint(v[4 * k + 1]),
+                          __float_as_uint(v[4 * k + 2]), __float_as_uint(v[4 * k + 3]));
+}
+__device__ __forceinline__ void ld_half_f32_sw128(const uint8_t* box, int row, int h, float* v) {
+    const uint32_t base = ptx::smem_u32(box) + row * 128;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const float4 f = ptx::ld_shared_v4f(base + (((4 * h + k) ^ (row & 7)) << 4));
+        v[4 * k] = f.x; v[4 * k + 1] = f.y; v[4 * k + 2] = f.z; v[4 * k + 3] = f.w;
     }
 }
 
