@@ -34,6 +34,7 @@ namespace ab {
 
 extern bool g_use_pair_mma;  // gemm_lstm.cu
 extern bool g_use_wide_fwd;  // gemm_lstm.cu
+extern bool g_use_splitk_bwd;  // gemm_lstm.cu
 
 namespace {
 thread_local std::string g_last_error;
@@ -111,6 +112,7 @@ Ctx::Ctx(const adpsgd_config& c) : cfg(c) {
     if (const char* e = std::getenv("ADPSGD_NO_FUSED")) use_fused_cell = e[0] == '0';
     if (const char* e = std::getenv("ADPSGD_NO_PAIR")) g_use_pair_mma = e[0] == '0';
     if (const char* e = std::getenv("ADPSGD_NO_WIDE")) g_use_wide_fwd = e[0] == '0';
+    if (const char* e = std::getenv("ADPSGD_NO_SPLITK")) g_use_splitk_bwd = e[0] == '0';
 
     AB_CUDA(cudaSetDevice(c.device));
     AB_CUDA(cudaStreamCreateWithFlags(&s_main, cudaStreamNonBlocking));
@@ -144,6 +146,12 @@ Ctx::Ctx(const adpsgd_config& c) : cfg(c) {
         ce_part = static_cast<float2*>(alloc(ce_part_elems(static_cast<int>(TB), lay.C) * sizeof(float2)));
         ce_zlab = static_cast<float*>(alloc(TB * sizeof(float)));
         ce_lse = static_cast<float*>(alloc(TB * sizeof(float)));
+        if (H % 256 == 0) {
+            const int64_t slots = lstm_bwd_splitk_slots(nd, B, H);
+            sk_scratch = static_cast<float*>(alloc(static_cast<size_t>(slots) * 128 * 128 * sizeof(float)));
+            sk_flags = static_cast<unsigned int*>(alloc(static_cast<size_t>(slots) * sizeof(unsigned int)));
+            AB_CUDA(cudaMemsetAsync(sk_flags, 0, static_cast<size_t>(slots) * sizeof(unsigned int), s_main));
+        }
     } else {
         logits = static_cast<float*>(alloc(TB * lay.C * sizeof(float)));
     }
@@ -455,7 +463,7 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
                     a.c_prev = sn > 0 ? cst[l] + static_cast<int64_t>(tnp) * B * ndH + d * H : nullptr;
                     a.dz_dst = static_cast<bf16*>(off_ptr(dZ, static_cast<int64_t>(tn) * B * nd4H + d * G4, es));
                 }
-                lstm_bwd_step(dirs, nd, B, H, ndH, nd4H, ndH, nd4H, s);
+                lstm_bwd_step(dirs, nd, B, H, ndH, nd4H, ndH, nd4H, s, sk_scratch, sk_flags);
             }
         } else
         for (int st = 0; st < T; ++st) {

@@ -70,6 +70,8 @@ struct Ctx {
     float2* ce_part = nullptr;      // bf16 mode: fused CE scratch
     float* ce_zlab = nullptr;
     float* ce_lse = nullptr;
+    float* sk_scratch = nullptr;      // split-K BPTT partial exchange (gemm_lstm.cu)
+    unsigned int* sk_flags = nullptr;
     void* dlogits = nullptr;
     float* row_loss = nullptr;
     float *dHa = nullptr, *dHb = nullptr;

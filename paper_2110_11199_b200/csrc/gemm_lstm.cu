@@ -324,10 +324,167 @@ struct BwdParams {
     int ngroups, m_tiles, n_tiles, B, H, lddh, ldg, ldc, lddz;
     int epi_skip;  // debug: timing experiments only
     unsigned long long* trace;
+    float* sk_scratch;        // split-K partial exchange (BwdSplitTraits)
+    unsigned int* sk_flags;   // split-K epoch counters, one per CTA slot (zeroed once)
+};
+
+// BPTT cell-backward epilogue shared by the plain and the split-K recurrent dgrad kernels.
+struct BwdEpi {
+    // The epilogue inputs (dH, dc_rec, c, c_{t-1}, gates) do not depend on the GEMM: epi_begin
+    // issues the TMA loads of this warp's first two 16-unit chunks into smem and L2-prefetches
+    // the rest while the mainloop runs; body then consumes chunk c from buffer c&1 and refills
+    // that buffer with chunk c+2 (two chunks in flight per warp).
+    static constexpr int IN_BYTES = 12 * 1024;
+    __device__ static void issue(const BwdGroup& g, int H, int j0, int rowbase, uint8_t* in, uint64_t* bar) {
+        const bool has_prev = g.c_prev != nullptr;
+        ptx::mbar_arrive_expect_tx(bar, (has_prev ? 4 : 3) * 2048 + 4 * 1024);
+        const uint64_t stream = ptx::policy_evict_first();
+        ptx::tma_load_2d_hint(in, &g.m_dH, bar, j0, rowbase, stream);
+        ptx::tma_load_2d(in + 2048, &g.m_dc, bar, j0, rowbase);
+        ptx::tma_load_2d_hint(in + 4096, &g.m_c, bar, j0, rowbase, stream);
+        if (has_prev) ptx::tma_load_2d_hint(in + 6144, &g.m_cp, bar, j0, rowbase, stream);
+#pragma unroll
+        for (int gi = 0; gi < 4; ++gi) ptx::tma_load_2d_hint(in + 8192 + gi * 1024, &g.m_gates, bar, gi * H + j0, rowbase, stream);
+    }
+    // SMEM: issue the first two chunks into the warp's staging smem (not with an overlaid
+    // epilogue: the stages are busy during the mainloop) and L2-prefetch the rest; else
+    // L2-prefetch every chunk and let body() issue the first two.
+    template <int SPAN, bool SMEM = true>
+    __device__ static void begin(const BwdParams& p, int grp, int m0, int u0, int q, int lane, uint8_t* st, uint64_t* ebar,
+                                 tc::EpiSlot sl) {
+        const BwdGroup& g = p.g[grp];
+        const int rowbase = m0 + q * 32;
+        const int step = 16 * sl.n;
+        if (SMEM && lane == 0) {
+            int b = 0;
+            for (int uc = 16 * sl.sub; uc < SPAN && b < 2; uc += step, ++b) issue(g, p.H, u0 + uc, rowbase, st + b * IN_BYTES, ebar + b);
+        }
+        // L2 prefetch of the remaining chunks: one box per lane
+        const bool has_prev = g.c_prev != nullptr;
+        for (int uc = 16 * sl.sub + (SMEM ? 2 * step : 0), i = 0; uc < SPAN; uc += step, ++i) {
+            const int j0 = u0 + uc;
+            const int box = lane & 7;
+            if ((lane >> 3) != (i & 3)) continue;
+            if (box == 0) ptx::tma_prefetch_l2_2d(&g.m_dH, j0, rowbase);
+            else if (box == 1) ptx::tma_prefetch_l2_2d(&g.m_dc, j0, rowbase);
+            else if (box == 2) ptx::tma_prefetch_l2_2d(&g.m_c, j0, rowbase);
+            else if (box == 3) { if (has_prev) ptx::tma_prefetch_l2_2d(&g.m_cp, j0, rowbase); }
+            else ptx::tma_prefetch_l2_2d(&g.m_gates, (box - 4) * p.H + j0, rowbase);
+        }
+    }
+    // epilogue (thread = row), per 16-unit chunk: dh_rec leaves TMEM; the cell backward runs in
+    // registers on the chunk's prefetched inputs; dz (4 x bf16) and dc_rec leave by TMA stores.
+    // peer (split-K only): the partner CTA's fp32 partial of this CTA's units, [chunk][row][16]
+    // INPLACE: outputs are staged in the consumed input buffer (24 KB per warp instead of 30);
+    // the buffer is refilled with chunk c+2 once the chunk's stores have read it.
+    template <int SPAN, bool INPLACE = false, class Rel>
+    __device__ static void body(const BwdParams& p, int grp, int m0, int u0, uint32_t tbase, int q, int lane,
+                                Rel release, uint8_t* st, uint64_t* ebar, uint32_t& ephase, tc::EpiSlot sl,
+                                const float* peer, bool preissued = true) {
+        const BwdGroup& g = p.g[grp];
+        const int H = p.H;
+        const int rowbase = m0 + q * 32;
+        uint8_t* bdz = st + 2 * IN_BYTES;         // 4 x 1 KB (INPLACE: in the chunk's input buffer)
+        uint8_t* bdco = st + 2 * IN_BYTES + 4096;  // 2 KB
+        const bool has_prev = g.c_prev != nullptr;
+        const int step = 16 * sl.n;
+        if (!preissued && lane == 0) {
+            int bb = 0;
+            for (int uc = 16 * sl.sub; uc < SPAN && bb < 2; uc += step, ++bb) issue(g, H, u0 + uc, rowbase, st + bb * IN_BYTES, ebar + bb);
+        }
+        int b = 0;
+#pragma unroll 1
+        for (int uc = 16 * sl.sub; uc < SPAN; uc += step, b ^= 1) {
+            const int j0 = u0 + uc;
+            uint8_t* in = st + b * IN_BYTES;
+            uint32_t acc[16];
+            ptx::tmem_ld_32x32b_x16_(tbase + uc, acc);
+            ptx::tmem_ld_wait();
+            if (uc + step >= SPAN) release();
+            if (peer) {
+                const float4* pp = reinterpret_cast<const float4*>(peer + ((uc / 16) * 128 + q * 32 + lane) * 16);
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    const float4 f = __ldcg(pp + v);
+                    acc[4 * v] = __float_as_uint(__uint_as_float(acc[4 * v]) + f.x);
+                    acc[4 * v + 1] = __float_as_uint(__uint_as_float(acc[4 * v + 1]) + f.y);
+                    acc[4 * v + 2] = __float_as_uint(__uint_as_float(acc[4 * v + 2]) + f.z);
+                    acc[4 * v + 3] = __float_as_uint(__uint_as_float(acc[4 * v + 3]) + f.w);
+                }
+            }
+            ptx::mbar_wait(ebar + b, (ephase >> b) & 1u);
+            ephase ^= 1u << b;
+            uint32_t wdh[16], wdc[16], wc[16], wcp[16], wi[8], wf[8], wg[8], wo[8];
+            tc::ld_row_words<64>(in, lane, wdh);
+            tc::ld_row_words<64>(in + 2048, lane, wdc);
+            tc::ld_row_words<64>(in + 4096, lane, wc);
+            if (has_prev) tc::ld_row_words<64>(in + 6144, lane, wcp);
+            tc::ld_row_words<32>(in + 8192 + 0 * 1024, lane, wi);
+            tc::ld_row_words<32>(in + 8192 + 1 * 1024, lane, wf);
+            tc::ld_row_words<32>(in + 8192 + 2 * 1024, lane, wg);
+            tc::ld_row_words<32>(in + 8192 + 3 * 1024, lane, wo);
+            uint32_t zi[8], zf[8], zg[8], zo[8], dco[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+                const int w = e >> 1;
+                const bool hi = e & 1;
+                const float ig = hi ? tc::bf16_hi(wi[w]) : tc::bf16_lo(wi[w]);
+                const float fg = hi ? tc::bf16_hi(wf[w]) : tc::bf16_lo(wf[w]);
+                const float gg = hi ? tc::bf16_hi(wg[w]) : tc::bf16_lo(wg[w]);
+                const float og = hi ? tc::bf16_hi(wo[w]) : tc::bf16_lo(wo[w]);
+                const float dh = __uint_as_float(wdh[e]) + __uint_as_float(acc[e]);
+                const float tc = tanhf_fast(__uint_as_float(wc[e]));
+                const float cp = has_prev ? __uint_as_float(wcp[e]) : 0.f;
+                const float dc = __uint_as_float(wdc[e]) + dh * og * (1.f - tc * tc);
+                const float vi = dc * gg * ig * (1.f - ig);
+                const float vf = dc * cp * fg * (1.f - fg);
+                const float vg = dc * ig * (1.f - gg * gg);
+                const float vo = dh * tc * og * (1.f - og);
+                dco[e] = __float_as_uint(dc * fg);
+                if (hi) {
+                    zi[w] = tc::pack_bf16x2(__uint_as_float(zi[w]), vi);
+                    zf[w] = tc::pack_bf16x2(__uint_as_float(zf[w]), vf);
+                    zg[w] = tc::pack_bf16x2(__uint_as_float(zg[w]), vg);
+                    zo[w] = tc::pack_bf16x2(__uint_as_float(zo[w]), vo);
+                } else {
+                    zi[w] = __float_as_uint(vi); zf[w] = __float_as_uint(vf);
+                    zg[w] = __float_as_uint(vg); zo[w] = __float_as_uint(vo);
+                }
+            }
+            if (INPLACE) {
+                bdz = in;  // dz over the consumed dH | dc boxes, dc_rec over the c box
+                bdco = in + 4096;
+                __syncwarp();  // every lane has read its inputs
+            } else {
+                // every lane has consumed its inputs: refill this buffer with chunk c + 2; and the
+                // previous chunk's stores must have read the output boxes before they are rewritten
+                if (lane == 0) ptx::bulk_wait_read0();
+                __syncwarp();
+                if (lane == 0 && uc + 2 * step < SPAN) issue(g, H, j0 + 2 * step, rowbase, in, ebar + b);
+            }
+            tc::st_row_words<32>(bdz + 0 * 1024, lane, zi);
+            tc::st_row_words<32>(bdz + 1 * 1024, lane, zf);
+            tc::st_row_words<32>(bdz + 2 * 1024, lane, zg);
+            tc::st_row_words<32>(bdz + 3 * 1024, lane, zo);
+            tc::st_row_words<64>(bdco, lane, dco);
+            ptx::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+#pragma unroll
+                for (int gi = 0; gi < 4; ++gi) ptx::tma_store_2d(&g.m_dz, bdz + gi * 1024, gi * H + j0, rowbase);
+                ptx::tma_store_2d(&g.m_dc, bdco, j0, rowbase);
+                ptx::bulk_commit();
+                if (INPLACE && uc + 2 * step < SPAN) {
+                    ptx::bulk_wait_read0();  // the stores have read the buffer: refill it with chunk c + 2
+                    issue(g, H, j0 + 2 * step, rowbase, in, ebar + b);
+                }
+            }
+        }
+    }
 };
 
 template <int BN_>
-struct BwdTraits : tc::TraitsBase {
+struct BwdTraits : tc::TraitsBase, BwdEpi {
     static constexpr int BN = BN_;
     // per warp (30 KB): two input sets (12 KB each: dH | dc | c | c_prev fp32 16x32 SW64 2 KB each,
     // gates 4 x bf16 16x32 SW32 1 KB) | dz out 4 x 1 KB | dc out 2 KB
@@ -379,153 +536,128 @@ struct BwdTraits : tc::TraitsBase {
         for (int j = 0; j < BN / 128; ++j)
             ptx::tma_load_2d_2sm_hint(sB + j * 64 * kBK * 2, &g.tb, bar, u0 + rank * (BN / 2) + 64 * j, k0, keep);
     }
-    // The epilogue inputs (dH, dc_rec, c, c_{t-1}, gates) do not depend on the GEMM: epi_begin
-    // issues the TMA loads of this warp's first two 16-unit chunks into smem and L2-prefetches
-    // the rest while the mainloop runs; body then consumes chunk c from buffer c&1 and refills
-    // that buffer with chunk c+2 (two chunks in flight per warp).
-    static constexpr int IN_BYTES = 12 * 1024;
-    __device__ static void issue(const BwdGroup& g, int H, int j0, int rowbase, uint8_t* in, uint64_t* bar) {
-        const bool has_prev = g.c_prev != nullptr;
-        ptx::mbar_arrive_expect_tx(bar, (has_prev ? 4 : 3) * 2048 + 4 * 1024);
-        const uint64_t stream = ptx::policy_evict_first();
-        ptx::tma_load_2d_hint(in, &g.m_dH, bar, j0, rowbase, stream);
-        ptx::tma_load_2d(in + 2048, &g.m_dc, bar, j0, rowbase);
-        ptx::tma_load_2d_hint(in + 4096, &g.m_c, bar, j0, rowbase, stream);
-        if (has_prev) ptx::tma_load_2d_hint(in + 6144, &g.m_cp, bar, j0, rowbase, stream);
-#pragma unroll
-        for (int gi = 0; gi < 4; ++gi) ptx::tma_load_2d_hint(in + 8192 + gi * 1024, &g.m_gates, bar, gi * H + j0, rowbase, stream);
-    }
-    __device__ static void begin(const BwdParams& p, int grp, int m0, int u0, int q, int lane, uint8_t* st, uint64_t* ebar,
-                                 tc::EpiSlot sl) {
-        const BwdGroup& g = p.g[grp];
-        const int rowbase = m0 + q * 32;
-        const int step = 16 * sl.n;
-        if (lane == 0) {
-            int b = 0;
-            for (int uc = 16 * sl.sub; uc < BN && b < 2; uc += step, ++b) issue(g, p.H, u0 + uc, rowbase, st + b * IN_BYTES, ebar + b);
-        }
-        // L2 prefetch of the chunks after the first two: one box per lane
-        const bool has_prev = g.c_prev != nullptr;
-        for (int uc = 16 * sl.sub + 2 * step, i = 0; uc < BN; uc += step, ++i) {
-            const int j0 = u0 + uc;
-            const int box = lane & 7;
-            if ((lane >> 3) != (i & 3)) continue;
-            if (box == 0) ptx::tma_prefetch_l2_2d(&g.m_dH, j0, rowbase);
-            else if (box == 1) ptx::tma_prefetch_l2_2d(&g.m_dc, j0, rowbase);
-            else if (box == 2) ptx::tma_prefetch_l2_2d(&g.m_c, j0, rowbase);
-            else if (box == 3) { if (has_prev) ptx::tma_prefetch_l2_2d(&g.m_cp, j0, rowbase); }
-            else ptx::tma_prefetch_l2_2d(&g.m_gates, (box - 4) * p.H + j0, rowbase);
-        }
-    }
     template <class S>
     __device__ static void epi_begin2(const BwdParams& p, int tile, uint32_t rank, int q, int lane, uint8_t* st,
                                       uint64_t* ebar, S sl) {
         int grp, m0, u0;
         coords2(p, tile, grp, m0, u0);
-        begin(p, grp, m0 + kBM * rank, u0, q, lane, st, ebar, sl);
+        begin<BN>(p, grp, m0 + kBM * rank, u0, q, lane, st, ebar, sl);
     }
     template <class S>
     __device__ static void epi_begin(const BwdParams& p, int tile, int q, int lane, uint8_t* st, uint64_t* ebar, S sl) {
         int grp, m0, u0;
         coords(p, tile, grp, m0, u0);
-        begin(p, grp, m0, u0, q, lane, st, ebar, sl);
+        begin<BN>(p, grp, m0, u0, q, lane, st, ebar, sl);
     }
     __device__ static void epilogue2(const BwdParams& p, int tile, uint32_t rank, uint32_t tbase, int q, int lane,
                                      uint32_t tempty_leader, uint8_t* st, uint64_t* ebar, uint32_t& ephase,
                                      tc::EpiSlot sl) {
         int grp, m0, u0;
         coords2(p, tile, grp, m0, u0);
-        body(p, grp, m0 + kBM * rank, u0, tbase, q, lane, [&] { tc::release_acc_2sm(tempty_leader, lane); }, st,
-             ebar, ephase, sl);
+        body<BN>(p, grp, m0 + kBM * rank, u0, tbase, q, lane, [&] { tc::release_acc_2sm(tempty_leader, lane); }, st,
+                 ebar, ephase, sl, nullptr);
     }
     __device__ static void epilogue(const BwdParams& p, int tile, uint32_t tbase, int q, int lane, uint64_t* tempty,
                                     uint8_t* st, uint64_t* ebar, uint32_t& ephase, tc::EpiSlot sl) {
         int grp, m0, u0;
         coords(p, tile, grp, m0, u0);
-        body(p, grp, m0, u0, tbase, q, lane, [&] { tc::release_acc(tempty, lane); }, st, ebar, ephase, sl);
-    }
-    // epilogue (thread = row), per 16-unit chunk: dh_rec leaves TMEM; the cell backward runs in
-    // registers on the chunk's prefetched inputs; dz (4 x bf16) and dc_rec leave by TMA stores.
-    template <class Rel>
-    __device__ static void body(const BwdParams& p, int grp, int m0, int u0, uint32_t tbase, int q, int lane,
-                                Rel release, uint8_t* st, uint64_t* ebar, uint32_t& ephase, tc::EpiSlot sl) {
-        const BwdGroup& g = p.g[grp];
-        const int H = p.H;
-        const int rowbase = m0 + q * 32;
-        uint8_t* bdz = st + 2 * IN_BYTES;         // 4 x 1 KB
-        uint8_t* bdco = st + 2 * IN_BYTES + 4096;  // 2 KB
-        const bool has_prev = g.c_prev != nullptr;
-        const int step = 16 * sl.n;
-        int b = 0;
-#pragma unroll 1
-        for (int uc = 16 * sl.sub; uc < BN; uc += step, b ^= 1) {
-            const int j0 = u0 + uc;
-            uint8_t* in = st + b * IN_BYTES;
-            uint32_t acc[16];
-            ptx::tmem_ld_32x32b_x16_(tbase + uc, acc);
-            ptx::tmem_ld_wait();
-            if (uc + step >= BN) release();
-            ptx::mbar_wait(ebar + b, (ephase >> b) & 1u);
-            ephase ^= 1u << b;
-            uint32_t wdh[16], wdc[16], wc[16], wcp[16], wi[8], wf[8], wg[8], wo[8];
-            tc::ld_row_words<64>(in, lane, wdh);
-            tc::ld_row_words<64>(in + 2048, lane, wdc);
-            tc::ld_row_words<64>(in + 4096, lane, wc);
-            if (has_prev) tc::ld_row_words<64>(in + 6144, lane, wcp);
-            tc::ld_row_words<32>(in + 8192 + 0 * 1024, lane, wi);
-            tc::ld_row_words<32>(in + 8192 + 1 * 1024, lane, wf);
-            tc::ld_row_words<32>(in + 8192 + 2 * 1024, lane, wg);
-            tc::ld_row_words<32>(in + 8192 + 3 * 1024, lane, wo);
-            uint32_t zi[8], zf[8], zg[8], zo[8], dco[16];
-#pragma unroll
-            for (int e = 0; e < 16; ++e) {
-                const int w = e >> 1;
-                const bool hi = e & 1;
-                const float ig = hi ? tc::bf16_hi(wi[w]) : tc::bf16_lo(wi[w]);
-                const float fg = hi ? tc::bf16_hi(wf[w]) : tc::bf16_lo(wf[w]);
-                const float gg = hi ? tc::bf16_hi(wg[w]) : tc::bf16_lo(wg[w]);
-                const float og = hi ? tc::bf16_hi(wo[w]) : tc::bf16_lo(wo[w]);
-                const float dh = __uint_as_float(wdh[e]) + __uint_as_float(acc[e]);
-                const float tc = tanhf_fast(__uint_as_float(wc[e]));
-                const float cp = has_prev ? __uint_as_float(wcp[e]) : 0.f;
-                const float dc = __uint_as_float(wdc[e]) + dh * og * (1.f - tc * tc);
-                const float vi = dc * gg * ig * (1.f - ig);
-                const float vf = dc * cp * fg * (1.f - fg);
-                const float vg = dc * ig * (1.f - gg * gg);
-                const float vo = dh * tc * og * (1.f - og);
-                dco[e] = __float_as_uint(dc * fg);
-                if (hi) {
-                    zi[w] = tc::pack_bf16x2(__uint_as_float(zi[w]), vi);
-                    zf[w] = tc::pack_bf16x2(__uint_as_float(zf[w]), vf);
-                    zg[w] = tc::pack_bf16x2(__uint_as_float(zg[w]), vg);
-                    zo[w] = tc::pack_bf16x2(__uint_as_float(zo[w]), vo);
-                } else {
-                    zi[w] = __float_as_uint(vi); zf[w] = __float_as_uint(vf);
-                    zg[w] = __float_as_uint(vg); zo[w] = __float_as_uint(vo);
-                }
-            }
-            // every lane has consumed its inputs: refill this buffer with chunk c + 2; and the
-            // previous chunk's stores must have read the output boxes before they are rewritten
-            if (lane == 0) ptx::bulk_wait_read0();
-            __syncwarp();
-            if (lane == 0 && uc + 2 * step < BN) issue(g, H, j0 + 2 * step, rowbase, in, ebar + b);
-            tc::st_row_words<32>(bdz + 0 * 1024, lane, zi);
-            tc::st_row_words<32>(bdz + 1 * 1024, lane, zf);
-            tc::st_row_words<32>(bdz + 2 * 1024, lane, zg);
-            tc::st_row_words<32>(bdz + 3 * 1024, lane, zo);
-            tc::st_row_words<64>(bdco, lane, dco);
-            ptx::fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-#pragma unroll
-                for (int gi = 0; gi < 4; ++gi) ptx::tma_store_2d(&g.m_dz, bdz + gi * 1024, gi * H + j0, rowbase);
-                ptx::tma_store_2d(&g.m_dc, bdco, j0, rowbase);
-                ptx::bulk_commit();
-            }
-        }
+        body<BN>(p, grp, m0, u0, tbase, q, lane, [&] { tc::release_acc(tempty, lane); }, st, ebar, ephase, sl, nullptr);
     }
 };
 
+// Split-K BPTT dgrad (CTA pairs, 256 x 256 tiles, K = 4H halved): work unit w = (dir, m, n, kh)
+// computes a K-half partial of a 256-row x 256-unit tile; the two halves exchange the half of
+// the partial the other one finalises through a global scratch (64 KB per CTA, L2-resident) and
+// an epoch-counter handshake, then each CTA runs the cell backward on 128 rows x 128 units.
+// Operand traffic drops by a third vs 256 x 128 tiles. Requires every work unit resident at
+// once (host checks 2 x tiles <= 148 CTAs; one unit per CTA).
+struct BwdSplitTraits : tc::TraitsBase, BwdEpi {
+    static constexpr int BN = 256;
+    static constexpr int EPI_WARPS = 8;
+    static constexpr int EPI_SMEM = EPI_WARPS * 24 * 1024;  // BwdEpi::body<.., INPLACE>
+    static constexpr int ACC_STAGES = 1;
+    static constexpr bool EPI_OVERLAY = true;  // one unit per CTA: all smem to the mainloop stages
+    static constexpr bool A_MN = false;
+    static constexpr bool B_MN = true;
+    __device__ static int num_tiles(const BwdParams& p) { return p.ngroups * p.m_tiles * p.n_tiles * 2; }
+    __device__ static void prefetch(const BwdParams& p) {
+        for (int i = 0; i < p.ngroups; ++i) { ptx::tma_prefetch(&p.g[i].ta); ptx::tma_prefetch(&p.g[i].tb); }
+    }
+    // tile = ((grp * n_tiles + nt) * m_tiles + mt) * 2 + kh
+    __device__ static void coords2(const BwdParams& p, int tile, int& grp, int& m0, int& u0, int& kh) {
+        kh = tile & 1;
+        const int r = tile >> 1;
+        const int mt = r % p.m_tiles, rn = r / p.m_tiles;
+        m0 = mt * 2 * kBM;
+        u0 = (rn % p.n_tiles) * BN;
+        grp = rn / p.n_tiles;
+    }
+    __device__ static int kblocks(const BwdParams& p, int tile) {
+        int grp, m0, u0, kh;
+        coords2(p, tile, grp, m0, u0, kh);
+        const int kb = p.g[grp].kb;
+        return kh == 0 ? kb / 2 : kb - kb / 2;
+    }
+    __device__ static void load2(const BwdParams& p, int tile, int kb, uint32_t rank, uint8_t* sA, uint8_t* sB,
+                                 uint32_t bar) {
+        int grp, m0, u0, kh;
+        coords2(p, tile, grp, m0, u0, kh);
+        const BwdGroup& g = p.g[grp];
+        const int k0 = (kh * (g.kb / 2) + kb) * kBK;
+        ptx::tma_load_2d_2sm_hint(sA, &g.ta, bar, k0, m0 + kBM * rank, ptx::policy_evict_first());
+        const uint64_t keep = ptx::policy_evict_last();
+#pragma unroll
+        for (int j = 0; j < BN / 128; ++j)
+            ptx::tma_load_2d_2sm_hint(sB + j * 64 * kBK * 2, &g.tb, bar, u0 + rank * (BN / 2) + 64 * j, k0, keep);
+    }
+    template <class S>
+    __device__ static void epi_begin2(const BwdParams& p, int tile, uint32_t rank, int q, int lane, uint8_t* st,
+                                      uint64_t* ebar, S sl) {
+        int grp, m0, u0, kh;
+        coords2(p, tile, grp, m0, u0, kh);
+        begin<128, false>(p, grp, m0 + kBM * rank, u0 + 128 * kh, q, lane, st, ebar, sl);
+    }
+    __device__ static void epilogue2(const BwdParams& p, int tile, uint32_t rank, uint32_t tbase, int q, int lane,
+                                     uint32_t tempty_leader, uint8_t* st, uint64_t* ebar, uint32_t& ephase,
+                                     tc::EpiSlot sl) {
+        int grp, m0, u0, kh;
+        coords2(p, tile, grp, m0, u0, kh);
+        const int slot = tile * 2 + static_cast<int>(rank), peer_slot = (tile ^ 1) * 2 + static_cast<int>(rank);
+        constexpr int kSlot = 128 * 128;  // floats
+        // 1) export the half the partner finalises: [chunk][row][16] fp32 (coalesced 2 KB per warp chunk)
+        float* mine = p.sk_scratch + static_cast<int64_t>(slot) * kSlot;
+        const int row = q * 32 + lane;
+#pragma unroll 1
+        for (int c = sl.sub; c < 8; c += sl.n) {
+            uint32_t v[16];
+            ptx::tmem_ld_32x32b_x16_(tbase + (1 - kh) * 128 + 16 * c, v);
+            ptx::tmem_ld_wait();
+            float4* dst = reinterpret_cast<float4*>(mine + (c * 128 + row) * 16);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                __stcg(dst + k, make_float4(__uint_as_float(v[4 * k]), __uint_as_float(v[4 * k + 1]),
+                                            __uint_as_float(v[4 * k + 2]), __uint_as_float(v[4 * k + 3])));
+        }
+        // 2) handshake: epoch counters (one increment per launch per slot; no reset needed)
+        if (q == 2 && lane == 0) tc::trace_once(p.trace, 12);
+        ptx::named_sync(2, 32 * EPI_WARPS);
+        if (q == 0 && sl.sub == 0 && lane == 0) {
+            __threadfence();  // (8 epilogue warps: (q, sub) = (0, 0) is warp 2)
+            const unsigned mine_epoch = atomicAdd(p.sk_flags + slot, 1u) + 1u;
+            unsigned seen;
+            do {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(p.sk_flags + peer_slot) : "memory");
+            } while (static_cast<int>(seen - mine_epoch) < 0);
+            __threadfence();
+        }
+        ptx::named_sync(2, 32 * EPI_WARPS);
+        if (q == 2 && lane == 0) tc::trace_once(p.trace, 13);
+        // 3) cell backward on the owned 128 units with the partner's partial added
+        body<128, true>(p, grp, m0 + kBM * rank, u0 + 128 * kh, tbase + 128 * kh, q, lane,
+                  [&] { tc::release_acc_2sm(tempty_leader, lane); }, st, ebar, ephase, sl,
+                  p.sk_scratch + static_cast<int64_t>(peer_slot) * kSlot, false);
+    }
+};
 
 template <class Traits, class Params>
 void launch_persistent(const Params& p, int tiles, cudaStream_t s) {
@@ -571,6 +703,7 @@ void launch_pair(const Params& p, int pair_tiles, cudaStream_t s) {
 
 bool g_use_pair_mma = true;
 bool g_use_wide_fwd = true;
+bool g_use_splitk_bwd = true;
 
 void lstm_fwd_step(const LstmFwdDir* dirs, int ndirs, int B, int H, int ldg, int ldc, int ldh, cudaStream_t s) {
     AB_CHECK(H % 64 == 0 && ndirs >= 1 && ndirs <= 2, ADPSGD_E_DIMENSION, "fused LSTM step needs H % 64 == 0");
@@ -624,15 +757,22 @@ void lstm_fwd_step(const LstmFwdDir* dirs, int ndirs, int B, int H, int ldg, int
     }
 }
 
+int64_t lstm_bwd_splitk_slots(int ndirs, int B, int H) {
+    return static_cast<int64_t>(ndirs) * ((B + 2 * kBM - 1) / (2 * kBM)) * (H / 256 > 0 ? H / 256 : 1) * 2 * 2;
+}
+
 void lstm_bwd_step(const LstmBwdDir* dirs, int ndirs, int B, int H, int lddh, int ldg, int ldc, int lddz,
-                   cudaStream_t s) {
+                   cudaStream_t s, float* sk_scratch, unsigned int* sk_flags) {
     AB_CHECK(H % 64 == 0 && ndirs >= 1 && ndirs <= 2, ADPSGD_E_DIMENSION, "fused BPTT step needs H % 64 == 0");
     BwdParams p;
     std::memset(&p, 0, sizeof(p));
     // 128 x 64 tiles: a 1024 x 1024 dgrad per direction is only 64 tiles at BN = 128
     const bool pair = g_use_pair_mma && B > kBM && H % 128 == 0;
     const int m_tiles = pair ? (B + 2 * kBM - 1) / (2 * kBM) : (B + kBM - 1) / kBM;
-    const int bn = pair ? 128 : ((ndirs * m_tiles * (H / 128) >= num_sms()) ? 128 : 64);
+    // split-K 256 x 256 tiles when every (tile, K-half) work unit is resident at once
+    const bool split = pair && g_use_splitk_bwd && sk_scratch && sk_flags && H % 256 == 0 &&
+                       2 * ndirs * m_tiles * (H / 256) <= num_sms() / 2;
+    const int bn = split ? 256 : pair ? 128 : ((ndirs * m_tiles * (H / 128) >= num_sms()) ? 128 : 64);
     double flops = 0, bytes = 0;
     for (int d = 0; d < ndirs; ++d) {
         const LstmBwdDir& a = dirs[d];
@@ -656,8 +796,11 @@ void lstm_bwd_step(const LstmBwdDir* dirs, int ndirs, int B, int H, int lddh, in
     p.trace = trace_take();
     p.m_tiles = m_tiles;
     p.n_tiles = H / bn;
+    p.sk_scratch = sk_scratch;
+    p.sk_flags = sk_flags;
     ProfScope ps_(s, PROF_GEMM_REC_BWD, flops, bytes);
-    if (pair) launch_pair<BwdTraits<128>>(p, ndirs * p.m_tiles * p.n_tiles, s);
+    if (split) launch_pair<BwdSplitTraits>(p, 2 * ndirs * p.m_tiles * p.n_tiles, s);
+    else if (pair) launch_pair<BwdTraits<128>>(p, ndirs * p.m_tiles * p.n_tiles, s);
     else if (bn == 128) launch_persistent<BwdTraits<128>>(p, ndirs * p.m_tiles * p.n_tiles, s);
     else launch_persistent<BwdTraits<64>>(p, ndirs * p.m_tiles * p.n_tiles, s);
 }

@@ -35,7 +35,10 @@ struct LstmBwdDir {
 };
 
 void lstm_fwd_step(const LstmFwdDir* dirs, int ndirs, int B, int H, int ldg, int ldc, int ldh, cudaStream_t s);
+// sk_scratch / sk_flags: split-K exchange buffers (lstm_bwd_splitk_slots(..) x 64 KB fp32 and
+// x 1 u32, flags zeroed once); nullptr disables the split-K variant.
+int64_t lstm_bwd_splitk_slots(int ndirs, int B, int H);
 void lstm_bwd_step(const LstmBwdDir* dirs, int ndirs, int B, int H, int lddh, int ldg, int ldc, int lddz,
-                   cudaStream_t s);
+                   cudaStream_t s, float* sk_scratch = nullptr, unsigned int* sk_flags = nullptr);
 
 }  // namespace ab

@@ -129,8 +129,11 @@ __device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
     return r;
 }
+// Arrive on a barrier of another CTA in the cluster (default .release.cta semantics, as CUTLASS's
+// ClusterBarrier::arrive): the TMEM-empty handshake is ordered by tcgen05.wait::ld +
+// tcgen05.fence::before_thread_sync; a .cluster-scope release adds a full MEMBAR/ERRBAR per call.
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 // 2-SM TMA: data lands in this CTA's smem, completion bytes go to the leader's barrier.
 __device__ __forceinline__ void tma_load_2d_2sm(void* smem_dst, const CUtensorMap* m, uint32_t bar_cluster_addr, int c0,
