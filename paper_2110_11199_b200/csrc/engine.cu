@@ -35,6 +35,7 @@ namespace ab {
 extern bool g_use_pair_mma;  // gemm_lstm.cu
 extern bool g_use_wide_fwd;  // gemm_lstm.cu
 extern bool g_use_splitk_bwd;  // gemm_lstm.cu
+extern bool g_use_pdl;         // gemm_lstm.cu
 
 namespace {
 thread_local std::string g_last_error;
@@ -113,6 +114,10 @@ Ctx::Ctx(const adpsgd_config& c) : cfg(c) {
     if (const char* e = std::getenv("ADPSGD_NO_PAIR")) g_use_pair_mma = e[0] == '0';
     if (const char* e = std::getenv("ADPSGD_NO_WIDE")) g_use_wide_fwd = e[0] == '0';
     if (const char* e = std::getenv("ADPSGD_NO_SPLITK")) g_use_splitk_bwd = e[0] == '0';
+    if (const char* e = std::getenv("ADPSGD_NO_PDL")) g_use_pdl = e[0] == '0';
+    if (const char* e = std::getenv("ADPSGD_NO_STREAMK")) g_use_streamk = e[0] == '0';
+    if (const char* e = std::getenv("ADPSGD_NO_XTRA")) g_use_xtra = e[0] == '0';
+    if (const char* e = std::getenv("ADPSGD_FORCE_EXT")) g_force_ext = e[0] == '1';
 
     AB_CUDA(cudaSetDevice(c.device));
     AB_CUDA(cudaStreamCreateWithFlags(&s_main, cudaStreamNonBlocking));
@@ -146,6 +151,13 @@ Ctx::Ctx(const adpsgd_config& c) : cfg(c) {
         ce_part = static_cast<float2*>(alloc(ce_part_elems(static_cast<int>(TB), lay.C) * sizeof(float2)));
         ce_zlab = static_cast<float*>(alloc(TB * sizeof(float)));
         ce_lse = static_cast<float*>(alloc(TB * sizeof(float)));
+        {   // stream-K scratch: (SMs / 2) pairs x 2 CTAs x (8 + 1) chunks x 128 rows x 32 fp32
+            gemm_ws.floats = static_cast<size_t>(num_sms() / 2) * 2 * 9 * 128 * 32;
+            gemm_ws.ws = static_cast<float*>(alloc(gemm_ws.floats * sizeof(float)));
+            gemm_ws.flag_count = static_cast<size_t>(num_sms());
+            gemm_ws.flags = static_cast<unsigned int*>(alloc(gemm_ws.flag_count * sizeof(unsigned int)));
+            AB_CUDA(cudaMemsetAsync(gemm_ws.flags, 0, gemm_ws.flag_count * sizeof(unsigned int), s_main));
+        }
         if (H % 256 == 0) {
             const int64_t slots = lstm_bwd_splitk_slots(nd, B, H);
             sk_scratch = static_cast<float*>(alloc(static_cast<size_t>(slots) * 128 * 128 * sizeof(float)));
@@ -245,6 +257,7 @@ static inline void* off_ptr(void* p, int64_t elems, int es) { return static_cast
 // grad (fp32, flat layout) receives d(mean CE)/dw; loss_slot receives the mean CE.
 void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, float* loss_slot, cudaStream_t s,
                            bool backward) {
+    set_gemm_workspace(gemm_ws);
     const bool bf = bf16_mode;
     WView W{bf ? static_cast<const void*>(ln.shadow) : static_cast<const void*>(master), master, this, &ln};
     const int G4 = 4 * H;

@@ -1,6 +1,8 @@
 // Device-resident learner context behind the C ABI (engine.cu, capi.cu).
 #pragma once
 
+#include "gemm.hpp"
+
 #include <cuda_runtime.h>
 
 #include <map>
@@ -72,6 +74,7 @@ struct Ctx {
     float* ce_lse = nullptr;
     float* sk_scratch = nullptr;      // split-K BPTT partial exchange (gemm_lstm.cu)
     unsigned int* sk_flags = nullptr;
+    GemmWorkspace gemm_ws;             // stream-K scratch of the generic tcgen05 GEMMs
     void* dlogits = nullptr;
     float* row_loss = nullptr;
     float *dHa = nullptr, *dHb = nullptr;

@@ -41,6 +41,20 @@ struct GemmArgs {
     float* extra = nullptr;
 };
 
+// Stream-K scratch of the calling thread's engine (set before its GEMMs run; see gemm_tc.cu):
+// ws >= (SMs/2) * 2 * 9 * 128 * 32 floats, flags >= SMs u32 zeroed once. ws == nullptr: no stream-K.
+struct GemmWorkspace {
+    float* ws = nullptr;
+    size_t floats = 0;
+    unsigned int* flags = nullptr;
+    size_t flag_count = 0;
+};
+void set_gemm_workspace(const GemmWorkspace& w);
+const GemmWorkspace& gemm_workspace();
+extern bool g_use_xtra;
+extern bool g_use_streamk;
+extern bool g_force_ext;  // tests: take the extra-column / stream-K kernels whenever the layout allows
+
 // fp32 operands, fp32 or bf16 output, any majorness (gemm_simt.cu).
 void gemm_simt(const GemmArgs& g, cudaStream_t s);
 // bf16 operands, tcgen05 + TMA + TMEM, fp32 accumulate (gemm_tc.cu).

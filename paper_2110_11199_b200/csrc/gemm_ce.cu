@@ -252,19 +252,7 @@ void launch_any(const Params& p, int tiles, bool pair, cudaStream_t s) {
             attr = true;
         }
         const int pairs = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(2 * pairs);
-        cfg.blockDim = dim3(tc::threads_of<Traits>());
-        cfg.dynamicSmemBytes = SM;
-        cfg.stream = s;
-        cudaLaunchAttribute attrs[1];
-        attrs[0].id = cudaLaunchAttributeClusterDimension;
-        attrs[0].val.clusterDim.x = 2;
-        attrs[0].val.clusterDim.y = 1;
-        attrs[0].val.clusterDim.z = 1;
-        cfg.attrs = attrs;
-        cfg.numAttrs = 1;
-        AB_CUDA(cudaLaunchKernelEx(&cfg, k, p));
+        tc::launch_tc(k, p, 2 * pairs, tc::threads_of<Traits>(), SM, true, s);
     } else {
         auto k = tc::persistent_kernel<Traits, Params>;
         static bool attr = false;
@@ -274,7 +262,7 @@ void launch_any(const Params& p, int tiles, bool pair, cudaStream_t s) {
             attr = true;
         }
         const int grid = tiles < num_sms() ? tiles : num_sms();
-        k<<<grid, tc::threads_of<Traits>(), SM, s>>>(p);
+        tc::launch_tc(k, p, grid, tc::threads_of<Traits>(), SM, false, s);
     }
     count_launch();
     AB_CUDA(cudaGetLastError());

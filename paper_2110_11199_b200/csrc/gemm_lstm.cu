@@ -668,7 +668,7 @@ void launch_persistent(const Params& p, int tiles, cudaStream_t s) {
         attr = true;
     }
     const int grid = tiles < num_sms() ? tiles : num_sms();
-    k<<<grid, tc::threads_of<Traits>(), tc::Shape<Traits::BN, Traits::EPI_SMEM>::SMEM, s>>>(p);
+    tc::launch_tc(k, p, grid, tc::threads_of<Traits>(), tc::Shape<Traits::BN, Traits::EPI_SMEM>::SMEM, false, s);
     count_launch();
     AB_CUDA(cudaGetLastError());
 }
@@ -683,19 +683,7 @@ void launch_pair(const Params& p, int pair_tiles, cudaStream_t s) {
     }
     int pairs = num_sms() / 2;
     if (pair_tiles < pairs) pairs = pair_tiles;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(2 * pairs);
-    cfg.blockDim = dim3(tc::threads_of<Traits>());
-    cfg.dynamicSmemBytes = tc::ShapeOf2<Traits>::SMEM;
-    cfg.stream = s;
-    cudaLaunchAttribute attrs[1];
-    attrs[0].id = cudaLaunchAttributeClusterDimension;
-    attrs[0].val.clusterDim.x = 2;
-    attrs[0].val.clusterDim.y = 1;
-    attrs[0].val.clusterDim.z = 1;
-    cfg.attrs = attrs;
-    cfg.numAttrs = 1;
-    AB_CUDA(cudaLaunchKernelEx(&cfg, k, p));
+    tc::launch_tc(k, p, 2 * pairs, tc::threads_of<Traits>(), tc::ShapeOf2<Traits>::SMEM, true, s);
     count_launch();
 }
 
@@ -704,6 +692,7 @@ void launch_pair(const Params& p, int pair_tiles, cudaStream_t s) {
 bool g_use_pair_mma = true;
 bool g_use_wide_fwd = true;
 bool g_use_splitk_bwd = true;
+bool g_use_pdl = true;
 
 void lstm_fwd_step(const LstmFwdDir* dirs, int ndirs, int B, int H, int ldg, int ldc, int ldh, cudaStream_t s) {
     AB_CHECK(H % 64 == 0 && ndirs >= 1 && ndirs <= 2, ADPSGD_E_DIMENSION, "fused LSTM step needs H % 64 == 0");

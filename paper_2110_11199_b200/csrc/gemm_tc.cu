@@ -41,17 +41,50 @@ struct TcParams {
     unsigned long long* trace;
     int n_main;    // columns >= n_main are redirected to extra[row]
     float* extra;
+    // stream-K (GenTraits SK): pair cid owns iterations [cid * total / pairs, (cid + 1) * total / pairs)
+    // of the tile-major (tile, k-block) space; partials of split tiles meet in sk_ws.
+    float* sk_ws;              // [pair * 2 + rank][chunk][128 rows][32] fp32
+    unsigned int* sk_flags;    // [pair * 2 + rank], zeroed between launches by the owners
+    int64_t sk_total;          // tiles * k-blocks per tile
 };
 
 
 // Generic GEMM traits for the persistent skeletons in tc_core.cuh (single CTA and CTA pair).
-template <int BN_, bool AMN, bool BMN, bool CBF16>
+// XTRA: the B operand's "ones column" (bias gradient = row sums of A) comes from an extra
+//       N = 16 MMA against an all-ones smem tile on the tiles of n-tile 0 (TMEM cols [BN, BN+16)),
+//       so N stays a multiple of the tile width (CTA pairs, single accumulator stage).
+// SK:   stream-K work split (tc::Item): every CTA pair gets the same number of k-block iterations;
+//       a tile split between pairs is finished by the pair holding its k-block 0, which adds the
+//       other segments' partials in pair order (deterministic).
+template <int BN_, bool AMN, bool BMN, bool CBF16, bool XTRA = false, bool SK = false>
 struct GenTraits : tc::TraitsBase {
     static constexpr int BN = BN_;
     static constexpr int EPI_SMEM = 0;
     static constexpr int EPI_WARPS = 8;
     static constexpr bool A_MN = AMN;
     static constexpr bool B_MN = BMN;
+    static constexpr int EXTRA_COLS = XTRA ? 32 : 0;
+    static constexpr int ACC_STAGES = XTRA ? 1 : 2;
+    static constexpr bool STREAMK = SK;
+    static constexpr int NCH = BN / 32 + (XTRA ? 1 : 0);  // 32-column chunks of a partial (incl. the extra)
+    __device__ static bool extra_tile(const TcParams& p, int tile) { return XTRA && tile / p.m_tiles == 0; }
+    __device__ static int64_t sk_start(const TcParams& p, int c, int ncl) { return p.sk_total * c / ncl; }
+    __device__ static bool sk_item(const TcParams& p, int cid, int ncl, int it, tc::Item& w) {
+        const int kbt = kblocks(p, 0);
+        int64_t pos = sk_start(p, cid, ncl);
+        const int64_t end = sk_start(p, cid + 1, ncl);
+        for (int i = 0;; ++i) {
+            if (pos >= end) return false;
+            const int tile = static_cast<int>(pos / kbt), kb0 = static_cast<int>(pos % kbt);
+            const int kb1 = static_cast<int>(kb0 + (end - pos) < kbt ? kb0 + (end - pos) : kbt);
+            if (i == it) {
+                w.tile = tile; w.kb0 = kb0; w.kb1 = kb1;
+                w.role = (kb0 == 0 && kb1 == kbt) ? 0 : (kb0 == 0 ? 1 : 2);
+                return true;
+            }
+            pos += kb1 - kb0;
+        }
+    }
     __device__ static int num_tiles(const TcParams& p) { return p.m_tiles * p.n_tiles; }
     __device__ static void prefetch(const TcParams& p) {
         for (int s = 0; s < p.nseg; ++s) { ptx::tma_prefetch(&p.ta[s]); ptx::tma_prefetch(&p.tb[s]); }
@@ -82,7 +115,7 @@ struct GenTraits : tc::TraitsBase {
     __device__ static void epilogue(const TcParams& p, int tile, uint32_t tbase, int q, int lane, uint64_t* tempty,
                                     uint8_t*, uint64_t*, uint32_t&, tc::EpiSlot sl) {
         const int m0 = (tile % p.m_tiles) * BM, n0 = (tile / p.m_tiles) * BN;
-        body(p, m0 + q * 32, n0, tbase, lane, [&] { tc::release_acc(tempty, lane); }, sl);
+        body(p, m0 + q * 32, n0, tbase, lane, [&] { tc::release_acc(tempty, lane); }, sl, false, [](int, uint32_t*) {});
     }
     // ---- CTA pair: 256 x BN tiles, rank r holds A rows [m0 + 128 r, +128) and B rows [n0 + r BN/2, +BN/2) ----
     __device__ static void load2(const TcParams& p, int tile, int kb, uint32_t rank, uint8_t* sA, uint8_t* sB,
@@ -108,25 +141,109 @@ struct GenTraits : tc::TraitsBase {
     __device__ static void epilogue2(const TcParams& p, int tile, uint32_t rank, uint32_t tbase, int q, int lane,
                                      uint32_t tempty_leader, uint8_t*, uint64_t*, uint32_t&, tc::EpiSlot sl) {
         const int m0 = (tile % p.m_tiles) * 2 * BM + BM * rank, n0 = (tile / p.m_tiles) * BN;
-        body(p, m0 + q * 32, n0, tbase, lane, [&] { tc::release_acc_2sm(tempty_leader, lane); }, sl);
+        body(p, m0 + q * 32, n0, tbase, lane, [&] { tc::release_acc_2sm(tempty_leader, lane); }, sl,
+             extra_tile(p, tile), [](int, uint32_t*) {});
+    }
+    // stream-K epilogue: role 0 = plain tile; 2 = export the partial (all chunks incl. the extra)
+    // and flag it; 1 = wait for the later segments' pairs, add their partials, finish the tile.
+    __device__ static void epilogue_sk(const TcParams& p, const tc::Item& w, int cid, uint32_t rank, uint32_t tbase,
+                                       int q, int lane, uint32_t tempty_leader, tc::EpiSlot sl) {
+        const int m0 = (w.tile % p.m_tiles) * 2 * BM + BM * static_cast<int>(rank), n0 = (w.tile / p.m_tiles) * BN;
+        const int row = q * 32 + lane;
+        const bool xt = extra_tile(p, w.tile);
+        auto release = [&] { tc::release_acc_2sm(tempty_leader, lane); };
+        constexpr int kSlot = NCH * 128 * 32;  // floats per CTA slot
+        const int ncl = gridDim.x >> 1;
+        if (w.role == 2) {
+            float* ws = p.sk_ws + static_cast<int64_t>(cid * 2 + static_cast<int>(rank)) * kSlot;
+#pragma unroll 1
+            for (int c = sl.sub; c < NCH; c += sl.n) {
+                uint32_t r[32];
+                if (c < BN / 32) ptx::tmem_ld_32x32b_x32(tbase + 32 * c, r);
+                else if (xt) ptx::tmem_ld_32x32b_x16_(tbase + BN, r);
+                ptx::tmem_ld_wait();
+                if (c >= BN / 32 && !xt) continue;
+                float4* dst = reinterpret_cast<float4*>(ws + (static_cast<int64_t>(c) * 128 + row) * 32);
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    __stcg(dst + i, make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
+                                                __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3])));
+            }
+            release();
+            ptx::named_sync(2, 32 * EPI_WARPS);
+            if (q == 0 && sl.sub == 0 && lane == 0) {
+                __threadfence();
+                asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.sk_flags + cid * 2 + rank), "r"(1u) : "memory");
+            }
+            return;
+        }
+        int c_last = cid;  // owner: later pairs whose ranges start inside this tile contributed
+        if (w.role == 1) {
+            const int64_t tile_end = static_cast<int64_t>(w.tile + 1) * kblocks(p, 0);
+            while (c_last + 1 < ncl && sk_start(p, c_last + 1, ncl) < tile_end) ++c_last;
+            if (q == 0 && sl.sub == 0 && lane == 0) {
+                for (int j = cid + 1; j <= c_last; ++j) {
+                    if (sk_start(p, j, ncl) == sk_start(p, j + 1, ncl)) continue;  // empty range: no partial
+                    unsigned v;
+                    do {
+                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.sk_flags + j * 2 + rank) : "memory");
+                    } while (v == 0);
+                }
+                __threadfence();
+            }
+            ptx::named_sync(2, 32 * EPI_WARPS);
+        }
+        body(p, m0 + q * 32, n0, tbase, lane, release, sl, xt, [&](int c, uint32_t* r) {
+            for (int j = cid + 1; j <= c_last; ++j) {
+                if (sk_start(p, j, ncl) == sk_start(p, j + 1, ncl)) continue;
+                const float4* src = reinterpret_cast<const float4*>(
+                    p.sk_ws + static_cast<int64_t>(j * 2 + static_cast<int>(rank)) * kSlot + (static_cast<int64_t>(c) * 128 + row) * 32);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const float4 f = __ldcg(src + i);
+                    r[4 * i] = __float_as_uint(__uint_as_float(r[4 * i]) + f.x);
+                    r[4 * i + 1] = __float_as_uint(__uint_as_float(r[4 * i + 1]) + f.y);
+                    r[4 * i + 2] = __float_as_uint(__uint_as_float(r[4 * i + 2]) + f.z);
+                    r[4 * i + 3] = __float_as_uint(__uint_as_float(r[4 * i + 3]) + f.w);
+                }
+            }
+        });
+        if (w.role == 1) {  // every warp has read the partials: re-arm the contributors' flags
+            ptx::named_sync(2, 32 * EPI_WARPS);
+            if (q == 0 && sl.sub == 0 && lane == 0)
+                for (int j = cid + 1; j <= c_last; ++j)
+                    if (sk_start(p, j, ncl) != sk_start(p, j + 1, ncl)) p.sk_flags[j * 2 + rank] = 0u;
+        }
     }
     // TMEM accumulator (thread = row, 32-column chunks in registers) -> alpha / bias / accumulate
-    // -> vectorised row-segment stores.
-    template <class Rel>
+    // -> vectorised row-segment stores. fix(c, r) adds stream-K partials to chunk c; xt: also
+    // write the extra row-sum column (TMEM col BN) to extra[row].
+    template <class Rel, class Fix>
     __device__ static void body(const TcParams& p, int rowbase, int n0, uint32_t tbase, int lane, Rel release,
-                                tc::EpiSlot sl) {
+                                tc::EpiSlot sl, bool xt, Fix fix) {
         const int gm = rowbase + lane;
         const bool row_ok = gm < p.M;
+        if (XTRA && xt && sl.sub == 0) {
+            uint32_t r[32];
+            ptx::tmem_ld_32x32b_x16_(tbase + BN, r);
+            ptx::tmem_ld_wait();
+            fix(BN / 32, r);
+            if (row_ok) {
+                const float x = p.alpha * __uint_as_float(r[0]);
+                p.extra[gm] = p.accumulate ? p.extra[gm] + x : x;
+            }
+        }
 #pragma unroll 1
         for (int c = 32 * sl.sub; c < BN; c += 32 * sl.n) {
             uint32_t r[32];
             ptx::tmem_ld_32x32b_x32(tbase + c, r);
             ptx::tmem_ld_wait();
             if (c + 32 * sl.n >= BN) release();
+            fix(c / 32, r);
             if (!row_ok) continue;
             const int gn0 = n0 + c;
             if (gn0 >= p.N) continue;
-            if (p.extra && gn0 + 32 > p.n_main) {
+            if (!XTRA && p.extra && gn0 + 32 > p.n_main) {
                 // tail chunk containing redirected columns (fp32 output only)
                 float* crow = reinterpret_cast<float*>(p.C) + static_cast<int64_t>(gm) * p.ldc;
                 for (int i = 0; i < 32; ++i) {
@@ -241,7 +358,7 @@ void launch_single(const TcParams& p, cudaStream_t s) {
     }
     const int tiles = p.m_tiles * p.n_tiles;
     const int grid = tiles < num_sms() ? tiles : num_sms();
-    k<<<grid, tc::threads_of<Traits>(), tc::Shape<Traits::BN, Traits::EPI_SMEM>::SMEM, s>>>(p);
+    tc::launch_tc(k, p, grid, tc::threads_of<Traits>(), tc::Shape<Traits::BN, Traits::EPI_SMEM>::SMEM, false, s);
     count_launch();
     AB_CUDA(cudaGetLastError());
 }
@@ -255,20 +372,9 @@ void launch_pair(const TcParams& p, cudaStream_t s) {
         attr = true;
     }
     const int tiles = p.m_tiles * p.n_tiles;
-    const int pairs = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(2 * pairs);
-    cfg.blockDim = dim3(tc::threads_of<Traits>());
-    cfg.dynamicSmemBytes = tc::ShapeOf2<Traits>::SMEM;
-    cfg.stream = s;
-    cudaLaunchAttribute attrs[1];
-    attrs[0].id = cudaLaunchAttributeClusterDimension;
-    attrs[0].val.clusterDim.x = 2;
-    attrs[0].val.clusterDim.y = 1;
-    attrs[0].val.clusterDim.z = 1;
-    cfg.attrs = attrs;
-    cfg.numAttrs = 1;
-    AB_CUDA(cudaLaunchKernelEx(&cfg, k, p));
+    // stream-K spreads the k-block iterations over every pair; plain tiles use at most one pair per tile
+    const int pairs = Traits::STREAMK ? num_sms() / 2 : (tiles < num_sms() / 2 ? tiles : num_sms() / 2);
+    tc::launch_tc(k, p, 2 * pairs, tc::threads_of<Traits>(), tc::ShapeOf2<Traits>::SMEM, true, s);
     count_launch();
 }
 
@@ -276,6 +382,23 @@ template <int BN, bool AMN, bool BMN, bool CBF16>
 void launch_cfg(const TcParams& p, bool pair, cudaStream_t s) {
     if (pair) launch_pair<GenTraits<BN, AMN, BMN, CBF16>>(p, s);
     else launch_single<GenTraits<BN, AMN, BMN, CBF16>>(p, s);
+}
+
+// CTA-pair 256-wide variants with the extra row-sum MMA (xtra) and / or stream-K (sk).
+// Returns false for operand layouts that have no such instantiation.
+bool dispatch_ext(const TcParams& p, bool amn, bool bmn, bool cbf16, bool xtra, bool sk, cudaStream_t s) {
+    if (xtra) {
+        if (!(amn && bmn && !cbf16) || sk) return false;
+        launch_pair<GenTraits<256, true, true, false, true, false>>(p, s);
+        return true;
+    }
+    if (!sk) return false;
+    const int key = (amn ? 4 : 0) | (bmn ? 2 : 0) | (cbf16 ? 1 : 0);
+    switch (key) {
+        case 2: launch_pair<GenTraits<256, false, true, false, false, true>>(p, s); return true;  // dgrad, fp32 out
+        case 3: launch_pair<GenTraits<256, false, true, true, false, true>>(p, s); return true;   // dgrad, bf16 out
+        default: return false;
+    }
 }
 
 template <int BN>
@@ -296,7 +419,7 @@ void dispatch(const TcParams& p, bool amn, bool bmn, bool cbf16, bool pair, cuda
 struct PlanKey {
     const void* a[2]; const void* b[2];
     int64_t lda[2], ldb[2];
-    int K[2], M, N, nseg, bn;
+    int K[2], M, N, nseg, bn, mode;
     bool amn, bmn;
     bool operator==(const PlanKey& o) const { return std::memcmp(this, &o, sizeof(PlanKey)) == 0; }
 };
@@ -311,6 +434,15 @@ struct PlanHash {
 
 }  // namespace
 
+bool g_use_xtra = true;
+bool g_use_streamk = true;
+bool g_force_ext = false;
+namespace {
+thread_local GemmWorkspace t_ws;
+}
+void set_gemm_workspace(const GemmWorkspace& w) { t_ws = w; }
+const GemmWorkspace& gemm_workspace() { return t_ws; }
+
 void gemm_tc(const GemmArgs& g, cudaStream_t s) {
     if (g.M <= 0 || g.N <= 0) return;
     AB_CHECK(g.nseg >= 1 && g.nseg <= 2, ADPSGD_E_DIMENSION, "gemm_tc: 1 or 2 K segments");
@@ -323,7 +455,27 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
     const bool pair = g_use_pair_mma && g.M > BM;
     const int rows = pair ? 2 * BM : BM;
     const int m_tiles = (g.M + rows - 1) / rows;
-    const int bn = (g.N > 128 && m_tiles * ((g.N + 255) / 256) >= (pair ? num_sms() / 4 : num_sms() / 2)) ? 256 : 128;
+    const int bn = (g.N > 128 && (g_force_ext || m_tiles * ((g.N + 255) / 256) >= (pair ? num_sms() / 4 : num_sms() / 2)))
+                       ? 256 : 128;
+    // bias column (g.extra, one column past n_main) by the extra row-sum MMA instead of a ragged n-tile
+    // (only when it saves a round of CTA-pair waves: the extra MMA costs a single accumulator stage)
+    const int npairs = num_sms() / 2;
+    const int rounds_plain = (m_tiles * ((g.N + bn - 1) / bn) + npairs - 1) / npairs;
+    const int rounds_xtra = (m_tiles * (g.n_main / 256) + npairs - 1) / npairs;
+    const bool xtra = g_use_xtra && g.extra && pair && bn == 256 && !g.c_bf16 && amn && bmn && g.n_main == g.N - 1 &&
+                      g.n_main % 256 == 0 && (rounds_xtra < rounds_plain || g_force_ext);
+    const int n_eff = xtra ? g.n_main : g.N;
+    const int tiles = m_tiles * ((n_eff + bn - 1) / bn);
+    int kbt = 0;
+    for (int i = 0; i < g.nseg; ++i) kbt += (g.seg[i].K + BK - 1) / BK;
+    const GemmWorkspace& wsp = gemm_workspace();
+    // stream-K when the tiles do not fill whole waves of CTA pairs -- dgrad layouts only (A K-major
+    // activations, B MN-major weights that stay L2-resident): for the long-K weight-gradient
+    // GEMMs (both operands streamed) pairs drifting apart along K lose the L2 reuse of the
+    // lockstep wave order and run slower (measured).
+    const bool sk = g_use_streamk && pair && bn == 256 && wsp.ws && !xtra && !amn && bmn && (tiles % npairs != 0 || g_force_ext) &&
+                    kbt >= 8 && wsp.floats >= static_cast<size_t>(npairs) * 2 * (256 / 32 + 1) * 128 * 32 &&
+                    wsp.flag_count >= static_cast<size_t>(npairs) * 2;
 
     static std::unordered_map<PlanKey, TcParams, PlanHash> cache;
     static std::mutex mu;
@@ -334,6 +486,7 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
         key.lda[i] = g.seg[i].a.ld; key.ldb[i] = g.seg[i].b.ld; key.K[i] = g.seg[i].K;
     }
     key.M = g.M; key.N = g.N; key.nseg = g.nseg; key.bn = bn * (pair ? 2 : 1); key.amn = amn; key.bmn = bmn;
+    key.mode = (xtra ? 1 : 0) | (sk ? 2 : 0);
 
     TcParams p;
     {
@@ -353,9 +506,9 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
                 p.kblocks[i] = (sg.K + BK - 1) / BK;
             }
             p.nseg = g.nseg;
-            p.M = g.M; p.N = g.N;
+            p.M = g.M; p.N = n_eff;
             p.m_tiles = m_tiles;
-            p.n_tiles = (g.N + bn - 1) / bn;
+            p.n_tiles = (n_eff + bn - 1) / bn;
             if (cache.size() > 4096) cache.clear();
             cache.emplace(key, p);
         }
@@ -376,6 +529,11 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
     AB_CHECK(!g.extra || (!g.c_bf16 && g.N == p.n_main + 1), ADPSGD_E_DIMENSION,
              "column redirect: fp32 output, exactly one extra column");
     p.vec_ok = ((reinterpret_cast<uintptr_t>(g.C) & 15) == 0) && ((g.ldc * esz) % 16 == 0);
+    p.sk_ws = wsp.ws;
+    p.sk_flags = wsp.flags;
+    p.sk_total = static_cast<int64_t>(tiles) * kbt;
+    if ((xtra || sk) && dispatch_ext(p, amn, bmn, g.c_bf16, xtra, sk, s)) return;
+    AB_CHECK(!xtra, ADPSGD_E_INVALID_STATE, "gemm_tc: no plain kernel for the extra-column layout");
     if (bn == 256) dispatch<256>(p, amn, bmn, g.c_bf16, pair, s);
     else dispatch<128>(p, amn, bmn, g.c_bf16, pair, s);
 }

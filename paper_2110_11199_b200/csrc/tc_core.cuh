@@ -10,6 +10,10 @@
 #include "common.cuh"
 #include "tc_ptx.cuh"
 
+namespace ab {
+extern bool g_use_pdl;  // gemm_lstm.cu: programmatic dependent launch for the tcgen05 kernels
+}
+
 namespace ab::tc {
 
 // Debug timeline (adpsgd_debug_trace): per-CTA globaltimer stamps written by the MMA and
@@ -43,6 +47,8 @@ struct TraitsBase {
     static constexpr int ACC_STAGES = 2;      // TMEM accumulator stages (ACC_STAGES * BN <= 512 columns)
     static constexpr int MMA_N = 0;           // N of one MMA instruction (0: = BN); BN / MMA_N MMAs per k-step
     static constexpr bool EPI_OVERLAY = false; // epilogue smem overlays the pipeline stages (one tile per CTA only)
+    static constexpr bool STREAMK = false;     // work items from Traits::sk_item / epilogue via Traits::epilogue_sk
+    static constexpr int EXTRA_COLS = 0;       // extra TMEM columns: row sums of A (all-ones N = 16 MMA) on extra_tile()s
     template <class P, class S>
     __device__ static void epi_begin(const P&, int, int, int, uint8_t*, uint64_t*, S) {}
     template <class P, class S>
@@ -99,6 +105,9 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // prologue done: dependents may launch; inputs of the previous kernel must be complete
+    ptx::griddep_launch();
+    ptx::griddep_wait();
 
     if (warp == 0) {
         // whole warp walks the loop (lane 0 issues); after the first tile's first STAGES loads
@@ -187,21 +196,43 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
 // Traits: BN, B_MN, num_tiles (pair tiles), kblocks, prefetch,
 //         load2(p, tile, kb, rank, sA, sB, bar_cluster_addr), epilogue2(p, tile, rank, tbase, q, lane, tempty_leader)
 // ---------------------------------------------------------------------------
-template <int BN, int EPI = 0, bool OVERLAY = false, int ACC = 2>
+template <int BN, int EPI = 0, bool OVERLAY = false, int ACC = 2, int EXTRA = 0>
 struct Shape2 {
     static constexpr int BNH = BN / 2;  // B rows held per CTA
     static constexpr int A_BYTES = kBM * kBK * 2;
     static constexpr int B_BYTES = BNH * kBK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int FIT = (kSmemBudget - (OVERLAY ? 0 : EPI) - 2048) / STAGE_BYTES;
+    static constexpr int ONES_BYTES = EXTRA ? 2048 : 0;  // all-ones bf16 B operand of the extra MMA
+    static constexpr int FIT = (kSmemBudget - (OVERLAY ? 0 : EPI) - ONES_BYTES - 2048) / STAGE_BYTES;
     static constexpr int STAGES = FIT > 8 ? 8 : FIT;
-    static constexpr int TMEM_COLS = ACC * BN < 32 ? 32 : ACC * BN;
-    static constexpr int SMEM = STAGES * STAGE_BYTES + (OVERLAY ? 0 : EPI) + 2048;
+    static constexpr int COLS = ACC * BN + EXTRA;
+    static constexpr int TMEM_COLS = COLS <= 32 ? 32 : COLS <= 64 ? 64 : COLS <= 128 ? 128 : COLS <= 256 ? 256 : 512;
+    static constexpr int SMEM = STAGES * STAGE_BYTES + (OVERLAY ? 0 : EPI) + ONES_BYTES + 2048;
     static_assert(!OVERLAY || EPI <= STAGES * STAGE_BYTES, "overlaid epilogue smem must fit in the stages");
-    static_assert(ACC * BN <= 512, "TMEM has 512 columns");
+    static_assert(COLS <= 512, "TMEM has 512 columns");
 };
 template <class T>
-using ShapeOf2 = Shape2<T::BN, T::EPI_SMEM, T::EPI_OVERLAY, T::ACC_STAGES>;
+using ShapeOf2 = Shape2<T::BN, T::EPI_SMEM, T::EPI_OVERLAY, T::ACC_STAGES, T::EXTRA_COLS>;
+
+// One unit of work of a CTA pair: k-blocks [kb0, kb1) of a tile. role: 0 = whole tile,
+// 1 = stream-K owner (holds k-block 0, adds the later segments' partials), 2 = stream-K
+// contributor (exports its partial). Default traits: whole tiles strided over the pairs.
+struct Item {
+    int tile, kb0, kb1, role;
+};
+template <class Traits, class Params>
+__device__ __forceinline__ bool next_item(const Params& p, int cid, int ncl, int it, Item& w) {
+    if constexpr (Traits::STREAMK) {
+        return Traits::sk_item(p, cid, ncl, it, w);
+    } else {
+        w.tile = cid + it * ncl;
+        if (w.tile >= Traits::num_tiles(p)) return false;
+        w.kb0 = 0;
+        w.kb1 = Traits::kblocks(p, w.tile);
+        w.role = 0;
+        return true;
+    }
+}
 
 template <class Traits, class Params>
 __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_kernel_2cta(const __grid_constant__ Params p) {
@@ -212,6 +243,7 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
     constexpr int MN = Traits::MMA_N ? Traits::MMA_N : BN;  // N per MMA instruction
     constexpr int NSUB = BN / MN;                             // MMAs per k-step (B sub-tiles of MN/2 rows per CTA)
     static_assert(NSUB == 1 || !Traits::B_MN, "split MMA-N needs a K-major B");
+    static_assert(!Traits::EXTRA_COLS || ACC == 1, "extra accumulator columns need a single accumulator stage");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
@@ -226,12 +258,12 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bblk + 160);
     uint64_t* epi_bar = reinterpret_cast<uint64_t*>(bblk + 256);
     uint8_t* epi_smem = Traits::EPI_OVERLAY ? smem : bblk + 1024;  // 1024-aligned (TMA swizzle atoms)
+    uint8_t* ones = bblk + 1024 + (Traits::EPI_OVERLAY ? 0 : Traits::EPI_SMEM);  // S::ONES_BYTES, 1024-aligned
     static_assert(STAGES <= 8 && Traits::EPI_WARPS <= 8, "barrier block layout");
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const uint32_t rank = ptx::cluster_ctarank();
     const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
-    const int num_tiles = Traits::num_tiles(p);
     if (threadIdx.x == 0) trace(p.trace, kTraceEv - 2);
 
     if (warp == 0 && lane == 0) {
@@ -241,27 +273,34 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
         ptx::fence_barrier_init();
         Traits::prefetch(p);
     }
+    if constexpr (S::ONES_BYTES > 0) {
+        for (int i = threadIdx.x; i < S::ONES_BYTES / 16; i += blockDim.x)
+            ptx::st_shared_v4(ptx::smem_u32(ones) + 16 * i, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
+        ptx::fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
+    }
     if (warp == 1) ptx::tmem_alloc_2sm(tmem_slot, S::TMEM_COLS);
     ptx::tc_fence_before();
     ptx::cluster_sync();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    ptx::griddep_launch();
+    ptx::griddep_wait();
 
     if (warp == 0) {
         int stage = 0;
         uint32_t phase = 0;
         bool released = false;
-        for (int tile = cid; tile < num_tiles; tile += ncl) {
-            const int nkb = Traits::kblocks(p, tile);
-            for (int kb = 0; kb < nkb; ++kb) {
+        Item w;
+        for (int it = 0; next_item<Traits>(p, cid, ncl, it, w); ++it) {
+            for (int kb = w.kb0; kb < w.kb1; ++kb) {
                 if (lane == 0) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
                     const uint32_t bar0 = ptx::mapa(ptx::smem_u32(&full[stage]), 0);
                     if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * S::STAGE_BYTES);
-                    Traits::load2(p, tile, kb, rank, sA + stage * S::A_BYTES, sB + stage * S::B_BYTES, bar0);
+                    Traits::load2(p, w.tile, kb, rank, sA + stage * S::A_BYTES, sB + stage * S::B_BYTES, bar0);
                 }
                 if (++stage == STAGES) { stage = 0; phase ^= 1; }
-                if (!released && (kb + 1 == STAGES || kb + 1 == nkb)) {
+                if (!released && (kb + 1 - w.kb0 == STAGES || kb + 1 == w.kb1)) {
                     __syncwarp();
                     ptx::named_arrive(1, 32 + 32 * Traits::EPI_WARPS);
                     released = true;
@@ -272,20 +311,22 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
     } else if (warp == 1) {
         if (lane == 0 && rank == 0) {
             constexpr uint32_t idesc = ptx::idesc_bf16_f32(2 * kBM, MN, Traits::A_MN, Traits::B_MN);
+            constexpr uint32_t idesc_x = ptx::idesc_bf16_f32(2 * kBM, 16, Traits::A_MN, false);
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
             uint32_t aphase = 0;
-            int it = 0;
-            for (int tile = cid; tile < num_tiles; tile += ncl, ++it) {
-                const int nkb = Traits::kblocks(p, tile);
+            Item w;
+            for (int it = 0; next_item<Traits>(p, cid, ncl, it, w); ++it) {
                 ptx::mbar_wait(&tempty[acc], aphase ^ 1);
                 ptx::tc_fence_after();
                 trace(p.trace, 4 * it + 0);
                 const uint32_t tmem_d = tmem_base + acc * BN;
-                for (int kb = 0; kb < nkb; ++kb) {
+                bool extra = false;
+                if constexpr (Traits::EXTRA_COLS > 0) extra = Traits::extra_tile(p, w.tile);
+                for (int kb = w.kb0; kb < w.kb1; ++kb) {
                     ptx::mbar_wait(&full[stage], phase);
-                    if (kb == 0) trace(p.trace, 4 * it + 1);
+                    if (kb == w.kb0) trace(p.trace, 4 * it + 1);
                     ptx::tc_fence_after();
                     const uint32_t a_addr = ptx::smem_u32(sA + stage * S::A_BYTES);
                     const uint32_t b_addr = ptx::smem_u32(sB + stage * S::B_BYTES);
@@ -295,11 +336,18 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
                                                          : ptx::umma_desc_sw128(a_addr + kk * 32, 16, 1024);
                         const uint64_t bd = Traits::B_MN ? ptx::umma_desc_sw128(b_addr + kk * 2048, 64 * kBK * 2, 1024)
                                                          : ptx::umma_desc_sw128(b_addr + kk * 32, 16, 1024);
+                        const bool accum = kb != w.kb0 || kk != 0;
 #pragma unroll
                         for (int sub = 0; sub < NSUB; ++sub) {
                             // sub-MMA sub: B rows [sub MN/2, +MN/2) of this CTA's stage -> TMEM cols [sub MN, +MN)
                             const uint64_t bds = bd + static_cast<uint64_t>((sub * (MN / 2) * kBK * 2) >> 4);
-                            ptx::mma_bf16_2sm(tmem_d + sub * MN, ad, bds, idesc, (kb | kk) != 0);
+                            ptx::mma_bf16_2sm(tmem_d + sub * MN, ad, bds, idesc, accum);
+                        }
+                        if constexpr (Traits::EXTRA_COLS > 0) {
+                            // row sums of A: an N = 16 MMA against an all-ones K-major B -> TMEM cols [BN, BN + 16)
+                            if (extra)
+                                ptx::mma_bf16_2sm(tmem_d + BN, ad, ptx::umma_desc_sw128(ptx::smem_u32(ones) + kk * 32, 16, 1024),
+                                                  idesc_x, accum);
                         }
                     }
                     ptx::mma_commit_2sm(&empty[stage]);
@@ -317,15 +365,18 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
         const uint32_t tempty0 = ptx::mapa(ptx::smem_u32(&tempty[0]), 0);
         int acc = 0;
         uint32_t aphase = 0, ephase = 0;
-        int it = 0;
         uint8_t* est = epi_smem + e * (Traits::EPI_WARPS ? Traits::EPI_SMEM / Traits::EPI_WARPS : 0);
         ptx::named_sync(1, 32 + 32 * Traits::EPI_WARPS);
-        for (int tile = cid; tile < num_tiles; tile += ncl, ++it) {
-            Traits::epi_begin2(p, tile, rank, q, lane, est, &epi_bar[2 * e], slot);
+        Item w;
+        for (int it = 0; next_item<Traits>(p, cid, ncl, it, w); ++it) {
+            Traits::epi_begin2(p, w.tile, rank, q, lane, est, &epi_bar[2 * e], slot);
             ptx::mbar_wait(&tfull[acc], aphase);
             ptx::tc_fence_after();
             const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
-            Traits::epilogue2(p, tile, rank, tbase, q, lane, tempty0 + acc * 8, est, &epi_bar[2 * e], ephase, slot);
+            if constexpr (Traits::STREAMK)
+                Traits::epilogue_sk(p, w, cid, rank, tbase, q, lane, tempty0 + acc * 8, slot);
+            else
+                Traits::epilogue2(p, w.tile, rank, tbase, q, lane, tempty0 + acc * 8, est, &epi_bar[2 * e], ephase, slot);
             if (e == 0 && lane == 0) trace(p.trace, 4 * it + 3);
             if (++acc == ACC) { acc = 0; aphase ^= 1; }
         }
@@ -462,6 +513,35 @@ __device__ __forceinline__ void release_acc(uint64_t* tempty, int lane) {
     ptx::tc_fence_before();
     __syncwarp();
     if (lane == 0) ptx::mbar_arrive(tempty);
+}
+
+// Host: launch a persistent tcgen05 kernel (optionally as 2-CTA clusters) with programmatic
+// dependent launch, so its prologue (barrier init, TMEM alloc, tensor-map prefetch) overlaps
+// the previous kernel's tail; the kernel griddep_wait()s before touching dependent data.
+template <class P>
+inline void launch_tc(void (*kern)(P), const P& p, int grid, int threads, int smem, bool pair, cudaStream_t s) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attrs[2];
+    int n = 0;
+    if (pair) {
+        attrs[n].id = cudaLaunchAttributeClusterDimension;
+        attrs[n].val.clusterDim.x = 2;
+        attrs[n].val.clusterDim.y = 1;
+        attrs[n].val.clusterDim.z = 1;
+        ++n;
+    }
+    if (g_use_pdl) {
+        attrs[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attrs[n].val.programmaticStreamSerializationAllowed = 1;
+        ++n;
+    }
+    cfg.attrs = attrs;
+    cfg.numAttrs = n;
+    AB_CUDA(cudaLaunchKernelEx(&cfg, kern, p));
 }
 
 }  // namespace ab::tc

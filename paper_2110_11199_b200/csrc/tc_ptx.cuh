@@ -50,6 +50,11 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* m
         : "memory");
 }
 
+// Programmatic dependent launch: let the next kernel on the stream start its prologue now /
+// wait until the previous kernel's memory is complete and visible.
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // CTA named barrier 1: producer warp arrives, epilogue warps sync (whole warps only).
 __device__ __forceinline__ void named_arrive(uint32_t id, uint32_t nthreads) {
     asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");

@@ -90,6 +90,30 @@ def test_fused_softmax_ce_ragged_class_tiles(oracle_mod, classes):
     assert np.linalg.norm(grad - ograd) / np.linalg.norm(ograd) <= 5e-2
 
 
+@pytest.mark.parametrize("force", ["0", "1"])
+def test_extra_column_and_streamk_gemms(oracle_mod, monkeypatch, force):
+    """ADPSGD_FORCE_EXT=1 routes every eligible weight-gradient GEMM with a bias column through the
+    extra row-sum MMA (all-ones N = 16 B operand) and every eligible dgrad GEMM through stream-K
+    (CTA pairs splitting tiles along K, partials summed by the tile's k-block-0 owner); the
+    gradient must match the oracle (bf16 tolerance) and the default kernels closely."""
+    O = oracle_mod
+    m = ModelDesc(layers=2, hidden=128, bidirectional=True, input_dim=40, proj=256, classes=520, unroll=5)
+    feats, labels = _data(m)
+    M = 200  # T * M = 1000 frames: several 256-row pair tiles with a ragged last one
+    rng = np.random.default_rng(21)
+    idx = rng.integers(0, 40, size=M).astype(np.int32)
+    monkeypatch.setenv("ADPSGD_FORCE_EXT", force)
+    g = LearnerGroup(m, StrategyConfig(learners=1, batch=M, seed=1), precision=Precision.BF16)
+    g.set_dataset(feats, labels, 40)
+    w = np.random.default_rng(23).normal(0, 0.1, g.D)
+    loss, grad = g.gradient(w, idx)
+    g.close()
+    oloss, ograd = O.lstm_loss_grad(_odesc(O, m), w, feats, labels, idx)
+    assert np.isfinite(loss) and np.all(np.isfinite(grad))
+    assert abs(loss - oloss) <= 1e-2 * oloss
+    assert np.linalg.norm(grad - ograd) / np.linalg.norm(ograd) <= 5e-2
+
+
 @pytest.mark.parametrize("bidir,hidden,M,T", [(True, 64, 136, 9), (False, 64, 136, 9), (True, 256, 300, 5),
                                                (False, 128, 260, 4)])
 def test_fused_lstm_kernels_match_oracle_and_unfused(oracle_mod, monkeypatch, bidir, hidden, M, T):
