@@ -118,6 +118,7 @@ Ctx::Ctx(const adpsgd_config& c) : cfg(c) {
     if (const char* e = std::getenv("ADPSGD_NO_STREAMK")) g_use_streamk = e[0] == '0';
     if (const char* e = std::getenv("ADPSGD_NO_XTRA")) g_use_xtra = e[0] == '0';
     if (const char* e = std::getenv("ADPSGD_FORCE_EXT")) g_force_ext = e[0] == '1';
+    if (const char* e = std::getenv("ADPSGD_NO_WIDE_GEMM")) g_use_wide_gemm = e[0] == '0';
 
     AB_CUDA(cudaSetDevice(c.device));
     AB_CUDA(cudaStreamCreateWithFlags(&s_main, cudaStreamNonBlocking));
@@ -151,8 +152,8 @@ Ctx::Ctx(const adpsgd_config& c) : cfg(c) {
         ce_part = static_cast<float2*>(alloc(ce_part_elems(static_cast<int>(TB), lay.C) * sizeof(float2)));
         ce_zlab = static_cast<float*>(alloc(TB * sizeof(float)));
         ce_lse = static_cast<float*>(alloc(TB * sizeof(float)));
-        {   // stream-K scratch: (SMs / 2) pairs x 2 CTAs x (8 + 1) chunks x 128 rows x 32 fp32
-            gemm_ws.floats = static_cast<size_t>(num_sms() / 2) * 2 * 9 * 128 * 32;
+        {   // stream-K scratch: (SMs / 2) pairs x 2 CTAs x (16 + 1) chunks x 128 rows x 32 fp32
+            gemm_ws.floats = static_cast<size_t>(num_sms() / 2) * 2 * 17 * 128 * 32;
             gemm_ws.ws = static_cast<float*>(alloc(gemm_ws.floats * sizeof(float)));
             gemm_ws.flag_count = static_cast<size_t>(num_sms());
             gemm_ws.flags = static_cast<unsigned int*>(alloc(gemm_ws.flag_count * sizeof(unsigned int)));

@@ -42,7 +42,7 @@ struct GemmArgs {
 };
 
 // Stream-K scratch of the calling thread's engine (set before its GEMMs run; see gemm_tc.cu):
-// ws >= (SMs/2) * 2 * 9 * 128 * 32 floats, flags >= SMs u32 zeroed once. ws == nullptr: no stream-K.
+// ws >= (SMs/2) * 2 * 17 * 128 * 32 floats, flags >= SMs u32 zeroed once. ws == nullptr: no stream-K.
 struct GemmWorkspace {
     float* ws = nullptr;
     size_t floats = 0;
@@ -53,7 +53,8 @@ void set_gemm_workspace(const GemmWorkspace& w);
 const GemmWorkspace& gemm_workspace();
 extern bool g_use_xtra;
 extern bool g_use_streamk;
-extern bool g_force_ext;  // tests: take the extra-column / stream-K kernels whenever the layout allows
+extern bool g_force_ext;
+extern bool g_use_wide_gemm;  // 256 x 512 CTA-pair tiles for large stream-K dgrads  // tests: take the extra-column / stream-K kernels whenever the layout allows
 
 // fp32 operands, fp32 or bf16 output, any majorness (gemm_simt.cu).
 void gemm_simt(const GemmArgs& g, cudaStream_t s);

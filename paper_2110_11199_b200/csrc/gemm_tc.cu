@@ -64,7 +64,8 @@ struct GenTraits : tc::TraitsBase {
     static constexpr bool A_MN = AMN;
     static constexpr bool B_MN = BMN;
     static constexpr int EXTRA_COLS = XTRA ? 32 : 0;
-    static constexpr int ACC_STAGES = XTRA ? 1 : 2;
+    static constexpr int ACC_STAGES = (XTRA || BN_ > 256) ? 1 : 2;
+    static constexpr int MMA_N = BN_ > 256 ? 256 : 0;
     static constexpr bool STREAMK = SK;
     static constexpr int NCH = BN / 32 + (XTRA ? 1 : 0);  // 32-column chunks of a partial (incl. the extra)
     __device__ static bool extra_tile(const TcParams& p, int tile) { return XTRA && tile / p.m_tiles == 0; }
@@ -118,10 +119,12 @@ struct GenTraits : tc::TraitsBase {
         body(p, m0 + q * 32, n0, tbase, lane, [&] { tc::release_acc(tempty, lane); }, sl, false, [](int, uint32_t*) {});
     }
     // ---- CTA pair: 256 x BN tiles, rank r holds A rows [m0 + 128 r, +128) and B rows [n0 + r BN/2, +BN/2) ----
+    // BN = 512: two N = 256 sub-MMAs per k-step; for sub-MMA u CTA r holds B columns
+    // [n_base + 256 u + 128 r, +128) at smem offset u * 16 KB (TMEM cols [256 u, +256) = tile cols).
     __device__ static void load2(const TcParams& p, int tile, int kb, uint32_t rank, uint8_t* sA, uint8_t* sB,
                                  uint32_t bar) {
         const int m0 = (tile % p.m_tiles) * 2 * BM + BM * rank;
-        const int n0 = (tile / p.m_tiles) * BN + (BN / 2) * rank;
+        const int nb = (tile / p.m_tiles) * BN;
         int s, k0;
         seg_of(p, kb, s, k0);
         if (AMN) {
@@ -130,12 +133,17 @@ struct GenTraits : tc::TraitsBase {
         } else {
             ptx::tma_load_2d_2sm(sA, &p.ta[s], bar, k0, m0);
         }
-        if (BMN) {
+        constexpr int SUBN = BN > 256 ? 256 : BN;  // N of one sub-MMA
 #pragma unroll
-            for (int j = 0; j < BN / 128; ++j)
-                ptx::tma_load_2d_2sm(sB + j * 64 * BK * 2, &p.tb[s], bar, n0 + 64 * j, k0);
-        } else {
-            ptx::tma_load_2d_2sm(sB, &p.tb[s], bar, k0, n0);
+        for (int u = 0; u < BN / SUBN; ++u) {
+            const int n0 = nb + u * SUBN + (SUBN / 2) * static_cast<int>(rank);
+            uint8_t* dst = sB + u * (SUBN / 2) * BK * 2;
+            if (BMN) {
+#pragma unroll
+                for (int j = 0; j < SUBN / 128; ++j) ptx::tma_load_2d_2sm(dst + j * 64 * BK * 2, &p.tb[s], bar, n0 + 64 * j, k0);
+            } else {
+                ptx::tma_load_2d_2sm(dst, &p.tb[s], bar, k0, n0);
+            }
         }
     }
     __device__ static void epilogue2(const TcParams& p, int tile, uint32_t rank, uint32_t tbase, int q, int lane,
@@ -386,17 +394,21 @@ void launch_cfg(const TcParams& p, bool pair, cudaStream_t s) {
 
 // CTA-pair 256-wide variants with the extra row-sum MMA (xtra) and / or stream-K (sk).
 // Returns false for operand layouts that have no such instantiation.
+template <int BN>
 bool dispatch_ext(const TcParams& p, bool amn, bool bmn, bool cbf16, bool xtra, bool sk, cudaStream_t s) {
     if (xtra) {
         if (!(amn && bmn && !cbf16) || sk) return false;
-        launch_pair<GenTraits<256, true, true, false, true, false>>(p, s);
-        return true;
+        if constexpr (BN == 256) {
+            launch_pair<GenTraits<256, true, true, false, true, false>>(p, s);
+            return true;
+        }
+        return false;
     }
     if (!sk) return false;
     const int key = (amn ? 4 : 0) | (bmn ? 2 : 0) | (cbf16 ? 1 : 0);
     switch (key) {
-        case 2: launch_pair<GenTraits<256, false, true, false, false, true>>(p, s); return true;  // dgrad, fp32 out
-        case 3: launch_pair<GenTraits<256, false, true, true, false, true>>(p, s); return true;   // dgrad, bf16 out
+        case 2: launch_pair<GenTraits<BN, false, true, false, false, true>>(p, s); return true;  // dgrad, fp32 out
+        case 3: launch_pair<GenTraits<BN, false, true, true, false, true>>(p, s); return true;   // dgrad, bf16 out
         default: return false;
     }
 }
@@ -437,6 +449,7 @@ struct PlanHash {
 bool g_use_xtra = true;
 bool g_use_streamk = true;
 bool g_force_ext = false;
+bool g_use_wide_gemm = true;
 namespace {
 thread_local GemmWorkspace t_ws;
 }
@@ -455,27 +468,35 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
     const bool pair = g_use_pair_mma && g.M > BM;
     const int rows = pair ? 2 * BM : BM;
     const int m_tiles = (g.M + rows - 1) / rows;
-    const int bn = (g.N > 128 && (g_force_ext || m_tiles * ((g.N + 255) / 256) >= (pair ? num_sms() / 4 : num_sms() / 2)))
-                       ? 256 : 128;
+    const int bn0 = (g.N > 128 && (g_force_ext || m_tiles * ((g.N + 255) / 256) >= (pair ? num_sms() / 4 : num_sms() / 2)))
+                        ? 256 : 128;
     // bias column (g.extra, one column past n_main) by the extra row-sum MMA instead of a ragged n-tile
     // (only when it saves a round of CTA-pair waves: the extra MMA costs a single accumulator stage)
     const int npairs = num_sms() / 2;
-    const int rounds_plain = (m_tiles * ((g.N + bn - 1) / bn) + npairs - 1) / npairs;
+    const int rounds_plain = (m_tiles * ((g.N + bn0 - 1) / bn0) + npairs - 1) / npairs;
     const int rounds_xtra = (m_tiles * (g.n_main / 256) + npairs - 1) / npairs;
-    const bool xtra = g_use_xtra && g.extra && pair && bn == 256 && !g.c_bf16 && amn && bmn && g.n_main == g.N - 1 &&
+    const bool xtra = g_use_xtra && g.extra && pair && bn0 == 256 && !g.c_bf16 && amn && bmn && g.n_main == g.N - 1 &&
                       g.n_main % 256 == 0 && (rounds_xtra < rounds_plain || g_force_ext);
     const int n_eff = xtra ? g.n_main : g.N;
-    const int tiles = m_tiles * ((n_eff + bn - 1) / bn);
     int kbt = 0;
     for (int i = 0; i < g.nseg; ++i) kbt += (g.seg[i].K + BK - 1) / BK;
     const GemmWorkspace& wsp = gemm_workspace();
     // stream-K when the tiles do not fill whole waves of CTA pairs -- dgrad layouts only (A K-major
     // activations, B MN-major weights that stay L2-resident): for the long-K weight-gradient
     // GEMMs (both operands streamed) pairs drifting apart along K lose the L2 reuse of the
-    // lockstep wave order and run slower (measured).
-    const bool sk = g_use_streamk && pair && bn == 256 && wsp.ws && !xtra && !amn && bmn && (tiles % npairs != 0 || g_force_ext) &&
-                    kbt >= 8 && wsp.floats >= static_cast<size_t>(npairs) * 2 * (256 / 32 + 1) * 128 * 32 &&
-                    wsp.flag_count >= static_cast<size_t>(npairs) * 2;
+    // lockstep wave order and run slower (measured). Large dgrads take 256 x 512 pair tiles
+    // (two N = 256 MMAs per k-step: a quarter less L2->SM operand traffic per FLOP).
+    auto sk_ok = [&](int bnx) {
+        const int t = m_tiles * ((n_eff + bnx - 1) / bnx);
+        return g_use_streamk && pair && bnx >= 256 && wsp.ws && !xtra && !amn && bmn && (t % npairs != 0 || g_force_ext) &&
+               kbt >= 8 && wsp.floats >= static_cast<size_t>(npairs) * 2 * (bnx / 32 + 1) * 128 * 32 &&
+               wsp.flag_count >= static_cast<size_t>(npairs) * 2;
+    };
+    const bool wide = g_use_wide_gemm && bn0 == 256 && g.N >= 1024 && g.N % 512 == 0 &&
+                      (m_tiles * (g.N / 512) >= npairs || g_force_ext) && sk_ok(512);
+    const int bn = wide ? 512 : bn0;
+    const int tiles = m_tiles * ((n_eff + bn - 1) / bn);
+    const bool sk = sk_ok(bn);
 
     static std::unordered_map<PlanKey, TcParams, PlanHash> cache;
     static std::mutex mu;
@@ -502,7 +523,7 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
                 if (amn) make_map(&p.ta[i], sg.a.ptr, g.M, sg.K, sg.a.ld, BK);
                 else make_map(&p.ta[i], sg.a.ptr, sg.K, g.M, sg.a.ld, BM);
                 if (bmn) make_map(&p.tb[i], sg.b.ptr, g.N, sg.K, sg.b.ld, BK);
-                else make_map(&p.tb[i], sg.b.ptr, sg.K, g.N, sg.b.ld, pair ? bn / 2 : bn);
+                else make_map(&p.tb[i], sg.b.ptr, sg.K, g.N, sg.b.ld, pair ? (bn > 256 ? 128 : bn / 2) : bn);
                 p.kblocks[i] = (sg.K + BK - 1) / BK;
             }
             p.nseg = g.nseg;
@@ -532,7 +553,12 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
     p.sk_ws = wsp.ws;
     p.sk_flags = wsp.flags;
     p.sk_total = static_cast<int64_t>(tiles) * kbt;
-    if ((xtra || sk) && dispatch_ext(p, amn, bmn, g.c_bf16, xtra, sk, s)) return;
+    if (bn == 512) {
+        AB_CHECK(dispatch_ext<512>(p, amn, bmn, g.c_bf16, xtra, sk, s), ADPSGD_E_INVALID_STATE,
+                 "gemm_tc: no 512-wide kernel for this layout");
+        return;
+    }
+    if ((xtra || sk) && dispatch_ext<256>(p, amn, bmn, g.c_bf16, xtra, sk, s)) return;
     AB_CHECK(!xtra, ADPSGD_E_INVALID_STATE, "gemm_tc: no plain kernel for the extra-column layout");
     if (bn == 256) dispatch<256>(p, amn, bmn, g.c_bf16, pair, s);
     else dispatch<128>(p, amn, bmn, g.c_bf16, pair, s);

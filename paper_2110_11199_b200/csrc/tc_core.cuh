@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
     constexpr int ACC = Traits::ACC_STAGES;
     constexpr int MN = Traits::MMA_N ? Traits::MMA_N : BN;  // N per MMA instruction
     constexpr int NSUB = BN / MN;                             // MMAs per k-step (B sub-tiles of MN/2 rows per CTA)
-    static_assert(NSUB == 1 || !Traits::B_MN, "split MMA-N needs a K-major B");
+    // (sub-MMA u's B sub-tile sits at u * (MN/2) * kBK * 2 bytes for K-major and MN-major B alike)
     static_assert(!Traits::EXTRA_COLS || ACC == 1, "extra accumulator columns need a single accumulator stage");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));

@@ -114,6 +114,28 @@ def test_extra_column_and_streamk_gemms(oracle_mod, monkeypatch, force):
     assert np.linalg.norm(grad - ograd) / np.linalg.norm(ograd) <= 5e-2
 
 
+def test_wide_streamk_dgrad_matches_default_kernels(monkeypatch):
+    """H = 512: the layer-2 input dgrad (N = 2H = 1024, K = 8H) takes 256 x 512 CTA-pair tiles with
+    stream-K under ADPSGD_FORCE_EXT=1; its gradient must agree with the default kernels' (same
+    bf16 operands, different fp32 summation order)."""
+    m = ModelDesc(layers=2, hidden=512, bidirectional=True, input_dim=40, proj=256, classes=64, unroll=3)
+    feats, labels = _data(m)
+    M = 96
+    idx = np.random.default_rng(31).integers(0, 40, size=M).astype(np.int32)
+    out = {}
+    for force in ("0", "1"):
+        monkeypatch.setenv("ADPSGD_FORCE_EXT", force)
+        g = LearnerGroup(m, StrategyConfig(learners=1, batch=M, seed=1), precision=Precision.BF16)
+        g.set_dataset(feats, labels, 40)
+        w = np.random.default_rng(32).normal(0, 0.05, g.D)
+        out[force] = g.gradient(w, idx)
+        g.close()
+    (l0, g0), (l1, g1) = out["0"], out["1"]
+    assert np.all(np.isfinite(g1))
+    assert abs(l1 - l0) <= 1e-4 * abs(l0)
+    assert np.linalg.norm(g1 - g0) / np.linalg.norm(g0) <= 1e-2
+
+
 @pytest.mark.parametrize("bidir,hidden,M,T", [(True, 64, 136, 9), (False, 64, 136, 9), (True, 256, 300, 5),
                                                (False, 128, 260, 4)])
 def test_fused_lstm_kernels_match_oracle_and_unfused(oracle_mod, monkeypatch, bidir, hidden, M, T):
