@@ -512,14 +512,17 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
         }
         for (int d = 0; d < nd; ++d) {
             const DirOff& o = lay.dir[l][d];
+            // one-wave 256 x 512 tiles for dW_ih (the bias then by a column sum of dZ) when the
+            // 256-wide tiles plus the ones column would need a second wave (gemm_wgrad_wide)
+            const bool fold_ih = fold_bias && !gemm_wgrad_wide(G4, lay.in_dim[l]);
             {   // dW_ih = dZ_d^T Xin
                 GemmArgs g;
-                g.M = G4; g.N = lay.in_dim[l] + (fold_bias ? 1 : 0);
+                g.M = G4; g.N = lay.in_dim[l] + (fold_ih ? 1 : 0);
                 g.seg[0].a = {off_ptr(dZ, d * G4, es), nd4H, true};
                 g.seg[0].b = {Xin, ldx, true};
                 g.seg[0].K = static_cast<int>(TB);
                 g.C = grad + o.w_ih; g.ldc = lay.in_dim[l];
-                if (fold_bias) { g.n_main = lay.in_dim[l]; g.extra = grad + o.b; }  // ones column of the input -> db
+                if (fold_ih) { g.n_main = lay.in_dim[l]; g.extra = grad + o.b; }  // ones column of the input -> db
                 g.tag = PROF_GEMM_WGRAD;
                 gemm(bf, g, s);
             }
@@ -537,7 +540,7 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
             } else {
                 AB_CUDA(cudaMemsetAsync(grad + o.w_hh, 0, sizeof(float) * G4 * H, s));
             }
-            if (!fold_bias) colsum(off_ptr(dZ, d * G4, es), nd4H, static_cast<int>(TB), G4, grad + o.b);
+            if (!fold_ih) colsum(off_ptr(dZ, d * G4, es), nd4H, static_cast<int>(TB), G4, grad + o.b);
         }
         if (l > 0) {  // dXin = sum_d dZ_d W_ih_d
             GemmArgs g;

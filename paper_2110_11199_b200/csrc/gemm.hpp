@@ -54,7 +54,8 @@ const GemmWorkspace& gemm_workspace();
 extern bool g_use_xtra;
 extern bool g_use_streamk;
 extern bool g_force_ext;
-extern bool g_use_wide_gemm;  // 256 x 512 CTA-pair tiles for large stream-K dgrads  // tests: take the extra-column / stream-K kernels whenever the layout allows
+extern bool g_use_wide_gemm;  // 256 x 512 CTA-pair tiles for large stream-K dgrads
+bool gemm_wgrad_wide(int M, int N);  // see gemm_tc.cu  // tests: take the extra-column / stream-K kernels whenever the layout allows
 
 // fp32 operands, fp32 or bf16 output, any majorness (gemm_simt.cu).
 void gemm_simt(const GemmArgs& g, cudaStream_t s);

@@ -396,6 +396,11 @@ void launch_cfg(const TcParams& p, bool pair, cudaStream_t s) {
 // Returns false for operand layouts that have no such instantiation.
 template <int BN>
 bool dispatch_ext(const TcParams& p, bool amn, bool bmn, bool cbf16, bool xtra, bool sk, cudaStream_t s) {
+    if (BN == 512 && !sk && !xtra) {  // one-round weight-gradient GEMMs (gemm_wgrad_wide)
+        if (!(amn && bmn && !cbf16)) return false;
+        launch_pair<GenTraits<512, true, true, false, false, false>>(p, s);
+        return true;
+    }
     if (xtra) {
         if (!(amn && bmn && !cbf16) || sk) return false;
         if constexpr (BN == 256) {
@@ -446,6 +451,17 @@ struct PlanHash {
 
 }  // namespace
 
+// Weight-gradient GEMMs [M gates x N inputs] whose 256 x 512 pair tiles fit one wave while the
+// 256-wide tiles (+ the bias column) need two: the caller then computes the bias separately.
+// Off by default: measured on B200 (6x1024 BLSTM) the one-wave 512-wide dW_ih ran 0.65 ms/step
+// slower than two waves of 256-wide tiles, before the extra bias column sums (+0.65 ms).
+// ADPSGD_FORCE_EXT=1 (tests) still takes it.
+bool gemm_wgrad_wide(int M, int N) {
+    const int npairs = num_sms() / 2;
+    const int mt = (M + 255) / 256;
+    return g_force_ext && g_use_wide_gemm && M > 128 && N >= 1024 && N % 512 == 0 && mt * (N / 512) <= npairs;
+}
+
 bool g_use_xtra = true;
 bool g_use_streamk = true;
 bool g_force_ext = false;
@@ -492,11 +508,12 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
                kbt >= 8 && wsp.floats >= static_cast<size_t>(npairs) * 2 * (bnx / 32 + 1) * 128 * 32 &&
                wsp.flag_count >= static_cast<size_t>(npairs) * 2;
     };
-    const bool wide = g_use_wide_gemm && bn0 == 256 && g.N >= 1024 && g.N % 512 == 0 &&
-                      (m_tiles * (g.N / 512) >= npairs || g_force_ext) && sk_ok(512);
+    const bool wide_wgrad = g_use_wide_gemm && amn && bmn && !g.c_bf16 && !g.extra && gemm_wgrad_wide(g.M, g.N);
+    const bool wide = wide_wgrad || (g_use_wide_gemm && bn0 == 256 && g.N >= 1024 && g.N % 512 == 0 &&
+                                     (m_tiles * (g.N / 512) >= npairs || g_force_ext) && sk_ok(512));
     const int bn = wide ? 512 : bn0;
     const int tiles = m_tiles * ((n_eff + bn - 1) / bn);
-    const bool sk = sk_ok(bn);
+    const bool sk = !wide_wgrad && sk_ok(bn);
 
     static std::unordered_map<PlanKey, TcParams, PlanHash> cache;
     static std::mutex mu;
