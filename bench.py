@@ -69,12 +69,47 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    """SM clocks + clock-event (throttle) reasons sampled every 20 ms during the timed region
+    (NVML via nvidia_ml_py; nvidia-smi -lms 200 as the fallback)."""
+
+    _BITS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
 
     def __init__(self, device: int):
         self.device, self.proc, self.lines = device, None, []
+        self.samples, self.max_mhz, self.reason_bits = [], None, 0
+        self._stop = threading.Event()
+        self._thread = None
+
+    def _nvml_handle(self):
+        import pynvml
+        pynvml.nvmlInit()
+        idx = self.device
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+        if vis:  # NVML enumerates all GPUs; map the CUDA ordinal through the visible list
+            ids = [v.strip() for v in vis.split(",") if v.strip()]
+            if self.device < len(ids) and ids[self.device].isdigit():
+                idx = int(ids[self.device])
+        return pynvml, pynvml.nvmlDeviceGetHandleByIndex(idx)
+
+    def _poll(self, nv, h):
+        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self._stop.is_set():
+            try:
+                self.samples.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+                self.reason_bits |= int(get_reasons(h))
+            except Exception:
+                pass
+            self._stop.wait(0.02)
 
     def __enter__(self):
+        try:
+            nv, h = self._nvml_handle()
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            self._thread = threading.Thread(target=self._poll, args=(nv, h), daemon=True)
+            self._thread.start()
+            return self
+        except Exception:
+            self._thread = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
@@ -92,6 +127,9 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *exc):
+        if self._thread:
+            self._stop.set()
+            self._thread.join(timeout=2)
         if self.proc:
             self.proc.terminate()
             try:
@@ -100,6 +138,11 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
+        if self._thread is not None:
+            sm = sorted(self.samples)
+            reasons = sorted(n for n, b in self._BITS.items() if self.reason_bits & b)
+            return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                    "samples": len(sm), "source": "nvml 20 ms"}
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
@@ -117,7 +160,8 @@ class ClockSampler:
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
         sm.sort()
-        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm),
+                "source": "nvidia-smi 200 ms"}
 
 
 def dist_env():
@@ -310,8 +354,8 @@ def run_ours(a):
         "e2e": {"value": e2e_val, "unit": "frames/s", "h2d_bytes_per_step": nf * 4 + a.batch * T_UNROLL * 4,
                 "d2h_bytes_per_step": 4, "steps": e2e_steps},
         "roofline": {"bound": "tensor",
-                     "kernel": "persistent_kernel_2cta<FwdTraits>: fused recurrent GEMM [x_t|h_t-1][W_ih|W_hh]^T + LSTM "
-                               "cell, both directions, tcgen05 cta_group::2",
+                     "kernel": "persistent_kernel_2cta<FwdT<128>>: fused recurrent GEMM [x_t|h_t-1][W_ih|W_hh]^T + LSTM "
+                               "cell, both directions, 256x512 tcgen05 cta_group::2 tiles (one wave)",
                      "achieved": dom_tf, "peak": peak, "unit": "TFLOP/s", "frac": dom_tf / peak if peak else None,
                      "peak_kind": f"bf16_tflops_sustained ({pk_kind})", "traffic": traffic,
                      "algorithmic_flops_per_launch": dom_flops, "launches_per_step": dom_launches,

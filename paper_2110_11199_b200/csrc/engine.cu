@@ -36,6 +36,7 @@ extern bool g_use_pair_mma;  // gemm_lstm.cu
 extern bool g_use_wide_fwd;  // gemm_lstm.cu
 extern bool g_use_splitk_bwd;  // gemm_lstm.cu
 extern bool g_use_pdl;         // gemm_lstm.cu
+extern bool g_use_persist_bwd; // gemm_lstm.cu
 
 namespace {
 thread_local std::string g_last_error;
@@ -115,6 +116,7 @@ Ctx::Ctx(const adpsgd_config& c) : cfg(c) {
     if (const char* e = std::getenv("ADPSGD_NO_WIDE")) g_use_wide_fwd = e[0] == '0';
     if (const char* e = std::getenv("ADPSGD_NO_SPLITK")) g_use_splitk_bwd = e[0] == '0';
     if (const char* e = std::getenv("ADPSGD_NO_PDL")) g_use_pdl = e[0] == '0';
+    if (const char* e = std::getenv("ADPSGD_NO_PERSIST")) g_use_persist_bwd = e[0] == '0';
     if (const char* e = std::getenv("ADPSGD_NO_STREAMK")) g_use_streamk = e[0] == '0';
     if (const char* e = std::getenv("ADPSGD_NO_XTRA")) g_use_xtra = e[0] == '0';
     if (const char* e = std::getenv("ADPSGD_FORCE_EXT")) g_force_ext = e[0] == '1';
@@ -159,11 +161,13 @@ Ctx::Ctx(const adpsgd_config& c) : cfg(c) {
             gemm_ws.flags = static_cast<unsigned int*>(alloc(gemm_ws.flag_count * sizeof(unsigned int)));
             AB_CUDA(cudaMemsetAsync(gemm_ws.flags, 0, gemm_ws.flag_count * sizeof(unsigned int), s_main));
         }
-        if (H % 256 == 0) {
+        if (H % 128 == 0) {  // split-K (H % 256) and persistent (H % 128) BPTT exchange buffers
             const int64_t slots = lstm_bwd_splitk_slots(nd, B, H);
             sk_scratch = static_cast<float*>(alloc(static_cast<size_t>(slots) * 128 * 128 * sizeof(float)));
             sk_flags = static_cast<unsigned int*>(alloc(static_cast<size_t>(slots) * sizeof(unsigned int)));
             AB_CUDA(cudaMemsetAsync(sk_flags, 0, static_cast<size_t>(slots) * sizeof(unsigned int), s_main));
+            pb_sync = static_cast<unsigned int*>(alloc(520 * sizeof(unsigned int)));
+            AB_CUDA(cudaMemsetAsync(pb_sync, 0, 520 * sizeof(unsigned int), s_main));
         }
     } else {
         logits = static_cast<float*>(alloc(TB * lay.C * sizeof(float)));
@@ -459,7 +463,18 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
                                       static_cast<bf16*>(off_ptr(dZ, static_cast<int64_t>(t) * B * nd4H + d * G4, es)),
                                       nd4H, B, H, s);
             }
-            for (int st = 0; st + 1 < T; ++st) {
+            LstmBwdLayer PL;
+            PL.dZ = static_cast<bf16*>(dZ); PL.ld_dz = nd4H;
+            for (int d = 0; d < nd; ++d) {
+                PL.w_hh[d] = static_cast<const bf16*>(W.at(lay.dir[l][d].w_hh));
+                PL.dc_rec[d] = dc_rec + static_cast<int64_t>(d) * B * H;
+            }
+            PL.dH = dHcur; PL.lddh = ndH;
+            PL.gates = static_cast<const bf16*>(gates[l]); PL.ldg = nd4H;
+            PL.c = cst[l]; PL.ldc = ndH;
+            const bool persistent = pb_sync && sk_scratch &&
+                                    lstm_bwd_layer_persistent(PL, nd, B, H, T, s, sk_scratch, pb_sync, pb_sync + 256, pb_sync + 512);
+            for (int st = 0; !persistent && st + 1 < T; ++st) {
                 LstmBwdDir dirs[2];
                 for (int d = 0; d < nd; ++d) {
                     const int sf = T - 1 - st, sn = sf - 1;

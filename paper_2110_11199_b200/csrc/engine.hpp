@@ -74,6 +74,7 @@ struct Ctx {
     float* ce_lse = nullptr;
     float* sk_scratch = nullptr;      // split-K BPTT partial exchange (gemm_lstm.cu)
     unsigned int* sk_flags = nullptr;
+    unsigned int* pb_sync = nullptr;   // persistent BPTT: [0,256) exchange epochs, [256,512) step counters, [512] exit
     GemmWorkspace gemm_ws;             // stream-K scratch of the generic tcgen05 GEMMs
     void* dlogits = nullptr;
     float* row_loss = nullptr;

@@ -329,22 +329,35 @@ struct BwdParams {
 };
 
 // BPTT cell-backward epilogue shared by the plain and the split-K recurrent dgrad kernels.
+// Row coordinates of the epilogue I/O relative to the warp's local row: tensor maps spanning all
+// time steps (persistent BPTT) put dH / c / gates / dz at t*B + row, c_{t-1} at t'*B + row and
+// dc_rec at row; the per-step kernels use zero offsets.
+struct EpiRows {
+    int data = 0, cp = 0, dc = 0;
+    bool has_prev = false;
+};
+
 struct BwdEpi {
     // The epilogue inputs (dH, dc_rec, c, c_{t-1}, gates) do not depend on the GEMM: epi_begin
     // issues the TMA loads of this warp's first two 16-unit chunks into smem and L2-prefetches
     // the rest while the mainloop runs; body then consumes chunk c from buffer c&1 and refills
     // that buffer with chunk c+2 (two chunks in flight per warp).
     static constexpr int IN_BYTES = 12 * 1024;
-    __device__ static void issue(const BwdGroup& g, int H, int j0, int rowbase, uint8_t* in, uint64_t* bar) {
-        const bool has_prev = g.c_prev != nullptr;
-        ptx::mbar_arrive_expect_tx(bar, (has_prev ? 4 : 3) * 2048 + 4 * 1024);
+    __device__ static EpiRows rows0(const BwdGroup& g) {
+        EpiRows r;
+        r.has_prev = g.c_prev != nullptr;
+        return r;
+    }
+    __device__ static void issue(const BwdGroup& g, int H, int j0, int rowbase, uint8_t* in, uint64_t* bar, const EpiRows& r) {
+        ptx::mbar_arrive_expect_tx(bar, (r.has_prev ? 4 : 3) * 2048 + 4 * 1024);
         const uint64_t stream = ptx::policy_evict_first();
-        ptx::tma_load_2d_hint(in, &g.m_dH, bar, j0, rowbase, stream);
-        ptx::tma_load_2d(in + 2048, &g.m_dc, bar, j0, rowbase);
-        ptx::tma_load_2d_hint(in + 4096, &g.m_c, bar, j0, rowbase, stream);
-        if (has_prev) ptx::tma_load_2d_hint(in + 6144, &g.m_cp, bar, j0, rowbase, stream);
+        ptx::tma_load_2d_hint(in, &g.m_dH, bar, j0, rowbase + r.data, stream);
+        ptx::tma_load_2d(in + 2048, &g.m_dc, bar, j0, rowbase + r.dc);
+        ptx::tma_load_2d_hint(in + 4096, &g.m_c, bar, j0, rowbase + r.data, stream);
+        if (r.has_prev) ptx::tma_load_2d_hint(in + 6144, &g.m_cp, bar, j0, rowbase + r.cp, stream);
 #pragma unroll
-        for (int gi = 0; gi < 4; ++gi) ptx::tma_load_2d_hint(in + 8192 + gi * 1024, &g.m_gates, bar, gi * H + j0, rowbase, stream);
+        for (int gi = 0; gi < 4; ++gi)
+            ptx::tma_load_2d_hint(in + 8192 + gi * 1024, &g.m_gates, bar, gi * H + j0, rowbase + r.data, stream);
     }
     // SMEM: issue the first two chunks into the warp's staging smem (not with an overlaid
     // epilogue: the stages are busy during the mainloop) and L2-prefetch the rest; else
@@ -352,24 +365,28 @@ struct BwdEpi {
     template <int SPAN, bool SMEM = true>
     __device__ static void begin(const BwdParams& p, int grp, int m0, int u0, int q, int lane, uint8_t* st, uint64_t* ebar,
                                  tc::EpiSlot sl) {
-        const BwdGroup& g = p.g[grp];
+        begin_g<SPAN, SMEM>(p.g[grp], p.H, m0, u0, q, lane, st, ebar, sl, rows0(p.g[grp]));
+    }
+    template <int SPAN, bool SMEM = true>
+    __device__ static void begin_g(const BwdGroup& g, int H, int m0, int u0, int q, int lane, uint8_t* st, uint64_t* ebar,
+                                   tc::EpiSlot sl, const EpiRows& r) {
         const int rowbase = m0 + q * 32;
         const int step = 16 * sl.n;
         if (SMEM && lane == 0) {
             int b = 0;
-            for (int uc = 16 * sl.sub; uc < SPAN && b < 2; uc += step, ++b) issue(g, p.H, u0 + uc, rowbase, st + b * IN_BYTES, ebar + b);
+            for (int uc = 16 * sl.sub; uc < SPAN && b < 2; uc += step, ++b) issue(g, H, u0 + uc, rowbase, st + b * IN_BYTES, ebar + b, r);
         }
         // L2 prefetch of the remaining chunks: one box per lane
-        const bool has_prev = g.c_prev != nullptr;
+        const bool has_prev = r.has_prev;
         for (int uc = 16 * sl.sub + (SMEM ? 2 * step : 0), i = 0; uc < SPAN; uc += step, ++i) {
             const int j0 = u0 + uc;
             const int box = lane & 7;
             if ((lane >> 3) != (i & 3)) continue;
-            if (box == 0) ptx::tma_prefetch_l2_2d(&g.m_dH, j0, rowbase);
-            else if (box == 1) ptx::tma_prefetch_l2_2d(&g.m_dc, j0, rowbase);
-            else if (box == 2) ptx::tma_prefetch_l2_2d(&g.m_c, j0, rowbase);
-            else if (box == 3) { if (has_prev) ptx::tma_prefetch_l2_2d(&g.m_cp, j0, rowbase); }
-            else ptx::tma_prefetch_l2_2d(&g.m_gates, (box - 4) * p.H + j0, rowbase);
+            if (box == 0) ptx::tma_prefetch_l2_2d(&g.m_dH, j0, rowbase + r.data);
+            else if (box == 1) ptx::tma_prefetch_l2_2d(&g.m_dc, j0, rowbase + r.dc);
+            else if (box == 2) ptx::tma_prefetch_l2_2d(&g.m_c, j0, rowbase + r.data);
+            else if (box == 3) { if (has_prev) ptx::tma_prefetch_l2_2d(&g.m_cp, j0, rowbase + r.cp); }
+            else ptx::tma_prefetch_l2_2d(&g.m_gates, (box - 4) * H + j0, rowbase + r.data);
         }
     }
     // epilogue (thread = row), per 16-unit chunk: dh_rec leaves TMEM; the cell backward runs in
@@ -381,16 +398,21 @@ struct BwdEpi {
     __device__ static void body(const BwdParams& p, int grp, int m0, int u0, uint32_t tbase, int q, int lane,
                                 Rel release, uint8_t* st, uint64_t* ebar, uint32_t& ephase, tc::EpiSlot sl,
                                 const float* peer, bool preissued = true) {
-        const BwdGroup& g = p.g[grp];
-        const int H = p.H;
+        body_g<SPAN, INPLACE>(p.g[grp], p.H, m0, u0, tbase, q, lane, release, st, ebar, ephase, sl, peer, preissued,
+                              rows0(p.g[grp]));
+    }
+    template <int SPAN, bool INPLACE, class Rel>
+    __device__ static void body_g(const BwdGroup& g, int H, int m0, int u0, uint32_t tbase, int q, int lane,
+                                  Rel release, uint8_t* st, uint64_t* ebar, uint32_t& ephase, tc::EpiSlot sl,
+                                  const float* peer, bool preissued, const EpiRows& r) {
         const int rowbase = m0 + q * 32;
         uint8_t* bdz = st + 2 * IN_BYTES;         // 4 x 1 KB (INPLACE: in the chunk's input buffer)
         uint8_t* bdco = st + 2 * IN_BYTES + 4096;  // 2 KB
-        const bool has_prev = g.c_prev != nullptr;
+        const bool has_prev = r.has_prev;
         const int step = 16 * sl.n;
         if (!preissued && lane == 0) {
             int bb = 0;
-            for (int uc = 16 * sl.sub; uc < SPAN && bb < 2; uc += step, ++bb) issue(g, H, u0 + uc, rowbase, st + bb * IN_BYTES, ebar + bb);
+            for (int uc = 16 * sl.sub; uc < SPAN && bb < 2; uc += step, ++bb) issue(g, H, u0 + uc, rowbase, st + bb * IN_BYTES, ebar + bb, r);
         }
         int b = 0;
 #pragma unroll 1
@@ -460,7 +482,7 @@ struct BwdEpi {
                 // previous chunk's stores must have read the output boxes before they are rewritten
                 if (lane == 0) ptx::bulk_wait_read0();
                 __syncwarp();
-                if (lane == 0 && uc + 2 * step < SPAN) issue(g, H, j0 + 2 * step, rowbase, in, ebar + b);
+                if (lane == 0 && uc + 2 * step < SPAN) issue(g, H, j0 + 2 * step, rowbase, in, ebar + b, r);
             }
             tc::st_row_words<32>(bdz + 0 * 1024, lane, zi);
             tc::st_row_words<32>(bdz + 1 * 1024, lane, zf);
@@ -471,12 +493,12 @@ struct BwdEpi {
             __syncwarp();
             if (lane == 0) {
 #pragma unroll
-                for (int gi = 0; gi < 4; ++gi) ptx::tma_store_2d(&g.m_dz, bdz + gi * 1024, gi * H + j0, rowbase);
-                ptx::tma_store_2d(&g.m_dc, bdco, j0, rowbase);
+                for (int gi = 0; gi < 4; ++gi) ptx::tma_store_2d(&g.m_dz, bdz + gi * 1024, gi * H + j0, rowbase + r.data);
+                ptx::tma_store_2d(&g.m_dc, bdco, j0, rowbase + r.dc);
                 ptx::bulk_commit();
                 if (INPLACE && uc + 2 * step < SPAN) {
                     ptx::bulk_wait_read0();  // the stores have read the buffer: refill it with chunk c + 2
-                    issue(g, H, j0 + 2 * step, rowbase, in, ebar + b);
+                    issue(g, H, j0 + 2 * step, rowbase, in, ebar + b, r);
                 }
             }
         }
@@ -659,6 +681,157 @@ struct BwdSplitTraits : tc::TraitsBase, BwdEpi {
     }
 };
 
+// ---------------- persistent BPTT (one launch per layer) ----------------
+// All T-1 recurrent steps of both directions in one kernel. CTA pair c owns work unit
+// (m-tile, n-tile, K-half) for BOTH directions and walks items (step s, direction d) in the order
+// (0,0) (1,0)... i.e. d0(s0) d1(s0) d0(s1) d1(s1): with two TMEM accumulator stages the cell-
+// backward epilogue of one direction runs while the tensor cores work on the other direction,
+// so the epilogue hides behind the mainloop. Step s+1 of direction d needs dz_{t}(d) rows of its
+// m-tile from every (n-tile, K-half) unit: per (d, m-tile, rank) counters of finished
+// epilogues (release / acquire, proxy fences around the TMA traffic) replace kernel boundaries.
+// Split-K partials meet in a parity-double-buffered global scratch (see BwdSplitTraits).
+struct BwdPParams {
+    BwdGroup g[2];  // maps span all T*B rows: ta = dZ(d), tb = W_hh(d), m_dH / m_c / m_cp / m_gates / m_dz; m_dc = dc_rec(d)
+    int B, H, T, m_tiles, n_tiles, units, kbh;
+    float* sk_scratch;       // [pair * 2 + rank][parity][4 chunks][128 rows][16] fp32
+    unsigned int* sk_flags;  // [pair * 2 + rank] exchange epochs
+    unsigned int* dep;       // [dir][m_tile][rank] finished epilogues
+    unsigned int* exit_ctr;
+    int epi_skip;
+    unsigned long long* trace;
+};
+
+struct BwdPersistTraits : tc::TraitsBase, BwdEpi {
+    static constexpr int BN = 128;  // 256-row x 128-unit pair tiles, K halved: units per CTA = 64
+    static constexpr int EPI_WARPS = 4;
+    static constexpr int EPI_SMEM = EPI_WARPS * 24 * 1024;  // BwdEpi::body_g<64, INPLACE>
+    static constexpr int ACC_STAGES = 2;
+    static constexpr bool A_MN = false;
+    static constexpr bool B_MN = true;
+    static constexpr bool STREAMK = true;
+    struct U {
+        int mt, nt, kh, s, d;
+    };
+    __device__ static U unit(const BwdPParams& p, int cid, int it) {
+        U u;
+        u.mt = cid % p.m_tiles;
+        u.nt = (cid / p.m_tiles) % p.n_tiles;
+        u.kh = cid / (p.m_tiles * p.n_tiles);
+        u.s = it >> 1;
+        u.d = it & 1;
+        return u;
+    }
+    // time rows: A = dz_{t_src}; the cell backward runs at tn with c_{tnp}
+    __device__ static int t_src(const BwdPParams& p, const U& u) { return u.d == 0 ? p.T - 1 - u.s : u.s; }
+    __device__ static EpiRows rows(const BwdPParams& p, const U& u) {
+        const int tn = u.d == 0 ? p.T - 2 - u.s : u.s + 1;
+        const int tnp = u.d == 0 ? tn - 1 : tn + 1;
+        EpiRows r;
+        r.data = tn * p.B;
+        r.has_prev = tnp >= 0 && tnp < p.T;
+        r.cp = r.has_prev ? tnp * p.B : 0;
+        r.dc = 0;
+        return r;
+    }
+    __device__ static int num_tiles(const BwdPParams& p) { return 2 * (p.T - 1); }
+    __device__ static int kblocks(const BwdPParams& p, int) { return p.kbh; }
+    __device__ static void prefetch(const BwdPParams& p) {
+        for (int i = 0; i < 2; ++i) { ptx::tma_prefetch(&p.g[i].ta); ptx::tma_prefetch(&p.g[i].tb); }
+    }
+    __device__ static bool sk_item(const BwdPParams& p, int cid, int, int it, tc::Item& w) {
+        if (cid >= p.units || it >= 2 * (p.T - 1)) return false;
+        w.tile = it; w.kb0 = 0; w.kb1 = p.kbh; w.role = 0;
+        return true;
+    }
+    __device__ static void item_ready(const BwdPParams& p, const tc::Item& w, int cid, uint32_t rank) {
+        const U u = unit(p, cid, w.tile);
+        if (u.s == 0) return;  // dz of the first BPTT step comes from the previous kernel
+        const unsigned need = static_cast<unsigned>(u.s) * p.n_tiles * 2;
+        const unsigned* f = p.dep + (u.d * p.m_tiles + u.mt) * 2 + rank;
+        unsigned v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+        } while (v < need);
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // generic acquire -> async-proxy (TMA) reads
+    }
+    __device__ static void load2(const BwdPParams& p, int it, int kb, uint32_t rank, uint8_t* sA, uint8_t* sB,
+                                 uint32_t bar) {
+        const U u = unit(p, blockIdx.x >> 1, it);
+        const BwdGroup& g = p.g[u.d];
+        const int k0 = (u.kh * p.kbh + kb) * kBK;
+        ptx::tma_load_2d_2sm_hint(sA, &g.ta, bar, k0, t_src(p, u) * p.B + u.mt * 2 * kBM + kBM * static_cast<int>(rank),
+                                  ptx::policy_evict_first());
+        ptx::tma_load_2d_2sm_hint(sB, &g.tb, bar, u.nt * BN + static_cast<int>(rank) * (BN / 2), k0, ptx::policy_evict_last());
+    }
+    template <class S>
+    __device__ static void epi_begin2(const BwdPParams& p, int it, uint32_t rank, int q, int lane, uint8_t* st,
+                                      uint64_t* ebar, S sl) {
+        const U u = unit(p, blockIdx.x >> 1, it);
+        begin_g<64, true>(p.g[u.d], p.H, u.mt * 2 * kBM + kBM * static_cast<int>(rank), u.nt * BN + 64 * u.kh, q, lane, st,
+                          ebar, sl, rows(p, u));
+    }
+    __device__ static void epilogue_sk(const BwdPParams& p, const tc::Item& w, int cid, uint32_t rank, uint32_t tbase,
+                                       int q, int lane, uint32_t tempty_leader, tc::EpiSlot sl, uint8_t* st,
+                                       uint64_t* ebar, uint32_t& ephase) {
+        const U u = unit(p, cid, w.tile);
+        const int per = p.m_tiles * p.n_tiles;
+        const int partner = u.kh == 0 ? cid + per : cid - per;
+        const int slot = cid * 2 + static_cast<int>(rank), peer_slot = partner * 2 + static_cast<int>(rank);
+        constexpr int kHalf = 4 * 128 * 16;  // floats: 4 chunks x 128 rows x 16
+        const int par = w.tile & 1;
+        const int row = q * 32 + lane;
+        // 1) export the 64 units the partner finalises (TMEM cols [(1-kh) 64, +64))
+        float* mine = p.sk_scratch + (static_cast<int64_t>(slot) * 2 + par) * kHalf;
+#pragma unroll 1
+        for (int c = sl.sub; c < 4; c += sl.n) {
+            uint32_t v[16];
+            ptx::tmem_ld_32x32b_x16_(tbase + (1 - u.kh) * 64 + 16 * c, v);
+            ptx::tmem_ld_wait();
+            float4* dst = reinterpret_cast<float4*>(mine + (c * 128 + row) * 16);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                __stcg(dst + k, make_float4(__uint_as_float(v[4 * k]), __uint_as_float(v[4 * k + 1]),
+                                            __uint_as_float(v[4 * k + 2]), __uint_as_float(v[4 * k + 3])));
+        }
+        // 2) handshake (epoch counters, one increment per item)
+        ptx::named_sync(2, 32 * EPI_WARPS);
+        const bool leader = q == 0 && sl.sub == 0 && lane == 0;
+        if (leader) {
+            __threadfence();
+            const unsigned mine_epoch = atomicAdd(p.sk_flags + slot, 1u) + 1u;
+            unsigned seen;
+            do {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(p.sk_flags + peer_slot) : "memory");
+            } while (static_cast<int>(seen - mine_epoch) < 0);
+            __threadfence();
+        }
+        ptx::named_sync(2, 32 * EPI_WARPS);
+        // 3) cell backward on the owned 64 units (inputs pre-issued by epi_begin2)
+        body_g<64, true>(p.g[u.d], p.H, u.mt * 2 * kBM + kBM * static_cast<int>(rank), u.nt * BN + 64 * u.kh,
+                         tbase + 64 * u.kh, q, lane, [&] { tc::release_acc_2sm(tempty_leader, lane); }, st, ebar, ephase,
+                         sl, p.sk_scratch + (static_cast<int64_t>(peer_slot) * 2 + par) * kHalf, true, rows(p, u));
+        // 4) publish: this CTA's dz block of step tn is in memory (TMA stores complete)
+        if (lane == 0) {
+            ptx::bulk_wait0();
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+        ptx::named_sync(2, 32 * EPI_WARPS);
+        if (leader) {
+            __threadfence();
+            atomicAdd(p.dep + (u.d * p.m_tiles + u.mt) * 2 + rank, 1u);
+            if (w.tile == 2 * (p.T - 1) - 1) {  // last item: the last CTA out re-arms every counter
+                __threadfence();
+                if (atomicAdd(p.exit_ctr, 1u) == gridDim.x - 1) {
+                    for (int i = 0; i < 2 * p.m_tiles * 2; ++i) p.dep[i] = 0u;
+                    for (int i = 0; i < static_cast<int>(gridDim.x); ++i) p.sk_flags[i] = 0u;
+                    __threadfence();
+                    *p.exit_ctr = 0u;
+                }
+            }
+        }
+    }
+};
+
 template <class Traits, class Params>
 void launch_persistent(const Params& p, int tiles, cudaStream_t s) {
     auto k = tc::persistent_kernel<Traits, Params>;
@@ -693,6 +866,7 @@ bool g_use_pair_mma = true;
 bool g_use_wide_fwd = true;
 bool g_use_splitk_bwd = true;
 bool g_use_pdl = true;
+bool g_use_persist_bwd = true;
 
 void lstm_fwd_step(const LstmFwdDir* dirs, int ndirs, int B, int H, int ldg, int ldc, int ldh, cudaStream_t s) {
     AB_CHECK(H % 64 == 0 && ndirs >= 1 && ndirs <= 2, ADPSGD_E_DIMENSION, "fused LSTM step needs H % 64 == 0");
@@ -792,6 +966,46 @@ void lstm_bwd_step(const LstmBwdDir* dirs, int ndirs, int B, int H, int lddh, in
     else if (pair) launch_pair<BwdTraits<128>>(p, ndirs * p.m_tiles * p.n_tiles, s);
     else if (bn == 128) launch_persistent<BwdTraits<128>>(p, ndirs * p.m_tiles * p.n_tiles, s);
     else launch_persistent<BwdTraits<64>>(p, ndirs * p.m_tiles * p.n_tiles, s);
+}
+
+bool lstm_bwd_layer_persistent(const LstmBwdLayer& L, int ndirs, int B, int H, int T, cudaStream_t s, float* sk_scratch,
+                               unsigned int* sk_flags, unsigned int* dep, unsigned int* exit_ctr) {
+    const int m_tiles = B / (2 * kBM), n_tiles = H / 128;
+    const int units = m_tiles * n_tiles * 2;
+    if (!(g_use_persist_bwd && g_use_pair_mma && ndirs == 2 && T >= 2 && B % (2 * kBM) == 0 && H % 128 == 0 &&
+          units <= num_sms() / 2 && sk_scratch && sk_flags && dep && exit_ctr))
+        return false;
+    BwdPParams p;
+    std::memset(&p, 0, sizeof(p));
+    const int G4 = 4 * H;
+    for (int d = 0; d < 2; ++d) {
+        BwdGroup& g = p.g[d];
+        const int64_t TB = static_cast<int64_t>(T) * B;
+        make_map_box(&g.ta, L.dZ + d * G4, G4, TB, L.ld_dz, kBM);
+        make_map_box(&g.tb, L.w_hh[d], H, G4, H, 64);
+        make_map_gen(&g.m_dH, L.dH + d * H, true, H, TB, L.lddh, 16, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+        make_map_gen(&g.m_dc, L.dc_rec[d], true, H, B, H, 16, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+        make_map_gen(&g.m_c, L.c + d * H, true, H, TB, L.ldc, 16, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+        g.m_cp = g.m_c;
+        make_map_gen(&g.m_gates, L.gates + d * G4, false, G4, TB, L.ldg, 16, 32, CU_TENSOR_MAP_SWIZZLE_32B);
+        make_map_gen(&g.m_dz, L.dZ + d * G4, false, G4, TB, L.ld_dz, 16, 32, CU_TENSOR_MAP_SWIZZLE_32B);
+        g.kb = G4 / kBK;
+    }
+    p.B = B; p.H = H; p.T = T; p.m_tiles = m_tiles; p.n_tiles = n_tiles; p.units = units; p.kbh = G4 / kBK / 2;
+    p.sk_scratch = sk_scratch; p.sk_flags = sk_flags; p.dep = dep; p.exit_ctr = exit_ctr;
+    p.trace = trace_take();
+    const double flops = 2.0 * 2 * (T - 1) * static_cast<double>(B) * H * G4;
+    const double bytes = 2.0 * (T - 1) * (2.0 * (B + H) * G4 + static_cast<double>(B) * H * (4 + 8 + 8 + 4 + 4 + 8));
+    ProfScope ps_(s, PROF_GEMM_REC_BWD, flops, bytes);
+    auto k = tc::persistent_kernel_2cta<BwdPersistTraits, BwdPParams>;
+    static bool attr = false;
+    if (!attr) {
+        AB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::ShapeOf2<BwdPersistTraits>::SMEM));
+        attr = true;
+    }
+    tc::launch_tc(k, p, 2 * units, tc::threads_of<BwdPersistTraits>(), tc::ShapeOf2<BwdPersistTraits>::SMEM, true, s);
+    count_launch();
+    return true;
 }
 
 }  // namespace ab

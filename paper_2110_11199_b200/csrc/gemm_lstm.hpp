@@ -35,6 +35,19 @@ struct LstmBwdDir {
 };
 
 void lstm_fwd_step(const LstmFwdDir* dirs, int ndirs, int B, int H, int ldg, int ldc, int ldh, cudaStream_t s);
+// One layer's whole BPTT recurrence (both directions, steps after the first cell backward) in one
+// persistent kernel; returns false (nothing launched) when the shape is not eligible.
+struct LstmBwdLayer {
+    bf16* dZ; int64_t ld_dz;          // [T*B x 2*4H]: dz_{T-1} (dir 0) / dz_0 (dir 1) given, the rest produced
+    const bf16* w_hh[2];              // [4H x H] per direction
+    const float* dH; int64_t lddh;    // [T*B x 2H]
+    float* dc_rec[2];                 // [B x H] per direction (carries the first cell backward's dc)
+    const bf16* gates; int64_t ldg;   // [T*B x 2*4H]
+    const float* c; int64_t ldc;      // [T*B x 2H]
+};
+bool lstm_bwd_layer_persistent(const LstmBwdLayer& L, int ndirs, int B, int H, int T, cudaStream_t s, float* sk_scratch,
+                               unsigned int* sk_flags, unsigned int* dep, unsigned int* exit_ctr);
+
 // sk_scratch / sk_flags: split-K exchange buffers (lstm_bwd_splitk_slots(..) x 64 KB fp32 and
 // x 1 u32, flags zeroed once); nullptr disables the split-K variant.
 int64_t lstm_bwd_splitk_slots(int ndirs, int B, int H);

@@ -155,7 +155,8 @@ struct GenTraits : tc::TraitsBase {
     // stream-K epilogue: role 0 = plain tile; 2 = export the partial (all chunks incl. the extra)
     // and flag it; 1 = wait for the later segments' pairs, add their partials, finish the tile.
     __device__ static void epilogue_sk(const TcParams& p, const tc::Item& w, int cid, uint32_t rank, uint32_t tbase,
-                                       int q, int lane, uint32_t tempty_leader, tc::EpiSlot sl) {
+                                       int q, int lane, uint32_t tempty_leader, tc::EpiSlot sl, uint8_t*, uint64_t*,
+                                       uint32_t&) {
         const int m0 = (w.tile % p.m_tiles) * 2 * BM + BM * static_cast<int>(rank), n0 = (w.tile / p.m_tiles) * BN;
         const int row = q * 32 + lane;
         const bool xt = extra_tile(p, w.tile);

@@ -49,6 +49,10 @@ struct TraitsBase {
     static constexpr bool EPI_OVERLAY = false; // epilogue smem overlays the pipeline stages (one tile per CTA only)
     static constexpr bool STREAMK = false;     // work items from Traits::sk_item / epilogue via Traits::epilogue_sk
     static constexpr int EXTRA_COLS = 0;       // extra TMEM columns: row sums of A (all-ones N = 16 MMA) on extra_tile()s
+    // STREAMK-style item kernels: the producer lane calls item_ready(p, w, cid, rank) before the
+    // first TMA load of every item (cross-CTA dependencies of the A operand).
+    template <class P, class W>
+    __device__ static void item_ready(const P&, const W&, int, uint32_t) {}
     template <class P, class S>
     __device__ static void epi_begin(const P&, int, int, int, uint8_t*, uint64_t*, S) {}
     template <class P, class S>
@@ -292,6 +296,9 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
         bool released = false;
         Item w;
         for (int it = 0; next_item<Traits>(p, cid, ncl, it, w); ++it) {
+            if constexpr (Traits::STREAMK) {
+                if (lane == 0) Traits::item_ready(p, w, cid, rank);
+            }
             for (int kb = w.kb0; kb < w.kb1; ++kb) {
                 if (lane == 0) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
@@ -374,7 +381,7 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
             ptx::tc_fence_after();
             const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
             if constexpr (Traits::STREAMK)
-                Traits::epilogue_sk(p, w, cid, rank, tbase, q, lane, tempty0 + acc * 8, slot);
+                Traits::epilogue_sk(p, w, cid, rank, tbase, q, lane, tempty0 + acc * 8, slot, est, &epi_bar[2 * e], ephase);
             else
                 Traits::epilogue2(p, w.tile, rank, tbase, q, lane, tempty0 + acc * 8, est, &epi_bar[2 * e], ephase, slot);
             if (e == 0 && lane == 0) trace(p.trace, 4 * it + 3);

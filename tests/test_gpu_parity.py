@@ -137,12 +137,13 @@ def test_wide_streamk_dgrad_matches_default_kernels(monkeypatch):
 
 
 @pytest.mark.parametrize("bidir,hidden,M,T", [(True, 64, 136, 9), (False, 64, 136, 9), (True, 256, 300, 5),
-                                               (False, 128, 260, 4)])
+                                               (False, 128, 260, 4), (True, 128, 256, 6), (True, 256, 512, 4)])
 def test_fused_lstm_kernels_match_oracle_and_unfused(oracle_mod, monkeypatch, bidir, hidden, M, T):
     """H % 64 == 0 selects the fused tcgen05 recurrent kernels (cell fwd / bwd in the GEMM
     epilogue); they must agree with the oracle (bf16 tolerance) and with the unfused
     GEMM + pointwise path (same bf16 operands). M > 128 exercises the row mask; H % 128 == 0
-    with M > 128 selects the CTA-pair (cta_group::2) kernels, H = 256 gives several unit tiles."""
+    with M > 128 selects the CTA-pair (cta_group::2) kernels, H = 256 gives several unit tiles;
+    bidirectional with M % 256 == 0 runs the whole BPTT of a layer in the persistent kernel."""
     O = oracle_mod
     m = ModelDesc(layers=2, hidden=hidden, bidirectional=bidir, input_dim=40, proj=16, classes=48, unroll=T)
     feats, labels = _data(m)
