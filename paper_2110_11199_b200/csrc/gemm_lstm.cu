@@ -367,18 +367,18 @@ struct BwdEpi {
                                  tc::EpiSlot sl) {
         begin_g<SPAN, SMEM>(p.g[grp], p.H, m0, u0, q, lane, st, ebar, sl, rows0(p.g[grp]));
     }
-    template <int SPAN, bool SMEM = true>
+    template <int SPAN, bool SMEM = true, int NBUF = 2>
     __device__ static void begin_g(const BwdGroup& g, int H, int m0, int u0, int q, int lane, uint8_t* st, uint64_t* ebar,
                                    tc::EpiSlot sl, const EpiRows& r) {
         const int rowbase = m0 + q * 32;
         const int step = 16 * sl.n;
         if (SMEM && lane == 0) {
             int b = 0;
-            for (int uc = 16 * sl.sub; uc < SPAN && b < 2; uc += step, ++b) issue(g, H, u0 + uc, rowbase, st + b * IN_BYTES, ebar + b, r);
+            for (int uc = 16 * sl.sub; uc < SPAN && b < NBUF; uc += step, ++b) issue(g, H, u0 + uc, rowbase, st + b * IN_BYTES, ebar + b, r);
         }
         // L2 prefetch of the remaining chunks: one box per lane
         const bool has_prev = r.has_prev;
-        for (int uc = 16 * sl.sub + (SMEM ? 2 * step : 0), i = 0; uc < SPAN; uc += step, ++i) {
+        for (int uc = 16 * sl.sub + (SMEM ? NBUF * step : 0), i = 0; uc < SPAN; uc += step, ++i) {
             const int j0 = u0 + uc;
             const int box = lane & 7;
             if ((lane >> 3) != (i & 3)) continue;
@@ -401,10 +401,12 @@ struct BwdEpi {
         body_g<SPAN, INPLACE>(p.g[grp], p.H, m0, u0, tbase, q, lane, release, st, ebar, ephase, sl, peer, preissued,
                               rows0(p.g[grp]));
     }
-    template <int SPAN, bool INPLACE, class Rel>
+    // NBUF: input buffers per warp (chunks in flight); INPLACE with NBUF = 1 needs 12 KB per warp.
+    template <int SPAN, bool INPLACE, class Rel, int NBUF = 2>
     __device__ static void body_g(const BwdGroup& g, int H, int m0, int u0, uint32_t tbase, int q, int lane,
                                   Rel release, uint8_t* st, uint64_t* ebar, uint32_t& ephase, tc::EpiSlot sl,
                                   const float* peer, bool preissued, const EpiRows& r) {
+        static_assert(NBUF == 2 || INPLACE, "a single input buffer needs in-place outputs");
         const int rowbase = m0 + q * 32;
         uint8_t* bdz = st + 2 * IN_BYTES;         // 4 x 1 KB (INPLACE: in the chunk's input buffer)
         uint8_t* bdco = st + 2 * IN_BYTES + 4096;  // 2 KB
@@ -412,11 +414,11 @@ struct BwdEpi {
         const int step = 16 * sl.n;
         if (!preissued && lane == 0) {
             int bb = 0;
-            for (int uc = 16 * sl.sub; uc < SPAN && bb < 2; uc += step, ++bb) issue(g, H, u0 + uc, rowbase, st + bb * IN_BYTES, ebar + bb, r);
+            for (int uc = 16 * sl.sub; uc < SPAN && bb < NBUF; uc += step, ++bb) issue(g, H, u0 + uc, rowbase, st + bb * IN_BYTES, ebar + bb, r);
         }
         int b = 0;
 #pragma unroll 1
-        for (int uc = 16 * sl.sub; uc < SPAN; uc += step, b ^= 1) {
+        for (int uc = 16 * sl.sub; uc < SPAN; uc += step, b = (b + 1) % NBUF) {
             const int j0 = u0 + uc;
             uint8_t* in = st + b * IN_BYTES;
             uint32_t acc[16];
@@ -496,9 +498,9 @@ struct BwdEpi {
                 for (int gi = 0; gi < 4; ++gi) ptx::tma_store_2d(&g.m_dz, bdz + gi * 1024, gi * H + j0, rowbase + r.data);
                 ptx::tma_store_2d(&g.m_dc, bdco, j0, rowbase + r.dc);
                 ptx::bulk_commit();
-                if (INPLACE && uc + 2 * step < SPAN) {
-                    ptx::bulk_wait_read0();  // the stores have read the buffer: refill it with chunk c + 2
-                    issue(g, H, j0 + 2 * step, rowbase, in, ebar + b, r);
+                if (INPLACE && uc + NBUF * step < SPAN) {
+                    ptx::bulk_wait_read0();  // the stores have read the buffer: refill it with chunk c + NBUF
+                    issue(g, H, j0 + NBUF * step, rowbase, in, ebar + b, r);
                 }
             }
         }
@@ -703,8 +705,8 @@ struct BwdPParams {
 
 struct BwdPersistTraits : tc::TraitsBase, BwdEpi {
     static constexpr int BN = 128;  // 256-row x 128-unit pair tiles, K halved: units per CTA = 64
-    static constexpr int EPI_WARPS = 4;
-    static constexpr int EPI_SMEM = EPI_WARPS * 24 * 1024;  // BwdEpi::body_g<64, INPLACE>
+    static constexpr int EPI_WARPS = 8;
+    static constexpr int EPI_SMEM = EPI_WARPS * 12 * 1024;  // BwdEpi::body_g<64, INPLACE, .., NBUF = 1>
     static constexpr int ACC_STAGES = 2;
     static constexpr bool A_MN = false;
     static constexpr bool B_MN = true;
@@ -767,8 +769,8 @@ struct BwdPersistTraits : tc::TraitsBase, BwdEpi {
     __device__ static void epi_begin2(const BwdPParams& p, int it, uint32_t rank, int q, int lane, uint8_t* st,
                                       uint64_t* ebar, S sl) {
         const U u = unit(p, blockIdx.x >> 1, it);
-        begin_g<64, true>(p.g[u.d], p.H, u.mt * 2 * kBM + kBM * static_cast<int>(rank), u.nt * BN + 64 * u.kh, q, lane, st,
-                          ebar, sl, rows(p, u));
+        begin_g<64, true, 1>(p.g[u.d], p.H, u.mt * 2 * kBM + kBM * static_cast<int>(rank), u.nt * BN + 64 * u.kh, q, lane,
+                             st, ebar, sl, rows(p, u));
     }
     __device__ static void epilogue_sk(const BwdPParams& p, const tc::Item& w, int cid, uint32_t rank, uint32_t tbase,
                                        int q, int lane, uint32_t tempty_leader, tc::EpiSlot sl, uint8_t* st,
@@ -807,9 +809,11 @@ struct BwdPersistTraits : tc::TraitsBase, BwdEpi {
         }
         ptx::named_sync(2, 32 * EPI_WARPS);
         // 3) cell backward on the owned 64 units (inputs pre-issued by epi_begin2)
-        body_g<64, true>(p.g[u.d], p.H, u.mt * 2 * kBM + kBM * static_cast<int>(rank), u.nt * BN + 64 * u.kh,
-                         tbase + 64 * u.kh, q, lane, [&] { tc::release_acc_2sm(tempty_leader, lane); }, st, ebar, ephase,
-                         sl, p.sk_scratch + (static_cast<int64_t>(peer_slot) * 2 + par) * kHalf, true, rows(p, u));
+        auto rel = [&] { tc::release_acc_2sm(tempty_leader, lane); };
+        body_g<64, true, decltype(rel), 1>(p.g[u.d], p.H, u.mt * 2 * kBM + kBM * static_cast<int>(rank),
+                                          u.nt * BN + 64 * u.kh, tbase + 64 * u.kh, q, lane, rel, st, ebar, ephase, sl,
+                                          p.sk_scratch + (static_cast<int64_t>(peer_slot) * 2 + par) * kHalf, true,
+                                          rows(p, u));
         // 4) publish: this CTA's dz block of step tn is in memory (TMA stores complete)
         if (lane == 0) {
             ptx::bulk_wait0();
