@@ -12,7 +12,8 @@ from .errors import raise_for
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG_DIR)
-LIB_PATH = os.path.join(PKG_DIR, "libadpsgd_b200.so")
+# ADPSGD_LIB_PATH: an alternative build of the same library (A/B timing experiments, tools/ab.sh)
+LIB_PATH = os.environ.get("ADPSGD_LIB_PATH") or os.path.join(PKG_DIR, "libadpsgd_b200.so")
 HEADER = os.path.join(ROOT, "include", "adpsgd_b200.h")
 
 u64, i64, i32 = C.c_uint64, C.c_int64, C.c_int32

@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
         ptx::named_sync(1, 32 + 32 * Traits::EPI_WARPS);
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
             Traits::epi_begin(p, tile, q, lane, est, &epi_bar[2 * e], slot);
-            ptx::mbar_wait(&tfull[acc], aphase);
+            ptx::mbar_wait_sleep(&tfull[acc], aphase);
             ptx::tc_fence_after();
             const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
             Traits::epilogue(p, tile, tbase, q, lane, &tempty[acc], est, &epi_bar[2 * e], ephase, slot);
@@ -377,7 +377,7 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
         Item w;
         for (int it = 0; next_item<Traits>(p, cid, ncl, it, w); ++it) {
             Traits::epi_begin2(p, w.tile, rank, q, lane, est, &epi_bar[2 * e], slot);
-            ptx::mbar_wait(&tfull[acc], aphase);
+            ptx::mbar_wait_sleep(&tfull[acc], aphase);
             ptx::tc_fence_after();
             const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
             if constexpr (Traits::STREAMK)

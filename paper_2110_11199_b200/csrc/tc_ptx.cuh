@@ -18,7 +18,27 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void fence_barrier_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
+// Spin wait (latency-critical pipeline barriers: producer / MMA issue).
+#ifdef ADPSGD_WAIT_SLEEP_ALL
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity);
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) { mbar_wait_sleep(bar, parity); }
+#else
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+#endif
+// Suspending wait (long waits of otherwise idle warps, e.g. epilogue warps during the mainloop):
+// the hint lets the warp sleep in hardware instead of occupying issue slots.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
     asm volatile(
         "{\n"
