@@ -37,6 +37,7 @@ extern bool g_use_wide_fwd;  // gemm_lstm.cu
 extern bool g_use_splitk_bwd;  // gemm_lstm.cu
 extern bool g_use_pdl;         // gemm_lstm.cu
 extern bool g_use_persist_bwd; // gemm_lstm.cu
+extern bool g_use_persist_fwd; // gemm_lstm.cu
 
 namespace {
 thread_local std::string g_last_error;
@@ -117,6 +118,7 @@ Ctx::Ctx(const adpsgd_config& c) : cfg(c) {
     if (const char* e = std::getenv("ADPSGD_NO_SPLITK")) g_use_splitk_bwd = e[0] == '0';
     if (const char* e = std::getenv("ADPSGD_NO_PDL")) g_use_pdl = e[0] == '0';
     if (const char* e = std::getenv("ADPSGD_NO_PERSIST")) g_use_persist_bwd = e[0] == '0';
+    if (const char* e = std::getenv("ADPSGD_NO_PERSIST_FWD")) g_use_persist_fwd = e[0] == '0';
     if (const char* e = std::getenv("ADPSGD_NO_STREAMK")) g_use_streamk = e[0] == '0';
     if (const char* e = std::getenv("ADPSGD_NO_XTRA")) g_use_xtra = e[0] == '0';
     if (const char* e = std::getenv("ADPSGD_FORCE_EXT")) g_force_ext = e[0] == '1';
@@ -167,7 +169,7 @@ Ctx::Ctx(const adpsgd_config& c) : cfg(c) {
             sk_flags = static_cast<unsigned int*>(alloc(static_cast<size_t>(slots) * sizeof(unsigned int)));
             AB_CUDA(cudaMemsetAsync(sk_flags, 0, static_cast<size_t>(slots) * sizeof(unsigned int), s_main));
             pb_sync = static_cast<unsigned int*>(alloc(520 * sizeof(unsigned int)));
-            AB_CUDA(cudaMemsetAsync(pb_sync, 0, 520 * sizeof(unsigned int), s_main));
+            AB_CUDA(cudaMemsetAsync(pb_sync, 0, 520 * sizeof(unsigned int), s_main));  // [384,512) fwd step counters, [513] fwd exit
         }
     } else {
         logits = static_cast<float*>(alloc(TB * lay.C * sizeof(float)));
@@ -274,7 +276,20 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
         const int Kin = l == 0 ? Ipad : ndH;
         const int ldx = l == 0 ? Ipad : ldH;
         if (fused) {
-            for (int st = 0; st < T; ++st) {
+            LstmFwdLayer FL;
+            FL.x = static_cast<const bf16*>(Xin); FL.ldx = ldx; FL.Kx = Kin;
+            for (int d = 0; d < nd; ++d) {
+                int64_t ldw;
+                FL.w_ih[d] = static_cast<const bf16*>(W.wih(l, d, &ldw));
+                FL.ld_wih = ldw;
+                FL.w_hh[d] = static_cast<const bf16*>(W.at(lay.dir[l][d].w_hh));
+                FL.bias[d] = master + lay.dir[l][d].b;
+            }
+            FL.gates = static_cast<bf16*>(gates[l]); FL.ldg = nd4H;
+            FL.c = cst[l]; FL.ldc = ndH;
+            FL.h = static_cast<bf16*>(Hout[l]); FL.ldh = ldH;
+            const bool persistent = pb_sync && lstm_fwd_layer_persistent(FL, nd, B, H, T, s, pb_sync + 384, pb_sync + 513);
+            for (int st = 0; !persistent && st < T; ++st) {
                 LstmFwdDir dirs[2];
                 for (int d = 0; d < nd; ++d) {
                     const int t = d == 0 ? st : T - 1 - st;

@@ -182,15 +182,20 @@ struct FwdT : tc::TraitsBase {
     template <class Rel>
     __device__ static void body(const FwdParams& p, int grp, int m0, int u0, uint32_t tbase, int q, int lane,
                                 Rel release, uint8_t* st, uint64_t* ebar, uint32_t& ephase, tc::EpiSlot sl) {
-        const FwdGroup& g = p.g[grp];
-        const int H = p.H;
+        body_g(p.g[grp], p.H, m0, u0, tbase, q, lane, release, st, ebar, ephase, sl, p.trace, 0, 0,
+               p.g[grp].c_prev != nullptr);
+    }
+    // row_out / row_cp: row offsets of the outputs and of c_{t-1} (maps spanning all time steps)
+    template <class Rel>
+    __device__ static void body_g(const FwdGroup& g, int H, int m0, int u0, uint32_t tbase, int q, int lane,
+                                  Rel release, uint8_t* st, uint64_t* ebar, uint32_t& ephase, tc::EpiSlot sl,
+                                  unsigned long long* trace, int row_out, int row_cp, bool has_prev) {
         const int rowbase = m0 + q * 32;
-        const bool has_prev = g.c_prev != nullptr;
-        const bool tr = q == 2 && lane == 0;
+        const bool tr = trace && q == 2 && lane == 0;
         const int step = 32 * sl.n;
         auto issue_cprev = [&](int uc, int b) {
             ptx::mbar_arrive_expect_tx(ebar + b, 32 * 32 * 4);
-            ptx::tma_load_2d(st + b * 4096, &g.m_cprev, ebar + b, u0 + uc, rowbase);
+            ptx::tma_load_2d(st + b * 4096, &g.m_cprev, ebar + b, u0 + uc, rowbase + row_cp);
         };
         if (has_prev && lane == 0) issue_cprev(32 * sl.sub, 0);
         int ob = 0;
@@ -199,7 +204,7 @@ struct FwdT : tc::TraitsBase {
         for (int uc = 32 * sl.sub; uc < U; uc += step, cb ^= 1) {
             const int j0 = u0 + uc;
             if (has_prev && lane == 0 && uc + step < U) issue_cprev(uc + step, cb ^ 1);
-            if (tr) tc::trace_once(p.trace, 12 + (uc / 32) * 4 + 0);
+            if (tr) tc::trace_once(trace, 12 + (uc / 32) * 4 + 0);
             const uint8_t* cin = st + cb * 4096;
 #pragma unroll
             for (int h = 0; h < 2; ++h, ob ^= 1) {
@@ -222,7 +227,7 @@ struct FwdT : tc::TraitsBase {
 #pragma unroll
                     for (int i = 0; i < 16; ++i) cp[i] = 0.f;
                 }
-                if (tr && h == 0) tc::trace_once(p.trace, 12 + (uc / 32) * 4 + 1);
+                if (tr && h == 0) tc::trace_once(trace, 12 + (uc / 32) * 4 + 1);
                 uint8_t* out = st + 8192 + ob * 7168;
                 // the store that last used this output set (two halves ago) has read it
                 if (lane == 0) ptx::bulk_wait_read1();
@@ -292,13 +297,13 @@ struct FwdT : tc::TraitsBase {
                     const uint64_t stream = ptx::policy_evict_first();
 #pragma unroll
                     for (int gi = 0; gi < 4; ++gi)
-                        ptx::tma_store_2d_hint(&g.m_gates, out + 2048 + gi * 1024, gi * H + jb, rowbase, stream);
-                    ptx::tma_store_2d(&g.m_c, out, jb, rowbase);
-                    ptx::tma_store_2d(&g.m_h, out + 6144, jb, rowbase);
+                        ptx::tma_store_2d_hint(&g.m_gates, out + 2048 + gi * 1024, gi * H + jb, rowbase + row_out, stream);
+                    ptx::tma_store_2d(&g.m_c, out, jb, rowbase + row_out);
+                    ptx::tma_store_2d(&g.m_h, out + 6144, jb, rowbase + row_out);
                     ptx::bulk_commit();
                 }
             }
-            if (tr) tc::trace_once(p.trace, 12 + (uc / 32) * 4 + 2);
+            if (tr) tc::trace_once(trace, 12 + (uc / 32) * 4 + 2);
         }
     }
 };
@@ -683,6 +688,119 @@ struct BwdSplitTraits : tc::TraitsBase, BwdEpi {
     }
 };
 
+// ---------------- persistent forward recurrence (one launch per layer) ----------------
+// All T steps of both directions in one kernel: CTA pair c owns (m-tile, 64-unit tile) for both
+// directions and walks items (step s, direction d) = d0(s0) d1(s0) d0(s1) ...; 256 x 256 tiles
+// (64 units x 4 gates, FwdT<64> layout) with two TMEM accumulator stages, so one direction's
+// cell epilogue runs under the other direction's mainloop. Each item's k-blocks run x_t first
+// (no dependency) and h_{t-1} last: only the recurrent k-blocks wait for the previous step's
+// h rows of the m-tile (per (d, m-tile, rank) counters of finished epilogues).
+struct FwdPParams {
+    FwdGroup g[2];  // ta[0] = X (T*B rows), tb[0] = W_ih(d); ta[1] = Hout(d) (T*B rows), tb[1] = W_hh(d);
+                    // m_cprev / m_gates / m_c / m_h span T*B rows; bias per direction
+    int B, H, T, m_tiles, n_tiles, units, kbx, kbh;
+    unsigned int* dep;       // [dir][m_tile][rank] finished epilogues
+    unsigned int* exit_ctr;
+    unsigned long long* trace;
+};
+
+struct FwdPersistTraits : tc::TraitsBase {
+    using F = FwdT<64>;
+    static constexpr int BN = 256;
+    static constexpr int EPI_WARP = F::EPI_WARP;
+    static constexpr int EPI_WARPS = 4;
+    static constexpr int EPI_SMEM = EPI_WARPS * EPI_WARP;
+    static constexpr int ACC_STAGES = 2;
+    static constexpr bool A_MN = false;
+    static constexpr bool B_MN = false;
+    static constexpr bool STREAMK = true;
+    struct U {
+        int mt, nt, s, d, t, tp;
+    };
+    __device__ static U unit(const FwdPParams& p, int cid, int it) {
+        U u;
+        u.mt = cid % p.m_tiles;
+        u.nt = cid / p.m_tiles;
+        u.s = it >> 1;
+        u.d = it & 1;
+        u.t = u.d == 0 ? u.s : p.T - 1 - u.s;
+        u.tp = u.d == 0 ? u.t - 1 : u.t + 1;
+        return u;
+    }
+    __device__ static int num_tiles(const FwdPParams& p) { return 2 * p.T; }
+    __device__ static int kblocks(const FwdPParams& p, int it) { return p.kbx + ((it >> 1) > 0 ? p.kbh : 0); }
+    __device__ static void prefetch(const FwdPParams& p) {
+        for (int i = 0; i < 2; ++i)
+            for (int s = 0; s < 2; ++s) { ptx::tma_prefetch(&p.g[i].ta[s]); ptx::tma_prefetch(&p.g[i].tb[s]); }
+    }
+    __device__ static bool sk_item(const FwdPParams& p, int cid, int, int it, tc::Item& w) {
+        if (cid >= p.units || it >= 2 * p.T) return false;
+        w.tile = it; w.kb0 = 0; w.kb1 = kblocks(p, it); w.role = 0;
+        return true;
+    }
+    __device__ static void kb_ready(const FwdPParams& p, const tc::Item& w, int kb, int cid, uint32_t rank) {
+        if (kb != p.kbx) return;  // first recurrent k-block: h_{t-1} of every unit tile of this m-tile
+        const U u = unit(p, cid, w.tile);
+        const unsigned need = static_cast<unsigned>(u.s) * p.n_tiles;
+        const unsigned* f = p.dep + (u.d * p.m_tiles + u.mt) * 2 + rank;
+        unsigned v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+        } while (v < need);
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
+    __device__ static void load2(const FwdPParams& p, int it, int kb, uint32_t rank, uint8_t* sA, uint8_t* sB,
+                                 uint32_t bar) {
+        const U u = unit(p, blockIdx.x >> 1, it);
+        const FwdGroup& g = p.g[u.d];
+        const int seg = kb < p.kbx ? 0 : 1;
+        const int k0 = (seg == 0 ? kb : kb - p.kbx) * kBK;
+        const int row = (seg == 0 ? u.t : u.tp) * p.B + u.mt * 2 * kBM + kBM * static_cast<int>(rank);
+        ptx::tma_load_2d_2sm_hint(sA, &g.ta[seg], bar, k0, row, ptx::policy_evict_first());
+        const uint64_t keep = ptx::policy_evict_last();
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+            ptx::tma_load_2d_2sm_hint(sB + j * 64 * kBK * 2, &g.tb[seg], bar, k0,
+                                      (2 * static_cast<int>(rank) + j) * p.H + u.nt * 64, keep);
+    }
+    template <class S>
+    __device__ static void epi_begin2(const FwdPParams& p, int it, uint32_t rank, int q, int lane, uint8_t*, uint64_t*,
+                                      S sl) {
+        const U u = unit(p, blockIdx.x >> 1, it);
+        if (u.s == 0) return;
+        const int uc = 32 * sl.sub + 32 * sl.n * (lane & 1);
+        if (lane < 2 && uc < 64)
+            ptx::tma_prefetch_l2_2d(&p.g[u.d].m_cprev, u.nt * 64 + uc,
+                                    u.tp * p.B + u.mt * 2 * kBM + kBM * static_cast<int>(rank) + q * 32);
+    }
+    __device__ static void epilogue_sk(const FwdPParams& p, const tc::Item& w, int cid, uint32_t rank, uint32_t tbase,
+                                       int q, int lane, uint32_t tempty_leader, tc::EpiSlot sl, uint8_t* st,
+                                       uint64_t* ebar, uint32_t& ephase) {
+        const U u = unit(p, cid, w.tile);
+        F::body_g(p.g[u.d], p.H, u.mt * 2 * kBM + kBM * static_cast<int>(rank), u.nt * 64, tbase, q, lane,
+                  [&] { tc::release_acc_2sm(tempty_leader, lane); }, st, ebar, ephase, sl, nullptr, u.t * p.B,
+                  u.s > 0 ? u.tp * p.B : 0, u.s > 0);
+        // publish: this CTA's h_t (and c_t) block is in memory
+        if (lane == 0) {
+            ptx::bulk_wait0();
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+        ptx::named_sync(2, 32 * EPI_WARPS);
+        if (q == 0 && sl.sub == 0 && lane == 0) {
+            __threadfence();
+            atomicAdd(p.dep + (u.d * p.m_tiles + u.mt) * 2 + rank, 1u);
+            if (w.tile == 2 * p.T - 1) {
+                __threadfence();
+                if (atomicAdd(p.exit_ctr, 1u) == gridDim.x - 1) {
+                    for (int i = 0; i < 2 * p.m_tiles * 2; ++i) p.dep[i] = 0u;
+                    __threadfence();
+                    *p.exit_ctr = 0u;
+                }
+            }
+        }
+    }
+};
+
 // ---------------- persistent BPTT (one launch per layer) ----------------
 // All T-1 recurrent steps of both directions in one kernel. CTA pair c owns work unit
 // (m-tile, n-tile, K-half) for BOTH directions and walks items (step s, direction d) in the order
@@ -871,6 +989,7 @@ bool g_use_wide_fwd = true;
 bool g_use_splitk_bwd = true;
 bool g_use_pdl = true;
 bool g_use_persist_bwd = true;
+bool g_use_persist_fwd = true;
 
 void lstm_fwd_step(const LstmFwdDir* dirs, int ndirs, int B, int H, int ldg, int ldc, int ldh, cudaStream_t s) {
     AB_CHECK(H % 64 == 0 && ndirs >= 1 && ndirs <= 2, ADPSGD_E_DIMENSION, "fused LSTM step needs H % 64 == 0");
@@ -970,6 +1089,48 @@ void lstm_bwd_step(const LstmBwdDir* dirs, int ndirs, int B, int H, int lddh, in
     else if (pair) launch_pair<BwdTraits<128>>(p, ndirs * p.m_tiles * p.n_tiles, s);
     else if (bn == 128) launch_persistent<BwdTraits<128>>(p, ndirs * p.m_tiles * p.n_tiles, s);
     else launch_persistent<BwdTraits<64>>(p, ndirs * p.m_tiles * p.n_tiles, s);
+}
+
+bool lstm_fwd_layer_persistent(const LstmFwdLayer& L, int ndirs, int B, int H, int T, cudaStream_t s, unsigned int* dep,
+                               unsigned int* exit_ctr) {
+    const int m_tiles = B / (2 * kBM), n_tiles = H / 64;
+    const int units = m_tiles * n_tiles;
+    if (!(g_use_persist_fwd && g_use_pair_mma && ndirs == 2 && B % (2 * kBM) == 0 && H % 64 == 0 &&
+          units <= num_sms() / 2 && dep && exit_ctr))
+        return false;
+    FwdPParams p;
+    std::memset(&p, 0, sizeof(p));
+    const int64_t TB = static_cast<int64_t>(T) * B;
+    double flops = 0;
+    for (int d = 0; d < 2; ++d) {
+        FwdGroup& g = p.g[d];
+        make_map_box(&g.ta[0], L.x, L.Kx, TB, L.ldx, kBM);
+        make_map_box(&g.tb[0], L.w_ih[d], L.Kx, 4 * H, L.ld_wih, 64);
+        make_map_box(&g.ta[1], L.h + d * H, H, TB, L.ldh, kBM);
+        make_map_box(&g.tb[1], L.w_hh[d], H, 4 * H, H, 64);
+        make_map_gen(&g.m_cprev, L.c + d * H, true, H, TB, L.ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+        make_map_gen(&g.m_gates, L.gates + d * 4 * H, false, 4 * H, TB, L.ldg, 16, 32, CU_TENSOR_MAP_SWIZZLE_32B);
+        make_map_gen(&g.m_c, L.c + d * H, true, H, TB, L.ldc, 16, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+        make_map_gen(&g.m_h, L.h + d * H, false, H, TB, L.ldh, 16, 32, CU_TENSOR_MAP_SWIZZLE_32B);
+        g.bias = L.bias[d];
+        g.kb0 = (L.Kx + kBK - 1) / kBK; g.kb1 = (H + kBK - 1) / kBK; g.nseg = 2;
+        flops += 2.0 * TB * 4.0 * H * (L.Kx + H) - 2.0 * B * 4.0 * H * H;
+    }
+    p.B = B; p.H = H; p.T = T; p.m_tiles = m_tiles; p.n_tiles = n_tiles; p.units = units;
+    p.kbx = (L.Kx + kBK - 1) / kBK; p.kbh = (H + kBK - 1) / kBK;
+    p.dep = dep; p.exit_ctr = exit_ctr;
+    p.trace = trace_take();
+    const double bytes = 2.0 * T * (2.0 * (B + 4.0 * H) * (L.Kx + H) + static_cast<double>(B) * H * 22);
+    ProfScope ps_(s, PROF_GEMM_REC_FWD, flops, bytes);
+    auto k = tc::persistent_kernel_2cta<FwdPersistTraits, FwdPParams>;
+    static bool attr = false;
+    if (!attr) {
+        AB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::ShapeOf2<FwdPersistTraits>::SMEM));
+        attr = true;
+    }
+    tc::launch_tc(k, p, 2 * units, tc::threads_of<FwdPersistTraits>(), tc::ShapeOf2<FwdPersistTraits>::SMEM, true, s);
+    count_launch();
+    return true;
 }
 
 bool lstm_bwd_layer_persistent(const LstmBwdLayer& L, int ndirs, int B, int H, int T, cudaStream_t s, float* sk_scratch,

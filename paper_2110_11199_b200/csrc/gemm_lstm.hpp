@@ -35,6 +35,20 @@ struct LstmBwdDir {
 };
 
 void lstm_fwd_step(const LstmFwdDir* dirs, int ndirs, int B, int H, int ldg, int ldc, int ldh, cudaStream_t s);
+// One layer's whole forward recurrence (both directions, all T steps) in one persistent kernel;
+// returns false (nothing launched) when the shape is not eligible.
+struct LstmFwdLayer {
+    const bf16* x; int64_t ldx; int Kx;  // layer input [T*B x Kx] (row pitch ldx)
+    const bf16* w_ih[2]; int64_t ld_wih; // [4H x Kx] per direction
+    const bf16* w_hh[2];                 // [4H x H] per direction
+    const float* bias[2];                // [4H] per direction (fp32 master)
+    bf16* gates; int64_t ldg;            // [T*B x 2*4H] out
+    float* c; int64_t ldc;               // [T*B x 2H] out
+    bf16* h; int64_t ldh;                // [T*B x 2H] out (and the recurrent operand)
+};
+bool lstm_fwd_layer_persistent(const LstmFwdLayer& L, int ndirs, int B, int H, int T, cudaStream_t s, unsigned int* dep,
+                               unsigned int* exit_ctr);
+
 // One layer's whole BPTT recurrence (both directions, steps after the first cell backward) in one
 // persistent kernel; returns false (nothing launched) when the shape is not eligible.
 struct LstmBwdLayer {

@@ -53,6 +53,9 @@ struct TraitsBase {
     // first TMA load of every item (cross-CTA dependencies of the A operand).
     template <class P, class W>
     __device__ static void item_ready(const P&, const W&, int, uint32_t) {}
+    // ... and kb_ready(p, w, kb, cid, rank) before the load of k-block kb (mid-item dependencies).
+    template <class P, class W>
+    __device__ static void kb_ready(const P&, const W&, int, int, uint32_t) {}
     template <class P, class S>
     __device__ static void epi_begin(const P&, int, int, int, uint8_t*, uint64_t*, S) {}
     template <class P, class S>
@@ -301,6 +304,7 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
             }
             for (int kb = w.kb0; kb < w.kb1; ++kb) {
                 if (lane == 0) {
+                    if constexpr (Traits::STREAMK) Traits::kb_ready(p, w, kb, cid, rank);
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
                     const uint32_t bar0 = ptx::mapa(ptx::smem_u32(&full[stage]), 0);
                     if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * S::STAGE_BYTES);
