@@ -673,10 +673,7 @@ struct BwdSplitTraits : tc::TraitsBase, BwdEpi {
         if (q == 0 && sl.sub == 0 && lane == 0) {
             __threadfence();  // (8 epilogue warps: (q, sub) = (0, 0) is warp 2)
             const unsigned mine_epoch = atomicAdd(p.sk_flags + slot, 1u) + 1u;
-            unsigned seen;
-            do {
-                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(p.sk_flags + peer_slot) : "memory");
-            } while (static_cast<int>(seen - mine_epoch) < 0);
+            ptx::spin_until_geq(p.sk_flags + peer_slot, mine_epoch);
             __threadfence();
         }
         ptx::named_sync(2, 32 * EPI_WARPS);
@@ -743,10 +740,7 @@ struct FwdPersistTraits : tc::TraitsBase {
         const U u = unit(p, cid, w.tile);
         const unsigned need = static_cast<unsigned>(u.s) * p.n_tiles;
         const unsigned* f = p.dep + (u.d * p.m_tiles + u.mt) * 2 + rank;
-        unsigned v;
-        do {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-        } while (v < need);
+        ptx::spin_until_geq(f, need);
         asm volatile("fence.proxy.async.global;" ::: "memory");
     }
     __device__ static void load2(const FwdPParams& p, int it, int kb, uint32_t rank, uint8_t* sA, uint8_t* sB,
@@ -868,10 +862,7 @@ struct BwdPersistTraits : tc::TraitsBase, BwdEpi {
         if (u.s == 0) return;  // dz of the first BPTT step comes from the previous kernel
         const unsigned need = static_cast<unsigned>(u.s) * p.n_tiles * 2;
         const unsigned* f = p.dep + (u.d * p.m_tiles + u.mt) * 2 + rank;
-        unsigned v;
-        do {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-        } while (v < need);
+        ptx::spin_until_geq(f, need);
         asm volatile("fence.proxy.async.global;" ::: "memory");  // generic acquire -> async-proxy (TMA) reads
     }
     __device__ static void load2(const BwdPParams& p, int it, int kb, uint32_t rank, uint8_t* sA, uint8_t* sB,
@@ -919,10 +910,7 @@ struct BwdPersistTraits : tc::TraitsBase, BwdEpi {
         if (leader) {
             __threadfence();
             const unsigned mine_epoch = atomicAdd(p.sk_flags + slot, 1u) + 1u;
-            unsigned seen;
-            do {
-                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(p.sk_flags + peer_slot) : "memory");
-            } while (static_cast<int>(seen - mine_epoch) < 0);
+            ptx::spin_until_geq(p.sk_flags + peer_slot, mine_epoch);
             __threadfence();
         }
         ptx::named_sync(2, 32 * EPI_WARPS);

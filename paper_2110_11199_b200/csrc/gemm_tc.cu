@@ -193,10 +193,7 @@ struct GenTraits : tc::TraitsBase {
             if (q == 0 && sl.sub == 0 && lane == 0) {
                 for (int j = cid + 1; j <= c_last; ++j) {
                     if (sk_start(p, j, ncl) == sk_start(p, j + 1, ncl)) continue;  // empty range: no partial
-                    unsigned v;
-                    do {
-                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.sk_flags + j * 2 + rank) : "memory");
-                    } while (v == 0);
+                    ptx::spin_until_geq(p.sk_flags + j * 2 + rank, 1u);
                 }
                 __threadfence();
             }

@@ -75,6 +75,22 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* m
 __device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// Cross-CTA flag spin with back-off (acquire at gpu scope): probes L2 at most every ~100 ns
+// once the first probe fails, instead of a tight loop that burns L2 bandwidth and power.
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* f) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+    return v;
+}
+__device__ __forceinline__ void spin_until_geq(const unsigned* f, unsigned need) {
+    if (static_cast<int>(ld_acquire_u32(f) - need) >= 0) return;
+    unsigned ns = 32;
+    while (static_cast<int>(ld_acquire_u32(f) - need) < 0) {
+        __nanosleep(ns);
+        if (ns < 128) ns <<= 1;
+    }
+}
+
 // CTA named barrier 1: producer warp arrives, epilogue warps sync (whole warps only).
 __device__ __forceinline__ void named_arrive(uint32_t id, uint32_t nthreads) {
     asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
