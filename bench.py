@@ -354,8 +354,9 @@ def run_ours(a):
         "e2e": {"value": e2e_val, "unit": "frames/s", "h2d_bytes_per_step": nf * 4 + a.batch * T_UNROLL * 4,
                 "d2h_bytes_per_step": 4, "steps": e2e_steps},
         "roofline": {"bound": "tensor",
-                     "kernel": "persistent_kernel_2cta<FwdT<128>>: fused recurrent GEMM [x_t|h_t-1][W_ih|W_hh]^T + LSTM "
-                               "cell, both directions, 256x512 tcgen05 cta_group::2 tiles (one wave)",
+                     "kernel": "persistent_kernel_2cta<FwdPersistTraits>: one launch per layer = 21 steps x 2 "
+                               "directions of the fused recurrent GEMM [x_t|h_t-1][W_ih|W_hh]^T + LSTM cell, "
+                               "tcgen05 cta_group::2 256x256 tiles",
                      "achieved": dom_tf, "peak": peak, "unit": "TFLOP/s", "frac": dom_tf / peak if peak else None,
                      "peak_kind": f"bf16_tflops_sustained ({pk_kind})", "traffic": traffic,
                      "algorithmic_flops_per_launch": dom_flops, "launches_per_step": dom_launches,

@@ -11,10 +11,10 @@ cap() {  # name regex skip count
   ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:$2" -s $3 -c ${4:-1} \
       -o gpurun_out/${tag}_$1 $B > gpurun_out/${tag}_$1.log 2>&1
 }
-cap fwd "FwdT<.int.128>" 30
-cap bwd "BwdSplitTraits" 30
+cap fwd "FwdPersistTraits" 2
+cap bwd "BwdPersistTraits" 2
 cap ce "CeTraits" 0 2
-cap wgrad "GenTraits<.int.256, .bool.1, .bool.1, .bool.0>" 2
+cap wgrad "GenTraits<.int.256, .bool.1, .bool.1, .bool.0, .bool.0, .bool.0>" 2
 cap dgrad "GenTraits<.int.512" 0
 python bench.py > gpurun_out/${tag}_bench.log 2>&1
 tail -1 gpurun_out/${tag}_bench.log > gpurun_out/${tag}_bench.json
