@@ -38,6 +38,7 @@ extern bool g_use_splitk_bwd;  // gemm_lstm.cu
 extern bool g_use_pdl;         // gemm_lstm.cu
 extern bool g_use_persist_bwd; // gemm_lstm.cu
 extern bool g_use_persist_fwd; // gemm_lstm.cu
+extern bool g_bwd_kq4;         // gemm_lstm.cu
 
 namespace {
 thread_local std::string g_last_error;
@@ -119,6 +120,7 @@ Ctx::Ctx(const adpsgd_config& c) : cfg(c) {
     if (const char* e = std::getenv("ADPSGD_NO_PDL")) g_use_pdl = e[0] == '0';
     if (const char* e = std::getenv("ADPSGD_NO_PERSIST")) g_use_persist_bwd = e[0] == '0';
     if (const char* e = std::getenv("ADPSGD_NO_PERSIST_FWD")) g_use_persist_fwd = e[0] == '0';
+    if (const char* e = std::getenv("ADPSGD_BWD_KQ4")) g_bwd_kq4 = e[0] == '1';
     if (const char* e = std::getenv("ADPSGD_NO_STREAMK")) g_use_streamk = e[0] == '0';
     if (const char* e = std::getenv("ADPSGD_NO_XTRA")) g_use_xtra = e[0] == '0';
     if (const char* e = std::getenv("ADPSGD_FORCE_EXT")) g_force_ext = e[0] == '1';
@@ -165,7 +167,8 @@ Ctx::Ctx(const adpsgd_config& c) : cfg(c) {
         }
         if (H % 128 == 0) {  // split-K (H % 256) and persistent (H % 128) BPTT exchange buffers
             const int64_t slots = lstm_bwd_splitk_slots(nd, B, H);
-            sk_scratch = static_cast<float*>(alloc(static_cast<size_t>(slots) * 128 * 128 * sizeof(float)));
+            // per CTA slot: 2 parities x up to 4 K-split blocks x 32 KB (persistent BPTT, KQ <= 4)
+            sk_scratch = static_cast<float*>(alloc(static_cast<size_t>(slots) * 4 * 128 * 128 * sizeof(float)));
             sk_flags = static_cast<unsigned int*>(alloc(static_cast<size_t>(slots) * sizeof(unsigned int)));
             AB_CUDA(cudaMemsetAsync(sk_flags, 0, static_cast<size_t>(slots) * sizeof(unsigned int), s_main));
             pb_sync = static_cast<unsigned int*>(alloc(520 * sizeof(unsigned int)));

@@ -410,7 +410,8 @@ struct BwdEpi {
     template <int SPAN, bool INPLACE, class Rel, int NBUF = 2>
     __device__ static void body_g(const BwdGroup& g, int H, int m0, int u0, uint32_t tbase, int q, int lane,
                                   Rel release, uint8_t* st, uint64_t* ebar, uint32_t& ephase, tc::EpiSlot sl,
-                                  const float* peer, bool preissued, const EpiRows& r) {
+                                  const float* peer, bool preissued, const EpiRows& r, const float* peer2 = nullptr,
+                                  const float* peer3 = nullptr) {
         static_assert(NBUF == 2 || INPLACE, "a single input buffer needs in-place outputs");
         const int rowbase = m0 + q * 32;
         uint8_t* bdz = st + 2 * IN_BYTES;         // 4 x 1 KB (INPLACE: in the chunk's input buffer)
@@ -430,15 +431,21 @@ struct BwdEpi {
             ptx::tmem_ld_32x32b_x16_(tbase + uc, acc);
             ptx::tmem_ld_wait();
             if (uc + step >= SPAN) release();
-            if (peer) {
-                const float4* pp = reinterpret_cast<const float4*>(peer + ((uc / 16) * 128 + q * 32 + lane) * 16);
+            // split-K partners' partials of these units, added in a fixed order (deterministic)
+            const float* peers[3] = {peer, peer2, peer3};
+#pragma unroll
+            for (int pi = 0; pi < 3; ++pi) {
+                if (!peers[pi]) continue;
+                const float4* pp = reinterpret_cast<const float4*>(peers[pi] + ((uc / 16) * 128 + q * 32 + lane) * 16);
+                float4 f[4];
+#pragma unroll
+                for (int v = 0; v < 4; ++v) f[v] = __ldcg(pp + v);
 #pragma unroll
                 for (int v = 0; v < 4; ++v) {
-                    const float4 f = __ldcg(pp + v);
-                    acc[4 * v] = __float_as_uint(__uint_as_float(acc[4 * v]) + f.x);
-                    acc[4 * v + 1] = __float_as_uint(__uint_as_float(acc[4 * v + 1]) + f.y);
-                    acc[4 * v + 2] = __float_as_uint(__uint_as_float(acc[4 * v + 2]) + f.z);
-                    acc[4 * v + 3] = __float_as_uint(__uint_as_float(acc[4 * v + 3]) + f.w);
+                    acc[4 * v] = __float_as_uint(__uint_as_float(acc[4 * v]) + f[v].x);
+                    acc[4 * v + 1] = __float_as_uint(__uint_as_float(acc[4 * v + 1]) + f[v].y);
+                    acc[4 * v + 2] = __float_as_uint(__uint_as_float(acc[4 * v + 2]) + f[v].z);
+                    acc[4 * v + 3] = __float_as_uint(__uint_as_float(acc[4 * v + 3]) + f[v].w);
                 }
             }
             ptx::mbar_wait(ebar + b, (ephase >> b) & 1u);
@@ -815,14 +822,18 @@ struct BwdPParams {
     unsigned long long* trace;
 };
 
+// KQ = K splits per tile: KQ = 2 -> 256 x 128 pair tiles (K halves); KQ = 4 -> 256 x 256 tiles
+// (K quarters: a third less operand ingress per FLOP, three partials per owned block).
+template <int KQ>
 struct BwdPersistTraits : tc::TraitsBase, BwdEpi {
-    static constexpr int BN = 128;  // 256-row x 128-unit pair tiles, K halved: units per CTA = 64
+    static constexpr int BN = 64 * KQ;  // pair tile width; each CTA finalises 64 units
     static constexpr int EPI_WARPS = 8;
     static constexpr int EPI_SMEM = EPI_WARPS * 12 * 1024;  // BwdEpi::body_g<64, INPLACE, .., NBUF = 1>
     static constexpr int ACC_STAGES = 2;
     static constexpr bool A_MN = false;
     static constexpr bool B_MN = true;
     static constexpr bool STREAMK = true;
+    static constexpr int kBlock = 4 * 128 * 16;  // floats of one exported 64-unit block: [4 chunks][128 rows][16]
     struct U {
         int mt, nt, kh, s, d;
     };
@@ -860,9 +871,8 @@ struct BwdPersistTraits : tc::TraitsBase, BwdEpi {
     __device__ static void item_ready(const BwdPParams& p, const tc::Item& w, int cid, uint32_t rank) {
         const U u = unit(p, cid, w.tile);
         if (u.s == 0) return;  // dz of the first BPTT step comes from the previous kernel
-        const unsigned need = static_cast<unsigned>(u.s) * p.n_tiles * 2;
-        const unsigned* f = p.dep + (u.d * p.m_tiles + u.mt) * 2 + rank;
-        ptx::spin_until_geq(f, need);
+        const unsigned need = static_cast<unsigned>(u.s) * p.n_tiles * KQ;
+        ptx::spin_until_geq(p.dep + (u.d * p.m_tiles + u.mt) * 2 + rank, need);
         asm volatile("fence.proxy.async.global;" ::: "memory");  // generic acquire -> async-proxy (TMA) reads
     }
     __device__ static void load2(const BwdPParams& p, int it, int kb, uint32_t rank, uint8_t* sA, uint8_t* sB,
@@ -872,7 +882,11 @@ struct BwdPersistTraits : tc::TraitsBase, BwdEpi {
         const int k0 = (u.kh * p.kbh + kb) * kBK;
         ptx::tma_load_2d_2sm_hint(sA, &g.ta, bar, k0, t_src(p, u) * p.B + u.mt * 2 * kBM + kBM * static_cast<int>(rank),
                                   ptx::policy_evict_first());
-        ptx::tma_load_2d_2sm_hint(sB, &g.tb, bar, u.nt * BN + static_cast<int>(rank) * (BN / 2), k0, ptx::policy_evict_last());
+        const uint64_t keep = ptx::policy_evict_last();
+#pragma unroll
+        for (int j = 0; j < BN / 128; ++j)
+            ptx::tma_load_2d_2sm_hint(sB + j * 64 * kBK * 2, &g.tb, bar, u.nt * BN + static_cast<int>(rank) * (BN / 2) + 64 * j,
+                                      k0, keep);
     }
     template <class S>
     __device__ static void epi_begin2(const BwdPParams& p, int it, uint32_t rank, int q, int lane, uint8_t* st,
@@ -886,19 +900,22 @@ struct BwdPersistTraits : tc::TraitsBase, BwdEpi {
                                        uint64_t* ebar, uint32_t& ephase) {
         const U u = unit(p, cid, w.tile);
         const int per = p.m_tiles * p.n_tiles;
-        const int partner = u.kh == 0 ? cid + per : cid - per;
-        const int slot = cid * 2 + static_cast<int>(rank), peer_slot = partner * 2 + static_cast<int>(rank);
-        constexpr int kHalf = 4 * 128 * 16;  // floats: 4 chunks x 128 rows x 16
+        const int base = cid % per;  // partners: base + j * per, j = K split
         const int par = w.tile & 1;
         const int row = q * 32 + lane;
-        // 1) export the 64 units the partner finalises (TMEM cols [(1-kh) 64, +64))
-        float* mine = p.sk_scratch + (static_cast<int64_t>(slot) * 2 + par) * kHalf;
+        // slot layout: [cta slot][parity][destination split j][kBlock]
+        auto block = [&](int c_id, int j) {
+            return p.sk_scratch + ((static_cast<int64_t>(c_id * 2 + static_cast<int>(rank)) * 2 + par) * KQ + j) * kBlock;
+        };
+        // 1) export the blocks the partners finalise (TMEM cols [64 j, +64) for j != kh)
 #pragma unroll 1
-        for (int c = sl.sub; c < 4; c += sl.n) {
+        for (int x = sl.sub; x < 4 * KQ; x += sl.n) {
+            const int j = x >> 2, c = x & 3;
+            if (j == u.kh) continue;
             uint32_t v[16];
-            ptx::tmem_ld_32x32b_x16_(tbase + (1 - u.kh) * 64 + 16 * c, v);
+            ptx::tmem_ld_32x32b_x16_(tbase + 64 * j + 16 * c, v);
             ptx::tmem_ld_wait();
-            float4* dst = reinterpret_cast<float4*>(mine + (c * 128 + row) * 16);
+            float4* dst = reinterpret_cast<float4*>(block(cid, j) + (c * 128 + row) * 16);
 #pragma unroll
             for (int k = 0; k < 4; ++k)
                 __stcg(dst + k, make_float4(__uint_as_float(v[4 * k]), __uint_as_float(v[4 * k + 1]),
@@ -909,17 +926,20 @@ struct BwdPersistTraits : tc::TraitsBase, BwdEpi {
         const bool leader = q == 0 && sl.sub == 0 && lane == 0;
         if (leader) {
             __threadfence();
-            const unsigned mine_epoch = atomicAdd(p.sk_flags + slot, 1u) + 1u;
-            ptx::spin_until_geq(p.sk_flags + peer_slot, mine_epoch);
+            const unsigned mine_epoch = atomicAdd(p.sk_flags + cid * 2 + rank, 1u) + 1u;
+            for (int j = 0; j < KQ; ++j)
+                if (j != u.kh) ptx::spin_until_geq(p.sk_flags + (base + j * per) * 2 + rank, mine_epoch);
             __threadfence();
         }
         ptx::named_sync(2, 32 * EPI_WARPS);
-        // 3) cell backward on the owned 64 units (inputs pre-issued by epi_begin2)
+        // 3) cell backward on the owned 64 units (inputs pre-issued by epi_begin2), partners' partials added
+        const float* pr[3] = {nullptr, nullptr, nullptr};
+        for (int j = 0, n = 0; j < KQ; ++j)
+            if (j != u.kh) pr[n++] = block(base + j * per, u.kh);
         auto rel = [&] { tc::release_acc_2sm(tempty_leader, lane); };
         body_g<64, true, decltype(rel), 1>(p.g[u.d], p.H, u.mt * 2 * kBM + kBM * static_cast<int>(rank),
                                           u.nt * BN + 64 * u.kh, tbase + 64 * u.kh, q, lane, rel, st, ebar, ephase, sl,
-                                          p.sk_scratch + (static_cast<int64_t>(peer_slot) * 2 + par) * kHalf, true,
-                                          rows(p, u));
+                                          pr[0], true, rows(p, u), pr[1], pr[2]);
         // 4) publish: this CTA's dz block of step tn is in memory (TMA stores complete)
         if (lane == 0) {
             ptx::bulk_wait0();
@@ -978,6 +998,7 @@ bool g_use_splitk_bwd = true;
 bool g_use_pdl = true;
 bool g_use_persist_bwd = true;
 bool g_use_persist_fwd = true;
+bool g_bwd_kq4 = false;  // KQ = 4 measured slower (3 pipeline stages, 4-way exchange); ADPSGD_BWD_KQ4=1
 
 void lstm_fwd_step(const LstmFwdDir* dirs, int ndirs, int B, int H, int ldg, int ldc, int ldh, cudaStream_t s) {
     AB_CHECK(H % 64 == 0 && ndirs >= 1 && ndirs <= 2, ADPSGD_E_DIMENSION, "fused LSTM step needs H % 64 == 0");
@@ -1123,8 +1144,10 @@ bool lstm_fwd_layer_persistent(const LstmFwdLayer& L, int ndirs, int B, int H, i
 
 bool lstm_bwd_layer_persistent(const LstmBwdLayer& L, int ndirs, int B, int H, int T, cudaStream_t s, float* sk_scratch,
                                unsigned int* sk_flags, unsigned int* dep, unsigned int* exit_ctr) {
-    const int m_tiles = B / (2 * kBM), n_tiles = H / 128;
-    const int units = m_tiles * n_tiles * 2;
+    // 256 x 256 tiles in K quarters when H allows and the units fit, else 256 x 128 in K halves
+    const int kq = (g_bwd_kq4 && H % 256 == 0 && (B / (2 * kBM)) * (H / 256) * 4 <= num_sms() / 2) ? 4 : 2;
+    const int m_tiles = B / (2 * kBM), n_tiles = H / (64 * kq);
+    const int units = m_tiles * n_tiles * kq;
     if (!(g_use_persist_bwd && g_use_pair_mma && ndirs == 2 && T >= 2 && B % (2 * kBM) == 0 && H % 128 == 0 &&
           units <= num_sms() / 2 && sk_scratch && sk_flags && dep && exit_ctr))
         return false;
@@ -1144,19 +1167,24 @@ bool lstm_bwd_layer_persistent(const LstmBwdLayer& L, int ndirs, int B, int H, i
         make_map_gen(&g.m_dz, L.dZ + d * G4, false, G4, TB, L.ld_dz, 16, 32, CU_TENSOR_MAP_SWIZZLE_32B);
         g.kb = G4 / kBK;
     }
-    p.B = B; p.H = H; p.T = T; p.m_tiles = m_tiles; p.n_tiles = n_tiles; p.units = units; p.kbh = G4 / kBK / 2;
+    p.B = B; p.H = H; p.T = T; p.m_tiles = m_tiles; p.n_tiles = n_tiles; p.units = units; p.kbh = G4 / kBK / kq;
     p.sk_scratch = sk_scratch; p.sk_flags = sk_flags; p.dep = dep; p.exit_ctr = exit_ctr;
     p.trace = trace_take();
     const double flops = 2.0 * 2 * (T - 1) * static_cast<double>(B) * H * G4;
     const double bytes = 2.0 * (T - 1) * (2.0 * (B + H) * G4 + static_cast<double>(B) * H * (4 + 8 + 8 + 4 + 4 + 8));
     ProfScope ps_(s, PROF_GEMM_REC_BWD, flops, bytes);
-    auto k = tc::persistent_kernel_2cta<BwdPersistTraits, BwdPParams>;
-    static bool attr = false;
-    if (!attr) {
-        AB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::ShapeOf2<BwdPersistTraits>::SMEM));
-        attr = true;
-    }
-    tc::launch_tc(k, p, 2 * units, tc::threads_of<BwdPersistTraits>(), tc::ShapeOf2<BwdPersistTraits>::SMEM, true, s);
+    auto launch = [&](auto tr) {
+        using Tr = decltype(tr);
+        auto k = tc::persistent_kernel_2cta<Tr, BwdPParams>;
+        static bool attr = false;
+        if (!attr) {
+            AB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::ShapeOf2<Tr>::SMEM));
+            attr = true;
+        }
+        tc::launch_tc(k, p, 2 * units, tc::threads_of<Tr>(), tc::ShapeOf2<Tr>::SMEM, true, s);
+    };
+    if (kq == 4) launch(BwdPersistTraits<4>{});
+    else launch(BwdPersistTraits<2>{});
     count_launch();
     return true;
 }

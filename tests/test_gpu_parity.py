@@ -136,6 +136,26 @@ def test_wide_streamk_dgrad_matches_default_kernels(monkeypatch):
     assert np.linalg.norm(g1 - g0) / np.linalg.norm(g0) <= 1e-2
 
 
+@pytest.mark.parametrize("kq4", ["0", "1"])
+def test_persistent_bptt_k_quarters(oracle_mod, monkeypatch, kq4):
+    """Persistent BPTT with the K dimension split in halves (256 x 128 tiles, default) or quarters
+    (256 x 256 tiles, ADPSGD_BWD_KQ4=1): same gradient as the oracle within bf16 tolerance."""
+    O = oracle_mod
+    monkeypatch.setenv("ADPSGD_BWD_KQ4", kq4)
+    m = ModelDesc(layers=2, hidden=256, bidirectional=True, input_dim=40, proj=16, classes=48, unroll=4)
+    feats, labels = _data(m)
+    M = 512
+    idx = np.random.default_rng(41).integers(0, 40, size=M).astype(np.int32)
+    g = LearnerGroup(m, StrategyConfig(learners=1, batch=M, seed=1), precision=Precision.BF16)
+    g.set_dataset(feats, labels, 40)
+    w = np.random.default_rng(42).normal(0, 0.2, g.D)
+    loss, grad = g.gradient(w, idx)
+    g.close()
+    oloss, ograd = O.lstm_loss_grad(_odesc(O, m), w, feats, labels, idx)
+    assert abs(loss - oloss) <= 1e-2 * oloss
+    assert np.linalg.norm(grad - ograd) / np.linalg.norm(ograd) <= 5e-2
+
+
 @pytest.mark.parametrize("bidir,hidden,M,T", [(True, 64, 136, 9), (False, 64, 136, 9), (True, 256, 300, 5),
                                                (False, 128, 260, 4), (True, 128, 256, 6), (True, 256, 512, 4)])
 def test_fused_lstm_kernels_match_oracle_and_unfused(oracle_mod, monkeypatch, bidir, hidden, M, T):
