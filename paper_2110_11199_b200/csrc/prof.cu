@@ -19,8 +19,8 @@ unsigned long long* trace_take() {
 void trace_enable(int on) {
     if (on) g_trace_skip = on - 1;
     if (on && !g_trace_buf) {
-        AB_CUDA(cudaMalloc(&g_trace_buf, sizeof(unsigned long long) * 160 * 32));
-        AB_CUDA(cudaMemset(g_trace_buf, 0, sizeof(unsigned long long) * 160 * 32));
+        AB_CUDA(cudaMalloc(&g_trace_buf, sizeof(unsigned long long) * 160 * 48));
+        AB_CUDA(cudaMemset(g_trace_buf, 0, sizeof(unsigned long long) * 160 * 48));
     }
     if (!on && g_trace_buf) {
         AB_CUDA(cudaDeviceSynchronize());
@@ -32,7 +32,7 @@ void trace_read(unsigned long long* out, int n) {
     AB_CUDA(cudaDeviceSynchronize());
     if (!g_trace_buf) return;
     AB_CUDA(cudaMemcpy(out, g_trace_buf, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost));
-    AB_CUDA(cudaMemset(g_trace_buf, 0, sizeof(unsigned long long) * 160 * 32));
+    AB_CUDA(cudaMemset(g_trace_buf, 0, sizeof(unsigned long long) * 160 * 48));
 }
 
 bool g_prof_enabled = false;

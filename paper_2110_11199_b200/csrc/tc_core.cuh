@@ -19,9 +19,9 @@ namespace ab::tc {
 // Debug timeline (adpsgd_debug_trace): per-CTA globaltimer stamps written by the MMA and
 // epilogue warps of persistent_kernel_2cta into p.trace (nullptr = off).
 // Slot layout: [cta][event] u64, event = 4 * tile_iter + kind.
-constexpr int kTraceCtas = 160, kTraceEv = 32;
+constexpr int kTraceCtas = 160, kTraceEv = 48;  // events: 4 per item (items 0..9), 40..45 free, 46 start, 47 end
 __device__ __forceinline__ void trace(unsigned long long* buf, int ev) {
-    if (buf && blockIdx.x < kTraceCtas && ev < kTraceEv) {
+    if (buf && blockIdx.x < kTraceCtas && ev < 40 || (buf && blockIdx.x < kTraceCtas && ev >= kTraceEv - 2 && ev < kTraceEv)) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         buf[blockIdx.x * kTraceEv + ev] = t;

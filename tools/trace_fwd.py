@@ -15,24 +15,24 @@ g.step(0.1)
 L = _lib.lib()
 names = {0: "mma_start", 1: "first_stage", 2: "last_mma", 3: "epi_done"}
 for n in ns:
-    buf = (C.c_uint64 * (160 * 32))()
+    buf = (C.c_uint64 * (160 * 48))()
     L.adpsgd_debug_trace(n, None, 0)
     g.step(0.1)
-    L.adpsgd_debug_trace(0, buf, 160 * 32)
-    a = np.array(buf, dtype=np.uint64).reshape(160, 32).astype(np.int64)
-    ctas = int((a[:, 30] > 0).sum())
+    L.adpsgd_debug_trace(0, buf, 160 * 48)
+    a = np.array(buf, dtype=np.uint64).reshape(160, 48).astype(np.int64)
+    ctas = int((a[:, 46] > 0).sum())
     t0 = a[a > 0].min()
     rel = np.where(a > 0, (a - t0) / 1000.0, np.nan)
     print(f"launch {n}: ctas {ctas} span {(a.max() - t0) / 1000.0:.1f} us")
-    parts = [f"start {np.nanmedian(rel[:, 30]):.1f}", f"end {np.nanmedian(rel[:, 31]):.1f} (max {np.nanmax(rel[:, 31]):.1f})"]
-    for i in range(7):
+    parts = [f"start {np.nanmedian(rel[:, 46]):.1f}", f"end {np.nanmedian(rel[:, 47]):.1f} (max {np.nanmax(rel[:, 47]):.1f})"]
+    for i in range(10):
         for k in range(4):
             col = rel[:, 4 * i + k]
             if np.isfinite(col).any():
                 parts.append(f"t{i}.{names[k]} {np.nanmedian(col):.1f}")
-    for i in range(12, 28):
+    for i in list(range(12, 40)) + [40, 41, 42, 43]:
         col = rel[:, i]
-        if np.isfinite(col).any() and i >= 12 and not np.isfinite(rel[:, 4 * (i // 4)]).any():
+        if np.isfinite(col).any() and (i >= 40 or not np.isfinite(rel[:, 4 * (i // 4)]).any()):
             parts.append(f"ev{i} {np.nanmedian(col):.1f}")
     print("   ", " | ".join(parts))
 L.adpsgd_debug_trace(0, None, 0)
