@@ -410,6 +410,12 @@ bool dispatch_ext(const TcParams& p, bool amn, bool bmn, bool cbf16, bool xtra, 
     if (!sk) return false;
     const int key = (amn ? 4 : 0) | (bmn ? 2 : 0) | (cbf16 ? 1 : 0);
     switch (key) {
+        case 6:
+            if constexpr (BN == 256) {  // small weight gradients (dW_proj)
+                launch_pair<GenTraits<256, true, true, false, false, true>>(p, s);
+                return true;
+            }
+            return false;
         case 2: launch_pair<GenTraits<BN, false, true, false, false, true>>(p, s); return true;  // dgrad, fp32 out
         case 3: launch_pair<GenTraits<BN, false, true, true, false, true>>(p, s); return true;   // dgrad, bf16 out
         default: return false;
@@ -482,7 +488,13 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
     const bool pair = g_use_pair_mma && g.M > BM;
     const int rows = pair ? 2 * BM : BM;
     const int m_tiles = (g.M + rows - 1) / rows;
-    const int bn0 = (g.N > 128 && (g_force_ext || m_tiles * ((g.N + 255) / 256) >= (pair ? num_sms() / 4 : num_sms() / 2)))
+    int kbt_all = 0;
+    for (int i = 0; i < g.nseg; ++i) kbt_all += (g.seg[i].K + BK - 1) / BK;
+    // few-tile, long-K weight gradients (dW_proj) go 256-wide and stream-K over every pair
+    const bool tiny_wgrad = g_use_streamk && pair && amn && bmn && !g.c_bf16 && g.N > 128 && kbt_all >= 64 &&
+                            m_tiles * ((g.N + 255) / 256) * 4 <= num_sms() / 2 && gemm_workspace().ws;
+    const int bn0 = (g.N > 128 && (g_force_ext || tiny_wgrad ||
+                                   m_tiles * ((g.N + 255) / 256) >= (pair ? num_sms() / 4 : num_sms() / 2)))
                         ? 256 : 128;
     // bias column (g.extra, one column past n_main) by the extra row-sum MMA instead of a ragged n-tile
     // (only when it saves a round of CTA-pair waves: the extra MMA costs a single accumulator stage)
@@ -502,7 +514,10 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
     // (two N = 256 MMAs per k-step: a quarter less L2->SM operand traffic per FLOP).
     auto sk_ok = [&](int bnx) {
         const int t = m_tiles * ((n_eff + bnx - 1) / bnx);
-        return g_use_streamk && pair && bnx >= 256 && wsp.ws && !xtra && !amn && bmn && (t % npairs != 0 || g_force_ext) &&
+        // weight-gradient layout only for tiny tile counts (e.g. dW_proj: 9 tiles), where the L2
+        // reuse of the lockstep wave order does not matter
+        const bool layout_ok = (!amn && bmn) || (amn && bmn && !g.c_bf16 && bnx == 256 && t * 4 <= npairs);
+        return g_use_streamk && pair && bnx >= 256 && wsp.ws && !xtra && layout_ok && (t % npairs != 0 || g_force_ext) &&
                kbt >= 8 && wsp.floats >= static_cast<size_t>(npairs) * 2 * (bnx / 32 + 1) * 128 * 32 &&
                wsp.flag_count >= static_cast<size_t>(npairs) * 2;
     };
