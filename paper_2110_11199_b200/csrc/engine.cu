@@ -104,6 +104,7 @@ Ctx::Ctx(const adpsgd_config& c) : cfg(c) {
     T = lay.T; B = c.batch; H = lay.H; nd = lay.nd; I = lay.I;
     fold_bias = bf16_mode;  // bias grads from a ones column of the wgrad B operands (no colsum passes)
     if (const char* e = std::getenv("ADPSGD_NO_FOLD_BIAS")) fold_bias = fold_bias && e[0] == '0';
+    if (const char* e = std::getenv("ADPSGD_NO_FOLD_IH")) fold_ih_ok = e[0] == '0';
     Ipad = bf16_mode ? static_cast<int>(round_up(I + (fold_bias ? 1 : 0), 8)) : I;
     ldH = nd * H + (fold_bias ? 8 : 0);
     ldY = lay.P > 0 ? (fold_bias ? lay.P + 8 : lay.P) : 0;
@@ -547,7 +548,7 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
             const DirOff& o = lay.dir[l][d];
             // one-wave 256 x 512 tiles for dW_ih (the bias then by a column sum of dZ) when the
             // 256-wide tiles plus the ones column would need a second wave (gemm_wgrad_wide)
-            const bool fold_ih = fold_bias && !gemm_wgrad_wide(G4, lay.in_dim[l]);
+            const bool fold_ih = fold_bias && fold_ih_ok && !gemm_wgrad_wide(G4, lay.in_dim[l]);
             {   // dW_ih = dZ_d^T Xin
                 GemmArgs g;
                 g.M = G4; g.N = lay.in_dim[l] + (fold_ih ? 1 : 0);

@@ -45,6 +45,7 @@ struct Ctx {
     int T = 0, B = 0, H = 0, nd = 1, I = 0, Ipad = 0, ndH = 0, nd4H = 0;
     int64_t TB = 0;
     bool fold_bias = false;  // bf16 mode: bias grads via a ones column (no colsum passes)
+    bool fold_ih_ok = true;  // ... also for the input-weight GEMMs (else a vectorised column sum of dZ)
     int ldH = 0, ldY = 0;     // row pitch of the layer outputs / projection output
     int64_t k = 0;
     int history_depth = 1;

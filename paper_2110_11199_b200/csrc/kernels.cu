@@ -147,6 +147,30 @@ __global__ void colsum_partial_kernel(const AT* __restrict__ X, int64_t ld, int 
     for (int r = r0; r < r1; ++r) s += to_f<AT>(X[static_cast<int64_t>(r) * ld + n]);
     part[static_cast<int64_t>(chunk) * N + n] = s;
 }
+// bf16 rows, 8 columns per thread (16-byte loads): the bias-gradient column sums of dZ / dY
+__global__ void colsum_partial_bf16x8_kernel(const bf16* __restrict__ X, int64_t ld, int R, int N, int rows_per_chunk,
+                                             float* __restrict__ part) {
+    const int n0 = 8 * (blockIdx.x * blockDim.x + threadIdx.x);
+    const int chunk = blockIdx.y;
+    if (n0 >= N) return;
+    const int r0 = chunk * rows_per_chunk;
+    const int r1 = min(R, r0 + rows_per_chunk);
+    float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+    for (int r = r0; r < r1; ++r) {
+        const uint4 v = __ldcs(reinterpret_cast<const uint4*>(X + static_cast<int64_t>(r) * ld + n0));
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float2 f = __bfloat1622float2(h[i]);
+            s[2 * i] += f.x;
+            s[2 * i + 1] += f.y;
+        }
+    }
+    float4* o = reinterpret_cast<float4*>(part + static_cast<int64_t>(chunk) * N + n0);
+    o[0] = make_float4(s[0], s[1], s[2], s[3]);
+    o[1] = make_float4(s[4], s[5], s[6], s[7]);
+}
 __global__ void colsum_final_kernel(const float* __restrict__ part, int chunks, int N, float* __restrict__ out) {
     const int n = blockIdx.x * blockDim.x + threadIdx.x;
     if (n >= N) return;
@@ -457,8 +481,14 @@ void launch_colsum(const AT* X, int64_t ld, int R, int N, float* out, float* ws,
     if (chunks > 128) chunks = 128;
     while (chunks > 1 && static_cast<int64_t>(chunks) * N > ws_elems) chunks /= 2;
     const int rpc = (R + chunks - 1) / chunks;
-    dim3 grid((N + 255) / 256, chunks);
-    colsum_partial_kernel<AT><<<grid, 256, 0, s>>>(X, ld, R, N, rpc, ws);
+    const bool vec8 = sizeof(AT) == 2 && N % 8 == 0 && ld % 8 == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0;
+    if (vec8) {
+        dim3 grid((N / 8 + 127) / 128, chunks);
+        colsum_partial_bf16x8_kernel<<<grid, 128, 0, s>>>(reinterpret_cast<const bf16*>(X), ld, R, N, rpc, ws);
+    } else {
+        dim3 grid((N + 255) / 256, chunks);
+        colsum_partial_kernel<AT><<<grid, 256, 0, s>>>(X, ld, R, N, rpc, ws);
+    }
     colsum_final_kernel<<<(N + 255) / 256, 256, 0, s>>>(ws, chunks, N, out);
     count_launch(2);
 }
