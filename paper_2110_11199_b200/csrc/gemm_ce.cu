@@ -48,7 +48,7 @@ struct CeTraits : tc::TraitsBase {
     static constexpr bool A_MN = false;
     static constexpr bool B_MN = false;
     static constexpr int EPI_WARPS = 8;
-    static constexpr int EPI_SMEM = EPI_WARPS * 2 * 2048;  // per warp: 2 x (bf16 32 cols x 32 rows, SW64)
+    static constexpr int EPI_SMEM = EPI_WARPS * 2 * 4096;  // per warp: 2 x (bf16 64 cols x 32 rows, SW128)
     __device__ static int num_tiles(const CeParams& p) { return p.m_tiles * p.n_tiles; }
     __device__ static void prefetch(const CeParams& p) {
         ptx::tma_prefetch(&p.ta);
@@ -163,13 +163,13 @@ struct CeTraits : tc::TraitsBase {
         if (p.mode == 0) {
             float m = -INFINITY, s = 0.f;
 #pragma unroll 1
-            for (int j = sl.sub; j < PER; j += 2 * sl.n) {
-                const int ca = 32 * j, cb = 32 * (j + sl.n);
+            for (int jp = sl.sub; jp < PER / 2; jp += sl.n) {  // adjacent chunk pairs: 64 columns
+                const int ca = 64 * jp, cb = ca + 32;
                 uint32_t va[32], vb[32];
                 ptx::tmem_ld_32x32b_x32(tbase + ca, va);
                 ptx::tmem_ld_32x32b_x32(tbase + cb, vb);
                 ptx::tmem_ld_wait();
-                if (j + 2 * sl.n >= PER) release();
+                if (jp + sl.n >= PER / 2) release();
                 float za[32], zb[32];
                 logits32<FULL>(p, n0 + ca, va, za);
                 logits32<FULL>(p, n0 + cb, vb, zb);
@@ -186,39 +186,40 @@ struct CeTraits : tc::TraitsBase {
             const float dlab = ok ? ex2(fmaf(p.zlab[r], kLog2e, q)) - sc : 0.f;
             int buf = 0;
 #pragma unroll 1
-            for (int j = sl.sub; j < PER; j += 2 * sl.n) {
+            for (int jp = sl.sub; jp < PER / 2; jp += sl.n, buf ^= 1) {  // 64 adjacent columns per iteration
+                const int col = n0 + 64 * jp;
                 uint32_t v[2][32];
-                ptx::tmem_ld_32x32b_x32(tbase + 32 * j, v[0]);
-                ptx::tmem_ld_32x32b_x32(tbase + 32 * (j + sl.n), v[1]);
+                ptx::tmem_ld_32x32b_x32(tbase + 64 * jp, v[0]);
+                ptx::tmem_ld_32x32b_x32(tbase + 64 * jp + 32, v[1]);
                 ptx::tmem_ld_wait();
-                if (j + 2 * sl.n >= PER) release();
+                if (jp + sl.n >= PER / 2) release();
+                uint32_t w[32];
 #pragma unroll
-                for (int h = 0; h < 2; ++h, buf ^= 1) {
-                    const int col = n0 + 32 * (j + h * sl.n);
+                for (int h = 0; h < 2; ++h) {
                     float z[32];
-                    logits32<FULL>(p, col, v[h], z);
-                    uint32_t w[16];
+                    logits32<FULL>(p, col + 32 * h, v[h], z);
 #pragma unroll
                     for (int i = 0; i < 32; i += 2) {
                         fma2(z[i], z[i + 1], kLog2e, q);
-                        w[i / 2] = tc::pack_bf16x2(ex2(z[i]), ex2(z[i + 1]));
+                        w[16 * h + i / 2] = tc::pack_bf16x2(ex2(z[i]), ex2(z[i + 1]));
                     }
-                    uint8_t* box = st + buf * 2048;
-                    if (lane == 0) ptx::bulk_wait_read1();  // the store that last used this buffer has read it
-                    __syncwarp();
-                    tc::st_row_words<64>(box, lane, w);
-                    const int ll = lab - col;
-                    if (ll >= 0 && ll < 32) {  // softmax - onehot at the label column
-                        const uint32_t a = ptx::smem_u32(box) + lane * 64 + ((((ll >> 3) ^ ((lane >> 1) & 3))) << 4) + (ll & 7) * 2;
-                        const __nv_bfloat16 hv = __float2bfloat16_rn(dlab);
-                        asm volatile("st.shared.b16 [%0], %1;" ::"r"(a), "h"(*reinterpret_cast<const unsigned short*>(&hv)) : "memory");
-                    }
-                    ptx::fence_proxy_async_smem();
-                    __syncwarp();
-                    if (lane == 0) {
-                        ptx::tma_store_2d_hint(&p.m_dl, box, col, rowbase, ptx::policy_evict_first());
-                        ptx::bulk_commit();
-                    }
+                }
+                // one 32-row x 64-column bf16 box (SW128) per iteration: one fence and one TMA store
+                uint8_t* box = st + buf * 4096;
+                if (lane == 0) ptx::bulk_wait_read1();  // the store that last used this buffer has read it
+                __syncwarp();
+                tc::st_row_words<128>(box, lane, w);
+                const int ll = lab - col;
+                if (ll >= 0 && ll < 64) {  // softmax - onehot at the label column
+                    const uint32_t a = ptx::smem_u32(box) + lane * 128 + (((ll >> 3) ^ (lane & 7)) << 4) + (ll & 7) * 2;
+                    const __nv_bfloat16 hv = __float2bfloat16_rn(dlab);
+                    asm volatile("st.shared.b16 [%0], %1;" ::"r"(a), "h"(*reinterpret_cast<const unsigned short*>(&hv)) : "memory");
+                }
+                ptx::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    ptx::tma_store_2d_hint(&p.m_dl, box, col, rowbase, ptx::policy_evict_first());
+                    ptx::bulk_commit();
                 }
             }
         }
@@ -312,7 +313,7 @@ void ce_forward_backward(const CeArgs& a, cudaStream_t s) {
     const bool pair = g_use_pair_mma && a.M > kBM;
     make_map_gen(&p.ta, a.Y, false, a.K, a.M, a.ldY, 64, kBM, CU_TENSOR_MAP_SWIZZLE_128B);
     make_map_gen(&p.tb, a.W, false, a.K, a.N, a.K, 64, pair ? 128 : 256, CU_TENSOR_MAP_SWIZZLE_128B);
-    make_map_gen(&p.m_dl, a.dlogits, false, a.N, a.M, a.N, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+    make_map_gen(&p.m_dl, a.dlogits, false, a.N, a.M, a.N, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B);
     p.kb = (a.K + kBK - 1) / kBK;
     p.M = a.M; p.N = a.N;
     p.m_tiles = pair ? (a.M + 2 * kBM - 1) / (2 * kBM) : (a.M + kBM - 1) / kBM;
