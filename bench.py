@@ -196,7 +196,14 @@ def run_reference(a):
     if rank != 0:
         return
     ncpu = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
-    threads = max(1, min(ncpu, 8))  # per-thread fp64 gradient partials are 1.16 GB each
+    # every usable host thread, as long as the per-thread fp64 gradient partials (1.16 GB each at
+    # H = 1024) fit in the available memory
+    try:
+        avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
+        by_mem = max(1, int(0.6 * avail / 1.3e9))
+    except (ValueError, OSError, AttributeError):
+        by_mem = 8
+    threads = max(1, min(ncpu, by_mem))
     segs = threads
     times = []
     budget = 150.0
