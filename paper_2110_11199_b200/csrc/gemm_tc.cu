@@ -9,6 +9,7 @@
 // LSTM's dgrad / wgrad contractions run without explicit transposes.
 #include <cuda.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <unordered_map>
@@ -56,9 +57,10 @@ struct TcParams {
 // SK:   stream-K work split (tc::Item): every CTA pair gets the same number of k-block iterations;
 //       a tile split between pairs is finished by the pair holding its k-block 0, which adds the
 //       other segments' partials in pair order (deterministic).
-template <int BN_, bool AMN, bool BMN, bool CBF16, bool XTRA = false, bool SK = false>
+template <int BN_, bool AMN, bool BMN, bool CBF16, bool XTRA = false, bool SK = false, bool MCB = false>
 struct GenTraits : tc::TraitsBase {
     static constexpr int BN = BN_;
+    static constexpr int CLUSTER = MCB ? 4 : 2;  // MCB: two pairs (same n-tile) share B by TMA multicast
     static constexpr int EPI_SMEM = 0;
     static constexpr int EPI_WARPS = 8;
     static constexpr bool A_MN = AMN;
@@ -145,6 +147,26 @@ struct GenTraits : tc::TraitsBase {
                 ptx::tma_load_2d_2sm(dst, &p.tb[s], bar, k0, n0);
             }
         }
+    }
+    // MCB (MN-major B, BN = 256): cluster CTA c = 2 pc + r loads A rows as usual and B chunk pc of
+    // its pair-rank half, multicast to CTA c and CTA c ^ 2 (the other pair's same-rank CTA).
+    __device__ static void load2_mc(const TcParams& p, int tile, int kb, uint32_t crank, uint8_t* sA, uint8_t* sB,
+                                    uint32_t bar) {
+        const uint32_t rank = crank & 1, pc = crank >> 1;
+        const int m0 = (tile % p.m_tiles) * 2 * BM + BM * rank;
+        const int nb = (tile / p.m_tiles) * BN;
+        int s, k0;
+        seg_of(p, kb, s, k0);
+        if (AMN) {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j) ptx::tma_load_2d_2sm(sA + j * 64 * BK * 2, &p.ta[s], bar, m0 + 64 * j, k0);
+        } else {
+            ptx::tma_load_2d_2sm(sA, &p.ta[s], bar, k0, m0);
+        }
+        static_assert(!MCB || (BMN && BN == 256), "B multicast: MN-major B, 256-wide tiles");
+        const int n0 = nb + (BN / 2) * static_cast<int>(rank);
+        const uint16_t mask = static_cast<uint16_t>((1u << crank) | (1u << (crank ^ 2)));
+        ptx::tma_load_2d_2sm_mc(sB + pc * 64 * BK * 2, &p.tb[s], bar, n0 + 64 * static_cast<int>(pc), k0, mask);
     }
     __device__ static void epilogue2(const TcParams& p, int tile, uint32_t rank, uint32_t tbase, int q, int lane,
                                      uint32_t tempty_leader, uint8_t*, uint64_t*, uint32_t&, tc::EpiSlot sl) {
@@ -380,7 +402,7 @@ void launch_pair(const TcParams& p, cudaStream_t s) {
     const int tiles = p.m_tiles * p.n_tiles;
     // stream-K spreads the k-block iterations over every pair; plain tiles use at most one pair per tile
     const int pairs = Traits::STREAMK ? num_sms() / 2 : (tiles < num_sms() / 2 ? tiles : num_sms() / 2);
-    tc::launch_tc(k, p, 2 * pairs, tc::threads_of<Traits>(), tc::ShapeOf2<Traits>::SMEM, true, s);
+    tc::launch_tc(k, p, 2 * pairs, tc::threads_of<Traits>(), tc::ShapeOf2<Traits>::SMEM, true, s, Traits::CLUSTER);
     count_launch();
 }
 
@@ -425,6 +447,15 @@ bool dispatch_ext(const TcParams& p, bool amn, bool bmn, bool cbf16, bool xtra, 
 template <int BN>
 void dispatch(const TcParams& p, bool amn, bool bmn, bool cbf16, bool pair, cudaStream_t s) {
     const int key = (amn ? 4 : 0) | (bmn ? 2 : 0) | (cbf16 ? 1 : 0);
+    if constexpr (BN == 256) {
+        // B multicast across two CTA pairs (experiment / where tiles pair up along M)
+        const int tiles = p.m_tiles * p.n_tiles;
+        const int pairs = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
+        if (g_use_mcb && pair && bmn && p.m_tiles % 2 == 0 && tiles % 2 == 0 && pairs % 2 == 0) {
+            if (key == 6) { launch_pair<GenTraits<256, true, true, false, false, false, true>>(p, s); return; }
+            if (key == 2) { launch_pair<GenTraits<256, false, true, false, false, false, true>>(p, s); return; }
+        }
+    }
     switch (key) {
         case 0: launch_cfg<BN, false, false, false>(p, pair, s); break;
         case 1: launch_cfg<BN, false, false, true>(p, pair, s); break;
@@ -470,6 +501,7 @@ bool g_use_xtra = true;
 bool g_use_streamk = true;
 bool g_force_ext = false;
 bool g_use_wide_gemm = true;
+bool g_use_mcb = false;
 namespace {
 thread_local GemmWorkspace t_ws;
 }
@@ -477,6 +509,11 @@ void set_gemm_workspace(const GemmWorkspace& w) { t_ws = w; }
 const GemmWorkspace& gemm_workspace() { return t_ws; }
 
 void gemm_tc(const GemmArgs& g, cudaStream_t s) {
+    static const bool mcb_env = [] {
+        if (const char* e = std::getenv("ADPSGD_MCB")) g_use_mcb = e[0] == '1';
+        return true;
+    }();
+    (void)mcb_env;
     if (g.M <= 0 || g.N <= 0) return;
     AB_CHECK(g.nseg >= 1 && g.nseg <= 2, ADPSGD_E_DIMENSION, "gemm_tc: 1 or 2 K segments");
     const bool amn = g.seg[0].a.mn, bmn = g.seg[0].b.mn;
@@ -493,9 +530,12 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
     // few-tile, long-K weight gradients (dW_proj) go 256-wide and stream-K over every pair
     const bool tiny_wgrad = g_use_streamk && pair && amn && bmn && !g.c_bf16 && g.N > 128 && kbt_all >= 64 &&
                             m_tiles * ((g.N + 255) / 256) * 4 <= num_sms() / 2 && gemm_workspace().ws;
-    const int bn0 = (g.N > 128 && (g_force_ext || tiny_wgrad ||
-                                   m_tiles * ((g.N + 255) / 256) >= (pair ? num_sms() / 4 : num_sms() / 2)))
-                        ? 256 : 128;
+    static const int force_bn = std::getenv("ADPSGD_FORCE_BN") ? std::atoi(std::getenv("ADPSGD_FORCE_BN")) : 0;  // experiments
+    const int bn0 = force_bn == 128 || force_bn == 256
+                        ? force_bn
+                        : (g.N > 128 && (g_force_ext || tiny_wgrad ||
+                                         m_tiles * ((g.N + 255) / 256) >= (pair ? num_sms() / 4 : num_sms() / 2)))
+                              ? 256 : 128;
     // bias column (g.extra, one column past n_main) by the extra row-sum MMA instead of a ragged n-tile
     // (only when it saves a round of CTA-pair waves: the extra MMA costs a single accumulator stage)
     const int npairs = num_sms() / 2;

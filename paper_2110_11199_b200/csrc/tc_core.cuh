@@ -49,6 +49,7 @@ struct TraitsBase {
     static constexpr bool EPI_OVERLAY = false; // epilogue smem overlays the pipeline stages (one tile per CTA only)
     static constexpr bool STREAMK = false;     // work items from Traits::sk_item / epilogue via Traits::epilogue_sk
     static constexpr int EXTRA_COLS = 0;       // extra TMEM columns: row sums of A (all-ones N = 16 MMA) on extra_tile()s
+    static constexpr int CLUSTER = 2;          // 4: two CTA pairs per cluster sharing B by TMA multicast (load2_mc)
     // STREAMK-style item kernels: the producer lane calls item_ready(p, w, cid, rank) before the
     // first TMA load of every item (cross-CTA dependencies of the A operand).
     template <class P, class W>
@@ -269,12 +270,17 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
     static_assert(STAGES <= 8 && Traits::EPI_WARPS <= 8, "barrier block layout");
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const uint32_t rank = ptx::cluster_ctarank();
+    constexpr bool MC = Traits::CLUSTER == 4;
+    const uint32_t crank = ptx::cluster_ctarank();  // rank in the cluster (2 or 4 CTAs)
+    const uint32_t rank = crank & 1;                // rank in the CTA pair
+    const uint32_t leader = crank & ~1u;            // the pair's MMA-issuing CTA
+    const uint16_t pair_mask = static_cast<uint16_t>(3u << leader);
     const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
     if (threadIdx.x == 0) trace(p.trace, kTraceEv - 2);
 
     if (warp == 0 && lane == 0) {
-        for (int i = 0; i < STAGES; ++i) { ptx::mbar_init(&full[i], 1); ptx::mbar_init(&empty[i], 1); }
+        // MC: a stage is written by both pairs' TMA multicasts, so both pairs' MMAs must free it
+        for (int i = 0; i < STAGES; ++i) { ptx::mbar_init(&full[i], 1); ptx::mbar_init(&empty[i], MC ? 2 : 1); }
         for (int i = 0; i < 2; ++i) { ptx::mbar_init(&tfull[i], 1); ptx::mbar_init(&tempty[i], 2 * Traits::EPI_WARPS); }
         for (int i = 0; i < 2 * Traits::EPI_WARPS; ++i) ptx::mbar_init(&epi_bar[i], 1);
         ptx::fence_barrier_init();
@@ -306,9 +312,12 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
                 if (lane == 0) {
                     if constexpr (Traits::STREAMK) Traits::kb_ready(p, w, kb, cid, rank);
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
-                    const uint32_t bar0 = ptx::mapa(ptx::smem_u32(&full[stage]), 0);
+                    const uint32_t bar0 = ptx::mapa(ptx::smem_u32(&full[stage]), leader);
                     if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * S::STAGE_BYTES);
-                    Traits::load2(p, w.tile, kb, rank, sA + stage * S::A_BYTES, sB + stage * S::B_BYTES, bar0);
+                    if constexpr (MC)
+                        Traits::load2_mc(p, w.tile, kb, crank, sA + stage * S::A_BYTES, sB + stage * S::B_BYTES, bar0);
+                    else
+                        Traits::load2(p, w.tile, kb, rank, sA + stage * S::A_BYTES, sB + stage * S::B_BYTES, bar0);
                 }
                 if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 if (!released && (kb + 1 - w.kb0 == STAGES || kb + 1 == w.kb1)) {
@@ -361,10 +370,10 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
                                                   idesc_x, accum);
                         }
                     }
-                    ptx::mma_commit_2sm(&empty[stage]);
+                    ptx::mma_commit_2sm(&empty[stage], MC ? static_cast<uint16_t>(0xF) : pair_mask);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
-                ptx::mma_commit_2sm(&tfull[acc]);
+                ptx::mma_commit_2sm(&tfull[acc], pair_mask);
                 trace(p.trace, 4 * it + 2);
                 if (++acc == ACC) { acc = 0; aphase ^= 1; }
             }
@@ -373,7 +382,7 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
         const int q = warp % 4;
         const int e = warp - 2;
         const EpiSlot slot{(e / 4), Traits::EPI_WARPS / 4};
-        const uint32_t tempty0 = ptx::mapa(ptx::smem_u32(&tempty[0]), 0);
+        const uint32_t tempty0 = ptx::mapa(ptx::smem_u32(&tempty[0]), leader);
         int acc = 0;
         uint32_t aphase = 0, ephase = 0;
         uint8_t* est = epi_smem + e * (Traits::EPI_WARPS ? Traits::EPI_SMEM / Traits::EPI_WARPS : 0);
@@ -530,7 +539,8 @@ __device__ __forceinline__ void release_acc(uint64_t* tempty, int lane) {
 // dependent launch, so its prologue (barrier init, TMEM alloc, tensor-map prefetch) overlaps
 // the previous kernel's tail; the kernel griddep_wait()s before touching dependent data.
 template <class P>
-inline void launch_tc(void (*kern)(P), const P& p, int grid, int threads, int smem, bool pair, cudaStream_t s) {
+inline void launch_tc(void (*kern)(P), const P& p, int grid, int threads, int smem, bool pair, cudaStream_t s,
+                      int cluster = 2) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(threads);
@@ -540,7 +550,7 @@ inline void launch_tc(void (*kern)(P), const P& p, int grid, int threads, int sm
     int n = 0;
     if (pair) {
         attrs[n].id = cudaLaunchAttributeClusterDimension;
-        attrs[n].val.clusterDim.x = 2;
+        attrs[n].val.clusterDim.x = cluster;
         attrs[n].val.clusterDim.y = 1;
         attrs[n].val.clusterDim.z = 1;
         ++n;

@@ -213,12 +213,23 @@ __device__ __forceinline__ void mma_bf16_2sm(uint32_t tmem_d, uint64_t adesc, ui
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
-// commit of the pair's MMAs, arriving on the barrier at the same offset in both CTAs
-__device__ __forceinline__ void mma_commit_2sm(uint64_t* bar) {
+// commit of the pair's MMAs, arriving on the barrier at the same offset in the CTAs of `mask`
+// (default: both CTAs of a 2-CTA cluster)
+__device__ __forceinline__ void mma_commit_2sm(uint64_t* bar, uint16_t mask = 3) {
     asm volatile(
         "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
             smem_u32(bar)),
-        "h"(static_cast<uint16_t>(3))
+        "h"(mask)
+        : "memory");
+}
+// 2-SM TMA multicast: the box lands at the same smem offset in every CTA of `mask`; completion
+// bytes go to each destination pair's leader barrier (the address passed is this pair's leader's).
+__device__ __forceinline__ void tma_load_2d_2sm_mc(void* smem_dst, const CUtensorMap* m, uint32_t bar_cluster_addr, int c0,
+                                                   int c1, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
+        "[%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(bar_cluster_addr), "h"(mask)
         : "memory");
 }
 
