@@ -908,13 +908,20 @@ struct BwdPersistTraits : tc::TraitsBase, BwdEpi {
             return p.sk_scratch + ((static_cast<int64_t>(c_id * 2 + static_cast<int>(rank)) * 2 + par) * KQ + j) * kBlock;
         };
         // 1) export the blocks the partners finalise (TMEM cols [64 j, +64) for j != kh)
+        //    (p.epi_skip: diagnosis only -- 1 skips the TMEM loads, 2 skips the stores)
 #pragma unroll 1
         for (int x = sl.sub; x < 4 * KQ; x += sl.n) {
             const int j = x >> 2, c = x & 3;
             if (j == u.kh) continue;
             uint32_t v[16];
-            ptx::tmem_ld_32x32b_x16_(tbase + 64 * j + 16 * c, v);
-            ptx::tmem_ld_wait();
+            if (p.epi_skip != 1) {
+                ptx::tmem_ld_32x32b_x16_(tbase + 64 * j + 16 * c, v);
+                ptx::tmem_ld_wait();
+            } else {
+#pragma unroll
+                for (int k = 0; k < 16; ++k) v[k] = 0u;
+            }
+            if (p.epi_skip == 2) continue;
             float4* dst = reinterpret_cast<float4*>(block(cid, j) + (c * 128 + row) * 16);
 #pragma unroll
             for (int k = 0; k < 4; ++k)
@@ -922,8 +929,10 @@ struct BwdPersistTraits : tc::TraitsBase, BwdEpi {
                                             __uint_as_float(v[4 * k + 2]), __uint_as_float(v[4 * k + 3])));
         }
         // 2) handshake (epoch counters, one increment per item)
-        ptx::named_sync(2, 32 * EPI_WARPS);
         const bool leader = q == 0 && sl.sub == 0 && lane == 0;
+        if (leader && w.tile == 2) tc::trace_once(p.trace, 42);  // this warp's export done
+        ptx::named_sync(2, 32 * EPI_WARPS);
+        if (leader && w.tile == 2) tc::trace_once(p.trace, 40);  // export done (all warps)
         if (leader) {
             __threadfence();
             const unsigned mine_epoch = atomicAdd(p.sk_flags + cid * 2 + rank, 1u) + 1u;
@@ -932,6 +941,7 @@ struct BwdPersistTraits : tc::TraitsBase, BwdEpi {
             __threadfence();
         }
         ptx::named_sync(2, 32 * EPI_WARPS);
+        if (leader && w.tile == 2) tc::trace_once(p.trace, 41);  // handshake done
         // 3) cell backward on the owned 64 units (inputs pre-issued by epi_begin2), partners' partials added
         const float* pr[3] = {nullptr, nullptr, nullptr};
         for (int j = 0, n = 0; j < KQ; ++j)
@@ -1169,6 +1179,8 @@ bool lstm_bwd_layer_persistent(const LstmBwdLayer& L, int ndirs, int B, int H, i
     }
     p.B = B; p.H = H; p.T = T; p.m_tiles = m_tiles; p.n_tiles = n_tiles; p.units = units; p.kbh = G4 / kBK / kq;
     p.sk_scratch = sk_scratch; p.sk_flags = sk_flags; p.dep = dep; p.exit_ctr = exit_ctr;
+    static const int export_dbg = std::getenv("ADPSGD_EXPORT_DBG") ? std::atoi(std::getenv("ADPSGD_EXPORT_DBG")) : 0;
+    p.epi_skip = export_dbg;
     p.trace = trace_take();
     const double flops = 2.0 * 2 * (T - 1) * static_cast<double>(B) * H * G4;
     const double bytes = 2.0 * (T - 1) * (2.0 * (B + H) * G4 + static_cast<double>(B) * H * (4 + 8 + 8 + 4 + 4 + 8));
