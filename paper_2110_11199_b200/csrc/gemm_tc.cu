@@ -494,7 +494,8 @@ struct PlanHash {
 bool gemm_wgrad_wide(int M, int N) {
     const int npairs = num_sms() / 2;
     const int mt = (M + 255) / 256;
-    return g_force_ext && g_use_wide_gemm && M > 128 && N >= 1024 && N % 512 == 0 && mt * (N / 512) <= npairs;
+    static const bool on = std::getenv("ADPSGD_WIDE_WGRAD") && std::getenv("ADPSGD_WIDE_WGRAD")[0] == '1';
+    return (g_force_ext || on) && g_use_wide_gemm && M > 128 && N >= 1024 && N % 512 == 0 && mt * (N / 512) <= npairs;
 }
 
 bool g_use_xtra = true;
@@ -511,6 +512,7 @@ const GemmWorkspace& gemm_workspace() { return t_ws; }
 void gemm_tc(const GemmArgs& g, cudaStream_t s) {
     static const bool mcb_env = [] {
         if (const char* e = std::getenv("ADPSGD_MCB")) g_use_mcb = e[0] == '1';
+        if (const char* e = std::getenv("ADPSGD_FORCE_EXT")) g_force_ext = e[0] == '1';
         return true;
     }();
     (void)mcb_env;
