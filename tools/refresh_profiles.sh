@@ -14,8 +14,11 @@ cap() {  # name regex skip count
 cap fwd "FwdPersistTraits" 2
 cap bwd "BwdPersistTraits" 2
 cap ce "CeTraits" 0 2
-cap wgrad "GenTraits<.int.256, .bool.1, .bool.1, .bool.0, .bool.0, .bool.0>" 2
+cap wgrad "GenTraits<.int.256, .bool.1, .bool.1, .bool.0, .bool.0, .bool.0, .bool.0>" 2
 cap dgrad "GenTraits<.int.512" 0
+cap update "sdpsgd_kernel" 0
+cap gather "gather_kernel" 1
 python bench.py > gpurun_out/${tag}_bench.log 2>&1
+python tools/ingress_probe.py > gpurun_out/${tag}_ingress.txt 2>&1
 tail -1 gpurun_out/${tag}_bench.log > gpurun_out/${tag}_bench.json
 ls -la gpurun_out | grep $tag
