@@ -340,6 +340,13 @@ struct BwdParams {
 struct EpiRows {
     int data = 0, cp = 0, dc = 0;
     bool has_prev = false;
+    // persistent BPTT: dc_rec lives in TMEM (column base, per-warp lane quarter) after the first
+    // step, and c_t is the c_{t-1} the same CTA loaded one step earlier (also kept in TMEM)
+    bool dc_tmem = false;    // read dc_rec from TMEM (else TMA) -- written to TMEM whenever tdc != 0
+    bool c_tmem = false;     // read c from TMEM (else TMA); c_{t-1} is written to TMEM whenever tc != 0
+    bool tstate = false;     // TMEM state addresses present (TMEM address 0 is a valid lane-quarter-0 address)
+    bool tdc_valid = false, tc_valid = false;
+    uint32_t tdc = 0, tc_ = 0;
 };
 
 struct BwdEpi {
@@ -354,11 +361,11 @@ struct BwdEpi {
         return r;
     }
     __device__ static void issue(const BwdGroup& g, int H, int j0, int rowbase, uint8_t* in, uint64_t* bar, const EpiRows& r) {
-        ptx::mbar_arrive_expect_tx(bar, (r.has_prev ? 4 : 3) * 2048 + 4 * 1024);
+        ptx::mbar_arrive_expect_tx(bar, (1 + (r.dc_tmem ? 0 : 1) + (r.c_tmem ? 0 : 1) + (r.has_prev ? 1 : 0)) * 2048 + 4 * 1024);
         const uint64_t stream = ptx::policy_evict_first();
         ptx::tma_load_2d_hint(in, &g.m_dH, bar, j0, rowbase + r.data, stream);
-        ptx::tma_load_2d(in + 2048, &g.m_dc, bar, j0, rowbase + r.dc);
-        ptx::tma_load_2d_hint(in + 4096, &g.m_c, bar, j0, rowbase + r.data, stream);
+        if (!r.dc_tmem) ptx::tma_load_2d(in + 2048, &g.m_dc, bar, j0, rowbase + r.dc);
+        if (!r.c_tmem) ptx::tma_load_2d_hint(in + 4096, &g.m_c, bar, j0, rowbase + r.data, stream);
         if (r.has_prev) ptx::tma_load_2d_hint(in + 6144, &g.m_cp, bar, j0, rowbase + r.cp, stream);
 #pragma unroll
         for (int gi = 0; gi < 4; ++gi)
@@ -388,8 +395,8 @@ struct BwdEpi {
             const int box = lane & 7;
             if ((lane >> 3) != (i & 3)) continue;
             if (box == 0) ptx::tma_prefetch_l2_2d(&g.m_dH, j0, rowbase + r.data);
-            else if (box == 1) ptx::tma_prefetch_l2_2d(&g.m_dc, j0, rowbase + r.dc);
-            else if (box == 2) ptx::tma_prefetch_l2_2d(&g.m_c, j0, rowbase + r.data);
+            else if (box == 1) { if (!r.dc_tmem) ptx::tma_prefetch_l2_2d(&g.m_dc, j0, rowbase + r.dc); }
+            else if (box == 2) { if (!r.c_tmem) ptx::tma_prefetch_l2_2d(&g.m_c, j0, rowbase + r.data); }
             else if (box == 3) { if (has_prev) ptx::tma_prefetch_l2_2d(&g.m_cp, j0, rowbase + r.cp); }
             else ptx::tma_prefetch_l2_2d(&g.m_gates, (box - 4) * H + j0, rowbase + r.data);
         }
@@ -429,7 +436,7 @@ struct BwdEpi {
             uint8_t* in = st + b * IN_BYTES;
             uint32_t acc[16];
             ptx::tmem_ld_32x32b_x16_(tbase + uc, acc);
-            ptx::tmem_ld_wait();
+            ptx::tmem_ld_wait_regs(acc);
             if (uc + step >= SPAN) release();
             // split-K partners' partials of these units, added in a fixed order (deterministic)
             const float* peers[3] = {peer, peer2, peer3};
@@ -451,10 +458,21 @@ struct BwdEpi {
             ptx::mbar_wait(ebar + b, (ephase >> b) & 1u);
             ephase ^= 1u << b;
             uint32_t wdh[16], wdc[16], wc[16], wcp[16], wi[8], wf[8], wg[8], wo[8];
+            if (r.dc_tmem || r.c_tmem) {  // (same lane quarter as the accumulator; uc = the chunk's column)
+                __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge after the per-thread mbarrier spin
+                if (r.dc_tmem) ptx::tmem_ld_32x32b_x16_(r.tdc + uc, wdc);
+                if (r.c_tmem) ptx::tmem_ld_32x32b_x16_(r.tc_ + uc, wc);
+                if (r.dc_tmem) ptx::tmem_ld_wait_regs(wdc);
+                if (r.c_tmem) ptx::tmem_ld_wait_regs(wc);
+            }
             tc::ld_row_words<64>(in, lane, wdh);
-            tc::ld_row_words<64>(in + 2048, lane, wdc);
-            tc::ld_row_words<64>(in + 4096, lane, wc);
+            if (!r.dc_tmem) tc::ld_row_words<64>(in + 2048, lane, wdc);
+            if (!r.c_tmem) tc::ld_row_words<64>(in + 4096, lane, wc);
             if (has_prev) tc::ld_row_words<64>(in + 6144, lane, wcp);
+            if (r.tstate && r.tc_valid && has_prev) {  // c_{t-1} is the next step's c
+                __syncwarp();
+                ptx::tmem_st_32x32b_x16(r.tc_ + uc, wcp);
+            }
             tc::ld_row_words<32>(in + 8192 + 0 * 1024, lane, wi);
             tc::ld_row_words<32>(in + 8192 + 1 * 1024, lane, wf);
             tc::ld_row_words<32>(in + 8192 + 2 * 1024, lane, wg);
@@ -502,13 +520,19 @@ struct BwdEpi {
             tc::st_row_words<32>(bdz + 1 * 1024, lane, zf);
             tc::st_row_words<32>(bdz + 2 * 1024, lane, zg);
             tc::st_row_words<32>(bdz + 3 * 1024, lane, zo);
-            tc::st_row_words<64>(bdco, lane, dco);
+            if (r.tstate && r.tdc_valid) {
+                __syncwarp();
+                ptx::tmem_st_32x32b_x16(r.tdc + uc, dco);
+                ptx::tmem_st_wait();
+            } else {
+                tc::st_row_words<64>(bdco, lane, dco);
+            }
             ptx::fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
 #pragma unroll
                 for (int gi = 0; gi < 4; ++gi) ptx::tma_store_2d(&g.m_dz, bdz + gi * 1024, gi * H + j0, rowbase + r.data);
-                ptx::tma_store_2d(&g.m_dc, bdco, j0, rowbase + r.dc);
+                if (!(r.tstate && r.tdc_valid)) ptx::tma_store_2d(&g.m_dc, bdco, j0, rowbase + r.dc);
                 ptx::bulk_commit();
                 if (INPLACE && uc + NBUF * step < SPAN) {
                     ptx::bulk_wait_read0();  // the stores have read the buffer: refill it with chunk c + NBUF
@@ -833,6 +857,14 @@ struct BwdPersistTraits : tc::TraitsBase, BwdEpi {
     static constexpr bool A_MN = false;
     static constexpr bool B_MN = true;
     static constexpr bool STREAMK = true;
+    // TMEM past the accumulators (KQ = 2 only: 2 x 128 + 256 = 512 columns): per direction d,
+    // dc_rec at [2 BN + 64 d, +64) and the carried c at [2 BN + 128 + 64 d, +64), 64 owned units each
+#ifdef ADPSGD_NO_TSTATE
+    static constexpr bool TSTATE = false;
+#else
+    static constexpr bool TSTATE = KQ == 2;
+#endif
+    static constexpr int TMEM_EXTRA = TSTATE ? 256 : 0;
     static constexpr int kBlock = 4 * 128 * 16;  // floats of one exported 64-unit block: [4 chunks][128 rows][16]
     struct U {
         int mt, nt, kh, s, d;
@@ -848,7 +880,7 @@ struct BwdPersistTraits : tc::TraitsBase, BwdEpi {
     }
     // time rows: A = dz_{t_src}; the cell backward runs at tn with c_{tnp}
     __device__ static int t_src(const BwdPParams& p, const U& u) { return u.d == 0 ? p.T - 1 - u.s : u.s; }
-    __device__ static EpiRows rows(const BwdPParams& p, const U& u) {
+    __device__ static EpiRows rows(const BwdPParams& p, const U& u, uint32_t tmem_q = 0, bool have_q = false) {
         const int tn = u.d == 0 ? p.T - 2 - u.s : u.s + 1;
         const int tnp = u.d == 0 ? tn - 1 : tn + 1;
         EpiRows r;
@@ -856,6 +888,17 @@ struct BwdPersistTraits : tc::TraitsBase, BwdEpi {
         r.has_prev = tnp >= 0 && tnp < p.T;
         r.cp = r.has_prev ? tnp * p.B : 0;
         r.dc = 0;
+        if (TSTATE) {
+            r.dc_tmem = u.s > 0;  // the first step's dc_rec comes from the first cell backward (memory)
+            r.c_tmem = u.s > 0;   // c_t = the c_{t-1} this CTA loaded one step earlier
+            if (have_q) {         // tmem_q: TMEM base of this warp's lane quarter (epilogue only)
+                r.tstate = true;
+                r.tdc = tmem_q + 2 * BN + 64 * u.d;
+                r.tc_ = tmem_q + 2 * BN + 128 + 64 * u.d;
+                r.tdc_valid = true;
+                r.tc_valid = true;
+            }
+        }
         return r;
     }
     __device__ static int num_tiles(const BwdPParams& p) { return 2 * (p.T - 1); }
@@ -949,7 +992,7 @@ struct BwdPersistTraits : tc::TraitsBase, BwdEpi {
         auto rel = [&] { tc::release_acc_2sm(tempty_leader, lane); };
         body_g<64, true, decltype(rel), 1>(p.g[u.d], p.H, u.mt * 2 * kBM + kBM * static_cast<int>(rank),
                                           u.nt * BN + 64 * u.kh, tbase + 64 * u.kh, q, lane, rel, st, ebar, ephase, sl,
-                                          pr[0], true, rows(p, u), pr[1], pr[2]);
+                                          pr[0], true, rows(p, u, tbase - (tbase & 0xFFFFu) % (2 * BN), true), pr[1], pr[2]);
         // 4) publish: this CTA's dz block of step tn is in memory (TMA stores complete)
         if (lane == 0) {
             ptx::bulk_wait0();

@@ -50,6 +50,7 @@ struct TraitsBase {
     static constexpr bool STREAMK = false;     // work items from Traits::sk_item / epilogue via Traits::epilogue_sk
     static constexpr int EXTRA_COLS = 0;       // extra TMEM columns: row sums of A (all-ones N = 16 MMA) on extra_tile()s
     static constexpr int CLUSTER = 2;          // 4: two CTA pairs per cluster sharing B by TMA multicast (load2_mc)
+    static constexpr int TMEM_EXTRA = 0;       // TMEM columns past the accumulators for the epilogue's own state
     // STREAMK-style item kernels: the producer lane calls item_ready(p, w, cid, rank) before the
     // first TMA load of every item (cross-CTA dependencies of the A operand).
     template <class P, class W>
@@ -204,7 +205,7 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
 // Traits: BN, B_MN, num_tiles (pair tiles), kblocks, prefetch,
 //         load2(p, tile, kb, rank, sA, sB, bar_cluster_addr), epilogue2(p, tile, rank, tbase, q, lane, tempty_leader)
 // ---------------------------------------------------------------------------
-template <int BN, int EPI = 0, bool OVERLAY = false, int ACC = 2, int EXTRA = 0>
+template <int BN, int EPI = 0, bool OVERLAY = false, int ACC = 2, int EXTRA = 0, int TX = 0>
 struct Shape2 {
     static constexpr int BNH = BN / 2;  // B rows held per CTA
     static constexpr int A_BYTES = kBM * kBK * 2;
@@ -213,14 +214,14 @@ struct Shape2 {
     static constexpr int ONES_BYTES = EXTRA ? 2048 : 0;  // all-ones bf16 B operand of the extra MMA
     static constexpr int FIT = (kSmemBudget - (OVERLAY ? 0 : EPI) - ONES_BYTES - 2048) / STAGE_BYTES;
     static constexpr int STAGES = FIT > 8 ? 8 : FIT;
-    static constexpr int COLS = ACC * BN + EXTRA;
+    static constexpr int COLS = ACC * BN + EXTRA + TX;
     static constexpr int TMEM_COLS = COLS <= 32 ? 32 : COLS <= 64 ? 64 : COLS <= 128 ? 128 : COLS <= 256 ? 256 : 512;
     static constexpr int SMEM = STAGES * STAGE_BYTES + (OVERLAY ? 0 : EPI) + ONES_BYTES + 2048;
     static_assert(!OVERLAY || EPI <= STAGES * STAGE_BYTES, "overlaid epilogue smem must fit in the stages");
     static_assert(COLS <= 512, "TMEM has 512 columns");
 };
 template <class T>
-using ShapeOf2 = Shape2<T::BN, T::EPI_SMEM, T::EPI_OVERLAY, T::ACC_STAGES, T::EXTRA_COLS>;
+using ShapeOf2 = Shape2<T::BN, T::EPI_SMEM, T::EPI_OVERLAY, T::ACC_STAGES, T::EXTRA_COLS, T::TMEM_EXTRA>;
 
 // One unit of work of a CTA pair: k-blocks [kb0, kb1) of a tile. role: 0 = whole tile,
 // 1 = stream-K owner (holds k-block 0, adds the later segments' partials), 2 = stream-K
