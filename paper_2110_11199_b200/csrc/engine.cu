@@ -23,6 +23,7 @@
 
 #include "comm.hpp"
 #include "engine.hpp"
+#include "knobs.hpp"
 #include "gemm.hpp"
 #include "gemm_ce.hpp"
 #include "gemm_lstm.hpp"
@@ -32,13 +33,6 @@
 
 namespace ab {
 
-extern bool g_use_pair_mma;  // gemm_lstm.cu
-extern bool g_use_wide_fwd;  // gemm_lstm.cu
-extern bool g_use_splitk_bwd;  // gemm_lstm.cu
-extern bool g_use_pdl;         // gemm_lstm.cu
-extern bool g_use_persist_bwd; // gemm_lstm.cu
-extern bool g_use_persist_fwd; // gemm_lstm.cu
-extern bool g_bwd_kq4;         // gemm_lstm.cu
 
 namespace {
 thread_local std::string g_last_error;
@@ -102,9 +96,9 @@ Ctx::Ctx(const adpsgd_config& c) : cfg(c) {
     bf16_mode = c.precision == ADPSGD_PREC_BF16;
     es = bf16_mode ? 2 : 4;
     T = lay.T; B = c.batch; H = lay.H; nd = lay.nd; I = lay.I;
-    fold_bias = bf16_mode;  // bias grads from a ones column of the wgrad B operands (no colsum passes)
-    if (const char* e = std::getenv("ADPSGD_NO_FOLD_BIAS")) fold_bias = fold_bias && e[0] == '0';
-    if (const char* e = std::getenv("ADPSGD_NO_FOLD_IH")) fold_ih_ok = e[0] == '0';
+    reload_knobs();  // tuning / experiment switches (knobs.hpp), re-read per context
+    fold_bias = bf16_mode && knobs().fold_bias;  // bias grads from a ones column of the wgrad B operands
+    fold_ih_ok = knobs().fold_ih;
     Ipad = bf16_mode ? static_cast<int>(round_up(I + (fold_bias ? 1 : 0), 8)) : I;
     ldH = nd * H + (fold_bias ? 8 : 0);
     ldY = lay.P > 0 ? (fold_bias ? lay.P + 8 : lay.P) : 0;
@@ -113,19 +107,8 @@ Ctx::Ctx(const adpsgd_config& c) : cfg(c) {
     nd4H = nd * 4 * H;
     k = 0;
     history_depth = c.strategy == ADPSGD_GENERIC ? c.staleness_cap + 1 : 1;  // engine.cpp:216-217
-    if (const char* e = std::getenv("ADPSGD_NO_GRAPHS")) use_graphs = e[0] == '0';
-    if (const char* e = std::getenv("ADPSGD_NO_FUSED")) use_fused_cell = e[0] == '0';
-    if (const char* e = std::getenv("ADPSGD_NO_PAIR")) g_use_pair_mma = e[0] == '0';
-    if (const char* e = std::getenv("ADPSGD_NO_WIDE")) g_use_wide_fwd = e[0] == '0';
-    if (const char* e = std::getenv("ADPSGD_NO_SPLITK")) g_use_splitk_bwd = e[0] == '0';
-    if (const char* e = std::getenv("ADPSGD_NO_PDL")) g_use_pdl = e[0] == '0';
-    if (const char* e = std::getenv("ADPSGD_NO_PERSIST")) g_use_persist_bwd = e[0] == '0';
-    if (const char* e = std::getenv("ADPSGD_NO_PERSIST_FWD")) g_use_persist_fwd = e[0] == '0';
-    if (const char* e = std::getenv("ADPSGD_BWD_KQ4")) g_bwd_kq4 = e[0] == '1';
-    if (const char* e = std::getenv("ADPSGD_NO_STREAMK")) g_use_streamk = e[0] == '0';
-    if (const char* e = std::getenv("ADPSGD_NO_XTRA")) g_use_xtra = e[0] == '0';
-    if (const char* e = std::getenv("ADPSGD_FORCE_EXT")) g_force_ext = e[0] == '1';
-    if (const char* e = std::getenv("ADPSGD_NO_WIDE_GEMM")) g_use_wide_gemm = e[0] == '0';
+    use_graphs = knobs().graphs;
+    use_fused_cell = knobs().fused_cell;
 
     AB_CUDA(cudaSetDevice(c.device));
     AB_CUDA(cudaStreamCreateWithFlags(&s_main, cudaStreamNonBlocking));

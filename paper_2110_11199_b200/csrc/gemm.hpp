@@ -7,6 +7,8 @@
 // and for the two directions of dX = sum_d dZ_d W_ih_d).
 #pragma once
 
+#include "knobs.hpp"
+
 #include <cstdint>
 
 #include "common.cuh"
@@ -51,11 +53,6 @@ struct GemmWorkspace {
 };
 void set_gemm_workspace(const GemmWorkspace& w);
 const GemmWorkspace& gemm_workspace();
-extern bool g_use_xtra;
-extern bool g_use_streamk;
-extern bool g_force_ext;
-extern bool g_use_mcb;  // experimental: B operand TMA-multicast across two CTA pairs
-extern bool g_use_wide_gemm;  // 256 x 512 CTA-pair tiles for large stream-K dgrads
 bool gemm_wgrad_wide(int M, int N);  // see gemm_tc.cu  // tests: take the extra-column / stream-K kernels whenever the layout allows
 
 // fp32 operands, fp32 or bf16 output, any majorness (gemm_simt.cu).

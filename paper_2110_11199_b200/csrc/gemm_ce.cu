@@ -21,7 +21,6 @@ namespace ab {
 
 EncodeFnT get_encode_fn();                // gemm_tc.cu
 unsigned long long* trace_take();         // prof.cu
-extern bool g_use_pair_mma;               // gemm_lstm.cu
 void make_map_gen(CUtensorMap* m, const void* base, bool f32, uint64_t inner, uint64_t outer, int64_t ld,
                   uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle sw);  // gemm_lstm.cu
 
@@ -310,7 +309,7 @@ void ce_forward_backward(const CeArgs& a, cudaStream_t s) {
     AB_CHECK(a.N % 8 == 0 && a.K % 8 == 0, ADPSGD_E_DIMENSION, "fused CE needs C, P multiples of 8");
     CeParams p;
     std::memset(&p, 0, sizeof(p));
-    const bool pair = g_use_pair_mma && a.M > kBM;
+    const bool pair = knobs().pair_mma && a.M > kBM;
     make_map_gen(&p.ta, a.Y, false, a.K, a.M, a.ldY, 64, kBM, CU_TENSOR_MAP_SWIZZLE_128B);
     make_map_gen(&p.tb, a.W, false, a.K, a.N, a.K, 64, pair ? 128 : 256, CU_TENSOR_MAP_SWIZZLE_128B);
     make_map_gen(&p.m_dl, a.dlogits, false, a.N, a.M, a.N, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B);
@@ -319,7 +318,7 @@ void ce_forward_backward(const CeArgs& a, cudaStream_t s) {
     p.m_tiles = pair ? (a.M + 2 * kBM - 1) / (2 * kBM) : (a.M + kBM - 1) / kBM;
     p.n_tiles = (a.N + 255) / 256;
     p.bias = a.bias; p.labels = a.labels; p.part = a.part; p.zlab = a.zlab; p.lse = a.lse; p.scale = a.scale;
-    static const int skip = std::getenv("ADPSGD_EPI_SKIP") ? std::atoi(std::getenv("ADPSGD_EPI_SKIP")) : 0;
+    const int skip = knobs().epi_skip;
     p.epi_skip = skip == 2 ? 1 : (skip >= 3 ? skip : 0);
     const int tiles = p.m_tiles * p.n_tiles;
     const double gemm_flops = 2.0 * a.M * a.N * a.K;

@@ -1045,21 +1045,14 @@ void launch_pair(const Params& p, int pair_tiles, cudaStream_t s) {
 
 }  // namespace
 
-bool g_use_pair_mma = true;
-bool g_use_wide_fwd = true;
-bool g_use_splitk_bwd = true;
-bool g_use_pdl = true;
-bool g_use_persist_bwd = true;
-bool g_use_persist_fwd = true;
-bool g_bwd_kq4 = false;  // KQ = 4 measured slower (3 pipeline stages, 4-way exchange); ADPSGD_BWD_KQ4=1
 
 void lstm_fwd_step(const LstmFwdDir* dirs, int ndirs, int B, int H, int ldg, int ldc, int ldh, cudaStream_t s) {
     AB_CHECK(H % 64 == 0 && ndirs >= 1 && ndirs <= 2, ADPSGD_E_DIMENSION, "fused LSTM step needs H % 64 == 0");
     FwdParams p;
     std::memset(&p, 0, sizeof(p));
-    const bool pair = g_use_pair_mma && B > kBM;
+    const bool pair = knobs().pair_mma && B > kBM;
     // one wave of 256 x 512 pair tiles when every CTA pair gets exactly one tile
-    const bool wide = pair && g_use_wide_fwd && H % 128 == 0 &&
+    const bool wide = pair && knobs().wide_fwd && H % 128 == 0 &&
                       ndirs * ((B + 2 * kBM - 1) / (2 * kBM)) * (H / 128) <= num_sms() / 2;
     const uint32_t wbox = wide ? 128 : 64;
     double flops = 0, bytes = 0;
@@ -1088,8 +1081,7 @@ void lstm_fwd_step(const LstmFwdDir* dirs, int ndirs, int B, int H, int ldg, int
         bytes += 2.0 * (B + 4.0 * H) * K + B * H * (8.0 + 4 + 2 + (a.c_prev ? 4 : 0));
     }
     p.ngroups = ndirs; p.B = B; p.H = H; p.ldg = ldg; p.ldc = ldc; p.ldh = ldh;
-    static const int skip = std::getenv("ADPSGD_EPI_SKIP") ? std::atoi(std::getenv("ADPSGD_EPI_SKIP")) : 0;
-    p.epi_skip = skip;
+    p.epi_skip = knobs().epi_skip;
     p.trace = trace_take();
     p.n_tiles = H / (wide ? 128 : 64);
     ProfScope ps_(s, PROF_GEMM_REC_FWD, flops, bytes);
@@ -1115,10 +1107,10 @@ void lstm_bwd_step(const LstmBwdDir* dirs, int ndirs, int B, int H, int lddh, in
     BwdParams p;
     std::memset(&p, 0, sizeof(p));
     // 128 x 64 tiles: a 1024 x 1024 dgrad per direction is only 64 tiles at BN = 128
-    const bool pair = g_use_pair_mma && B > kBM && H % 128 == 0;
+    const bool pair = knobs().pair_mma && B > kBM && H % 128 == 0;
     const int m_tiles = pair ? (B + 2 * kBM - 1) / (2 * kBM) : (B + kBM - 1) / kBM;
     // split-K 256 x 256 tiles when every (tile, K-half) work unit is resident at once
-    const bool split = pair && g_use_splitk_bwd && sk_scratch && sk_flags && H % 256 == 0 &&
+    const bool split = pair && knobs().splitk_bwd && sk_scratch && sk_flags && H % 256 == 0 &&
                        2 * ndirs * m_tiles * (H / 256) <= num_sms() / 2;
     const int bn = split ? 256 : pair ? 128 : ((ndirs * m_tiles * (H / 128) >= num_sms()) ? 128 : 64);
     double flops = 0, bytes = 0;
@@ -1139,8 +1131,7 @@ void lstm_bwd_step(const LstmBwdDir* dirs, int ndirs, int B, int H, int lddh, in
         bytes += 2.0 * (B + H) * 4.0 * H + B * H * (4 + 8 + 8 + 4 + (a.c_prev ? 4 : 0) + 8);
     }
     p.ngroups = ndirs; p.B = B; p.H = H; p.lddh = lddh; p.ldg = ldg; p.ldc = ldc; p.lddz = lddz;
-    static const int skip = std::getenv("ADPSGD_EPI_SKIP") ? std::atoi(std::getenv("ADPSGD_EPI_SKIP")) : 0;
-    p.epi_skip = skip;
+    p.epi_skip = knobs().epi_skip;
     p.trace = trace_take();
     p.m_tiles = m_tiles;
     p.n_tiles = H / bn;
@@ -1157,7 +1148,7 @@ bool lstm_fwd_layer_persistent(const LstmFwdLayer& L, int ndirs, int B, int H, i
                                unsigned int* exit_ctr) {
     const int m_tiles = B / (2 * kBM), n_tiles = H / 64;
     const int units = m_tiles * n_tiles;
-    if (!(g_use_persist_fwd && g_use_pair_mma && ndirs == 2 && B % (2 * kBM) == 0 && H % 64 == 0 &&
+    if (!(knobs().persist_fwd && knobs().pair_mma && ndirs == 2 && B % (2 * kBM) == 0 && H % 64 == 0 &&
           units <= num_sms() / 2 && dep && exit_ctr))
         return false;
     FwdPParams p;
@@ -1198,10 +1189,10 @@ bool lstm_fwd_layer_persistent(const LstmFwdLayer& L, int ndirs, int B, int H, i
 bool lstm_bwd_layer_persistent(const LstmBwdLayer& L, int ndirs, int B, int H, int T, cudaStream_t s, float* sk_scratch,
                                unsigned int* sk_flags, unsigned int* dep, unsigned int* exit_ctr) {
     // 256 x 256 tiles in K quarters when H allows and the units fit, else 256 x 128 in K halves
-    const int kq = (g_bwd_kq4 && H % 256 == 0 && (B / (2 * kBM)) * (H / 256) * 4 <= num_sms() / 2) ? 4 : 2;
+    const int kq = (knobs().bwd_kq4 && H % 256 == 0 && (B / (2 * kBM)) * (H / 256) * 4 <= num_sms() / 2) ? 4 : 2;
     const int m_tiles = B / (2 * kBM), n_tiles = H / (64 * kq);
     const int units = m_tiles * n_tiles * kq;
-    if (!(g_use_persist_bwd && g_use_pair_mma && ndirs == 2 && T >= 2 && B % (2 * kBM) == 0 && H % 128 == 0 &&
+    if (!(knobs().persist_bwd && knobs().pair_mma && ndirs == 2 && T >= 2 && B % (2 * kBM) == 0 && H % 128 == 0 &&
           units <= num_sms() / 2 && sk_scratch && sk_flags && dep && exit_ctr))
         return false;
     BwdPParams p;
@@ -1222,8 +1213,7 @@ bool lstm_bwd_layer_persistent(const LstmBwdLayer& L, int ndirs, int B, int H, i
     }
     p.B = B; p.H = H; p.T = T; p.m_tiles = m_tiles; p.n_tiles = n_tiles; p.units = units; p.kbh = G4 / kBK / kq;
     p.sk_scratch = sk_scratch; p.sk_flags = sk_flags; p.dep = dep; p.exit_ctr = exit_ctr;
-    static const int export_dbg = std::getenv("ADPSGD_EXPORT_DBG") ? std::atoi(std::getenv("ADPSGD_EXPORT_DBG")) : 0;
-    p.epi_skip = export_dbg;
+    p.epi_skip = knobs().export_dbg;
     p.trace = trace_take();
     const double flops = 2.0 * 2 * (T - 1) * static_cast<double>(B) * H * G4;
     const double bytes = 2.0 * (T - 1) * (2.0 * (B + H) * G4 + static_cast<double>(B) * H * (4 + 8 + 8 + 4 + 4 + 8));

@@ -451,7 +451,7 @@ void dispatch(const TcParams& p, bool amn, bool bmn, bool cbf16, bool pair, cuda
         // B multicast across two CTA pairs (experiment / where tiles pair up along M)
         const int tiles = p.m_tiles * p.n_tiles;
         const int pairs = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
-        if (g_use_mcb && pair && bmn && p.m_tiles % 2 == 0 && tiles % 2 == 0 && pairs % 2 == 0) {
+        if (knobs().mcb && pair && bmn && p.m_tiles % 2 == 0 && tiles % 2 == 0 && pairs % 2 == 0) {
             if (key == 6) { launch_pair<GenTraits<256, true, true, false, false, false, true>>(p, s); return; }
             if (key == 2) { launch_pair<GenTraits<256, false, true, false, false, false, true>>(p, s); return; }
         }
@@ -494,15 +494,9 @@ struct PlanHash {
 bool gemm_wgrad_wide(int M, int N) {
     const int npairs = num_sms() / 2;
     const int mt = (M + 255) / 256;
-    static const bool on = std::getenv("ADPSGD_WIDE_WGRAD") && std::getenv("ADPSGD_WIDE_WGRAD")[0] == '1';
-    return (g_force_ext || on) && g_use_wide_gemm && M > 128 && N >= 1024 && N % 512 == 0 && mt * (N / 512) <= npairs;
+    return (knobs().force_ext || knobs().wide_wgrad) && knobs().wide_gemm && M > 128 && N >= 1024 && N % 512 == 0 && mt * (N / 512) <= npairs;
 }
 
-bool g_use_xtra = true;
-bool g_use_streamk = true;
-bool g_force_ext = false;
-bool g_use_wide_gemm = true;
-bool g_use_mcb = false;
 namespace {
 thread_local GemmWorkspace t_ws;
 }
@@ -510,32 +504,25 @@ void set_gemm_workspace(const GemmWorkspace& w) { t_ws = w; }
 const GemmWorkspace& gemm_workspace() { return t_ws; }
 
 void gemm_tc(const GemmArgs& g, cudaStream_t s) {
-    static const bool mcb_env = [] {
-        if (const char* e = std::getenv("ADPSGD_MCB")) g_use_mcb = e[0] == '1';
-        if (const char* e = std::getenv("ADPSGD_FORCE_EXT")) g_force_ext = e[0] == '1';
-        return true;
-    }();
-    (void)mcb_env;
     if (g.M <= 0 || g.N <= 0) return;
     AB_CHECK(g.nseg >= 1 && g.nseg <= 2, ADPSGD_E_DIMENSION, "gemm_tc: 1 or 2 K segments");
     const bool amn = g.seg[0].a.mn, bmn = g.seg[0].b.mn;
     for (int i = 1; i < g.nseg; ++i)
         AB_CHECK(g.seg[i].a.mn == amn && g.seg[i].b.mn == bmn, ADPSGD_E_DIMENSION,
                  "gemm_tc: segments must share operand majorness");
-    extern bool g_use_pair_mma;
     // CTA pairs (256-row tiles) whenever there are at least two row blocks
-    const bool pair = g_use_pair_mma && g.M > BM;
+    const bool pair = knobs().pair_mma && g.M > BM;
     const int rows = pair ? 2 * BM : BM;
     const int m_tiles = (g.M + rows - 1) / rows;
     int kbt_all = 0;
     for (int i = 0; i < g.nseg; ++i) kbt_all += (g.seg[i].K + BK - 1) / BK;
     // few-tile, long-K weight gradients (dW_proj) go 256-wide and stream-K over every pair
-    const bool tiny_wgrad = g_use_streamk && pair && amn && bmn && !g.c_bf16 && g.N > 128 && kbt_all >= 64 &&
+    const bool tiny_wgrad = knobs().streamk && pair && amn && bmn && !g.c_bf16 && g.N > 128 && kbt_all >= 64 &&
                             m_tiles * ((g.N + 255) / 256) * 4 <= num_sms() / 2 && gemm_workspace().ws;
-    static const int force_bn = std::getenv("ADPSGD_FORCE_BN") ? std::atoi(std::getenv("ADPSGD_FORCE_BN")) : 0;  // experiments
+    const int force_bn = knobs().force_bn;  // probes
     const int bn0 = force_bn == 128 || force_bn == 256
                         ? force_bn
-                        : (g.N > 128 && (g_force_ext || tiny_wgrad ||
+                        : (g.N > 128 && (knobs().force_ext || tiny_wgrad ||
                                          m_tiles * ((g.N + 255) / 256) >= (pair ? num_sms() / 4 : num_sms() / 2)))
                               ? 256 : 128;
     // bias column (g.extra, one column past n_main) by the extra row-sum MMA instead of a ragged n-tile
@@ -543,8 +530,8 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
     const int npairs = num_sms() / 2;
     const int rounds_plain = (m_tiles * ((g.N + bn0 - 1) / bn0) + npairs - 1) / npairs;
     const int rounds_xtra = (m_tiles * (g.n_main / 256) + npairs - 1) / npairs;
-    const bool xtra = g_use_xtra && g.extra && pair && bn0 == 256 && !g.c_bf16 && amn && bmn && g.n_main == g.N - 1 &&
-                      g.n_main % 256 == 0 && (rounds_xtra < rounds_plain || g_force_ext);
+    const bool xtra = knobs().xtra && g.extra && pair && bn0 == 256 && !g.c_bf16 && amn && bmn && g.n_main == g.N - 1 &&
+                      g.n_main % 256 == 0 && (rounds_xtra < rounds_plain || knobs().force_ext);
     const int n_eff = xtra ? g.n_main : g.N;
     int kbt = 0;
     for (int i = 0; i < g.nseg; ++i) kbt += (g.seg[i].K + BK - 1) / BK;
@@ -559,13 +546,13 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
         // weight-gradient layout only for tiny tile counts (e.g. dW_proj: 9 tiles), where the L2
         // reuse of the lockstep wave order does not matter
         const bool layout_ok = (!amn && bmn) || (amn && bmn && !g.c_bf16 && bnx == 256 && t * 4 <= npairs);
-        return g_use_streamk && pair && bnx >= 256 && wsp.ws && !xtra && layout_ok && (t % npairs != 0 || g_force_ext) &&
+        return knobs().streamk && pair && bnx >= 256 && wsp.ws && !xtra && layout_ok && (t % npairs != 0 || knobs().force_ext) &&
                kbt >= 8 && wsp.floats >= static_cast<size_t>(npairs) * 2 * (bnx / 32 + 1) * 128 * 32 &&
                wsp.flag_count >= static_cast<size_t>(npairs) * 2;
     };
-    const bool wide_wgrad = g_use_wide_gemm && amn && bmn && !g.c_bf16 && !g.extra && gemm_wgrad_wide(g.M, g.N);
-    const bool wide = wide_wgrad || (g_use_wide_gemm && bn0 == 256 && g.N >= 1024 && g.N % 512 == 0 &&
-                                     (m_tiles * (g.N / 512) >= npairs || g_force_ext) && sk_ok(512));
+    const bool wide_wgrad = knobs().wide_gemm && amn && bmn && !g.c_bf16 && !g.extra && gemm_wgrad_wide(g.M, g.N);
+    const bool wide = wide_wgrad || (knobs().wide_gemm && bn0 == 256 && g.N >= 1024 && g.N % 512 == 0 &&
+                                     (m_tiles * (g.N / 512) >= npairs || knobs().force_ext) && sk_ok(512));
     const int bn = wide ? 512 : bn0;
     const int tiles = m_tiles * ((n_eff + bn - 1) / bn);
     const bool sk = !wide_wgrad && sk_ok(bn);

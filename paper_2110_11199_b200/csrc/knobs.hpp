@@ -1,0 +1,36 @@
+// Process-wide tuning / experiment switches, read once from the environment (knobs.cu).
+// Defaults are the measured-best configuration; every switch is documented in DESIGN.md §4a.
+#pragma once
+
+namespace ab {
+
+struct Knobs {
+    // kernel selection (defaults on)
+    bool pair_mma = true;      // ADPSGD_NO_PAIR=1: single-CTA tcgen05 tiles instead of CTA pairs
+    bool wide_fwd = true;      // ADPSGD_NO_WIDE=1: per-step forward without 256x512 one-wave tiles
+    bool splitk_bwd = true;    // ADPSGD_NO_SPLITK=1: per-step BPTT without the split-K variant
+    bool persist_fwd = true;   // ADPSGD_NO_PERSIST_FWD=1: per-step forward launches
+    bool persist_bwd = true;   // ADPSGD_NO_PERSIST=1: per-step BPTT launches
+    bool pdl = true;           // ADPSGD_NO_PDL=1: no programmatic dependent launch
+    bool streamk = true;       // ADPSGD_NO_STREAMK=1: no stream-K GEMMs
+    bool xtra = true;          // ADPSGD_NO_XTRA=1: no extra row-sum MMA for bias columns
+    bool wide_gemm = true;     // ADPSGD_NO_WIDE_GEMM=1: no 256x512 generic GEMM tiles
+    bool graphs = true;        // ADPSGD_NO_GRAPHS=1: eager launches instead of CUDA graphs
+    bool fused_cell = true;    // ADPSGD_NO_FUSED=1: unfused GEMM + pointwise LSTM cell
+    bool fold_bias = true;     // ADPSGD_NO_FOLD_BIAS=1: bias gradients by column sums
+    bool fold_ih = true;       // ADPSGD_NO_FOLD_IH=1: dW_ih bias gradients by column sums
+    // measured slower, kept opt-in
+    bool bwd_kq4 = false;      // ADPSGD_BWD_KQ4=1: persistent BPTT in K quarters
+    bool wide_wgrad = false;   // ADPSGD_WIDE_WGRAD=1: one-wave 512-wide weight gradients
+    bool mcb = false;          // ADPSGD_MCB=1: B operand TMA-multicast across two CTA pairs
+    // tests / diagnosis
+    bool force_ext = false;    // ADPSGD_FORCE_EXT=1: take the extra-column / stream-K / wide kernels wherever legal
+    int force_bn = 0;          // ADPSGD_FORCE_BN=128|256: generic GEMM tile width (probes)
+    int epi_skip = 0;          // ADPSGD_EPI_SKIP=n: epilogue timing experiments
+    int export_dbg = 0;        // ADPSGD_EXPORT_DBG=1|2: split-K export diagnosis
+};
+
+const Knobs& knobs();
+void reload_knobs();  // re-read the environment (engine context creation)
+
+}  // namespace ab

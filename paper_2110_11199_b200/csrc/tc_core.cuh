@@ -8,11 +8,8 @@
 #pragma once
 
 #include "common.cuh"
+#include "knobs.hpp"
 #include "tc_ptx.cuh"
-
-namespace ab {
-extern bool g_use_pdl;  // gemm_lstm.cu: programmatic dependent launch for the tcgen05 kernels
-}
 
 namespace ab::tc {
 
@@ -556,7 +553,7 @@ inline void launch_tc(void (*kern)(P), const P& p, int grid, int threads, int sm
         attrs[n].val.clusterDim.z = 1;
         ++n;
     }
-    if (g_use_pdl) {
+    if (knobs().pdl) {
         attrs[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attrs[n].val.programmaticStreamSerializationAllowed = 1;
         ++n;
