@@ -94,3 +94,24 @@ def test_consensus_distance_bf16_group():
         g.set_weights(j, w)
     want = _consensus([w.astype(np.float32).astype(np.float64) for w in ws])
     assert abs(g.consensus_distance() - want) <= 1e-5 * want
+
+
+@pytest.mark.parametrize("strategy", [Strategy.ADPSGD_RM, Strategy.ADPSGD_D1D])
+def test_bf16_steps_bit_identical_across_runs(strategy):
+    """Two engines with the same seed and data produce bit-identical weights after several bf16
+    steps (the reference's run_training determinism, test_engine.cpp:344-365): every reduction on
+    the path -- stream-K and split-K partial sums, the CE log-sum-exp, bias column sums -- runs in
+    a fixed order, and the persistent kernels use atomics only for their step counters."""
+    m = ModelDesc(layers=2, hidden=128, bidirectional=True, input_dim=40, proj=256, classes=304, unroll=5)
+    cfg = StrategyConfig(strategy=strategy, learners=3, batch=256, seed=11)
+    out = []
+    for _ in range(2):
+        g = LearnerGroup(m, cfg, precision=Precision.BF16)
+        g.synth_dataset(1024, 1000, seed=5)
+        losses = [g.step(0.5).copy() for _ in range(3)]
+        out.append((np.stack(losses), [g.weights(j) for j in range(3)]))
+        g.close()
+    (l0, w0), (l1, w1) = out
+    assert np.array_equal(l0, l1)
+    for a, b in zip(w0, w1):
+        assert np.array_equal(a, b)
