@@ -781,7 +781,13 @@ struct FwdPersistTraits : tc::TraitsBase {
         const int seg = kb < p.kbx ? 0 : 1;
         const int k0 = (seg == 0 ? kb : kb - p.kbx) * kBK;
         const int row = (seg == 0 ? u.t : u.tp) * p.B + u.mt * 2 * kBM + kBM * static_cast<int>(rank);
+#ifdef ADPSGD_A_EVICT_FIRST
         ptx::tma_load_2d_2sm_hint(sA, &g.ta[seg], bar, k0, row, ptx::policy_evict_first());
+#else
+        // A rows are read by every unit tile of the m-tile, at different times in the persistent
+        // schedule: default L2 policy (evict_first cost DRAM re-reads)
+        ptx::tma_load_2d_2sm(sA, &g.ta[seg], bar, k0, row);
+#endif
         const uint64_t keep = ptx::policy_evict_last();
 #pragma unroll
         for (int j = 0; j < 2; ++j)
@@ -923,8 +929,7 @@ struct BwdPersistTraits : tc::TraitsBase, BwdEpi {
         const U u = unit(p, blockIdx.x >> 1, it);
         const BwdGroup& g = p.g[u.d];
         const int k0 = (u.kh * p.kbh + kb) * kBK;
-        ptx::tma_load_2d_2sm_hint(sA, &g.ta, bar, k0, t_src(p, u) * p.B + u.mt * 2 * kBM + kBM * static_cast<int>(rank),
-                                  ptx::policy_evict_first());
+        ptx::tma_load_2d_2sm(sA, &g.ta, bar, k0, t_src(p, u) * p.B + u.mt * 2 * kBM + kBM * static_cast<int>(rank));
         const uint64_t keep = ptx::policy_evict_last();
 #pragma unroll
         for (int j = 0; j < BN / 128; ++j)
