@@ -9,6 +9,7 @@ Tolerances (stated):
 """
 import numpy as np
 import pytest
+import torch
 
 from paper_2110_11199_b200 import LearnerGroup, MixKind, ModelDesc, Precision, Strategy, StrategyConfig
 from paper_2110_11199_b200.errors import StalenessOverflowError, SyncViolationError
@@ -314,3 +315,56 @@ def test_bf16_training_reduces_loss():
     for _ in range(40):
         last = g.step(1.0).mean()
     assert np.isfinite(last) and last < first
+
+
+def _full_size_grads(layers, weights_round):
+    m = ModelDesc(layers=layers, hidden=1024, bidirectional=True, input_dim=260, proj=256, classes=32000, unroll=21)
+    M = 256
+    rng = np.random.default_rng(101)
+    n_seg = 512
+    feats = rng.normal(size=(n_seg, m.unroll, m.input_dim)).astype(np.float32)
+    labels = rng.integers(0, m.classes, size=(n_seg, m.unroll)).astype(np.int32)
+    idx = rng.integers(0, n_seg, size=M).astype(np.int32)
+    groups = {}
+    for prec in (Precision.BF16, Precision.FP32):
+        groups[prec] = LearnerGroup(m, StrategyConfig(learners=1, batch=M, seed=3), precision=prec)
+        groups[prec].set_dataset(feats, labels, n_seg)
+    w = groups[Precision.FP32].weights(0).copy()  # the engine's own w0 (0.1 N(0,1), engine.cpp:99-116)
+    wr = torch.from_numpy(w).to(torch.bfloat16).float().numpy()
+    out = {"bf16": groups[Precision.BF16].gradient(wr, idx), "fp32_r": groups[Precision.FP32].gradient(wr, idx)}
+    if weights_round:
+        out["fp32"] = groups[Precision.FP32].gradient(w, idx)
+    for g in groups.values():
+        g.close()
+    return out
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def test_full_width_two_layer_bf16_gradient_matches_fp32_engine():
+    """BASELINE configs[1] widths (1024 units/dir, proj 256, 32k classes, T = 21, 256 segments) at
+    2 layers: bf16 tcgen05 path (persistent recurrent kernels, fused 32k-class softmax-CE,
+    stream-K / extra-column GEMMs) against the FP32 SIMT engine on the same bf16-representable
+    weights. Bar: loss rel err <= 1e-2, gradient rel L2 err <= 5e-2 (bf16 operands; measured 1.7e-2)."""
+    out = _full_size_grads(2, False)
+    (lb, gb), (lf, gf) = out["bf16"], out["fp32_r"]
+    assert np.isfinite(lb) and np.all(np.isfinite(gb))
+    assert abs(lb - lf) <= 1e-2 * abs(lf)
+    assert _rel(gb, gf) <= 5e-2
+
+
+def test_full_size_bf16_gradient_at_fp32_conditioning_floor():
+    """Full BASELINE configs[1] model (6 layers). With the reference's init (0.1 N(0,1) at 1024
+    units, recurrent gain ~3) the 6-layer objective is ill-conditioned: rounding the weights to
+    bf16 alone moves the FP32 engine's gradient by ~48 % (measured; tools/fullsize_sens.py), so a
+    fixed tolerance is meaningless. Property instead: the bf16 path's distance from the FP32
+    engine (same rounded weights) is no larger than 1.5x the FP32 engine's own sensitivity to a
+    bf16-sized weight perturbation, and the loss agrees to 1e-2."""
+    out = _full_size_grads(6, True)
+    (lb, gb), (lr, gr), (lf, gf) = out["bf16"], out["fp32_r"], out["fp32"]
+    assert np.isfinite(lb) and np.all(np.isfinite(gb))
+    assert abs(lb - lr) <= 1e-2 * abs(lr)
+    floor = _rel(gr, gf)
+    assert _rel(gb, gr) <= 1.5 * floor + 2e-2, (_rel(gb, gr), floor)
