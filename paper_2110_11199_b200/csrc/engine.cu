@@ -124,6 +124,10 @@ Ctx::Ctx(const adpsgd_config& c) : cfg(c) {
     // ---- workspace (shared by the local learners; they are computed in turn) ----
     idx_dev = static_cast<int32_t*>(alloc(sizeof(int32_t) * B));
     X0 = alloc(TB * Ipad * es);
+    if (bf16_mode && Ipad > 256 && Ipad <= 264) {
+        X0tail = alloc(16 * TB * sizeof(bf16));
+        AB_CUDA(cudaMemset(X0tail, 0, 16 * TB * sizeof(bf16)));
+    }
     lab_step = static_cast<int32_t*>(alloc(sizeof(int32_t) * TB));
     for (int l = 0; l < lay.L; ++l) {
         Hout.push_back(alloc(TB * ldH * es));
@@ -145,7 +149,7 @@ Ctx::Ctx(const adpsgd_config& c) : cfg(c) {
         {   // stream-K scratch: (SMs / 2) pairs x 2 CTAs x (16 + 1) chunks x 128 rows x 32 fp32
             gemm_ws.floats = static_cast<size_t>(num_sms() / 2) * 2 * 17 * 128 * 32;
             gemm_ws.ws = static_cast<float*>(alloc(gemm_ws.floats * sizeof(float)));
-            gemm_ws.flag_count = static_cast<size_t>(num_sms());
+            gemm_ws.flag_count = static_cast<size_t>(num_sms()) + 2 * 128;  // + split-K tile counters
             gemm_ws.flags = static_cast<unsigned int*>(alloc(gemm_ws.flag_count * sizeof(unsigned int)));
             AB_CUDA(cudaMemsetAsync(gemm_ws.flags, 0, gemm_ws.flag_count * sizeof(unsigned int), s_main));
         }
@@ -454,7 +458,19 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
         if (fused) {
             // BPTT: first cell backward unfused (no recurrent term), then one launch per step
             // doing dh_rec = dz_t W_hh for both directions with the next cell backward fused.
+            const float* f_dh[2]; const bf16* f_g[2]; const float* f_c[2]; const float* f_cp[2]; bf16* f_dz[2]; float* f_dc[2];
             for (int d = 0; d < nd; ++d) {
+                const int t = d == 0 ? T - 1 : 0;
+                const int tp = d == 0 ? t - 1 : t + 1;
+                f_dh[d] = dHcur + static_cast<int64_t>(t) * B * ndH + d * H;
+                f_g[d] = static_cast<const bf16*>(off_ptr(gates[l], static_cast<int64_t>(t) * B * nd4H + d * G4, es));
+                f_c[d] = cst[l] + static_cast<int64_t>(t) * B * ndH + d * H;
+                f_cp[d] = T > 1 ? cst[l] + static_cast<int64_t>(tp) * B * ndH + d * H : nullptr;
+                f_dz[d] = static_cast<bf16*>(off_ptr(dZ, static_cast<int64_t>(t) * B * nd4H + d * G4, es));
+                f_dc[d] = dc_rec + static_cast<int64_t>(d) * B * H;
+            }
+            const bool first2 = nd == 2 && launch_cell_bwd_first2(f_dh, f_g, f_c, f_cp, f_dz, f_dc, ndH, nd4H, ndH, nd4H, B, H, s);
+            for (int d = 0; d < nd && !first2; ++d) {
                 const int t = d == 0 ? T - 1 : 0;
                 const int tp = d == 0 ? t - 1 : t + 1;
                 const float* cp = T > 1 ? cst[l] + static_cast<int64_t>(tp) * B * ndH + d * H : nullptr;
@@ -540,6 +556,7 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
                 g.seg[0].K = static_cast<int>(TB);
                 g.C = grad + o.w_ih; g.ldc = lay.in_dim[l];
                 if (fold_ih) { g.n_main = lay.in_dim[l]; g.extra = grad + o.b; }  // ones column of the input -> db
+                if (fold_ih && l == 0 && X0tail) { g.b_tail = X0tail; g.ld_tail = TB; }  // features 256.. + ones column
                 g.tag = PROF_GEMM_WGRAD;
                 gemm(bf, g, s);
             }
@@ -580,7 +597,8 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
 
 void Ctx::gather_batch(const float* feats_src, const int32_t* labels_src, const int32_t* idx, cudaStream_t s) {
     if (bf16_mode)
-        launch_gather<bf16>(feats_src, labels_src, idx, B, T, I, Ipad, static_cast<bf16*>(X0), lab_step, s, fold_bias);
+        launch_gather<bf16>(feats_src, labels_src, idx, B, T, I, Ipad, static_cast<bf16*>(X0), lab_step, s, fold_bias,
+                            static_cast<bf16*>(X0tail), 256);
     else
         launch_gather<float>(feats_src, labels_src, idx, B, T, I, Ipad, static_cast<float*>(X0), lab_step, s, false);
 }

@@ -41,10 +41,16 @@ struct GemmArgs {
     // B operand so a weight-gradient GEMM also yields the bias gradient). n_main < 0: off.
     int n_main = -1;
     float* extra = nullptr;
+    // Optional K-major copy of B's columns [256 * floor(n_main / 256), +16) as [16 rows x K] bf16
+    // (row pitch ld_tail elements): lets <= 8 columns past the last full 256-wide tile ride on an
+    // extra N = 16 MMA of that tile instead of a mostly empty extra n-tile (tcgen05 path only).
+    const void* b_tail = nullptr;
+    int64_t ld_tail = 0;
 };
 
 // Stream-K scratch of the calling thread's engine (set before its GEMMs run; see gemm_tc.cu):
-// ws >= (SMs/2) * 2 * 17 * 128 * 32 floats, flags >= SMs u32 zeroed once. ws == nullptr: no stream-K.
+// ws >= (SMs/2) * 2 * 17 * 128 * 32 floats, flags >= SMs (+ 2 per split-K tile) u32 zeroed once.
+// ws == nullptr: no stream-K.
 struct GemmWorkspace {
     float* ws = nullptr;
     size_t floats = 0;

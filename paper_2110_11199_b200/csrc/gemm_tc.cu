@@ -47,17 +47,25 @@ struct TcParams {
     float* sk_ws;              // [pair * 2 + rank][chunk][128 rows][32] fp32
     unsigned int* sk_flags;    // [pair * 2 + rank], zeroed between launches by the owners
     int64_t sk_total;          // tiles * k-blocks per tile
+    int sk_split;              // > 0: one-wave split-K instead -- pair c < sk_split * tiles takes K slice
+                               //      c / tiles of tile c % tiles (slice 0 owns the tile)
+    CUtensorMap tx;            // XTRA = 2: K-major tail columns [16 rows x K] (B columns n_tail0 + row)
+    int n_tail0;
 };
 
 
 // Generic GEMM traits for the persistent skeletons in tc_core.cuh (single CTA and CTA pair).
-// XTRA: the B operand's "ones column" (bias gradient = row sums of A) comes from an extra
-//       N = 16 MMA against an all-ones smem tile on the tiles of n-tile 0 (TMEM cols [BN, BN+16)),
+// XTRA: an extra N = 16 MMA per k-step on the tiles of the last n-tile (TMEM cols [BN, BN+16)),
 //       so N stays a multiple of the tile width (CTA pairs, single accumulator stage).
+//       1: against an all-ones smem tile -- the B operand's "ones column" (bias gradient = row
+//          sums of A) without a ragged n-tile;
+//       2: against B columns [n_tail0, n_tail0 + 16) loaded per stage from a K-major copy of
+//          them (p.tx): a few real columns past the last full tile (layer-1 input features
+//          256..259 + the ones column of a 260-feature input) ride on the last tile.
 // SK:   stream-K work split (tc::Item): every CTA pair gets the same number of k-block iterations;
 //       a tile split between pairs is finished by the pair holding its k-block 0, which adds the
 //       other segments' partials in pair order (deterministic).
-template <int BN_, bool AMN, bool BMN, bool CBF16, bool XTRA = false, bool SK = false, bool MCB = false>
+template <int BN_, bool AMN, bool BMN, bool CBF16, int XTRA = 0, bool SK = false, bool MCB = false>
 struct GenTraits : tc::TraitsBase {
     static constexpr int BN = BN_;
     static constexpr int CLUSTER = MCB ? 4 : 2;  // MCB: two pairs (same n-tile) share B by TMA multicast
@@ -66,14 +74,29 @@ struct GenTraits : tc::TraitsBase {
     static constexpr bool A_MN = AMN;
     static constexpr bool B_MN = BMN;
     static constexpr int EXTRA_COLS = XTRA ? 32 : 0;
+    static constexpr int XB_BYTES = XTRA == 2 ? 1024 : 0;  // per CTA: 8 tail rows x 64 k, K-major SW128
     static constexpr int ACC_STAGES = (XTRA || BN_ > 256) ? 1 : 2;
     static constexpr int MMA_N = BN_ > 256 ? 256 : 0;
     static constexpr bool STREAMK = SK;
     static constexpr int NCH = BN / 32 + (XTRA ? 1 : 0);  // 32-column chunks of a partial (incl. the extra)
-    __device__ static bool extra_tile(const TcParams& p, int tile) { return XTRA && tile / p.m_tiles == 0; }
+    __device__ static bool extra_tile(const TcParams& p, int tile) { return XTRA && tile / p.m_tiles == p.n_tiles - 1; }
+    // XTRA = 2: rank r loads tail rows [8 r, +8) of k-block kb (single K segment)
+    __device__ static void load_x(const TcParams& p, int, int kb, uint32_t rank, uint8_t* sX, uint32_t bar) {
+        ptx::tma_load_2d_2sm(sX, &p.tx, bar, kb * BK, 8 * static_cast<int>(rank));
+    }
     __device__ static int64_t sk_start(const TcParams& p, int c, int ncl) { return p.sk_total * c / ncl; }
     __device__ static bool sk_item(const TcParams& p, int cid, int ncl, int it, tc::Item& w) {
         const int kbt = kblocks(p, 0);
+        if (p.sk_split > 0) {  // split-K: concurrent pairs walk the same K range (DRAM row locality)
+            const int tiles = num_tiles(p), S = p.sk_split;
+            if (it > 0 || cid >= S * tiles) return false;
+            const int slice = cid / tiles;
+            w.tile = cid % tiles;
+            w.kb0 = static_cast<int>(static_cast<int64_t>(slice) * kbt / S);
+            w.kb1 = static_cast<int>(static_cast<int64_t>(slice + 1) * kbt / S);
+            w.role = S == 1 ? 0 : (slice == 0 ? 1 : 2);
+            return true;
+        }
         int64_t pos = sk_start(p, cid, ncl);
         const int64_t end = sk_start(p, cid + 1, ncl);
         for (int i = 0;; ++i) {
@@ -174,6 +197,88 @@ struct GenTraits : tc::TraitsBase {
         body(p, m0 + q * 32, n0, tbase, lane, [&] { tc::release_acc_2sm(tempty_leader, lane); }, sl,
              extra_tile(p, tile), [](int, uint32_t*) {});
     }
+    // One-wave split-K epilogue as a reduce-scatter: the S units of a tile (K slices, pairs
+    // j * tiles + tile) each finalise one group of its 32-column chunks (chunk c -> slice c * S / NCH)
+    // and export the others. Every output element is summed in slice order 0..S-1 whichever unit
+    // finalises it (deterministic). The last unit through re-arms the tile's flags.
+    template <class Rel>
+    __device__ static void split_epilogue(const TcParams& p, const tc::Item& w, int cid, uint32_t rank, uint32_t tbase,
+                                          int q, int lane, tc::EpiSlot sl, Rel release) {
+        const int tiles = num_tiles(p), S = p.sk_split;
+        const int m0 = (w.tile % p.m_tiles) * 2 * BM + BM * static_cast<int>(rank), n0 = (w.tile / p.m_tiles) * BN;
+        const int row = q * 32 + lane;
+        const bool xt = extra_tile(p, w.tile);
+        const int slice = cid / tiles;
+        constexpr int kSlot = NCH * 128 * 32;
+        auto group = [&](int c) { return c * S / NCH; };
+        auto slot = [&](int j) { return p.sk_ws + static_cast<int64_t>((j * tiles + w.tile) * 2 + static_cast<int>(rank)) * kSlot; };
+        const bool leader = q == 0 && sl.sub == 0 && lane == 0;
+        if (S > 1) {
+            // 1) export the chunks the other units finalise
+#pragma unroll 1
+            for (int c = sl.sub; c < NCH; c += sl.n) {
+                if (group(c) == slice) continue;
+                const bool xc = c >= BN / 32;
+                if (xc && !xt) continue;
+                uint32_t r[32];
+                if (!xc) ptx::tmem_ld_32x32b_x32(tbase + 32 * c, r);
+                else ptx::tmem_ld_32x32b_x16_(tbase + BN, r);
+                ptx::tmem_ld_wait();
+                float4* dst = reinterpret_cast<float4*>(slot(slice) + (static_cast<int64_t>(c) * 128 + row) * 32);
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    __stcg(dst + i, make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
+                                                __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3])));
+            }
+            // 2) handshake with the other S - 1 units of the tile
+            ptx::named_sync(2, 32 * EPI_WARPS);
+            if (leader) {
+                __threadfence();
+                asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.sk_flags + cid * 2 + rank), "r"(1u) : "memory");
+                for (int j = 0; j < S; ++j)
+                    if (j != slice) ptx::spin_until_geq(p.sk_flags + (j * tiles + w.tile) * 2 + rank, 1u);
+                __threadfence();
+            }
+            ptx::named_sync(2, 32 * EPI_WARPS);
+        }
+        // 3) finalise this unit's chunks: sum over slices in order, own TMEM value at position `slice`
+        body(p, m0 + q * 32, n0, tbase, lane, release, sl, xt, [&](int c, uint32_t* r) {
+            if (S == 1) return;
+            float acc[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) acc[i] = 0.f;
+            for (int j = 0; j < S; ++j) {
+                if (j == slice) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) acc[i] = j == 0 ? __uint_as_float(r[i]) : acc[i] + __uint_as_float(r[i]);
+                } else {
+                    const float4* src = reinterpret_cast<const float4*>(slot(j) + (static_cast<int64_t>(c) * 128 + row) * 32);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const float4 f = __ldcg(src + i);
+                        acc[4 * i] = j == 0 ? f.x : acc[4 * i] + f.x;
+                        acc[4 * i + 1] = j == 0 ? f.y : acc[4 * i + 1] + f.y;
+                        acc[4 * i + 2] = j == 0 ? f.z : acc[4 * i + 2] + f.z;
+                        acc[4 * i + 3] = j == 0 ? f.w : acc[4 * i + 3] + f.w;
+                    }
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(acc[i]);
+        }, [&](int c) { return S == 1 || group(c) == slice; });
+        if (S > 1) {  // 4) every unit has read the tile's partials: the last one re-arms the flags
+            ptx::named_sync(2, 32 * EPI_WARPS);
+            if (leader) {
+                unsigned int* ctr = p.sk_flags + gridDim.x + w.tile * 2 + rank;
+                __threadfence();
+                if (atomicAdd(ctr, 1u) == static_cast<unsigned>(S - 1)) {
+                    for (int j = 0; j < S; ++j) p.sk_flags[(j * tiles + w.tile) * 2 + rank] = 0u;
+                    *ctr = 0u;
+                    __threadfence();
+                }
+            }
+        }
+    }
     // stream-K epilogue: role 0 = plain tile; 2 = export the partial (all chunks incl. the extra)
     // and flag it; 1 = wait for the later segments' pairs, add their partials, finish the tile.
     __device__ static void epilogue_sk(const TcParams& p, const tc::Item& w, int cid, uint32_t rank, uint32_t tbase,
@@ -185,6 +290,10 @@ struct GenTraits : tc::TraitsBase {
         auto release = [&] { tc::release_acc_2sm(tempty_leader, lane); };
         constexpr int kSlot = NCH * 128 * 32;  // floats per CTA slot
         const int ncl = gridDim.x >> 1;
+        if (p.sk_split > 0) {
+            split_epilogue(p, w, cid, rank, tbase, q, lane, sl, release);
+            return;
+        }
         if (w.role == 2) {
             float* ws = p.sk_ws + static_cast<int64_t>(cid * 2 + static_cast<int>(rank)) * kSlot;
 #pragma unroll 1
@@ -246,23 +355,40 @@ struct GenTraits : tc::TraitsBase {
     // TMEM accumulator (thread = row, 32-column chunks in registers) -> alpha / bias / accumulate
     // -> vectorised row-segment stores. fix(c, r) adds stream-K partials to chunk c; xt: also
     // write the extra row-sum column (TMEM col BN) to extra[row].
-    template <class Rel, class Fix>
+    struct KeepAll {
+        __device__ bool operator()(int) const { return true; }
+    };
+    template <class Rel, class Fix, class Keep = KeepAll>
     __device__ static void body(const TcParams& p, int rowbase, int n0, uint32_t tbase, int lane, Rel release,
-                                tc::EpiSlot sl, bool xt, Fix fix) {
+                                tc::EpiSlot sl, bool xt, Fix fix, Keep keep = Keep()) {
         const int gm = rowbase + lane;
         const bool row_ok = gm < p.M;
-        if (XTRA && xt && sl.sub == 0) {
+        if (XTRA && xt && sl.sub == 0 && keep(BN / 32)) {
             uint32_t r[32];
             ptx::tmem_ld_32x32b_x16_(tbase + BN, r);
             ptx::tmem_ld_wait();
             fix(BN / 32, r);
-            if (row_ok) {
+            if (row_ok && XTRA == 1) {
                 const float x = p.alpha * __uint_as_float(r[0]);
                 p.extra[gm] = p.accumulate ? p.extra[gm] + x : x;
+            }
+            if (row_ok && XTRA == 2) {  // tail columns n_tail0 + f: the C row below n_main, extra[] at n_main
+                float* crow = reinterpret_cast<float*>(p.C) + static_cast<int64_t>(gm) * p.ldc;
+#pragma unroll
+                for (int f = 0; f < 16; ++f) {
+                    const int gn = p.n_tail0 + f;
+                    const float x = p.alpha * __uint_as_float(r[f]);
+                    if (gn < p.n_main) crow[gn] = p.accumulate ? crow[gn] + x : x;
+                    else if (gn == p.n_main) p.extra[gm] = p.accumulate ? p.extra[gm] + x : x;
+                }
             }
         }
 #pragma unroll 1
         for (int c = 32 * sl.sub; c < BN; c += 32 * sl.n) {
+            if (!keep(c / 32)) {
+                if (c + 32 * sl.n >= BN) release();
+                continue;
+            }
             uint32_t r[32];
             ptx::tmem_ld_32x32b_x32(tbase + c, r);
             ptx::tmem_ld_wait();
@@ -415,16 +541,22 @@ void launch_cfg(const TcParams& p, bool pair, cudaStream_t s) {
 // CTA-pair 256-wide variants with the extra row-sum MMA (xtra) and / or stream-K (sk).
 // Returns false for operand layouts that have no such instantiation.
 template <int BN>
-bool dispatch_ext(const TcParams& p, bool amn, bool bmn, bool cbf16, bool xtra, bool sk, cudaStream_t s) {
+bool dispatch_ext(const TcParams& p, bool amn, bool bmn, bool cbf16, int xtra, bool sk, cudaStream_t s) {
     if (BN == 512 && !sk && !xtra) {  // one-round weight-gradient GEMMs (gemm_wgrad_wide)
         if (!(amn && bmn && !cbf16)) return false;
         launch_pair<GenTraits<512, true, true, false, false, false>>(p, s);
         return true;
     }
-    if (xtra) {
-        if (!(amn && bmn && !cbf16) || sk) return false;
+    if (xtra) {  // 1: ones column, 2: tail columns (p.tx)
+        if (!(amn && bmn && !cbf16)) return false;
         if constexpr (BN == 256) {
-            launch_pair<GenTraits<256, true, true, false, true, false>>(p, s);
+            if (xtra == 2) {
+                if (sk) launch_pair<GenTraits<256, true, true, false, 2, true>>(p, s);
+                else launch_pair<GenTraits<256, true, true, false, 2, false>>(p, s);
+            } else {
+                if (sk) launch_pair<GenTraits<256, true, true, false, 1, true>>(p, s);
+                else launch_pair<GenTraits<256, true, true, false, 1, false>>(p, s);
+            }
             return true;
         }
         return false;
@@ -469,7 +601,7 @@ void dispatch(const TcParams& p, bool amn, bool bmn, bool cbf16, bool pair, cuda
 }
 
 struct PlanKey {
-    const void* a[2]; const void* b[2];
+    const void* a[2]; const void* b[2]; const void* tail;
     int64_t lda[2], ldb[2];
     int K[2], M, N, nseg, bn, mode;
     bool amn, bmn;
@@ -530,9 +662,14 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
     const int npairs = num_sms() / 2;
     const int rounds_plain = (m_tiles * ((g.N + bn0 - 1) / bn0) + npairs - 1) / npairs;
     const int rounds_xtra = (m_tiles * (g.n_main / 256) + npairs - 1) / npairs;
-    const bool xtra = knobs().xtra && g.extra && pair && bn0 == 256 && !g.c_bf16 && amn && bmn && g.n_main == g.N - 1 &&
-                      g.n_main % 256 == 0 && (rounds_xtra < rounds_plain || knobs().force_ext);
-    const int n_eff = xtra ? g.n_main : g.N;
+    // a few columns past the last full 256-wide tile (+ the bias column) from the K-major tail copy
+    const int n_tail0 = g.n_main > 0 ? (g.n_main / 256) * 256 : 0;
+    const bool xb = knobs().xtra && g.b_tail && g.extra && pair && !g.c_bf16 && amn && bmn && g.nseg == 1 &&
+                    g.n_main == g.N - 1 && n_tail0 >= 256 && g.N - n_tail0 <= 8;
+    const bool xtra = xb || (knobs().xtra && g.extra && pair && bn0 == 256 && !g.c_bf16 && amn && bmn && g.n_main == g.N - 1 &&
+                             g.n_main % 256 == 0 && (rounds_xtra < rounds_plain || knobs().force_ext));
+    const int xmode = xb ? 2 : (xtra ? 1 : 0);
+    const int n_eff = xb ? n_tail0 : (xtra ? g.n_main : g.N);
     int kbt = 0;
     for (int i = 0; i < g.nseg; ++i) kbt += (g.seg[i].K + BK - 1) / BK;
     const GemmWorkspace& wsp = gemm_workspace();
@@ -543,17 +680,20 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
     // (two N = 256 MMAs per k-step: a quarter less L2->SM operand traffic per FLOP).
     auto sk_ok = [&](int bnx) {
         const int t = m_tiles * ((n_eff + bnx - 1) / bnx);
-        // weight-gradient layout only for tiny tile counts (e.g. dW_proj: 9 tiles), where the L2
-        // reuse of the lockstep wave order does not matter
-        const bool layout_ok = (!amn && bmn) || (amn && bmn && !g.c_bf16 && bnx == 256 && t * 4 <= npairs);
-        return knobs().streamk && pair && bnx >= 256 && wsp.ws && !xtra && layout_ok && (t % npairs != 0 || knobs().force_ext) &&
+        // weight-gradient layout (both operands MN-major, long K) only when the tiles fill at most
+        // half the pairs (dW_proj: 9 tiles, layer-1 dW_ih: 16): those run one-wave split-K with
+        // every pair of a K slice in lockstep (p.sk_split); stream-K's pairs drift apart along K and
+        // read scattered 512-byte pieces of the MN-major rows (measured slower for dW_out)
+        const bool layout_ok = (!amn && bmn) || (amn && bmn && !g.c_bf16 && bnx == 256 && t * 2 <= npairs);
+        return knobs().streamk && pair && bnx >= 256 && wsp.ws && (!xtra || bnx == 256) && layout_ok &&
+               (t % npairs != 0 || knobs().force_ext) &&
                kbt >= 8 && wsp.floats >= static_cast<size_t>(npairs) * 2 * (bnx / 32 + 1) * 128 * 32 &&
                wsp.flag_count >= static_cast<size_t>(npairs) * 2;
     };
     const bool wide_wgrad = knobs().wide_gemm && amn && bmn && !g.c_bf16 && !g.extra && gemm_wgrad_wide(g.M, g.N);
-    const bool wide = wide_wgrad || (knobs().wide_gemm && bn0 == 256 && g.N >= 1024 && g.N % 512 == 0 &&
+    const bool wide = (!xtra && wide_wgrad) || (!xtra && knobs().wide_gemm && bn0 == 256 && g.N >= 1024 && g.N % 512 == 0 &&
                                      (m_tiles * (g.N / 512) >= npairs || knobs().force_ext) && sk_ok(512));
-    const int bn = wide ? 512 : bn0;
+    const int bn = wide ? 512 : (xb ? 256 : bn0);
     const int tiles = m_tiles * ((n_eff + bn - 1) / bn);
     const bool sk = !wide_wgrad && sk_ok(bn);
 
@@ -565,8 +705,9 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
         key.a[i] = g.seg[i].a.ptr; key.b[i] = g.seg[i].b.ptr;
         key.lda[i] = g.seg[i].a.ld; key.ldb[i] = g.seg[i].b.ld; key.K[i] = g.seg[i].K;
     }
+    key.tail = xb ? g.b_tail : nullptr;
     key.M = g.M; key.N = g.N; key.nseg = g.nseg; key.bn = bn * (pair ? 2 : 1); key.amn = amn; key.bmn = bmn;
-    key.mode = (xtra ? 1 : 0) | (sk ? 2 : 0);
+    key.mode = (xtra ? 1 : 0) | (sk ? 2 : 0) | (xb ? 4 : 0);
 
     TcParams p;
     {
@@ -584,6 +725,10 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
                 if (bmn) make_map(&p.tb[i], sg.b.ptr, g.N, sg.K, sg.b.ld, BK);
                 else make_map(&p.tb[i], sg.b.ptr, sg.K, g.N, sg.b.ld, pair ? (bn > 256 ? 128 : bn / 2) : bn);
                 p.kblocks[i] = (sg.K + BK - 1) / BK;
+            }
+            if (xb) {
+                make_map(&p.tx, g.b_tail, g.seg[0].K, 16, g.ld_tail, 8);
+                p.n_tail0 = n_tail0;
             }
             p.nseg = g.nseg;
             p.M = g.M; p.N = n_eff;
@@ -612,12 +757,22 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
     p.sk_ws = wsp.ws;
     p.sk_flags = wsp.flags;
     p.sk_total = static_cast<int64_t>(tiles) * kbt;
+    // slices of >= 16 k-blocks, at most 4 (the owner adds S - 1 partials on its own)
+    if (sk && amn && bmn && wsp.flag_count >= static_cast<size_t>(2 * npairs + 2 * tiles)) {
+        int S = npairs / tiles;
+        if (S > knobs().split_max) S = knobs().split_max;
+        if (S < 1) S = 1;
+        while (S > 1 && kbt / S < 16) --S;
+        p.sk_split = S;
+    } else {
+        p.sk_split = 0;
+    }
     if (bn == 512) {
-        AB_CHECK(dispatch_ext<512>(p, amn, bmn, g.c_bf16, xtra, sk, s), ADPSGD_E_INVALID_STATE,
+        AB_CHECK(dispatch_ext<512>(p, amn, bmn, g.c_bf16, xmode, sk, s), ADPSGD_E_INVALID_STATE,
                  "gemm_tc: no 512-wide kernel for this layout");
         return;
     }
-    if ((xtra || sk) && dispatch_ext<256>(p, amn, bmn, g.c_bf16, xtra, sk, s)) return;
+    if ((xtra || sk) && dispatch_ext<256>(p, amn, bmn, g.c_bf16, xmode, sk, s)) return;
     AB_CHECK(!xtra, ADPSGD_E_INVALID_STATE, "gemm_tc: no plain kernel for the extra-column layout");
     if (bn == 256) dispatch<256>(p, amn, bmn, g.c_bf16, pair, s);
     else dispatch<128>(p, amn, bmn, g.c_bf16, pair, s);

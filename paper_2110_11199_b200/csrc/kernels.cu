@@ -25,7 +25,7 @@ inline int grid_for(int64_t work, int threads = 256, int per_sm = 8) {
 template <typename AT>
 __global__ void gather_kernel(const float* __restrict__ feats, const int32_t* __restrict__ labels,
                               const int32_t* __restrict__ idx, int B, int T, int I, int ldx, AT* __restrict__ X,
-                              int32_t* __restrict__ lab, int ones_col) {
+                              int32_t* __restrict__ lab, int ones_col, AT* __restrict__ tail, int tail_n0) {
     const int64_t total = static_cast<int64_t>(T) * B * ldx;
     for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -35,6 +35,8 @@ __global__ void gather_kernel(const float* __restrict__ feats, const int32_t* __
         const int64_t n = idx[b];
         const float v = i < I ? feats[(n * T + t) * I + i] : ((ones_col && i == I) ? 1.f : 0.f);
         X[e] = from_f<AT>(v);
+        // K-major copy of columns [tail_n0, tail_n0 + 8) for the tail-column weight-gradient MMA
+        if (tail && i >= tail_n0 && i < tail_n0 + 8) tail[static_cast<int64_t>(i - tail_n0) * T * B + r] = from_f<AT>(v);
         if (i == 0) lab[r] = labels[n * T + t];
     }
 }
@@ -85,6 +87,68 @@ __global__ void cell_bwd_kernel(const float* __restrict__ dH, int lddh, const fl
         dzr[2 * H + j] = from_f<AT>(dc * ig * (1.f - gg * gg));
         dzr[3 * H + j] = from_f<AT>(dh * tc * og * (1.f - og));
         dc_rec[e] = dc * fg;
+    }
+}
+
+// First BPTT cell backward (no recurrent term) of both directions in one launch, 8 units per
+// thread with 16-byte accesses (bf16 gates / dz, fp32 dH / c / c_prev / dc_rec).
+struct CellFirstDir {
+    const float* dH; const bf16* gates; const float* c; const float* c_prev; bf16* dz; float* dc_rec;
+};
+struct CellFirstArgs {
+    CellFirstDir d[2];
+    int lddh, ldg, ldc, lddz, B, H;
+};
+__global__ void cell_bwd_first2_kernel(const __grid_constant__ CellFirstArgs a) {
+    const CellFirstDir& D = a.d[blockIdx.y];
+    const int hv = a.H / 8;
+    const int64_t total = static_cast<int64_t>(a.B) * hv;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int b = static_cast<int>(e / hv), j = static_cast<int>(e % hv) * 8;
+        float dh[8], c[8], cp[8], gi[8], gf[8], gg[8], go[8];
+        const float4* ph = reinterpret_cast<const float4*>(D.dH + static_cast<int64_t>(b) * a.lddh + j);
+        const float4* pc = reinterpret_cast<const float4*>(D.c + static_cast<int64_t>(b) * a.ldc + j);
+        for (int v = 0; v < 2; ++v) {
+            const float4 x = __ldg(ph + v), y = __ldg(pc + v);
+            dh[4 * v] = x.x; dh[4 * v + 1] = x.y; dh[4 * v + 2] = x.z; dh[4 * v + 3] = x.w;
+            c[4 * v] = y.x; c[4 * v + 1] = y.y; c[4 * v + 2] = y.z; c[4 * v + 3] = y.w;
+        }
+        if (D.c_prev) {
+            const float4* pp = reinterpret_cast<const float4*>(D.c_prev + static_cast<int64_t>(b) * a.ldc + j);
+            for (int v = 0; v < 2; ++v) {
+                const float4 z = __ldg(pp + v);
+                cp[4 * v] = z.x; cp[4 * v + 1] = z.y; cp[4 * v + 2] = z.z; cp[4 * v + 3] = z.w;
+            }
+        } else {
+            for (int i = 0; i < 8; ++i) cp[i] = 0.f;
+        }
+        const bf16* gr = D.gates + static_cast<int64_t>(b) * a.ldg + j;
+        float* gsets[4] = {gi, gf, gg, go};
+        for (int q = 0; q < 4; ++q) {
+            const uint4 u = __ldg(reinterpret_cast<const uint4*>(gr + static_cast<int64_t>(q) * a.H));
+            const bf16* ub = reinterpret_cast<const bf16*>(&u);
+            for (int i = 0; i < 8; ++i) gsets[q][i] = __bfloat162float(ub[i]);
+        }
+        bf16 zi[8], zf[8], zg[8], zo[8];
+        float dco[8];
+        for (int i = 0; i < 8; ++i) {
+            const float tc = tanhf(c[i]);
+            const float dc = dh[i] * go[i] * (1.f - tc * tc);
+            zi[i] = __float2bfloat16_rn(dc * gg[i] * gi[i] * (1.f - gi[i]));
+            zf[i] = __float2bfloat16_rn(dc * cp[i] * gf[i] * (1.f - gf[i]));
+            zg[i] = __float2bfloat16_rn(dc * gi[i] * (1.f - gg[i] * gg[i]));
+            zo[i] = __float2bfloat16_rn(dh[i] * tc * go[i] * (1.f - go[i]));
+            dco[i] = dc * gf[i];
+        }
+        bf16* dzr = D.dz + static_cast<int64_t>(b) * a.lddz + j;
+        *reinterpret_cast<uint4*>(dzr) = *reinterpret_cast<const uint4*>(zi);
+        *reinterpret_cast<uint4*>(dzr + a.H) = *reinterpret_cast<const uint4*>(zf);
+        *reinterpret_cast<uint4*>(dzr + 2 * a.H) = *reinterpret_cast<const uint4*>(zg);
+        *reinterpret_cast<uint4*>(dzr + 3 * a.H) = *reinterpret_cast<const uint4*>(zo);
+        float4* pd = reinterpret_cast<float4*>(D.dc_rec + static_cast<int64_t>(b) * a.H + j);
+        pd[0] = make_float4(dco[0], dco[1], dco[2], dco[3]);
+        pd[1] = make_float4(dco[4], dco[5], dco[6], dco[7]);
     }
 }
 
@@ -440,10 +504,10 @@ __global__ void delay_kernel(uint64_t ns) {
 
 template <typename AT>
 void launch_gather(const float* feats, const int32_t* labels, const int32_t* idx, int B, int T, int I, int ldx, AT* X,
-                   int32_t* lab, cudaStream_t s, bool ones_col) {
+                   int32_t* lab, cudaStream_t s, bool ones_col, AT* tail, int tail_n0) {
     ProfScope ps_(s, PROF_GATHER, 0, (double)T * B * ldx * (sizeof(AT) + 4.0) + (double)T * B * 8);
     const int64_t total = static_cast<int64_t>(T) * B * ldx;
-    gather_kernel<AT><<<grid_for(total), 256, 0, s>>>(feats, labels, idx, B, T, I, ldx, X, lab, ones_col ? 1 : 0);
+    gather_kernel<AT><<<grid_for(total), 256, 0, s>>>(feats, labels, idx, B, T, I, ldx, X, lab, ones_col ? 1 : 0, tail, tail_n0);
     count_launch();
 }
 
@@ -621,9 +685,28 @@ void launch_delay(uint64_t ns, cudaStream_t s) {
     count_launch();
 }
 
+bool launch_cell_bwd_first2(const float* const dH[2], const bf16* const gates[2], const float* const c[2],
+                            const float* const c_prev[2], bf16* const dz[2], float* const dc_rec[2], int lddh, int ldg,
+                            int ldc, int lddz, int B, int H, cudaStream_t s) {
+    auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+    bool ok = H % 8 == 0 && lddh % 4 == 0 && ldc % 4 == 0 && ldg % 8 == 0 && lddz % 8 == 0;
+    for (int d = 0; d < 2 && ok; ++d)
+        ok = al(dH[d]) && al(gates[d]) && al(c[d]) && (!c_prev[d] || al(c_prev[d])) && al(dz[d]) && al(dc_rec[d]);
+    if (!ok) return false;
+    CellFirstArgs a;
+    for (int d = 0; d < 2; ++d) a.d[d] = {dH[d], gates[d], c[d], c_prev[d], dz[d], dc_rec[d]};
+    a.lddh = lddh; a.ldg = ldg; a.ldc = ldc; a.lddz = lddz; a.B = B; a.H = H;
+    ProfScope ps_(s, PROF_CELL, 0, 2.0 * B * H * (4 + 8 + 4 + 4 + 8 + 4));
+    const int64_t per = static_cast<int64_t>(B) * (H / 8);
+    const int gx = static_cast<int>((per + 255) / 256 < 1184 ? (per + 255) / 256 : 1184);
+    cell_bwd_first2_kernel<<<dim3(gx, 2), 256, 0, s>>>(a);
+    count_launch();
+    return true;
+}
+
 #define AB_INST(AT)                                                                                                  \
     template void launch_gather<AT>(const float*, const int32_t*, const int32_t*, int, int, int, int, AT*, int32_t*, \
-                                    cudaStream_t, bool);                                                            \
+                                    cudaStream_t, bool, AT*, int);                                                  \
     template void launch_cell_fwd<AT>(const float*, int, const float*, int, AT*, int, float*, AT*, int, int, int, \
                                       cudaStream_t);                                                                \
     template void launch_cell_bwd<AT>(const float*, int, const float*, float*, bool, const AT*, int, const float*, \

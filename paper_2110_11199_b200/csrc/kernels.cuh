@@ -8,7 +8,7 @@ namespace ab {
 // X[(t*B + b)*ldx + i] = feats[idx[b]][t][i] (i < I), 0 for I <= i < ldx; lab[t*B+b] = labels[idx[b]][t]
 template <typename AT>
 void launch_gather(const float* feats, const int32_t* labels, const int32_t* idx, int B, int T, int I, int ldx,
-                   AT* X, int32_t* lab, cudaStream_t s, bool ones_col);
+                   AT* X, int32_t* lab, cudaStream_t s, bool ones_col, AT* tail = nullptr, int tail_n0 = 0);
 
 // LSTM cell forward for one (layer, direction, time step) over B rows (gate order i,f,g,o).
 template <typename AT>
@@ -20,6 +20,12 @@ template <typename AT>
 void launch_cell_bwd(const float* dH, int lddh, const float* dh_rec, float* dc_rec, bool first, const AT* gates,
                      int ldg, const float* c, const float* c_prev, int ldc, AT* dz, int lddz, int B, int H,
                      cudaStream_t s);
+
+// First BPTT cell backward (no recurrent term) of both directions in one vectorised launch;
+// false (nothing launched) when the layout does not allow 16-byte accesses.
+bool launch_cell_bwd_first2(const float* const dH[2], const bf16* const gates[2], const float* const c[2],
+                            const float* const c_prev[2], bf16* const dz[2], float* const dc_rec[2], int lddh, int ldg,
+                            int ldc, int lddz, int B, int H, cudaStream_t s);
 
 // Softmax cross-entropy over rows of fp32 logits: row_loss[r] = lse - logit[label],
 // dlogits = (softmax - onehot) * scale.

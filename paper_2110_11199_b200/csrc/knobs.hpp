@@ -27,7 +27,8 @@ struct Knobs {
     bool force_ext = false;    // ADPSGD_FORCE_EXT=1: take the extra-column / stream-K / wide kernels wherever legal
     int force_bn = 0;          // ADPSGD_FORCE_BN=128|256: generic GEMM tile width (probes)
     int epi_skip = 0;          // ADPSGD_EPI_SKIP=n: epilogue timing experiments
-    int export_dbg = 0;        // ADPSGD_EXPORT_DBG=1|2: split-K export diagnosis
+    int export_dbg = 0;
+    int split_max = 4;         // ADPSGD_SPLIT_MAX=n: K slices of the one-wave split-K weight gradients (1: off)        // ADPSGD_EXPORT_DBG=1|2: split-K export diagnosis
 };
 
 const Knobs& knobs();

@@ -48,6 +48,9 @@ struct TraitsBase {
     static constexpr int EXTRA_COLS = 0;       // extra TMEM columns: row sums of A (all-ones N = 16 MMA) on extra_tile()s
     static constexpr int CLUSTER = 2;          // 4: two CTA pairs per cluster sharing B by TMA multicast (load2_mc)
     static constexpr int TMEM_EXTRA = 0;       // TMEM columns past the accumulators for the epilogue's own state
+    // > 0: the extra N = 16 MMA reads a per-stage K-major B tile of XB_BYTES per CTA loaded by
+    // Traits::load_x (real operand columns past the main tile) instead of the all-ones tile
+    static constexpr int XB_BYTES = 0;
     // STREAMK-style item kernels: the producer lane calls item_ready(p, w, cid, rank) before the
     // first TMA load of every item (cross-CTA dependencies of the A operand).
     template <class P, class W>
@@ -202,13 +205,14 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
 // Traits: BN, B_MN, num_tiles (pair tiles), kblocks, prefetch,
 //         load2(p, tile, kb, rank, sA, sB, bar_cluster_addr), epilogue2(p, tile, rank, tbase, q, lane, tempty_leader)
 // ---------------------------------------------------------------------------
-template <int BN, int EPI = 0, bool OVERLAY = false, int ACC = 2, int EXTRA = 0, int TX = 0>
+template <int BN, int EPI = 0, bool OVERLAY = false, int ACC = 2, int EXTRA = 0, int TX = 0, int XB = 0>
 struct Shape2 {
     static constexpr int BNH = BN / 2;  // B rows held per CTA
     static constexpr int A_BYTES = kBM * kBK * 2;
     static constexpr int B_BYTES = BNH * kBK * 2;
-    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int ONES_BYTES = EXTRA ? 2048 : 0;  // all-ones bf16 B operand of the extra MMA
+    static constexpr int X_BYTES = XB;  // per-stage extra B tile (after the A and B regions)
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES + X_BYTES;
+    static constexpr int ONES_BYTES = (EXTRA && !XB) ? 2048 : 0;  // all-ones bf16 B operand of the extra MMA
     static constexpr int FIT = (kSmemBudget - (OVERLAY ? 0 : EPI) - ONES_BYTES - 2048) / STAGE_BYTES;
     static constexpr int STAGES = FIT > 8 ? 8 : FIT;
     static constexpr int COLS = ACC * BN + EXTRA + TX;
@@ -218,7 +222,7 @@ struct Shape2 {
     static_assert(COLS <= 512, "TMEM has 512 columns");
 };
 template <class T>
-using ShapeOf2 = Shape2<T::BN, T::EPI_SMEM, T::EPI_OVERLAY, T::ACC_STAGES, T::EXTRA_COLS, T::TMEM_EXTRA>;
+using ShapeOf2 = Shape2<T::BN, T::EPI_SMEM, T::EPI_OVERLAY, T::ACC_STAGES, T::EXTRA_COLS, T::TMEM_EXTRA, T::XB_BYTES>;
 
 // One unit of work of a CTA pair: k-blocks [kb0, kb1) of a tile. role: 0 = whole tile,
 // 1 = stream-K owner (holds k-block 0, adds the later segments' partials), 2 = stream-K
@@ -254,6 +258,7 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
     uint8_t* sB = smem + STAGES * S::A_BYTES;
+    uint8_t* sX = sB + STAGES * S::B_BYTES;  // XB_BYTES per stage (1024-aligned when XB_BYTES is)
     // 1 KB barrier block: full[<=8] @0, empty[<=8] @64, tfull[2] @128, tempty[2] @144,
     // TMEM slot @160, per-epilogue-warp barrier pairs[<=16] @256
     uint8_t* bblk = smem + STAGES * S::STAGE_BYTES;
@@ -316,6 +321,7 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
                         Traits::load2_mc(p, w.tile, kb, crank, sA + stage * S::A_BYTES, sB + stage * S::B_BYTES, bar0);
                     else
                         Traits::load2(p, w.tile, kb, rank, sA + stage * S::A_BYTES, sB + stage * S::B_BYTES, bar0);
+                    if constexpr (S::X_BYTES > 0) Traits::load_x(p, w.tile, kb, rank, sX + stage * S::X_BYTES, bar0);
                 }
                 if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 if (!released && (kb + 1 - w.kb0 == STAGES || kb + 1 == w.kb1)) {
@@ -363,9 +369,9 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
                         }
                         if constexpr (Traits::EXTRA_COLS > 0) {
                             // row sums of A: an N = 16 MMA against an all-ones K-major B -> TMEM cols [BN, BN + 16)
+                            const uint32_t xb = S::X_BYTES > 0 ? ptx::smem_u32(sX + stage * S::X_BYTES) : ptx::smem_u32(ones);
                             if (extra)
-                                ptx::mma_bf16_2sm(tmem_d + BN, ad, ptx::umma_desc_sw128(ptx::smem_u32(ones) + kk * 32, 16, 1024),
-                                                  idesc_x, accum);
+                                ptx::mma_bf16_2sm(tmem_d + BN, ad, ptx::umma_desc_sw128(xb + kk * 32, 16, 1024), idesc_x, accum);
                         }
                     }
                     ptx::mma_commit_2sm(&empty[stage], MC ? static_cast<uint16_t>(0xF) : pair_mask);

@@ -115,6 +115,73 @@ def test_extra_column_and_streamk_gemms(oracle_mod, monkeypatch, force):
     assert np.linalg.norm(grad - ograd) / np.linalg.norm(ograd) <= 5e-2
 
 
+def test_tail_column_wgrad_and_streamk_extra(oracle_mod, monkeypatch):
+    """260 input features (the BASELINE shape's input width): the layer-1 dW_ih GEMM takes one
+    256-wide tile per row block and carries features 256..259 plus the bias column on an extra
+    N = 16 MMA fed from a K-major copy of those columns, stream-K over every CTA pair. Must match
+    the oracle (bf16 tolerance) and the plain ragged-tile kernels (ADPSGD_NO_XTRA=1) to fp32
+    summation-order noise."""
+    O = oracle_mod
+    m = ModelDesc(layers=2, hidden=128, bidirectional=True, input_dim=260, proj=256, classes=520, unroll=11)
+    feats, labels = _data(m)
+    M = 256  # 2816 frames: the long-K weight gradients split K in two (one-wave split-K)
+    idx = np.random.default_rng(41).integers(0, 40, size=M).astype(np.int32)
+    w = None
+    out = {}
+    for noxtra in ("0", "1"):
+        monkeypatch.setenv("ADPSGD_NO_XTRA", noxtra)
+        g = LearnerGroup(m, StrategyConfig(learners=1, batch=M, seed=1), precision=Precision.BF16)
+        g.set_dataset(feats, labels, 40)
+        if w is None:
+            w = np.random.default_rng(43).normal(0, 0.1, g.D)
+        out[noxtra] = g.gradient(w, idx)
+        g.close()
+    (l0, g0), (l1, g1) = out["0"], out["1"]
+    assert np.all(np.isfinite(g0))
+    assert abs(l0 - l1) <= 1e-6 * abs(l1)
+    assert np.linalg.norm(g0 - g1) / np.linalg.norm(g1) <= 1e-3
+    oloss, ograd = O.lstm_loss_grad(_odesc(O, m), w, feats, labels, idx)
+    assert abs(l0 - oloss) <= 1e-2 * oloss
+    assert np.linalg.norm(g0 - ograd) / np.linalg.norm(ograd) <= 5e-2
+    # the layer-1 input-weight block and its bias (first direction) on their own
+    H, I = m.hidden, m.input_dim
+    wih = slice(0, 4 * H * I)
+    b = slice(4 * H * I + 4 * H * H, 4 * H * I + 4 * H * H + 4 * H)
+    for sl in (wih, b):
+        assert np.linalg.norm(g0[sl] - g1[sl]) / np.linalg.norm(g1[sl]) <= 1e-3
+
+
+@pytest.mark.parametrize("smax", ["2", "4"])
+def test_split_k_weight_gradients_match_unsplit(monkeypatch, smax):
+    """Few-tile, long-K weight gradients (dW_proj here: 5 tiles, K = 5376 frames) run one-wave
+    split-K: S K-slices per tile on separate CTA pairs, each pair finalising 1/S of the tile's
+    columns from the others' fp32 partials (reduce-scatter, slice-order sums). Must equal the
+    unsplit kernel (ADPSGD_SPLIT_MAX=1) to fp32 summation-order noise, column block by block."""
+    m = ModelDesc(layers=1, hidden=512, bidirectional=True, input_dim=40, proj=256, classes=64, unroll=21)
+    rng = np.random.default_rng(1)
+    feats = rng.normal(size=(300, m.unroll, m.input_dim)).astype(np.float32)
+    labels = rng.integers(0, m.classes, size=(300, m.unroll)).astype(np.int32)
+    idx = rng.integers(0, 300, size=256).astype(np.int32)
+    out = {}
+    w = None
+    for s_ in ("1", smax):
+        monkeypatch.setenv("ADPSGD_SPLIT_MAX", s_)
+        g = LearnerGroup(m, StrategyConfig(learners=1, batch=256, seed=3), precision=Precision.BF16)
+        g.set_dataset(feats, labels, 300)
+        if w is None:
+            w = g.weights(0)
+        out[s_] = g.gradient(w, idx)[1]
+        g.close()
+    H = m.hidden
+    off = 2 * (4 * H * m.input_dim + 4 * H * H + 4 * H)
+    a = out["1"][off:off + 256 * 2 * H].reshape(256, 2 * H)
+    b = out[smax][off:off + 256 * 2 * H].reshape(256, 2 * H)
+    for c in range(0, 2 * H, 32):
+        blk = (slice(None), slice(c, c + 32))
+        assert np.linalg.norm(b[blk] - a[blk]) <= 1e-4 * np.linalg.norm(a[blk]), c
+    assert np.linalg.norm(out[smax] - out["1"]) <= 1e-4 * np.linalg.norm(out["1"])
+
+
 def test_wide_streamk_dgrad_matches_default_kernels(monkeypatch):
     """H = 512: the layer-2 input dgrad (N = 2H = 1024, K = 8H) takes 256 x 512 CTA-pair tiles with
     stream-K under ADPSGD_FORCE_EXT=1; its gradient must agree with the default kernels' (same
