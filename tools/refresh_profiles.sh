@@ -2,7 +2,7 @@
 # Round evidence (1 GPU, under gpurun): launch list of one step, full ncu captures of the top
 # kernels, and a bench line. Output: gpurun_out/<tag>_*. Summarise locally with
 #   python tools/summarize_ncu.py <tag> gpurun_out/<tag>_*.ncu-rep --launches gpurun_out/<tag>_launches.csv
-tag=${1:-r01c}
+tag=${1:-r01g}
 B="python bench.py --steps 1 --warmup 0 --no-cpu-baseline --e2e-steps 1"
 ncu --metrics gpu__time_duration.sum,launch__grid_size --clock-control none -c 700 --csv \
     --log-file gpurun_out/${tag}_launches.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --e2e-steps 1 \
@@ -14,7 +14,8 @@ cap() {  # name regex skip count
 cap fwd "FwdPersistTraits" 2
 cap bwd "BwdPersistTraits" 2
 cap ce "CeTraits" 0 2
-cap wgrad "GenTraits<.int.256, .bool.1, .bool.1, .bool.0, .bool.0, .bool.0, .bool.0>" 2
+cap wgrad "GenTraits<.int.256, .bool.1, .bool.1, .bool.0, .int.0, .bool.0, .bool.0>" 2
+cap wsplit "GenTraits<.int.256, .bool.1, .bool.1, .bool.0, .int.2, .bool.1" 0
 cap dgrad "GenTraits<.int.512" 0
 cap update "sdpsgd_kernel" 0
 cap gather "gather_kernel" 1
