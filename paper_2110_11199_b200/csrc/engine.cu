@@ -68,6 +68,7 @@ Ctx::~Ctx() {
     if (s_main) cudaStreamDestroy(s_main);
     if (h_loss) cudaFreeHost(h_loss);
     if (h_idx) cudaFreeHost(h_idx);
+    if (h_lr) cudaFreeHost(h_lr);
 }
 
 static void validate_config(const adpsgd_config& c) {
@@ -177,6 +178,8 @@ Ctx::Ctx(const adpsgd_config& c) : cfg(c) {
     ws_elems = std::max<int64_t>(int64_t(128) * std::max<int64_t>(nd4H, lay.C), 1 << 20);
     colsum_ws = static_cast<float*>(alloc(ws_elems * sizeof(float)));
     loss_dev = static_cast<float*>(alloc(sizeof(float) * 64));
+    lr_dev = static_cast<float*>(alloc(sizeof(float) * 4));
+    AB_CUDA(cudaMallocHost(&h_lr, sizeof(float) * 4));
     scratch_f = static_cast<float*>(alloc(sizeof(float) * 16));
     // staging for host batches (end-to-end path)
     stage_feats = static_cast<float*>(alloc(static_cast<size_t>(B) * T * I * sizeof(float)));
@@ -254,7 +257,7 @@ static inline void* off_ptr(void* p, int64_t elems, int es) { return static_cast
 // Forward + backward of the BLSTM on the batch already gathered into X0 / lab_step.
 // grad (fp32, flat layout) receives d(mean CE)/dw; loss_slot receives the mean CE.
 void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, float* loss_slot, cudaStream_t s,
-                           bool backward) {
+                           bool backward, const FusedUpd* fu) {
     set_gemm_workspace(gemm_ws);
     const bool bf = bf16_mode;
     WView W{bf ? static_cast<const void*>(ln.shadow) : static_cast<const void*>(master), master, this, &ln};
@@ -392,7 +395,19 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
         if (bf) launch_colsum<bf16>(static_cast<const bf16*>(X), ld, R, N, out, colsum_ws, ws_elems, s);
         else launch_colsum<float>(static_cast<const float*>(X), ld, R, N, out, colsum_ws, ws_elems, s);
     };
-    {   // dW_out = dlogits^T Yin
+    // fused SGD update: the weight-gradient GEMMs write w[nxt] and the shadow instead of the gradient
+    auto upd = [&](GemmArgs& g) {
+        if (!fu) return;
+        const int64_t off = static_cast<float*>(g.C) - grad;
+        g.upd_w = fu->w + off; g.upd_o = fu->o + off; g.upd_sh = fu->sh + off; g.upd_lr = fu->lr;
+        if (g.extra) {
+            const int64_t ox = g.extra - grad;
+            g.upd_xw = fu->w + ox; g.upd_xo = fu->o + ox; g.upd_xsh = fu->sh + ox;
+        }
+    };
+    // order: every GEMM that reads a weight's shadow runs before that weight's gradient GEMM (which,
+    // fused, overwrites the shadow): dY before dW_out, dTop before dW_proj, dX before dW_ih / dW_hh
+    auto dw_out = [&] {  // dW_out = dlogits^T Yin
         GemmArgs g;
         g.M = lay.C; g.N = oi + (fold_bias ? 1 : 0);
         g.seg[0].a = {dlogits, lay.C, true};
@@ -401,11 +416,13 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
         g.C = grad + lay.w_out; g.ldc = oi;
         if (fold_bias) { g.n_main = oi; g.extra = grad + lay.b_out; }  // ones column of Y -> db_out
         g.tag = PROF_GEMM_WGRAD;
+        upd(g);
         gemm(bf, g, s);
-    }
-    if (!fold_bias) colsum(dlogits, lay.C, static_cast<int>(TB), lay.C, grad + lay.b_out);
+        if (!fold_bias) colsum(dlogits, lay.C, static_cast<int>(TB), lay.C, grad + lay.b_out);
+    };
     float* dHcur = dHa;
     float* dHnext = dHb;
+    if (!fu) dw_out();
     if (lay.P > 0) {
         {   // dY = dlogits W_out  (bf16/fp32 activation type: it is a GEMM operand next)
             GemmArgs g;
@@ -417,6 +434,18 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
             g.tag = PROF_GEMM_DGRAD_X;
             gemm(bf, g, s);
         }
+        if (fu) dw_out();
+        auto dtop = [&] {  // dTop = dY W_proj
+            GemmArgs g;
+            g.M = static_cast<int>(TB); g.N = ndH;
+            g.seg[0].a = {dY, lay.P, false};
+            g.seg[0].b = {W.at(lay.w_proj), ndH, true};
+            g.seg[0].K = lay.P;
+            g.C = dHcur; g.ldc = ndH;
+            g.tag = PROF_GEMM_DGRAD_X;
+            gemm(bf, g, s);
+        };
+        if (fu) dtop();
         {   // dW_proj = dY^T top
             GemmArgs g;
             g.M = lay.P; g.N = ndH + (fold_bias ? 1 : 0);
@@ -426,19 +455,11 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
             g.C = grad + lay.w_proj; g.ldc = ndH;
             if (fold_bias) { g.n_main = ndH; g.extra = grad + lay.b_proj; }  // ones column of the top layer -> db_proj
             g.tag = PROF_GEMM_WGRAD;
+            upd(g);
             gemm(bf, g, s);
         }
         if (!fold_bias) colsum(dY, lay.P, static_cast<int>(TB), lay.P, grad + lay.b_proj);
-        {   // dTop = dY W_proj
-            GemmArgs g;
-            g.M = static_cast<int>(TB); g.N = ndH;
-            g.seg[0].a = {dY, lay.P, false};
-            g.seg[0].b = {W.at(lay.w_proj), ndH, true};
-            g.seg[0].K = lay.P;
-            g.C = dHcur; g.ldc = ndH;
-            g.tag = PROF_GEMM_DGRAD_X;
-            gemm(bf, g, s);
-        }
+        if (!fu) dtop();
     } else {
         GemmArgs g;
         g.M = static_cast<int>(TB); g.N = ndH;
@@ -448,6 +469,7 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
         g.C = dHcur; g.ldc = ndH;
         g.tag = PROF_GEMM_DGRAD_X;
         gemm(bf, g, s);
+        if (fu) dw_out();
     }
 
     // ---------------- backward: LSTM layers (BPTT) ----------------
@@ -543,55 +565,63 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
                 }
             }
         }
-        for (int d = 0; d < nd; ++d) {
-            const DirOff& o = lay.dir[l][d];
-            // one-wave 256 x 512 tiles for dW_ih (the bias then by a column sum of dZ) when the
-            // 256-wide tiles plus the ones column would need a second wave (gemm_wgrad_wide)
-            const bool fold_ih = fold_bias && fold_ih_ok && !gemm_wgrad_wide(G4, lay.in_dim[l]);
-            {   // dW_ih = dZ_d^T Xin
-                GemmArgs g;
-                g.M = G4; g.N = lay.in_dim[l] + (fold_ih ? 1 : 0);
-                g.seg[0].a = {off_ptr(dZ, d * G4, es), nd4H, true};
-                g.seg[0].b = {Xin, ldx, true};
-                g.seg[0].K = static_cast<int>(TB);
-                g.C = grad + o.w_ih; g.ldc = lay.in_dim[l];
-                if (fold_ih) { g.n_main = lay.in_dim[l]; g.extra = grad + o.b; }  // ones column of the input -> db
-                if (fold_ih && l == 0 && X0tail) { g.b_tail = X0tail; g.ld_tail = TB; }  // features 256.. + ones column
-                g.tag = PROF_GEMM_WGRAD;
-                gemm(bf, g, s);
-            }
-            if (T > 1) {  // dW_hh = sum_t dz_t^T h_prev(t)
-                GemmArgs g;
-                g.M = G4; g.N = H;
-                const int64_t a_row0 = d == 0 ? B : 0;
-                const int64_t b_row0 = d == 0 ? 0 : B;
-                g.seg[0].a = {off_ptr(dZ, a_row0 * nd4H + d * G4, es), nd4H, true};
-                g.seg[0].b = {off_ptr(Hout[l], b_row0 * ldH + d * H, es), ldH, true};
-                g.seg[0].K = static_cast<int>((T - 1) * static_cast<int64_t>(B));
-                g.C = grad + o.w_hh; g.ldc = H;
-                g.tag = PROF_GEMM_WGRAD;
-                gemm(bf, g, s);
-            } else {
-                AB_CUDA(cudaMemsetAsync(grad + o.w_hh, 0, sizeof(float) * G4 * H, s));
-            }
-            if (!fold_ih) colsum(off_ptr(dZ, d * G4, es), nd4H, static_cast<int>(TB), G4, grad + o.b);
-        }
+        auto dgrad_x = [&] {
         if (l > 0) {  // dXin = sum_d dZ_d W_ih_d
-            GemmArgs g;
-            g.M = static_cast<int>(TB); g.N = Kin;
-            for (int d = 0; d < nd; ++d) {
-                int64_t ldw;
-                const void* wih = W.wih(l, d, &ldw);
-                g.seg[d].a = {off_ptr(dZ, d * G4, es), nd4H, false};
-                g.seg[d].b = {wih, ldw, true};
-                g.seg[d].K = G4;
+                GemmArgs g;
+                g.M = static_cast<int>(TB); g.N = Kin;
+                for (int d = 0; d < nd; ++d) {
+                    int64_t ldw;
+                    const void* wih = W.wih(l, d, &ldw);
+                    g.seg[d].a = {off_ptr(dZ, d * G4, es), nd4H, false};
+                    g.seg[d].b = {wih, ldw, true};
+                    g.seg[d].K = G4;
+                }
+                g.nseg = nd;
+                g.C = dHnext; g.ldc = Kin;
+                g.tag = PROF_GEMM_DGRAD_X;
+                gemm(bf, g, s);
+                std::swap(dHcur, dHnext);
             }
-            g.nseg = nd;
-            g.C = dHnext; g.ldc = Kin;
-            g.tag = PROF_GEMM_DGRAD_X;
-            gemm(bf, g, s);
-            std::swap(dHcur, dHnext);
-        }
+        };
+        auto wgrads = [&] {
+        for (int d = 0; d < nd; ++d) {
+                const DirOff& o = lay.dir[l][d];
+                // one-wave 256 x 512 tiles for dW_ih (the bias then by a column sum of dZ) when the
+                // 256-wide tiles plus the ones column would need a second wave (gemm_wgrad_wide)
+                const bool fold_ih = fold_bias && fold_ih_ok && !gemm_wgrad_wide(G4, lay.in_dim[l]);
+                {   // dW_ih = dZ_d^T Xin
+                    GemmArgs g;
+                    g.M = G4; g.N = lay.in_dim[l] + (fold_ih ? 1 : 0);
+                    g.seg[0].a = {off_ptr(dZ, d * G4, es), nd4H, true};
+                    g.seg[0].b = {Xin, ldx, true};
+                    g.seg[0].K = static_cast<int>(TB);
+                    g.C = grad + o.w_ih; g.ldc = lay.in_dim[l];
+                    if (fold_ih) { g.n_main = lay.in_dim[l]; g.extra = grad + o.b; }  // ones column of the input -> db
+                    if (fold_ih && l == 0 && X0tail) { g.b_tail = X0tail; g.ld_tail = TB; }  // features 256.. + ones column
+                    g.tag = PROF_GEMM_WGRAD;
+                    upd(g);
+                    gemm(bf, g, s);
+                }
+                if (T > 1) {  // dW_hh = sum_t dz_t^T h_prev(t)
+                    GemmArgs g;
+                    g.M = G4; g.N = H;
+                    const int64_t a_row0 = d == 0 ? B : 0;
+                    const int64_t b_row0 = d == 0 ? 0 : B;
+                    g.seg[0].a = {off_ptr(dZ, a_row0 * nd4H + d * G4, es), nd4H, true};
+                    g.seg[0].b = {off_ptr(Hout[l], b_row0 * ldH + d * H, es), ldH, true};
+                    g.seg[0].K = static_cast<int>((T - 1) * static_cast<int64_t>(B));
+                    g.C = grad + o.w_hh; g.ldc = H;
+                    g.tag = PROF_GEMM_WGRAD;
+                    upd(g);
+                    gemm(bf, g, s);
+                } else {
+                    AB_CUDA(cudaMemsetAsync(grad + o.w_hh, 0, sizeof(float) * G4 * H, s));
+                }
+                if (!fold_ih) colsum(off_ptr(dZ, d * G4, es), nd4H, static_cast<int>(TB), G4, grad + o.b);
+            }
+        };
+        // fused update: this layer's W_ih shadow is read by dX before its update (see upd)
+        if (fu) { dgrad_x(); wgrads(); } else { wgrads(); dgrad_x(); }
     }
 }
 
@@ -614,6 +644,18 @@ void Ctx::sample_indices(Learner& ln, int j) {
 // The learner's gradient computation as one replayable unit: batch upload + gather +
 // BLSTM forward/backward. mode 0 = indices from the pinned slot into the device dataset,
 // mode 1 = batch already staged in stage_feats / stage_labels.
+// The update folds into the weight-gradient GEMM epilogues when this context is the only
+// learner (every strategy is SGD, engine.cpp:245-247) and every gradient block comes from a
+// tcgen05 GEMM (bf16 mode, bias gradients folded into the GEMMs, T > 1).
+bool Ctx::fused_update_ok() const {
+    if (!(knobs().fused_update && bf16_mode && cfg.learners == 1 && cfg.local_learners == 1 && !(comm && comm->world > 1)))
+        return false;
+    if (!fold_bias || !fold_ih_ok || T < 2) return false;
+    for (int l = 0; l < lay.L; ++l)
+        if (gemm_wgrad_wide(4 * H, lay.in_dim[l])) return false;  // its bias would come from a column sum
+    return true;
+}
+
 void Ctx::compute_body(int j, int mode, const float* wpt, cudaStream_t s) {
     Learner& ln = learners[j];
     if (mode == 0) {
@@ -623,7 +665,14 @@ void Ctx::compute_body(int j, int mode, const float* wpt, cudaStream_t s) {
     } else {
         gather_batch(stage_feats, stage_labels, ident_idx, s);
     }
-    forward_backward(ln, wpt, ln.g, loss_dev + j, s);
+    if (fuse_now) {
+        const int cur = static_cast<int>(k & 1);
+        FusedUpd fu;
+        fu.w = ln.w[cur]; fu.o = ln.w[cur ^ 1]; fu.sh = ln.shadow; fu.lr = lr_dev;
+        forward_backward(ln, wpt, ln.g, loss_dev + j, s, true, &fu);
+    } else {
+        forward_backward(ln, wpt, ln.g, loss_dev + j, s);
+    }
 }
 
 // Runs compute_body through a CUDA graph keyed by (learner, weight parity, mode, profiling):
@@ -637,7 +686,7 @@ void Ctx::run_compute(int j, int mode, const float* wpt, cudaStream_t s, int par
         compute_body(j, mode, wpt, s);
         return;
     }
-    const int key = ((j * 2 + parity) * 2 + mode) * 2 + (g_prof_enabled ? 1 : 0);
+    const int key = (((j * 2 + parity) * 2 + mode) * 2 + (g_prof_enabled ? 1 : 0)) * 2 + (fuse_now ? 1 : 0);
     auto it = graphs.find(key);
     if (it == graphs.end()) {
         StepGraph sg;
@@ -796,7 +845,9 @@ void Ctx::mix_and_update(double lr_d, const int32_t* taus) {
     if (Lg == 1) strategy = ADPSGD_SDPSGD;  // engine.cpp:245-247
     last_gossip_bytes = 0;
 
-    if (strategy == ADPSGD_SDPSGD) {
+    if (fused_done) {
+        // the weight-gradient GEMMs already wrote w[nxt] = w[cur] - lr g and the shadow
+    } else if (strategy == ADPSGD_SDPSGD) {
         if (comm && comm->world > 1) {
             // gradient allreduce (sum over ranks of the local sums), then the shared update
             const float* gsum = comm->allreduce_sum_grads(*this, s);
@@ -927,6 +978,14 @@ void Ctx::step(double lr, const int32_t* taus, float* loss_out, const float* hos
     cudaStream_t s = s_main;
     if (!injected && !host_feats)
         for (int j = 0; j < cfg.local_learners; ++j) sample_indices(learners[j], j);
+    // single learner: the update happens inside the gradient GEMMs (lr via a device scalar, so
+    // the captured graph serves every step)
+    fuse_now = !injected && fused_update_ok() && !(strategy == ADPSGD_GENERIC && taus && taus[0] > 0);
+    fused_done = false;
+    if (fuse_now) {
+        *h_lr = static_cast<float>(lr);
+        AB_CUDA(cudaMemcpyAsync(lr_dev, h_lr, sizeof(float), cudaMemcpyHostToDevice, s));
+    }
     AB_CUDA(cudaEventRecord(ev0, s));
     // D1D: start the weight allreduce on the comm stream before the gradient compute
     if (strategy == ADPSGD_D1D && comm && comm->world > 1) comm->start_weight_sum(*this, s);
@@ -960,7 +1019,10 @@ void Ctx::step(double lr, const int32_t* taus, float* loss_out, const float* hos
         if (bf16_mode && lagged) refresh_shadow(ln, ln.w[k & 1], s);
     }
     AB_CUDA(cudaEventRecord(ev_mix, s));
+    fused_done = fuse_now;
+    fuse_now = false;
     mix_and_update(lr, taus);
+    fused_done = false;
     AB_CUDA(cudaEventRecord(ev1, s));
     if (!injected && loss_out) {
         AB_CUDA(cudaMemcpyAsync(h_loss, loss_dev, sizeof(float) * cfg.local_learners, cudaMemcpyDeviceToHost, s));

@@ -120,8 +120,21 @@ struct Ctx {
                       int n_epochs, int32_t* ev_learner, double* ev_time);
     std::vector<float*> pubs;  // coupled-async publications, 4 per learner
     void clear_graphs();
+    // Single learner (SGD, engine.cpp:245-247): the weight-gradient GEMM epilogues apply the update
+    // w[nxt] = w[cur] - lr g and refresh the bf16 shadow in place (the gradient is never stored).
+    struct FusedUpd {
+        const float* w = nullptr;  // w[cur] (flat, like the gradient)
+        float* o = nullptr;        // w[nxt]
+        bf16* sh = nullptr;        // the learner's bf16 shadow (updated in place)
+        const float* lr = nullptr; // device scalar
+    };
     void forward_backward(const Learner& ln, const float* master, float* grad, float* loss_slot, cudaStream_t s,
-                          bool backward = true);
+                          bool backward = true, const FusedUpd* fu = nullptr);
+    bool fused_update_ok() const;
+    bool fuse_now = false;      // compute_body: apply the fused update in this compute
+    bool fused_done = false;    // mix_and_update: this step's update already happened
+    float* lr_dev = nullptr;
+    float* h_lr = nullptr;      // pinned
     double evaluate(const double* w, const int32_t* idx, int M, double* g_out);
     void averaged_model(double* out);
     double consensus_distance();

@@ -46,6 +46,16 @@ struct GemmArgs {
     // extra N = 16 MMA of that tile instead of a mostly empty extra n-tile (tcgen05 path only).
     const void* b_tail = nullptr;
     int64_t ld_tail = 0;
+    // Fused SGD update (tcgen05 path, fp32 output, no accumulate): instead of storing the
+    // gradient value x of element (m, n) of C [of extra[m]], store o = upd_w - lr * x to upd_o and
+    // bf16(o) to upd_sh, each laid out exactly like C [like extra]; lr = *upd_lr (device scalar).
+    const float* upd_w = nullptr;
+    float* upd_o = nullptr;
+    bf16* upd_sh = nullptr;
+    const float* upd_xw = nullptr;
+    float* upd_xo = nullptr;
+    bf16* upd_xsh = nullptr;
+    const float* upd_lr = nullptr;
 };
 
 // Stream-K scratch of the calling thread's engine (set before its GEMMs run; see gemm_tc.cu):

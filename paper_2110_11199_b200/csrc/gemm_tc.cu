@@ -51,7 +51,36 @@ struct TcParams {
                                //      c / tiles of tile c % tiles (slice 0 owns the tile)
     CUtensorMap tx;            // XTRA = 2: K-major tail columns [16 rows x K] (B columns n_tail0 + row)
     int n_tail0;
+    // fused SGD update (GemmArgs::upd_*): C / extra element x -> o = w - lr x into o and bf16 shadow
+    const float* upd_w;
+    float* upd_o;
+    bf16* upd_sh;
+    const float* upd_xw;
+    float* upd_xo;
+    bf16* upd_xsh;
+    const float* upd_lr;
 };
+
+// Final store of one fp32 output element (gradient or, fused, the SGD-updated weight + shadow).
+__device__ __forceinline__ void put_c(const TcParams& p, int64_t idx, float x, float lr) {
+    if (p.upd_o) {
+        const float o = p.upd_w[idx] - lr * x;
+        p.upd_o[idx] = o;
+        p.upd_sh[idx] = __float2bfloat16_rn(o);
+    } else {
+        float* C = reinterpret_cast<float*>(p.C);
+        C[idx] = p.accumulate ? C[idx] + x : x;
+    }
+}
+__device__ __forceinline__ void put_x(const TcParams& p, int gm, float x, float lr) {
+    if (p.upd_xo) {
+        const float o = p.upd_xw[gm] - lr * x;
+        p.upd_xo[gm] = o;
+        p.upd_xsh[gm] = __float2bfloat16_rn(o);
+    } else {
+        p.extra[gm] = p.accumulate ? p.extra[gm] + x : x;
+    }
+}
 
 
 // Generic GEMM traits for the persistent skeletons in tc_core.cuh (single CTA and CTA pair).
@@ -363,23 +392,20 @@ struct GenTraits : tc::TraitsBase {
                                 tc::EpiSlot sl, bool xt, Fix fix, Keep keep = Keep()) {
         const int gm = rowbase + lane;
         const bool row_ok = gm < p.M;
+        const float lr = p.upd_lr ? *p.upd_lr : 0.f;
         if (XTRA && xt && sl.sub == 0 && keep(BN / 32)) {
             uint32_t r[32];
             ptx::tmem_ld_32x32b_x16_(tbase + BN, r);
             ptx::tmem_ld_wait();
             fix(BN / 32, r);
-            if (row_ok && XTRA == 1) {
-                const float x = p.alpha * __uint_as_float(r[0]);
-                p.extra[gm] = p.accumulate ? p.extra[gm] + x : x;
-            }
+            if (row_ok && XTRA == 1) put_x(p, gm, p.alpha * __uint_as_float(r[0]), lr);
             if (row_ok && XTRA == 2) {  // tail columns n_tail0 + f: the C row below n_main, extra[] at n_main
-                float* crow = reinterpret_cast<float*>(p.C) + static_cast<int64_t>(gm) * p.ldc;
 #pragma unroll
                 for (int f = 0; f < 16; ++f) {
                     const int gn = p.n_tail0 + f;
                     const float x = p.alpha * __uint_as_float(r[f]);
-                    if (gn < p.n_main) crow[gn] = p.accumulate ? crow[gn] + x : x;
-                    else if (gn == p.n_main) p.extra[gm] = p.accumulate ? p.extra[gm] + x : x;
+                    if (gn < p.n_main) put_c(p, static_cast<int64_t>(gm) * p.ldc + gn, x, lr);
+                    else if (gn == p.n_main) put_x(p, gm, x, lr);
                 }
             }
         }
@@ -399,13 +425,12 @@ struct GenTraits : tc::TraitsBase {
             if (gn0 >= p.N) continue;
             if (!XTRA && p.extra && gn0 + 32 > p.n_main) {
                 // tail chunk containing redirected columns (fp32 output only)
-                float* crow = reinterpret_cast<float*>(p.C) + static_cast<int64_t>(gm) * p.ldc;
                 for (int i = 0; i < 32; ++i) {
                     const int gn = gn0 + i;
                     if (gn >= p.N) break;
                     const float x = p.alpha * __uint_as_float(r[i]) + (p.bias ? p.bias[gn] : 0.f);
-                    if (gn < p.n_main) crow[gn] = p.accumulate ? crow[gn] + x : x;
-                    else if (gn == p.n_main) p.extra[gm] = p.accumulate ? p.extra[gm] + x : x;
+                    if (gn < p.n_main) put_c(p, static_cast<int64_t>(gm) * p.ldc + gn, x, lr);
+                    else if (gn == p.n_main) put_x(p, gm, x, lr);
                 }
                 continue;
             }
@@ -440,6 +465,23 @@ struct GenTraits : tc::TraitsBase {
                         if (p.accumulate) x += __bfloat162float(crow[i]);
                         crow[i] = __float2bfloat16_rn(x);
                     }
+                }
+            } else if (p.upd_o) {  // fused SGD update: w' = w - lr g (+ bf16 shadow), the gradient never stored
+                const int64_t i0 = static_cast<int64_t>(gm) * p.ldc + gn0;
+                if (p.vec_ok && gn0 + 32 <= p.N) {
+#pragma unroll
+                    for (int i = 0; i < 32; i += 4) {
+                        const float4 wv = *reinterpret_cast<const float4*>(p.upd_w + i0 + i);
+                        const float4 o = make_float4(wv.x - lr * v[i], wv.y - lr * v[i + 1], wv.z - lr * v[i + 2],
+                                                     wv.w - lr * v[i + 3]);
+                        *reinterpret_cast<float4*>(p.upd_o + i0 + i) = o;
+                        uint2 sh;
+                        sh.x = tc::pack_bf16x2(o.x, o.y);
+                        sh.y = tc::pack_bf16x2(o.z, o.w);
+                        *reinterpret_cast<uint2*>(p.upd_sh + i0 + i) = sh;
+                    }
+                } else {
+                    for (int i = 0; i < 32 && gn0 + i < p.N; ++i) put_c(p, i0 + i, v[i], lr);
                 }
             } else {
                 float* crow = reinterpret_cast<float*>(p.C) + static_cast<int64_t>(gm) * p.ldc + gn0;
@@ -754,6 +796,15 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
     AB_CHECK(!g.extra || (!g.c_bf16 && g.N == p.n_main + 1), ADPSGD_E_DIMENSION,
              "column redirect: fp32 output, exactly one extra column");
     p.vec_ok = ((reinterpret_cast<uintptr_t>(g.C) & 15) == 0) && ((g.ldc * esz) % 16 == 0);
+    p.upd_w = g.upd_w; p.upd_o = g.upd_o; p.upd_sh = g.upd_sh;
+    p.upd_xw = g.upd_xw; p.upd_xo = g.upd_xo; p.upd_xsh = g.upd_xsh;
+    p.upd_lr = g.upd_lr;
+    if (g.upd_o) {
+        AB_CHECK(!g.c_bf16 && !g.accumulate && g.upd_w && g.upd_sh && g.upd_lr && (!g.extra || (g.upd_xw && g.upd_xo && g.upd_xsh)),
+                 ADPSGD_E_INVALID_STATE, "fused update: fp32 output, no accumulate, complete pointers");
+        p.vec_ok = p.vec_ok && ((reinterpret_cast<uintptr_t>(g.upd_w) & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(g.upd_o) & 15) == 0) && ((reinterpret_cast<uintptr_t>(g.upd_sh) & 7) == 0);
+    }
     p.sk_ws = wsp.ws;
     p.sk_flags = wsp.flags;
     p.sk_total = static_cast<int64_t>(tiles) * kbt;

@@ -23,6 +23,7 @@ struct Knobs {
     bool bwd_kq4 = false;      // ADPSGD_BWD_KQ4=1: persistent BPTT in K quarters
     bool wide_wgrad = false;   // ADPSGD_WIDE_WGRAD=1: one-wave 512-wide weight gradients
     bool mcb = false;          // ADPSGD_MCB=1: B operand TMA-multicast across two CTA pairs
+    bool fused_update = false; // ADPSGD_FUSED_UPDATE=1: single learner's SGD update in the weight-gradient epilogues
     // tests / diagnosis
     bool force_ext = false;    // ADPSGD_FORCE_EXT=1: take the extra-column / stream-K / wide kernels wherever legal
     int force_bn = 0;          // ADPSGD_FORCE_BN=128|256: generic GEMM tile width (probes)
