@@ -305,9 +305,15 @@ def run_ours(a):
     lptr = C.cast(hl.data_ptr(), C.POINTER(C.c_int32))
     loss = (C.c_float * 1)()
     _lib.check(_lib.lib().adpsgd_step_host_batch(g.handle, lr, fptr, lptr, loss))  # warm
+    # data-loader pattern: step k's batch was prefetched (H2D on the copy stream) while step k-1
+    # computed; every timed step still moves its whole batch host -> device inside the region
+    pf = _lib.lib().adpsgd_prefetch_host_batch
     barrier()
     t0 = time.perf_counter()
-    for _ in range(e2e_steps):
+    _lib.check(pf(g.handle, fptr, lptr))
+    for i in range(e2e_steps):
+        if i + 1 < e2e_steps:
+            _lib.check(pf(g.handle, fptr, lptr))
         _lib.check(_lib.lib().adpsgd_step_host_batch(g.handle, lr, fptr, lptr, loss))
     e2e_s = P.max_over_ranks(time.perf_counter() - t0)
     barrier()
@@ -359,7 +365,8 @@ def run_ours(a):
                    "l2": "per-step working set (~12 GB) >> 126 MB L2; no flush needed",
                    "train_flops_per_frame": m.train_flops_per_frame()},
         "e2e": {"value": e2e_val, "unit": "frames/s", "h2d_bytes_per_step": nf * 4 + a.batch * T_UNROLL * 4,
-                "d2h_bytes_per_step": 4, "steps": e2e_steps},
+                "d2h_bytes_per_step": 4, "steps": e2e_steps,
+                "h2d": "pinned host batch, prefetched one step ahead on a copy stream (adpsgd_prefetch_host_batch)"},
         "roofline": {"bound": "tensor",
                      "kernel": "persistent_kernel_2cta<FwdPersistTraits>: one launch per layer = 21 steps x 2 "
                                "directions of the fused recurrent GEMM [x_t|h_t-1][W_ih|W_hh]^T + LSTM cell, "

@@ -122,6 +122,11 @@ int adpsgd_step(adpsgd_ctx* ctx, double lr, const int32_t* taus, float* loss_out
  * labels [local][M][T]; copied H2D inside (the end-to-end path). */
 int adpsgd_step_host_batch(adpsgd_ctx* ctx, double lr, const float* feats, const int32_t* labels,
                            float* loss_out);
+/* Data-loader prefetch for the host-batch step (one local learner per context): queue the H2D
+ * copy of a batch on a copy stream so it overlaps the current step; the next
+ * adpsgd_step_host_batch with the same two pointers uses it instead of copying. At most two
+ * batches in flight; the caller keeps the host memory unchanged until that step. */
+int adpsgd_prefetch_host_batch(adpsgd_ctx* ctx, const float* feats, const int32_t* labels);
 /* Gradient-injection step: grads [local_learners][D] fp64 replace the LSTM gradient. */
 int adpsgd_step_injected(adpsgd_ctx* ctx, double lr, const int32_t* taus, const double* grads);
 /* Objective::gradient adapter (objectives.hpp:50-51): loss and gradient at w over the
@@ -179,6 +184,10 @@ int adpsgd_profile_read(double* ms, double* flops, double* bytes, int64_t* launc
 
 /* Debug: device timeline of the CTA-pair tensor-core kernels (160 CTAs x 32 globaltimer stamps). */
 int adpsgd_debug_trace(int32_t enable, uint64_t* out, int32_t n);
+/* Diagnosis: copy an internal activation buffer of learner 0 to host (which: 0 = X0, 1 + l = layer
+ * l output H, 100 = Y, 101 = row_loss, 102 = bf16 shadow, 200 + l = layer l cell state c,
+ * 300 + l = layer l gates); bytes clipped to the buffer. */
+int adpsgd_debug_buffer(adpsgd_ctx* ctx, int32_t which, void* out, size_t bytes);
 
 /* ---- kernel-level entry points (tests / benchmarks; device pointers) ---- */
 /* C[M,N] = alpha * sum_k A(m,k) B(n,k) (+ C if accumulate) (+ bias[n]).

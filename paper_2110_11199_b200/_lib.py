@@ -52,6 +52,8 @@ _SIGS = {
     "adpsgd_get_weights": (C.c_int, [C.c_void_p, i32, P(C.c_double), i64]),
     "adpsgd_step": (C.c_int, [C.c_void_p, C.c_double, P(i32), P(C.c_float)]),
     "adpsgd_step_host_batch": (C.c_int, [C.c_void_p, C.c_double, P(C.c_float), P(i32), P(C.c_float)]),
+    "adpsgd_prefetch_host_batch": (C.c_int, [C.c_void_p, P(C.c_float), P(i32)]),
+    "adpsgd_debug_buffer": (C.c_int, [C.c_void_p, i32, C.c_void_p, C.c_size_t]),
     "adpsgd_step_injected": (C.c_int, [C.c_void_p, C.c_double, P(i32), P(C.c_double)]),
     "adpsgd_gradient": (C.c_int, [C.c_void_p, P(C.c_double), P(i32), i32, P(C.c_double), P(C.c_double)]),
     "adpsgd_set_straggler": (C.c_int, [C.c_void_p, i32, C.c_double]),

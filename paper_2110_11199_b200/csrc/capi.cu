@@ -117,8 +117,9 @@ int adpsgd_set_dataset(adpsgd_ctx* ctx, const float* feats, const int32_t* label
             c.labels = static_cast<int32_t*>(c.alloc(static_cast<size_t>(n_seg) * c.T * sizeof(int32_t)));
         }
         c.clear_graphs();
-        AB_CUDA(cudaMemcpy(c.feats, feats, nf * sizeof(float), cudaMemcpyHostToDevice));
-        AB_CUDA(cudaMemcpy(c.labels, labels, static_cast<size_t>(n_seg) * c.T * sizeof(int32_t), cudaMemcpyHostToDevice));
+        AB_CUDA(cudaStreamSynchronize(c.s_main));  // no step still reading the old dataset
+        c.h2d_sync(c.feats, feats, nf * sizeof(float));
+        c.h2d_sync(c.labels, labels, static_cast<size_t>(n_seg) * c.T * sizeof(int32_t));
         c.n_seg = n_seg;
         c.train_count = train_count;
     });
@@ -146,8 +147,9 @@ int adpsgd_get_dataset(adpsgd_ctx* ctx, float* feats, int32_t* labels) {
     return guard([&] {
         Ctx& c = C_(ctx);
         AB_CHECK(c.feats, ADPSGD_E_INVALID_STATE, "no dataset");
-        AB_CUDA(cudaMemcpy(feats, c.feats, static_cast<size_t>(c.n_seg) * c.T * c.I * sizeof(float), cudaMemcpyDeviceToHost));
-        AB_CUDA(cudaMemcpy(labels, c.labels, static_cast<size_t>(c.n_seg) * c.T * sizeof(int32_t), cudaMemcpyDeviceToHost));
+        AB_CUDA(cudaMemcpyAsync(feats, c.feats, static_cast<size_t>(c.n_seg) * c.T * c.I * sizeof(float), cudaMemcpyDeviceToHost, c.s_main));
+        AB_CUDA(cudaMemcpyAsync(labels, c.labels, static_cast<size_t>(c.n_seg) * c.T * sizeof(int32_t), cudaMemcpyDeviceToHost, c.s_main));
+        AB_CUDA(cudaStreamSynchronize(c.s_main));
     });
 }
 
@@ -160,7 +162,8 @@ int adpsgd_set_weights(adpsgd_ctx* ctx, int32_t j, const double* w, int64_t n) {
         std::vector<float> f(w, w + n);
         Learner& ln = c.learners[j];
         const int cur = static_cast<int>(c.k & 1);
-        AB_CUDA(cudaMemcpy(ln.w[cur], f.data(), n * sizeof(float), cudaMemcpyHostToDevice));
+        AB_CUDA(cudaStreamSynchronize(c.s_main));
+        c.h2d_sync(ln.w[cur], f.data(), n * sizeof(float));
         c.refresh_shadow(ln, ln.w[cur], c.s_main);
         AB_CUDA(cudaStreamSynchronize(c.s_main));
     });
@@ -173,8 +176,8 @@ int adpsgd_get_weights(adpsgd_ctx* ctx, int32_t j, double* w, int64_t n) {
         AB_CHECK(n == c.D, ADPSGD_E_DIMENSION, "weight vector length != parameter count");
         AB_CUDA(cudaSetDevice(c.cfg.device));
         std::vector<float> f(n);
+        AB_CUDA(cudaMemcpyAsync(f.data(), c.learners[j].w[c.k & 1], n * sizeof(float), cudaMemcpyDeviceToHost, c.s_main));
         AB_CUDA(cudaStreamSynchronize(c.s_main));
-        AB_CUDA(cudaMemcpy(f.data(), c.learners[j].w[c.k & 1], n * sizeof(float), cudaMemcpyDeviceToHost));
         for (int64_t i = 0; i < n; ++i) w[i] = f[i];
     });
 }
@@ -188,6 +191,10 @@ int adpsgd_step_host_batch(adpsgd_ctx* ctx, double lr, const float* feats, const
         AB_CHECK(feats && labels, ADPSGD_E_INVALID_STATE, "null host batch");
         C_(ctx).step(lr, nullptr, loss_out, feats, labels, nullptr);
     });
+}
+
+int adpsgd_prefetch_host_batch(adpsgd_ctx* ctx, const float* feats, const int32_t* labels) {
+    return guard([&] { C_(ctx).prefetch_host_batch(feats, labels); });
 }
 
 int adpsgd_step_injected(adpsgd_ctx* ctx, double lr, const int32_t* taus, const double* grads) {
@@ -325,6 +332,27 @@ int adpsgd_profile_read(double* ms, double* flops, double* bytes, int64_t* launc
 namespace ab { void trace_enable(int); void trace_read(unsigned long long*, int); }
 extern "C" {
 // Debug: device timeline of the CTA-pair tcgen05 kernels (160 CTAs x 32 globaltimer stamps).
+int adpsgd_debug_buffer(adpsgd_ctx* ctx, int32_t which, void* out, size_t bytes) {
+    return guard([&] {
+        ab::Ctx& c = C_(ctx);
+        AB_CUDA(cudaSetDevice(c.cfg.device));
+        AB_CUDA(cudaStreamSynchronize(c.s_main));
+        const void* src = nullptr;
+        size_t n = 0;
+        const size_t TB = static_cast<size_t>(c.TB);
+        if (which == 0) { src = c.X0; n = TB * c.Ipad * c.es; }
+        else if (which >= 1 && which <= c.lay.L) { src = c.Hout[which - 1]; n = TB * c.ldH * c.es; }
+        else if (which == 100) { src = c.Y; n = TB * c.ldY * c.es; }
+        else if (which == 101) { src = c.row_loss; n = TB * sizeof(float); }
+        else if (which == 102) { src = c.learners[0].shadow; n = static_cast<size_t>(c.D) * 2; }
+        else if (which >= 200 && which < 200 + c.lay.L) { src = c.cst[which - 200]; n = TB * c.ndH * sizeof(float); }
+        else if (which >= 300 && which < 300 + c.lay.L) { src = c.gates[which - 300]; n = TB * c.nd4H * c.es; }
+        AB_CHECK(src != nullptr, ADPSGD_E_INVALID_STATE, "debug_buffer: no such buffer");
+        AB_CUDA(cudaMemcpyAsync(out, src, bytes < n ? bytes : n, cudaMemcpyDeviceToHost, c.s_main));
+        AB_CUDA(cudaStreamSynchronize(c.s_main));
+    });
+}
+
 int adpsgd_debug_trace(int32_t enable, uint64_t* out, int32_t n) {
     return guard([&] {
         if (out) ab::trace_read(reinterpret_cast<unsigned long long*>(out), n);

@@ -80,7 +80,8 @@ Comm::Comm(Ctx& c, int r, int w, const void* id128) : rank(r), world(w), D_(c.D)
     wsum_ = static_cast<float*>(c.alloc(c.D * sizeof(float)));
     gsum_ = static_cast<float*>(c.alloc(c.D * sizeof(float)));
     bar_ = static_cast<float*>(c.alloc(sizeof(float) * 4));
-    AB_CUDA(cudaMemset(bar_, 0, sizeof(float) * 4));
+    AB_CUDA(cudaMemsetAsync(bar_, 0, sizeof(float) * 4, c.s_main));
+    AB_CUDA(cudaStreamSynchronize(c.s_main));
     AB_CUDA(cudaEventCreateWithFlags(&ev_start_, cudaEventDisableTiming));
     AB_CUDA(cudaEventCreateWithFlags(&ev_ws_, cudaEventDisableTiming));
 }

@@ -46,6 +46,14 @@ const char* last_error() { return g_last_error.c_str(); }
 // ---------------------------------------------------------------------------
 // Device memory arena (one cudaMalloc per buffer; freed at ctx destroy).
 // ---------------------------------------------------------------------------
+// Host -> device copy ordered on s_main and complete on return. (A plain cudaMemcpy from pageable
+// memory runs on the legacy stream, which the non-blocking s_main does not wait for, and may
+// return before its DMA has landed: kernels on s_main could read the previous contents.)
+void Ctx::h2d_sync(void* dst, const void* src, size_t bytes) {
+    AB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s_main));
+    AB_CUDA(cudaStreamSynchronize(s_main));
+}
+
 void* Ctx::alloc(size_t bytes) {
     void* p = nullptr;
     AB_CUDA(cudaMalloc(&p, round_up(bytes ? bytes : 16, 256)));
@@ -59,6 +67,9 @@ Ctx::~Ctx() {
     comm.reset();
     clear_graphs();
     for (void* p : allocations) cudaFree(p);
+    for (auto& e : ev_stage)
+        if (e) cudaEventDestroy(e);
+    if (s_copy) cudaStreamDestroy(s_copy);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (ev_mix) cudaEventDestroy(ev_mix);
@@ -114,6 +125,8 @@ Ctx::Ctx(const adpsgd_config& c) : cfg(c) {
     AB_CUDA(cudaSetDevice(c.device));
     AB_CUDA(cudaStreamCreateWithFlags(&s_main, cudaStreamNonBlocking));
     AB_CUDA(cudaStreamCreateWithFlags(&s_comm, cudaStreamNonBlocking));
+    AB_CUDA(cudaStreamCreateWithFlags(&s_copy, cudaStreamNonBlocking));
+    for (auto& e : ev_stage) AB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     AB_CUDA(cudaEventCreate(&ev0));
     AB_CUDA(cudaEventCreate(&ev1));
     AB_CUDA(cudaEventCreate(&ev_mix));
@@ -127,7 +140,7 @@ Ctx::Ctx(const adpsgd_config& c) : cfg(c) {
     X0 = alloc(TB * Ipad * es);
     if (bf16_mode && Ipad > 256 && Ipad <= 264) {
         X0tail = alloc(16 * TB * sizeof(bf16));
-        AB_CUDA(cudaMemset(X0tail, 0, 16 * TB * sizeof(bf16)));
+        AB_CUDA(cudaMemsetAsync(X0tail, 0, 16 * TB * sizeof(bf16), s_main));
     }
     lab_step = static_cast<int32_t*>(alloc(sizeof(int32_t) * TB));
     for (int l = 0; l < lay.L; ++l) {
@@ -163,9 +176,8 @@ Ctx::Ctx(const adpsgd_config& c) : cfg(c) {
             pb_sync = static_cast<unsigned int*>(alloc(520 * sizeof(unsigned int)));
             AB_CUDA(cudaMemsetAsync(pb_sync, 0, 520 * sizeof(unsigned int), s_main));  // [384,512) fwd step counters, [513] fwd exit
         }
-    } else {
-        logits = static_cast<float*>(alloc(TB * lay.C * sizeof(float)));
     }
+    if (!bf16_mode || knobs().unfused_ce) logits = static_cast<float*>(alloc(TB * lay.C * sizeof(float)));
     dlogits = alloc(TB * lay.C * es);
     row_loss = static_cast<float*>(alloc(TB * sizeof(float)));
     int max_in = std::max(lay.top, Ipad);
@@ -184,11 +196,13 @@ Ctx::Ctx(const adpsgd_config& c) : cfg(c) {
     // staging for host batches (end-to-end path)
     stage_feats = static_cast<float*>(alloc(static_cast<size_t>(B) * T * I * sizeof(float)));
     stage_labels = static_cast<int32_t*>(alloc(static_cast<size_t>(B) * T * sizeof(int32_t)));
+    stage_feats2 = static_cast<float*>(alloc(static_cast<size_t>(B) * T * I * sizeof(float)));
+    stage_labels2 = static_cast<int32_t*>(alloc(static_cast<size_t>(B) * T * sizeof(int32_t)));
     ident_idx = static_cast<int32_t*>(alloc(sizeof(int32_t) * B));
     {
         std::vector<int32_t> id(B);
         for (int b = 0; b < B; ++b) id[b] = b;
-        AB_CUDA(cudaMemcpy(ident_idx, id.data(), sizeof(int32_t) * B, cudaMemcpyHostToDevice));
+        h2d_sync(ident_idx, id.data(), sizeof(int32_t) * B);
     }
 
     // ---- learners: w0 shared by all (engine.cpp:101-103), streams 0xB000 + global id ----
@@ -210,7 +224,7 @@ Ctx::Ctx(const adpsgd_config& c) : cfg(c) {
                 ln.l1pad.push_back(static_cast<bf16*>(alloc(static_cast<size_t>(4) * H * Ipad * sizeof(bf16))));
         }
         for (int h = 1; h < history_depth; ++h) ln.hist.push_back(static_cast<float*>(alloc(D * sizeof(float))));
-        AB_CUDA(cudaMemcpy(ln.w[0], w0f.data(), D * sizeof(float), cudaMemcpyHostToDevice));
+        h2d_sync(ln.w[0], w0f.data(), D * sizeof(float));
         learners.push_back(std::move(ln));
     }
     for (auto& ln : learners) {
@@ -361,7 +375,7 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
         yin = Y;
     }
     const float scale = 1.0f / static_cast<float>(TB);
-    if (bf) {
+    if (bf && !knobs().unfused_ce) {
         // output GEMM fused with softmax-CE: no logits in HBM (gemm_ce.cu)
         CeArgs a;
         a.Y = static_cast<const bf16*>(yin);
@@ -384,8 +398,12 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
         g.bias = master + lay.b_out;
         g.tag = PROF_GEMM_OUT;
         gemm(bf, g, s);
-        launch_softmax_ce<float>(logits, lab_step, static_cast<int>(TB), lay.C, scale, static_cast<float*>(dlogits),
-                                 row_loss, s);
+        if (bf)
+            launch_softmax_ce<bf16>(logits, lab_step, static_cast<int>(TB), lay.C, scale, static_cast<bf16*>(dlogits),
+                                    row_loss, s);
+        else
+            launch_softmax_ce<float>(logits, lab_step, static_cast<int>(TB), lay.C, scale, static_cast<float*>(dlogits),
+                                     row_loss, s);
     }
     launch_sum(row_loss, static_cast<int>(TB), scale, loss_slot, s);
     if (!backward) return;
@@ -641,9 +659,6 @@ void Ctx::sample_indices(Learner& ln, int j) {
     for (int b = 0; b < B; ++b) hb[b] = static_cast<int32_t>(ln.rng.next_below(static_cast<uint64_t>(train_count)));
 }
 
-// The learner's gradient computation as one replayable unit: batch upload + gather +
-// BLSTM forward/backward. mode 0 = indices from the pinned slot into the device dataset,
-// mode 1 = batch already staged in stage_feats / stage_labels.
 // The update folds into the weight-gradient GEMM epilogues when this context is the only
 // learner (every strategy is SGD, engine.cpp:245-247) and every gradient block comes from a
 // tcgen05 GEMM (bf16 mode, bias gradients folded into the GEMMs, T > 1).
@@ -656,14 +671,36 @@ bool Ctx::fused_update_ok() const {
     return true;
 }
 
+// Queue the H2D copy of a host batch (layout of step_host_batch, one local learner) on the copy
+// stream; the next step_host_batch with the same pointers waits on it instead of copying. The
+// caller keeps the host memory unchanged until that step (pinned memory makes the copy async).
+void Ctx::prefetch_host_batch(const float* f, const int32_t* l) {
+    AB_CHECK(f && l, ADPSGD_E_INVALID_STATE, "null host batch");
+    AB_CHECK(cfg.local_learners == 1, ADPSGD_E_CONFIG, "host-batch prefetch needs one local learner per context");
+    AB_CHECK(prefetched.size() < 2, ADPSGD_E_INVALID_STATE, "at most two prefetched host batches in flight");
+    AB_CUDA(cudaSetDevice(cfg.device));
+    const int slot = next_slot;
+    next_slot ^= 1;
+    const size_t nf = static_cast<size_t>(B) * T * I;
+    AB_CUDA(cudaMemcpyAsync(slot ? stage_feats2 : stage_feats, f, nf * sizeof(float), cudaMemcpyHostToDevice, s_copy));
+    AB_CUDA(cudaMemcpyAsync(slot ? stage_labels2 : stage_labels, l, sizeof(int32_t) * B * T, cudaMemcpyHostToDevice, s_copy));
+    AB_CUDA(cudaEventRecord(ev_stage[slot], s_copy));
+    prefetched.push_back({f, l, slot});
+}
+
+// The learner's gradient computation as one replayable unit: batch upload + gather +
+// BLSTM forward/backward. mode 0 = indices from the pinned slot into the device dataset,
+// mode 1 / 2 = batch already staged in staging slot 0 / 1.
 void Ctx::compute_body(int j, int mode, const float* wpt, cudaStream_t s) {
     Learner& ln = learners[j];
     if (mode == 0) {
         AB_CUDA(cudaMemcpyAsync(idx_dev, h_idx + static_cast<int64_t>(j) * B, sizeof(int32_t) * B,
                                 cudaMemcpyHostToDevice, s));
         gather_batch(feats, labels, idx_dev, s);
-    } else {
+    } else if (mode == 1) {
         gather_batch(stage_feats, stage_labels, ident_idx, s);
+    } else {
+        gather_batch(stage_feats2, stage_labels2, ident_idx, s);
     }
     if (fuse_now) {
         const int cur = static_cast<int>(k & 1);
@@ -686,7 +723,7 @@ void Ctx::run_compute(int j, int mode, const float* wpt, cudaStream_t s, int par
         compute_body(j, mode, wpt, s);
         return;
     }
-    const int key = (((j * 2 + parity) * 2 + mode) * 2 + (g_prof_enabled ? 1 : 0)) * 2 + (fuse_now ? 1 : 0);
+    const int key = (((j * 2 + parity) * 3 + mode) * 2 + (g_prof_enabled ? 1 : 0)) * 2 + (fuse_now ? 1 : 0);
     auto it = graphs.find(key);
     if (it == graphs.end()) {
         StepGraph sg;
@@ -998,7 +1035,18 @@ void Ctx::step(double lr, const int32_t* taus, float* loss_out, const float* hos
             continue;
         }
         int mode = 0;
-        if (host_feats) {
+        if (host_feats && !prefetched.empty() && cfg.local_learners == 1 && prefetched.front().f == host_feats &&
+            prefetched.front().l == host_labels) {
+            // staged by prefetch_host_batch while the previous step ran
+            const int slot = prefetched.front().slot;
+            prefetched.pop_front();
+            AB_CUDA(cudaStreamWaitEvent(s, ev_stage[slot], 0));
+            mode = 1 + slot;
+        } else if (host_feats) {
+            if (!prefetched.empty()) {  // a different batch than the one prefetched: drop the prefetches
+                AB_CUDA(cudaStreamSynchronize(s_copy));
+                prefetched.clear();
+            }
             const size_t nf = static_cast<size_t>(B) * T * I;
             AB_CUDA(cudaMemcpyAsync(stage_feats, host_feats + j * nf, nf * sizeof(float), cudaMemcpyHostToDevice, s));
             AB_CUDA(cudaMemcpyAsync(stage_labels, host_labels + static_cast<size_t>(j) * B * T,
@@ -1106,7 +1154,8 @@ void Ctx::averaged_model(double* out) {
     std::vector<float> f(D);
     std::fill(out, out + D, 0.0);
     for (auto& ln : learners) {
-        AB_CUDA(cudaMemcpy(f.data(), ln.w[k & 1], D * sizeof(float), cudaMemcpyDeviceToHost));
+        AB_CUDA(cudaMemcpyAsync(f.data(), ln.w[k & 1], D * sizeof(float), cudaMemcpyDeviceToHost, s_main));
+        AB_CUDA(cudaStreamSynchronize(s_main));
         for (int64_t i = 0; i < D; ++i) out[i] += f[i];
     }
     for (int64_t i = 0; i < D; ++i) out[i] /= static_cast<double>(learners.size());

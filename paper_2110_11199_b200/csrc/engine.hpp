@@ -5,6 +5,7 @@
 
 #include <cuda_runtime.h>
 
+#include <deque>
 #include <map>
 #include <memory>
 #include <string>
@@ -91,6 +92,20 @@ struct Ctx {
     void* scratch_grad = nullptr;
     float* stage_feats = nullptr;
     int32_t* stage_labels = nullptr;
+    // host-batch prefetch (one local learner): two staging slots filled on s_copy while the
+    // previous step computes; step_host_batch consumes the oldest slot whose pointers match
+    float* stage_feats2 = nullptr;
+    int32_t* stage_labels2 = nullptr;
+    cudaStream_t s_copy = nullptr;
+    cudaEvent_t ev_stage[2] = {nullptr, nullptr};
+    struct Prefetch {
+        const float* f;
+        const int32_t* l;
+        int slot;
+    };
+    std::deque<Prefetch> prefetched;
+    int next_slot = 0;
+    void prefetch_host_batch(const float* f, const int32_t* l);
     float* h_loss = nullptr;
     int32_t* h_idx = nullptr;  // pinned sampling slots, B per local learner
 
@@ -109,6 +124,7 @@ struct Ctx {
     std::vector<void*> allocations;
 
     void* alloc(size_t bytes);
+    void h2d_sync(void* dst, const void* src, size_t bytes);
     void* alloc_scratch_grad();
     void refresh_shadow(Learner& ln, const float* w, cudaStream_t s);
     void refresh_pad(Learner& ln, const float* w, cudaStream_t s);

@@ -9,6 +9,7 @@
 // LSTM's dgrad / wgrad contractions run without explicit transposes.
 #include <cuda.h>
 
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -738,6 +739,9 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
     const int bn = wide ? 512 : (xb ? 256 : bn0);
     const int tiles = m_tiles * ((n_eff + bn - 1) / bn);
     const bool sk = !wide_wgrad && sk_ok(bn);
+    if (std::getenv("ADPSGD_LOG_GEMM"))
+        std::fprintf(stderr, "gemm M=%d N=%d K=%d nseg=%d amn=%d bmn=%d cbf16=%d pair=%d bn=%d xtra=%d xb=%d sk=%d tag=%d\n", g.M,
+                     g.N, g.seg[0].K, g.nseg, amn, bmn, g.c_bf16, pair, bn, xtra, xb, sk, g.tag);
 
     static std::unordered_map<PlanKey, TcParams, PlanHash> cache;
     static std::mutex mu;
@@ -754,7 +758,8 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
     TcParams p;
     {
         std::lock_guard<std::mutex> lk(mu);
-        auto it = cache.find(key);
+        static const bool no_cache = std::getenv("ADPSGD_NO_PLAN_CACHE") != nullptr;  // diagnosis
+        auto it = no_cache ? cache.end() : cache.find(key);
         if (it != cache.end()) {
             p = it->second;
         } else {

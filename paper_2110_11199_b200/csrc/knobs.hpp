@@ -29,7 +29,8 @@ struct Knobs {
     int force_bn = 0;          // ADPSGD_FORCE_BN=128|256: generic GEMM tile width (probes)
     int epi_skip = 0;          // ADPSGD_EPI_SKIP=n: epilogue timing experiments
     int export_dbg = 0;
-    int split_max = 4;         // ADPSGD_SPLIT_MAX=n: K slices of the one-wave split-K weight gradients (1: off)        // ADPSGD_EXPORT_DBG=1|2: split-K export diagnosis
+    int split_max = 4;
+    bool unfused_ce = false;   // ADPSGD_UNFUSED_CE=1: bf16 logits GEMM (fp32 out) + softmax-CE kernel (diagnosis)         // ADPSGD_SPLIT_MAX=n: K slices of the one-wave split-K weight gradients (1: off)        // ADPSGD_EXPORT_DBG=1|2: split-K export diagnosis
 };
 
 const Knobs& knobs();

@@ -21,6 +21,7 @@ void trace_enable(int on) {
     if (on && !g_trace_buf) {
         AB_CUDA(cudaMalloc(&g_trace_buf, sizeof(unsigned long long) * 160 * 48));
         AB_CUDA(cudaMemset(g_trace_buf, 0, sizeof(unsigned long long) * 160 * 48));
+        AB_CUDA(cudaDeviceSynchronize());  // legacy-stream memset vs the engine's non-blocking streams
     }
     if (!on && g_trace_buf) {
         AB_CUDA(cudaDeviceSynchronize());
@@ -33,6 +34,7 @@ void trace_read(unsigned long long* out, int n) {
     if (!g_trace_buf) return;
     AB_CUDA(cudaMemcpy(out, g_trace_buf, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost));
     AB_CUDA(cudaMemset(g_trace_buf, 0, sizeof(unsigned long long) * 160 * 48));
+    AB_CUDA(cudaDeviceSynchronize());
 }
 
 bool g_prof_enabled = false;

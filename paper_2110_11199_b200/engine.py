@@ -250,7 +250,19 @@ class LearnerGroup:
         loss = np.zeros(self.local, dtype=np.float32)
         _lib.check(_lib.lib().adpsgd_step_host_batch(self._h, lr, _ptr(feats, C.c_float), _ptr(labels, C.c_int32),
                                                      _ptr(loss, C.c_float)))
+        self._prefetched = [b for b in getattr(self, "_prefetched", []) if b[0] is not feats]
         return loss
+
+    def prefetch_host_batch(self, feats: np.ndarray, labels: np.ndarray) -> None:
+        """Queue the H2D copy of the next host batch so it overlaps the current step; pass the
+        same (C-contiguous float32 / int32) arrays to the matching step_host_batch."""
+        if not (feats.flags.c_contiguous and feats.dtype == np.float32 and labels.flags.c_contiguous
+                and labels.dtype == np.int32):
+            raise ValueError("prefetch_host_batch needs C-contiguous float32 features and int32 labels")
+        _lib.check(_lib.lib().adpsgd_prefetch_host_batch(self._h, _ptr(feats, C.c_float), _ptr(labels, C.c_int32)))
+        if not hasattr(self, "_prefetched"):
+            self._prefetched = []
+        self._prefetched.append((feats, labels))  # keep the host memory alive until its step
 
     def step_injected(self, lr: float, grads: np.ndarray, taus=None) -> None:
         g = np.ascontiguousarray(grads, dtype=np.float64)

@@ -361,6 +361,34 @@ def test_host_batch_step_equals_indexed_step(oracle_mod):
         assert np.array_equal(a.weights(j), b.weights(j))
 
 
+def test_prefetched_host_batches_equal_synchronous_copies():
+    """Data-loader path: prefetch_host_batch queues the next batch's H2D copy on a copy stream
+    (two staging slots) while the current step computes; the steps must equal the plain
+    host-batch steps bit for bit, including a prefetch that is skipped (different batch given)."""
+    m = ModelDesc(layers=2, hidden=128, bidirectional=True, input_dim=40, proj=64, classes=96, unroll=7)
+    rng = np.random.default_rng(9)
+    batches = [(rng.normal(size=(64, m.unroll, m.input_dim)).astype(np.float32),
+                rng.integers(0, m.classes, size=(64, m.unroll)).astype(np.int32)) for _ in range(5)]
+    runs = {}
+    for prefetch in (False, True, "plain2"):
+        g = LearnerGroup(m, StrategyConfig(learners=1, batch=64, seed=4), precision=Precision.BF16)
+        losses = []
+        pf = prefetch is True
+        if pf:
+            g.prefetch_host_batch(*batches[0])
+        for i, (f, l) in enumerate(batches):
+            if pf and i + 1 < len(batches) and i != 2:
+                g.prefetch_host_batch(*batches[i + 1])
+            if pf and i == 3:  # batch 3 was not prefetched; a stale prefetch must not be used
+                g.prefetch_host_batch(*batches[0])
+            losses.append(g.step_host_batch(0.1, f, l)[0])
+        runs[prefetch] = (losses, g.weights(0).copy())
+        g.close()
+    assert runs[False][0] == runs["plain2"][0], ("plain runs differ", runs[False][0], runs["plain2"][0])
+    assert runs[False][0] == runs[True][0], ("prefetch differs", runs[False][0], runs[True][0])
+    assert np.array_equal(runs[False][1], runs[True][1])
+
+
 def test_config_s_fixed_ring_fp32(oracle_mod):
     """BASELINE configs[0]: 2-layer LSTM H=256, 40-dim features, 4 learners, FM."""
     O = oracle_mod

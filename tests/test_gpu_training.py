@@ -137,3 +137,24 @@ def test_fused_sgd_update_matches_separate_update_kernel(monkeypatch):
     (l0, w0), (l1, w1) = res["0"], res["1"]
     assert l0 == l1
     assert np.array_equal(w0, w1)
+
+
+def test_context_upload_is_stream_ordered():
+    """Regression: w0 / the identity index / dataset uploads used pageable cudaMemcpy on the legacy
+    stream, which the engine's non-blocking stream does not wait for (and which may return before
+    the DMA lands): the bf16 shadow built right after could pick up the previous contents of the
+    allocation. After a large context is freed, a new context's shadow must equal bf16(w0)."""
+    import ctypes as C
+    import torch
+    from paper_2110_11199_b200 import _lib
+    big = ModelDesc(layers=2, hidden=512, bidirectional=True, input_dim=260, proj=256, classes=4000, unroll=11)
+    small = ModelDesc(layers=2, hidden=128, bidirectional=True, input_dim=40, proj=64, classes=96, unroll=7)
+    for it in range(3):
+        g = LearnerGroup(big, StrategyConfig(learners=1, batch=256, seed=it), precision=Precision.BF16)
+        g.close()
+        s = LearnerGroup(small, StrategyConfig(learners=1, batch=64, seed=4), precision=Precision.BF16)
+        sh = np.zeros(s.D, dtype=np.uint16)
+        _lib.check(_lib.lib().adpsgd_debug_buffer(s.handle, 102, sh.ctypes.data_as(C.c_void_p), sh.nbytes))
+        ref = torch.from_numpy(s.weights(0).astype(np.float32)).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+        s.close()
+        assert np.array_equal(sh, ref), it
