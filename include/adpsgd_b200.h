@@ -159,7 +159,10 @@ int adpsgd_async_run(adpsgd_ctx* ctx, int32_t strategy, const double* durations,
                      int64_t* processed);
 
 /* ---- multi-process (one process per GPU) ---- */
-/* NCCL communicator over all ranks; nccl_id = 128-byte ncclUniqueId from rank 0. */
+/* NCCL communicator over all ranks; nccl_id = 128-byte ncclUniqueId from rank 0.
+ * nccl_id = NULL: CUDA-IPC-only transport (FM / RM peer gossip; no device barrier, so the caller
+ * separates steps with a host barrier) for ranks that share one GPU, where NCCL refuses
+ * duplicate devices. */
 int adpsgd_nccl_unique_id(void* out128);
 int adpsgd_comm_init(adpsgd_ctx* ctx, int32_t rank, int32_t world, const void* nccl_id128);
 /* CUDA IPC handles of this context's weight buffers, for peer (NVLink P2P) gossip pulls. */

@@ -72,6 +72,13 @@ Comm::Comm(Ctx& c, int r, int w, const void* id128) : rank(r), world(w), D_(c.D)
     AB_CHECK(w >= 1 && r >= 0 && r < w, ADPSGD_E_CONFIG, "bad rank/world");
     AB_CHECK(w == 1 || c.cfg.local_learners == 1, ADPSGD_E_CONFIG,
              "multi-process runs host exactly one learner per rank");
+    if (id128 == nullptr) {
+        // CUDA-IPC-only transport: FM/RM pulls from peer buffers; the caller separates steps with
+        // a host barrier (there is no device barrier). For ranks sharing one GPU, where NCCL
+        // refuses duplicate devices -- tests of the multi-process gossip path on one B200.
+        ipc_only = true;
+        return;
+    }
     ncclUniqueId id;
     std::memcpy(&id, id128, sizeof(id));
     ncclComm_t comm;
@@ -94,15 +101,18 @@ Comm::~Comm() {
 }
 
 void Comm::barrier(cudaStream_t s) {
+    if (ipc_only) return;  // steps are separated on the host
     AB_NCCL(nccl().AllReduce(bar_, bar_ + 1, 1, ncclFloat32, ncclSum, static_cast<ncclComm_t>(nccl_), s));
 }
 
 const float* Comm::allreduce_sum_grads(Ctx& c, cudaStream_t s) {
+    AB_CHECK(!ipc_only, ADPSGD_E_CONFIG, "IPC-only transport: FM / RM only (SDPSGD needs NCCL)");
     AB_NCCL(nccl().AllReduce(c.learners[0].g, gsum_, c.D, ncclFloat32, ncclSum, static_cast<ncclComm_t>(nccl_), s));
     return gsum_;
 }
 
 void Comm::start_weight_sum(Ctx& c, cudaStream_t s) {
+    AB_CHECK(!ipc_only, ADPSGD_E_CONFIG, "IPC-only transport: FM / RM only (D1D needs NCCL)");
     // w_k is final once the previous iteration's update (enqueued on s) has run.
     AB_CUDA(cudaEventRecord(ev_start_, s));
     AB_CUDA(cudaStreamWaitEvent(c.s_comm, ev_start_, 0));

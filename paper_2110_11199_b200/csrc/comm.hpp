@@ -21,6 +21,7 @@ class Comm {
     static void unique_id(void* out128);
 
     int rank = 0, world = 1;
+    bool ipc_only = false;  // no NCCL (ranks sharing one GPU): FM/RM peer gossip, host-separated steps
     int gossip_mode = 0;  // 0 direct peer loads, 1 copy-engine prefetch, 2 NCCL send/recv
 
     // SDPSGD: sum of every learner's gradient (in place in a comm buffer).

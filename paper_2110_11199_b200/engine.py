@@ -306,8 +306,9 @@ class LearnerGroup:
         return out.value
 
     # ---- multi-process plumbing (one process per GPU) ----
-    def comm_init(self, rank: int, world: int, nccl_id: bytes) -> None:
-        buf = C.create_string_buffer(nccl_id, 128)
+    def comm_init(self, rank: int, world: int, nccl_id: bytes | None) -> None:
+        """nccl_id None: CUDA-IPC-only transport (FM/RM; steps separated by a host barrier)."""
+        buf = None if nccl_id is None else C.create_string_buffer(nccl_id, 128)
         _lib.check(_lib.lib().adpsgd_comm_init(self._h, rank, world, buf))
 
     def export_ipc(self) -> bytes:
