@@ -160,7 +160,7 @@ int adpsgd_async_run(adpsgd_ctx* ctx, int32_t strategy, const double* durations,
 
 /* ---- multi-process (one process per GPU) ---- */
 /* NCCL communicator over all ranks; nccl_id = 128-byte ncclUniqueId from rank 0.
- * nccl_id = NULL: CUDA-IPC-only transport (FM / RM peer gossip; no device barrier, so the caller
+ * nccl_id = NULL: CUDA-IPC-only transport (FM / RM / D1D by peer reads; no device barrier, so the caller
  * separates steps with a host barrier) for ranks that share one GPU, where NCCL refuses
  * duplicate devices. */
 int adpsgd_nccl_unique_id(void* out128);

@@ -893,7 +893,12 @@ void Ctx::mix_and_update(double lr_d, const int32_t* taus) {
             launch_sdpsgd(D, Lg, learners[0].w[cur], gtab.data(), nullptr, nloc, lr, otab.data(), stab.data(), s);
         }
     } else if (strategy == ADPSGD_D1D) {
-        if (comm && comm->world > 1) {
+        if (comm && comm->world > 1 && comm->ipc_only) {
+            // CUDA-IPC-only transport: the mean reads every learner's w_k directly (learner order,
+            // as the local path); w_k is final because the caller separates steps on the host
+            for (int gid = 0; gid < Lg; ++gid) wtab.push_back(weight_ptr(gid, cur));
+            launch_d1d(D, Lg, wtab.data(), nullptr, nloc, gtab.data(), lr, otab.data(), stab.data(), s);
+        } else if (comm && comm->world > 1) {
             const float* wsum = comm->wait_weight_sum(*this, s);  // allreduce started before the compute
             launch_d1d(D, Lg, nullptr, wsum, nloc, gtab.data(), lr, otab.data(), stab.data(), s);
         } else {
@@ -1025,7 +1030,7 @@ void Ctx::step(double lr, const int32_t* taus, float* loss_out, const float* hos
     }
     AB_CUDA(cudaEventRecord(ev0, s));
     // D1D: start the weight allreduce on the comm stream before the gradient compute
-    if (strategy == ADPSGD_D1D && comm && comm->world > 1) comm->start_weight_sum(*this, s);
+    if (strategy == ADPSGD_D1D && comm && comm->world > 1 && !comm->ipc_only) comm->start_weight_sum(*this, s);
     for (int j = 0; j < cfg.local_learners; ++j) {
         Learner& ln = learners[j];
         if (injected) {

@@ -2,7 +2,8 @@
 through CUDA IPC inside the fused mix kernel) run as 3 processes sharing one B200 with the
 CUDA-IPC-only transport (NCCL refuses duplicate devices), against the same 3-learner ring hosted
 by one process. The per-learner gradients, pairings and mixing arithmetic are identical, so the
-weights must agree bit for bit (FM: engine.cpp:156-171; RM pairing: chronos.cpp:227-235)."""
+weights must agree bit for bit (FM: engine.cpp:156-171; RM pairing: chronos.cpp:227-235; D1D:
+the mean over every learner's w_k read through IPC in learner order, engine.cpp:173-184)."""
 import multiprocessing as mp
 import os
 import socket
@@ -61,7 +62,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("strategy_name", ["ADPSGD_FM", "ADPSGD_RM"])
+@pytest.mark.parametrize("strategy_name", ["ADPSGD_FM", "ADPSGD_RM", "ADPSGD_D1D"])
 @pytest.mark.parametrize("prec_name", ["FP32", "BF16"])
 def test_multiprocess_ipc_gossip_equals_single_process_ring(strategy_name, prec_name):
     from paper_2110_11199_b200 import LearnerGroup, Precision, Strategy, StrategyConfig
