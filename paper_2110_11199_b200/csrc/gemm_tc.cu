@@ -739,7 +739,8 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
     const int bn = wide ? 512 : (xb ? 256 : bn0);
     const int tiles = m_tiles * ((n_eff + bn - 1) / bn);
     const bool sk = !wide_wgrad && sk_ok(bn);
-    if (std::getenv("ADPSGD_LOG_GEMM"))
+    static const bool log_gemm = std::getenv("ADPSGD_LOG_GEMM") != nullptr;  // diagnosis
+    if (log_gemm)
         std::fprintf(stderr, "gemm M=%d N=%d K=%d nseg=%d amn=%d bmn=%d cbf16=%d pair=%d bn=%d xtra=%d xb=%d sk=%d tag=%d\n", g.M,
                      g.N, g.seg[0].K, g.nseg, amn, bmn, g.c_bf16, pair, bn, xtra, xb, sk, g.tag);
 
