@@ -21,6 +21,9 @@ CASES = {
     "bi2p": ModelDesc(layers=2, hidden=16, bidirectional=True, input_dim=20, proj=8, classes=40, unroll=7),
     "bi3p_t21": ModelDesc(layers=3, hidden=32, bidirectional=True, input_dim=36, proj=16, classes=64, unroll=21),
     "odd_in": ModelDesc(layers=2, hidden=24, bidirectional=True, input_dim=13, proj=8, classes=16, unroll=4),
+    # edge cases: no recurrence (T = 1: dW_hh = 0), and T = 1 on the fused tcgen05 recurrent path
+    "t1": ModelDesc(layers=1, hidden=16, bidirectional=True, input_dim=12, proj=8, classes=10, unroll=1),
+    "t1_fused": ModelDesc(layers=2, hidden=64, bidirectional=True, input_dim=40, proj=16, classes=32, unroll=1),
 }
 
 
@@ -463,3 +466,25 @@ def test_full_size_bf16_gradient_at_fp32_conditioning_floor():
     assert abs(lb - lr) <= 1e-2 * abs(lr)
     floor = _rel(gr, gf)
     assert _rel(gb, gr) <= 1.5 * floor + 2e-2, (_rel(gb, gr), floor)
+
+
+def test_single_segment_batch_and_errors(oracle_mod):
+    """Edge cases of the reference's input checks: a one-segment batch matches the oracle;
+    stepping without a dataset and a zero batch raise InvalidStateError / ConfigError
+    (objectives.cpp:240-241, engine.cpp:60-77)."""
+    from paper_2110_11199_b200.errors import AdpsgdError, InvalidStateError
+    O, m = oracle_mod, CASES["bi2p"]
+    feats, labels = _data(m)
+    g = LearnerGroup(m, StrategyConfig(learners=1, batch=1, seed=1), precision=Precision.FP32)
+    with pytest.raises(InvalidStateError):
+        g.step(0.1)
+    g.set_dataset(feats, labels, 40)
+    w = np.random.default_rng(3).normal(0, 0.2, g.D)
+    idx = np.array([17], dtype=np.int32)
+    loss, grad = g.gradient(w, idx)
+    oloss, ograd = O.lstm_loss_grad(_odesc(O, m), w, feats, labels, idx)
+    assert abs(loss - oloss) <= 1e-5 * abs(oloss)
+    assert np.max(np.abs(grad - ograd)) <= 2e-5 * np.max(np.abs(ograd))
+    g.close()
+    with pytest.raises((AdpsgdError, ValueError)):
+        StrategyConfig(learners=1, batch=0, seed=1).validate()
