@@ -93,7 +93,40 @@ Comm::Comm(Ctx& c, int r, int w, const void* id128) : rank(r), world(w), D_(c.D)
     AB_CUDA(cudaEventCreateWithFlags(&ev_ws_, cudaEventDisableTiming));
 }
 
+void Comm::ensure_nb(Ctx& c) {
+    if (!nb_[0]) {
+        nb_[0] = static_cast<float*>(c.alloc(c.D * sizeof(float)));
+        nb_[1] = static_cast<float*>(c.alloc(c.D * sizeof(float)));
+        AB_CUDA(cudaEventCreateWithFlags(&nb_ready, cudaEventDisableTiming));
+    }
+}
+
+void Comm::prefetch_neighbours(Ctx& c, const float* wl, const float* wr, cudaStream_t s) {
+    ensure_nb(c);
+    // (NCCL transport: every rank's w_k is final once the barrier on s has completed)
+    barrier(s);
+    AB_CUDA(cudaEventRecord(nb_ready, s));
+    AB_CUDA(cudaStreamWaitEvent(c.s_comm, nb_ready, 0));
+    AB_CUDA(cudaMemcpyAsync(nb_[0], wl, c.D * sizeof(float), cudaMemcpyDeviceToDevice, c.s_comm));
+    AB_CUDA(cudaMemcpyAsync(nb_[1], wr, c.D * sizeof(float), cudaMemcpyDeviceToDevice, c.s_comm));
+    AB_CUDA(cudaEventRecord(nb_ready, c.s_comm));
+}
+
+void Comm::sendrecv_neighbours(Ctx& c, int left, int right, cudaStream_t s) {
+    AB_CHECK(!ipc_only, ADPSGD_E_CONFIG, "gossip mode 2 (NCCL send/recv) needs the NCCL transport");
+    ensure_nb(c);
+    const float* w = c.learners[0].w[c.k & 1];
+    const int rl = left - c.cfg.first_learner + rank, rr = right - c.cfg.first_learner + rank;  // one learner per rank
+    AB_NCCL(nccl().GroupStart());
+    AB_NCCL(nccl().Send(w, c.D, ncclFloat32, rl, static_cast<ncclComm_t>(nccl_), s));
+    AB_NCCL(nccl().Send(w, c.D, ncclFloat32, rr, static_cast<ncclComm_t>(nccl_), s));
+    AB_NCCL(nccl().Recv(nb_[0], c.D, ncclFloat32, rl, static_cast<ncclComm_t>(nccl_), s));
+    AB_NCCL(nccl().Recv(nb_[1], c.D, ncclFloat32, rr, static_cast<ncclComm_t>(nccl_), s));
+    AB_NCCL(nccl().GroupEnd());
+}
+
 Comm::~Comm() {
+    if (nb_ready) cudaEventDestroy(nb_ready);
     for (void* p : opened_) cudaIpcCloseMemHandle(p);
     if (nccl_) nccl().CommDestroy(static_cast<ncclComm_t>(nccl_));
     if (ev_start_) cudaEventDestroy(ev_start_);

@@ -34,6 +34,14 @@ class Comm {
     void pre_gossip(Ctx& c, cudaStream_t s);
     void barrier(cudaStream_t s);
     const float* peer_weight(int gid, int buf) const;
+    // gossip_mode 1: copy-engine pulls of the two neighbours' w_k into local buffers on the comm
+    // stream (issued at step start, overlapping the gradient compute; `ready` event joined by the mix)
+    void prefetch_neighbours(Ctx& c, const float* wl, const float* wr, cudaStream_t s);
+    // gossip_mode 2 (baseline): NCCL send of w_k to both neighbours / receive of theirs, on s
+    void sendrecv_neighbours(Ctx& c, int left, int right, cudaStream_t s);
+    const float* nb_left() const { return nb_[0]; }
+    const float* nb_right() const { return nb_[1]; }
+    cudaEvent_t nb_ready = nullptr;
 
     int64_t ipc_size(const Ctx& c) const;
     void export_ipc(const Ctx& c, void* out, int64_t size) const;
@@ -47,6 +55,8 @@ class Comm {
     cudaEvent_t ev_start_ = nullptr, ev_ws_ = nullptr;
     std::map<int, std::pair<float*, float*>> peers_;  // gid -> (w[0], w[1]) mapped over NVLink
     std::vector<void*> opened_;
+    float* nb_[2] = {nullptr, nullptr};  // local copies of the neighbours' w_k (modes 1, 2)
+    void ensure_nb(Ctx& c);
     int64_t D_ = 0;
 };
 

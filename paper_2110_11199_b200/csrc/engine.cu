@@ -906,23 +906,20 @@ void Ctx::mix_and_update(double lr_d, const int32_t* taus) {
             launch_d1d(D, Lg, wtab.data(), nullptr, nloc, gtab.data(), lr, otab.data(), stab.data(), s);
         }
     } else if (strategy == ADPSGD_FM || strategy == ADPSGD_RM) {
-        std::vector<int32_t> map(Lg);
-        if (strategy == ADPSGD_RM) permutation_for_iteration(cfg.seed, Lg, k, map.data());
-        if (comm && comm->world > 1) comm->pre_gossip(*this, s);
+        const int mode = (comm && comm->world > 1) ? comm->gossip_mode : 0;
+        if (comm && comm->world > 1 && mode == 0) comm->pre_gossip(*this, s);
         for (int j = 0; j < nloc; ++j) {
-            const int l = learners[j].gid;
             int left, right;
-            if (strategy == ADPSGD_FM) {
-                left = (l + Lg - 1) % Lg;
-                right = (l + 1) % Lg;
-            } else {  // chronos.cpp:227-235
-                int pos = 0;
-                for (int i = 0; i < Lg; ++i) if (map[i] == l) { pos = i; break; }
-                left = map[(pos + Lg - 1) % Lg];
-                right = map[(pos + 1) % Lg];
-            }
+            neighbours(strategy, learners[j].gid, &left, &right);
             const float* wl = weight_ptr(left, cur);
             const float* wr = weight_ptr(right, cur);
+            if (mode == 1) {  // pulled by the copy engines while the gradient was computed
+                AB_CUDA(cudaStreamWaitEvent(s, comm->nb_ready, 0));
+                wl = comm->nb_left(); wr = comm->nb_right();
+            } else if (mode == 2) {  // NCCL send / recv baseline
+                comm->sendrecv_neighbours(*this, left, right, s);
+                wl = comm->nb_left(); wr = comm->nb_right();
+            }
             if (!is_local(left)) last_gossip_bytes += D * 4.0;
             if (!is_local(right)) last_gossip_bytes += D * 4.0;
             launch_mix3(D, learners[j].w[cur], wl, wr, learners[j].g, lr, learners[j].w[nxt], stab[j], s);
@@ -969,6 +966,23 @@ void Ctx::mix_and_update(double lr_d, const int32_t* taus) {
             AB_CUDA(cudaMemcpyAsync(oldest, ln.w[cur], D * sizeof(float), cudaMemcpyDeviceToDevice, s));
         }
     }
+}
+
+// Ring neighbours of global learner l at the current iteration: FM l-1 / l+1, RM from the
+// seeded permutation of iteration k (chronos.cpp:227-235).
+void Ctx::neighbours(int strategy, int l, int* left, int* right) const {
+    const int Lg = cfg.learners;
+    if (strategy == ADPSGD_FM) {
+        *left = (l + Lg - 1) % Lg;
+        *right = (l + 1) % Lg;
+        return;
+    }
+    std::vector<int32_t> map(Lg);
+    permutation_for_iteration(cfg.seed, Lg, k, map.data());
+    int pos = 0;
+    for (int i = 0; i < Lg; ++i) if (map[i] == l) { pos = i; break; }
+    *left = map[(pos + Lg - 1) % Lg];
+    *right = map[(pos + 1) % Lg];
 }
 
 const float* Ctx::weight_ptr(int gid, int buf) const {
@@ -1031,6 +1045,12 @@ void Ctx::step(double lr, const int32_t* taus, float* loss_out, const float* hos
     AB_CUDA(cudaEventRecord(ev0, s));
     // D1D: start the weight allreduce on the comm stream before the gradient compute
     if (strategy == ADPSGD_D1D && comm && comm->world > 1 && !comm->ipc_only) comm->start_weight_sum(*this, s);
+    // FM / RM, gossip mode 1: the neighbours' w_k travel by copy engine while this learner computes
+    if ((strategy == ADPSGD_FM || strategy == ADPSGD_RM) && comm && comm->world > 1 && comm->gossip_mode == 1 && !injected) {
+        int left, right;
+        neighbours(strategy, learners[0].gid, &left, &right);
+        comm->prefetch_neighbours(*this, weight_ptr(left, static_cast<int>(k & 1)), weight_ptr(right, static_cast<int>(k & 1)), s);
+    }
     for (int j = 0; j < cfg.local_learners; ++j) {
         Learner& ln = learners[j];
         if (injected) {

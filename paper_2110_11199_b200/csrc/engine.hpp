@@ -158,6 +158,7 @@ struct Ctx {
     void mix_and_update(double lr, const int32_t* taus);
     const float* grad_point(const Learner& ln, const int32_t* taus);
     const float* weight_ptr(int gid, int buf) const;
+    void neighbours(int strategy, int l, int* left, int* right) const;
     bool is_local(int gid) const;
     void check_sync();
     void step(double lr, const int32_t* taus, float* loss_out, const float* host_feats, const int32_t* host_labels,

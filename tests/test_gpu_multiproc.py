@@ -27,7 +27,7 @@ def _data(m):
             rng.integers(0, m.classes, size=(64, m.unroll)).astype(np.int32))
 
 
-def _worker(rank, port, strategy, prec, q):
+def _worker(rank, port, strategy, prec, mode, q):
     try:
         os.environ.update({"MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port)})
         import torch.distributed as dist
@@ -43,6 +43,7 @@ def _worker(rank, port, strategy, prec, q):
         dist.all_gather_object(handles, g.export_ipc())
         for r, h in enumerate(handles):
             g.import_ipc(r, r, 1, h)
+        g.set_gossip_mode(mode)
         dist.barrier()
         losses = []
         for _ in range(STEPS):
@@ -62,15 +63,20 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("strategy_name", ["ADPSGD_FM", "ADPSGD_RM", "ADPSGD_D1D"])
-@pytest.mark.parametrize("prec_name", ["FP32", "BF16"])
-def test_multiprocess_ipc_gossip_equals_single_process_ring(strategy_name, prec_name):
+CASES = [(s, p, 0) for s in ("ADPSGD_FM", "ADPSGD_RM", "ADPSGD_D1D") for p in ("FP32", "BF16")] + \
+        [("ADPSGD_FM", "FP32", 1), ("ADPSGD_RM", "BF16", 1)]
+
+
+@pytest.mark.parametrize("strategy_name,prec_name,mode", CASES)
+def test_multiprocess_ipc_gossip_equals_single_process_ring(strategy_name, prec_name, mode):
+    """mode 0: neighbours read inside the fused mix kernel; mode 1: pulled by the copy engines on
+    the comm stream while the gradient is computed, then mixed from local copies."""
     from paper_2110_11199_b200 import LearnerGroup, Precision, Strategy, StrategyConfig
     strategy, prec = int(Strategy[strategy_name]), int(Precision[prec_name])
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, port, strategy, prec, q)) for r in range(WORLD)]
+    procs = [ctx.Process(target=_worker, args=(r, port, strategy, prec, mode, q)) for r in range(WORLD)]
     for p in procs:
         p.start()
     got = {}
