@@ -2,7 +2,7 @@
 # Round evidence (1 GPU, under gpurun): launch list of one step, full ncu captures of the top
 # kernels, and a bench line. Output: gpurun_out/<tag>_*. Summarise locally with
 #   python tools/summarize_ncu.py <tag> gpurun_out/<tag>_*.ncu-rep --launches gpurun_out/<tag>_launches.csv
-tag=${1:-r01g}
+tag=${1:-r01i}
 B="python bench.py --steps 1 --warmup 0 --no-cpu-baseline --e2e-steps 1"
 ncu --metrics gpu__time_duration.sum,launch__grid_size --clock-control none -c 700 --csv \
     --log-file gpurun_out/${tag}_launches.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --e2e-steps 1 \
