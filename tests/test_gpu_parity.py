@@ -441,6 +441,31 @@ def _rel(a, b):
     return float(np.linalg.norm(a - b) / np.linalg.norm(b))
 
 
+@pytest.mark.parametrize("hidden,batch", [(512, 256), (512, 512), (256, 256)])
+def test_paper_widths_bf16_gradient_matches_fp32_engine(hidden, batch):
+    """BASELINE's paper shape P uses 512 units/direction: the persistent recurrent kernels at
+    H = 512 (and 256) with one or two 256-row blocks per direction, against the FP32 engine on the
+    same bf16-representable weights (2 layers, T = 21)."""
+    m = ModelDesc(layers=2, hidden=hidden, bidirectional=True, input_dim=260, proj=256, classes=2000, unroll=21)
+    rng = np.random.default_rng(5)
+    n_seg = 600
+    feats = rng.normal(size=(n_seg, m.unroll, m.input_dim)).astype(np.float32)
+    labels = rng.integers(0, m.classes, size=(n_seg, m.unroll)).astype(np.int32)
+    idx = rng.integers(0, n_seg, size=batch).astype(np.int32)
+    out, w = {}, None
+    for prec in (Precision.FP32, Precision.BF16):
+        g = LearnerGroup(m, StrategyConfig(learners=1, batch=batch, seed=3), precision=prec)
+        g.set_dataset(feats, labels, n_seg)
+        if w is None:
+            w = torch.from_numpy(g.weights(0).copy()).to(torch.bfloat16).float().numpy()
+        out[prec] = g.gradient(w, idx)
+        g.close()
+    (lf, gf), (lb, gb) = out[Precision.FP32], out[Precision.BF16]
+    assert np.isfinite(lb) and np.all(np.isfinite(gb))
+    assert abs(lb - lf) <= 1e-2 * abs(lf)
+    assert _rel(gb, gf) <= 5e-2, _rel(gb, gf)
+
+
 def test_full_width_two_layer_bf16_gradient_matches_fp32_engine():
     """BASELINE configs[1] widths (1024 units/dir, proj 256, 32k classes, T = 21, 256 segments) at
     2 layers: bf16 tcgen05 path (persistent recurrent kernels, fused 32k-class softmax-CE,
