@@ -218,7 +218,7 @@ def run_reference(a):
     val = frames / tot
     m = model_desc(a)
     line = {
-        "impl": "reference", "metric": "frames/sec (6x1024 BLSTM ADPSGD learner step)", "value": val,
+        "impl": "reference", "metric": f"frames/sec ({m.layers}x{m.hidden} BLSTM ADPSGD learner step)", "value": val,
         "unit": "frames/s", "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": 1000.0 * tot / len(times), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -353,7 +353,7 @@ def run_ours(a):
                "sample": f"1 segment x 21 frames of the same model, fp64 oracle gradient + SGD update, "
                          f"single thread ({dt:.1f} s)"}
     line = {
-        "metric": "frames/sec (6x1024 BLSTM ADPSGD learner step)",
+        "metric": f"frames/sec ({m.layers}x{m.hidden} BLSTM ADPSGD learner step)",
         "value": value, "unit": "frames/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": tot_ms / a.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": a.precision, "data": "synthetic (device-generated SWB-shaped frames, 260-dim, 32k labels)",
