@@ -368,7 +368,7 @@ def run_ours(a):
                 "d2h_bytes_per_step": 4, "steps": e2e_steps,
                 "h2d": "pinned host batch, prefetched one step ahead on a copy stream (adpsgd_prefetch_host_batch)"},
         "roofline": {"bound": "tensor",
-                     "kernel": "persistent_kernel_2cta<FwdPersistTraits>: one launch per layer = 21 steps x 2 "
+                     "kernel": "persistent_kernel_2cta<FwdPersistT<64>>: one launch per layer = 21 steps x 2 "
                                "directions of the fused recurrent GEMM [x_t|h_t-1][W_ih|W_hh]^T + LSTM cell, "
                                "tcgen05 cta_group::2 256x256 tiles",
                      "achieved": dom_tf, "peak": peak, "unit": "TFLOP/s", "frac": dom_tf / peak if peak else None,

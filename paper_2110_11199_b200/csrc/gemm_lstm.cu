@@ -732,9 +732,12 @@ struct FwdPParams {
     unsigned long long* trace;
 };
 
-struct FwdPersistTraits : tc::TraitsBase {
-    using F = FwdT<64>;
-    static constexpr int BN = 256;
+// UW = hidden units per tile (x 4 gates = BN): 64 by default; 32 when 64-unit tiles would leave
+// most CTA pairs idle (H = 512: 4 row blocks x 8 unit blocks = 32 tiles for 74 pairs).
+template <int UW>
+struct FwdPersistT : tc::TraitsBase {
+    using F = FwdT<UW>;
+    static constexpr int BN = 4 * UW;
     static constexpr int EPI_WARP = F::EPI_WARP;
     static constexpr int EPI_WARPS = 4;
     static constexpr int EPI_SMEM = EPI_WARPS * EPI_WARP;
@@ -791,8 +794,8 @@ struct FwdPersistTraits : tc::TraitsBase {
         const uint64_t keep = ptx::policy_evict_last();
 #pragma unroll
         for (int j = 0; j < 2; ++j)
-            ptx::tma_load_2d_2sm_hint(sB + j * 64 * kBK * 2, &g.tb[seg], bar, k0,
-                                      (2 * static_cast<int>(rank) + j) * p.H + u.nt * 64, keep);
+            ptx::tma_load_2d_2sm_hint(sB + j * UW * kBK * 2, &g.tb[seg], bar, k0,
+                                      (2 * static_cast<int>(rank) + j) * p.H + u.nt * UW, keep);
     }
     template <class S>
     __device__ static void epi_begin2(const FwdPParams& p, int it, uint32_t rank, int q, int lane, uint8_t*, uint64_t*,
@@ -800,15 +803,15 @@ struct FwdPersistTraits : tc::TraitsBase {
         const U u = unit(p, blockIdx.x >> 1, it);
         if (u.s == 0) return;
         const int uc = 32 * sl.sub + 32 * sl.n * (lane & 1);
-        if (lane < 2 && uc < 64)
-            ptx::tma_prefetch_l2_2d(&p.g[u.d].m_cprev, u.nt * 64 + uc,
+        if (lane < 2 && uc < UW)
+            ptx::tma_prefetch_l2_2d(&p.g[u.d].m_cprev, u.nt * UW + uc,
                                     u.tp * p.B + u.mt * 2 * kBM + kBM * static_cast<int>(rank) + q * 32);
     }
     __device__ static void epilogue_sk(const FwdPParams& p, const tc::Item& w, int cid, uint32_t rank, uint32_t tbase,
                                        int q, int lane, uint32_t tempty_leader, tc::EpiSlot sl, uint8_t* st,
                                        uint64_t* ebar, uint32_t& ephase) {
         const U u = unit(p, cid, w.tile);
-        F::body_g(p.g[u.d], p.H, u.mt * 2 * kBM + kBM * static_cast<int>(rank), u.nt * 64, tbase, q, lane,
+        F::body_g(p.g[u.d], p.H, u.mt * 2 * kBM + kBM * static_cast<int>(rank), u.nt * UW, tbase, q, lane,
                   [&] { tc::release_acc_2sm(tempty_leader, lane); }, st, ebar, ephase, sl, nullptr, u.t * p.B,
                   u.s > 0 ? u.tp * p.B : 0, u.s > 0);
         // publish: this CTA's h_t (and c_t) block is in memory
@@ -831,6 +834,8 @@ struct FwdPersistTraits : tc::TraitsBase {
         }
     }
 };
+
+using FwdPersistTraits = FwdPersistT<64>;
 
 // ---------------- persistent BPTT (one launch per layer) ----------------
 // All T-1 recurrent steps of both directions in one kernel. CTA pair c owns work unit
@@ -1151,7 +1156,10 @@ void lstm_bwd_step(const LstmBwdDir* dirs, int ndirs, int B, int H, int lddh, in
 
 bool lstm_fwd_layer_persistent(const LstmFwdLayer& L, int ndirs, int B, int H, int T, cudaStream_t s, unsigned int* dep,
                                unsigned int* exit_ctr) {
-    const int m_tiles = B / (2 * kBM), n_tiles = H / 64;
+    // 32-unit tiles when 64-unit ones would leave more than half of the CTA pairs idle
+    const int m_tiles = B / (2 * kBM);
+    const int uw = (knobs().fwd_u32 && H % 32 == 0 && m_tiles * (H / 64) * 2 <= num_sms() / 2) ? 32 : 64;
+    const int n_tiles = H / uw;
     const int units = m_tiles * n_tiles;
     if (!(knobs().persist_fwd && knobs().pair_mma && ndirs == 2 && B % (2 * kBM) == 0 && H % 64 == 0 &&
           units <= num_sms() / 2 && dep && exit_ctr))
@@ -1163,9 +1171,9 @@ bool lstm_fwd_layer_persistent(const LstmFwdLayer& L, int ndirs, int B, int H, i
     for (int d = 0; d < 2; ++d) {
         FwdGroup& g = p.g[d];
         make_map_box(&g.ta[0], L.x, L.Kx, TB, L.ldx, kBM);
-        make_map_box(&g.tb[0], L.w_ih[d], L.Kx, 4 * H, L.ld_wih, 64);
+        make_map_box(&g.tb[0], L.w_ih[d], L.Kx, 4 * H, L.ld_wih, uw);
         make_map_box(&g.ta[1], L.h + d * H, H, TB, L.ldh, kBM);
-        make_map_box(&g.tb[1], L.w_hh[d], H, 4 * H, H, 64);
+        make_map_box(&g.tb[1], L.w_hh[d], H, 4 * H, H, uw);
         make_map_gen(&g.m_cprev, L.c + d * H, true, H, TB, L.ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
         make_map_gen(&g.m_gates, L.gates + d * 4 * H, false, 4 * H, TB, L.ldg, 16, 32, CU_TENSOR_MAP_SWIZZLE_32B);
         make_map_gen(&g.m_c, L.c + d * H, true, H, TB, L.ldc, 16, 32, CU_TENSOR_MAP_SWIZZLE_64B);
@@ -1180,13 +1188,18 @@ bool lstm_fwd_layer_persistent(const LstmFwdLayer& L, int ndirs, int B, int H, i
     p.trace = trace_take();
     const double bytes = 2.0 * T * (2.0 * (B + 4.0 * H) * (L.Kx + H) + static_cast<double>(B) * H * 22);
     ProfScope ps_(s, PROF_GEMM_REC_FWD, flops, bytes);
-    auto k = tc::persistent_kernel_2cta<FwdPersistTraits, FwdPParams>;
-    static bool attr = false;
-    if (!attr) {
-        AB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::ShapeOf2<FwdPersistTraits>::SMEM));
-        attr = true;
-    }
-    tc::launch_tc(k, p, 2 * units, tc::threads_of<FwdPersistTraits>(), tc::ShapeOf2<FwdPersistTraits>::SMEM, true, s);
+    auto launch = [&](auto tr) {
+        using Tr = decltype(tr);
+        auto k = tc::persistent_kernel_2cta<Tr, FwdPParams>;
+        static bool attr = false;
+        if (!attr) {
+            AB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::ShapeOf2<Tr>::SMEM));
+            attr = true;
+        }
+        tc::launch_tc(k, p, 2 * units, tc::threads_of<Tr>(), tc::ShapeOf2<Tr>::SMEM, true, s);
+    };
+    if (uw == 32) launch(FwdPersistT<32>{});
+    else launch(FwdPersistT<64>{});
     count_launch();
     return true;
 }

@@ -11,7 +11,7 @@ cap() {  # name regex skip count
   ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:$2" -s $3 -c ${4:-1} \
       -o gpurun_out/${tag}_$1 $B > gpurun_out/${tag}_$1.log 2>&1
 }
-cap fwd "FwdPersistTraits" 2
+cap fwd "FwdPersistT" 2
 cap bwd "BwdPersistTraits" 2
 cap ce "CeTraits" 0 2
 cap wgrad "GenTraits<.int.256, .bool.1, .bool.1, .bool.0, .int.0, .bool.0, .bool.0>" 2
