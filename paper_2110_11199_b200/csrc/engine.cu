@@ -138,6 +138,8 @@ Ctx::Ctx(const adpsgd_config& c) : cfg(c) {
     // ---- workspace (shared by the local learners; they are computed in turn) ----
     idx_dev = static_cast<int32_t*>(alloc(sizeof(int32_t) * B));
     X0 = alloc(TB * Ipad * es);
+    if (bf16_mode && lstm_bwd_wants_whh_t(nd, B, H))
+        for (auto& p : whh_t) p = static_cast<bf16*>(alloc(static_cast<size_t>(4) * H * H * sizeof(bf16)));
     if (bf16_mode && Ipad > 256 && Ipad <= 264) {
         X0tail = alloc(16 * TB * sizeof(bf16));
         AB_CUDA(cudaMemsetAsync(X0tail, 0, 16 * TB * sizeof(bf16), s_main));
@@ -526,6 +528,10 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
             for (int d = 0; d < nd; ++d) {
                 PL.w_hh[d] = static_cast<const bf16*>(W.at(lay.dir[l][d].w_hh));
                 PL.dc_rec[d] = dc_rec + static_cast<int64_t>(d) * B * H;
+                if (whh_t[d] && knobs().bwd_u32) {  // K-major copy for the 32-unit BPTT tiles
+                    launch_transpose_bf16(PL.w_hh[d], whh_t[d], G4, H, s);
+                    PL.w_hh_t[d] = whh_t[d];
+                }
             }
             PL.dH = dHcur; PL.lddh = ndH;
             PL.gates = static_cast<const bf16*>(gates[l]); PL.ldg = nd4H;

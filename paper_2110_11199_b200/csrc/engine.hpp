@@ -64,7 +64,8 @@ struct Ctx {
     int32_t* idx_dev = nullptr;
     int32_t* ident_idx = nullptr;
     void* X0 = nullptr;
-    void* X0tail = nullptr;  // bf16 [16 x T*B]: K-major copy of X0 columns [256, 264) (tail-column dW_ih MMA)
+    void* X0tail = nullptr;
+    bf16* whh_t[2] = {nullptr, nullptr};  // W_hh^T of the layer in BPTT (32-unit persistent BPTT tiles)  // bf16 [16 x T*B]: K-major copy of X0 columns [256, 264) (tail-column dW_ih MMA)
     int32_t* lab_step = nullptr;
     std::vector<void*> Hout;
     std::vector<void*> gates;  // gate activations i,f,g,o (activation type)

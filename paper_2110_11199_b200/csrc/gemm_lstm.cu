@@ -859,24 +859,28 @@ struct BwdPParams {
 
 // KQ = K splits per tile: KQ = 2 -> 256 x 128 pair tiles (K halves); KQ = 4 -> 256 x 256 tiles
 // (K quarters: a third less operand ingress per FLOP, three partials per owned block).
-template <int KQ>
+// UC = units each CTA finalises: 64, or 32 (H <= 512: twice the CTA pairs, half the epilogue per
+// item). UC = 32 reads B = W_hh^T (a K-major transposed copy, [H x 4H]) so 32-unit B tiles
+// stay in the 128-byte-swizzle layout.
+template <int KQ, int UC = 64>
 struct BwdPersistTraits : tc::TraitsBase, BwdEpi {
-    static constexpr int BN = 64 * KQ;  // pair tile width; each CTA finalises 64 units
+    static constexpr int BN = UC * KQ;  // pair tile width
+    static constexpr int NCHK = UC / 16;  // 16-unit chunks per finalised block
     static constexpr int EPI_WARPS = 8;
     static constexpr int EPI_SMEM = EPI_WARPS * 12 * 1024;  // BwdEpi::body_g<64, INPLACE, .., NBUF = 1>
     static constexpr int ACC_STAGES = 2;
     static constexpr bool A_MN = false;
-    static constexpr bool B_MN = true;
+    static constexpr bool B_MN = UC == 64;
     static constexpr bool STREAMK = true;
-    // TMEM past the accumulators (KQ = 2 only: 2 x 128 + 256 = 512 columns): per direction d,
-    // dc_rec at [2 BN + 64 d, +64) and the carried c at [2 BN + 128 + 64 d, +64), 64 owned units each
+    // TMEM past the accumulators (KQ = 2 only: 2 BN + 4 UC <= 512 columns): per direction d,
+    // dc_rec at [2 BN + UC d, +UC) and the carried c at [2 BN + 2 UC + UC d, +UC)
 #ifdef ADPSGD_NO_TSTATE
     static constexpr bool TSTATE = false;
 #else
     static constexpr bool TSTATE = KQ == 2;
 #endif
-    static constexpr int TMEM_EXTRA = TSTATE ? 256 : 0;
-    static constexpr int kBlock = 4 * 128 * 16;  // floats of one exported 64-unit block: [4 chunks][128 rows][16]
+    static constexpr int TMEM_EXTRA = TSTATE ? 4 * UC : 0;
+    static constexpr int kBlock = NCHK * 128 * 16;  // floats of one exported block: [chunks][128 rows][16]
     struct U {
         int mt, nt, kh, s, d;
     };
@@ -904,8 +908,8 @@ struct BwdPersistTraits : tc::TraitsBase, BwdEpi {
             r.c_tmem = u.s > 0;   // c_t = the c_{t-1} this CTA loaded one step earlier
             if (have_q) {         // tmem_q: TMEM base of this warp's lane quarter (epilogue only)
                 r.tstate = true;
-                r.tdc = tmem_q + 2 * BN + 64 * u.d;
-                r.tc_ = tmem_q + 2 * BN + 128 + 64 * u.d;
+                r.tdc = tmem_q + 2 * BN + UC * u.d;
+                r.tc_ = tmem_q + 2 * BN + 2 * UC + UC * u.d;
                 r.tdc_valid = true;
                 r.tc_valid = true;
             }
@@ -936,16 +940,20 @@ struct BwdPersistTraits : tc::TraitsBase, BwdEpi {
         const int k0 = (u.kh * p.kbh + kb) * kBK;
         ptx::tma_load_2d_2sm(sA, &g.ta, bar, k0, t_src(p, u) * p.B + u.mt * 2 * kBM + kBM * static_cast<int>(rank));
         const uint64_t keep = ptx::policy_evict_last();
+        if constexpr (UC == 64) {
 #pragma unroll
-        for (int j = 0; j < BN / 128; ++j)
-            ptx::tma_load_2d_2sm_hint(sB + j * 64 * kBK * 2, &g.tb, bar, u.nt * BN + static_cast<int>(rank) * (BN / 2) + 64 * j,
-                                      k0, keep);
+            for (int j = 0; j < BN / 128; ++j)
+                ptx::tma_load_2d_2sm_hint(sB + j * 64 * kBK * 2, &g.tb, bar, u.nt * BN + static_cast<int>(rank) * (BN / 2) + 64 * j,
+                                          k0, keep);
+        } else {  // K-major W_hh^T: BN / 2 unit rows x 64 gate columns
+            ptx::tma_load_2d_2sm_hint(sB, &g.tb, bar, k0, u.nt * BN + static_cast<int>(rank) * (BN / 2), keep);
+        }
     }
     template <class S>
     __device__ static void epi_begin2(const BwdPParams& p, int it, uint32_t rank, int q, int lane, uint8_t* st,
                                       uint64_t* ebar, S sl) {
         const U u = unit(p, blockIdx.x >> 1, it);
-        begin_g<64, true, 1>(p.g[u.d], p.H, u.mt * 2 * kBM + kBM * static_cast<int>(rank), u.nt * BN + 64 * u.kh, q, lane,
+        begin_g<UC, true, 1>(p.g[u.d], p.H, u.mt * 2 * kBM + kBM * static_cast<int>(rank), u.nt * BN + UC * u.kh, q, lane,
                              st, ebar, sl, rows(p, u));
     }
     __device__ static void epilogue_sk(const BwdPParams& p, const tc::Item& w, int cid, uint32_t rank, uint32_t tbase,
@@ -960,15 +968,15 @@ struct BwdPersistTraits : tc::TraitsBase, BwdEpi {
         auto block = [&](int c_id, int j) {
             return p.sk_scratch + ((static_cast<int64_t>(c_id * 2 + static_cast<int>(rank)) * 2 + par) * KQ + j) * kBlock;
         };
-        // 1) export the blocks the partners finalise (TMEM cols [64 j, +64) for j != kh)
+        // 1) export the blocks the partners finalise (TMEM cols [UC j, +UC) for j != kh)
         //    (p.epi_skip: diagnosis only -- 1 skips the TMEM loads, 2 skips the stores)
 #pragma unroll 1
-        for (int x = sl.sub; x < 4 * KQ; x += sl.n) {
-            const int j = x >> 2, c = x & 3;
+        for (int x = sl.sub; x < NCHK * KQ; x += sl.n) {
+            const int j = x / NCHK, c = x % NCHK;
             if (j == u.kh) continue;
             uint32_t v[16];
             if (p.epi_skip != 1) {
-                ptx::tmem_ld_32x32b_x16_(tbase + 64 * j + 16 * c, v);
+                ptx::tmem_ld_32x32b_x16_(tbase + UC * j + 16 * c, v);
                 ptx::tmem_ld_wait();
             } else {
 #pragma unroll
@@ -1000,8 +1008,8 @@ struct BwdPersistTraits : tc::TraitsBase, BwdEpi {
         for (int j = 0, n = 0; j < KQ; ++j)
             if (j != u.kh) pr[n++] = block(base + j * per, u.kh);
         auto rel = [&] { tc::release_acc_2sm(tempty_leader, lane); };
-        body_g<64, true, decltype(rel), 1>(p.g[u.d], p.H, u.mt * 2 * kBM + kBM * static_cast<int>(rank),
-                                          u.nt * BN + 64 * u.kh, tbase + 64 * u.kh, q, lane, rel, st, ebar, ephase, sl,
+        body_g<UC, true, decltype(rel), 1>(p.g[u.d], p.H, u.mt * 2 * kBM + kBM * static_cast<int>(rank),
+                                          u.nt * BN + UC * u.kh, tbase + UC * u.kh, q, lane, rel, st, ebar, ephase, sl,
                                           pr[0], true, rows(p, u, tbase - (tbase & 0xFFFFu) % (2 * BN), true), pr[1], pr[2]);
         // 4) publish: this CTA's dz block of step tn is in memory (TMA stores complete)
         if (lane == 0) {
@@ -1204,11 +1212,19 @@ bool lstm_fwd_layer_persistent(const LstmFwdLayer& L, int ndirs, int B, int H, i
     return true;
 }
 
+bool lstm_bwd_wants_whh_t(int ndirs, int B, int H) {
+    return knobs().persist_bwd && knobs().pair_mma && knobs().bwd_u32 && !knobs().bwd_kq4 && ndirs == 2 &&
+           B % (2 * kBM) == 0 && H % 128 == 0 && (B / (2 * kBM)) * (H / 128) * 2 * 2 <= num_sms() / 2;
+}
+
 bool lstm_bwd_layer_persistent(const LstmBwdLayer& L, int ndirs, int B, int H, int T, cudaStream_t s, float* sk_scratch,
                                unsigned int* sk_flags, unsigned int* dep, unsigned int* exit_ctr) {
     // 256 x 256 tiles in K quarters when H allows and the units fit, else 256 x 128 in K halves
     const int kq = (knobs().bwd_kq4 && H % 256 == 0 && (B / (2 * kBM)) * (H / 256) * 4 <= num_sms() / 2) ? 4 : 2;
-    const int m_tiles = B / (2 * kBM), n_tiles = H / (64 * kq);
+    // 32 units per CTA when 64-unit blocks would leave more than half of the pairs idle (needs W_hh^T)
+    const int uc = (kq == 2 && knobs().bwd_u32 && L.w_hh_t[0] && L.w_hh_t[1] && H % 64 == 0 &&
+                    (B / (2 * kBM)) * (H / 128) * 2 * 2 <= num_sms() / 2) ? 32 : 64;
+    const int m_tiles = B / (2 * kBM), n_tiles = H / (uc * kq);
     const int units = m_tiles * n_tiles * kq;
     if (!(knobs().persist_bwd && knobs().pair_mma && ndirs == 2 && T >= 2 && B % (2 * kBM) == 0 && H % 128 == 0 &&
           units <= num_sms() / 2 && sk_scratch && sk_flags && dep && exit_ctr))
@@ -1220,7 +1236,8 @@ bool lstm_bwd_layer_persistent(const LstmBwdLayer& L, int ndirs, int B, int H, i
         BwdGroup& g = p.g[d];
         const int64_t TB = static_cast<int64_t>(T) * B;
         make_map_box(&g.ta, L.dZ + d * G4, G4, TB, L.ld_dz, kBM);
-        make_map_box(&g.tb, L.w_hh[d], H, G4, H, 64);
+        if (uc == 32) make_map_box(&g.tb, L.w_hh_t[d], G4, H, G4, uc * kq / 2);  // K-major W_hh^T [H x 4H]
+        else make_map_box(&g.tb, L.w_hh[d], H, G4, H, 64);
         make_map_gen(&g.m_dH, L.dH + d * H, true, H, TB, L.lddh, 16, 32, CU_TENSOR_MAP_SWIZZLE_64B);
         make_map_gen(&g.m_dc, L.dc_rec[d], true, H, B, H, 16, 32, CU_TENSOR_MAP_SWIZZLE_64B);
         make_map_gen(&g.m_c, L.c + d * H, true, H, TB, L.ldc, 16, 32, CU_TENSOR_MAP_SWIZZLE_64B);
@@ -1247,6 +1264,7 @@ bool lstm_bwd_layer_persistent(const LstmBwdLayer& L, int ndirs, int B, int H, i
         tc::launch_tc(k, p, 2 * units, tc::threads_of<Tr>(), tc::ShapeOf2<Tr>::SMEM, true, s);
     };
     if (kq == 4) launch(BwdPersistTraits<4>{});
+    else if (uc == 32) launch(BwdPersistTraits<2, 32>{});
     else launch(BwdPersistTraits<2>{});
     count_launch();
     return true;

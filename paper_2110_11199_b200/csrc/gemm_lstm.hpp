@@ -54,11 +54,14 @@ bool lstm_fwd_layer_persistent(const LstmFwdLayer& L, int ndirs, int B, int H, i
 struct LstmBwdLayer {
     bf16* dZ; int64_t ld_dz;          // [T*B x 2*4H]: dz_{T-1} (dir 0) / dz_0 (dir 1) given, the rest produced
     const bf16* w_hh[2];              // [4H x H] per direction
+    const bf16* w_hh_t[2] = {nullptr, nullptr};  // optional [H x 4H] transposes (32-unit BPTT tiles)
     const float* dH; int64_t lddh;    // [T*B x 2H]
     float* dc_rec[2];                 // [B x H] per direction (carries the first cell backward's dc)
     const bf16* gates; int64_t ldg;   // [T*B x 2*4H]
     const float* c; int64_t ldc;      // [T*B x 2H]
 };
+// true when the persistent BPTT will take 32-unit tiles and so wants LstmBwdLayer::w_hh_t
+bool lstm_bwd_wants_whh_t(int ndirs, int B, int H);
 bool lstm_bwd_layer_persistent(const LstmBwdLayer& L, int ndirs, int B, int H, int T, cudaStream_t s, float* sk_scratch,
                                unsigned int* sk_flags, unsigned int* dep, unsigned int* exit_ctr);
 

@@ -685,6 +685,27 @@ void launch_delay(uint64_t ns, cudaStream_t s) {
     count_launch();
 }
 
+// out[c * rows + r] = in[r * cols + c] (bf16, 32 x 32 smem tiles)
+__global__ void transpose_bf16_kernel(const bf16* __restrict__ in, bf16* __restrict__ out, int rows, int cols) {
+    __shared__ bf16 tile[32][33];
+    const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int r = r0 + i, c = c0 + threadIdx.x;
+        if (r < rows && c < cols) tile[i][threadIdx.x] = in[static_cast<int64_t>(r) * cols + c];
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int c = c0 + i, r = r0 + threadIdx.x;
+        if (r < rows && c < cols) out[static_cast<int64_t>(c) * rows + r] = tile[threadIdx.x][i];
+    }
+}
+
+void launch_transpose_bf16(const bf16* in, bf16* out, int rows, int cols, cudaStream_t s) {
+    ProfScope ps_(s, PROF_REDUCE, 0, 4.0 * rows * cols);
+    transpose_bf16_kernel<<<dim3((cols + 31) / 32, (rows + 31) / 32), dim3(32, 8), 0, s>>>(in, out, rows, cols);
+    count_launch();
+}
+
 bool launch_cell_bwd_first2(const float* const dH[2], const bf16* const gates[2], const float* const c[2],
                             const float* const c_prev[2], bf16* const dz[2], float* const dc_rec[2], int lddh, int ldg,
                             int ldc, int lddz, int B, int H, cudaStream_t s) {

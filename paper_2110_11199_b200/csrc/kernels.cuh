@@ -21,6 +21,9 @@ void launch_cell_bwd(const float* dH, int lddh, const float* dh_rec, float* dc_r
                      int ldg, const float* c, const float* c_prev, int ldc, AT* dz, int lddz, int B, int H,
                      cudaStream_t s);
 
+// out [cols x rows] = in [rows x cols]^T (bf16)
+void launch_transpose_bf16(const bf16* in, bf16* out, int rows, int cols, cudaStream_t s);
+
 // First BPTT cell backward (no recurrent term) of both directions in one vectorised launch;
 // false (nothing launched) when the layout does not allow 16-byte accesses.
 bool launch_cell_bwd_first2(const float* const dH[2], const bf16* const gates[2], const float* const c[2],
