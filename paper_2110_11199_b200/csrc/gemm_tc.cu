@@ -709,8 +709,12 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
     const int n_tail0 = g.n_main > 0 ? (g.n_main / 256) * 256 : 0;
     const bool xb = knobs().xtra && g.b_tail && g.extra && pair && !g.c_bf16 && amn && bmn && g.nseg == 1 &&
                     g.n_main == g.N - 1 && n_tail0 >= 256 && g.N - n_tail0 <= 8;
+    // ... or when dropping the bias tile brings the weight gradient within one-wave split-K reach
+    // (tiles <= pairs / 2: every pair busy instead of one tile per pair)
+    const int tiles_plain = m_tiles * ((g.N + bn0 - 1) / bn0), tiles_xtra = m_tiles * (g.n_main / 256);
+    const bool xtra_splits = knobs().streamk && tiles_xtra * 2 <= npairs && tiles_plain * 2 > npairs;
     const bool xtra = xb || (knobs().xtra && g.extra && pair && bn0 == 256 && !g.c_bf16 && amn && bmn && g.n_main == g.N - 1 &&
-                             g.n_main % 256 == 0 && (rounds_xtra < rounds_plain || knobs().force_ext));
+                             g.n_main % 256 == 0 && (rounds_xtra < rounds_plain || xtra_splits || knobs().force_ext));
     const int xmode = xb ? 2 : (xtra ? 1 : 0);
     const int n_eff = xb ? n_tail0 : (xtra ? g.n_main : g.N);
     int kbt = 0;
