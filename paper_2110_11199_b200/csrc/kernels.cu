@@ -41,6 +41,45 @@ __global__ void gather_kernel(const float* __restrict__ feats, const int32_t* __
     }
 }
 
+// 4 columns per thread (I % 4 == 0, ldx % 4 == 0): one 16-byte feature load, one 8-byte bf16 /
+// 16-byte fp32 store; the group holding column I also writes the ones column and the zero pad.
+template <typename AT>
+__global__ void gather4_kernel(const float* __restrict__ feats, const int32_t* __restrict__ labels,
+                               const int32_t* __restrict__ idx, int B, int T, int I, int ldx, AT* __restrict__ X,
+                               int32_t* __restrict__ lab, int ones_col, AT* __restrict__ tail, int tail_n0) {
+    const int g4 = ldx / 4;
+    const int64_t total = static_cast<int64_t>(T) * B * g4;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int i0 = static_cast<int>(e % g4) * 4;
+        const int64_t r = e / g4;  // r = t*B + b
+        const int b = static_cast<int>(r % B), t = static_cast<int>(r / B);
+        const int64_t n = idx[b];
+        float v[4];
+        if (i0 + 4 <= I) {
+            const float4 f = __ldg(reinterpret_cast<const float4*>(feats + (n * T + t) * I + i0));
+            v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int i = i0 + k;
+                v[k] = i < I ? feats[(n * T + t) * I + i] : ((ones_col && i == I) ? 1.f : 0.f);
+            }
+        }
+        AT* dst = X + r * ldx + i0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) dst[k] = from_f<AT>(v[k]);
+        if (tail && i0 + 4 > tail_n0 && i0 < tail_n0 + 8) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int i = i0 + k;
+                if (i >= tail_n0 && i < tail_n0 + 8) tail[static_cast<int64_t>(i - tail_n0) * T * B + r] = from_f<AT>(v[k]);
+            }
+        }
+        if (i0 == 0) lab[r] = labels[n * T + t];
+    }
+}
+
 // ---- LSTM cell ----
 template <typename AT>
 __global__ void cell_fwd_kernel(const float* __restrict__ z, int ldz, const float* __restrict__ c_prev, int ldc,
@@ -507,7 +546,12 @@ void launch_gather(const float* feats, const int32_t* labels, const int32_t* idx
                    int32_t* lab, cudaStream_t s, bool ones_col, AT* tail, int tail_n0) {
     ProfScope ps_(s, PROF_GATHER, 0, (double)T * B * ldx * (sizeof(AT) + 4.0) + (double)T * B * 8);
     const int64_t total = static_cast<int64_t>(T) * B * ldx;
-    gather_kernel<AT><<<grid_for(total), 256, 0, s>>>(feats, labels, idx, B, T, I, ldx, X, lab, ones_col ? 1 : 0, tail, tail_n0);
+    if (I % 4 == 0 && ldx % 4 == 0)
+        gather4_kernel<AT><<<grid_for(total / 4), 256, 0, s>>>(feats, labels, idx, B, T, I, ldx, X, lab, ones_col ? 1 : 0,
+                                                               tail, tail_n0);
+    else
+        gather_kernel<AT><<<grid_for(total), 256, 0, s>>>(feats, labels, idx, B, T, I, ldx, X, lab, ones_col ? 1 : 0, tail,
+                                                          tail_n0);
     count_launch();
 }
 
