@@ -285,7 +285,12 @@ __global__ void colsum_final_kernel(const float* __restrict__ part, int chunks, 
 __global__ void sum_kernel(const float* __restrict__ x, int n, float scale, float* __restrict__ out) {
     __shared__ float sh[32];
     float s = 0.f;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) s += x[i];
+    const int n4 = (reinterpret_cast<uintptr_t>(x) & 15) == 0 ? n / 4 : 0;  // 16-byte loads, fixed order
+    for (int i = threadIdx.x; i < n4; i += blockDim.x) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(x) + i);
+        s += (v.x + v.y) + (v.z + v.w);
+    }
+    for (int i = 4 * n4 + threadIdx.x; i < n; i += blockDim.x) s += x[i];
     s = block_reduce(s, false, sh);
     if (threadIdx.x == 0) out[0] = s * scale;
 }
