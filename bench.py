@@ -219,7 +219,7 @@ def run_reference(a):
     m = model_desc(a)
     line = {
         "impl": "reference", "metric": f"frames/sec ({m.layers}x{m.hidden} BLSTM ADPSGD learner step)", "value": val,
-        "unit": "frames/s", "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
+        "unit": "frames/s", "n_gpus": a.gpus, "steps": len(times), "steps_requested": a.steps, "warmup": a.warmup,
         "ms_per_step": 1000.0 * tot / len(times), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "configs[1]/[3] BLSTM learner step", "model": f"{m.layers}x{m.hidden}/dir BLSTM",
@@ -227,7 +227,7 @@ def run_reference(a):
         "cpu_baseline": {"value": val, "unit": "frames/s", "cores": threads, "kind": "port",
                          "sample": f"{segs} segments x 21 frames per step (one per thread), fp64 oracle "
                                    f"(reference cannot build: Eigen absent); {len(times)} timed steps "
-                                   f"of {a.steps} requested (150 s budget)"},
+                                   f"of {a.steps} requested (150 s budget; 'steps' is the count timed)"},
         "e2e": {"value": val, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -258,8 +258,10 @@ def run_ours(a):
         g.barrier()
         torch.cuda.synchronize()
 
+    _lib.kernel_variants(reset=True)
     for _ in range(a.warmup):
         g.step(lr)
+    variants = _lib.kernel_variants(reset=True)
     barrier()
     dev = local
     # ---- timed region (the value): K steps, CUDA events on the library stream ----
@@ -318,6 +320,19 @@ def run_ours(a):
     e2e_s = P.max_over_ranks(time.perf_counter() - t0)
     barrier()
     e2e_val = world * a.batch * T_UNROLL * e2e_steps / e2e_s
+
+    # ---- gossip path (BASELINE metric, second half): the fused FM/RM mix kernel at this model size
+    # reading the ring neighbours' weights -- over NVLink P2P when N >= 3 (IPC-mapped peers), local
+    # stand-in buffers at N < 3 (HBM-only figure) -- and a copy-engine pull of both neighbours ----
+    if world >= 3:
+        left, right = (rank + world - 1) % world, (rank + 1) % world
+    else:
+        left = right = -1
+    barrier()
+    gp = g.gossip_probe(left, right, reps=5)
+    barrier()
+    gp["mix_ms"] = P.max_over_ranks(gp["mix_ms"])
+    gp["copy_ms"] = P.max_over_ranks(gp["copy_ms"])
 
     if rank != 0:
         return
@@ -380,6 +395,18 @@ def run_ours(a):
                      "profiled_ms_per_step": prof_step_ms, "by_gemm": gemm_detail,
                      "step_tflops": frames * m.train_flops_per_frame() / (tot_ms / 1000.0) / 1e12 / world},
         "mix_update": {"ms_per_step": mix["ms"] / a.steps, "achieved_gbs": mix_gbs, "peak_hbm_gbs": pk.get("hbm_gbs")},
+        "gossip": {
+            "path": "NVLink P2P peer reads (CUDA IPC), ring neighbours" if world >= 3 else
+                    "local HBM stand-ins (N < 3: no ring neighbours to pull)",
+            "mix_kernel_ms": gp["mix_ms"], "mix_kernel_hbm_gbs": 22.0 * g.D / (gp["mix_ms"] * 1e6),
+            "mix_kernel_bytes_per_param": 22,
+            "nvlink_ingress_gbs_per_gpu": (8.0 * g.D / (gp["mix_ms"] * 1e6)) if world >= 3 else None,
+            "copy_engine_pull_gbs": 8.0 * g.D / (gp["copy_ms"] * 1e6),
+            "peak_hbm_gbs": pk.get("hbm_gbs"),
+            "nvlink_spec_gbs_per_dir": 900.0,
+            "frac_of_nvlink_spec": (8.0 * g.D / (gp["mix_ms"] * 1e6)) / 900.0 if world >= 3 else None,
+        },
+        "kernel_variants": variants,
         "kernel_ms_per_step": kernel_ms,
         "gpu_launches": launches,
         "cpu_baseline": cpu,

@@ -173,6 +173,13 @@ int adpsgd_import_ipc(adpsgd_ctx* ctx, int32_t rank, int32_t rank_first_learner,
 /* Gossip transport for FM/RM: 0 = direct peer loads inside the fused mix kernel,
  * 1 = copy-engine prefetch overlapped with compute, 2 = NCCL send/recv (baseline). */
 int adpsgd_set_gossip_mode(adpsgd_ctx* ctx, int32_t mode);
+/* Gossip bandwidth probe (bench): `reps` timed runs (CUDA events) of the fused FM/RM mix kernel reading
+ * global learners `left` and `right`'s current weights -- local, or peers mapped over NVLink P2P --
+ * and of a copy-engine pull of both, into scratch buffers (learner state untouched). left = right = -1:
+ * two local stand-in buffers (the N = 1, HBM-only figure). out[0] = mix ms per call, out[1] = neighbour
+ * bytes per call that crossed NVLink, out[2] = copy ms per call (both neighbours), out[3] = HBM +
+ * NVLink bytes the mix kernel moves per call. */
+int adpsgd_gossip_probe(adpsgd_ctx* ctx, int32_t left, int32_t right, int32_t reps, double* out4);
 int adpsgd_barrier(adpsgd_ctx* ctx);
 
 /* ---- live kernel profiling (CUDA events around every library launch) ---- */
@@ -184,6 +191,11 @@ int adpsgd_profile_enable(int32_t on);
 /* Synchronises the device; returns per-class device ms, algorithmic FLOPs, algorithmic
  * bytes and launch counts accumulated since the last read, then clears them. */
 int adpsgd_profile_read(double* ms, double* flops, double* bytes, int64_t* launches, int32_t ncat);
+
+/* Kernel variants selected so far (tcgen05 template instantiations, host-side record at eager launch or
+ * graph capture): "name=count;..." written to out (NUL-terminated, truncated to n bytes); reset != 0
+ * clears the record. Lets tests assert which kernel a shape exercised. */
+int adpsgd_kernel_variants(char* out, size_t n, int32_t reset);
 
 /* Debug: device timeline of the CTA-pair tensor-core kernels (160 CTAs x 32 globaltimer stamps). */
 int adpsgd_debug_trace(int32_t enable, uint64_t* out, int32_t n);

@@ -201,6 +201,8 @@ class OracleEngine:
         et = np.zeros(target, dtype=np.float64)
         n = lib().or_coupled_async(self._h, strategy, _p(d, C.c_double), target, ipe, _p(lrs, C.c_double),
                                    len(lrs), _p(ev, C.c_int32), _p(et, C.c_double))
+        if n < 0:
+            raise ValueError(f"coupled_async failed with status {-n} (lr table shorter than the rounds run?)")
         return ev[:n], et[:n]
 
     def step_injected(self, strategy: int, lr: float, k: int, grads, generic_mix: int = 2,

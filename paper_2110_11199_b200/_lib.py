@@ -72,8 +72,10 @@ _SIGS = {
     "adpsgd_import_ipc": (C.c_int, [C.c_void_p, i32, i32, i32, C.c_void_p, i64]),
     "adpsgd_set_gossip_mode": (C.c_int, [C.c_void_p, i32]),
     "adpsgd_barrier": (C.c_int, [C.c_void_p]),
+    "adpsgd_gossip_probe": (C.c_int, [C.c_void_p, i32, i32, i32, P(C.c_double)]),
     "adpsgd_profile_enable": (C.c_int, [i32]),
     "adpsgd_profile_read": (C.c_int, [P(C.c_double), P(C.c_double), P(C.c_double), P(i64), i32]),
+    "adpsgd_kernel_variants": (C.c_int, [C.c_char_p, C.c_size_t, i32]),
     "adpsgd_debug_trace": (C.c_int, [i32, C.c_void_p, i32]),
     "adpsgd_gemm": (C.c_int, [i32, i32, i32, i32, C.c_void_p, i64, i32, C.c_void_p, i64, i32, C.c_void_p, i64,
                               i32, C.c_float, i32, C.c_void_p, C.c_void_p]),
@@ -131,3 +133,16 @@ def profile_read() -> dict:
     la = (C.c_int64 * n)()
     check(lib().adpsgd_profile_read(ms, fl, by, la, n))
     return {c: {"ms": ms[i], "flops": fl[i], "bytes": by[i], "launches": la[i]} for i, c in enumerate(PROF_CATS)}
+
+
+def kernel_variants(reset: bool = True) -> dict:
+    """Kernel variants (tcgen05 template instantiations) selected since the last reset, with the
+    number of times each was chosen (eager launches and graph captures; replays are not counted)."""
+    buf = C.create_string_buffer(1 << 16)
+    check(lib().adpsgd_kernel_variants(buf, len(buf), int(reset)))
+    out = {}
+    for item in buf.value.decode().split(";"):
+        if item:
+            name, _, n = item.rpartition("=")
+            out[name] = int(n)
+    return out

@@ -120,6 +120,9 @@ def coupled_run(profile: ClusterProfile, cfg: StrategyConfig, group: LearnerGrou
         raise ConfigError("coupled async runs FM or RM (synchronous strategies use run_training)")
     ipe = iterations_per_epoch(cfg, train_count)
     dur = [max(profile.effective_compute(l), profile.comm_pairwise) for l in range(cfg.learners)]
-    lrs = [lr_at(cfg.lr, e) for e in range(cfg.epochs)]
-    ev, et = async_run(group, cfg.strategy, dur, cfg.epochs * ipe * cfg.learners, ipe, lrs)
+    target = cfg.epochs * ipe * cfg.learners
+    # lr of a learner's own round r is lr_at(cfg.lr, r / ipe) (chronos.cpp:216); a fast learner can
+    # run up to `target` rounds, past cfg.epochs epochs, so the table covers every reachable epoch
+    lrs = [lr_at(cfg.lr, e) for e in range((target - 1) // ipe + 1)]
+    ev, et = async_run(group, cfg.strategy, dur, target, ipe, lrs)
     return ev, et, float(et[-1]) if len(et) else 0.0

@@ -311,6 +311,13 @@ int adpsgd_set_gossip_mode(adpsgd_ctx* ctx, int32_t mode) {
     });
 }
 
+int adpsgd_gossip_probe(adpsgd_ctx* ctx, int32_t left, int32_t right, int32_t reps, double* out4) {
+    return guard([&] {
+        AB_CHECK(out4 && reps >= 1, ADPSGD_E_INVALID_STATE, "gossip probe: out4 and reps >= 1 required");
+        C_(ctx).gossip_probe(left, right, reps, out4);
+    });
+}
+
 int adpsgd_barrier(adpsgd_ctx* ctx) {
     return guard([&] {
         Ctx& c = C_(ctx);
@@ -322,6 +329,17 @@ int adpsgd_barrier(adpsgd_ctx* ctx) {
 
 int adpsgd_profile_enable(int32_t on) {
     return guard([&] { g_prof_enabled = on != 0; });
+}
+
+int adpsgd_kernel_variants(char* out, size_t n, int32_t reset) {
+    return guard([&] {
+        const std::string v = variants_string(reset != 0);
+        if (out && n) {
+            const size_t m = v.size() < n - 1 ? v.size() : n - 1;
+            std::memcpy(out, v.data(), m);
+            out[m] = 0;
+        }
+    });
 }
 
 int adpsgd_profile_read(double* ms, double* flops, double* bytes, int64_t* launches, int32_t ncat) {

@@ -175,8 +175,8 @@ Ctx::Ctx(const adpsgd_config& c) : cfg(c) {
             sk_scratch = static_cast<float*>(alloc(static_cast<size_t>(slots) * 4 * 128 * 128 * sizeof(float)));
             sk_flags = static_cast<unsigned int*>(alloc(static_cast<size_t>(slots) * sizeof(unsigned int)));
             AB_CUDA(cudaMemsetAsync(sk_flags, 0, static_cast<size_t>(slots) * sizeof(unsigned int), s_main));
-            pb_sync = static_cast<unsigned int*>(alloc(520 * sizeof(unsigned int)));
-            AB_CUDA(cudaMemsetAsync(pb_sync, 0, 520 * sizeof(unsigned int), s_main));  // [384,512) fwd step counters, [513] fwd exit
+            pb_sync = static_cast<unsigned int*>(alloc(kPbSyncWords * sizeof(unsigned int)));
+            AB_CUDA(cudaMemsetAsync(pb_sync, 0, kPbSyncWords * sizeof(unsigned int), s_main));  // layout: gemm_lstm.hpp
         }
     }
     if (!bf16_mode || knobs().unfused_ce) logits = static_cast<float*>(alloc(TB * lay.C * sizeof(float)));
@@ -298,7 +298,7 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
             FL.gates = static_cast<bf16*>(gates[l]); FL.ldg = nd4H;
             FL.c = cst[l]; FL.ldc = ndH;
             FL.h = static_cast<bf16*>(Hout[l]); FL.ldh = ldH;
-            const bool persistent = pb_sync && lstm_fwd_layer_persistent(FL, nd, B, H, T, s, pb_sync + 384, pb_sync + 513);
+            const bool persistent = pb_sync && lstm_fwd_layer_persistent(FL, nd, B, H, T, s, pb_sync + 512 - kFwdDepSlots, pb_sync + 513);
             for (int st = 0; !persistent && st < T; ++st) {
                 LstmFwdDir dirs[2];
                 for (int d = 0; d < nd; ++d) {
@@ -537,7 +537,7 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
             PL.gates = static_cast<const bf16*>(gates[l]); PL.ldg = nd4H;
             PL.c = cst[l]; PL.ldc = ndH;
             const bool persistent = pb_sync && sk_scratch &&
-                                    lstm_bwd_layer_persistent(PL, nd, B, H, T, s, sk_scratch, pb_sync, pb_sync + 256, pb_sync + 512);
+                                    lstm_bwd_layer_persistent(PL, nd, B, H, T, s, sk_scratch, pb_sync, pb_sync + 512 - kBwdDepSlots, pb_sync + 512);
             for (int st = 0; !persistent && st + 1 < T; ++st) {
                 LstmBwdDir dirs[2];
                 for (int d = 0; d < nd; ++d) {
@@ -809,7 +809,12 @@ int64_t Ctx::async_run(int strategy, const double* durations, int64_t target, in
         q.pop();
         Learner& ln = learners[l];
         const int64_t r = round[l];
-        const int ep = std::min<int64_t>(r / ipe, n_epochs - 1);
+        // lr_at(cfg.lr, r / ipe) of the learner's own round (chronos.cpp:216): no clamp -- a fast
+        // learner can run past cfg.epochs x ipe rounds, so the caller sizes the table for `target`
+        const int64_t ep = r / ipe;
+        AB_CHECK(ep < n_epochs, ADPSGD_E_CONFIG,
+                 "lr table covers " + std::to_string(n_epochs) + " epochs, round " + std::to_string(r) + " needs epoch " +
+                     std::to_string(ep));
         const float lr = static_cast<float>(lr_per_epoch[ep]);
         AB_CUDA(cudaStreamSynchronize(s));  // pinned sampling slot reuse
         sample_indices(ln, l);
@@ -1052,7 +1057,7 @@ void Ctx::step(double lr, const int32_t* taus, float* loss_out, const float* hos
     // D1D: start the weight allreduce on the comm stream before the gradient compute
     if (strategy == ADPSGD_D1D && comm && comm->world > 1 && !comm->ipc_only) comm->start_weight_sum(*this, s);
     // FM / RM, gossip mode 1: the neighbours' w_k travel by copy engine while this learner computes
-    if ((strategy == ADPSGD_FM || strategy == ADPSGD_RM) && comm && comm->world > 1 && comm->gossip_mode == 1 && !injected) {
+    if ((strategy == ADPSGD_FM || strategy == ADPSGD_RM) && comm && comm->world > 1 && comm->gossip_mode == 1) {
         int left, right;
         neighbours(strategy, learners[0].gid, &left, &right);
         comm->prefetch_neighbours(*this, weight_ptr(left, static_cast<int>(k & 1)), weight_ptr(right, static_cast<int>(k & 1)), s);
@@ -1137,17 +1142,19 @@ double Ctx::evaluate(const double* w, const int32_t* idx, int M, double* g_out) 
     AB_CUDA(cudaSetDevice(cfg.device));
     cudaStream_t s = s_main;
     Learner& ln = learners[0];
-    // evaluate at w in the learner's spare buffer (w[nxt]); the shadow is restored after
-    const int nxt = static_cast<int>((k & 1) ^ 1);
+    // evaluate at w in a private scratch buffer (w[nxt] is exported over CUDA IPC: a peer may still
+    // be reading it); the learner's bf16 shadow is restored after
+    if (!scratch_w) scratch_w = static_cast<float*>(alloc(D * sizeof(float)));
     std::vector<float> wf(w, w + D);
-    AB_CUDA(cudaMemcpyAsync(ln.w[nxt], wf.data(), D * sizeof(float), cudaMemcpyHostToDevice, s));
-    refresh_shadow(ln, ln.w[nxt], s);
+    AB_CUDA(cudaMemcpyAsync(scratch_w, wf.data(), D * sizeof(float), cudaMemcpyHostToDevice, s));
+    AB_CUDA(cudaStreamSynchronize(s));  // wf is pageable and goes out of scope
+    refresh_shadow(ln, scratch_w, s);
     double result = 0.0;
     if (g_out) {
         AB_CUDA(cudaMemcpyAsync(idx_dev, idx, sizeof(int32_t) * B, cudaMemcpyHostToDevice, s));
         gather_batch(feats, labels, idx_dev, s);
         float* gtmp = static_cast<float*>(alloc_scratch_grad());
-        forward_backward(ln, ln.w[nxt], gtmp, loss_dev + 63, s, true);
+        forward_backward(ln, scratch_w, gtmp, loss_dev + 63, s, true);
         std::vector<float> gh(D);
         float lh = 0;
         AB_CUDA(cudaMemcpyAsync(gh.data(), gtmp, D * sizeof(float), cudaMemcpyDeviceToHost, s));
@@ -1164,7 +1171,7 @@ double Ctx::evaluate(const double* w, const int32_t* idx, int M, double* g_out) 
             for (int b = 0; b < B; ++b) chunk[b] = idx[start + (b < valid ? b : 0)];
             AB_CUDA(cudaMemcpyAsync(idx_dev, chunk.data(), sizeof(int32_t) * B, cudaMemcpyHostToDevice, s));
             gather_batch(feats, labels, idx_dev, s);
-            forward_backward(ln, ln.w[nxt], nullptr, loss_dev + 63, s, false);
+            forward_backward(ln, scratch_w, nullptr, loss_dev + 63, s, false);
             launch_sum_masked(row_loss, T, B, valid, loss_dev + 62, s);
             float part = 0;
             AB_CUDA(cudaMemcpyAsync(&part, loss_dev + 62, sizeof(float), cudaMemcpyDeviceToHost, s));
@@ -1236,6 +1243,47 @@ double Ctx::consensus_distance() {
     double lam = 0;
     for (int p = 0; p < L; ++p) lam = std::max(lam, A[p * L + p]);
     return std::sqrt(std::max(0.0, lam));
+}
+
+// Bandwidth of the gossip data path at this context's model size: the fused mix kernel (22 B per
+// parameter: w, w_L, w_R, g read, w' written fp32, the bf16 shadow) and the copy-engine pull of
+// both neighbours, each timed over `reps` calls with CUDA events on s_main. Scratch outputs only.
+void Ctx::gossip_probe(int left, int right, int reps, double* out) {
+    AB_CUDA(cudaSetDevice(cfg.device));
+    cudaStream_t s = s_main;
+    AB_CUDA(cudaStreamSynchronize(s));
+    if (!probe_buf[0]) {
+        for (auto& p : probe_buf) p = static_cast<float*>(alloc(D * sizeof(float)));
+        probe_shadow = static_cast<bf16*>(alloc(D * sizeof(bf16)));
+        AB_CUDA(cudaMemsetAsync(probe_buf[0], 0, D * sizeof(float), s));
+    }
+    if (!scratch_w) scratch_w = static_cast<float*>(alloc(D * sizeof(float)));
+    const int cur = static_cast<int>(k & 1);
+    const Learner& ln = learners[0];
+    // stand-ins at N = 1: the learner's spare weight buffer and its gradient buffer (distinct
+    // 4 D-byte streams, so nothing is served from L2)
+    const float* wl = left >= 0 ? weight_ptr(left, cur) : ln.w[cur ^ 1];
+    const float* wr = right >= 0 ? weight_ptr(right, cur) : probe_buf[0];
+    const double nv = (left >= 0 && !is_local(left) ? 4.0 * D : 0.0) + (right >= 0 && !is_local(right) ? 4.0 * D : 0.0);
+    launch_mix3(D, ln.w[cur], wl, wr, ln.g, 0.0f, scratch_w, probe_shadow, s);  // warm
+    AB_CUDA(cudaEventRecord(ev0, s));
+    for (int r = 0; r < reps; ++r) launch_mix3(D, ln.w[cur], wl, wr, ln.g, 0.0f, scratch_w, probe_shadow, s);
+    AB_CUDA(cudaEventRecord(ev1, s));
+    AB_CUDA(cudaStreamSynchronize(s));
+    float ms = 0;
+    AB_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+    out[0] = ms / reps;
+    out[1] = nv;
+    AB_CUDA(cudaEventRecord(ev0, s));
+    for (int r = 0; r < reps; ++r) {
+        AB_CUDA(cudaMemcpyAsync(scratch_w, wl, D * sizeof(float), cudaMemcpyDeviceToDevice, s));
+        AB_CUDA(cudaMemcpyAsync(probe_buf[1], wr, D * sizeof(float), cudaMemcpyDeviceToDevice, s));
+    }
+    AB_CUDA(cudaEventRecord(ev1, s));
+    AB_CUDA(cudaStreamSynchronize(s));
+    AB_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+    out[2] = ms / reps;
+    out[3] = 22.0 * D;
 }
 
 void* Ctx::alloc_scratch_grad() {

@@ -64,8 +64,8 @@ struct Ctx {
     int32_t* idx_dev = nullptr;
     int32_t* ident_idx = nullptr;
     void* X0 = nullptr;
-    void* X0tail = nullptr;
-    bf16* whh_t[2] = {nullptr, nullptr};  // W_hh^T of the layer in BPTT (32-unit persistent BPTT tiles)  // bf16 [16 x T*B]: K-major copy of X0 columns [256, 264) (tail-column dW_ih MMA)
+    void* X0tail = nullptr;  // bf16 [16 x T*B]: K-major copy of X0 columns [256, 264) (tail-column dW_ih MMA)
+    bf16* whh_t[2] = {nullptr, nullptr};  // W_hh^T of the layer in BPTT (32-unit persistent BPTT tiles)
     int32_t* lab_step = nullptr;
     std::vector<void*> Hout;
     std::vector<void*> gates;  // gate activations i,f,g,o (activation type)
@@ -78,7 +78,7 @@ struct Ctx {
     float* ce_lse = nullptr;
     float* sk_scratch = nullptr;      // split-K BPTT partial exchange (gemm_lstm.cu)
     unsigned int* sk_flags = nullptr;
-    unsigned int* pb_sync = nullptr;   // persistent BPTT: [0,256) exchange epochs, [256,512) step counters, [512] exit
+    unsigned int* pb_sync = nullptr;   // persistent recurrent kernels' counters (layout: gemm_lstm.hpp kPbSyncWords)
     GemmWorkspace gemm_ws;             // stream-K scratch of the generic tcgen05 GEMMs
     void* dlogits = nullptr;
     float* row_loss = nullptr;
@@ -91,6 +91,7 @@ struct Ctx {
     float* loss_dev = nullptr;
     float* scratch_f = nullptr;
     void* scratch_grad = nullptr;
+    float* scratch_w = nullptr;  // evaluate() / gradient() probe weights (never IPC-exported)
     float* stage_feats = nullptr;
     int32_t* stage_labels = nullptr;
     // host-batch prefetch (one local learner): two staging slots filled on s_copy while the
@@ -165,6 +166,9 @@ struct Ctx {
     void step(double lr, const int32_t* taus, float* loss_out, const float* host_feats, const int32_t* host_labels,
               const double* injected);
     double gradient(const double* w, const int32_t* idx, int M, double* g_out);
+    void gossip_probe(int left, int right, int reps, double* out4);
+    float* probe_buf[2] = {nullptr, nullptr};
+    bf16* probe_shadow = nullptr;
 };
 
 void set_last_error(const std::string& s);

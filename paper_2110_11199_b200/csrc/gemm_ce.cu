@@ -245,6 +245,7 @@ template <class Traits, class Params>
 void launch_any(const Params& p, int tiles, bool pair, cudaStream_t s) {
     if (pair) {
         auto k = tc::persistent_kernel_2cta<Traits, Params>;
+        note_kernel<cta_pair<Traits>>();
         static bool attr = false;
         constexpr int SM = tc::ShapeOf2<Traits>::SMEM;
         if (!attr) {
@@ -255,6 +256,7 @@ void launch_any(const Params& p, int tiles, bool pair, cudaStream_t s) {
         tc::launch_tc(k, p, 2 * pairs, tc::threads_of<Traits>(), SM, true, s);
     } else {
         auto k = tc::persistent_kernel<Traits, Params>;
+        note_kernel<cta_single<Traits>>();
         static bool attr = false;
         constexpr int SM = tc::Shape<Traits::BN, Traits::EPI_SMEM>::SMEM;
         if (!attr) {
@@ -339,7 +341,9 @@ void ce_forward_backward(const CeArgs& a, cudaStream_t s) {
     {
         p.mode = 1;
         p.trace = trace_take();
-        ProfScope ps_(s, PROF_GEMM_OUT, gemm_flops, in_bytes + static_cast<double>(a.M) * a.N * 2);
+        // pass 2 recomputes the logits tile to write dlogits: time counted, FLOPs not (the
+        // algorithmic output-layer work is the pass-1 GEMM plus dY / dW_out)
+        ProfScope ps_(s, PROF_GEMM_OUT, 0.0, in_bytes + static_cast<double>(a.M) * a.N * 2);
         launch_any<CeTraits>(p, tiles, pair, s);
     }
 }

@@ -1036,6 +1036,7 @@ struct BwdPersistTraits : tc::TraitsBase, BwdEpi {
 template <class Traits, class Params>
 void launch_persistent(const Params& p, int tiles, cudaStream_t s) {
     auto k = tc::persistent_kernel<Traits, Params>;
+    note_kernel<cta_single<Traits>>();
     static bool attr = false;
     if (!attr) {
         AB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::Shape<Traits::BN, Traits::EPI_SMEM>::SMEM));
@@ -1050,6 +1051,7 @@ void launch_persistent(const Params& p, int tiles, cudaStream_t s) {
 template <class Traits, class Params>
 void launch_pair(const Params& p, int pair_tiles, cudaStream_t s) {
     auto k = tc::persistent_kernel_2cta<Traits, Params>;
+    note_kernel<cta_pair<Traits>>();
     static bool attr = false;
     if (!attr) {
         AB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::ShapeOf2<Traits>::SMEM));
@@ -1170,7 +1172,7 @@ bool lstm_fwd_layer_persistent(const LstmFwdLayer& L, int ndirs, int B, int H, i
     const int n_tiles = H / uw;
     const int units = m_tiles * n_tiles;
     if (!(knobs().persist_fwd && knobs().pair_mma && ndirs == 2 && B % (2 * kBM) == 0 && H % 64 == 0 &&
-          units <= num_sms() / 2 && dep && exit_ctr))
+          units <= num_sms() / 2 && dep && exit_ctr && 4 * m_tiles <= kFwdDepSlots))
         return false;
     FwdPParams p;
     std::memset(&p, 0, sizeof(p));
@@ -1199,6 +1201,7 @@ bool lstm_fwd_layer_persistent(const LstmFwdLayer& L, int ndirs, int B, int H, i
     auto launch = [&](auto tr) {
         using Tr = decltype(tr);
         auto k = tc::persistent_kernel_2cta<Tr, FwdPParams>;
+        note_kernel<cta_pair<Tr>>();
         static bool attr = false;
         if (!attr) {
             AB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::ShapeOf2<Tr>::SMEM));
@@ -1227,7 +1230,7 @@ bool lstm_bwd_layer_persistent(const LstmBwdLayer& L, int ndirs, int B, int H, i
     const int m_tiles = B / (2 * kBM), n_tiles = H / (uc * kq);
     const int units = m_tiles * n_tiles * kq;
     if (!(knobs().persist_bwd && knobs().pair_mma && ndirs == 2 && T >= 2 && B % (2 * kBM) == 0 && H % 128 == 0 &&
-          units <= num_sms() / 2 && sk_scratch && sk_flags && dep && exit_ctr))
+          units <= num_sms() / 2 && sk_scratch && sk_flags && dep && exit_ctr && 4 * m_tiles <= kBwdDepSlots))
         return false;
     BwdPParams p;
     std::memset(&p, 0, sizeof(p));
@@ -1256,6 +1259,7 @@ bool lstm_bwd_layer_persistent(const LstmBwdLayer& L, int ndirs, int B, int H, i
     auto launch = [&](auto tr) {
         using Tr = decltype(tr);
         auto k = tc::persistent_kernel_2cta<Tr, BwdPParams>;
+        note_kernel<cta_pair<Tr>>();
         static bool attr = false;
         if (!attr) {
             AB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::ShapeOf2<Tr>::SMEM));

@@ -11,6 +11,13 @@
 
 namespace ab {
 
+// Sync scratch of the persistent recurrent kernels (engine: pb_sync, 520 u32): the BPTT uses
+// [0, 256) exchange epochs, [256, 512) per-(dir, row-block, CTA) step counters, [512] exit; the
+// forward [384, 512) step counters, [513] exit. Each kernel needs 2 dirs x m_tiles x 2 counters.
+constexpr int kPbSyncWords = 520;
+constexpr int kBwdDepSlots = 256;
+constexpr int kFwdDepSlots = 128;
+
 using EncodeFnT = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);

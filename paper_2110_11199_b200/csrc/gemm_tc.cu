@@ -548,6 +548,7 @@ void make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, 
 template <class Traits>
 void launch_single(const TcParams& p, cudaStream_t s) {
     auto k = tc::persistent_kernel<Traits, TcParams>;
+    note_kernel<cta_single<Traits>>();
     static bool attr = false;
     if (!attr) {
         AB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::Shape<Traits::BN, Traits::EPI_SMEM>::SMEM));
@@ -563,6 +564,7 @@ void launch_single(const TcParams& p, cudaStream_t s) {
 template <class Traits>
 void launch_pair(const TcParams& p, cudaStream_t s) {
     auto k = tc::persistent_kernel_2cta<Traits, TcParams>;
+    note_kernel<cta_pair<Traits>>();
     static bool attr = false;
     if (!attr) {
         AB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::ShapeOf2<Traits>::SMEM));

@@ -28,11 +28,11 @@ struct Knobs {
     bool force_ext = false;    // ADPSGD_FORCE_EXT=1: take the extra-column / stream-K / wide kernels wherever legal
     int force_bn = 0;          // ADPSGD_FORCE_BN=128|256: generic GEMM tile width (probes)
     int epi_skip = 0;          // ADPSGD_EPI_SKIP=n: epilogue timing experiments
-    int export_dbg = 0;
-    int split_max = 4;
-    bool fwd_u32 = true;
-    bool bwd_u32 = true;       // ADPSGD_NO_BWD_U32=1: persistent BPTT always with 64 units per CTA       // ADPSGD_NO_FWD_U32=1: persistent forward always in 64-unit tiles
-    bool unfused_ce = false;   // ADPSGD_UNFUSED_CE=1: bf16 logits GEMM (fp32 out) + softmax-CE kernel (diagnosis)         // ADPSGD_SPLIT_MAX=n: K slices of the one-wave split-K weight gradients (1: off)        // ADPSGD_EXPORT_DBG=1|2: split-K export diagnosis
+    int export_dbg = 0;        // ADPSGD_EXPORT_DBG=1|2: split-K export diagnosis
+    int split_max = 4;         // ADPSGD_SPLIT_MAX=n: K slices of the one-wave split-K weight gradients (1: off)
+    bool fwd_u32 = true;       // ADPSGD_NO_FWD_U32=1: persistent forward always in 64-unit tiles
+    bool bwd_u32 = true;       // ADPSGD_NO_BWD_U32=1: persistent BPTT always with 64 units per CTA
+    bool unfused_ce = false;   // ADPSGD_UNFUSED_CE=1: bf16 logits GEMM (fp32 out) + softmax-CE kernel (diagnosis)
 };
 
 const Knobs& knobs();

@@ -1,8 +1,11 @@
 #include "prof.hpp"
 
+#include <map>
 #include <mutex>
+#include <string>
 
 #include "common.cuh"
+#include <cstring>
 
 namespace ab {
 unsigned long long* g_trace_buf = nullptr;  // device buffer while tracing is on (tc_core.cuh)
@@ -96,6 +99,43 @@ void prof_read(double* ms, double* flops, double* bytes, int64_t* launches, int 
         ms[c] = g_ms[c]; flops[c] = g_flops[c]; bytes[c] = g_bytes[c]; launches[c] = g_launches[c];
     }
     for (int c = 0; c < PROF_NCAT; ++c) { g_ms[c] = 0; g_flops[c] = 0; g_bytes[c] = 0; g_launches[c] = 0; }
+}
+
+namespace {
+std::map<std::string, int64_t> g_variants;
+std::mutex g_var_mu;
+}  // namespace
+
+// __PRETTY_FUNCTION__ of note_kernel<T>() ends in "[with T = <type>]"; keep <type> without the
+// namespace prefix.
+void note_variant(const char* pretty) {
+    std::string s(pretty);
+    const auto at = s.find("T = ");
+    if (at != std::string::npos) {
+        s = s.substr(at + 4);
+        const auto end = s.rfind(']');
+        if (end != std::string::npos) s = s.substr(0, end);
+        const auto semi = s.find(';');
+        if (semi != std::string::npos) s = s.substr(0, semi);
+    }
+    for (const char* ns : {"ab::", "tc::", "{anonymous}::", "(anonymous namespace)::"})
+        for (auto p = s.find(ns); p != std::string::npos; p = s.find(ns)) s.erase(p, std::strlen(ns));
+    // nvcc names anonymous namespaces _GLOBAL__N__<hash>_<file>::
+    for (auto p = s.find("_GLOBAL__N_"); p != std::string::npos; p = s.find("_GLOBAL__N_")) {
+        const auto e = s.find("::", p);
+        if (e == std::string::npos) break;
+        s.erase(p, e + 2 - p);
+    }
+    std::lock_guard<std::mutex> lk(g_var_mu);
+    ++g_variants[s];
+}
+
+std::string variants_string(bool reset) {
+    std::lock_guard<std::mutex> lk(g_var_mu);
+    std::string out;
+    for (const auto& kv : g_variants) out += kv.first + "=" + std::to_string(kv.second) + ";";
+    if (reset) g_variants.clear();
+    return out;
 }
 
 }  // namespace ab

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <string>
 #include <vector>
 
 namespace ab {
@@ -53,5 +54,16 @@ struct ProfScope {
         if (id >= 0) prof_end(id, s, cat, flops, bytes);
     }
 };
+
+// Kernel-variant registry: every tcgen05 launch site records the template instantiation it
+// selected (host-side, at eager launch or graph capture), so tests can assert which kernel a
+// shape exercised (adpsgd_kernel_variants).
+void note_variant(const char* pretty_function);
+template <class T> struct cta_pair;    // markers: tile on a CTA pair (cta_group::2) ...
+template <class T> struct cta_single;  // ... or on one CTA
+template <class T>
+inline void note_kernel() { note_variant(__PRETTY_FUNCTION__); }
+// "name=count;..." of every variant noted since the last reset.
+std::string variants_string(bool reset);
 
 }  // namespace ab

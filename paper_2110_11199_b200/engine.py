@@ -108,6 +108,32 @@ class ModelDesc:
         nd = 2 if self.bidirectional else 1
         return 3.0 * self.fwd_flops_per_frame() - 2.0 * nd * 4 * self.hidden * self.input_dim
 
+    def param_blocks(self) -> list:
+        """(name, slice, fan_in) of every parameter block of the flat vector, in layout order
+        (csrc/model.hpp: per layer, per direction W_ih, W_hh, b; then W_proj, b_proj, W_out, b_out)."""
+        nd = 2 if self.bidirectional else 1
+        H, off, out = self.hidden, 0, []
+
+        def add(name, n, fan_in):
+            nonlocal off
+            out.append((name, slice(off, off + n), fan_in))
+            off += n
+
+        for l in range(self.layers):
+            i = self.input_dim if l == 0 else nd * H
+            for d in range(nd):
+                add(f"l{l}d{d}.w_ih", 4 * H * i, i)
+                add(f"l{l}d{d}.w_hh", 4 * H * H, H)
+                add(f"l{l}d{d}.b", 4 * H, H)
+        top = nd * H
+        if self.proj > 0:
+            add("w_proj", self.proj * top, top)
+            add("b_proj", self.proj, top)
+        oi = self.proj if self.proj > 0 else top
+        add("w_out", self.classes * oi, oi)
+        add("b_out", self.classes, oi)
+        return out
+
 
 @dataclass
 class StrategyConfig:
@@ -326,6 +352,18 @@ class LearnerGroup:
 
     def barrier(self) -> None:
         _lib.check(_lib.lib().adpsgd_barrier(self._h))
+
+    def gossip_probe(self, left: int = -1, right: int = -1, reps: int = 5) -> dict:
+        """Bandwidth of the FM/RM gossip path at this model size (adpsgd_gossip_probe): the fused
+        mix kernel reading learners `left` / `right` (peers over NVLink, or local stand-ins at -1) and a
+        copy-engine pull of both neighbours."""
+        out = (C.c_double * 4)()
+        _lib.check(_lib.lib().adpsgd_gossip_probe(self._h, left, right, reps, out))
+        mix_ms, nvlink_bytes, copy_ms, mix_bytes = out[0], out[1], out[2], out[3]
+        return {"mix_ms": mix_ms, "mix_hbm_gbs": mix_bytes / (mix_ms * 1e6) if mix_ms > 0 else None,
+                "mix_nvlink_gbs": nvlink_bytes / (mix_ms * 1e6) if mix_ms > 0 and nvlink_bytes else None,
+                "nvlink_bytes": nvlink_bytes, "copy_ms": copy_ms,
+                "copy_gbs": 8.0 * self.D / (copy_ms * 1e6) if copy_ms > 0 else None}
 
 
 def nccl_unique_id() -> bytes:

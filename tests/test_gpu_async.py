@@ -32,7 +32,7 @@ def test_async_with_straggler_matches_oracle(oracle_mod, strategy):
     ref = O.OracleEngine(_odesc(O), L, 3, 31, feats, labels, 36)
     prof = CH.ClusterProfile(learners=L, compute_time=1.0, comm_pairwise=0.05, stragglers=[(0, 2.5)])
     dur = [max(prof.effective_compute(l), prof.comm_pairwise) for l in range(L)]
-    lrs = [0.3, 0.15]
+    lrs = [0.3, 0.15, 0.1, 0.05, 0.025, 0.0125, 0.01, 0.01]  # a fast learner's rounds run past 2 epochs
     ev, et = CH.async_run(g, strategy, dur, 23, 3, lrs)
     oev, oet = ref.coupled_async(int(strategy), dur, 23, 3, lrs)
     assert ev.tolist() == oev.tolist() and np.array_equal(et, oet)
@@ -55,6 +55,16 @@ def test_homogeneous_coupled_equals_synchronous(oracle_mod):
         b.step(0.2)
     for l in range(L):
         assert np.max(np.abs(a.weights(l) - b.weights(l))) <= 1e-6
+
+
+def test_async_lr_table_must_cover_every_round():
+    # no silent clamp of the epoch index (chronos.cpp:216 uses lr_at(cfg.lr, r / ipe) unbounded)
+    from paper_2110_11199_b200.errors import ConfigError
+    feats, labels = _data()
+    g = LearnerGroup(M, StrategyConfig(strategy=Strategy.ADPSGD_FM, learners=3, batch=3, seed=2), precision=Precision.FP32)
+    g.set_dataset(feats, labels, 36)
+    with pytest.raises(ConfigError):
+        CH.async_run(g, Strategy.ADPSGD_FM, [1.0, 1.0, 5.0], 12, 2, [0.1])
 
 
 def test_coupled_run_profile_checks():
