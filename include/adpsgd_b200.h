@@ -158,6 +158,43 @@ int adpsgd_async_run(adpsgd_ctx* ctx, int32_t strategy, const double* durations,
                      const double* lr_per_epoch, int32_t n_epochs, int32_t* event_learner, double* event_time,
                      int64_t* processed);
 
+/* ---- free-running asynchronous FM / RM across processes (one learner per process) ----
+ * chronos::coupled_async's semantics on real clocks (chronos.cpp:171-176, 237-259): every learner
+ * iterates at its own rate with no barrier, mixing with its ring neighbours' latest *published*
+ * models -- w <- (w + p_L + p_R)/3 - lr g, chronos.cpp:256 -- and publishing the result into a ring
+ * of 4 versioned buffers (4 publications kept, chronos.cpp:258-259) exported over CUDA IPC. Version
+ * counters are device memory read with ld.acquire.sys / written with st.release.sys; a reader whose
+ * chosen slot a neighbour started overwriting before its mix finished (torn read) redoes the mix.
+ * RM pairs by the learner's own round (chronos.cpp:228). */
+typedef enum adpsgd_async_mode {
+    ADPSGD_ASYNC_FREE = 0,      /* latest publication, never wait (the paper's asynchronous ADPSGD) */
+    ADPSGD_ASYNC_LOCKSTEP = 1,  /* exactly the neighbours' version k (waits): equals synchronous FM/RM */
+    ADPSGD_ASYNC_BOUNDED = 2    /* latest publication, waiting until it is >= k - max_lag */
+} adpsgd_async_mode;
+
+typedef struct adpsgd_async_info {
+    int64_t version;        /* this learner's model version after the step (its round count) */
+    int64_t left_version;   /* neighbour versions mixed with */
+    int64_t right_version;
+    int32_t left, right;    /* global ids of the neighbours */
+    int32_t retries;        /* torn-read retries of the mix */
+    int32_t reserved;
+    double wait_ms;         /* device time the select kernel waited for neighbours */
+    double step_ms;         /* device time of the whole step */
+} adpsgd_async_info;
+
+/* Switch this context (one local learner, FM or RM) to the 4-slot publication ring; call before
+ * adpsgd_export_ipc. timeout_s bounds every wait for a neighbour (ADPSGD_E_INVALID_STATE on expiry). */
+int adpsgd_async_init(adpsgd_ctx* ctx, int32_t mode, int32_t max_lag, double timeout_s);
+/* One free-running iteration of this learner: sample, forward/backward, select neighbour versions,
+ * mix + update into the next slot, publish. info (nullable) describes what was mixed. */
+int adpsgd_async_step(adpsgd_ctx* ctx, double lr, float* loss_out, adpsgd_async_info* info);
+/* Fixed extra time per step for a local learner (emulated compute for straggler studies), as a
+ * device spin after the gradient (on_host = 0) or a host sleep after the step (on_host = 1, for
+ * processes sharing one GPU). The straggler factor (adpsgd_set_straggler) then stretches measured
+ * compute + this delay, on the same side. */
+int adpsgd_set_step_delay(adpsgd_ctx* ctx, int32_t local_learner, double ms, int32_t on_host);
+
 /* ---- multi-process (one process per GPU) ---- */
 /* NCCL communicator over all ranks; nccl_id = 128-byte ncclUniqueId from rank 0.
  * nccl_id = NULL: CUDA-IPC-only transport (FM / RM / D1D by peer reads; no device barrier, so the caller
@@ -200,7 +237,7 @@ int adpsgd_kernel_variants(char* out, size_t n, int32_t reset);
 /* Debug: device timeline of the CTA-pair tensor-core kernels (160 CTAs x 32 globaltimer stamps). */
 int adpsgd_debug_trace(int32_t enable, uint64_t* out, int32_t n);
 /* Diagnosis: copy an internal activation buffer of learner 0 to host (which: 0 = X0, 1 + l = layer
- * l output H, 100 = Y, 101 = row_loss, 102 = bf16 shadow, 200 + l = layer l cell state c,
+ * l output H, 100 = Y, 101 = row_loss, 102 = bf16 shadow, 103 = last fp32 gradient, 200 + l = layer l cell state c,
  * 300 + l = layer l gates); bytes clipped to the buffer. */
 int adpsgd_debug_buffer(adpsgd_ctx* ctx, int32_t which, void* out, size_t bytes);
 

@@ -36,6 +36,11 @@ class Perf(C.Structure):
                 ("steps", i64), ("kernel_launches", i64)]
 
 
+class AsyncInfo(C.Structure):
+    _fields_ = [("version", i64), ("left_version", i64), ("right_version", i64), ("left", i32), ("right", i32),
+                ("retries", i32), ("reserved", i32), ("wait_ms", C.c_double), ("step_ms", C.c_double)]
+
+
 _SIGS = {
     "adpsgd_param_count": (i64, [P(ModelDesc)]),
     "adpsgd_permutation_for_iteration": (C.c_int, [u64, i32, i64, P(i32)]),
@@ -72,6 +77,9 @@ _SIGS = {
     "adpsgd_import_ipc": (C.c_int, [C.c_void_p, i32, i32, i32, C.c_void_p, i64]),
     "adpsgd_set_gossip_mode": (C.c_int, [C.c_void_p, i32]),
     "adpsgd_barrier": (C.c_int, [C.c_void_p]),
+    "adpsgd_async_init": (C.c_int, [C.c_void_p, i32, i32, C.c_double]),
+    "adpsgd_async_step": (C.c_int, [C.c_void_p, C.c_double, P(C.c_float), P(AsyncInfo)]),
+    "adpsgd_set_step_delay": (C.c_int, [C.c_void_p, i32, C.c_double, i32]),
     "adpsgd_gossip_probe": (C.c_int, [C.c_void_p, i32, i32, i32, P(C.c_double)]),
     "adpsgd_profile_enable": (C.c_int, [i32]),
     "adpsgd_profile_read": (C.c_int, [P(C.c_double), P(C.c_double), P(C.c_double), P(i64), i32]),

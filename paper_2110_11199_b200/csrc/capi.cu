@@ -161,7 +161,7 @@ int adpsgd_set_weights(adpsgd_ctx* ctx, int32_t j, const double* w, int64_t n) {
         AB_CUDA(cudaSetDevice(c.cfg.device));
         std::vector<float> f(w, w + n);
         Learner& ln = c.learners[j];
-        const int cur = static_cast<int>(c.k & 1);
+        const int cur = c.slot(c.k);
         AB_CUDA(cudaStreamSynchronize(c.s_main));
         c.h2d_sync(ln.w[cur], f.data(), n * sizeof(float));
         c.refresh_shadow(ln, ln.w[cur], c.s_main);
@@ -176,7 +176,7 @@ int adpsgd_get_weights(adpsgd_ctx* ctx, int32_t j, double* w, int64_t n) {
         AB_CHECK(n == c.D, ADPSGD_E_DIMENSION, "weight vector length != parameter count");
         AB_CUDA(cudaSetDevice(c.cfg.device));
         std::vector<float> f(n);
-        AB_CUDA(cudaMemcpyAsync(f.data(), c.learners[j].w[c.k & 1], n * sizeof(float), cudaMemcpyDeviceToHost, c.s_main));
+        AB_CUDA(cudaMemcpyAsync(f.data(), c.learners[j].w[c.slot(c.k)], n * sizeof(float), cudaMemcpyDeviceToHost, c.s_main));
         AB_CUDA(cudaStreamSynchronize(c.s_main));
         for (int64_t i = 0; i < n; ++i) w[i] = f[i];
     });
@@ -282,7 +282,7 @@ int adpsgd_comm_init(adpsgd_ctx* ctx, int32_t rank, int32_t world, const void* i
 }
 
 int64_t adpsgd_ipc_handle_size(adpsgd_ctx* ctx) {
-    return ctx && ctx->impl ? static_cast<int64_t>(ctx->impl->cfg.local_learners) * 2 * sizeof(cudaIpcMemHandle_t) : -1;
+    return ctx && ctx->impl ? static_cast<int64_t>(ctx->impl->cfg.local_learners) * Comm::ipc_record_bytes() : -1;
 }
 
 int adpsgd_export_ipc(adpsgd_ctx* ctx, void* out, int64_t size) {
@@ -290,6 +290,7 @@ int adpsgd_export_ipc(adpsgd_ctx* ctx, void* out, int64_t size) {
         Ctx& c = C_(ctx);
         AB_CHECK(c.comm, ADPSGD_E_INVALID_STATE, "adpsgd_comm_init first");
         c.comm->export_ipc(c, out, size);
+        c.ipc_exported = true;
     });
 }
 
@@ -308,6 +309,24 @@ int adpsgd_set_gossip_mode(adpsgd_ctx* ctx, int32_t mode) {
         AB_CHECK(mode >= 0 && mode <= 2, ADPSGD_E_CONFIG, "gossip mode must be 0, 1 or 2");
         AB_CHECK(c.comm, ADPSGD_E_INVALID_STATE, "adpsgd_comm_init first");
         c.comm->gossip_mode = mode;
+    });
+}
+
+int adpsgd_async_init(adpsgd_ctx* ctx, int32_t mode, int32_t max_lag, double timeout_s) {
+    return guard([&] { C_(ctx).async_init(mode, max_lag, timeout_s); });
+}
+
+int adpsgd_async_step(adpsgd_ctx* ctx, double lr, float* loss_out, adpsgd_async_info* info) {
+    return guard([&] { C_(ctx).async_step(lr, loss_out, info); });
+}
+
+int adpsgd_set_step_delay(adpsgd_ctx* ctx, int32_t j, double ms, int32_t on_host) {
+    return guard([&] {
+        Ctx& c = C_(ctx);
+        AB_CHECK(j >= 0 && j < c.cfg.local_learners, ADPSGD_E_DIMENSION, "local learner out of range");
+        AB_CHECK(ms >= 0, ADPSGD_E_CONFIG, "step delay must be >= 0");
+        c.learners[j].delay_ms = ms;
+        c.learners[j].delay_on_host = on_host != 0;
     });
 }
 
@@ -363,6 +382,7 @@ int adpsgd_debug_buffer(adpsgd_ctx* ctx, int32_t which, void* out, size_t bytes)
         else if (which == 100) { src = c.Y; n = TB * c.ldY * c.es; }
         else if (which == 101) { src = c.row_loss; n = TB * sizeof(float); }
         else if (which == 102) { src = c.learners[0].shadow; n = static_cast<size_t>(c.D) * 2; }
+        else if (which == 103) { src = c.learners[0].g; n = static_cast<size_t>(c.D) * sizeof(float); }
         else if (which >= 200 && which < 200 + c.lay.L) { src = c.cst[which - 200]; n = TB * c.ndH * sizeof(float); }
         else if (which >= 300 && which < 300 + c.lay.L) { src = c.gates[which - 300]; n = TB * c.nd4H * c.es; }
         AB_CHECK(src != nullptr, ADPSGD_E_INVALID_STATE, "debug_buffer: no such buffer");

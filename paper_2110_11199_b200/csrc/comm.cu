@@ -115,7 +115,7 @@ void Comm::prefetch_neighbours(Ctx& c, const float* wl, const float* wr, cudaStr
 void Comm::sendrecv_neighbours(Ctx& c, int left, int right, cudaStream_t s) {
     AB_CHECK(!ipc_only, ADPSGD_E_CONFIG, "gossip mode 2 (NCCL send/recv) needs the NCCL transport");
     ensure_nb(c);
-    const float* w = c.learners[0].w[c.k & 1];
+    const float* w = c.learners[0].w[c.slot(c.k)];
     const int rl = left - c.cfg.first_learner + rank, rr = right - c.cfg.first_learner + rank;  // one learner per rank
     AB_NCCL(nccl().GroupStart());
     AB_NCCL(nccl().Send(w, c.D, ncclFloat32, rl, static_cast<ncclComm_t>(nccl_), s));
@@ -149,7 +149,7 @@ void Comm::start_weight_sum(Ctx& c, cudaStream_t s) {
     // w_k is final once the previous iteration's update (enqueued on s) has run.
     AB_CUDA(cudaEventRecord(ev_start_, s));
     AB_CUDA(cudaStreamWaitEvent(c.s_comm, ev_start_, 0));
-    const float* w = c.learners[0].w[c.k & 1];
+    const float* w = c.learners[0].w[c.slot(c.k)];
     AB_NCCL(nccl().AllReduce(w, wsum_, c.D, ncclFloat32, ncclSum, static_cast<ncclComm_t>(nccl_), c.s_comm));
     AB_CUDA(cudaEventRecord(ev_ws_, c.s_comm));
 }
@@ -169,37 +169,69 @@ const float* Comm::peer_weight(int gid, int buf) const {
     auto it = peers_.find(gid);
     AB_CHECK(it != peers_.end(), ADPSGD_E_INVALID_STATE,
              "learner " + std::to_string(gid) + " has no mapped weights (adpsgd_import_ipc)");
-    return buf ? it->second.second : it->second.first;
+    AB_CHECK(buf >= 0 && buf < it->second.nbuf, ADPSGD_E_INVALID_STATE,
+             "learner " + std::to_string(gid) + " exports " + std::to_string(it->second.nbuf) +
+                 " model versions (async rings must be enabled on every rank before export)");
+    return it->second.w[buf];
 }
 
-int64_t Comm::ipc_size(const Ctx& c) const { return static_cast<int64_t>(c.cfg.local_learners) * 2 * kHandle; }
+const unsigned long long* Comm::peer_ver(int gid) const {
+    auto it = peers_.find(gid);
+    AB_CHECK(it != peers_.end() && it->second.ver, ADPSGD_E_INVALID_STATE,
+             "learner " + std::to_string(gid) + " has no mapped publication counters (adpsgd_import_ipc)");
+    return it->second.ver;
+}
+
+// Export record per local learner: int32 nbuf, int32 reserved, then 4 weight-slot handles (the
+// first nbuf valid) and the publication-counter handle.
+namespace {
+constexpr int kRec = 8 + 5 * kHandle;
+}
+
+int64_t Comm::ipc_record_bytes() { return kRec; }
+int64_t Comm::ipc_size(const Ctx& c) const { return static_cast<int64_t>(c.cfg.local_learners) * kRec; }
 
 void Comm::export_ipc(const Ctx& c, void* out, int64_t size) const {
     AB_CHECK(size >= ipc_size(c), ADPSGD_E_DIMENSION, "ipc buffer too small");
     uint8_t* o = static_cast<uint8_t*>(out);
-    for (int j = 0; j < c.cfg.local_learners; ++j)
-        for (int b = 0; b < 2; ++b) {
+    std::memset(o, 0, static_cast<size_t>(ipc_size(c)));
+    for (int j = 0; j < c.cfg.local_learners; ++j) {
+        uint8_t* r = o + static_cast<int64_t>(j) * kRec;
+        const int32_t hdr[2] = {c.nbuf, 0};
+        std::memcpy(r, hdr, sizeof(hdr));
+        for (int b = 0; b < c.nbuf; ++b) {
             cudaIpcMemHandle_t h;
             AB_CUDA(cudaIpcGetMemHandle(&h, c.learners[j].w[b]));
-            std::memcpy(o + (j * 2 + b) * kHandle, &h, kHandle);
+            std::memcpy(r + 8 + b * kHandle, &h, kHandle);
         }
+        cudaIpcMemHandle_t h;
+        AB_CUDA(cudaIpcGetMemHandle(&h, c.learners[j].ver));
+        std::memcpy(r + 8 + 4 * kHandle, &h, kHandle);
+    }
 }
 
 void Comm::import_ipc(int peer_rank, int first, int count, const void* handles, int64_t size) {
-    AB_CHECK(size >= static_cast<int64_t>(count) * 2 * kHandle, ADPSGD_E_DIMENSION, "ipc buffer too small");
+    AB_CHECK(size >= static_cast<int64_t>(count) * kRec, ADPSGD_E_DIMENSION, "ipc buffer too small");
     if (peer_rank == rank) return;
     const uint8_t* in = static_cast<const uint8_t*>(handles);
+    auto open = [&](const uint8_t* src) {
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, src, kHandle);
+        void* ptr = nullptr;
+        AB_CUDA(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+        opened_.push_back(ptr);
+        return ptr;
+    };
     for (int j = 0; j < count; ++j) {
-        float* p[2];
-        for (int b = 0; b < 2; ++b) {
-            cudaIpcMemHandle_t h;
-            std::memcpy(&h, in + (j * 2 + b) * kHandle, kHandle);
-            void* ptr = nullptr;
-            AB_CUDA(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
-            opened_.push_back(ptr);
-            p[b] = static_cast<float*>(ptr);
-        }
-        peers_[first + j] = {p[0], p[1]};
+        const uint8_t* r = in + static_cast<int64_t>(j) * kRec;
+        int32_t hdr[2];
+        std::memcpy(hdr, r, sizeof(hdr));
+        AB_CHECK(hdr[0] == 2 || hdr[0] == 4, ADPSGD_E_INVALID_STATE, "corrupt IPC export record");
+        PeerMap pm;
+        pm.nbuf = hdr[0];
+        for (int b = 0; b < pm.nbuf; ++b) pm.w[b] = static_cast<float*>(open(r + 8 + b * kHandle));
+        pm.ver = static_cast<unsigned long long*>(open(r + 8 + 4 * kHandle));
+        peers_[first + j] = pm;
     }
 }
 

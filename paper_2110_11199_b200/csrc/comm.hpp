@@ -34,6 +34,7 @@ class Comm {
     void pre_gossip(Ctx& c, cudaStream_t s);
     void barrier(cudaStream_t s);
     const float* peer_weight(int gid, int buf) const;
+    const unsigned long long* peer_ver(int gid) const;  // publication counters (async FM/RM)
     // gossip_mode 1: copy-engine pulls of the two neighbours' w_k into local buffers on the comm
     // stream (issued at step start, overlapping the gradient compute; `ready` event joined by the mix)
     void prefetch_neighbours(Ctx& c, const float* wl, const float* wr, cudaStream_t s);
@@ -44,6 +45,7 @@ class Comm {
     cudaEvent_t nb_ready = nullptr;
 
     int64_t ipc_size(const Ctx& c) const;
+    static int64_t ipc_record_bytes();  // export bytes per local learner
     void export_ipc(const Ctx& c, void* out, int64_t size) const;
     void import_ipc(int peer_rank, int first, int count, const void* handles, int64_t size);
 
@@ -53,7 +55,12 @@ class Comm {
     float* gsum_ = nullptr;
     float* bar_ = nullptr;
     cudaEvent_t ev_start_ = nullptr, ev_ws_ = nullptr;
-    std::map<int, std::pair<float*, float*>> peers_;  // gid -> (w[0], w[1]) mapped over NVLink
+    struct PeerMap {
+        float* w[4] = {nullptr, nullptr, nullptr, nullptr};  // model versions (ring of nbuf)
+        int nbuf = 0;
+        unsigned long long* ver = nullptr;                   // publication counters
+    };
+    std::map<int, PeerMap> peers_;  // gid -> that learner's buffers mapped over NVLink (CUDA IPC)
     std::vector<void*> opened_;
     float* nb_[2] = {nullptr, nullptr};  // local copies of the neighbours' w_k (modes 1, 2)
     void ensure_nb(Ctx& c);

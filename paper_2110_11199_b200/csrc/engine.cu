@@ -18,7 +18,9 @@
 #include <cstring>
 #include <memory>
 #include <queue>
+#include <chrono>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "comm.hpp"
@@ -219,6 +221,8 @@ Ctx::Ctx(const adpsgd_config& c) : cfg(c) {
         ln.gid = c.first_learner + j;
         ln.rng = Rng(derive_seed(c.seed, kLearnerStream + static_cast<uint64_t>(ln.gid)));
         for (int b = 0; b < 2; ++b) ln.w[b] = static_cast<float*>(alloc(D * sizeof(float)));
+        ln.ver = static_cast<unsigned long long*>(alloc(4 * sizeof(unsigned long long)));
+        AB_CUDA(cudaMemsetAsync(ln.ver, 0, 4 * sizeof(unsigned long long), s_main));
         ln.g = static_cast<float*>(alloc(D * sizeof(float)));
         if (bf16_mode) {
             ln.shadow = static_cast<bf16*>(alloc(D * sizeof(bf16)));
@@ -709,9 +713,8 @@ void Ctx::compute_body(int j, int mode, const float* wpt, cudaStream_t s) {
         gather_batch(stage_feats2, stage_labels2, ident_idx, s);
     }
     if (fuse_now) {
-        const int cur = static_cast<int>(k & 1);
         FusedUpd fu;
-        fu.w = ln.w[cur]; fu.o = ln.w[cur ^ 1]; fu.sh = ln.shadow; fu.lr = lr_dev;
+        fu.w = ln.w[slot(k)]; fu.o = ln.w[slot(k + 1)]; fu.sh = ln.shadow; fu.lr = lr_dev;
         forward_backward(ln, wpt, ln.g, loss_dev + j, s, true, &fu);
     } else {
         forward_backward(ln, wpt, ln.g, loss_dev + j, s);
@@ -723,13 +726,13 @@ void Ctx::compute_body(int j, int mode, const float* wpt, cudaStream_t s) {
 // later ones replay — ~1000 launches per learner step become one graph launch.
 void Ctx::run_compute(int j, int mode, const float* wpt, cudaStream_t s, int parity) {
     Learner& ln = learners[j];
-    if (parity < 0) parity = static_cast<int>(k & 1);
+    if (parity < 0) parity = slot(k);
     const bool lagged = wpt != ln.w[parity];
     if (lagged || !use_graphs) {
         compute_body(j, mode, wpt, s);
         return;
     }
-    const int key = (((j * 2 + parity) * 3 + mode) * 2 + (g_prof_enabled ? 1 : 0)) * 2 + (fuse_now ? 1 : 0);
+    const int key = (((j * 4 + parity) * 3 + mode) * 2 + (g_prof_enabled ? 1 : 0)) * 2 + (fuse_now ? 1 : 0);
     auto it = graphs.find(key);
     if (it == graphs.end()) {
         StepGraph sg;
@@ -788,7 +791,8 @@ int64_t Ctx::async_run(int strategy, const double* durations, int64_t target, in
             for (int q = 0; q < kPubs; ++q) pubs.push_back(static_cast<float*>(alloc(D * sizeof(float))));
     struct Pub { double t; int slot; };
     std::vector<std::vector<Pub>> pl(L);  // oldest first
-    std::vector<int> par(L, static_cast<int>(k & 1));
+    AB_CHECK(nbuf == 2, ADPSGD_E_CONFIG, "coupled async replay runs on the double-buffered (synchronous) context");
+    std::vector<int> par(L, slot(k));
     for (int l = 0; l < L; ++l) {
         AB_CUDA(cudaMemcpyAsync(pubs[l * kPubs], learners[l].w[par[l]], D * sizeof(float), cudaMemcpyDeviceToDevice, s));
         pl[l].push_back({0.0, 0});
@@ -854,7 +858,7 @@ int64_t Ctx::async_run(int strategy, const double* durations, int64_t target, in
     // leave every model in the context's current buffer
     for (int l = 0; l < L; ++l) {
         Learner& ln = learners[l];
-        const int cur = static_cast<int>(k & 1);
+        const int cur = slot(k);
         if (par[l] != cur) {
             AB_CUDA(cudaMemcpyAsync(ln.w[cur], ln.w[par[l]], D * sizeof(float), cudaMemcpyDeviceToDevice, s));
             refresh_shadow(ln, ln.w[cur], s);
@@ -877,7 +881,7 @@ void Ctx::clear_graphs() {
 // ---------------------------------------------------------------------------
 void Ctx::mix_and_update(double lr_d, const int32_t* taus) {
     const float lr = static_cast<float>(lr_d);
-    const int cur = static_cast<int>(k & 1), nxt = cur ^ 1;
+    const int cur = slot(k), nxt = slot(k + 1);
     const int Lg = cfg.learners;
     const int nloc = cfg.local_learners;
     std::vector<const float*> wtab, gtab;
@@ -1009,7 +1013,7 @@ bool Ctx::is_local(int gid) const {
 // Model each learner evaluates its gradient at: its own model (FM/RM/D1D), the shared
 // model (SDPSGD; identical on every learner), or the tau-lagged model (GENERIC).
 const float* Ctx::grad_point(const Learner& ln, const int32_t* taus) {
-    const int cur = static_cast<int>(k & 1);
+    const int cur = slot(k);
     if (cfg.strategy == ADPSGD_GENERIC && cfg.learners > 1 && taus) {
         const int tau = taus[ln.gid];
         AB_CHECK(tau >= 0 && tau < history_depth, ADPSGD_E_STALENESS_OVERFLOW,
@@ -1023,7 +1027,7 @@ void Ctx::check_sync() {
     // engine.cpp:139-144 — models must agree within 1e-12 before an SDPSGD step
     // (local learners; identical fp32 arithmetic keeps them bit-identical).
     if (cfg.local_learners < 2) return;
-    const int cur = static_cast<int>(k & 1);
+    const int cur = slot(k);
     AB_CUDA(cudaMemsetAsync(scratch_f, 0, sizeof(float), s_main));
     for (int j = 1; j < cfg.local_learners; ++j) launch_maxdiff(D, learners[j].w[cur], learners[0].w[cur], scratch_f, s_main);
     float h = 0;
@@ -1060,7 +1064,7 @@ void Ctx::step(double lr, const int32_t* taus, float* loss_out, const float* hos
     if ((strategy == ADPSGD_FM || strategy == ADPSGD_RM) && comm && comm->world > 1 && comm->gossip_mode == 1) {
         int left, right;
         neighbours(strategy, learners[0].gid, &left, &right);
-        comm->prefetch_neighbours(*this, weight_ptr(left, static_cast<int>(k & 1)), weight_ptr(right, static_cast<int>(k & 1)), s);
+        comm->prefetch_neighbours(*this, weight_ptr(left, slot(k)), weight_ptr(right, slot(k)), s);
     }
     for (int j = 0; j < cfg.local_learners; ++j) {
         Learner& ln = learners[j];
@@ -1090,17 +1094,18 @@ void Ctx::step(double lr, const int32_t* taus, float* loss_out, const float* hos
             mode = 1;
         }
         const float* wpt = grad_point(ln, taus);
-        const bool lagged = wpt != ln.w[k & 1];
+        const bool lagged = wpt != ln.w[slot(k)];
         if (bf16_mode && lagged) refresh_shadow(ln, wpt, s);  // GENERIC: shadow of the lagged model
-        if (ln.straggle > 1.0) AB_CUDA(cudaEventRecord(ev_comp0, s));
+        const bool stretch = ln.straggle > 1.0 || ln.delay_ms > 0;
+        if (stretch) AB_CUDA(cudaEventRecord(ev_comp0, s));
         run_compute(j, mode, wpt, s);
-        if (ln.straggle > 1.0) {
+        if (stretch) {
             AB_CUDA(cudaEventRecord(ev_comp1, s));
-            // stretch this learner's compute by (factor - 1) x its last measured compute time
-            if (ln.last_compute_ms > 0)
-                launch_delay(static_cast<uint64_t>((ln.straggle - 1.0) * ln.last_compute_ms * 1e6), s);
+            // emulated compute (delay_ms) plus the straggler's (factor - 1) x its last measured compute
+            if (!ln.delay_on_host && extra_delay_ms(ln) > 0)
+                launch_delay(static_cast<uint64_t>(extra_delay_ms(ln) * 1e6), s);
         }
-        if (bf16_mode && lagged) refresh_shadow(ln, ln.w[k & 1], s);
+        if (bf16_mode && lagged) refresh_shadow(ln, ln.w[slot(k)], s);
     }
     AB_CUDA(cudaEventRecord(ev_mix, s));
     fused_done = fuse_now;
@@ -1121,11 +1126,134 @@ void Ctx::step(double lr, const int32_t* taus, float* loss_out, const float* hos
     last_step_ms = ms;
     last_mix_ms = mms;
     for (auto& ln : learners) {
-        if (ln.straggle > 1.0) {
+        if (ln.straggle > 1.0 || ln.delay_ms > 0) {
             float cm = 0;
             if (cudaEventElapsedTime(&cm, ev_comp0, ev_comp1) == cudaSuccess) ln.last_compute_ms = cm;
         }
     }
+    for (auto& ln : learners) host_delay(ln);
+    ++k;
+}
+
+// Straggler hook (chronos.cpp:51-58): a learner's compute is stretched to factor x (measured
+// compute + emulated compute); the emulated part alone for factor 1.
+double Ctx::extra_delay_ms(const Learner& ln) const {
+    const double measured = ln.last_compute_ms;  // events around the gradient compute only
+    return ln.delay_ms + (ln.straggle - 1.0) * (measured + ln.delay_ms);
+}
+
+void Ctx::host_delay(const Learner& ln) {
+    if (!ln.delay_on_host) return;
+    const double ms = extra_delay_ms(ln);
+    if (ms > 0) std::this_thread::sleep_for(std::chrono::microseconds(static_cast<int64_t>(ms * 1000.0)));
+}
+
+// ---------------------------------------------------------------------------
+// Free-running asynchronous FM / RM across processes (chronos.cpp:171-176, 178-299 on real clocks)
+// ---------------------------------------------------------------------------
+void Ctx::async_init(int mode, int64_t max_lag, double timeout_s) {
+    AB_CHECK(mode >= ADPSGD_ASYNC_FREE && mode <= ADPSGD_ASYNC_BOUNDED, ADPSGD_E_CONFIG, "unknown async mode");
+    AB_CHECK(max_lag >= 0 && timeout_s > 0, ADPSGD_E_CONFIG, "async: max_lag >= 0 and timeout > 0 required");
+    AB_CHECK(cfg.strategy == ADPSGD_FM || cfg.strategy == ADPSGD_RM, ADPSGD_E_CONFIG, "async runs FM or RM");
+    AB_CHECK(cfg.learners >= 3, ADPSGD_E_CONFIG, "FM/RM mixing requires at least 3 learners");
+    AB_CHECK(cfg.local_learners == 1, ADPSGD_E_CONFIG, "async: one learner per context (process)");
+    AB_CHECK(!ipc_exported, ADPSGD_E_INVALID_STATE, "async: call adpsgd_async_init before adpsgd_export_ipc");
+    AB_CUDA(cudaSetDevice(cfg.device));
+    AB_CUDA(cudaStreamSynchronize(s_main));
+    Learner& ln = learners[0];
+    if (nbuf == 2) {
+        const int old = slot(k);
+        ln.w[2] = static_cast<float*>(alloc(D * sizeof(float)));
+        ln.w[3] = static_cast<float*>(alloc(D * sizeof(float)));
+        nbuf = 4;
+        if (slot(k) != old)
+            AB_CUDA(cudaMemcpyAsync(ln.w[slot(k)], ln.w[old], D * sizeof(float), cudaMemcpyDeviceToDevice, s_main));
+        clear_graphs();  // graphs are keyed by slot
+    }
+    const unsigned long long v[2] = {static_cast<unsigned long long>(k), static_cast<unsigned long long>(k)};
+    h2d_sync(ln.ver, v, sizeof(v));
+    if (!async_sel) {
+        async_sel = alloc(sizeof(AsyncSel));
+        AB_CUDA(cudaMallocHost(&async_sel_host, sizeof(AsyncSel)));
+    }
+    async_mode = mode;
+    async_lag = max_lag;
+    async_timeout_s = timeout_s;
+}
+
+void Ctx::async_step(double lr_d, float* loss_out, adpsgd_async_info* info) {
+    AB_CHECK(async_mode >= 0, ADPSGD_E_INVALID_STATE, "async: call adpsgd_async_init first");
+    AB_CHECK(comm != nullptr, ADPSGD_E_INVALID_STATE, "async: neighbours not mapped (adpsgd_comm_init / import_ipc)");
+    AB_CUDA(cudaSetDevice(cfg.device));
+    cudaStream_t s = s_main;
+    Learner& ln = learners[0];
+    const int cur = slot(k), nxt = slot(k + 1);
+    const float lr = static_cast<float>(lr_d);
+    sample_indices(ln, 0);
+    AB_CUDA(cudaEventRecord(ev0, s));
+    const bool stretch = ln.straggle > 1.0 || ln.delay_ms > 0;
+    if (stretch) AB_CUDA(cudaEventRecord(ev_comp0, s));
+    run_compute(0, 0, ln.w[cur], s, cur);
+    if (stretch) {
+        AB_CUDA(cudaEventRecord(ev_comp1, s));
+        if (!ln.delay_on_host && extra_delay_ms(ln) > 0) launch_delay(static_cast<uint64_t>(extra_delay_ms(ln) * 1e6), s);
+    }
+    AB_CUDA(cudaEventRecord(ev_mix, s));
+    int nb[2];
+    neighbours(cfg.strategy, ln.gid, &nb[0], &nb[1]);  // RM: permutation of the learner's own round k
+    AsyncPeers pe;
+    for (int side = 0; side < 2; ++side) {
+        AB_CHECK(!is_local(nb[side]), ADPSGD_E_INVALID_STATE, "async: neighbours live in other processes");
+        pe.ver[side] = comm->peer_ver(nb[side]);
+        for (int q = 0; q < 4; ++q) pe.slots[side][q] = comm->peer_weight(nb[side], q);
+    }
+    AsyncSel* sel = static_cast<AsyncSel*>(async_sel);
+    AsyncSel* hsel = static_cast<AsyncSel*>(async_sel_host);
+    const auto timeout_ns = static_cast<unsigned long long>(async_timeout_s * 1e9);
+    int retries = 0;
+    for (;;) {
+        launch_async_select(pe, async_mode, k, async_lag, ln.ver, sel, timeout_ns, s);
+        launch_mix3_sel(D, ln.w[cur], sel, ln.g, lr, ln.w[nxt], bf16_mode ? ln.shadow : nullptr, s);
+        if (retries == 0 && knobs().async_hold_ms > 0)  // tests: widen the read window of the first attempt
+            launch_delay(static_cast<uint64_t>(knobs().async_hold_ms) * 1000000ull, s);
+        launch_async_publish(pe, sel, ln.ver, k, s);
+        AB_CUDA(cudaMemcpyAsync(hsel, sel, sizeof(AsyncSel), cudaMemcpyDeviceToHost, s));
+        AB_CUDA(cudaStreamSynchronize(s));
+        AB_CHECK(!hsel->err, ADPSGD_E_INVALID_STATE,
+                 "async: timed out waiting for neighbour versions (learner " + std::to_string(ln.gid) + ", round " +
+                     std::to_string(k) + ")");
+        if (!hsel->torn) break;
+        AB_CHECK(++retries < 1000, ADPSGD_E_INVALID_STATE, "async: neighbour slots overwritten on every retry");
+    }
+    refresh_pad(ln, ln.w[nxt], s);
+    AB_CUDA(cudaEventRecord(ev1, s));
+    if (loss_out) AB_CUDA(cudaMemcpyAsync(h_loss, loss_dev, sizeof(float), cudaMemcpyDeviceToHost, s));
+    AB_CUDA(cudaStreamSynchronize(s));
+    for (auto* recs : replayed_prof) prof_accumulate(*recs);
+    replayed_prof.clear();
+    if (loss_out) *loss_out = h_loss[0];
+    float ms = 0, mms = 0;
+    AB_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+    AB_CUDA(cudaEventElapsedTime(&mms, ev_mix, ev1));
+    last_step_ms = ms;
+    last_mix_ms = mms;
+    last_gossip_bytes = 8.0 * D * (retries + 1);
+    if (stretch) {
+        float cm = 0;
+        if (cudaEventElapsedTime(&cm, ev_comp0, ev_comp1) == cudaSuccess) ln.last_compute_ms = cm;
+    }
+    if (info) {
+        info->version = k + 1;
+        info->left_version = hsel->ver[0];
+        info->right_version = hsel->ver[1];
+        info->left = nb[0];
+        info->right = nb[1];
+        info->retries = retries;
+        info->reserved = 0;
+        info->wait_ms = hsel->wait_ns * 1e-6;
+        info->step_ms = ms;
+    }
+    host_delay(ln);
     ++k;
 }
 
@@ -1180,7 +1308,7 @@ double Ctx::evaluate(const double* w, const int32_t* idx, int M, double* g_out) 
         }
         result = total / (static_cast<double>(M) * T);
     }
-    refresh_shadow(ln, ln.w[k & 1], s);
+    refresh_shadow(ln, ln.w[slot(k)], s);
     AB_CUDA(cudaStreamSynchronize(s));
     return result;
 }
@@ -1192,7 +1320,7 @@ void Ctx::averaged_model(double* out) {
     std::vector<float> f(D);
     std::fill(out, out + D, 0.0);
     for (auto& ln : learners) {
-        AB_CUDA(cudaMemcpyAsync(f.data(), ln.w[k & 1], D * sizeof(float), cudaMemcpyDeviceToHost, s_main));
+        AB_CUDA(cudaMemcpyAsync(f.data(), ln.w[slot(k)], D * sizeof(float), cudaMemcpyDeviceToHost, s_main));
         AB_CUDA(cudaStreamSynchronize(s_main));
         for (int64_t i = 0; i < D; ++i) out[i] += f[i];
     }
@@ -1207,7 +1335,7 @@ double Ctx::consensus_distance() {
     if (L < 2) return 0.0;
     if (!gram_dev) gram_dev = static_cast<double*>(alloc(sizeof(double) * 16 * 16));
     std::vector<const float*> wt;
-    for (auto& ln : learners) wt.push_back(ln.w[k & 1]);
+    for (auto& ln : learners) wt.push_back(ln.w[slot(k)]);
     launch_gram(D, L, wt.data(), gram_dev, s_main);
     std::vector<double> G(static_cast<size_t>(L) * L);
     AB_CUDA(cudaMemcpyAsync(G.data(), gram_dev, sizeof(double) * L * L, cudaMemcpyDeviceToHost, s_main));
@@ -1258,11 +1386,11 @@ void Ctx::gossip_probe(int left, int right, int reps, double* out) {
         AB_CUDA(cudaMemsetAsync(probe_buf[0], 0, D * sizeof(float), s));
     }
     if (!scratch_w) scratch_w = static_cast<float*>(alloc(D * sizeof(float)));
-    const int cur = static_cast<int>(k & 1);
+    const int cur = slot(k);
     const Learner& ln = learners[0];
     // stand-ins at N = 1: the learner's spare weight buffer and its gradient buffer (distinct
     // 4 D-byte streams, so nothing is served from L2)
-    const float* wl = left >= 0 ? weight_ptr(left, cur) : ln.w[cur ^ 1];
+    const float* wl = left >= 0 ? weight_ptr(left, cur) : ln.w[slot(k + 1)];
     const float* wr = right >= 0 ? weight_ptr(right, cur) : probe_buf[0];
     const double nv = (left >= 0 && !is_local(left) ? 4.0 * D : 0.0) + (right >= 0 && !is_local(right) ? 4.0 * D : 0.0);
     launch_mix3(D, ln.w[cur], wl, wr, ln.g, 0.0f, scratch_w, probe_shadow, s);  // warm

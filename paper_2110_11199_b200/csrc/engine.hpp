@@ -20,11 +20,16 @@ namespace ab {
 
 class Comm;
 
-// engine.hpp:67-72 (LearnerState): model (double-buffered fp32 master + bf16 shadow),
+// engine.hpp:67-72 (LearnerState): model (fp32 master in a ring of nbuf versions + bf16 shadow),
 // history (GENERIC), sampling stream.
 struct Learner {
     int gid = 0;
-    float* w[2] = {nullptr, nullptr};
+    // version v of the model lives in w[v % nbuf]: nbuf = 2 (double buffer) for the synchronous
+    // strategies, 4 for free-running async FM/RM (the publication ring, chronos.cpp:258-259)
+    float* w[4] = {nullptr, nullptr, nullptr, nullptr};
+    // publication counters, device memory exported over CUDA IPC: [0] = last published version,
+    // [1] = version being written (its slot is being overwritten); async FM/RM only
+    unsigned long long* ver = nullptr;
     float* g = nullptr;
     bf16* shadow = nullptr;          // bf16 copy of the current model (GEMM operand)
     std::vector<bf16*> l1pad;        // layer-1 W_ih per direction, rows padded for TMA
@@ -32,6 +37,8 @@ struct Learner {
     Rng rng{0};
     double straggle = 1.0;
     float last_compute_ms = 0.f;
+    double delay_ms = 0.0;       // fixed extra time per step (emulated compute, straggler studies)
+    bool delay_on_host = false;  // ... as a host sleep (processes sharing one GPU) or a device spin
 };
 
 struct Ctx {
@@ -50,6 +57,8 @@ struct Ctx {
     int ldH = 0, ldY = 0;     // row pitch of the layer outputs / projection output
     int64_t k = 0;
     int history_depth = 1;
+    int nbuf = 2;  // model versions per learner (Learner::w)
+    int slot(int64_t v) const { return static_cast<int>(v % nbuf); }
 
     cudaStream_t s_main = nullptr, s_comm = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_mix = nullptr, ev_comp0 = nullptr, ev_comp1 = nullptr;
@@ -167,6 +176,17 @@ struct Ctx {
               const double* injected);
     double gradient(const double* w, const int32_t* idx, int M, double* g_out);
     void gossip_probe(int left, int right, int reps, double* out4);
+    // free-running async FM / RM across processes (engine.cu async_*)
+    int async_mode = -1;  // -1 off; ADPSGD_ASYNC_FREE / _LOCKSTEP / _BOUNDED
+    int64_t async_lag = 0;
+    double async_timeout_s = 60.0;
+    void* async_sel = nullptr;       // device selection record (AsyncSel, kernels.cuh)
+    void* async_sel_host = nullptr;  // pinned mirror
+    void async_init(int mode, int64_t max_lag, double timeout_s);
+    void async_step(double lr, float* loss_out, adpsgd_async_info* info);
+    void host_delay(const Learner& ln);
+    double extra_delay_ms(const Learner& ln) const;
+    bool ipc_exported = false;
     float* probe_buf[2] = {nullptr, nullptr};
     bf16* probe_shadow = nullptr;
 };

@@ -533,6 +533,93 @@ __global__ void synth_kernel(float* __restrict__ feats, int32_t* __restrict__ la
     }
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return static_cast<long long>(v);
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+constexpr int kAsyncFree = 0, kAsyncLockstep = 1, kAsyncBounded = 2;
+
+__global__ void async_select_kernel(AsyncPeers pe, int mode, long long k, long long lag, unsigned long long* my_ver,
+                                    AsyncSel* sel, unsigned long long timeout_ns) {
+    if (threadIdx.x != 0) return;
+    const unsigned long long t0 = gtimer();
+    sel->torn = 0;
+    sel->err = 0;
+    for (int side = 0; side < 2; ++side) {
+        long long v = ld_acquire_sys(pe.ver[side]);
+        const bool wait = mode == kAsyncLockstep || mode == kAsyncBounded;
+        const long long need = mode == kAsyncLockstep ? k : k - lag;
+        while (wait && v < need) {
+            if (gtimer() - t0 > timeout_ns) {
+                sel->err = 1;
+                return;
+            }
+            __nanosleep(2000);
+            v = ld_acquire_sys(pe.ver[side]);
+        }
+        const long long c = mode == kAsyncLockstep ? k : v;
+        sel->ptr[side] = pe.slots[side][c & 3];
+        sel->ver[side] = c;
+    }
+    sel->wait_ns = static_cast<long long>(gtimer() - t0);
+    // slot (k + 1) % 4 is about to be overwritten: readers of version k - 3 must see it first
+    st_relaxed_sys(my_ver + 1, static_cast<unsigned long long>(k + 1));
+    __threadfence_system();
+}
+
+__global__ void mix3_sel_kernel(int64_t n, const float* __restrict__ w, const AsyncSel* __restrict__ sel,
+                                const float* __restrict__ g, float lr, float* __restrict__ out, bf16* __restrict__ shadow) {
+    if (sel->err) return;
+    const float* __restrict__ wl = sel->ptr[0];
+    const float* __restrict__ wr = sel->ptr[1];
+    const float third = 1.0f / 3.0f;
+    const int64_t n4 = n / 4;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4; i += stride) {
+        const float4 a = reinterpret_cast<const float4*>(w)[i];
+        const float4 b = reinterpret_cast<const float4*>(wl)[i];
+        const float4 c = reinterpret_cast<const float4*>(wr)[i];
+        const float4 d = reinterpret_cast<const float4*>(g)[i];
+        float4 o;
+        o.x = (a.x + b.x + c.x) * third - lr * d.x;
+        o.y = (a.y + b.y + c.y) * third - lr * d.y;
+        o.z = (a.z + b.z + c.z) * third - lr * d.z;
+        o.w = (a.w + b.w + c.w) * third - lr * d.w;
+        reinterpret_cast<float4*>(out)[i] = o;
+        if (shadow) {
+            reinterpret_cast<__nv_bfloat162*>(shadow)[2 * i] = __floats2bfloat162_rn(o.x, o.y);
+            reinterpret_cast<__nv_bfloat162*>(shadow)[2 * i + 1] = __floats2bfloat162_rn(o.z, o.w);
+        }
+    }
+    for (int64_t i = n4 * 4 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
+        const float o = (w[i] + wl[i] + wr[i]) * third - lr * g[i];
+        out[i] = o;
+        if (shadow) shadow[i] = __float2bfloat16_rn(o);
+    }
+}
+
+__global__ void async_publish_kernel(AsyncPeers pe, AsyncSel* sel, unsigned long long* my_ver, long long k) {
+    if (threadIdx.x != 0 || sel->err) return;
+    __threadfence_system();  // the mix (previous kernel) has read the neighbour slots
+    const long long wl = ld_acquire_sys(pe.ver[0] + 1), wr = ld_acquire_sys(pe.ver[1] + 1);
+    const int torn = (wl >= sel->ver[0] + 4) || (wr >= sel->ver[1] + 4);
+    sel->torn = torn;
+    if (!torn) st_release_sys(my_ver, static_cast<unsigned long long>(k + 1));
+}
+
 __global__ void delay_kernel(uint64_t ns) {
     uint64_t t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
@@ -725,6 +812,29 @@ void launch_maxdiff(int64_t n, const float* a, const float* b, float* out, cudaS
 void launch_synth(float* feats, int32_t* labels, int n_seg, int T, int I, int C, uint64_t seed, cudaStream_t s) {
     ProfScope ps_(s, PROF_OTHER, 0, (double)n_seg * T * I * 4);
     synth_kernel<<<grid_for(static_cast<int64_t>(n_seg) * T * I), 256, 0, s>>>(feats, labels, n_seg, T, I, C, seed);
+    count_launch();
+}
+
+void launch_async_select(const AsyncPeers& pe, int mode, long long k, long long lag, unsigned long long* my_ver,
+                         AsyncSel* sel, unsigned long long timeout_ns, cudaStream_t s) {
+    ProfScope ps_(s, PROF_MIX, 0, 0);
+    async_select_kernel<<<1, 32, 0, s>>>(pe, mode, k, lag, my_ver, sel, timeout_ns);
+    count_launch();
+}
+
+void launch_mix3_sel(int64_t n, const float* w, const AsyncSel* sel, const float* g, float lr, float* w_out,
+                     bf16* shadow, cudaStream_t s) {
+    ProfScope ps_(s, PROF_MIX, 0, (double)n * (20.0 + (shadow ? 2.0 : 0.0)));
+    AB_CHECK((reinterpret_cast<uintptr_t>(w) & 15) == 0 && (reinterpret_cast<uintptr_t>(w_out) & 15) == 0,
+             ADPSGD_E_INVALID_STATE, "mix3_sel: 16-byte aligned weights required");
+    mix3_sel_kernel<<<grid_for((n + 3) / 4, 256, 4), 256, 0, s>>>(n, w, sel, g, lr, w_out, shadow);
+    count_launch();
+}
+
+void launch_async_publish(const AsyncPeers& pe, AsyncSel* sel, unsigned long long* my_ver, long long k,
+                          cudaStream_t s) {
+    ProfScope ps_(s, PROF_MIX, 0, 0);
+    async_publish_kernel<<<1, 32, 0, s>>>(pe, sel, my_ver, k);
     count_launch();
 }
 

@@ -74,6 +74,34 @@ void launch_maxdiff(int64_t n, const float* a, const float* b, float* out, cudaS
 // Device synthetic dataset (hash-based, deterministic in (seed, n, t, i)).
 void launch_synth(float* feats, int32_t* labels, int n_seg, int T, int I, int C, uint64_t seed, cudaStream_t s);
 
+// ---- free-running async FM / RM: versioned publication ring (engine.cu Ctx::async_step) ----
+// Each learner's model version v lives in slot v % 4 of its ring; its counter block holds
+// [0] = last published version (release-stored at system scope once the slot is complete) and
+// [1] = version being written (announced before the slot's first byte is overwritten).
+struct AsyncPeers {
+    const unsigned long long* ver[2];  // left / right neighbour counter blocks (CUDA-IPC mapped)
+    const float* slots[2][4];          // their publication rings
+};
+struct AsyncSel {
+    const float* ptr[2];  // chosen neighbour versions' slots
+    long long ver[2];     // chosen versions
+    int torn;             // a neighbour began overwriting a chosen slot before the mix finished
+    int err;              // wait timed out
+    long long wait_ns;    // time spent waiting for neighbours
+};
+// select (1 thread): per neighbour, wait (mode LOCKSTEP: until version >= k; BOUNDED: >= k - lag;
+// FREE: never) with ld.acquire.sys, choose the version (LOCKSTEP: k, else the latest), then
+// announce this learner's write of version k + 1.
+void launch_async_select(const AsyncPeers& pe, int mode, long long k, long long lag, unsigned long long* my_ver,
+                         AsyncSel* sel, unsigned long long timeout_ns, cudaStream_t s);
+// FM/RM mix against the selected slots: w_out = (w + w_L + w_R) / 3 - lr g (+ bf16 shadow).
+void launch_mix3_sel(int64_t n, const float* w, const AsyncSel* sel, const float* g, float lr, float* w_out,
+                     bf16* shadow, cudaStream_t s);
+// publish (1 thread): torn-read check against the neighbours' write announcements, then a
+// release store of version k + 1 (only if nothing was torn; the host then retries the mix).
+void launch_async_publish(const AsyncPeers& pe, AsyncSel* sel, unsigned long long* my_ver, long long k,
+                          cudaStream_t s);
+
 // Device-side delay (straggler hook): spins for ns nanoseconds.
 void launch_delay(uint64_t ns, cudaStream_t s);
 

@@ -38,6 +38,14 @@ class MixKind(enum.IntEnum):
     UNIFORM = 2
 
 
+class AsyncMode(enum.IntEnum):
+    """adpsgd_async_mode: FREE reads neighbours' latest publications (never waits); LOCKSTEP reads
+    exactly version k (== synchronous FM/RM); BOUNDED waits until the latest is >= k - max_lag."""
+    FREE = 0
+    LOCKSTEP = 1
+    BOUNDED = 2
+
+
 class Precision(enum.IntEnum):
     FP32 = 0
     BF16 = 1
@@ -352,6 +360,29 @@ class LearnerGroup:
 
     def barrier(self) -> None:
         _lib.check(_lib.lib().adpsgd_barrier(self._h))
+
+    def async_init(self, mode: "AsyncMode" = None, max_lag: int = 0, timeout_s: float = 60.0) -> None:
+        """Free-running async FM / RM (one learner per process): switch to the 4-slot publication
+        ring (call before export_ipc)."""
+        mode = AsyncMode.FREE if mode is None else AsyncMode(mode)
+        _lib.check(_lib.lib().adpsgd_async_init(self._h, int(mode), max_lag, timeout_s))
+
+    def async_step(self, lr: float):
+        """One free-running iteration (no barrier): returns (loss, info dict: versions mixed with,
+        neighbours, torn-read retries, wait / step device ms)."""
+        loss = C.c_float()
+        info = _lib.AsyncInfo()
+        _lib.check(_lib.lib().adpsgd_async_step(self._h, lr, C.byref(loss), C.byref(info)))
+        return float(loss.value), {f: getattr(info, f) for f, _ in _lib.AsyncInfo._fields_ if f != "reserved"}
+
+    def last_gradient(self) -> np.ndarray:
+        """fp32 gradient of local learner 0's last step (diagnosis / async-consistency tests)."""
+        out = np.empty(self.D, dtype=np.float32)
+        _lib.check(_lib.lib().adpsgd_debug_buffer(self._h, 103, out.ctypes.data_as(C.c_void_p), out.nbytes))
+        return out
+
+    def set_step_delay(self, j: int, ms: float, on_host: bool = False) -> None:
+        _lib.check(_lib.lib().adpsgd_set_step_delay(self._h, j, ms, int(on_host)))
 
     def gossip_probe(self, left: int = -1, right: int = -1, reps: int = 5) -> dict:
         """Bandwidth of the FM/RM gossip path at this model size (adpsgd_gossip_probe): the fused
