@@ -82,6 +82,12 @@ typedef struct adpsgd_perf {
     double gossip_bytes;      /* bytes pulled from neighbours in the last step */
     int64_t steps;            /* global iteration counter k */
     int64_t kernel_launches;  /* this library's kernel launches so far */
+    /* D1D across ranks: device times (ms after the step's start) at which the weight allreduce on
+     * the comm stream started and finished, and at which the gradient compute finished; -1 when
+     * no allreduce ran in the last step. comm_end <= compute_end means the allreduce was hidden. */
+    double comm_start_ms;
+    double comm_end_ms;
+    double compute_end_ms;
 } adpsgd_perf;
 
 typedef struct adpsgd_ctx adpsgd_ctx;

@@ -33,7 +33,8 @@ class Config(C.Structure):
 
 class Perf(C.Structure):
     _fields_ = [("last_step_ms", C.c_double), ("last_mix_ms", C.c_double), ("gossip_bytes", C.c_double),
-                ("steps", i64), ("kernel_launches", i64)]
+                ("steps", i64), ("kernel_launches", i64), ("comm_start_ms", C.c_double),
+                ("comm_end_ms", C.c_double), ("compute_end_ms", C.c_double)]
 
 
 class AsyncInfo(C.Structure):

@@ -228,6 +228,9 @@ int adpsgd_get_stats(adpsgd_ctx* ctx, adpsgd_perf* out) {
         out->gossip_bytes = c.last_gossip_bytes;
         out->steps = c.k;
         out->kernel_launches = g_launch_count;
+        out->comm_start_ms = c.last_comm_start_ms;
+        out->comm_end_ms = c.last_comm_end_ms;
+        out->compute_end_ms = c.last_compute_end_ms;
     });
 }
 

@@ -10,6 +10,8 @@
 #include <string>
 
 #include "engine.hpp"
+#include "kernels.cuh"
+#include "knobs.hpp"
 
 namespace ab {
 
@@ -79,6 +81,7 @@ Comm::Comm(Ctx& c, int r, int w, const void* id128) : rank(r), world(w), D_(c.D)
         ipc_only = true;
         return;
     }
+    forced = w == 1 && knobs().comm_force;
     ncclUniqueId id;
     std::memcpy(&id, id128, sizeof(id));
     ncclComm_t comm;
@@ -91,6 +94,8 @@ Comm::Comm(Ctx& c, int r, int w, const void* id128) : rank(r), world(w), D_(c.D)
     AB_CUDA(cudaStreamSynchronize(c.s_main));
     AB_CUDA(cudaEventCreateWithFlags(&ev_start_, cudaEventDisableTiming));
     AB_CUDA(cudaEventCreateWithFlags(&ev_ws_, cudaEventDisableTiming));
+    AB_CUDA(cudaEventCreate(&t_ar0));
+    AB_CUDA(cudaEventCreate(&t_ar1));
 }
 
 void Comm::ensure_nb(Ctx& c) {
@@ -112,16 +117,29 @@ void Comm::prefetch_neighbours(Ctx& c, const float* wl, const float* wr, cudaStr
     AB_CUDA(cudaEventRecord(nb_ready, c.s_comm));
 }
 
-void Comm::sendrecv_neighbours(Ctx& c, int left, int right, cudaStream_t s) {
+void Comm::sendrecv_neighbours(Ctx& c, int j, int left, int right, cudaStream_t s) {
     AB_CHECK(!ipc_only, ADPSGD_E_CONFIG, "gossip mode 2 (NCCL send/recv) needs the NCCL transport");
     ensure_nb(c);
+    auto* comm = static_cast<ncclComm_t>(nccl_);
+    if (world == 1) {
+        // forced single-rank mode: every neighbour is local -- each one's w_k goes through an NCCL
+        // send / recv pair with this rank itself
+        AB_NCCL(nccl().GroupStart());
+        AB_NCCL(nccl().Send(c.weight_ptr(left, c.slot(c.k)), c.D, ncclFloat32, 0, comm, s));
+        AB_NCCL(nccl().Send(c.weight_ptr(right, c.slot(c.k)), c.D, ncclFloat32, 0, comm, s));
+        AB_NCCL(nccl().Recv(nb_[0], c.D, ncclFloat32, 0, comm, s));
+        AB_NCCL(nccl().Recv(nb_[1], c.D, ncclFloat32, 0, comm, s));
+        AB_NCCL(nccl().GroupEnd());
+        return;
+    }
+    AB_CHECK(c.cfg.local_learners == 1 && j == 0, ADPSGD_E_CONFIG, "NCCL send/recv gossip hosts one learner per rank");
     const float* w = c.learners[0].w[c.slot(c.k)];
     const int rl = left - c.cfg.first_learner + rank, rr = right - c.cfg.first_learner + rank;  // one learner per rank
     AB_NCCL(nccl().GroupStart());
-    AB_NCCL(nccl().Send(w, c.D, ncclFloat32, rl, static_cast<ncclComm_t>(nccl_), s));
-    AB_NCCL(nccl().Send(w, c.D, ncclFloat32, rr, static_cast<ncclComm_t>(nccl_), s));
-    AB_NCCL(nccl().Recv(nb_[0], c.D, ncclFloat32, rl, static_cast<ncclComm_t>(nccl_), s));
-    AB_NCCL(nccl().Recv(nb_[1], c.D, ncclFloat32, rr, static_cast<ncclComm_t>(nccl_), s));
+    AB_NCCL(nccl().Send(w, c.D, ncclFloat32, rl, comm, s));
+    AB_NCCL(nccl().Send(w, c.D, ncclFloat32, rr, comm, s));
+    AB_NCCL(nccl().Recv(nb_[0], c.D, ncclFloat32, rl, comm, s));
+    AB_NCCL(nccl().Recv(nb_[1], c.D, ncclFloat32, rr, comm, s));
     AB_NCCL(nccl().GroupEnd());
 }
 
@@ -131,6 +149,8 @@ Comm::~Comm() {
     if (nccl_) nccl().CommDestroy(static_cast<ncclComm_t>(nccl_));
     if (ev_start_) cudaEventDestroy(ev_start_);
     if (ev_ws_) cudaEventDestroy(ev_ws_);
+    if (t_ar0) cudaEventDestroy(t_ar0);
+    if (t_ar1) cudaEventDestroy(t_ar1);
 }
 
 void Comm::barrier(cudaStream_t s) {
@@ -138,9 +158,20 @@ void Comm::barrier(cudaStream_t s) {
     AB_NCCL(nccl().AllReduce(bar_, bar_ + 1, 1, ncclFloat32, ncclSum, static_cast<ncclComm_t>(nccl_), s));
 }
 
+// Local learners' contribution in learner order (the single-process kernels' summation order),
+// then the sum over ranks in place.
+static const float* local_sum(Ctx& c, bool grads, float* buf, cudaStream_t s) {
+    if (c.cfg.local_learners == 1) return grads ? c.learners[0].g : c.learners[0].w[c.slot(c.k)];
+    std::vector<const float*> tab;
+    for (auto& ln : c.learners) tab.push_back(grads ? ln.g : ln.w[c.slot(c.k)]);
+    launch_sum_tab(c.D, static_cast<int>(tab.size()), tab.data(), buf, s);
+    return buf;
+}
+
 const float* Comm::allreduce_sum_grads(Ctx& c, cudaStream_t s) {
     AB_CHECK(!ipc_only, ADPSGD_E_CONFIG, "IPC-only transport: FM / RM only (SDPSGD needs NCCL)");
-    AB_NCCL(nccl().AllReduce(c.learners[0].g, gsum_, c.D, ncclFloat32, ncclSum, static_cast<ncclComm_t>(nccl_), s));
+    const float* src = local_sum(c, true, gsum_, s);
+    AB_NCCL(nccl().AllReduce(src, gsum_, c.D, ncclFloat32, ncclSum, static_cast<ncclComm_t>(nccl_), s));
     return gsum_;
 }
 
@@ -149,9 +180,12 @@ void Comm::start_weight_sum(Ctx& c, cudaStream_t s) {
     // w_k is final once the previous iteration's update (enqueued on s) has run.
     AB_CUDA(cudaEventRecord(ev_start_, s));
     AB_CUDA(cudaStreamWaitEvent(c.s_comm, ev_start_, 0));
-    const float* w = c.learners[0].w[c.slot(c.k)];
-    AB_NCCL(nccl().AllReduce(w, wsum_, c.D, ncclFloat32, ncclSum, static_cast<ncclComm_t>(nccl_), c.s_comm));
+    AB_CUDA(cudaEventRecord(t_ar0, c.s_comm));
+    const float* src = local_sum(c, false, wsum_, c.s_comm);
+    AB_NCCL(nccl().AllReduce(src, wsum_, c.D, ncclFloat32, ncclSum, static_cast<ncclComm_t>(nccl_), c.s_comm));
+    AB_CUDA(cudaEventRecord(t_ar1, c.s_comm));
     AB_CUDA(cudaEventRecord(ev_ws_, c.s_comm));
+    ar_pending = true;
 }
 
 const float* Comm::wait_weight_sum(Ctx& c, cudaStream_t s) {

@@ -23,6 +23,14 @@ class Comm {
     int rank = 0, world = 1;
     bool ipc_only = false;  // no NCCL (ranks sharing one GPU): FM/RM peer gossip, host-separated steps
     int gossip_mode = 0;  // 0 direct peer loads, 1 copy-engine prefetch, 2 NCCL send/recv
+    // ADPSGD_COMM_FORCE=1 with a world-1 NCCL communicator: take every multi-rank branch (device
+    // barrier, D1D weight allreduce overlapped with the compute, SDPSGD gradient allreduce, NCCL
+    // send/recv gossip as self exchanges) so those call sites run, and are checked, on one GPU
+    bool forced = false;
+    bool multi() const { return world > 1 || forced; }
+    // device-time stamps (ms after the step's start event) of the last D1D weight allreduce
+    cudaEvent_t t_ar0 = nullptr, t_ar1 = nullptr;
+    bool ar_pending = false;  // a D1D weight allreduce was issued this step (t_ar0 / t_ar1 valid)
 
     // SDPSGD: sum of every learner's gradient (in place in a comm buffer).
     const float* allreduce_sum_grads(Ctx& c, cudaStream_t s);
@@ -39,7 +47,7 @@ class Comm {
     // stream (issued at step start, overlapping the gradient compute; `ready` event joined by the mix)
     void prefetch_neighbours(Ctx& c, const float* wl, const float* wr, cudaStream_t s);
     // gossip_mode 2 (baseline): NCCL send of w_k to both neighbours / receive of theirs, on s
-    void sendrecv_neighbours(Ctx& c, int left, int right, cudaStream_t s);
+    void sendrecv_neighbours(Ctx& c, int j, int left, int right, cudaStream_t s);
     const float* nb_left() const { return nb_[0]; }
     const float* nb_right() const { return nb_[1]; }
     cudaEvent_t nb_ready = nullptr;

@@ -673,7 +673,7 @@ void Ctx::sample_indices(Learner& ln, int j) {
 // learner (every strategy is SGD, engine.cpp:245-247) and every gradient block comes from a
 // tcgen05 GEMM (bf16 mode, bias gradients folded into the GEMMs, T > 1).
 bool Ctx::fused_update_ok() const {
-    if (!(knobs().fused_update && bf16_mode && cfg.learners == 1 && cfg.local_learners == 1 && !(comm && comm->world > 1)))
+    if (!(knobs().fused_update && bf16_mode && cfg.learners == 1 && cfg.local_learners == 1 && !(comm && comm->multi())))
         return false;
     if (!fold_bias || !fold_ih_ok || T < 2) return false;
     for (int l = 0; l < lay.L; ++l)
@@ -777,7 +777,7 @@ void Ctx::run_compute(int j, int mode, const float* wpt, cudaStream_t s, int par
 int64_t Ctx::async_run(int strategy, const double* durations, int64_t target, int ipe, const double* lr_per_epoch,
                        int n_epochs, int32_t* ev_learner, double* ev_time) {
     AB_CHECK(strategy == ADPSGD_FM || strategy == ADPSGD_RM, ADPSGD_E_CONFIG, "coupled async runs FM or RM");
-    AB_CHECK(!(comm && comm->world > 1) && cfg.local_learners == cfg.learners, ADPSGD_E_CONFIG,
+    AB_CHECK(!(comm && comm->multi()) && cfg.local_learners == cfg.learners, ADPSGD_E_CONFIG,
              "coupled async: every learner hosted by this context");
     const int L = cfg.learners;
     AB_CHECK(L >= 3, ADPSGD_E_CONFIG, "FM/RM mixing requires at least 3 learners");
@@ -900,7 +900,7 @@ void Ctx::mix_and_update(double lr_d, const int32_t* taus) {
     if (fused_done) {
         // the weight-gradient GEMMs already wrote w[nxt] = w[cur] - lr g and the shadow
     } else if (strategy == ADPSGD_SDPSGD) {
-        if (comm && comm->world > 1) {
+        if (comm && comm->multi()) {
             // gradient allreduce (sum over ranks of the local sums), then the shared update
             const float* gsum = comm->allreduce_sum_grads(*this, s);
             launch_sdpsgd(D, Lg, learners[0].w[cur], nullptr, gsum, nloc, lr, otab.data(), stab.data(), s);
@@ -908,12 +908,12 @@ void Ctx::mix_and_update(double lr_d, const int32_t* taus) {
             launch_sdpsgd(D, Lg, learners[0].w[cur], gtab.data(), nullptr, nloc, lr, otab.data(), stab.data(), s);
         }
     } else if (strategy == ADPSGD_D1D) {
-        if (comm && comm->world > 1 && comm->ipc_only) {
+        if (comm && comm->multi() && comm->ipc_only) {
             // CUDA-IPC-only transport: the mean reads every learner's w_k directly (learner order,
             // as the local path); w_k is final because the caller separates steps on the host
             for (int gid = 0; gid < Lg; ++gid) wtab.push_back(weight_ptr(gid, cur));
             launch_d1d(D, Lg, wtab.data(), nullptr, nloc, gtab.data(), lr, otab.data(), stab.data(), s);
-        } else if (comm && comm->world > 1) {
+        } else if (comm && comm->multi()) {
             const float* wsum = comm->wait_weight_sum(*this, s);  // allreduce started before the compute
             launch_d1d(D, Lg, nullptr, wsum, nloc, gtab.data(), lr, otab.data(), stab.data(), s);
         } else {
@@ -921,8 +921,8 @@ void Ctx::mix_and_update(double lr_d, const int32_t* taus) {
             launch_d1d(D, Lg, wtab.data(), nullptr, nloc, gtab.data(), lr, otab.data(), stab.data(), s);
         }
     } else if (strategy == ADPSGD_FM || strategy == ADPSGD_RM) {
-        const int mode = (comm && comm->world > 1) ? comm->gossip_mode : 0;
-        if (comm && comm->world > 1 && mode == 0) comm->pre_gossip(*this, s);
+        const int mode = (comm && comm->multi()) ? comm->gossip_mode : 0;
+        if (comm && comm->multi() && mode == 0) comm->pre_gossip(*this, s);
         for (int j = 0; j < nloc; ++j) {
             int left, right;
             neighbours(strategy, learners[j].gid, &left, &right);
@@ -932,7 +932,7 @@ void Ctx::mix_and_update(double lr_d, const int32_t* taus) {
                 AB_CUDA(cudaStreamWaitEvent(s, comm->nb_ready, 0));
                 wl = comm->nb_left(); wr = comm->nb_right();
             } else if (mode == 2) {  // NCCL send / recv baseline
-                comm->sendrecv_neighbours(*this, left, right, s);
+                comm->sendrecv_neighbours(*this, j, left, right, s);
                 wl = comm->nb_left(); wr = comm->nb_right();
             }
             if (!is_local(left)) last_gossip_bytes += D * 4.0;
@@ -940,7 +940,7 @@ void Ctx::mix_and_update(double lr_d, const int32_t* taus) {
             launch_mix3(D, learners[j].w[cur], wl, wr, learners[j].g, lr, learners[j].w[nxt], stab[j], s);
         }
     } else {  // GENERIC: W T - lr G(tau-lagged), engine.cpp:186-204
-        AB_CHECK(!(comm && comm->world > 1), ADPSGD_E_CONFIG, "GENERIC staleness is single-process only");
+        AB_CHECK(!(comm && comm->multi()), ADPSGD_E_CONFIG, "GENERIC staleness is single-process only");
         std::vector<double> Tm(static_cast<size_t>(Lg) * Lg, 0.0);
         const int kind = cfg.generic_mix;
         if (kind == ADPSGD_MIX_UNIFORM) {
@@ -1059,9 +1059,10 @@ void Ctx::step(double lr, const int32_t* taus, float* loss_out, const float* hos
     }
     AB_CUDA(cudaEventRecord(ev0, s));
     // D1D: start the weight allreduce on the comm stream before the gradient compute
-    if (strategy == ADPSGD_D1D && comm && comm->world > 1 && !comm->ipc_only) comm->start_weight_sum(*this, s);
+    if (strategy == ADPSGD_D1D && comm && comm->multi() && !comm->ipc_only) comm->start_weight_sum(*this, s);
     // FM / RM, gossip mode 1: the neighbours' w_k travel by copy engine while this learner computes
-    if ((strategy == ADPSGD_FM || strategy == ADPSGD_RM) && comm && comm->world > 1 && comm->gossip_mode == 1) {
+    if ((strategy == ADPSGD_FM || strategy == ADPSGD_RM) && comm && comm->multi() && comm->gossip_mode == 1) {
+        AB_CHECK(cfg.local_learners == 1, ADPSGD_E_CONFIG, "gossip mode 1 (copy-engine prefetch) hosts one learner per rank");
         int left, right;
         neighbours(strategy, learners[0].gid, &left, &right);
         comm->prefetch_neighbours(*this, weight_ptr(left, slot(k)), weight_ptr(right, slot(k)), s);
@@ -1125,6 +1126,16 @@ void Ctx::step(double lr, const int32_t* taus, float* loss_out, const float* hos
     AB_CUDA(cudaEventElapsedTime(&mms, ev_mix, ev1));
     last_step_ms = ms;
     last_mix_ms = mms;
+    last_compute_end_ms = ms - mms;
+    last_comm_start_ms = last_comm_end_ms = -1;
+    if (comm && comm->ar_pending) {  // the D1D weight allreduce on the comm stream (overlap evidence)
+        float a = 0, b = 0;
+        AB_CUDA(cudaEventElapsedTime(&a, ev0, comm->t_ar0));
+        AB_CUDA(cudaEventElapsedTime(&b, ev0, comm->t_ar1));
+        last_comm_start_ms = a;
+        last_comm_end_ms = b;
+        comm->ar_pending = false;
+    }
     for (auto& ln : learners) {
         if (ln.straggle > 1.0 || ln.delay_ms > 0) {
             float cm = 0;

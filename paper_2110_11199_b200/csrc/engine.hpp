@@ -63,6 +63,7 @@ struct Ctx {
     cudaStream_t s_main = nullptr, s_comm = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_mix = nullptr, ev_comp0 = nullptr, ev_comp1 = nullptr;
     double last_step_ms = 0, last_mix_ms = 0, last_gossip_bytes = 0;
+    double last_comm_start_ms = -1, last_comm_end_ms = -1, last_compute_end_ms = -1;
 
     // dataset (device)
     float* feats = nullptr;

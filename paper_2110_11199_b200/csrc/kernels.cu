@@ -406,6 +406,22 @@ __global__ void d1d_kernel(int64_t n, int L, PtrTab w, const float* __restrict__
 }
 
 // SDPSGD update (engine.cpp:145-153), float4-vectorised.
+// out = in[0] + in[1] + ... (learner order, the same summation order as d1d / sdpsgd kernels)
+__global__ void sum_tab_kernel(int64_t n, int L, PtrTab in, float* __restrict__ out) {
+    const int64_t n4 = n / 4;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4; i += stride) {
+        float4 s = reinterpret_cast<const float4*>(in.p[0])[i];
+        for (int l = 1; l < L; ++l) s = f4add(s, reinterpret_cast<const float4*>(in.p[l])[i]);
+        reinterpret_cast<float4*>(out)[i] = s;
+    }
+    for (int64_t i = n4 * 4 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
+        float s = in.p[0][i];
+        for (int l = 1; l < L; ++l) s += in.p[l][i];
+        out[i] = s;
+    }
+}
+
 __global__ void sdpsgd_kernel(int64_t n, int L, const float* __restrict__ w, PtrTab g, const float* __restrict__ g_sum,
                               int nloc, float lr, MutTab out, BfTab sh) {
     const float invL = 1.0f / static_cast<float>(L);
@@ -740,6 +756,15 @@ void launch_d1d(int64_t n, int L, const float* const* w_tab, const float* w_sum,
         for (int i = 0; i < L; ++i) w.p[i] = w_tab[i];
     for (int j = 0; j < nloc; ++j) { g.p[j] = g_tab[j]; o.p[j] = out_tab[j]; sh.p[j] = shadow_tab[j]; }
     d1d_kernel<<<grid_for((n + 3) / 4, 256, 4), 256, 0, s>>>(n, L, w, w_sum, nloc, g, lr, o, sh);
+    count_launch();
+}
+
+void launch_sum_tab(int64_t n, int L, const float* const* tab, float* out, cudaStream_t s) {
+    ProfScope ps_(s, PROF_MIX, 0, (double)n * 4.0 * (L + 1));
+    AB_CHECK(L >= 1 && L <= kMaxTab, ADPSGD_E_CONFIG, "sum_tab: 1..64 inputs");
+    PtrTab t{};
+    for (int i = 0; i < L; ++i) t.p[i] = tab[i];
+    sum_tab_kernel<<<grid_for((n + 3) / 4, 256, 4), 256, 0, s>>>(n, L, t, out);
     count_launch();
 }
 

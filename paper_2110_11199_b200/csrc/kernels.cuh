@@ -59,6 +59,8 @@ void launch_mix3(int64_t n, const float* w, const float* wl, const float* wr, co
 // w_sum != nullptr supplies a precomputed sum (allreduce result) instead of the w[] table.
 void launch_d1d(int64_t n, int L, const float* const* w_tab, const float* w_sum, int nloc, const float* const* g_tab,
                 float lr, float* const* out_tab, bf16* const* shadow_tab, cudaStream_t s);
+// out = sum_i tab[i] in learner order (the local part of a multi-rank weight / gradient sum)
+void launch_sum_tab(int64_t n, int L, const float* const* tab, float* out, cudaStream_t s);
 // SDPSGD: w_out[j] = w - lr * (sum_i g[i]) / L (engine.cpp:145-153); g_sum as for d1d.
 void launch_sdpsgd(int64_t n, int L, const float* w, const float* const* g_tab, const float* g_sum, int nloc,
                    float lr, float* const* out_tab, bf16* const* shadow_tab, cudaStream_t s);

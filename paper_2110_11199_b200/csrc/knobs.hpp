@@ -29,6 +29,7 @@ struct Knobs {
     int force_bn = 0;          // ADPSGD_FORCE_BN=128|256: generic GEMM tile width (probes)
     int epi_skip = 0;          // ADPSGD_EPI_SKIP=n: epilogue timing experiments
     int export_dbg = 0;        // ADPSGD_EXPORT_DBG=1|2: split-K export diagnosis
+    bool comm_force = false;   // ADPSGD_COMM_FORCE=1: a world-1 NCCL communicator takes the multi-rank branches (tests)
     int async_hold_ms = 0;     // ADPSGD_ASYNC_HOLD_MS=n: device delay between the first async mix and its torn-read check (tests the retry path)
     int split_max = 4;         // ADPSGD_SPLIT_MAX=n: K slices of the one-wave split-K weight gradients (1: off)
     bool fwd_u32 = true;       // ADPSGD_NO_FWD_U32=1: persistent forward always in 64-unit tiles

@@ -319,7 +319,8 @@ class LearnerGroup:
         p = _lib.Perf()
         _lib.check(_lib.lib().adpsgd_get_stats(self._h, C.byref(p)))
         return {"last_step_ms": p.last_step_ms, "last_mix_ms": p.last_mix_ms, "gossip_bytes": p.gossip_bytes,
-                "steps": p.steps, "kernel_launches": p.kernel_launches}
+                "steps": p.steps, "kernel_launches": p.kernel_launches, "comm_start_ms": p.comm_start_ms,
+                "comm_end_ms": p.comm_end_ms, "compute_end_ms": p.compute_end_ms}
 
     def consensus_distance(self) -> float:
         out = C.c_double()
