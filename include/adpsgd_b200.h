@@ -153,6 +153,15 @@ int adpsgd_consensus_distance(adpsgd_ctx* ctx, double* out);
 int adpsgd_eval_loss(adpsgd_ctx* ctx, const double* w, const int32_t* idx, int32_t M, double* loss_out);
 /* engine.cpp:124-128 averaged_model over the local learners (fp64 host vector). */
 int adpsgd_averaged_model(adpsgd_ctx* ctx, double* out, int64_t n);
+/* Multi-rank consensus distance (mixing.cpp:159-180 with one learner per GPU): the L x L Gram
+ * (row-major, L = cfg.learners) of every global learner's deviation from the learner mean over
+ * parameters [begin, end) -- local models and peers mapped over NVLink (adpsgd_import_ipc). Each
+ * rank computes its shard, the shards are summed across ranks, then adpsgd_consensus_from_gram. */
+int adpsgd_consensus_gram(adpsgd_ctx* ctx, int64_t begin, int64_t end, double* gram);
+/* sqrt(largest eigenvalue) of a symmetric PSD L x L Gram (L <= 16). */
+int adpsgd_consensus_from_gram(const double* gram, int32_t L, double* out);
+/* averaged_model over ALL global learners (mapped peers included), fp64, learner order. */
+int adpsgd_averaged_model_all(adpsgd_ctx* ctx, double* out, int64_t n);
 
 /* chronos::coupled_async (chronos.cpp:178-299) on the device: FM/RM learners iterate at their
  * own rates (durations[l] seconds per update = max(compute_l x straggler_l, comm_pairwise),
@@ -163,6 +172,17 @@ int adpsgd_averaged_model(adpsgd_ctx* ctx, double* out, int64_t n);
 int adpsgd_async_run(adpsgd_ctx* ctx, int32_t strategy, const double* durations, int64_t target, int32_t ipe,
                      const double* lr_per_epoch, int32_t n_epochs, int32_t* event_learner, double* event_time,
                      int64_t* processed);
+
+/* ---- single-process multi-GPU drop-in (engine.cpp:212-304 drives all L learners from one process) ----
+ * Link n contexts that together host learners [0, L) (typically one context per GPU, each with the same
+ * config but its own device / first_learner / local_learners): every context then reads the others'
+ * weights (and, for SDPSGD, gradients) in place -- direct NVLink peer loads after
+ * cudaDeviceEnablePeerAccess, no IPC, no NCCL. */
+int adpsgd_group_link(adpsgd_ctx* const* ctxs, int32_t n);
+/* One iteration k of every linked context, the GPUs running concurrently: all gradient computes are
+ * launched, then all mixes / updates (SDPSGD's waits on the other contexts' gradients by CUDA events),
+ * then all are joined. loss_out[cfg.learners] (nullable) in global learner order. */
+int adpsgd_group_step(adpsgd_ctx* const* ctxs, int32_t n, double lr, float* loss_out);
 
 /* ---- free-running asynchronous FM / RM across processes (one learner per process) ----
  * chronos::coupled_async's semantics on real clocks (chronos.cpp:171-176, 237-259): every learner

@@ -69,6 +69,9 @@ _SIGS = {
     "adpsgd_consensus_distance": (C.c_int, [C.c_void_p, P(C.c_double)]),
     "adpsgd_eval_loss": (C.c_int, [C.c_void_p, P(C.c_double), P(i32), i32, P(C.c_double)]),
     "adpsgd_averaged_model": (C.c_int, [C.c_void_p, P(C.c_double), i64]),
+    "adpsgd_consensus_gram": (C.c_int, [C.c_void_p, i64, i64, P(C.c_double)]),
+    "adpsgd_consensus_from_gram": (C.c_int, [P(C.c_double), i32, P(C.c_double)]),
+    "adpsgd_averaged_model_all": (C.c_int, [C.c_void_p, P(C.c_double), i64]),
     "adpsgd_async_run": (C.c_int, [C.c_void_p, i32, P(C.c_double), i64, i32, P(C.c_double), i32, P(i32),
                                    P(C.c_double), P(i64)]),
     "adpsgd_nccl_unique_id": (C.c_int, [C.c_void_p]),
@@ -78,6 +81,8 @@ _SIGS = {
     "adpsgd_import_ipc": (C.c_int, [C.c_void_p, i32, i32, i32, C.c_void_p, i64]),
     "adpsgd_set_gossip_mode": (C.c_int, [C.c_void_p, i32]),
     "adpsgd_barrier": (C.c_int, [C.c_void_p]),
+    "adpsgd_group_link": (C.c_int, [P(C.c_void_p), i32]),
+    "adpsgd_group_step": (C.c_int, [P(C.c_void_p), i32, C.c_double, P(C.c_float)]),
     "adpsgd_async_init": (C.c_int, [C.c_void_p, i32, i32, C.c_double]),
     "adpsgd_async_step": (C.c_int, [C.c_void_p, C.c_double, P(C.c_float), P(AsyncInfo)]),
     "adpsgd_set_step_delay": (C.c_int, [C.c_void_p, i32, C.c_double, i32]),

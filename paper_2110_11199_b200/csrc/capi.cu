@@ -1,5 +1,6 @@
 // extern "C" boundary (include/adpsgd_b200.h). Every entry point converts library
 // exceptions into adpsgd_status codes and records the message for adpsgd_last_error().
+#include <algorithm>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -253,6 +254,25 @@ int adpsgd_eval_loss(adpsgd_ctx* ctx, const double* w, const int32_t* idx, int32
     return guard([&] { *loss_out = C_(ctx).evaluate(w, idx, M, nullptr); });
 }
 
+int adpsgd_consensus_gram(adpsgd_ctx* ctx, int64_t begin, int64_t end, double* gram) {
+    return guard([&] { C_(ctx).consensus_gram(begin, end, gram); });
+}
+
+int adpsgd_consensus_from_gram(const double* gram, int32_t L, double* out) {
+    return guard([&] {
+        AB_CHECK(gram && out && L >= 1 && L <= 16, ADPSGD_E_DIMENSION, "consensus_from_gram: 1 <= L <= 16");
+        *out = consensus_from_gram(gram, L);
+    });
+}
+
+int adpsgd_averaged_model_all(adpsgd_ctx* ctx, double* out, int64_t n) {
+    return guard([&] {
+        Ctx& c = C_(ctx);
+        AB_CHECK(n == c.D, ADPSGD_E_DIMENSION, "averaged model length != parameter count");
+        c.averaged_model_all(out);
+    });
+}
+
 int adpsgd_averaged_model(adpsgd_ctx* ctx, double* out, int64_t n) {
     return guard([&] {
         Ctx& c = C_(ctx);
@@ -312,6 +332,61 @@ int adpsgd_set_gossip_mode(adpsgd_ctx* ctx, int32_t mode) {
         AB_CHECK(mode >= 0 && mode <= 2, ADPSGD_E_CONFIG, "gossip mode must be 0, 1 or 2");
         AB_CHECK(c.comm, ADPSGD_E_INVALID_STATE, "adpsgd_comm_init first");
         c.comm->gossip_mode = mode;
+    });
+}
+
+int adpsgd_group_link(adpsgd_ctx* const* ctxs, int32_t n) {
+    return guard([&] {
+        AB_CHECK(ctxs && n >= 1, ADPSGD_E_CONFIG, "group: at least one context");
+        std::vector<Ctx*> cs;
+        for (int i = 0; i < n; ++i) cs.push_back(&C_(ctxs[i]));
+        std::sort(cs.begin(), cs.end(), [](const Ctx* a, const Ctx* b) { return a->cfg.first_learner < b->cfg.first_learner; });
+        const adpsgd_config& c0 = cs[0]->cfg;
+        int next = 0;
+        for (Ctx* c : cs) {
+            AB_CHECK(c->cfg.first_learner == next, ADPSGD_E_CONFIG, "group: contexts must host contiguous learner ranges from 0");
+            next += c->cfg.local_learners;
+            AB_CHECK(std::memcmp(&c->cfg.model, &c0.model, sizeof(c0.model)) == 0 && c->cfg.strategy == c0.strategy &&
+                         c->cfg.learners == c0.learners && c->cfg.batch == c0.batch && c->cfg.seed == c0.seed &&
+                         c->cfg.precision == c0.precision && c->k == cs[0]->k && c->nbuf == cs[0]->nbuf,
+                     ADPSGD_E_CONFIG, "group: contexts differ in model / strategy / learners / batch / seed / precision / iteration");
+            AB_CHECK(!c->comm, ADPSGD_E_INVALID_STATE, "group: context already has a communicator");
+        }
+        AB_CHECK(next == c0.learners, ADPSGD_E_CONFIG, "group: contexts must host all cfg.learners learners");
+        for (Ctx* a : cs)
+            for (Ctx* b : cs)
+                if (a->cfg.device != b->cfg.device) {
+                    AB_CUDA(cudaSetDevice(a->cfg.device));
+                    const cudaError_t e = cudaDeviceEnablePeerAccess(b->cfg.device, 0);
+                    if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+                    else AB_CUDA(e);
+                }
+        for (size_t i = 0; i < cs.size(); ++i) {
+            Ctx* c = cs[i];
+            c->comm = std::make_unique<Comm>(*c, static_cast<int>(i), static_cast<int>(cs.size()), Comm::LocalGroupTag{});
+            c->comm->group_ctxs = cs;
+            for (Ctx* o : cs)
+                if (o != c) c->comm->link_local(*o);
+        }
+    });
+}
+
+int adpsgd_group_step(adpsgd_ctx* const* ctxs, int32_t n, double lr, float* loss_out) {
+    return guard([&] {
+        AB_CHECK(ctxs && n >= 1, ADPSGD_E_CONFIG, "group: at least one context");
+        std::vector<Ctx*> cs;
+        for (int i = 0; i < n; ++i) cs.push_back(&C_(ctxs[i]));
+        for (Ctx* c : cs)
+            AB_CHECK(n == 1 || (c->comm && c->comm->local_group && static_cast<int>(c->comm->group_ctxs.size()) == n),
+                     ADPSGD_E_INVALID_STATE, "group: adpsgd_group_link these contexts first");
+        for (Ctx* c : cs) c->step_compute(lr, nullptr, nullptr, nullptr, nullptr);  // all GPUs compute concurrently
+        for (Ctx* c : cs) c->step_mix(lr, nullptr);
+        std::vector<float> part(64);
+        for (Ctx* c : cs) {
+            c->step_finish(part.data(), false);
+            if (loss_out)
+                for (int j = 0; j < c->cfg.local_learners; ++j) loss_out[c->cfg.first_learner + j] = part[j];
+        }
     });
 }
 

@@ -98,6 +98,32 @@ Comm::Comm(Ctx& c, int r, int w, const void* id128) : rank(r), world(w), D_(c.D)
     AB_CUDA(cudaEventCreate(&t_ar1));
 }
 
+Comm::Comm(Ctx& c, int r, int w, LocalGroupTag) : rank(r), world(w), D_(c.D) {
+    AB_CHECK(w >= 1 && r >= 0 && r < w, ADPSGD_E_CONFIG, "bad group rank/size");
+    ipc_only = true;  // the host joins every context at the end of each group step
+    local_group = true;
+}
+
+// Map a linked context's learners into this one: weights, publication counters and gradients are
+// read in place (same process; P2P over NVLink when the devices differ).
+void Comm::link_local(Ctx& peer) {
+    for (const Learner& ln : peer.learners) {
+        PeerMap pm;
+        pm.nbuf = peer.nbuf;
+        for (int b = 0; b < peer.nbuf; ++b) pm.w[b] = ln.w[b];
+        pm.ver = ln.ver;
+        pm.g = ln.g;
+        peers_[ln.gid] = pm;
+    }
+}
+
+const float* Comm::peer_grad(int gid) const {
+    auto it = peers_.find(gid);
+    AB_CHECK(it != peers_.end() && it->second.g, ADPSGD_E_INVALID_STATE,
+             "learner " + std::to_string(gid) + "'s gradient is not mapped (single-process groups only)");
+    return it->second.g;
+}
+
 void Comm::ensure_nb(Ctx& c) {
     if (!nb_[0]) {
         nb_[0] = static_cast<float*>(c.alloc(c.D * sizeof(float)));

@@ -17,6 +17,14 @@ struct Ctx;
 class Comm {
   public:
     Comm(Ctx& ctx, int rank, int world, const void* nccl_id128);
+    // single-process group transport (adpsgd_group_link): no NCCL, no IPC -- the other contexts'
+    // buffers are read in place (cudaDeviceEnablePeerAccess across devices)
+    struct LocalGroupTag {};
+    Comm(Ctx& ctx, int rank, int world, LocalGroupTag);
+    bool local_group = false;
+    std::vector<Ctx*> group_ctxs;
+    void link_local(Ctx& peer);
+    const float* peer_grad(int gid) const;
     ~Comm();
     static void unique_id(void* out128);
 
@@ -67,6 +75,7 @@ class Comm {
         float* w[4] = {nullptr, nullptr, nullptr, nullptr};  // model versions (ring of nbuf)
         int nbuf = 0;
         unsigned long long* ver = nullptr;                   // publication counters
+        const float* g = nullptr;                            // gradient (single-process group only)
     };
     std::map<int, PeerMap> peers_;  // gid -> that learner's buffers mapped over NVLink (CUDA IPC)
     std::vector<void*> opened_;

@@ -900,7 +900,15 @@ void Ctx::mix_and_update(double lr_d, const int32_t* taus) {
     if (fused_done) {
         // the weight-gradient GEMMs already wrote w[nxt] = w[cur] - lr g and the shadow
     } else if (strategy == ADPSGD_SDPSGD) {
-        if (comm && comm->multi()) {
+        if (comm && comm->local_group) {
+            // single-process group: every learner's gradient read in place (NVLink peer loads), in
+            // learner order, once the other contexts' gradient computes have finished
+            for (Ctx* o : comm->group_ctxs)
+                if (o != this) AB_CUDA(cudaStreamWaitEvent(s, o->ev_mix, 0));
+            std::vector<const float*> gall;
+            for (int gid = 0; gid < Lg; ++gid) gall.push_back(grad_ptr(gid));
+            launch_sdpsgd(D, Lg, learners[0].w[cur], gall.data(), nullptr, nloc, lr, otab.data(), stab.data(), s);
+        } else if (comm && comm->multi()) {
             // gradient allreduce (sum over ranks of the local sums), then the shared update
             const float* gsum = comm->allreduce_sum_grads(*this, s);
             launch_sdpsgd(D, Lg, learners[0].w[cur], nullptr, gsum, nloc, lr, otab.data(), stab.data(), s);
@@ -1006,6 +1014,12 @@ const float* Ctx::weight_ptr(int gid, int buf) const {
     AB_CHECK(comm != nullptr, ADPSGD_E_INVALID_STATE, "neighbour weights not mapped (call adpsgd_import_ipc)");
     return comm->peer_weight(gid, buf);
 }
+const float* Ctx::grad_ptr(int gid) const {
+    const int j = gid - cfg.first_learner;
+    if (j >= 0 && j < cfg.local_learners) return learners[j].g;
+    AB_CHECK(comm != nullptr, ADPSGD_E_INVALID_STATE, "neighbour gradients not mapped");
+    return comm->peer_grad(gid);
+}
 bool Ctx::is_local(int gid) const {
     return gid >= cfg.first_learner && gid < cfg.first_learner + cfg.local_learners;
 }
@@ -1026,10 +1040,12 @@ const float* Ctx::grad_point(const Learner& ln, const int32_t* taus) {
 void Ctx::check_sync() {
     // engine.cpp:139-144 — models must agree within 1e-12 before an SDPSGD step
     // (local learners; identical fp32 arithmetic keeps them bit-identical).
-    if (cfg.local_learners < 2) return;
+    const bool group = comm && comm->local_group && cfg.first_learner != 0;
+    if (cfg.local_learners < 2 && !group) return;
     const int cur = slot(k);
     AB_CUDA(cudaMemsetAsync(scratch_f, 0, sizeof(float), s_main));
     for (int j = 1; j < cfg.local_learners; ++j) launch_maxdiff(D, learners[j].w[cur], learners[0].w[cur], scratch_f, s_main);
+    if (group) launch_maxdiff(D, learners[0].w[cur], weight_ptr(0, cur), scratch_f, s_main);  // vs global learner 0
     float h = 0;
     AB_CUDA(cudaMemcpyAsync(&h, scratch_f, sizeof(float), cudaMemcpyDeviceToHost, s_main));
     AB_CUDA(cudaStreamSynchronize(s_main));
@@ -1038,6 +1054,15 @@ void Ctx::check_sync() {
 
 void Ctx::step(double lr, const int32_t* taus, float* loss_out, const float* host_feats, const int32_t* host_labels,
                const double* injected) {
+    step_compute(lr, taus, host_feats, host_labels, injected);
+    step_mix(lr, taus);
+    step_finish(loss_out, injected != nullptr);
+}
+
+// Phase 1 of an iteration: sampling, comm-stream starts, every local learner's gradient (graph
+// replays) on s_main; returns without waiting (ev_mix marks the gradients done).
+void Ctx::step_compute(double lr, const int32_t* taus, const float* host_feats, const int32_t* host_labels,
+                       const double* injected) {
     AB_CUDA(cudaSetDevice(cfg.device));
     const int strategy = cfg.learners == 1 ? ADPSGD_SDPSGD : cfg.strategy;
     if (strategy == ADPSGD_SDPSGD) check_sync();
@@ -1109,11 +1134,22 @@ void Ctx::step(double lr, const int32_t* taus, float* loss_out, const float* hos
         if (bf16_mode && lagged) refresh_shadow(ln, ln.w[slot(k)], s);
     }
     AB_CUDA(cudaEventRecord(ev_mix, s));
+}
+
+// Phase 2: the mixing + update of cfg.strategy (engine.cpp:136-204).
+void Ctx::step_mix(double lr, const int32_t* taus) {
+    AB_CUDA(cudaSetDevice(cfg.device));
     fused_done = fuse_now;
     fuse_now = false;
     mix_and_update(lr, taus);
     fused_done = false;
-    AB_CUDA(cudaEventRecord(ev1, s));
+    AB_CUDA(cudaEventRecord(ev1, s_main));
+}
+
+// Phase 3: join, losses to the host, step statistics, host-side delays; k -> k + 1.
+void Ctx::step_finish(float* loss_out, bool injected) {
+    AB_CUDA(cudaSetDevice(cfg.device));
+    cudaStream_t s = s_main;
     if (!injected && loss_out) {
         AB_CUDA(cudaMemcpyAsync(h_loss, loss_dev, sizeof(float) * cfg.local_learners, cudaMemcpyDeviceToHost, s));
     }
@@ -1344,17 +1380,45 @@ double Ctx::consensus_distance() {
     AB_CUDA(cudaSetDevice(cfg.device));
     const int L = cfg.local_learners;
     if (L < 2) return 0.0;
-    if (!gram_dev) gram_dev = static_cast<double*>(alloc(sizeof(double) * 16 * 16));
     std::vector<const float*> wt;
     for (auto& ln : learners) wt.push_back(ln.w[slot(k)]);
-    launch_gram(D, L, wt.data(), gram_dev, s_main);
     std::vector<double> G(static_cast<size_t>(L) * L);
-    AB_CUDA(cudaMemcpyAsync(G.data(), gram_dev, sizeof(double) * L * L, cudaMemcpyDeviceToHost, s_main));
+    gram(wt, 0, D, G.data());
+    return consensus_from_gram(G.data(), L);
+}
+
+// Gram of the deviations from the learner mean over parameters [begin, end) of the given models.
+void Ctx::gram(const std::vector<const float*>& models, int64_t begin, int64_t end, double* out) {
+    const int L = static_cast<int>(models.size());
+    if (!gram_dev) gram_dev = static_cast<double*>(alloc(sizeof(double) * 16 * 16));
+    std::vector<const float*> wt;
+    for (const float* w : models) wt.push_back(w + begin);
+    launch_gram(end - begin, L, wt.data(), gram_dev, s_main);
+    AB_CUDA(cudaMemcpyAsync(out, gram_dev, sizeof(double) * L * L, cudaMemcpyDeviceToHost, s_main));
     AB_CUDA(cudaStreamSynchronize(s_main));
     for (int a = 0; a < L; ++a)
-        for (int b = 0; b < a; ++b) G[a * L + b] = G[b * L + a];
-    // symmetric PSD L x L: cyclic Jacobi eigenvalues (exact enough for L <= 16)
-    std::vector<double> A = G;
+        for (int b = 0; b < a; ++b) out[a * L + b] = out[b * L + a];
+}
+
+// The shard [begin, end) of the consensus Gram over ALL global learners: local ones and peers
+// mapped over NVLink (CUDA IPC). Ranks sum their shards (a small allreduce), then
+// consensus_from_gram -- the multi-rank form of mixing.cpp:159-180.
+void Ctx::consensus_gram(int64_t begin, int64_t end, double* out) {
+    AB_CHECK(0 <= begin && begin <= end && end <= D, ADPSGD_E_DIMENSION, "consensus shard outside [0, D)");
+    AB_CUDA(cudaSetDevice(cfg.device));
+    std::vector<const float*> wt;
+    for (int gid = 0; gid < cfg.learners; ++gid) wt.push_back(weight_ptr(gid, slot(k)));
+    const int L = cfg.learners;
+    if (end == begin) {
+        std::fill(out, out + static_cast<size_t>(L) * L, 0.0);
+        return;
+    }
+    gram(wt, begin, end, out);
+}
+
+// largest eigenvalue of the symmetric PSD L x L Gram by cyclic Jacobi (exact enough for L <= 16)
+double consensus_from_gram(const double* G, int L) {
+    std::vector<double> A(G, G + static_cast<size_t>(L) * L);
     for (int sweep = 0; sweep < 100; ++sweep) {
         double off = 0;
         for (int p = 0; p < L; ++p)
@@ -1382,6 +1446,21 @@ double Ctx::consensus_distance() {
     double lam = 0;
     for (int p = 0; p < L; ++p) lam = std::max(lam, A[p * L + p]);
     return std::sqrt(std::max(0.0, lam));
+}
+
+// engine.cpp:124-128 averaged_model over ALL global learners (mapped peers included), fp64
+// accumulation in learner order on the host.
+void Ctx::averaged_model_all(double* out) {
+    AB_CUDA(cudaSetDevice(cfg.device));
+    AB_CUDA(cudaStreamSynchronize(s_main));
+    std::vector<float> f(D);
+    std::fill(out, out + D, 0.0);
+    for (int gid = 0; gid < cfg.learners; ++gid) {
+        AB_CUDA(cudaMemcpyAsync(f.data(), weight_ptr(gid, slot(k)), D * sizeof(float), cudaMemcpyDeviceToHost, s_main));
+        AB_CUDA(cudaStreamSynchronize(s_main));
+        for (int64_t i = 0; i < D; ++i) out[i] += f[i];
+    }
+    for (int64_t i = 0; i < D; ++i) out[i] /= static_cast<double>(cfg.learners);
 }
 
 // Bandwidth of the gossip data path at this context's model size: the fused mix kernel (22 B per

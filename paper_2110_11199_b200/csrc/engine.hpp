@@ -166,6 +166,9 @@ struct Ctx {
     double evaluate(const double* w, const int32_t* idx, int M, double* g_out);
     void averaged_model(double* out);
     double consensus_distance();
+    void gram(const std::vector<const float*>& models, int64_t begin, int64_t end, double* out);
+    void consensus_gram(int64_t begin, int64_t end, double* out);
+    void averaged_model_all(double* out);
     double* gram_dev = nullptr;
     void mix_and_update(double lr, const int32_t* taus);
     const float* grad_point(const Learner& ln, const int32_t* taus);
@@ -175,6 +178,11 @@ struct Ctx {
     void check_sync();
     void step(double lr, const int32_t* taus, float* loss_out, const float* host_feats, const int32_t* host_labels,
               const double* injected);
+    void step_compute(double lr, const int32_t* taus, const float* host_feats, const int32_t* host_labels,
+                      const double* injected);
+    void step_mix(double lr, const int32_t* taus);
+    void step_finish(float* loss_out, bool injected);
+    const float* grad_ptr(int gid) const;
     double gradient(const double* w, const int32_t* idx, int M, double* g_out);
     void gossip_probe(int left, int right, int reps, double* out4);
     // free-running async FM / RM across processes (engine.cu async_*)
@@ -192,6 +200,7 @@ struct Ctx {
     bf16* probe_shadow = nullptr;
 };
 
+double consensus_from_gram(const double* G, int L);
 void set_last_error(const std::string& s);
 const char* last_error();
 

@@ -120,3 +120,33 @@ def connect(group, plumbing: Plumbing) -> None:
     handles = plumbing.all_gather_bytes(group.export_ipc())
     for r, h in enumerate(handles):
         group.import_ipc(r, r, 1, h)
+
+
+def shard_range(D: int, rank: int, world: int):
+    """Contiguous parameter shard [begin, end) of rank (sizes differ by at most one)."""
+    if not (0 <= rank < world):
+        raise ValueError("rank outside world")
+    q, r = divmod(D, world)
+    begin = rank * q + min(rank, r)
+    return begin, begin + q + (1 if rank < r else 0)
+
+
+def reduce_gram(partial, plumbing: "Plumbing"):
+    """Sum the ranks' consensus-Gram shards (a small gloo allreduce on the host)."""
+    import numpy as np
+    G = np.ascontiguousarray(partial, dtype=np.float64)
+    if plumbing.env.world == 1:
+        return G
+    import torch
+    t = torch.from_numpy(G.copy())
+    plumbing.dist.all_reduce(t)
+    return t.numpy()
+
+
+def consensus_distance(group, plumbing: "Plumbing") -> float:
+    """mixing.cpp:159-180 across ranks (one learner per GPU, engine.cpp:284-289): each rank reads
+    1/world of every learner's model -- its own from HBM, the others over NVLink -- into a Gram
+    shard; the shards are summed across ranks and the largest eigenvalue taken."""
+    from .engine import consensus_from_gram
+    b, e = shard_range(group.D, plumbing.env.rank, plumbing.env.world)
+    return consensus_from_gram(reduce_gram(group.consensus_gram(b, e), plumbing))

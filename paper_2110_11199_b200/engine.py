@@ -200,6 +200,7 @@ class LearnerGroup:
         cfg.validate()
         self.model, self.cfg, self.precision = model, cfg, Precision(precision)
         self.local = cfg.learners if local_learners is None else local_learners
+        self.first = first_learner
         c = _lib.Config()
         c.model = model.c()
         c.precision = int(precision)
@@ -332,6 +333,19 @@ class LearnerGroup:
         _lib.check(_lib.lib().adpsgd_averaged_model(self._h, _ptr(out, C.c_double), self.D))
         return out
 
+    def averaged_model_all(self) -> np.ndarray:
+        """averaged_model over every global learner (peers mapped over NVLink included)."""
+        out = np.zeros(self.D, dtype=np.float64)
+        _lib.check(_lib.lib().adpsgd_averaged_model_all(self._h, _ptr(out, C.c_double), self.D))
+        return out
+
+    def consensus_gram(self, begin: int, end: int) -> np.ndarray:
+        """Shard [begin, end) of the Gram of all global learners' deviations from their mean."""
+        L = self.cfg.learners
+        out = np.zeros(L * L, dtype=np.float64)
+        _lib.check(_lib.lib().adpsgd_consensus_gram(self._h, begin, end, _ptr(out, C.c_double)))
+        return out.reshape(L, L)
+
     def eval_loss(self, w, idx) -> float:
         w = np.ascontiguousarray(w, dtype=np.float64)
         idx = np.ascontiguousarray(idx, dtype=np.int32)
@@ -396,6 +410,73 @@ class LearnerGroup:
                 "mix_nvlink_gbs": nvlink_bytes / (mix_ms * 1e6) if mix_ms > 0 and nvlink_bytes else None,
                 "nvlink_bytes": nvlink_bytes, "copy_ms": copy_ms,
                 "copy_gbs": 8.0 * self.D / (copy_ms * 1e6) if copy_ms > 0 else None}
+
+
+class DeviceGroup:
+    """engine::run_training's vector<LearnerState> spread over several GPUs of ONE process
+    (engine.cpp:212-304): one context per entry of `devices`, hosting a contiguous share of the
+    cfg.learners learners, linked so that each reads the others' models (and SDPSGD gradients) in
+    place over NVLink (adpsgd_group_link); step() runs every GPU concurrently (adpsgd_group_step)."""
+
+    def __init__(self, model: ModelDesc, cfg: StrategyConfig, devices, precision: Precision = Precision.BF16,
+                 shares=None):
+        cfg.validate()
+        n = len(devices)
+        if shares is None:
+            q, r = divmod(cfg.learners, n)
+            shares = [q + (1 if i < r else 0) for i in range(n)]
+        if sum(shares) != cfg.learners or min(shares) < 1:
+            raise ConfigError("device group: shares must be >= 1 and sum to cfg.learners")
+        self.cfg, self.model = cfg, model
+        self.groups, first = [], 0
+        for dev, cnt in zip(devices, shares):
+            self.groups.append(LearnerGroup(model, cfg, precision=precision, device=dev, first_learner=first,
+                                            local_learners=cnt))
+            first += cnt
+        self._arr = (C.c_void_p * n)(*[g.handle for g in self.groups])
+        _lib.check(_lib.lib().adpsgd_group_link(self._arr, n))
+        self.D = self.groups[0].D
+
+    def _owner(self, gid: int):
+        for g in self.groups:
+            if g.first <= gid < g.first + g.local:
+                return g, gid - g.first
+        raise InvalidStateError(f"learner {gid} outside the group")
+
+    def set_dataset(self, feats, labels, train_count: int) -> None:
+        for g in self.groups:
+            g.set_dataset(feats, labels, train_count)
+
+    def step(self, lr: float) -> np.ndarray:
+        loss = np.zeros(self.cfg.learners, dtype=np.float32)
+        _lib.check(_lib.lib().adpsgd_group_step(self._arr, len(self.groups), lr, _ptr(loss, C.c_float)))
+        return loss
+
+    def weights(self, gid: int) -> np.ndarray:
+        g, j = self._owner(gid)
+        return g.weights(j)
+
+    def averaged_model(self) -> np.ndarray:
+        return self.groups[0].averaged_model_all()
+
+    def consensus_distance(self) -> float:
+        """Each context reduces its share of the parameters over every learner (peer loads), the
+        shards are summed on the host (mixing.cpp:159-180)."""
+        from .dist import shard_range
+        G = sum(g.consensus_gram(*shard_range(self.D, i, len(self.groups))) for i, g in enumerate(self.groups))
+        return consensus_from_gram(G)
+
+    def close(self) -> None:
+        for g in self.groups:
+            g.close()
+
+
+def consensus_from_gram(gram) -> float:
+    """sqrt(lambda_max) of a consensus Gram (mixing.cpp:174-179)."""
+    G = np.ascontiguousarray(gram, dtype=np.float64)
+    out = C.c_double()
+    _lib.check(_lib.lib().adpsgd_consensus_from_gram(_ptr(G, C.c_double), G.shape[0], C.byref(out)))
+    return float(out.value)
 
 
 def nccl_unique_id() -> bytes:

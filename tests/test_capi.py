@@ -124,3 +124,16 @@ def test_wallclock_model_matches_reference_known_answers():
     assert CH.slowdown_experiment(S.ADPSGD_FM, h(16), [100.0], 20)[0]["ratio"] <= 2.0
     with pytest.raises(ConfigError):
         CH.slowdown_experiment(S.ADPSGD_FM, h(16), [0.5], 20)
+
+
+def test_consensus_from_gram_matches_numpy():
+    """adpsgd_consensus_from_gram (host Jacobi) = sqrt(lambda_max) as SelfAdjointEigenSolver gives
+    it (mixing.cpp:174-179); pure host code, no GPU."""
+    from paper_2110_11199_b200.engine import consensus_from_gram
+    rng = np.random.default_rng(5)
+    for L in (2, 3, 8, 16):
+        X = rng.normal(size=(L, 40))
+        X -= X.mean(axis=0)
+        G = X @ X.T
+        want = np.sqrt(np.linalg.eigvalsh(G).max())
+        assert abs(consensus_from_gram(G) - want) <= 1e-10 * want

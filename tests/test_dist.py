@@ -94,3 +94,47 @@ def test_gossip_bytes():
     assert D.gossip_ingress_bytes(Strategy.ADPSGD_FM, D_, 8) == 8 * D_
     assert D.gossip_ingress_bytes(Strategy.ADPSGD_D1D, D_, 8) == int(2 * 7 / 8 * 4 * D_)
     assert D.gossip_ingress_bytes(Strategy.ADPSGD_RM, D_, 1) == 0
+
+
+def test_shard_ranges_cover_parameters():
+    for D_, world in ((145145344, 8), (10, 3), (2, 4), (0, 2)):
+        rs = [D.shard_range(D_, r, world) for r in range(world)]
+        assert rs[0][0] == 0 and rs[-1][1] == D_
+        assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
+        assert max(e - b for b, e in rs) - min(e - b for b, e in rs) <= 1
+
+
+def _gram_worker(rank, world, port, q):
+    os.environ.update({"RANK": str(rank), "WORLD_SIZE": str(world), "LOCAL_RANK": str(rank),
+                       "MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port)})
+    try:
+        P = D.Plumbing(D.rank_env())
+        rng = np.random.default_rng(0)
+        W = rng.normal(size=(3, 101))  # 3 learners' models, the same on every rank
+        b, e = D.shard_range(101, rank, world)
+        dev = W[:, b:e] - W[:, b:e].mean(axis=0)
+        G = D.reduce_gram(dev @ dev.T, P)
+        P.barrier()
+        q.put((rank, G))
+    except Exception as e:  # pragma: no cover
+        q.put((rank, repr(e)))
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_gram_sums_to_full_gram(world):
+    """The multi-rank consensus distance: per-rank Gram shards summed by the gloo allreduce equal
+    the Gram over the whole parameter vector (mixing.cpp:159-180)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_gram_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in ps:
+        p.join(timeout=60)
+    W = np.random.default_rng(0).normal(size=(3, 101))
+    dev = W - W.mean(axis=0)
+    for r in range(world):
+        assert not isinstance(res[r], str), res[r]
+        assert np.allclose(res[r], dev @ dev.T, rtol=1e-12, atol=1e-12)

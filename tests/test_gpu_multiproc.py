@@ -49,12 +49,21 @@ def _worker(rank, port, strategy, prec, mode, q):
         for _ in range(STEPS):
             losses.append(float(g.step(0.1)[0]))
             dist.barrier()  # every rank's w_{k+1} is written before anyone pulls it
-        q.put((rank, losses, g.weights(0)))
+        # multi-rank consensus distance (sharded Gram over NVLink-mapped peers + a gloo sum) and
+        # the all-learner averaged model (engine.cpp:124-128, 284-289; mixing.cpp:159-180)
+        import torch
+        from paper_2110_11199_b200.dist import shard_range
+        from paper_2110_11199_b200.engine import consensus_from_gram
+        b, e = shard_range(g.D, rank, WORLD)
+        part = torch.from_numpy(g.consensus_gram(b, e).copy())
+        dist.all_reduce(part)
+        extra = {"consensus": consensus_from_gram(part.numpy()), "avg": g.averaged_model_all()}
+        q.put((rank, losses, g.weights(0), extra))
         dist.barrier()
         g.close()
         dist.destroy_process_group()
     except Exception as e:  # surface worker failures in the parent
-        q.put((rank, repr(e), None))
+        q.put((rank, repr(e), None, None))
 
 
 def _free_port():
@@ -81,9 +90,9 @@ def test_multiprocess_ipc_gossip_equals_single_process_ring(strategy_name, prec_
         p.start()
     got = {}
     for _ in range(WORLD):
-        rank, losses, w = q.get(timeout=300)
+        rank, losses, w, extra = q.get(timeout=300)
         assert w is not None, f"rank {rank} failed: {losses}"
-        got[rank] = (losses, w)
+        got[rank] = (losses, w, extra)
     for p in procs:
         p.join(timeout=120)
     m = _model()
@@ -95,4 +104,9 @@ def test_multiprocess_ipc_gossip_equals_single_process_ring(strategy_name, prec_
     for r in range(WORLD):
         assert got[r][0] == [float(l[r]) for l in ref_losses], r
         assert np.array_equal(got[r][1], ref.weights(r)), r
+    want = ref.consensus_distance()
+    avg = ref.averaged_model()
+    for r in range(WORLD):
+        assert abs(got[r][2]["consensus"] - want) <= 1e-6 * max(want, 1e-12), (r, got[r][2]["consensus"], want)
+        assert np.array_equal(got[r][2]["avg"], avg), r
     ref.close()
