@@ -342,6 +342,13 @@ def run_ours(a):
     g_fl = sum(prof[c]["flops"] for c in cats)
     achieved = g_fl / (g_ms / 1000.0) / 1e12 if g_ms > 0 else 0.0
     peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
+    peak_kind = f"bf16_tflops_sustained ({pk_kind})"
+    if prec != Precision.BF16:
+        # FP32 engine: SIMT FFMA GEMMs; nominal fp32 peak = SMs x 128 lanes x 2 FLOP x max SM clock
+        props = torch.cuda.get_device_properties(dev)
+        mhz = clk.summary().get("sm_max_mhz") or 1965
+        peak = props.multi_processor_count * 128 * 2 * mhz * 1e6 / 1e12
+        peak_kind = "fp32 SIMT nominal (SMs x 128 x 2 x max SM clock)"
     traffic = None
     tp = os.path.join(ROOT, "profiles", "gemm_tc_traffic.json")
     if os.path.exists(tp):
@@ -383,11 +390,12 @@ def run_ours(a):
                 "d2h_bytes_per_step": 4, "steps": e2e_steps,
                 "h2d": "pinned host batch, prefetched one step ahead on a copy stream (adpsgd_prefetch_host_batch)"},
         "roofline": {"bound": "tensor",
-                     "kernel": "persistent_kernel_2cta<FwdPersistT<64>>: one launch per layer = 21 steps x 2 "
-                               "directions of the fused recurrent GEMM [x_t|h_t-1][W_ih|W_hh]^T + LSTM cell, "
-                               "tcgen05 cta_group::2 256x256 tiles",
+                     "kernel": ("persistent_kernel_2cta<FwdPersistT<64>>: one launch per layer = 21 steps x 2 "
+                                "directions of the fused recurrent GEMM [x_t|h_t-1][W_ih|W_hh]^T + LSTM cell, "
+                                "tcgen05 cta_group::2 256x256 tiles") if prec == Precision.BF16 else
+                               "simt_gemm (FP32 engine): all GEMMs, FFMA tiles",
                      "achieved": dom_tf, "peak": peak, "unit": "TFLOP/s", "frac": dom_tf / peak if peak else None,
-                     "peak_kind": f"bf16_tflops_sustained ({pk_kind})", "traffic": traffic,
+                     "peak_kind": peak_kind, "traffic": traffic if prec == Precision.BF16 else None,
                      "algorithmic_flops_per_launch": dom_flops, "launches_per_step": dom_launches,
                      "kernel_share_of_step": dom_ms / a.steps / prof_step_ms if prof_step_ms else None,
                      "all_tcgen05_gemms": {"achieved": achieved, "frac": achieved / peak if peak else None,

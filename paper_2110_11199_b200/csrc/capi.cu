@@ -2,6 +2,8 @@
 // exceptions into adpsgd_status codes and records the message for adpsgd_last_error().
 #include <algorithm>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <new>
 #include <vector>
 
@@ -35,6 +37,26 @@ int guard(F&& f) {
         set_last_error(e.what());
         return ADPSGD_E_INVALID_STATE;
     }
+}
+// Stream-K / split-K scratch of the standalone adpsgd_gemm entry point: one per device, owned by
+// the library for the life of the process (the engines bind their own; see GemmWorkspaceScope).
+const GemmWorkspace& standalone_gemm_workspace() {
+    static std::mutex mu;
+    static std::map<int, GemmWorkspace> per_dev;
+    int dev = 0;
+    AB_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = per_dev.find(dev);
+    if (it == per_dev.end()) {
+        GemmWorkspace w;
+        w.floats = static_cast<size_t>(num_sms() / 2) * 2 * 17 * 128 * 32;
+        w.flag_count = static_cast<size_t>(num_sms()) + 2 * 128;
+        AB_CUDA(cudaMalloc(&w.ws, w.floats * sizeof(float)));
+        AB_CUDA(cudaMalloc(&w.flags, w.flag_count * sizeof(unsigned int)));
+        AB_CUDA(cudaMemset(w.flags, 0, w.flag_count * sizeof(unsigned int)));
+        it = per_dev.emplace(dev, w).first;
+    }
+    return it->second;
 }
 Ctx& C_(adpsgd_ctx* c) {
     AB_CHECK(c && c->impl, ADPSGD_E_INVALID_STATE, "null context");
@@ -487,6 +509,7 @@ int adpsgd_gemm(int32_t bf, int32_t M, int32_t N, int32_t K, const void* A, int6
         g.seg[0].K = K;
         g.C = Cout; g.ldc = ldc; g.c_bf16 = c_bf16 != 0;
         g.alpha = alpha; g.accumulate = accumulate != 0; g.bias = bias;
+        GemmWorkspaceScope ws_scope(standalone_gemm_workspace());
         gemm(bf != 0, g, static_cast<cudaStream_t>(stream));
     });
 }

@@ -278,7 +278,7 @@ static inline void* off_ptr(void* p, int64_t elems, int es) { return static_cast
 // grad (fp32, flat layout) receives d(mean CE)/dw; loss_slot receives the mean CE.
 void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, float* loss_slot, cudaStream_t s,
                            bool backward, const FusedUpd* fu) {
-    set_gemm_workspace(gemm_ws);
+    GemmWorkspaceScope ws_scope(gemm_ws);
     const bool bf = bf16_mode;
     WView W{bf ? static_cast<const void*>(ln.shadow) : static_cast<const void*>(master), master, this, &ln};
     const int G4 = 4 * H;

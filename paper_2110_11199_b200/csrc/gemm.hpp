@@ -69,6 +69,15 @@ struct GemmWorkspace {
 };
 void set_gemm_workspace(const GemmWorkspace& w);
 const GemmWorkspace& gemm_workspace();
+// Binds a workspace for the GEMMs issued in this scope and restores the previous binding on exit,
+// so no thread keeps a pointer into an engine that has since been destroyed.
+struct GemmWorkspaceScope {
+    GemmWorkspace prev;
+    explicit GemmWorkspaceScope(const GemmWorkspace& w) : prev(gemm_workspace()) { set_gemm_workspace(w); }
+    ~GemmWorkspaceScope() { set_gemm_workspace(prev); }
+    GemmWorkspaceScope(const GemmWorkspaceScope&) = delete;
+    GemmWorkspaceScope& operator=(const GemmWorkspaceScope&) = delete;
+};
 bool gemm_wgrad_wide(int M, int N);  // see gemm_tc.cu  // tests: take the extra-column / stream-K kernels whenever the layout allows
 
 // fp32 operands, fp32 or bf16 output, any majorness (gemm_simt.cu).
