@@ -167,11 +167,35 @@ int adpsgd_averaged_model_all(adpsgd_ctx* ctx, double* out, int64_t n);
  * own rates (durations[l] seconds per update = max(compute_l x straggler_l, comm_pairwise),
  * chronos.cpp:51-58, 207), each update mixing with the neighbours' latest publications strictly
  * before its time; `target` updates in the reference's event order. lr of update round r is
- * lr_per_epoch[min(r / ipe, n_epochs - 1)]. event_learner / event_time (nullable, length target)
- * receive the event log. */
+ * lr_per_epoch[r / ipe] (no clamp, chronos.cpp:216: a fast learner can run past cfg.epochs x ipe
+ * rounds, so the table must cover (target - 1) / ipe + 1 epochs, else ADPSGD_E_CONFIG).
+ * event_learner / event_time (nullable, length target) receive the event log. */
 int adpsgd_async_run(adpsgd_ctx* ctx, int32_t strategy, const double* durations, int64_t target, int32_t ipe,
                      const double* lr_per_epoch, int32_t n_epochs, int32_t* event_learner, double* event_time,
                      int64_t* processed);
+
+/* The RunRecord of a coupled run (chronos.cpp:271-289): after every L updates the consensus
+ * distance of the learners' current models (mixing.cpp:159-180); after every L x ipe updates the
+ * held-out and full-train loss of their average, and the divergence rule (non-finite, or more than
+ * 10 x initial_heldout, engine.cpp:291-299) that stops the run. Inputs first, then outputs. */
+typedef struct adpsgd_async_record {
+    const int32_t* heldout_idx; /* segments of the held-out split (may be NULL with n_heldout 0) */
+    int32_t n_heldout;
+    const int32_t* train_idx;   /* segments of the full training split */
+    int32_t n_train;
+    double initial_heldout;     /* held-out loss of the initial averaged model */
+    double* consensus;          /* out [cap_iters]: k = updates / L - 1 */
+    int64_t cap_iters;
+    double* heldout;            /* out [cap_epochs] */
+    double* train;              /* out [cap_epochs] */
+    int32_t cap_epochs;
+    int64_t n_iters;            /* out: consensus points written */
+    int32_t n_epochs;           /* out: epoch points written */
+    int32_t diverged_epoch;     /* out: -1, or the epoch whose held-out loss diverged (run stopped) */
+} adpsgd_async_record;
+int adpsgd_async_run_record(adpsgd_ctx* ctx, int32_t strategy, const double* durations, int64_t target, int32_t ipe,
+                            const double* lr_per_epoch, int32_t n_epochs, int32_t* event_learner, double* event_time,
+                            adpsgd_async_record* record, int64_t* processed);
 
 /* ---- single-process multi-GPU drop-in (engine.cpp:212-304 drives all L learners from one process) ----
  * Link n contexts that together host learners [0, L) (typically one context per GPU, each with the same

@@ -42,6 +42,13 @@ class AsyncInfo(C.Structure):
                 ("retries", i32), ("reserved", i32), ("wait_ms", C.c_double), ("step_ms", C.c_double)]
 
 
+class AsyncRecord(C.Structure):  # adpsgd_async_record
+    _fields_ = [("heldout_idx", P(i32)), ("n_heldout", i32), ("train_idx", P(i32)), ("n_train", i32),
+                ("initial_heldout", C.c_double), ("consensus", P(C.c_double)), ("cap_iters", i64),
+                ("heldout", P(C.c_double)), ("train", P(C.c_double)), ("cap_epochs", i32), ("n_iters", i64),
+                ("n_epochs", i32), ("diverged_epoch", i32)]
+
+
 _SIGS = {
     "adpsgd_param_count": (i64, [P(ModelDesc)]),
     "adpsgd_permutation_for_iteration": (C.c_int, [u64, i32, i64, P(i32)]),
@@ -74,6 +81,8 @@ _SIGS = {
     "adpsgd_averaged_model_all": (C.c_int, [C.c_void_p, P(C.c_double), i64]),
     "adpsgd_async_run": (C.c_int, [C.c_void_p, i32, P(C.c_double), i64, i32, P(C.c_double), i32, P(i32),
                                    P(C.c_double), P(i64)]),
+    "adpsgd_async_run_record": (C.c_int, [C.c_void_p, i32, P(C.c_double), i64, i32, P(C.c_double), i32, P(i32),
+                                          P(C.c_double), P(AsyncRecord), P(i64)]),
     "adpsgd_nccl_unique_id": (C.c_int, [C.c_void_p]),
     "adpsgd_comm_init": (C.c_int, [C.c_void_p, i32, i32, C.c_void_p]),
     "adpsgd_ipc_handle_size": (i64, [C.c_void_p]),

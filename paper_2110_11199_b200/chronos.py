@@ -15,7 +15,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from .engine import LearnerGroup, Strategy, StrategyConfig, iterations_per_epoch, lr_at
+from .engine import (LearnerGroup, ModelDesc, Precision, RunRecord, Strategy, StrategyConfig, iterations_per_epoch,
+                     lr_at, run_training)
 from .errors import ConfigError
 
 
@@ -126,3 +127,69 @@ def coupled_run(profile: ClusterProfile, cfg: StrategyConfig, group: LearnerGrou
     lrs = [lr_at(cfg.lr, e) for e in range((target - 1) // ipe + 1)]
     ev, et = async_run(group, cfg.strategy, dur, target, ipe, lrs)
     return ev, et, float(et[-1]) if len(et) else 0.0
+
+
+@dataclass
+class CoupledResult:
+    record: RunRecord
+    total_time: float
+
+
+def coupled_training(profile: ClusterProfile, cfg: StrategyConfig, model: ModelDesc, feats, labels,
+                     train_count: int, precision: Precision = Precision.BF16, device: int = 0,
+                     synth: tuple | None = None) -> CoupledResult:
+    """chronos::coupled_run (chronos.cpp:303-321) with its RunRecord. FM/RM: the coupled
+    asynchronous replay on the device with the record of chronos.cpp:271-289 (consensus after
+    every L updates, per-epoch held-out / train loss of the averaged model, divergence stop);
+    synchronous strategies: run_training for the record and the cost model for the clock.
+    synth = (n_seg, seed) selects the device-generated dataset when feats is None."""
+    profile.validate()
+    cfg.validate()
+    if profile.learners != cfg.learners:
+        raise ConfigError("cluster profile learner count does not match strategy config")
+    ipe = iterations_per_epoch(cfg, train_count)
+    if cfg.strategy not in (Strategy.ADPSGD_FM, Strategy.ADPSGD_RM):
+        rec = run_training(cfg, model, feats, labels, train_count, precision=precision, device=device, synth=synth)
+        return CoupledResult(rec, simulate_wallclock(cfg.strategy, profile, ipe * cfg.epochs))
+    g = LearnerGroup(model, cfg, precision=precision, device=device)
+    try:
+        if feats is None:
+            n_seg, seed = synth
+            g.synth_dataset(n_seg, train_count, seed)
+        else:
+            g.set_dataset(feats, labels, train_count)
+            n_seg = np.asarray(feats).shape[0]
+        L = cfg.learners
+        held = np.arange(train_count, n_seg, dtype=np.int32)
+        train = np.arange(train_count, dtype=np.int32)
+        initial = g.eval_loss(g.averaged_model(), held) if len(held) else float("nan")
+        dur = np.ascontiguousarray([max(profile.effective_compute(l), profile.comm_pairwise) for l in range(L)],
+                                   dtype=np.float64)
+        target = cfg.epochs * ipe * L
+        lrs = np.ascontiguousarray([lr_at(cfg.lr, e) for e in range((target - 1) // ipe + 1)], dtype=np.float64)
+        cons = np.zeros(cfg.epochs * ipe, dtype=np.float64)
+        hl = np.zeros(cfg.epochs, dtype=np.float64)
+        tl = np.zeros(cfg.epochs, dtype=np.float64)
+        et = np.zeros(target, dtype=np.float64)
+        dp = C.POINTER(C.c_double)
+        ip = C.POINTER(C.c_int32)
+        r = _lib.AsyncRecord()
+        r.heldout_idx, r.n_heldout = held.ctypes.data_as(ip), len(held)
+        r.train_idx, r.n_train = train.ctypes.data_as(ip), len(train)
+        r.initial_heldout = initial
+        r.consensus, r.cap_iters = cons.ctypes.data_as(dp), len(cons)
+        r.heldout, r.train, r.cap_epochs = hl.ctypes.data_as(dp), tl.ctypes.data_as(dp), cfg.epochs
+        n = C.c_int64()
+        _lib.check(_lib.lib().adpsgd_async_run_record(g.handle, int(cfg.strategy), dur.ctypes.data_as(dp), target, ipe,
+                                                      lrs.ctypes.data_as(dp), len(lrs), None, et.ctypes.data_as(dp),
+                                                      C.byref(r), C.byref(n)))
+        rec = RunRecord()
+        rec.iterations = [(k, float(cons[k]), lr_at(cfg.lr, k // ipe)) for k in range(r.n_iters)]
+        rec.epochs = [(e, float(hl[e]), float(tl[e]), lr_at(cfg.lr, e)) for e in range(r.n_epochs)]
+        rec.diverged = r.diverged_epoch >= 0
+        rec.divergence_epoch = r.diverged_epoch
+        rec.iteration_count = len(rec.iterations)
+        rec.final_model = g.averaged_model()
+        return CoupledResult(rec, float(et[n.value - 1]) if n.value else 0.0)
+    finally:
+        g.close()

@@ -316,6 +316,31 @@ int adpsgd_async_run(adpsgd_ctx* ctx, int32_t strategy, const double* durations,
     });
 }
 
+int adpsgd_async_run_record(adpsgd_ctx* ctx, int32_t strategy, const double* durations, int64_t target, int32_t ipe,
+                            const double* lr_per_epoch, int32_t n_epochs, int32_t* event_learner, double* event_time,
+                            adpsgd_async_record* record, int64_t* processed) {
+    return guard([&] {
+        AB_CHECK(durations && lr_per_epoch && record, ADPSGD_E_CONFIG, "null durations / lr table / record");
+        for (int l = 0; l < C_(ctx).cfg.learners; ++l)
+            AB_CHECK(durations[l] > 0.0, ADPSGD_E_CONFIG, "cluster profile: compute_time must be > 0");
+        AB_CHECK(record->n_heldout >= 0 && record->n_train >= 0 && (record->n_heldout == 0 || record->heldout_idx) &&
+                     (record->n_train == 0 || record->train_idx),
+                 ADPSGD_E_CONFIG, "record: index lists");
+        for (int i = 0; i < record->n_heldout; ++i)
+            AB_CHECK(record->heldout_idx[i] >= 0 && record->heldout_idx[i] < C_(ctx).n_seg, ADPSGD_E_DIMENSION,
+                     "record: held-out index outside the dataset");
+        for (int i = 0; i < record->n_train; ++i)
+            AB_CHECK(record->train_idx[i] >= 0 && record->train_idx[i] < C_(ctx).n_seg, ADPSGD_E_DIMENSION,
+                     "record: train index outside the dataset");
+        record->n_iters = 0;
+        record->n_epochs = 0;
+        record->diverged_epoch = -1;
+        const int64_t n = C_(ctx).async_run(strategy, durations, target, ipe, lr_per_epoch, n_epochs, event_learner,
+                                            event_time, record);
+        if (processed) *processed = n;
+    });
+}
+
 int adpsgd_nccl_unique_id(void* out128) { return guard([&] { Comm::unique_id(out128); }); }
 
 int adpsgd_comm_init(adpsgd_ctx* ctx, int32_t rank, int32_t world, const void* id) {

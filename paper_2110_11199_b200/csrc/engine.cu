@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <limits>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -775,7 +776,7 @@ void Ctx::run_compute(int j, int mode, const float* wpt, cudaStream_t s, int par
 // The event order is the reference's min-heap order; gradients, mixing and publication run on
 // the GPU in that order. Returns the number of updates applied.
 int64_t Ctx::async_run(int strategy, const double* durations, int64_t target, int ipe, const double* lr_per_epoch,
-                       int n_epochs, int32_t* ev_learner, double* ev_time) {
+                       int n_epochs, int32_t* ev_learner, double* ev_time, adpsgd_async_record* rec) {
     AB_CHECK(strategy == ADPSGD_FM || strategy == ADPSGD_RM, ADPSGD_E_CONFIG, "coupled async runs FM or RM");
     AB_CHECK(!(comm && comm->multi()) && cfg.local_learners == cfg.learners, ADPSGD_E_CONFIG,
              "coupled async: every learner hosted by this context");
@@ -854,6 +855,7 @@ int64_t Ctx::async_run(int strategy, const double* durations, int64_t target, in
         ++round[l];
         ++processed;
         q.push({t_done + durations[l], l});
+        if (rec && observe_coupled(*rec, par, processed, ipe)) break;  // diverged
     }
     // leave every model in the context's current buffer
     for (int l = 0; l < L; ++l) {
@@ -1310,7 +1312,7 @@ double Ctx::gradient(const double* w, const int32_t* idx, int M, double* g_out) 
 
 // Loss (and, if g_out != nullptr, gradient) at w over the given segments, chunked by the
 // context batch B (the last chunk wraps); the mean is over all frames (objectives.cpp:144-157).
-double Ctx::evaluate(const double* w, const int32_t* idx, int M, double* g_out) {
+double Ctx::evaluate(const double* w, const int32_t* idx, int M, double* g_out, const float* restore) {
     AB_CHECK(!g_out || M == B, ADPSGD_E_DIMENSION, "gradient(): M must equal the context batch");
     AB_CHECK(M >= 1, ADPSGD_E_INVALID_STATE, "batch size must be >= 1");
     AB_CHECK(feats != nullptr, ADPSGD_E_INVALID_STATE, "dataset has no training samples");
@@ -1355,9 +1357,53 @@ double Ctx::evaluate(const double* w, const int32_t* idx, int M, double* g_out) 
         }
         result = total / (static_cast<double>(M) * T);
     }
-    refresh_shadow(ln, ln.w[slot(k)], s);
+    refresh_shadow(ln, restore ? restore : ln.w[slot(k)], s);
     AB_CUDA(cudaStreamSynchronize(s));
     return result;
+}
+
+// The coupled run's record (chronos.cpp:271-289) on the models the replay currently holds
+// (learner l's model is w[par[l]]). Returns true when the divergence rule stops the run.
+bool Ctx::observe_coupled(adpsgd_async_record& r, const std::vector<int>& par, int64_t processed, int ipe) {
+    const int L = cfg.learners;
+    if (processed % L == 0) {
+        const int64_t kk = processed / L - 1;
+        double c = 0.0;
+        if (L >= 2) {
+            std::vector<const float*> wt;
+            for (int l = 0; l < L; ++l) wt.push_back(learners[l].w[par[l]]);
+            std::vector<double> G(static_cast<size_t>(L) * L);
+            gram(wt, 0, D, G.data());
+            c = consensus_from_gram(G.data(), L);
+        }
+        if (r.consensus && kk < r.cap_iters) r.consensus[kk] = c;
+        r.n_iters = kk + 1;
+    }
+    if (processed % (static_cast<int64_t>(L) * ipe) != 0) return false;
+    const int epoch = static_cast<int>(processed / (static_cast<int64_t>(L) * ipe)) - 1;
+    // averaged_model (engine.cpp:124-128) of the current models, fp64 in learner order
+    std::vector<double> avg(D, 0.0);
+    std::vector<float> f(D);
+    AB_CUDA(cudaStreamSynchronize(s_main));
+    for (int l = 0; l < L; ++l) {
+        AB_CUDA(cudaMemcpy(f.data(), learners[l].w[par[l]], D * sizeof(float), cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < D; ++i) avg[i] += f[i];
+    }
+    for (int64_t i = 0; i < D; ++i) avg[i] /= static_cast<double>(L);
+    const float* keep = learners[0].w[par[0]];
+    const double nan = std::numeric_limits<double>::quiet_NaN();
+    const double h = r.n_heldout > 0 ? evaluate(avg.data(), r.heldout_idx, r.n_heldout, nullptr, keep) : nan;
+    const double t = r.n_train > 0 ? evaluate(avg.data(), r.train_idx, r.n_train, nullptr, keep) : nan;
+    if (epoch < r.cap_epochs) {
+        if (r.heldout) r.heldout[epoch] = h;
+        if (r.train) r.train[epoch] = t;
+    }
+    r.n_epochs = epoch + 1;
+    if (!std::isfinite(h) || h > 10.0 * r.initial_heldout) {
+        r.diverged_epoch = epoch;
+        return true;
+    }
+    return false;
 }
 
 // engine.cpp:124-128 (averaged_model) over the local learners, fp64 on the host.

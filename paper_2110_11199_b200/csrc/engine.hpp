@@ -11,6 +11,7 @@
 #include <string>
 #include <vector>
 
+#include "adpsgd_b200.h"
 #include "common.cuh"
 #include "model.hpp"
 #include "prof.hpp"
@@ -145,7 +146,7 @@ struct Ctx {
     void compute_body(int j, int mode, const float* wpt, cudaStream_t s);
     void run_compute(int j, int mode, const float* wpt, cudaStream_t s, int parity = -1);
     int64_t async_run(int strategy, const double* durations, int64_t target, int ipe, const double* lr_per_epoch,
-                      int n_epochs, int32_t* ev_learner, double* ev_time);
+                      int n_epochs, int32_t* ev_learner, double* ev_time, adpsgd_async_record* rec = nullptr);
     std::vector<float*> pubs;  // coupled-async publications, 4 per learner
     void clear_graphs();
     // Single learner (SGD, engine.cpp:245-247): the weight-gradient GEMM epilogues apply the update
@@ -163,10 +164,12 @@ struct Ctx {
     bool fused_done = false;    // mix_and_update: this step's update already happened
     float* lr_dev = nullptr;
     float* h_lr = nullptr;      // pinned
-    double evaluate(const double* w, const int32_t* idx, int M, double* g_out);
+    // restore: the model learner 0's bf16 shadow is rebuilt from afterwards (default: its current buffer)
+    double evaluate(const double* w, const int32_t* idx, int M, double* g_out, const float* restore = nullptr);
     void averaged_model(double* out);
     double consensus_distance();
     void gram(const std::vector<const float*>& models, int64_t begin, int64_t end, double* out);
+    bool observe_coupled(adpsgd_async_record& r, const std::vector<int>& par, int64_t processed, int ipe);
     void consensus_gram(int64_t begin, int64_t end, double* out);
     void averaged_model_all(double* out);
     double* gram_dev = nullptr;

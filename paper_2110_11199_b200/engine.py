@@ -525,16 +525,21 @@ def iterations_per_epoch(cfg: StrategyConfig, train_count: int) -> int:
 
 def run_training(cfg: StrategyConfig, model: ModelDesc, feats, labels, train_count: int,
                  precision: Precision = Precision.BF16, device: int = 0, consensus_every: int = 1,
-                 eval_train: bool = True) -> RunRecord:
+                 eval_train: bool = True, synth: tuple | None = None) -> RunRecord:
     """engine::run_training on the device: every local learner on one GPU, the mixing of
     cfg.strategy each iteration, consensus distance (every `consensus_every` iterations; the
     reference measures every iteration), per-epoch heldout / full-train loss of the averaged
-    model and the divergence rule (non-finite or > 10x the initial heldout loss)."""
+    model and the divergence rule (non-finite or > 10x the initial heldout loss).
+    synth = (n_seg, seed): with feats None, the device-generated synthetic dataset instead."""
     cfg.validate()
     g = LearnerGroup(model, cfg, precision=precision, device=device)
     try:
-        g.set_dataset(feats, labels, train_count)
-        n_seg = np.asarray(feats).shape[0]
+        if feats is None:
+            n_seg, seed = synth
+            g.synth_dataset(n_seg, train_count, seed)
+        else:
+            g.set_dataset(feats, labels, train_count)
+            n_seg = np.asarray(feats).shape[0]
         heldout_idx = np.arange(train_count, n_seg, dtype=np.int32)
         train_idx = np.arange(train_count, dtype=np.int32)
         rec = RunRecord()
@@ -571,16 +576,16 @@ def fmt_double(x: float) -> str:
     return "%.17g" % x
 
 
-def write_csv(record: RunRecord, out_dir: str) -> None:
-    """run.csv (epoch, heldout_loss, train_loss, lr) and consensus.csv (k, consensus, lr), the
-    schema written by tools/main.cpp:99-105."""
+def write_csv(record: RunRecord, out_dir: str, stem: str = "") -> None:
+    """<stem>run.csv (epoch,heldout_loss,lr) and <stem>consensus.csv (k,distance): the reference
+    CLI's write_run_outputs (tools/main.cpp:99-105), floats at 17 significant digits."""
     import os
     os.makedirs(out_dir, exist_ok=True)
-    with open(os.path.join(out_dir, "run.csv"), "w") as f:
-        f.write("epoch,heldout_loss,train_loss,lr\n")
-        for e, h, t, lr in record.epochs:
-            f.write(f"{e},{fmt_double(h)},{fmt_double(t)},{fmt_double(lr)}\n")
-    with open(os.path.join(out_dir, "consensus.csv"), "w") as f:
-        f.write("k,consensus,lr\n")
-        for k, c, lr in record.iterations:
-            f.write(f"{k},{fmt_double(c)},{fmt_double(lr)}\n")
+    with open(os.path.join(out_dir, stem + "run.csv"), "w") as f:
+        f.write("epoch,heldout_loss,lr\n")
+        for e, h, _t, lr in record.epochs:
+            f.write(f"{e},{fmt_double(h)},{fmt_double(lr)}\n")
+    with open(os.path.join(out_dir, stem + "consensus.csv"), "w") as f:
+        f.write("k,distance\n")
+        for k, c, _lr in record.iterations:
+            f.write(f"{k},{fmt_double(c)}\n")

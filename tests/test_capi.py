@@ -105,7 +105,11 @@ def test_csv_format_and_ipe():
     r = RunRecord(iterations=[(0, 0.5, 0.1)], epochs=[(0, 2.5, 2.25, 0.1)])
     with tempfile.TemporaryDirectory() as d:
         write_csv(r, d)
-        assert open(os.path.join(d, "consensus.csv")).read().splitlines() == ["k,consensus,lr", "0,0.5,0.10000000000000001"]
+        assert open(os.path.join(d, "consensus.csv")).read().splitlines() == ["k,distance", "0,0.5"]
+        assert open(os.path.join(d, "run.csv")).read().splitlines() == ["epoch,heldout_loss,lr",
+                                                                          "0,2.5,0.10000000000000001"]
+        write_csv(r, d, stem="ADPSGD_FM_f5_")
+        assert os.path.exists(os.path.join(d, "ADPSGD_FM_f5_run.csv"))
 
 
 def test_wallclock_model_matches_reference_known_answers():

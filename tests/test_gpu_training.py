@@ -58,7 +58,7 @@ def test_run_training_matches_oracle(oracle_mod, strategy, tmp_path):
     assert np.max(np.abs(rec.final_model - np.mean([ref.model(l) for l in range(4)], 0))) <= 1e-5
     write_csv(rec, str(tmp_path))
     lines = (tmp_path / "run.csv").read_text().splitlines()
-    assert lines[0] == "epoch,heldout_loss,train_loss,lr" and len(lines) == 3
+    assert lines[0] == "epoch,heldout_loss,lr" and len(lines) == 3
     assert float(lines[1].split(",")[1]) == rec.epochs[0][1]  # %.17g round-trips
 
 
