@@ -290,6 +290,9 @@ int adpsgd_debug_trace(int32_t enable, uint64_t* out, int32_t n);
  * l output H, 100 = Y, 101 = row_loss, 102 = bf16 shadow, 103 = last fp32 gradient, 200 + l = layer l cell state c,
  * 300 + l = layer l gates); bytes clipped to the buffer. */
 int adpsgd_debug_buffer(adpsgd_ctx* ctx, int32_t which, void* out, size_t bytes);
+/* Diagnosis: device address and size of an engine buffer (which as adpsgd_debug_buffer; 400 / 401 =
+ * the BPTT dH ping-pong buffers), to attribute sanitizer reports. */
+int adpsgd_debug_buffer_range(adpsgd_ctx* ctx, int32_t which, uint64_t* addr, uint64_t* bytes);
 
 /* ---- kernel-level entry points (tests / benchmarks; device pointers) ---- */
 /* C[M,N] = alpha * sum_k A(m,k) B(n,k) (+ C if accumulate) (+ bias[n]).

@@ -67,6 +67,7 @@ _SIGS = {
     "adpsgd_step_host_batch": (C.c_int, [C.c_void_p, C.c_double, P(C.c_float), P(i32), P(C.c_float)]),
     "adpsgd_prefetch_host_batch": (C.c_int, [C.c_void_p, P(C.c_float), P(i32)]),
     "adpsgd_debug_buffer": (C.c_int, [C.c_void_p, i32, C.c_void_p, C.c_size_t]),
+    "adpsgd_debug_buffer_range": (C.c_int, [C.c_void_p, i32, P(u64), P(u64)]),
     "adpsgd_step_injected": (C.c_int, [C.c_void_p, C.c_double, P(i32), P(C.c_double)]),
     "adpsgd_gradient": (C.c_int, [C.c_void_p, P(C.c_double), P(i32), i32, P(C.c_double), P(C.c_double)]),
     "adpsgd_set_straggler": (C.c_int, [C.c_void_p, i32, C.c_double]),

@@ -516,6 +516,25 @@ int adpsgd_debug_buffer(adpsgd_ctx* ctx, int32_t which, void* out, size_t bytes)
     });
 }
 
+// Device address range of an engine buffer (diagnosis: mapping sanitizer reports to buffers).
+// which: as adpsgd_debug_buffer, plus 400 / 401 = the two BPTT dH ping-pong buffers.
+int adpsgd_debug_buffer_range(adpsgd_ctx* ctx, int32_t which, uint64_t* addr, uint64_t* bytes) {
+    return guard([&] {
+        ab::Ctx& c = C_(ctx);
+        const size_t TB = static_cast<size_t>(c.TB);
+        const void* src = nullptr;
+        size_t n = 0;
+        if (which == 0) { src = c.X0; n = TB * c.Ipad * c.es; }
+        else if (which >= 1 && which <= c.lay.L) { src = c.Hout[which - 1]; n = TB * c.ldH * c.es; }
+        else if (which >= 200 && which < 200 + c.lay.L) { src = c.cst[which - 200]; n = TB * c.ndH * sizeof(float); }
+        else if (which >= 300 && which < 300 + c.lay.L) { src = c.gates[which - 300]; n = TB * c.nd4H * c.es; }
+        else if (which == 400 || which == 401) { src = which == 400 ? c.dHa : c.dHb; n = TB * c.ndH * sizeof(float); }
+        AB_CHECK(src != nullptr, ADPSGD_E_INVALID_STATE, "debug_buffer_range: no such buffer");
+        *addr = reinterpret_cast<uint64_t>(src);
+        *bytes = n;
+    });
+}
+
 int adpsgd_debug_trace(int32_t enable, uint64_t* out, int32_t n) {
     return guard([&] {
         if (out) ab::trace_read(reinterpret_cast<unsigned long long*>(out), n);

@@ -60,6 +60,7 @@ void Ctx::h2d_sync(void* dst, const void* src, size_t bytes) {
 void* Ctx::alloc(size_t bytes) {
     void* p = nullptr;
     AB_CUDA(cudaMalloc(&p, round_up(bytes ? bytes : 16, 256)));
+    if (knobs().poison_alloc >= 0) AB_CUDA(cudaMemset(p, knobs().poison_alloc & 0xFF, round_up(bytes ? bytes : 16, 256)));
     allocations.push_back(p);
     return p;
 }
@@ -1436,10 +1437,10 @@ double Ctx::consensus_distance() {
 // Gram of the deviations from the learner mean over parameters [begin, end) of the given models.
 void Ctx::gram(const std::vector<const float*>& models, int64_t begin, int64_t end, double* out) {
     const int L = static_cast<int>(models.size());
-    if (!gram_dev) gram_dev = static_cast<double*>(alloc(sizeof(double) * 16 * 16));
+    if (!gram_dev) gram_dev = static_cast<double*>(alloc(sizeof(double) * (16 * 16 + gram_partial_doubles())));
     std::vector<const float*> wt;
     for (const float* w : models) wt.push_back(w + begin);
-    launch_gram(end - begin, L, wt.data(), gram_dev, s_main);
+    launch_gram(end - begin, L, wt.data(), gram_dev, gram_dev + 16 * 16, s_main);
     AB_CUDA(cudaMemcpyAsync(out, gram_dev, sizeof(double) * L * L, cudaMemcpyDeviceToHost, s_main));
     AB_CUDA(cudaStreamSynchronize(s_main));
     for (int a = 0; a < L; ++a)

@@ -511,11 +511,20 @@ __global__ void gram_kernel(int64_t n, int L, PtrTab w, PairList pl, double* __r
         if (lane == 0 && wid < 8) sh[q][wid] = x;
     }
     __syncthreads();
-    if (threadIdx.x < pl.n) {
+    if (threadIdx.x < pl.n) {  // this block's partial; gram_reduce_kernel sums blocks in order (deterministic)
         double x = 0.0;
         for (int j = 0; j < (blockDim.x >> 5) && j < 8; ++j) x += sh[threadIdx.x][j];
-        atomicAdd(&G[pl.a[threadIdx.x] * L + pl.b[threadIdx.x]], x);
+        G[static_cast<int64_t>(blockIdx.x) * 36 + threadIdx.x] = x;
     }
+}
+
+__global__ void gram_reduce_kernel(int nblocks, int L, PairList pl, const double* __restrict__ part,
+                                   double* __restrict__ G) {
+    const int q = threadIdx.x;
+    if (q >= pl.n) return;
+    double x = 0.0;
+    for (int b = 0; b < nblocks; ++b) x += part[static_cast<int64_t>(b) * 36 + q];
+    G[pl.a[q] * L + pl.b[q]] = x;
 }
 
 __device__ __forceinline__ uint64_t hash64(uint64_t x) {
@@ -805,28 +814,31 @@ void launch_dense_mix(int64_t n, int L, const float* const* w_tab, const double*
     count_launch();
 }
 
-void launch_gram(int64_t n, int L, const float* const* w_tab, double* G, cudaStream_t s) {
+void launch_gram(int64_t n, int L, const float* const* w_tab, double* G, double* partial, cudaStream_t s) {
     AB_CHECK(L >= 1 && L <= 16, ADPSGD_E_CONFIG, "device consensus distance supports up to 16 local learners");
     ProfScope ps_(s, PROF_OTHER, 0, static_cast<double>(n) * 4 * L);
     PtrTab w{};
     for (int l = 0; l < L; ++l) w.p[l] = w_tab[l];
     AB_CUDA(cudaMemsetAsync(G, 0, sizeof(double) * L * L, s));
+    const int grid = grid_for(n, 256, 4);  // <= gram_partial_doubles() / 36 blocks
     PairList pl{};
+    auto run = [&] {
+        gram_kernel<<<grid, 256, 0, s>>>(n, L, w, pl, partial);
+        gram_reduce_kernel<<<1, 64, 0, s>>>(grid, L, pl, partial, G);
+        count_launch();
+        count_launch();
+        pl.n = 0;
+    };
     for (int a = 0; a < L; ++a)
         for (int b = a; b < L; ++b) {
             pl.a[pl.n] = a;
             pl.b[pl.n] = b;
-            if (++pl.n == 36) {
-                gram_kernel<<<grid_for(n, 256, 4), 256, 0, s>>>(n, L, w, pl, G);
-                count_launch();
-                pl.n = 0;
-            }
+            if (++pl.n == 36) run();
         }
-    if (pl.n) {
-        gram_kernel<<<grid_for(n, 256, 4), 256, 0, s>>>(n, L, w, pl, G);
-        count_launch();
-    }
+    if (pl.n) run();
 }
+
+size_t gram_partial_doubles() { return static_cast<size_t>(num_sms()) * 4 * 36; }
 
 void launch_maxdiff(int64_t n, const float* a, const float* b, float* out, cudaStream_t s) {
     ProfScope ps_(s, PROF_OTHER, 0, (double)n * 8);

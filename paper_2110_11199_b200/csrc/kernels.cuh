@@ -69,7 +69,10 @@ void launch_dense_mix(int64_t n, int L, const float* const* w_tab, const double*
                       const float* const* g_tab, float lr, float* const* out_tab, bf16* const* shadow_tab,
                       cudaStream_t s);
 // Upper triangle of the Gram of deviations from the learner mean (fp64), L <= 16.
-void launch_gram(int64_t n, int L, const float* const* w_tab, double* G, cudaStream_t s);
+// Gram of the deviations from the learner mean (fp64 sums, deterministic: per-block partials in
+// `partial` (>= gram_partial_doubles()) reduced in block order).
+void launch_gram(int64_t n, int L, const float* const* w_tab, double* G, double* partial, cudaStream_t s);
+size_t gram_partial_doubles();
 // max_j max_p |w_j[p] - w_0[p]| -> out (float, atomicMax on bits)
 void launch_maxdiff(int64_t n, const float* a, const float* b, float* out, cudaStream_t s);
 
