@@ -47,6 +47,34 @@ __device__ __forceinline__ float sigmoidf_(float x) { return 1.0f / (1.0f + __ex
 extern int64_t g_launch_count;
 inline void count_launch(int64_t n = 1) { g_launch_count += n; }
 
+// L2 persisting set-aside (reserved on first use; 0 when the device has none) and the largest
+// access-policy window.
+inline size_t l2_persist_bytes() {
+    static long long v = -1;
+    if (v < 0) {
+        int dev = 0, mx = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, dev);
+        size_t want = static_cast<size_t>(mx) < (size_t(64) << 20) ? static_cast<size_t>(mx) : (size_t(64) << 20);
+        size_t got = 0;
+        if (want && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) == cudaSuccess)
+            cudaDeviceGetLimit(&got, cudaLimitPersistingL2CacheSize);
+        cudaGetLastError();
+        v = static_cast<long long>(got);
+    }
+    return static_cast<size_t>(v);
+}
+inline size_t l2_window_max() {
+    static int v = -1;
+    if (v < 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+        if (v < 0) v = 0;
+    }
+    return static_cast<size_t>(v);
+}
+
 inline int num_sms() {
     static int sms = 0;
     if (!sms) {

@@ -866,7 +866,11 @@ template <int KQ, int UC = 64>
 struct BwdPersistTraits : tc::TraitsBase, BwdEpi {
     static constexpr int BN = UC * KQ;  // pair tile width
     static constexpr int NCHK = UC / 16;  // 16-unit chunks per finalised block
+#ifdef ADPSGD_BWD_EPI_WARPS
+    static constexpr int EPI_WARPS = ADPSGD_BWD_EPI_WARPS;  // A/B experiments
+#else
     static constexpr int EPI_WARPS = 8;
+#endif
     static constexpr int EPI_SMEM = EPI_WARPS * 12 * 1024;  // BwdEpi::body_g<64, INPLACE, .., NBUF = 1>
     static constexpr int ACC_STAGES = 2;
     static constexpr bool A_MN = false;
@@ -1197,6 +1201,25 @@ bool lstm_fwd_layer_persistent(const LstmFwdLayer& L, int ndirs, int B, int H, i
     p.dep = dep; p.exit_ctr = exit_ctr;
     p.trace = trace_take();
     const double bytes = 2.0 * T * (2.0 * (B + 4.0 * H) * (L.Kx + H) + static_cast<double>(B) * H * 22);
+    // ADPSGD_FWD_L2WIN=1: keep the layer's recurrent-kernel weights (read every step by the m-tiles)
+    // in the persisting L2 set-aside (the streaming gate / c / h stores otherwise evict them)
+    cudaAccessPolicyWindow win = {};
+    if (knobs().fwd_l2win && l2_persist_bytes() > 0) {
+        uintptr_t lo = UINTPTR_MAX, hi = 0;
+        for (int d = 0; d < 2; ++d) {
+            const uintptr_t a = reinterpret_cast<uintptr_t>(L.w_ih[d]), b = reinterpret_cast<uintptr_t>(L.w_hh[d]);
+            lo = std::min(lo, std::min(a, b));
+            hi = std::max(hi, std::max(a + static_cast<uintptr_t>(4 * H) * L.ld_wih * 2, b + static_cast<uintptr_t>(4 * H) * H * 2));
+        }
+        const size_t span = hi - lo, need = static_cast<size_t>(2) * 4 * H * (L.ld_wih + H) * 2;
+        if (span <= need + need / 4 && span <= l2_window_max()) {  // contiguous enough (layer 1's padded W_ih is not)
+            win.base_ptr = reinterpret_cast<void*>(lo);
+            win.num_bytes = span;
+            win.hitRatio = std::min(1.0f, static_cast<float>(l2_persist_bytes()) / static_cast<float>(span));
+            win.hitProp = cudaAccessPropertyPersisting;
+            win.missProp = cudaAccessPropertyStreaming;
+        }
+    }
     ProfScope ps_(s, PROF_GEMM_REC_FWD, flops, bytes);
     auto launch = [&](auto tr) {
         using Tr = decltype(tr);
@@ -1207,7 +1230,8 @@ bool lstm_fwd_layer_persistent(const LstmFwdLayer& L, int ndirs, int B, int H, i
             AB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::ShapeOf2<Tr>::SMEM));
             attr = true;
         }
-        tc::launch_tc(k, p, 2 * units, tc::threads_of<Tr>(), tc::ShapeOf2<Tr>::SMEM, true, s);
+        tc::launch_tc(k, p, 2 * units, tc::threads_of<Tr>(), tc::ShapeOf2<Tr>::SMEM, true, s, 2,
+                      win.num_bytes ? &win : nullptr);
     };
     if (uw == 32) launch(FwdPersistT<32>{});
     else launch(FwdPersistT<64>{});

@@ -34,6 +34,9 @@ struct EpiSlot {
 };
 
 constexpr int kSmemBudget = 225 * 1024;
+#ifndef ADPSGD_STAGE_CAP
+#define ADPSGD_STAGE_CAP 8  // A/B experiments only: cap on the CTA-pair mainloop stages
+#endif
 
 // Default hooks: Traits inherit from TraitsBase and may shadow these.
 // epi_begin / epi_begin2 run on every epilogue warp BEFORE it waits for the tile's accumulator:
@@ -214,7 +217,8 @@ struct Shape2 {
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES + X_BYTES;
     static constexpr int ONES_BYTES = (EXTRA && !XB) ? 2048 : 0;  // all-ones bf16 B operand of the extra MMA
     static constexpr int FIT = (kSmemBudget - (OVERLAY ? 0 : EPI) - ONES_BYTES - 2048) / STAGE_BYTES;
-    static constexpr int STAGES = FIT > 8 ? 8 : FIT;
+    static constexpr int CAP = OVERLAY ? 8 : ADPSGD_STAGE_CAP;
+    static constexpr int STAGES = FIT > CAP ? CAP : FIT;
     static constexpr int COLS = ACC * BN + EXTRA + TX;
     static constexpr int TMEM_COLS = COLS <= 32 ? 32 : COLS <= 64 ? 64 : COLS <= 128 ? 128 : COLS <= 256 ? 256 : 512;
     static constexpr int SMEM = STAGES * STAGE_BYTES + (OVERLAY ? 0 : EPI) + ONES_BYTES + 2048;
@@ -544,13 +548,13 @@ __device__ __forceinline__ void release_acc(uint64_t* tempty, int lane) {
 // the previous kernel's tail; the kernel griddep_wait()s before touching dependent data.
 template <class P>
 inline void launch_tc(void (*kern)(P), const P& p, int grid, int threads, int smem, bool pair, cudaStream_t s,
-                      int cluster = 2) {
+                      int cluster = 2, const cudaAccessPolicyWindow* l2win = nullptr) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(threads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute attrs[2];
+    cudaLaunchAttribute attrs[3];
     int n = 0;
     if (pair) {
         attrs[n].id = cudaLaunchAttributeClusterDimension;
@@ -562,6 +566,11 @@ inline void launch_tc(void (*kern)(P), const P& p, int grid, int threads, int sm
     if (knobs().pdl) {
         attrs[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attrs[n].val.programmaticStreamSerializationAllowed = 1;
+        ++n;
+    }
+    if (l2win) {  // L2 persisting window (e.g. the recurrent weights of a persistent layer kernel)
+        attrs[n].id = cudaLaunchAttributeAccessPolicyWindow;
+        attrs[n].val.accessPolicyWindow = *l2win;
         ++n;
     }
     cfg.attrs = attrs;

@@ -2,13 +2,14 @@
 # Round evidence (1 GPU, under gpurun): launch list of one step, full ncu captures of the top
 # kernels, and a bench line. Output: gpurun_out/<tag>_*. Summarise locally with
 #   python tools/summarize_ncu.py <tag> gpurun_out/<tag>_*.ncu-rep --launches gpurun_out/<tag>_launches.csv
-tag=${1:-r01i}
+tag=${1:-r02}
 B="python bench.py --steps 1 --warmup 0 --no-cpu-baseline --e2e-steps 1"
 ncu --metrics gpu__time_duration.sum,launch__grid_size --clock-control none -c 700 --csv \
     --log-file gpurun_out/${tag}_launches.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --e2e-steps 1 \
     > gpurun_out/${tag}_launches_bench.log 2>&1
 cap() {  # name regex skip count
-  ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:$2" -s $3 -c ${4:-1} \
+  ncu --set full --metrics sm__ops_path_tensor_op_utchmma_src_bf16_dst_fp32.sum,sm__ops_path_tensor_op_utchmma_src_bf16_dst_fp32.sum.pct_of_peak_sustained_elapsed \
+      --clock-control none --import-source on --kernel-name-base demangled -k "regex:$2" -s $3 -c ${4:-1} \
       -o gpurun_out/${tag}_$1 $B > gpurun_out/${tag}_$1.log 2>&1
 }
 cap fwd "FwdPersistT" 2
