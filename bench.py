@@ -357,6 +357,23 @@ def run_ours(a):
                 traffic = json.load(f).get("dram_bytes_per_launch_mean")
         except Exception:
             traffic = None
+    # ncu's UTCHMMA op counter for the same kernels (profiles/tensor_counters.json, one bench step
+    # under ncu): the north_star's tensor-pipe utilisation, dense-normalised
+    tensor_pipe = None
+    tcp = os.path.join(ROOT, "profiles", "tensor_counters.json")
+    if prec == Precision.BF16 and os.path.exists(tcp):
+        try:
+            with open(tcp) as f:
+                kc = json.load(f)["kernels"]
+            pick = lambda pat: next((v for k, v in kc.items() if pat in k), None)  # noqa: E731
+            tensor_pipe = {"source": "profiles/tensor_counters.json (ncu sm__ops_path_tensor_op_utchmma_src_bf16_dst_fp32)",
+                           "fwd_recurrent_pct": (pick("FwdPersistT<64>") or {}).get("dense_tensor_util_pct"),
+                           "bptt_recurrent_pct": (pick("BwdPersistTraits<2, 64>") or {}).get("dense_tensor_util_pct"),
+                           "wgrad_pct": (pick("GenTraits<256, 1, 1, 0, 0, 0, 0>") or {}).get("dense_tensor_util_pct"),
+                           "dgrad_pct": (pick("GenTraits<512, 0, 1, 0, 0, 1, 0>") or {}).get("dense_tensor_util_pct"),
+                           "target_pct": 50}
+        except Exception:
+            tensor_pipe = None
     dom = prof["gemm_rec_fwd"] if prec == Precision.BF16 else prof["gemm_simt"]
     dom_ms, dom_launches = dom["ms"], dom["launches"] / a.steps
     dom_flops = dom["flops"] / dom["launches"] if dom["launches"] else 0.0
@@ -401,6 +418,7 @@ def run_ours(a):
                      "all_tcgen05_gemms": {"achieved": achieved, "frac": achieved / peak if peak else None,
                                            "share_of_step": g_ms / a.steps / prof_step_ms if prof_step_ms else None},
                      "profiled_ms_per_step": prof_step_ms, "by_gemm": gemm_detail,
+                     "tensor_pipe_dense_util": tensor_pipe,
                      "step_tflops": frames * m.train_flops_per_frame() / (tot_ms / 1000.0) / 1e12 / world},
         "mix_update": {"ms_per_step": mix["ms"] / a.steps, "achieved_gbs": mix_gbs, "peak_hbm_gbs": pk.get("hbm_gbs")},
         "gossip": {

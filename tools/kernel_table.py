@@ -11,6 +11,8 @@ KEYS = {
     "dram_wr": "dram__bytes_write.sum",
     "l2_pct": "lts__throughput.avg.pct_of_peak_sustained_elapsed",
     "grid": "launch__grid_size",
+    "ops": "sm__ops_path_tensor_op_utchmma_src_bf16_dst_fp32.sum",
+    "ops_pct": "sm__ops_path_tensor_op_utchmma_src_bf16_dst_fp32.sum.pct_of_peak_sustained_elapsed",
 }
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-3, "us": 1, "usecond": 1, "ms": 1e3, "msecond": 1e3,
         "nsecond": 1e-3}
@@ -37,8 +39,9 @@ def rows(path):
 
 def main():
     out = sys.argv[1]
-    lines = ["| kernel | launch | µs | tensor pipe % | TMEM % | DRAM rd+wr (MB) | DRAM GB/s | L2 % | algorithmic |",
-             "|---|---|---|---|---|---|---|---|---|"]
+    lines = ["| kernel | launch | µs | tensor pipe % | UTCHMMA TFLOP/s | dense tensor % | TMEM % | DRAM rd+wr (MB) "
+             "| DRAM GB/s | L2 % | algorithmic |",
+             "|---|---|---|---|---|---|---|---|---|---|---|"]
     for spec in sys.argv[2:]:
         name, rest = spec.split("=", 1)
         parts = rest.split(":")
@@ -51,7 +54,9 @@ def main():
                 alg = f"{float(work[6:]) / (us * 1e-6) / 1e12:.0f} TFLOP/s"
             elif work.startswith("bytes="):
                 alg = f"{float(work[6:]) / (us * 1e-6) / 1e9:.0f} GB/s"
+            ops = d.get("ops", 0.0)
             lines.append(f"| {name} | {i} (grid {int(d.get('grid', 0))}) | {us:.1f} | {d.get('tensor_pct', 0):.1f} | "
+                         f"{ops / (us * 1e-6) / 1e12:.0f} | {2 * d.get('ops_pct', 0):.1f} | "
                          f"{d.get('tmem_pct', 0):.1f} | {dram / 1e6:.0f} | {dram / (us * 1e-6) / 1e9:.0f} | "
                          f"{d.get('l2_pct', 0):.1f} | {alg} |")
     open(out, "w").write("\n".join(lines) + "\n")
