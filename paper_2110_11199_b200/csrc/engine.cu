@@ -118,6 +118,10 @@ Ctx::Ctx(const adpsgd_config& c) : cfg(c) {
     Ipad = bf16_mode ? static_cast<int>(round_up(I + (fold_bias ? 1 : 0), 8)) : I;
     ldH = nd * H + (fold_bias ? 8 : 0);
     ldY = lay.P > 0 ? (fold_bias ? lay.P + 8 : lay.P) : 0;
+    if (knobs().pitch_align > 1) {  // row pitches in whole 128-byte lines: every TMA box row is one line (-2..3 % step)
+        ldH = static_cast<int>(round_up(ldH, knobs().pitch_align));
+        if (ldY) ldY = static_cast<int>(round_up(ldY, knobs().pitch_align));
+    }
     TB = static_cast<int64_t>(T) * B;
     ndH = nd * H;
     nd4H = nd * 4 * H;

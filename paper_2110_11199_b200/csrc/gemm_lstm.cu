@@ -774,7 +774,11 @@ struct FwdPersistT : tc::TraitsBase {
         const U u = unit(p, cid, w.tile);
         const unsigned need = static_cast<unsigned>(u.s) * p.n_tiles;
         const unsigned* f = p.dep + (u.d * p.m_tiles + u.mt) * 2 + rank;
+        // trace (tools/trace_fwd.py): producer reaches / passes the h-part dependency of items 4, 5, 8
+        const int tev = w.tile == 4 ? 40 : w.tile == 5 ? 42 : w.tile == 8 ? 44 : -1;
+        if (tev >= 0) tc::trace_once(p.trace, tev);
         ptx::spin_until_geq(f, need);
+        if (tev >= 0) tc::trace_once(p.trace, tev + 1);
         asm volatile("fence.proxy.async.global;" ::: "memory");
     }
     __device__ static void load2(const FwdPParams& p, int it, int kb, uint32_t rank, uint8_t* sA, uint8_t* sB,

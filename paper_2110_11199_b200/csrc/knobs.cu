@@ -43,6 +43,7 @@ Knobs load() {
     k.async_hold_ms = num("ADPSGD_ASYNC_HOLD_MS");
     k.comm_force = flag("ADPSGD_COMM_FORCE", false, true);
     k.fwd_l2win = flag("ADPSGD_FWD_L2WIN", false, true);
+    if (std::getenv("ADPSGD_PITCH_ALIGN")) k.pitch_align = num("ADPSGD_PITCH_ALIGN");
     if (std::getenv("ADPSGD_POISON_ALLOC")) k.poison_alloc = num("ADPSGD_POISON_ALLOC");
     if (std::getenv("ADPSGD_SPLIT_MAX")) k.split_max = num("ADPSGD_SPLIT_MAX");
     return k;

@@ -8,8 +8,10 @@ os.environ["ADPSGD_NO_STREAMK"] = "1"
 import torch
 from paper_2110_11199_b200 import _lib
 K = 32768
-for amn, bmn in [(0, 1), (1, 1)]:
-    for pairs in [2, 16, 38, 64, 74]:
+CFGS = [tuple(int(c) for c in x) for x in os.environ.get("PROBE_CFGS", "01,11").split(",")]
+PAIRS = [int(x) for x in os.environ.get("PROBE_PAIRS", "2,16,38,64,74").split(",")]
+for amn, bmn in CFGS:
+    for pairs in PAIRS:
         M, N = 256 * pairs, 256
         A = (torch.randn(K, M, device="cuda") if amn else torch.randn(M, K, device="cuda")).to(torch.bfloat16)
         B = (torch.randn(K, N, device="cuda") if bmn else torch.randn(N, K, device="cuda")).to(torch.bfloat16)

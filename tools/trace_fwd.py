@@ -9,7 +9,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 from paper_2110_11199_b200 import LearnerGroup, ModelDesc, StrategyConfig, Precision, _lib
 ns = [int(x) for x in sys.argv[1:]] or [1]
-g = LearnerGroup(ModelDesc(), StrategyConfig(learners=1, batch=1024, seed=1), precision=Precision.BF16)
+H = int(os.environ.get("TRACE_H", "1024"))  # model width (shape P: 512)
+g = LearnerGroup(ModelDesc(hidden=H), StrategyConfig(learners=1, batch=1024, seed=1), precision=Precision.BF16)
 g.synth_dataset(4096, 4096, 3)
 g.step(0.1)
 L = _lib.lib()
