@@ -27,6 +27,7 @@ void make_map_gen(CUtensorMap* m, const void* base, bool f32, uint64_t inner, ui
                   uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle sw) {
     const int esz = f32 ? 4 : 2;
     AB_CHECK((reinterpret_cast<uintptr_t>(base) & 15) == 0, ADPSGD_E_DIMENSION, "TMA base must be 16B aligned");
+    log_map_alignment(__FILE__, base, inner, outer, ld * esz);
     AB_CHECK(((ld * esz) & 15) == 0, ADPSGD_E_DIMENSION, "TMA row pitch must be a multiple of 16 bytes");
     cuuint64_t dims[2] = {inner, outer};
     cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * esz};

@@ -535,6 +535,7 @@ namespace {
 void make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, int64_t ld_elems, uint32_t box_outer) {
     AB_CHECK((reinterpret_cast<uintptr_t>(base) & 15) == 0, ADPSGD_E_DIMENSION, "TMA base must be 16B aligned");
     AB_CHECK(((ld_elems * 2) & 15) == 0, ADPSGD_E_DIMENSION, "TMA row pitch must be a multiple of 16 bytes");
+    log_map_alignment(__FILE__, base, inner, outer, ld_elems * 2);
     cuuint64_t dims[2] = {inner, outer};
     cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld_elems) * 2};
     cuuint32_t box[2] = {64, box_outer};

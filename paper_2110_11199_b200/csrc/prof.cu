@@ -5,6 +5,8 @@
 #include <string>
 
 #include "common.cuh"
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 namespace ab {
@@ -128,6 +130,23 @@ void note_variant(const char* pretty) {
     }
     std::lock_guard<std::mutex> lk(g_var_mu);
     ++g_variants[s];
+}
+
+void log_map_alignment(const char* where, const void* base, uint64_t inner, uint64_t outer, int64_t pitch_bytes) {
+    static const bool on = std::getenv("ADPSGD_LOG_ALIGN") != nullptr;
+    if (!on) return;
+    const bool bad_pitch = pitch_bytes % 128 != 0, bad_base = reinterpret_cast<uintptr_t>(base) % 128 != 0;
+    if (!bad_pitch && !bad_base) return;
+    static std::mutex mu;
+    static std::map<std::string, int> seen;
+    const std::string key = std::string(where) + ":" + std::to_string(inner) + "x" + std::to_string(outer) + "/" +
+                            std::to_string(pitch_bytes) + (bad_base ? "/base" : "");
+    std::lock_guard<std::mutex> lk(mu);
+    if (seen[key]++ == 0)
+        std::fprintf(stderr, "[align] %s inner %llu outer %llu pitch %lld B%s%s\n", where,
+                     static_cast<unsigned long long>(inner), static_cast<unsigned long long>(outer),
+                     static_cast<long long>(pitch_bytes), bad_pitch ? " (pitch not 128B)" : "",
+                     bad_base ? " (base not 128B)" : "");
 }
 
 std::string variants_string(bool reset) {

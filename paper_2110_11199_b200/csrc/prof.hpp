@@ -66,4 +66,7 @@ inline void note_kernel() { note_variant(__PRETTY_FUNCTION__); }
 // "name=count;..." of every variant noted since the last reset.
 std::string variants_string(bool reset);
 
+// ADPSGD_LOG_ALIGN=1 (diagnosis): report TMA maps whose base or row pitch is not a whole number of
+// 128-byte lines (every box row then straddles two lines), once per distinct shape.
+void log_map_alignment(const char* where, const void* base, uint64_t inner, uint64_t outer, int64_t pitch_bytes);
 }  // namespace ab
