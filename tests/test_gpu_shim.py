@@ -38,7 +38,7 @@ def test_shim_objective_matches_library(tmp_path, prec):
     res = np.frombuffer(out.read_bytes(), dtype=np.float64)
     loss, heldout, mapped, grad = res[0], res[1], res[2], res[3:]
     assert mapped == 1.0
-    want_g, want_loss = g.gradient(w, idx)
+    want_loss, want_g = g.gradient(w, idx)
     assert abs(loss - want_loss) <= 1e-6 * abs(want_loss)
     assert np.max(np.abs(grad - want_g)) <= 1e-6 * np.max(np.abs(want_g))
     want_h = g.eval_loss(w, np.arange(train, n_seg, dtype=np.int32))
