@@ -12,6 +12,7 @@
 //     dh = dH[t'] + dh_rec; dc = dc_rec + dh o (1 - tanh^2 c); dz_{t'} = ...; dc_rec = dc f
 #include <cuda.h>
 
+#include <cstdio>
 #include <cstdlib>
 
 #include "gemm_lstm.hpp"
@@ -295,10 +296,12 @@ struct FwdT : tc::TraitsBase {
                 ptx::fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) {
+#ifndef ADPSGD_DBG_NOSTORE  // timing experiments only: no gate stores (h, c still stored)
                     const uint64_t stream = ptx::policy_evict_first();
 #pragma unroll
                     for (int gi = 0; gi < 4; ++gi)
                         ptx::tma_store_2d_hint(&g.m_gates, out + 2048 + gi * 1024, gi * H + jb, rowbase + row_out, stream);
+#endif
                     ptx::tma_store_2d(&g.m_c, out, jb, rowbase + row_out);
                     ptx::tma_store_2d(&g.m_h, out + 6144, jb, rowbase + row_out);
                     ptx::bulk_commit();
@@ -771,6 +774,9 @@ struct FwdPersistT : tc::TraitsBase {
         return true;
     }
     __device__ static void kb_ready(const FwdPParams& p, const tc::Item& w, int kb, int cid, uint32_t rank) {
+#ifdef ADPSGD_DBG_NODEP  // timing experiments only: no cross-CTA step dependency
+        return;
+#endif
         if (kb != p.kbx) return;  // first recurrent k-block: h_{t-1} of every unit tile of this m-tile
         const U u = unit(p, cid, w.tile);
         const unsigned need = static_cast<unsigned>(u.s) * p.n_tiles;
@@ -782,30 +788,48 @@ struct FwdPersistT : tc::TraitsBase {
         if (tev >= 0) tc::trace_once(p.trace, tev + 1);
         asm volatile("fence.proxy.async.global;" ::: "memory");
     }
-    __device__ static void load2(const FwdPParams& p, int it, int kb, uint32_t rank, uint8_t* sA, uint8_t* sB,
-                                 uint32_t bar) {
+    // per-item TMA context (tc_core.cuh HasLoadCtx): segment 0 = x-part (X, W_ih), 1 = h-part (Hout, W_hh)
+    struct LoadCtx {
+        const CUtensorMap* a[2];
+        const CUtensorMap* b[2];
+        int row[2], brow, H, kbx;
+        uint64_t keep;
+    };
+    __device__ static LoadCtx load_ctx(const FwdPParams& p, int it, uint32_t rank) {
         const U u = unit(p, blockIdx.x >> 1, it);
         const FwdGroup& g = p.g[u.d];
-        const int seg = kb < p.kbx ? 0 : 1;
-        const int k0 = (seg == 0 ? kb : kb - p.kbx) * kBK;
-        const int row = (seg == 0 ? u.t : u.tp) * p.B + u.mt * 2 * kBM + kBM * static_cast<int>(rank);
-#ifdef ADPSGD_A_EVICT_FIRST
-        ptx::tma_load_2d_2sm_hint(sA, &g.ta[seg], bar, k0, row, ptx::policy_evict_first());
+        LoadCtx c;
+        const int r0 = u.mt * 2 * kBM + kBM * static_cast<int>(rank);
+        for (int sgm = 0; sgm < 2; ++sgm) { c.a[sgm] = &g.ta[sgm]; c.b[sgm] = &g.tb[sgm]; }
+#ifdef ADPSGD_DBG_FIXROWS  // timing experiments only: every step reads the rows of t = 0
+        c.row[0] = r0;
+        c.row[1] = r0;
 #else
-        // A rows are read by every unit tile of the m-tile, at different times in the persistent
-        // schedule: default L2 policy (evict_first cost DRAM re-reads)
-        ptx::tma_load_2d_2sm(sA, &g.ta[seg], bar, k0, row);
+        c.row[0] = u.t * p.B + r0;
+        c.row[1] = u.tp * p.B + r0;
 #endif
-        const uint64_t keep = ptx::policy_evict_last();
-#pragma unroll
-        for (int j = 0; j < 2; ++j)
-            ptx::tma_load_2d_2sm_hint(sB + j * UW * kBK * 2, &g.tb[seg], bar, k0,
-                                      (2 * static_cast<int>(rank) + j) * p.H + u.nt * UW, keep);
+        c.brow = 2 * static_cast<int>(rank) * p.H + u.nt * UW;
+        c.H = p.H;
+        c.kbx = p.kbx;
+        c.keep = ptx::policy_evict_last();
+        return c;
+    }
+    // A rows are read by every unit tile of the m-tile, at different times in the persistent
+    // schedule: default L2 policy (evict_first cost DRAM re-reads); B (weights) evict_last
+    __device__ static void load2c(const LoadCtx& c, int kb, uint8_t* sA, uint8_t* sB, uint32_t bar) {
+        const int seg = kb < c.kbx ? 0 : 1;
+        const int k0 = (kb - seg * c.kbx) * kBK;
+        ptx::tma_load_2d_2sm(sA, c.a[seg], bar, k0, c.row[seg]);
+        ptx::tma_load_2d_2sm_hint(sB, c.b[seg], bar, k0, c.brow, c.keep);
+        ptx::tma_load_2d_2sm_hint(sB + UW * kBK * 2, c.b[seg], bar, k0, c.brow + c.H, c.keep);
     }
     template <class S>
     __device__ static void epi_begin2(const FwdPParams& p, int it, uint32_t rank, int q, int lane, uint8_t*, uint64_t*,
                                       S sl) {
         const U u = unit(p, blockIdx.x >> 1, it);
+#ifdef ADPSGD_DBG_NOEPI
+        return;
+#endif
         if (u.s == 0) return;
         const int uc = 32 * sl.sub + 32 * sl.n * (lane & 1);
         if (lane < 2 && uc < UW)
@@ -816,17 +840,26 @@ struct FwdPersistT : tc::TraitsBase {
                                        int q, int lane, uint32_t tempty_leader, tc::EpiSlot sl, uint8_t* st,
                                        uint64_t* ebar, uint32_t& ephase) {
         const U u = unit(p, cid, w.tile);
+#ifdef ADPSGD_DBG_NOEPI  // timing experiments only: release the accumulator, publish, no cell
+        tc::release_acc_2sm(tempty_leader, lane);
+#else
         F::body_g(p.g[u.d], p.H, u.mt * 2 * kBM + kBM * static_cast<int>(rank), u.nt * UW, tbase, q, lane,
                   [&] { tc::release_acc_2sm(tempty_leader, lane); }, st, ebar, ephase, sl, nullptr, u.t * p.B,
                   u.s > 0 ? u.tp * p.B : 0, u.s > 0);
+#endif
         // publish: this CTA's h_t (and c_t) block is in memory
+#ifdef ADPSGD_DBG_NOPUB  // timing experiments only (with ADPSGD_DBG_NODEP): no publication at all
+        if (true) return;
+#endif
         if (lane == 0) {
             ptx::bulk_wait0();
             asm volatile("fence.proxy.async.global;" ::: "memory");
         }
         ptx::named_sync(2, 32 * EPI_WARPS);
         if (q == 0 && sl.sub == 0 && lane == 0) {
+#ifndef ADPSGD_DBG_NOFENCE
             __threadfence();
+#endif
             atomicAdd(p.dep + (u.d * p.m_tiles + u.mt) * 2 + rank, 1u);
             if (w.tile == 2 * p.T - 1) {
                 __threadfence();
@@ -937,31 +970,55 @@ struct BwdPersistTraits : tc::TraitsBase, BwdEpi {
     }
     __device__ static void item_ready(const BwdPParams& p, const tc::Item& w, int cid, uint32_t rank) {
         const U u = unit(p, cid, w.tile);
+#ifdef ADPSGD_DBG_NODEP
+        return;
+#endif
         if (u.s == 0) return;  // dz of the first BPTT step comes from the previous kernel
         const unsigned need = static_cast<unsigned>(u.s) * p.n_tiles * KQ;
         ptx::spin_until_geq(p.dep + (u.d * p.m_tiles + u.mt) * 2 + rank, need);
         asm volatile("fence.proxy.async.global;" ::: "memory");  // generic acquire -> async-proxy (TMA) reads
     }
-    __device__ static void load2(const BwdPParams& p, int it, int kb, uint32_t rank, uint8_t* sA, uint8_t* sB,
-                                 uint32_t bar) {
+    // per-item TMA context (tc_core.cuh HasLoadCtx): A = dz_{t_src} rows of this m-tile, B = W_hh
+    // (UC = 64: MN-major [4H x H] 64-unit boxes; UC = 32: K-major W_hh^T [H x 4H])
+    struct LoadCtx {
+        const CUtensorMap* a;
+        const CUtensorMap* b;
+        int rowA, kbase, bcol;
+        uint64_t keep;
+    };
+    __device__ static LoadCtx load_ctx(const BwdPParams& p, int it, uint32_t rank) {
         const U u = unit(p, blockIdx.x >> 1, it);
         const BwdGroup& g = p.g[u.d];
-        const int k0 = (u.kh * p.kbh + kb) * kBK;
-        ptx::tma_load_2d_2sm(sA, &g.ta, bar, k0, t_src(p, u) * p.B + u.mt * 2 * kBM + kBM * static_cast<int>(rank));
-        const uint64_t keep = ptx::policy_evict_last();
+        LoadCtx c;
+        c.a = &g.ta;
+        c.b = &g.tb;
+#ifdef ADPSGD_DBG_FIXROWS
+        c.rowA = u.mt * 2 * kBM + kBM * static_cast<int>(rank);
+#else
+        c.rowA = t_src(p, u) * p.B + u.mt * 2 * kBM + kBM * static_cast<int>(rank);
+#endif
+        c.kbase = u.kh * p.kbh;
+        c.bcol = u.nt * BN + static_cast<int>(rank) * (BN / 2);
+        c.keep = ptx::policy_evict_last();
+        return c;
+    }
+    __device__ static void load2c(const LoadCtx& c, int kb, uint8_t* sA, uint8_t* sB, uint32_t bar) {
+        const int k0 = (c.kbase + kb) * kBK;
+        ptx::tma_load_2d_2sm(sA, c.a, bar, k0, c.rowA);
         if constexpr (UC == 64) {
 #pragma unroll
-            for (int j = 0; j < BN / 128; ++j)
-                ptx::tma_load_2d_2sm_hint(sB + j * 64 * kBK * 2, &g.tb, bar, u.nt * BN + static_cast<int>(rank) * (BN / 2) + 64 * j,
-                                          k0, keep);
-        } else {  // K-major W_hh^T: BN / 2 unit rows x 64 gate columns
-            ptx::tma_load_2d_2sm_hint(sB, &g.tb, bar, k0, u.nt * BN + static_cast<int>(rank) * (BN / 2), keep);
+            for (int j = 0; j < BN / 128; ++j) ptx::tma_load_2d_2sm_hint(sB + j * 64 * kBK * 2, c.b, bar, c.bcol + 64 * j, k0, c.keep);
+        } else {
+            ptx::tma_load_2d_2sm_hint(sB, c.b, bar, k0, c.bcol, c.keep);
         }
     }
     template <class S>
     __device__ static void epi_begin2(const BwdPParams& p, int it, uint32_t rank, int q, int lane, uint8_t* st,
                                       uint64_t* ebar, S sl) {
         const U u = unit(p, blockIdx.x >> 1, it);
+#ifdef ADPSGD_DBG_NOEPI
+        return;
+#endif
         begin_g<UC, true, 1>(p.g[u.d], p.H, u.mt * 2 * kBM + kBM * static_cast<int>(rank), u.nt * BN + UC * u.kh, q, lane,
                              st, ebar, sl, rows(p, u));
     }
@@ -977,6 +1034,12 @@ struct BwdPersistTraits : tc::TraitsBase, BwdEpi {
         auto block = [&](int c_id, int j) {
             return p.sk_scratch + ((static_cast<int64_t>(c_id * 2 + static_cast<int>(rank)) * 2 + par) * KQ + j) * kBlock;
         };
+        const bool leader = q == 0 && sl.sub == 0 && lane == 0;
+#ifdef ADPSGD_DBG_NOEPI  // timing experiments only: release the accumulator, publish, no exchange / cell
+        tc::release_acc_2sm(tempty_leader, lane);
+        if (true) goto publish;
+#endif
+        {
         // 1) export the blocks the partners finalise (TMEM cols [UC j, +UC) for j != kh)
         //    (p.epi_skip: diagnosis only -- 1 skips the TMEM loads, 2 skips the stores)
 #pragma unroll 1
@@ -999,7 +1062,6 @@ struct BwdPersistTraits : tc::TraitsBase, BwdEpi {
                                             __uint_as_float(v[4 * k + 2]), __uint_as_float(v[4 * k + 3])));
         }
         // 2) handshake (epoch counters, one increment per item)
-        const bool leader = q == 0 && sl.sub == 0 && lane == 0;
         if (leader && w.tile == 2) tc::trace_once(p.trace, 42);  // this warp's export done
         ptx::named_sync(2, 32 * EPI_WARPS);
         if (leader && w.tile == 2) tc::trace_once(p.trace, 40);  // export done (all warps)
@@ -1020,7 +1082,11 @@ struct BwdPersistTraits : tc::TraitsBase, BwdEpi {
         body_g<UC, true, decltype(rel), 1>(p.g[u.d], p.H, u.mt * 2 * kBM + kBM * static_cast<int>(rank),
                                           u.nt * BN + UC * u.kh, tbase + UC * u.kh, q, lane, rel, st, ebar, ephase, sl,
                                           pr[0], true, rows(p, u, tbase - (tbase & 0xFFFFu) % (2 * BN), true), pr[1], pr[2]);
+        }
         // 4) publish: this CTA's dz block of step tn is in memory (TMA stores complete)
+#ifdef ADPSGD_DBG_NOEPI
+    publish:
+#endif
         if (lane == 0) {
             ptx::bulk_wait0();
             asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -1173,6 +1239,111 @@ void lstm_bwd_step(const LstmBwdDir* dirs, int ndirs, int B, int H, int lddh, in
     else launch_persistent<BwdTraits<64>>(p, ndirs * p.m_tiles * p.n_tiles, s);
 }
 
+#ifdef ADPSGD_DBG_PROBE
+// Timing experiments only: the persistent forward's TMA pipeline alone (no MMA, no epilogue, no
+// cross-CTA dependencies) on the layer's real tensor maps, with a minimal CTA pair: both CTAs'
+// loads complete on the leader's full barrier; the leader frees each stage in both CTAs.
+// flags: 1 = free stages by tcgen05.commit (TMEM allocated: 512 columns) instead of remote arrives
+__global__ void __launch_bounds__(192) fwd_probe_kernel(const __grid_constant__ FwdPParams p, int stages, int flags) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ __align__(8) uint64_t full[8], empty[8];
+    __shared__ uint32_t tslot;
+    using T = FwdPersistT<64>;
+    constexpr int AB = tc::kBM * tc::kBK * 2, BB = 128 * tc::kBK * 2;
+    const uint32_t rank = ptx::cluster_ctarank();
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < stages; ++i) { ptx::mbar_init(&full[i], 1); ptx::mbar_init(&empty[i], 1); }
+        ptx::fence_barrier_init();
+    }
+    if ((flags & 1) && threadIdx.x >= 32 && threadIdx.x < 64) ptx::tmem_alloc_2sm(&tslot, 512);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::cluster_sync();
+    ptx::tc_fence_after();
+    const int nitems = 2 * p.T;
+    if (threadIdx.x == 0) {
+        int st = 0;
+        uint32_t ph = 0;
+        for (int it = 0; it < nitems; ++it) {
+            const T::LoadCtx c = T::load_ctx(p, it, rank);
+            for (int kb = 0; kb < T::kblocks(p, it); ++kb) {
+                ptx::mbar_wait(&empty[st], ph ^ 1);
+                const uint32_t bar0 = ptx::mapa(ptx::smem_u32(&full[st]), 0);
+                if (rank == 0) ptx::mbar_arrive_expect_tx(&full[st], 2 * (AB + BB));
+                T::load2c(c, kb, smem + st * AB, smem + stages * AB + st * BB, bar0);
+                if (++st == stages) { st = 0; ph ^= 1; }
+            }
+        }
+    } else if (threadIdx.x == 32 && rank == 0) {
+        int st = 0;
+        uint32_t ph = 0;
+        for (int it = 0; it < nitems; ++it)
+            for (int kb = 0; kb < T::kblocks(p, it); ++kb) {
+                ptx::mbar_wait(&full[st], ph);
+                if (flags & 1) {
+                    ptx::tc_fence_after();
+                    ptx::mma_commit_2sm(&empty[st], 3);
+                } else {
+                    for (uint32_t r = 0; r < 2; ++r) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&empty[st]), r));
+                }
+                if (++st == stages) { st = 0; ph ^= 1; }
+            }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::cluster_sync();
+    if ((flags & 1) && threadIdx.x >= 32 && threadIdx.x < 64) ptx::tmem_dealloc_2sm(tslot, 512);
+}
+// ADPSGD_DBG_PROBE_STAGES=n: variants (flags | threads | smem | PDL), each timed best-of-4
+void fwd_probe(const FwdPParams& p, int units, cudaStream_t s) {
+    const char* e = std::getenv("ADPSGD_DBG_PROBE_STAGES");
+    const int stages = e ? std::atoi(e) : 4;
+    constexpr int SB = tc::kBM * tc::kBK * 2 + 128 * tc::kBK * 2;
+    static bool attr = false;
+    if (!attr) {
+        AB_CUDA(cudaFuncSetAttribute(fwd_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        attr = true;
+    }
+    struct V { int flags, threads, smem; bool pdl; const char* name; };
+    const V vs[] = {{0, 64, stages * SB + 1024, false, "base"},
+                    {1, 64, stages * SB + 1024, false, "commit+tmem512"},
+                    {1, 192, stages * SB + 1024, false, "+192 threads"},
+                    {1, 192, 220 * 1024, false, "+220KB smem"},
+                    {1, 192, 220 * 1024, true, "+PDL"}};
+    for (const V& v : vs) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(2 * units);
+        cfg.blockDim = dim3(v.threads);
+        cfg.dynamicSmemBytes = v.smem;
+        cfg.stream = s;
+        cudaLaunchAttribute a[2];
+        a[0].id = cudaLaunchAttributeClusterDimension;
+        a[0].val.clusterDim.x = 2; a[0].val.clusterDim.y = 1; a[0].val.clusterDim.z = 1;
+        a[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        a[1].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = a;
+        cfg.numAttrs = v.pdl ? 2 : 1;
+        cudaEvent_t e0, e1;
+        AB_CUDA(cudaEventCreate(&e0));
+        AB_CUDA(cudaEventCreate(&e1));
+        float best = 1e30f;
+        for (int rep = 0; rep < 5; ++rep) {
+            AB_CUDA(cudaEventRecord(e0, s));
+            AB_CUDA(cudaLaunchKernelEx(&cfg, fwd_probe_kernel, p, stages, v.flags));
+            AB_CUDA(cudaEventRecord(e1, s));
+            AB_CUDA(cudaEventSynchronize(e1));
+            float ms;
+            AB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+            if (rep > 0) best = ms < best ? ms : best;
+        }
+        std::fprintf(stderr, "[fwd_probe] K=%d stages=%d %-16s %.1f us per launch\n", p.kbx * 64, stages, v.name, best * 1e3);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+    }
+}
+#endif
+
 bool lstm_fwd_layer_persistent(const LstmFwdLayer& L, int ndirs, int B, int H, int T, cudaStream_t s, unsigned int* dep,
                                unsigned int* exit_ctr) {
     // 32-unit tiles when 64-unit ones would leave more than half of the CTA pairs idle
@@ -1238,11 +1409,32 @@ bool lstm_fwd_layer_persistent(const LstmFwdLayer& L, int ndirs, int B, int H, i
         tc::launch_tc(k, p, 2 * units, tc::threads_of<Tr>(), tc::ShapeOf2<Tr>::SMEM, true, s, 2,
                       win.num_bytes ? &win : nullptr);
     };
+#ifdef ADPSGD_DBG_PROBE
+    if (uw == 64 && std::getenv("ADPSGD_DBG_PROBE_STAGES")) {
+        fwd_probe(p, units, s);
+        cudaEvent_t e0, e1;
+        AB_CUDA(cudaEventCreate(&e0));
+        AB_CUDA(cudaEventCreate(&e1));
+        float best = 1e30f;
+        for (int rep = 0; rep < 5; ++rep) {
+            AB_CUDA(cudaEventRecord(e0, s));
+            launch(FwdPersistT<64>{});
+            AB_CUDA(cudaEventRecord(e1, s));
+            AB_CUDA(cudaEventSynchronize(e1));
+            float ms;
+            AB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+            if (rep > 0) best = ms < best ? ms : best;
+        }
+        std::fprintf(stderr, "[fwd_probe] K=%d stages=%d %-16s %.1f us per launch\n", p.kbx * 64,
+                     tc::ShapeOf2<FwdPersistT<64>>::STAGES, "skeleton", best * 1e3);
+    }
+#endif
     if (uw == 32) launch(FwdPersistT<32>{});
     else launch(FwdPersistT<64>{});
     count_launch();
     return true;
 }
+
 
 bool lstm_bwd_wants_whh_t(int ndirs, int B, int H) {
     return knobs().persist_bwd && knobs().pair_mma && knobs().bwd_u32 && !knobs().bwd_kq4 && ndirs == 2 &&

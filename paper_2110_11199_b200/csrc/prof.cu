@@ -10,6 +10,7 @@
 #include <cstring>
 
 namespace ab {
+constexpr size_t kTraceWords = 160 * 48 + 160 * 64 * 12 + 2 * 8 * 64 * 2;  // tc_core.cuh: stamps + per-item timeline
 unsigned long long* g_trace_buf = nullptr;  // device buffer while tracing is on (tc_core.cuh)
 int g_trace_skip = 0;                       // pair-kernel launches to skip before the traced one
 
@@ -24,8 +25,8 @@ unsigned long long* trace_take() {
 void trace_enable(int on) {
     if (on) g_trace_skip = on - 1;
     if (on && !g_trace_buf) {
-        AB_CUDA(cudaMalloc(&g_trace_buf, sizeof(unsigned long long) * 160 * 48));
-        AB_CUDA(cudaMemset(g_trace_buf, 0, sizeof(unsigned long long) * 160 * 48));
+        AB_CUDA(cudaMalloc(&g_trace_buf, sizeof(unsigned long long) * kTraceWords));
+        AB_CUDA(cudaMemset(g_trace_buf, 0, sizeof(unsigned long long) * kTraceWords));
         AB_CUDA(cudaDeviceSynchronize());  // legacy-stream memset vs the engine's non-blocking streams
     }
     if (!on && g_trace_buf) {
@@ -37,8 +38,9 @@ void trace_enable(int on) {
 void trace_read(unsigned long long* out, int n) {
     AB_CUDA(cudaDeviceSynchronize());
     if (!g_trace_buf) return;
+    if (n > static_cast<int>(kTraceWords)) n = static_cast<int>(kTraceWords);
     AB_CUDA(cudaMemcpy(out, g_trace_buf, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost));
-    AB_CUDA(cudaMemset(g_trace_buf, 0, sizeof(unsigned long long) * 160 * 48));
+    AB_CUDA(cudaMemset(g_trace_buf, 0, sizeof(unsigned long long) * kTraceWords));
     AB_CUDA(cudaDeviceSynchronize());
 }
 

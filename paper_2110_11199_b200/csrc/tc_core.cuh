@@ -7,6 +7,8 @@
 // per Traits::B_MN), fp32 accumulate in TMEM.
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "knobs.hpp"
 #include "tc_ptx.cuh"
@@ -23,6 +25,59 @@ __device__ __forceinline__ void trace(unsigned long long* buf, int ev) {
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         buf[blockIdx.x * kTraceEv + ev] = t;
     }
+}
+
+// Per-item timeline (tools/trace_items.py), after the block above: [cta][item < 64][8 events]
+// 0 producer: first load issued, 1 producer: mid-item dependency passed, 2 producer: last load issued,
+// 3 MMA: first stage landed, 4 MMA: last MMA committed, 5 epilogue: accumulator full, 6 epilogue done,
+// 7 producer: item reached (before its cross-CTA dependency wait); durations (ns, summed over the
+// item's k-blocks): 8 MMA warp waiting for full stages, 9 producer waiting for empty stages
+constexpr int kTraceItems = 64, kTraceItemEv = 12;  // 10 / 11: clock64 at MMA start / last MMA
+__device__ __forceinline__ void trace_item(unsigned long long* buf, int item, int ev) {
+#ifndef ADPSGD_ITEM_TRACE
+    return;
+#endif
+    if (buf && blockIdx.x < kTraceCtas && item < kTraceItems) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        buf[kTraceCtas * kTraceEv + (blockIdx.x * kTraceItems + item) * kTraceItemEv + ev] = t;
+    }
+}
+// per-k-block detail of CTAs 0 and 1, items < 8 (after the item block): [cta][item][kb < 64][2]
+// 0 = producer issued the k-block's loads, 1 = the MMA warp saw the stage full (leader CTA only)
+constexpr int kTraceDetailItems = 8, kTraceDetailKb = 64;
+__device__ __forceinline__ void trace_kb(unsigned long long* buf, int item, int kb, int ev) {
+#ifndef ADPSGD_ITEM_TRACE
+    return;
+#endif
+    if (buf && blockIdx.x < 2 && item < kTraceDetailItems && kb < kTraceDetailKb) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        buf[kTraceCtas * kTraceEv + kTraceCtas * kTraceItems * kTraceItemEv +
+            ((blockIdx.x * kTraceDetailItems + item) * kTraceDetailKb + kb) * 2 + ev] = t;
+    }
+}
+// per-item / per-k-block instrumentation (trace_item*, wait durations, trace_kb): only in ADPSGD_ITEM_TRACE builds
+// (tools/trace_items.py); the product build keeps the per-k-block loops free of it
+__device__ __forceinline__ unsigned long long gclock(const void* buf) {
+#ifdef ADPSGD_ITEM_TRACE
+    if (buf) return clock64();
+#endif
+    return 0;
+}
+__device__ __forceinline__ unsigned long long gtimer(const void* buf) {
+    unsigned long long t = 0;
+#ifdef ADPSGD_ITEM_TRACE
+    if (buf) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+#endif
+    return t;
+}
+__device__ __forceinline__ void trace_item_put(unsigned long long* buf, int item, int ev, unsigned long long v) {
+#ifndef ADPSGD_ITEM_TRACE
+    return;
+#endif
+    if (buf && blockIdx.x < kTraceCtas && item < kTraceItems)
+        buf[kTraceCtas * kTraceEv + (blockIdx.x * kTraceItems + item) * kTraceItemEv + ev] = v;
 }
 
 constexpr int kBM = 128, kBK = 64, kThreads = 192;
@@ -248,6 +303,25 @@ __device__ __forceinline__ bool next_item(const Params& p, int cid, int ncl, int
     }
 }
 
+// Optional per-item load context: Traits with a LoadCtx type compute every item-invariant part of
+// the TMA coordinates (tile rows, tensor-map pointers, cache policy) once per item in
+// load_ctx(p, tile, rank); the producer's per-k-block work is then load2c(ctx, kb, sA, sB, bar):
+// a handful of adds and the TMA issues. (The per-k-block path is a single thread's dependent
+// instruction chain -- divisions by runtime tile counts there made the producer, not the memory
+// system, the limit of the persistent recurrent kernels.)
+template <class T, class = void>
+struct HasLoadCtx : std::false_type {};
+template <class T>
+struct HasLoadCtx<T, std::void_t<typename T::LoadCtx>> : std::true_type {};
+template <class T, bool = HasLoadCtx<T>::value>
+struct LoadCtxOf {
+    struct type {};
+};
+template <class T>
+struct LoadCtxOf<T, true> {
+    using type = typename T::LoadCtx;
+};
+
 template <class Traits, class Params>
 __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_kernel_2cta(const __grid_constant__ Params p) {
     constexpr int BN = Traits::BN;
@@ -311,20 +385,32 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
         uint32_t phase = 0;
         bool released = false;
         Item w;
+        const uint32_t full0 = ptx::mapa(ptx::smem_u32(&full[0]), leader);  // the leader's full[stage] = full0 + 8 stage
         for (int it = 0; next_item<Traits>(p, cid, ncl, it, w); ++it) {
             if constexpr (Traits::STREAMK) {
-                if (lane == 0) Traits::item_ready(p, w, cid, rank);
+                if (lane == 0) { trace_item(p.trace, it, 7); Traits::item_ready(p, w, cid, rank); }
             }
+            unsigned long long ewait = 0;
+            typename LoadCtxOf<Traits>::type ctx;
+            if constexpr (HasLoadCtx<Traits>::value) ctx = Traits::load_ctx(p, w.tile, rank);
             for (int kb = w.kb0; kb < w.kb1; ++kb) {
                 if (lane == 0) {
                     if constexpr (Traits::STREAMK) Traits::kb_ready(p, w, kb, cid, rank);
+                    const unsigned long long tw0 = gtimer(p.trace);
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
-                    const uint32_t bar0 = ptx::mapa(ptx::smem_u32(&full[stage]), leader);
+                    ewait += gtimer(p.trace) - tw0;
+                    if (kb == w.kb0) trace_item(p.trace, it, 0);
+                    if (kb == w.kb0 + 32) trace_item(p.trace, it, 1);
+                    if (kb + 1 == w.kb1) trace_item(p.trace, it, 2);
+                    const uint32_t bar0 = full0 + 8 * stage;
                     if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * S::STAGE_BYTES);
                     if constexpr (MC)
                         Traits::load2_mc(p, w.tile, kb, crank, sA + stage * S::A_BYTES, sB + stage * S::B_BYTES, bar0);
+                    else if constexpr (HasLoadCtx<Traits>::value)
+                        Traits::load2c(ctx, kb, sA + stage * S::A_BYTES, sB + stage * S::B_BYTES, bar0);
                     else
                         Traits::load2(p, w.tile, kb, rank, sA + stage * S::A_BYTES, sB + stage * S::B_BYTES, bar0);
+                    trace_kb(p.trace, it, kb - w.kb0, 0);
                     if constexpr (S::X_BYTES > 0) Traits::load_x(p, w.tile, kb, rank, sX + stage * S::X_BYTES, bar0);
                 }
                 if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -334,6 +420,7 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
                     released = true;
                 }
             }
+            if (lane == 0) trace_item_put(p.trace, it, 9, ewait);
         }
         if (!released) ptx::named_arrive(1, 32 + 32 * Traits::EPI_WARPS);
     } else if (warp == 1) {
@@ -352,9 +439,13 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
                 const uint32_t tmem_d = tmem_base + acc * BN;
                 bool extra = false;
                 if constexpr (Traits::EXTRA_COLS > 0) extra = Traits::extra_tile(p, w.tile);
+                unsigned long long fwait = 0;
                 for (int kb = w.kb0; kb < w.kb1; ++kb) {
+                    const unsigned long long tw0 = gtimer(p.trace);
                     ptx::mbar_wait(&full[stage], phase);
-                    if (kb == w.kb0) trace(p.trace, 4 * it + 1);
+                    fwait += gtimer(p.trace) - tw0;
+                    trace_kb(p.trace, it, kb - w.kb0, 1);
+                    if (kb == w.kb0) { trace(p.trace, 4 * it + 1); trace_item(p.trace, it, 3); trace_item_put(p.trace, it, 10, gclock(p.trace)); }
                     ptx::tc_fence_after();
                     const uint32_t a_addr = ptx::smem_u32(sA + stage * S::A_BYTES);
                     const uint32_t b_addr = ptx::smem_u32(sB + stage * S::B_BYTES);
@@ -369,7 +460,9 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
                         for (int sub = 0; sub < NSUB; ++sub) {
                             // sub-MMA sub: B rows [sub MN/2, +MN/2) of this CTA's stage -> TMEM cols [sub MN, +MN)
                             const uint64_t bds = bd + static_cast<uint64_t>((sub * (MN / 2) * kBK * 2) >> 4);
+#ifndef ADPSGD_DBG_NOMMA  // timing experiments only: the pipeline without tensor work
                             ptx::mma_bf16_2sm(tmem_d + sub * MN, ad, bds, idesc, accum);
+#endif
                         }
                         if constexpr (Traits::EXTRA_COLS > 0) {
                             // row sums of A: an N = 16 MMA against an all-ones K-major B -> TMEM cols [BN, BN + 16)
@@ -383,6 +476,9 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
                 }
                 ptx::mma_commit_2sm(&tfull[acc], pair_mask);
                 trace(p.trace, 4 * it + 2);
+                trace_item(p.trace, it, 4);
+                trace_item_put(p.trace, it, 8, fwait);
+                trace_item_put(p.trace, it, 11, gclock(p.trace));
                 if (++acc == ACC) { acc = 0; aphase ^= 1; }
             }
         }
@@ -400,12 +496,13 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
             Traits::epi_begin2(p, w.tile, rank, q, lane, est, &epi_bar[2 * e], slot);
             ptx::mbar_wait_sleep(&tfull[acc], aphase);
             ptx::tc_fence_after();
+            if (e == 0 && lane == 0) trace_item(p.trace, it, 5);
             const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
             if constexpr (Traits::STREAMK)
                 Traits::epilogue_sk(p, w, cid, rank, tbase, q, lane, tempty0 + acc * 8, slot, est, &epi_bar[2 * e], ephase);
             else
                 Traits::epilogue2(p, w.tile, rank, tbase, q, lane, tempty0 + acc * 8, est, &epi_bar[2 * e], ephase, slot);
-            if (e == 0 && lane == 0) trace(p.trace, 4 * it + 3);
+            if (e == 0 && lane == 0) { trace(p.trace, 4 * it + 3); trace_item(p.trace, it, 6); }
             if (++acc == ACC) { acc = 0; aphase ^= 1; }
         }
         if (lane == 0) ptx::bulk_wait0();

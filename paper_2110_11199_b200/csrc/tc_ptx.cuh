@@ -36,6 +36,30 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 #endif
+#ifdef ADPSGD_SLEEP_BACKOFF
+// Backoff wait for long waits of otherwise idle warps (epilogue warps during the mainloop):
+// non-blocking test_wait, then __nanosleep with exponential backoff, so the idle warps do not
+// keep the mbarrier unit busy while the producer / MMA warps' pipeline barriers need it.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    uint32_t ns = 32;
+    for (;;) {
+        uint32_t ok;
+        asm volatile(
+            "{\n"
+            ".reg .pred P1;\n"
+            "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, P1;\n"
+            "}\n"
+            : "=r"(ok)
+            : "r"(a), "r"(parity)
+            : "memory");
+        if (ok) return;
+        __nanosleep(ns);
+        if (ns < ADPSGD_SLEEP_BACKOFF) ns <<= 1;
+    }
+}
+#else
 // Suspending wait (long waits of otherwise idle warps, e.g. epilogue warps during the mainloop):
 // the hint lets the warp sleep in hardware instead of occupying issue slots.
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
@@ -50,6 +74,7 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
         "r"(parity), "r"(0x989680)
         : "memory");
 }
+#endif
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");

@@ -38,6 +38,8 @@ def rows(path):
 
 
 def main():
+    if len(sys.argv) < 3 or not sys.argv[1].endswith(".md") or "=" not in sys.argv[2]:
+        sys.exit(__doc__)
     out = sys.argv[1]
     lines = ["| kernel | launch | µs | tensor pipe % | UTCHMMA TFLOP/s | dense tensor % | TMEM % | DRAM rd+wr (MB) "
              "| DRAM GB/s | L2 % | algorithmic |",
