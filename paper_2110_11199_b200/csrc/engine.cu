@@ -538,7 +538,7 @@ void Ctx::forward_backward(const Learner& ln, const float* master, float* grad, 
             for (int d = 0; d < nd; ++d) {
                 PL.w_hh[d] = static_cast<const bf16*>(W.at(lay.dir[l][d].w_hh));
                 PL.dc_rec[d] = dc_rec + static_cast<int64_t>(d) * B * H;
-                if (whh_t[d] && knobs().bwd_u32) {  // K-major copy for the 32-unit BPTT tiles
+                if (whh_t[d] && (knobs().bwd_u32 || knobs().bwd_kmajor)) {  // K-major copy for the BPTT B operand
                     launch_transpose_bf16(PL.w_hh[d], whh_t[d], G4, H, s);
                     PL.w_hh_t[d] = whh_t[d];
                 }

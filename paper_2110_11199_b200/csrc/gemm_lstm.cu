@@ -188,7 +188,9 @@ struct FwdT : tc::TraitsBase {
                p.g[grp].c_prev != nullptr);
     }
     // row_out / row_cp: row offsets of the outputs and of c_{t-1} (maps spanning all time steps)
-    template <class Rel>
+    // NSETS: output staging sets per warp (2: a half's stores overlap the next half's math;
+    // 1: 15 KB per warp instead of 22, so the persistent forward fits one more mainloop stage)
+    template <class Rel, int NSETS = 2>
     __device__ static void body_g(const FwdGroup& g, int H, int m0, int u0, uint32_t tbase, int q, int lane,
                                   Rel release, uint8_t* st, uint64_t* ebar, uint32_t& ephase, tc::EpiSlot sl,
                                   unsigned long long* trace, int row_out, int row_cp, bool has_prev) {
@@ -230,9 +232,12 @@ struct FwdT : tc::TraitsBase {
                     for (int i = 0; i < 16; ++i) cp[i] = 0.f;
                 }
                 if (tr && h == 0) tc::trace_once(trace, 12 + (uc / 32) * 4 + 1);
-                uint8_t* out = st + 8192 + ob * 7168;
-                // the store that last used this output set (two halves ago) has read it
-                if (lane == 0) ptx::bulk_wait_read1();
+                uint8_t* out = st + 8192 + (NSETS == 2 ? ob * 7168 : 0);
+                // the store that last used this output set (NSETS halves ago) has read it
+                if (lane == 0) {
+                    if constexpr (NSETS == 2) ptx::bulk_wait_read1();
+                    else ptx::bulk_wait_read0();
+                }
                 __syncwarp();
                 const int jb = j0 + 16 * h;
                 float a[16], gv[16];
@@ -742,7 +747,12 @@ template <int UW>
 struct FwdPersistT : tc::TraitsBase {
     using F = FwdT<UW>;
     static constexpr int BN = 4 * UW;
-    static constexpr int EPI_WARP = F::EPI_WARP;
+#ifdef ADPSGD_FWD_TWO_SETS
+    static constexpr int OUT_SETS = 2;
+#else
+    static constexpr int OUT_SETS = 1;  // one output staging set per warp: 15 KB, 5 mainloop stages instead of 4
+#endif
+    static constexpr int EPI_WARP = OUT_SETS == 2 ? F::EPI_WARP : 15 * 1024;
     static constexpr int EPI_WARPS = 4;
     static constexpr int EPI_SMEM = EPI_WARPS * EPI_WARP;
     static constexpr int ACC_STAGES = 2;
@@ -843,9 +853,10 @@ struct FwdPersistT : tc::TraitsBase {
 #ifdef ADPSGD_DBG_NOEPI  // timing experiments only: release the accumulator, publish, no cell
         tc::release_acc_2sm(tempty_leader, lane);
 #else
-        F::body_g(p.g[u.d], p.H, u.mt * 2 * kBM + kBM * static_cast<int>(rank), u.nt * UW, tbase, q, lane,
-                  [&] { tc::release_acc_2sm(tempty_leader, lane); }, st, ebar, ephase, sl, nullptr, u.t * p.B,
-                  u.s > 0 ? u.tp * p.B : 0, u.s > 0);
+        auto rel = [&] { tc::release_acc_2sm(tempty_leader, lane); };
+        F::template body_g<decltype(rel), OUT_SETS>(p.g[u.d], p.H, u.mt * 2 * kBM + kBM * static_cast<int>(rank), u.nt * UW,
+                                                    tbase, q, lane, rel, st, ebar, ephase, sl, nullptr, u.t * p.B,
+                                                    u.s > 0 ? u.tp * p.B : 0, u.s > 0);
 #endif
         // publish: this CTA's h_t (and c_t) block is in memory
 #ifdef ADPSGD_DBG_NOPUB  // timing experiments only (with ADPSGD_DBG_NODEP): no publication at all
@@ -900,7 +911,7 @@ struct BwdPParams {
 // UC = units each CTA finalises: 64, or 32 (H <= 512: twice the CTA pairs, half the epilogue per
 // item). UC = 32 reads B = W_hh^T (a K-major transposed copy, [H x 4H]) so 32-unit B tiles
 // stay in the 128-byte-swizzle layout.
-template <int KQ, int UC = 64>
+template <int KQ, int UC = 64, bool KMAJ = false>
 struct BwdPersistTraits : tc::TraitsBase, BwdEpi {
     static constexpr int BN = UC * KQ;  // pair tile width
     static constexpr int NCHK = UC / 16;  // 16-unit chunks per finalised block
@@ -912,7 +923,7 @@ struct BwdPersistTraits : tc::TraitsBase, BwdEpi {
     static constexpr int EPI_SMEM = EPI_WARPS * 12 * 1024;  // BwdEpi::body_g<64, INPLACE, .., NBUF = 1>
     static constexpr int ACC_STAGES = 2;
     static constexpr bool A_MN = false;
-    static constexpr bool B_MN = UC == 64;
+    static constexpr bool B_MN = UC == 64 && !KMAJ;  // KMAJ: K-major W_hh^T for the 64-unit tiles too
     static constexpr bool STREAMK = true;
     // TMEM past the accumulators (KQ = 2 only: 2 BN + 4 UC <= 512 columns): per direction d,
     // dc_rec at [2 BN + UC d, +UC) and the carried c at [2 BN + 2 UC + UC d, +UC)
@@ -1005,7 +1016,7 @@ struct BwdPersistTraits : tc::TraitsBase, BwdEpi {
     __device__ static void load2c(const LoadCtx& c, int kb, uint8_t* sA, uint8_t* sB, uint32_t bar) {
         const int k0 = (c.kbase + kb) * kBK;
         ptx::tma_load_2d_2sm(sA, c.a, bar, k0, c.rowA);
-        if constexpr (UC == 64) {
+        if constexpr (B_MN) {
 #pragma unroll
             for (int j = 0; j < BN / 128; ++j) ptx::tma_load_2d_2sm_hint(sB + j * 64 * kBK * 2, c.b, bar, c.bcol + 64 * j, k0, c.keep);
         } else {
@@ -1437,8 +1448,9 @@ bool lstm_fwd_layer_persistent(const LstmFwdLayer& L, int ndirs, int B, int H, i
 
 
 bool lstm_bwd_wants_whh_t(int ndirs, int B, int H) {
-    return knobs().persist_bwd && knobs().pair_mma && knobs().bwd_u32 && !knobs().bwd_kq4 && ndirs == 2 &&
-           B % (2 * kBM) == 0 && H % 128 == 0 && (B / (2 * kBM)) * (H / 128) * 2 * 2 <= num_sms() / 2;
+    if (!(knobs().persist_bwd && knobs().pair_mma && !knobs().bwd_kq4 && ndirs == 2 && B % (2 * kBM) == 0 && H % 128 == 0))
+        return false;
+    return knobs().bwd_kmajor || (knobs().bwd_u32 && (B / (2 * kBM)) * (H / 128) * 2 * 2 <= num_sms() / 2);
 }
 
 bool lstm_bwd_layer_persistent(const LstmBwdLayer& L, int ndirs, int B, int H, int T, cudaStream_t s, float* sk_scratch,
@@ -1448,6 +1460,7 @@ bool lstm_bwd_layer_persistent(const LstmBwdLayer& L, int ndirs, int B, int H, i
     // 32 units per CTA when 64-unit blocks would leave more than half of the pairs idle (needs W_hh^T)
     const int uc = (kq == 2 && knobs().bwd_u32 && L.w_hh_t[0] && L.w_hh_t[1] && H % 64 == 0 &&
                     (B / (2 * kBM)) * (H / 128) * 2 * 2 <= num_sms() / 2) ? 32 : 64;
+    const bool kmaj = uc == 64 && kq == 2 && knobs().bwd_kmajor && L.w_hh_t[0] && L.w_hh_t[1];
     const int m_tiles = B / (2 * kBM), n_tiles = H / (uc * kq);
     const int units = m_tiles * n_tiles * kq;
     if (!(knobs().persist_bwd && knobs().pair_mma && ndirs == 2 && T >= 2 && B % (2 * kBM) == 0 && H % 128 == 0 &&
@@ -1460,7 +1473,7 @@ bool lstm_bwd_layer_persistent(const LstmBwdLayer& L, int ndirs, int B, int H, i
         BwdGroup& g = p.g[d];
         const int64_t TB = static_cast<int64_t>(T) * B;
         make_map_box(&g.ta, L.dZ + d * G4, G4, TB, L.ld_dz, kBM);
-        if (uc == 32) make_map_box(&g.tb, L.w_hh_t[d], G4, H, G4, uc * kq / 2);  // K-major W_hh^T [H x 4H]
+        if (uc == 32 || kmaj) make_map_box(&g.tb, L.w_hh_t[d], G4, H, G4, uc * kq / 2);  // K-major W_hh^T [H x 4H]
         else make_map_box(&g.tb, L.w_hh[d], H, G4, H, 64);
         make_map_gen(&g.m_dH, L.dH + d * H, true, H, TB, L.lddh, 16, 32, CU_TENSOR_MAP_SWIZZLE_64B);
         make_map_gen(&g.m_dc, L.dc_rec[d], true, H, B, H, 16, 32, CU_TENSOR_MAP_SWIZZLE_64B);
@@ -1490,6 +1503,7 @@ bool lstm_bwd_layer_persistent(const LstmBwdLayer& L, int ndirs, int B, int H, i
     };
     if (kq == 4) launch(BwdPersistTraits<4>{});
     else if (uc == 32) launch(BwdPersistTraits<2, 32>{});
+    else if (kmaj) launch(BwdPersistTraits<2, 64, true>{});
     else launch(BwdPersistTraits<2>{});
     count_launch();
     return true;

@@ -1,0 +1,131 @@
+// tcgen05.mma issue-rate probe: one thread per CTA pair issues back-to-back
+// tcgen05.mma.cta_group::2.kind::f16 (bf16 in, fp32 accumulate) on smem-resident operands
+// (no TMA, no epilogue) and times them with clock64; N in {64, 128, 256}, B K- or MN-major,
+// and 1 or 74 pairs busy (one SM pair vs the whole chip, i.e. also the power / clock effect).
+//   build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I paper_2110_11199_b200/csrc -o tools/mma_rate tools/mma_rate.cu
+#include <cstdio>
+#include <cstdlib>
+
+#include "tc_ptx.cuh"
+
+using namespace ab;
+constexpr int NSLOT = 10;  // 160 KB bulk-copy ring
+
+#define CK(x)                                                                                 \
+    do {                                                                                      \
+        cudaError_t e_ = (x);                                                                 \
+        if (e_ != cudaSuccess) {                                                              \
+            std::fprintf(stderr, "%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e_)); \
+            std::exit(1);                                                                     \
+        }                                                                                     \
+    } while (0)
+
+// smem: A 16 KB (128 rows x 64 K, SW128 K-major) | B 16 KB (128 rows x 64 K, or MN-major 64 K-rows x 128)
+// load = 1: meanwhile one thread per CTA streams 16 KB bulk copies (global -> smem, a 4-slot ring
+// outside the operand tiles) as fast as they complete: MMA operand reads vs TMA writes in smem
+__global__ void __launch_bounds__(128) mma_rate(int N, int b_mn, int iters, unsigned long long* out, int load,
+                                                const uint8_t* src, unsigned long long* loaded) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ __align__(8) uint64_t done, lbar[NSLOT];
+    __shared__ uint32_t tslot;
+    const uint32_t rank = ptx::cluster_ctarank();
+    for (int i = threadIdx.x; i < 32768 / 16; i += blockDim.x) ptx::st_shared_v4(ptx::smem_u32(sm) + 16 * i, 0, 0, 0, 0);
+    ptx::fence_proxy_async_smem();
+    if (threadIdx.x == 0) {
+        ptx::mbar_init(&done, 1);
+        for (int i = 0; i < NSLOT; ++i) ptx::mbar_init(&lbar[i], 1);
+        ptx::fence_barrier_init();
+    }
+    if (threadIdx.x >= 32 && threadIdx.x < 64) ptx::tmem_alloc_2sm(&tslot, 512);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::cluster_sync();
+    ptx::tc_fence_after();
+    const uint32_t tbase = tslot;
+    if (threadIdx.x == 32 && rank == 0) {
+        const uint32_t idesc = ptx::idesc_bf16_f32(256, N, false, b_mn != 0);
+        const uint32_t a = ptx::smem_u32(sm), b = ptx::smem_u32(sm + 16384);
+        const long long t0 = clock64();
+        for (int i = 0; i < iters; ++i) {
+            const int kk = i & 3;
+            const uint64_t ad = ptx::umma_desc_sw128(a + kk * 32, 16, 1024);
+            const uint64_t bd = b_mn ? ptx::umma_desc_sw128(b + kk * 2048, 64 * 64 * 2, 1024) : ptx::umma_desc_sw128(b + kk * 32, 16, 1024);
+            ptx::mma_bf16_2sm(tbase + (i & 1) * 256, ad, bd, idesc, i > 1);
+        }
+        ptx::mma_commit_2sm(&done, 3);
+        ptx::mbar_wait(&done, 0);
+        const long long t1 = clock64();
+        out[blockIdx.x / 2] = static_cast<unsigned long long>(t1 - t0);
+    }
+    if (load && threadIdx.x == 64) {  // streaming loader (both CTAs) until the pair's MMAs are done
+        uint8_t* ring = sm + 32768;
+        unsigned long long n = 0;
+        uint32_t ph[NSLOT] = {};
+        for (int i = 0; i < NSLOT; ++i) {
+            ptx::mbar_arrive_expect_tx(&lbar[i], 16384);
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 16384, [%2];" ::"r"(
+                             ptx::smem_u32(ring + i * 16384)), "l"(src + (static_cast<size_t>(blockIdx.x) * NSLOT + i) * 16384),
+                         "r"(ptx::smem_u32(&lbar[i])) : "memory");
+        }
+        const long long t0 = clock64();
+        int last = 0;
+        for (int i = 0;; i = (i + 1) % NSLOT) {
+            last = i;
+            ptx::mbar_wait(&lbar[i], ph[i]);
+            ph[i] ^= 1;
+            ++n;
+            uint32_t fin;
+            asm volatile("{\n.reg .pred P;\nmbarrier.test_wait.parity.shared::cta.b64 P, [%1], 0;\nselp.u32 %0, 1, 0, P;\n}\n"
+                         : "=r"(fin) : "r"(ptx::smem_u32(&done)) : "memory");
+            if (fin) break;
+            ptx::mbar_arrive_expect_tx(&lbar[i], 16384);
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 16384, [%2];" ::"r"(
+                             ptx::smem_u32(ring + i * 16384)), "l"(src + (static_cast<size_t>(blockIdx.x) * NSLOT + i) * 16384),
+                         "r"(ptx::smem_u32(&lbar[i])) : "memory");
+        }
+        const long long t1 = clock64();
+        loaded[blockIdx.x] = n * 16384 * 1000 / static_cast<unsigned long long>(t1 - t0);  // milli-bytes per clock
+        for (int j = 1; j < NSLOT; ++j) ptx::mbar_wait(&lbar[(last + j) % NSLOT], ph[(last + j) % NSLOT]);  // outstanding copies
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::cluster_sync();
+    if (threadIdx.x >= 32 && threadIdx.x < 64) ptx::tmem_dealloc_2sm(tbase, 512);
+}
+
+int main() {
+    unsigned long long *out, *loaded;
+    uint8_t* src;
+    CK(cudaMallocManaged(&out, 8 * 128));
+    CK(cudaMallocManaged(&loaded, 8 * 160));
+    CK(cudaMalloc(&src, 160ull * NSLOT * 16384));
+    CK(cudaMemset(src, 0, 160ull * NSLOT * 16384));
+    CK(cudaFuncSetAttribute(mma_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, (33 + 16 * NSLOT) * 1024));
+    const int iters = 20000;
+    for (int load : {0, 1})
+    for (int pairs : {1, 74})
+        for (int b_mn : {0})
+            for (int N : {128, 256}) {
+                cudaLaunchConfig_t lc = {};
+                cudaLaunchAttribute at[1];
+                at[0].id = cudaLaunchAttributeClusterDimension;
+                at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+                lc.attrs = at; lc.numAttrs = 1;
+                lc.gridDim = dim3(2 * pairs); lc.blockDim = dim3(128); lc.dynamicSmemBytes = (33 + 16 * NSLOT) * 1024;
+                double best = 1e30;
+                for (int rep = 0; rep < 3; ++rep) {
+                    CK(cudaLaunchKernelEx(&lc, mma_rate, N, b_mn, iters, out, load, (const uint8_t*)src, loaded));
+                    CK(cudaDeviceSynchronize());
+                    unsigned long long mx = 0;
+                    for (int p = 0; p < pairs; ++p) mx = out[p] > mx ? out[p] : mx;
+                    best = mx < best ? mx : best;
+                }
+                const double per = best / iters, ideal = 256.0 * N * 16 * 2 / (2 * 8192.0);
+                double lb = 0;
+                for (int c = 0; c < 2 * pairs; ++c) lb += loaded[c] / 1000.0;
+                std::printf("load=%d pairs=%2d B %s N=%3d: %7.1f clk per MMA (ideal %5.1f): %5.1f%% of the tensor peak; bulk copies %.1f B/clk per SM\n",
+                            load, pairs, b_mn ? "MN-major" : "K-major ", N, per, ideal, 100.0 * ideal / per, load ? lb / (2 * pairs) : 0.0);
+            }
+    return 0;
+}
