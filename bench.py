@@ -77,6 +77,7 @@ class ClockSampler:
     def __init__(self, device: int):
         self.device, self.proc, self.lines = device, None, []
         self.samples, self.max_mhz, self.reason_bits = [], None, 0
+        self.e0 = self.e1 = self.t0 = self.t1 = None  # NVML total energy (mJ) and wall time around the region
         self._stop = threading.Event()
         self._thread = None
 
@@ -105,6 +106,11 @@ class ClockSampler:
         try:
             nv, h = self._nvml_handle()
             self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            self._nv, self._h = nv, h
+            try:
+                self.e0, self.t0 = nv.nvmlDeviceGetTotalEnergyConsumption(h), time.perf_counter()
+            except Exception:
+                self.e0 = None
             self._thread = threading.Thread(target=self._poll, args=(nv, h), daemon=True)
             self._thread.start()
             return self
@@ -127,6 +133,11 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *exc):
+        if self._thread and self.e0 is not None:
+            try:
+                self.e1, self.t1 = self._nv.nvmlDeviceGetTotalEnergyConsumption(self._h), time.perf_counter()
+            except Exception:
+                self.e1 = None
         if self._thread:
             self._stop.set()
             self._thread.join(timeout=2)
@@ -141,8 +152,12 @@ class ClockSampler:
         if self._thread is not None:
             sm = sorted(self.samples)
             reasons = sorted(n for n, b in self._BITS.items() if self.reason_bits & b)
-            return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": self.max_mhz, "reasons": reasons,
-                    "samples": len(sm), "source": "nvml 20 ms"}
+            out = {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                   "samples": len(sm), "source": "nvml 20 ms"}
+            if self.e0 is not None and self.e1 is not None and self.t1 > self.t0:
+                out["energy_j"] = (self.e1 - self.e0) / 1000.0  # board energy over the timed region (NVML, mJ counter)
+                out["power_w_avg"] = out["energy_j"] / (self.t1 - self.t0)
+            return out
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
@@ -443,6 +458,10 @@ def run_ours(a):
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
     }
+    cs = line["clocks"]
+    if cs.get("energy_j"):  # board energy of the timed region (power-capped part: J per step sets the step time)
+        line["energy"] = {"j_per_step": cs["energy_j"] / a.steps, "power_w_avg": cs["power_w_avg"],
+                          "frames_per_joule": a.batch * T_UNROLL * a.steps / cs["energy_j"], "source": "NVML total energy counter"}
     print(json.dumps(line), flush=True)
     g.close()
 

@@ -66,6 +66,26 @@ struct CeTraits : tc::TraitsBase {
         ptx::tma_load_2d_2sm(sA, &p.ta, bar, kb * kBK, m0);
         ptx::tma_load_2d_2sm_hint(sB, &p.tb, bar, kb * kBK, n0, ptx::policy_evict_last());
     }
+    // per-item TMA context (tc_core.cuh HasLoadCtx)
+    struct LoadCtx {
+        const CUtensorMap* a;
+        const CUtensorMap* b;
+        int m0, n0;
+        uint64_t keep;
+    };
+    __device__ static LoadCtx load_ctx(const CeParams& p, int tile, uint32_t rank) {
+        LoadCtx c;
+        c.a = &p.ta;
+        c.b = &p.tb;
+        c.m0 = (tile % p.m_tiles) * 2 * kBM + kBM * static_cast<int>(rank);
+        c.n0 = (tile / p.m_tiles) * BN + (BN / 2) * static_cast<int>(rank);
+        c.keep = ptx::policy_evict_last();
+        return c;
+    }
+    __device__ static void load2c(const LoadCtx& c, int kb, uint8_t* sA, uint8_t* sB, uint32_t bar) {
+        ptx::tma_load_2d_2sm(sA, c.a, bar, kb * kBK, c.m0);
+        ptx::tma_load_2d_2sm_hint(sB, c.b, bar, kb * kBK, c.n0, c.keep);
+    }
     __device__ static void epilogue(const CeParams& p, int tile, uint32_t tbase, int q, int lane, uint64_t* tempty,
                                     uint8_t* st, uint64_t*, uint32_t&, tc::EpiSlot sl) {
         const int m0 = (tile % p.m_tiles) * kBM, nt = tile / p.m_tiles;

@@ -201,6 +201,44 @@ struct GenTraits : tc::TraitsBase {
             }
         }
     }
+    // Per-item TMA context (tc_core.cuh HasLoadCtx): the tile's row / column bases and the segment
+    // boundary once per item; load2c is load2 without the per-k-block divisions by the tile counts.
+    struct LoadCtx {
+        const CUtensorMap* a[2];
+        const CUtensorMap* b[2];
+        int m0, nb, kbs;
+    };
+    __device__ static LoadCtx load_ctx(const TcParams& p, int tile, uint32_t rank) {
+        constexpr int SUBN = BN > 256 ? 256 : BN;
+        LoadCtx c;
+        for (int s = 0; s < 2; ++s) { c.a[s] = &p.ta[s]; c.b[s] = &p.tb[s]; }
+        c.m0 = (tile % p.m_tiles) * 2 * BM + BM * static_cast<int>(rank);
+        c.nb = (tile / p.m_tiles) * BN + (SUBN / 2) * static_cast<int>(rank);
+        c.kbs = p.kblocks[0];
+        return c;
+    }
+    __device__ static void load2c(const LoadCtx& c, int kb, uint8_t* sA, uint8_t* sB, uint32_t bar) {
+        const int s = kb < c.kbs ? 0 : 1;
+        const int k0 = (kb - s * c.kbs) * BK;
+        if (AMN) {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j) ptx::tma_load_2d_2sm(sA + j * 64 * BK * 2, c.a[s], bar, c.m0 + 64 * j, k0);
+        } else {
+            ptx::tma_load_2d_2sm(sA, c.a[s], bar, k0, c.m0);
+        }
+        constexpr int SUBN = BN > 256 ? 256 : BN;
+#pragma unroll
+        for (int u = 0; u < BN / SUBN; ++u) {
+            const int n0 = c.nb + u * SUBN;
+            uint8_t* dst = sB + u * (SUBN / 2) * BK * 2;
+            if (BMN) {
+#pragma unroll
+                for (int j = 0; j < SUBN / 128; ++j) ptx::tma_load_2d_2sm(dst + j * 64 * BK * 2, c.b[s], bar, n0 + 64 * j, k0);
+            } else {
+                ptx::tma_load_2d_2sm(dst, c.b[s], bar, k0, n0);
+            }
+        }
+    }
     // MCB (MN-major B, BN = 256): cluster CTA c = 2 pc + r loads A rows as usual and B chunk pc of
     // its pair-rank half, multicast to CTA c and CTA c ^ 2 (the other pair's same-rank CTA).
     __device__ static void load2_mc(const TcParams& p, int tile, int kb, uint32_t crank, uint8_t* sA, uint8_t* sB,

@@ -5,7 +5,8 @@ for cfg in "$@"; do
 import json,sys
 d=json.loads(sys.stdin.read())
 k=d['kernel_ms_per_step']
-print(round(d['value']), round(d['ms_per_step'],3), 'sm', d['clocks'].get('sm_mhz'), d['clocks'].get('reasons'),
+e=d.get('energy',{})
+print(round(d['value']), round(d['ms_per_step'],3), 'sm', d['clocks'].get('sm_mhz'), d['clocks'].get('reasons'), 'J/step', round(e.get('j_per_step',0),2), 'W', round(e.get('power_w_avg',0)),
       {x: round(k[x],3) for x in ('gemm_rec_fwd','gemm_rec_bwd','gemm_wgrad','gemm_dgrad_x','gemm_out') if x in k})")
   echo "[$cfg] $v"
 done
