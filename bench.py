@@ -326,13 +326,14 @@ def run_ours(a):
     # computed; every timed step still moves its whole batch host -> device inside the region
     pf = _lib.lib().adpsgd_prefetch_host_batch
     barrier()
-    t0 = time.perf_counter()
-    _lib.check(pf(g.handle, fptr, lptr))
-    for i in range(e2e_steps):
-        if i + 1 < e2e_steps:
-            _lib.check(pf(g.handle, fptr, lptr))
-        _lib.check(_lib.lib().adpsgd_step_host_batch(g.handle, lr, fptr, lptr, loss))
-    e2e_s = P.max_over_ranks(time.perf_counter() - t0)
+    with ClockSampler(dev) as clk_e2e:  # clocks of this region too (the device-timed value ran at its own clock)
+        t0 = time.perf_counter()
+        _lib.check(pf(g.handle, fptr, lptr))
+        for i in range(e2e_steps):
+            if i + 1 < e2e_steps:
+                _lib.check(pf(g.handle, fptr, lptr))
+            _lib.check(_lib.lib().adpsgd_step_host_batch(g.handle, lr, fptr, lptr, loss))
+        e2e_s = P.max_over_ranks(time.perf_counter() - t0)
     barrier()
     e2e_val = world * a.batch * T_UNROLL * e2e_steps / e2e_s
 
@@ -424,7 +425,8 @@ def run_ours(a):
                    "train_flops_per_frame": m.train_flops_per_frame()},
         "e2e": {"value": e2e_val, "unit": "frames/s", "h2d_bytes_per_step": nf * 4 + a.batch * T_UNROLL * 4,
                 "d2h_bytes_per_step": 4, "steps": e2e_steps,
-                "h2d": "pinned host batch, prefetched one step ahead on a copy stream (adpsgd_prefetch_host_batch)"},
+                "h2d": "pinned host batch, prefetched one step ahead on a copy stream (adpsgd_prefetch_host_batch)",
+                "clocks": clk_e2e.summary()},
         "roofline": {"bound": "tensor",
                      "kernel": ("persistent_kernel_2cta<FwdPersistT<64>>: one launch per layer = 21 steps x 2 "
                                 "directions of the fused recurrent GEMM [x_t|h_t-1][W_ih|W_hh]^T + LSTM cell, "

@@ -376,9 +376,16 @@ struct BwdEpi {
         if (!r.dc_tmem) ptx::tma_load_2d(in + 2048, &g.m_dc, bar, j0, rowbase + r.dc);
         if (!r.c_tmem) ptx::tma_load_2d_hint(in + 4096, &g.m_c, bar, j0, rowbase + r.data, stream);
         if (r.has_prev) ptx::tma_load_2d_hint(in + 6144, &g.m_cp, bar, j0, rowbase + r.cp, stream);
+#ifdef ADPSGD_DBG_BWD_NOGATES  // timing experiments only: gates not loaded (one box stands in for the bytes)
+        ptx::tma_load_2d_hint(in + 8192, &g.m_gates, bar, j0, rowbase + r.data, stream);
+        ptx::tma_load_2d_hint(in + 9216, &g.m_gates, bar, j0 + H, rowbase + r.data, stream);
+        ptx::tma_load_2d_hint(in + 10240, &g.m_gates, bar, j0 + 2 * H, rowbase + r.data, stream);
+        ptx::tma_load_2d_hint(in + 11264, &g.m_gates, bar, j0 + 3 * H, rowbase + r.data, stream);
+#else
 #pragma unroll
         for (int gi = 0; gi < 4; ++gi)
             ptx::tma_load_2d_hint(in + 8192 + gi * 1024, &g.m_gates, bar, gi * H + j0, rowbase + r.data, stream);
+#endif
     }
     // SMEM: issue the first two chunks into the warp's staging smem (not with an overlaid
     // epilogue: the stages are busy during the mainloop) and L2-prefetch the rest; else
@@ -539,8 +546,10 @@ struct BwdEpi {
             ptx::fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
+#ifndef ADPSGD_DBG_BWD_NOSTORE  // timing experiments only: dz not stored
 #pragma unroll
                 for (int gi = 0; gi < 4; ++gi) ptx::tma_store_2d(&g.m_dz, bdz + gi * 1024, gi * H + j0, rowbase + r.data);
+#endif
                 if (!(r.tstate && r.tdc_valid)) ptx::tma_store_2d(&g.m_dc, bdco, j0, rowbase + r.dc);
                 ptx::bulk_commit();
                 if (INPLACE && uc + NBUF * step < SPAN) {

@@ -10,7 +10,7 @@
 #include <cstring>
 
 namespace ab {
-constexpr size_t kTraceWords = 160 * 48 + 160 * 64 * 12 + 2 * 8 * 64 * 2;  // tc_core.cuh: stamps + per-item timeline
+constexpr size_t kTraceWords = 160 * 48 + 160 * 64 * 12 + 2 * 8 * 64 * 3;  // tc_core.cuh: stamps + per-item timeline
 unsigned long long* g_trace_buf = nullptr;  // device buffer while tracing is on (tc_core.cuh)
 int g_trace_skip = 0;                       // pair-kernel launches to skip before the traced one
 

@@ -43,8 +43,9 @@ __device__ __forceinline__ void trace_item(unsigned long long* buf, int item, in
         buf[kTraceCtas * kTraceEv + (blockIdx.x * kTraceItems + item) * kTraceItemEv + ev] = t;
     }
 }
-// per-k-block detail of CTAs 0 and 1, items < 8 (after the item block): [cta][item][kb < 64][2]
-// 0 = producer issued the k-block's loads, 1 = the MMA warp saw the stage full (leader CTA only)
+// per-k-block detail of CTAs 0 and 1, items < 8 (after the item block): [cta][item][kb < 64][3]
+// 0 = producer issued the k-block's loads, 1 = the MMA warp saw the stage full (leader CTA only),
+// 2 = producer got the empty stage (before issuing)
 constexpr int kTraceDetailItems = 8, kTraceDetailKb = 64;
 __device__ __forceinline__ void trace_kb(unsigned long long* buf, int item, int kb, int ev) {
 #ifndef ADPSGD_ITEM_TRACE
@@ -54,7 +55,7 @@ __device__ __forceinline__ void trace_kb(unsigned long long* buf, int item, int 
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         buf[kTraceCtas * kTraceEv + kTraceCtas * kTraceItems * kTraceItemEv +
-            ((blockIdx.x * kTraceDetailItems + item) * kTraceDetailKb + kb) * 2 + ev] = t;
+            ((blockIdx.x * kTraceDetailItems + item) * kTraceDetailKb + kb) * 3 + ev] = t;
     }
 }
 // per-item / per-k-block instrumentation (trace_item*, wait durations, trace_kb): only in ADPSGD_ITEM_TRACE builds
@@ -399,6 +400,7 @@ __global__ void __launch_bounds__(64 + 32 * Traits::EPI_WARPS, 1) persistent_ker
                     const unsigned long long tw0 = gtimer(p.trace);
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
                     ewait += gtimer(p.trace) - tw0;
+                    trace_kb(p.trace, it, kb - w.kb0, 2);
                     if (kb == w.kb0) trace_item(p.trace, it, 0);
                     if (kb == w.kb0 + 32) trace_item(p.trace, it, 1);
                     if (kb + 1 == w.kb1) trace_item(p.trace, it, 2);

@@ -24,13 +24,22 @@ constexpr int NSLOT = 10;  // 160 KB bulk-copy ring
 // load = 1: meanwhile one thread per CTA streams 16 KB bulk copies (global -> smem, a 4-slot ring
 // outside the operand tiles) as fast as they complete: MMA operand reads vs TMA writes in smem
 __global__ void __launch_bounds__(128) mma_rate(int N, int b_mn, int iters, unsigned long long* out, int load,
-                                                const uint8_t* src, unsigned long long* loaded) {
+                                                const uint8_t* src, unsigned long long* loaded, int rnd) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     __shared__ __align__(8) uint64_t done, lbar[NSLOT];
     __shared__ uint32_t tslot;
     const uint32_t rank = ptx::cluster_ctarank();
-    for (int i = threadIdx.x; i < 32768 / 16; i += blockDim.x) ptx::st_shared_v4(ptx::smem_u32(sm) + 16 * i, 0, 0, 0, 0);
+    for (int i = threadIdx.x; i < 32768 / 16; i += blockDim.x) {
+        // rnd = 1: pseudo-random bf16 operands (sign / exponent near 1, full mantissa) instead of zeros
+        uint32_t w[4];
+        for (int k = 0; k < 4; ++k) {
+            uint32_t h = (i * 4 + k + 1) * 2654435761u;
+            h ^= h >> 13; h *= 0x5bd1e995u; h ^= h >> 15;
+            w[k] = rnd ? ((h & 0x807F807Fu) | 0x3F003F00u) : 0u;
+        }
+        ptx::st_shared_v4(ptx::smem_u32(sm) + 16 * i, w[0], w[1], w[2], w[3]);
+    }
     ptx::fence_proxy_async_smem();
     if (threadIdx.x == 0) {
         ptx::mbar_init(&done, 1);
@@ -102,8 +111,9 @@ int main() {
     CK(cudaMalloc(&src, 160ull * NSLOT * 16384));
     CK(cudaMemset(src, 0, 160ull * NSLOT * 16384));
     CK(cudaFuncSetAttribute(mma_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, (33 + 16 * NSLOT) * 1024));
-    const int iters = 20000;
-    for (int load : {0, 1})
+    const int iters = 200000;
+    for (int rnd : {0, 1})
+    for (int load : {0})
     for (int pairs : {1, 74})
         for (int b_mn : {0})
             for (int N : {128, 256}) {
@@ -115,7 +125,7 @@ int main() {
                 lc.gridDim = dim3(2 * pairs); lc.blockDim = dim3(128); lc.dynamicSmemBytes = (33 + 16 * NSLOT) * 1024;
                 double best = 1e30;
                 for (int rep = 0; rep < 3; ++rep) {
-                    CK(cudaLaunchKernelEx(&lc, mma_rate, N, b_mn, iters, out, load, (const uint8_t*)src, loaded));
+                    CK(cudaLaunchKernelEx(&lc, mma_rate, N, b_mn, iters, out, load, (const uint8_t*)src, loaded, rnd));
                     CK(cudaDeviceSynchronize());
                     unsigned long long mx = 0;
                     for (int p = 0; p < pairs; ++p) mx = out[p] > mx ? out[p] : mx;
@@ -124,8 +134,8 @@ int main() {
                 const double per = best / iters, ideal = 256.0 * N * 16 * 2 / (2 * 8192.0);
                 double lb = 0;
                 for (int c = 0; c < 2 * pairs; ++c) lb += loaded[c] / 1000.0;
-                std::printf("load=%d pairs=%2d B %s N=%3d: %7.1f clk per MMA (ideal %5.1f): %5.1f%% of the tensor peak; bulk copies %.1f B/clk per SM\n",
-                            load, pairs, b_mn ? "MN-major" : "K-major ", N, per, ideal, 100.0 * ideal / per, load ? lb / (2 * pairs) : 0.0);
+                std::printf("rnd=%d load=%d pairs=%2d B %s N=%3d: %7.1f clk per MMA (ideal %5.1f): %5.1f%% of the tensor peak; bulk copies %.1f B/clk per SM\n",
+                            rnd, load, pairs, b_mn ? "MN-major" : "K-major ", N, per, ideal, 100.0 * ideal / per, load ? lb / (2 * pairs) : 0.0);
             }
     return 0;
 }

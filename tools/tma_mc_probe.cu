@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(64) probe(const __grid_constant__ CUtensorMap 
 //   pat 4 (forward): A = [x|h] [1024 x 3072] K-major, B = W [4096 x 3072] K-major, two 64-row gate
 //                 boxes per CTA (64 units x 4 gates per pair): 48 k-blocks
 __global__ void __launch_bounds__(64) probe2(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB,
-                                             int pat, int stages, int iters) {
+                                             int pat, int stages, int iters, int split) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     __shared__ __align__(8) uint64_t full[8], empty[8];
@@ -135,25 +135,27 @@ __global__ void __launch_bounds__(64) probe2(const __grid_constant__ CUtensorMap
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&full[s])), "r"(SB) : "memory");
             const int kb = i % kbs;
             uint8_t* dst = sm + s * SB;
-            int a0, a1, b0[2], b1[2], nb;
+            int a0, a1;
             if (pat == 3) {
                 const int mt = pair % 4, nt = (pair / 4) % 8, kh = pair / 32;
                 const int k0 = kh * 2048 + kb * 64;
                 a0 = k0; a1 = mt * 256 + r * 128;
-                b0[0] = nt * 128 + r * 64; b1[0] = k0; nb = 1;
+                asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+                                 su32(dst + 16384)), "l"(reinterpret_cast<uint64_t>(&mB)), "r"(nt * 128 + r * 64), "r"(k0),
+                             "r"(su32(&full[s])) : "memory");
             } else {
                 const int mt = pair % 4, nt = pair / 4;
                 const int k0 = kb * 64;
                 a0 = k0; a1 = mt * 256 + r * 128;
-                for (int j = 0; j < 2; ++j) { b0[j] = k0; b1[j] = (2 * r + j) * 1024 + nt * 64; }
-                nb = 2;
+                const int br = 64 / split;  // split: B boxes of 64 / split rows (same bytes, more TMA ops)
+                for (int j = 0; j < 2; ++j)
+                    for (int q = 0; q < split; ++q)
+                        asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+                                         su32(dst + 16384 + (j * split + q) * (8192 / split))), "l"(reinterpret_cast<uint64_t>(&mB)), "r"(k0),
+                                     "r"((2 * r + j) * 1024 + nt * 64 + q * br), "r"(su32(&full[s])) : "memory");
             }
             asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
                              su32(dst)), "l"(reinterpret_cast<uint64_t>(&mA)), "r"(a0), "r"(a1), "r"(su32(&full[s])) : "memory");
-            for (int j = 0; j < nb; ++j)
-                asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-                                 su32(dst + 16384 + j * 8192)), "l"(reinterpret_cast<uint64_t>(&mB)), "r"(b0[j]), "r"(b1[j]),
-                             "r"(su32(&full[s])) : "memory");
         }
     } else if (threadIdx.x == 32) {
         for (int i = 0; i < total; ++i) {
@@ -328,11 +330,13 @@ int main(int argc, char** argv) {
         CK(cudaMemset(B, 1, 4096ull * 3072 * 2));
         CK(cudaFuncSetAttribute(probe2, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
         for (int pat = 3; pat <= 4; ++pat)
-            for (int stages : {3, 5, 6, 8}) {
+            for (int split : {1, 2, 4, 8})
+            for (int stages : {5}) {
                 if (stages * (pat == 3 ? 24576 : 32768) + 1024 > 220 * 1024) continue;
+                if (pat == 3 && split > 1) continue;
                 CUtensorMap ma, mb;
                 if (pat == 3) { mk(&ma, A, 4096, 1024, 64, 128); mk(&mb, B, 1024, 4096, 64, 64); }
-                else { mk(&ma, A, 3072, 1024, 64, 128); mk(&mb, B, 3072, 4096, 64, 64); }
+                else { mk(&ma, A, 3072, 1024, 64, 128); mk(&mb, B, 3072, 4096, 64, 64 / split); }
                 const int SB = pat == 3 ? 24576 : 32768;
                 const int iters = 200;
                 cudaEvent_t e0, e1;
@@ -341,7 +345,7 @@ int main(int argc, char** argv) {
                 float best = 1e30f;
                 for (int rep = 0; rep < 4; ++rep) {
                     CK(cudaEventRecord(e0));
-                    probe2<<<128, 64, stages * SB + 1024>>>(ma, mb, pat, stages, iters);
+                    probe2<<<128, 64, stages * SB + 1024>>>(ma, mb, pat, stages, iters, split);
                     CK(cudaEventRecord(e1));
                     CK(cudaEventSynchronize(e1));
                     float ms;
@@ -351,8 +355,8 @@ int main(int argc, char** argv) {
                 CK(cudaGetLastError());
                 const int kbs = pat == 3 ? 32 : 48;
                 const double delivered = 128.0 * kbs * iters * SB;
-                std::printf("pat=%d (%s) stages=%d: %8.1f us  %6.2f TB/s delivered (%5.1f GB/s per SM), %.2f us per item\n", pat,
-                            pat == 3 ? "BPTT" : "fwd", stages, best * 1e3, delivered / best / 1e9, delivered / best / 1e6 / 128,
+                std::printf("pat=%d (%s) B boxes of %d rows, stages=%d: %8.1f us  %6.2f TB/s delivered (%5.1f GB/s per SM), %.2f us per item\n", pat,
+                            pat == 3 ? "BPTT" : "fwd", 64 / split, stages, best * 1e3, delivered / best / 1e9, delivered / best / 1e6 / 128,
                             best * 1e3 / iters);
             }
 

@@ -26,7 +26,7 @@ def main():
     g.step(0.1)
     L = _lib.lib()
     DI, DK = 8, 64
-    words = CTAS * EV + CTAS * ITEMS * IEV + 2 * DI * DK * 2
+    words = CTAS * EV + CTAS * ITEMS * IEV + 2 * DI * DK * 3
     for n in ns:
         buf = (C.c_uint64 * words)()
         L.adpsgd_debug_trace(n, None, 0)
@@ -34,7 +34,7 @@ def main():
         L.adpsgd_debug_trace(0, buf, words)
         a = np.array(buf, dtype=np.uint64).astype(np.int64)
         it = a[CTAS * EV:CTAS * EV + CTAS * ITEMS * IEV].reshape(CTAS, ITEMS, IEV)
-        det = a[CTAS * EV + CTAS * ITEMS * IEV:].reshape(2, DI, DK, 2)
+        det = a[CTAS * EV + CTAS * ITEMS * IEV:].reshape(2, DI, DK, 3)
         ctas = int((a[:CTAS * EV].reshape(CTAS, EV)[:, 46] > 0).sum())
         valid = it[:, :, :8] > 0
         if not valid.any():
@@ -60,6 +60,11 @@ def main():
             okc = (it[:, i, 10] > 0) & (it[:, i, 11] > 0)
             clk = f"  {np.median(ck[okc]):9.0f} clk" if okc.any() else ""
             print(f"  {i:4d} " + " ".join(cells) + f"   {mma:7.2f}  {dw:7.2f}{clk}")
+        stamps = a[:CTAS * EV].reshape(CTAS, EV).astype(np.int64)
+        for ev in (40, 41, 42, 43, 44, 45):
+            col = stamps[:, ev]
+            if (col > 0).any():
+                print(f"  stamp ev{ev}: median {np.median((col[col > 0] - t0) / 1000.0):.2f} us")
         # steady-state averages over items 4 .. n-2
         if nitems > 8:
             sl = slice(4, nitems - 2)
@@ -81,11 +86,11 @@ def main():
             base = d0[d0 > 0].min() if (d0 > 0).any() else 0
             print(f"  detail item {item} (CTA 0 / CTA 1 issue, CTA 0 stage full), us from first issue:")
             for kb in range(DK):
-                i0, f0, i1 = det[0, item, kb, 0], det[0, item, kb, 1], det[1, item, kb, 0]
+                i0, f0, i1, g0 = det[0, item, kb, 0], det[0, item, kb, 1], det[1, item, kb, 0], det[0, item, kb, 2]
                 if i0 == 0 and f0 == 0:
                     continue
                 f = lambda x: f"{(x - base) / 1000.0:7.2f}" if x > 0 else "      -"
-                print(f"    kb {kb:2d}: issue {f(i0)} / {f(i1)}  full {f(f0)}  latency {(f0 - max(i0, i1)) / 1000.0 if f0 and i0 and i1 else float('nan'):6.2f}")
+                print(f"    kb {kb:2d}: got-empty {f(g0)} issued {f(i0)} (issue took {(i0 - g0) / 1000.0 if g0 and i0 else float('nan'):5.2f}) / CTA1 {f(i1)}  full {f(f0)}  latency {(f0 - max(i0, i1)) / 1000.0 if f0 and i0 and i1 else float('nan'):6.2f}")
     L.adpsgd_debug_trace(0, None, 0)
 
 
