@@ -40,6 +40,23 @@ void make_map_gen(CUtensorMap* m, const void* base, bool f32, uint64_t inner, ui
     AB_CHECK(r == CUDA_SUCCESS, ADPSGD_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
 }
 
+// 3-D bf16 view [outer2][outer1][inner] (SWIZZLE_128B, 64-element inner box): rows of `ld`
+// elements, blocks of `blk_stride` elements; box {64, box1, box2}. Lands in smem exactly as box2
+// consecutive 2-D boxes of 64 x box1, i.e. the layout the MMA descriptors already expect.
+void make_map_3d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer1, uint64_t outer2, int64_t ld,
+                 int64_t blk_stride, uint32_t box1, uint32_t box2) {
+    AB_CHECK((reinterpret_cast<uintptr_t>(base) & 15) == 0, ADPSGD_E_DIMENSION, "TMA base must be 16B aligned");
+    AB_CHECK(((ld * 2) & 15) == 0 && ((blk_stride * 2) & 15) == 0, ADPSGD_E_DIMENSION, "TMA strides must be multiples of 16 bytes");
+    cuuint64_t dims[3] = {inner, outer1, outer2};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld) * 2, static_cast<cuuint64_t>(blk_stride) * 2};
+    cuuint32_t box[3] = {64, box1, box2};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = get_encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    AB_CHECK(r == CUDA_SUCCESS, ADPSGD_E_CUDA, "cuTensorMapEncodeTiled (3-D) failed: " + std::to_string(r));
+}
+
 namespace {
 
 using tc::kBK;
@@ -811,7 +828,7 @@ struct FwdPersistT : tc::TraitsBase {
     struct LoadCtx {
         const CUtensorMap* a[2];
         const CUtensorMap* b[2];
-        int row[2], brow, H, kbx;
+        int row[2], brow, bgate, H, kbx;
         uint64_t keep;
     };
     __device__ static LoadCtx load_ctx(const FwdPParams& p, int it, uint32_t rank) {
@@ -827,7 +844,8 @@ struct FwdPersistT : tc::TraitsBase {
         c.row[0] = u.t * p.B + r0;
         c.row[1] = u.tp * p.B + r0;
 #endif
-        c.brow = 2 * static_cast<int>(rank) * p.H + u.nt * UW;
+        c.brow = u.nt * UW;  // units of the 3-D gate-block view; gate blocks 2r, 2r + 1
+        c.bgate = 2 * static_cast<int>(rank);
         c.H = p.H;
         c.kbx = p.kbx;
         c.keep = ptx::policy_evict_last();
@@ -839,8 +857,7 @@ struct FwdPersistT : tc::TraitsBase {
         const int seg = kb < c.kbx ? 0 : 1;
         const int k0 = (kb - seg * c.kbx) * kBK;
         ptx::tma_load_2d_2sm(sA, c.a[seg], bar, k0, c.row[seg]);
-        ptx::tma_load_2d_2sm_hint(sB, c.b[seg], bar, k0, c.brow, c.keep);
-        ptx::tma_load_2d_2sm_hint(sB + UW * kBK * 2, c.b[seg], bar, k0, c.brow + c.H, c.keep);
+        ptx::tma_load_3d_2sm_hint(sB, c.b[seg], bar, k0, c.brow, c.bgate, c.keep);
     }
     template <class S>
     __device__ static void epi_begin2(const FwdPParams& p, int it, uint32_t rank, int q, int lane, uint8_t*, uint64_t*,
@@ -1381,9 +1398,10 @@ bool lstm_fwd_layer_persistent(const LstmFwdLayer& L, int ndirs, int B, int H, i
     for (int d = 0; d < 2; ++d) {
         FwdGroup& g = p.g[d];
         make_map_box(&g.ta[0], L.x, L.Kx, TB, L.ldx, kBM);
-        make_map_box(&g.tb[0], L.w_ih[d], L.Kx, 4 * H, L.ld_wih, uw);
+        // B: one 3-D box per k-block = the CTA's two gate blocks (rows 2r H + u0 .. and (2r+1) H + u0 ..)
+        make_map_3d(&g.tb[0], L.w_ih[d], L.Kx, H, 4, L.ld_wih, static_cast<int64_t>(H) * L.ld_wih, uw, 2);
         make_map_box(&g.ta[1], L.h + d * H, H, TB, L.ldh, kBM);
-        make_map_box(&g.tb[1], L.w_hh[d], H, 4 * H, H, uw);
+        make_map_3d(&g.tb[1], L.w_hh[d], H, H, 4, H, static_cast<int64_t>(H) * H, uw, 2);
         make_map_gen(&g.m_cprev, L.c + d * H, true, H, TB, L.ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
         make_map_gen(&g.m_gates, L.gates + d * 4 * H, false, 4 * H, TB, L.ldg, 16, 32, CU_TENSOR_MAP_SWIZZLE_32B);
         make_map_gen(&g.m_c, L.c + d * H, true, H, TB, L.ldc, 16, 32, CU_TENSOR_MAP_SWIZZLE_64B);
