@@ -373,6 +373,11 @@ struct EpiRows {
     bool tstate = false;     // TMEM state addresses present (TMEM address 0 is a valid lane-quarter-0 address)
     bool tdc_valid = false, tc_valid = false;
     uint32_t tdc = 0, tc_ = 0;
+    // compact (8 KB per chunk): dc_rec and c always come from TMEM, so the chunk buffer holds only
+    // dH | c_{t-1} | gates (else 12 KB: dH | dc | c | c_{t-1} | gates)
+    bool compact = false;
+    __device__ int o_cp() const { return compact ? 2048 : 6144; }
+    __device__ int o_g() const { return compact ? 4096 : 8192; }
 };
 
 struct BwdEpi {
@@ -392,17 +397,10 @@ struct BwdEpi {
         ptx::tma_load_2d_hint(in, &g.m_dH, bar, j0, rowbase + r.data, stream);
         if (!r.dc_tmem) ptx::tma_load_2d(in + 2048, &g.m_dc, bar, j0, rowbase + r.dc);
         if (!r.c_tmem) ptx::tma_load_2d_hint(in + 4096, &g.m_c, bar, j0, rowbase + r.data, stream);
-        if (r.has_prev) ptx::tma_load_2d_hint(in + 6144, &g.m_cp, bar, j0, rowbase + r.cp, stream);
-#ifdef ADPSGD_DBG_BWD_NOGATES  // timing experiments only: gates not loaded (one box stands in for the bytes)
-        ptx::tma_load_2d_hint(in + 8192, &g.m_gates, bar, j0, rowbase + r.data, stream);
-        ptx::tma_load_2d_hint(in + 9216, &g.m_gates, bar, j0 + H, rowbase + r.data, stream);
-        ptx::tma_load_2d_hint(in + 10240, &g.m_gates, bar, j0 + 2 * H, rowbase + r.data, stream);
-        ptx::tma_load_2d_hint(in + 11264, &g.m_gates, bar, j0 + 3 * H, rowbase + r.data, stream);
-#else
+        if (r.has_prev) ptx::tma_load_2d_hint(in + r.o_cp(), &g.m_cp, bar, j0, rowbase + r.cp, stream);
 #pragma unroll
         for (int gi = 0; gi < 4; ++gi)
-            ptx::tma_load_2d_hint(in + 8192 + gi * 1024, &g.m_gates, bar, gi * H + j0, rowbase + r.data, stream);
-#endif
+            ptx::tma_load_2d_hint(in + r.o_g() + gi * 1024, &g.m_gates, bar, gi * H + j0, rowbase + r.data, stream);
     }
     // SMEM: issue the first two chunks into the warp's staging smem (not with an overlaid
     // epilogue: the stages are busy during the mainloop) and L2-prefetch the rest; else
@@ -501,15 +499,15 @@ struct BwdEpi {
             tc::ld_row_words<64>(in, lane, wdh);
             if (!r.dc_tmem) tc::ld_row_words<64>(in + 2048, lane, wdc);
             if (!r.c_tmem) tc::ld_row_words<64>(in + 4096, lane, wc);
-            if (has_prev) tc::ld_row_words<64>(in + 6144, lane, wcp);
+            if (has_prev) tc::ld_row_words<64>(in + r.o_cp(), lane, wcp);
             if (r.tstate && r.tc_valid && has_prev) {  // c_{t-1} is the next step's c
                 __syncwarp();
                 ptx::tmem_st_32x32b_x16(r.tc_ + uc, wcp);
             }
-            tc::ld_row_words<32>(in + 8192 + 0 * 1024, lane, wi);
-            tc::ld_row_words<32>(in + 8192 + 1 * 1024, lane, wf);
-            tc::ld_row_words<32>(in + 8192 + 2 * 1024, lane, wg);
-            tc::ld_row_words<32>(in + 8192 + 3 * 1024, lane, wo);
+            tc::ld_row_words<32>(in + r.o_g() + 0 * 1024, lane, wi);
+            tc::ld_row_words<32>(in + r.o_g() + 1 * 1024, lane, wf);
+            tc::ld_row_words<32>(in + r.o_g() + 2 * 1024, lane, wg);
+            tc::ld_row_words<32>(in + r.o_g() + 3 * 1024, lane, wo);
             uint32_t zi[8], zf[8], zg[8], zo[8], dco[16];
 #pragma unroll
             for (int e = 0; e < 16; ++e) {
@@ -924,6 +922,7 @@ using FwdPersistTraits = FwdPersistT<64>;
 struct BwdPParams {
     BwdGroup g[2];  // maps span all T*B rows: ta = dZ(d), tb = W_hh(d), m_dH / m_c / m_cp / m_gates / m_dz; m_dc = dc_rec(d)
     int B, H, T, m_tiles, n_tiles, units, kbh;
+    int64_t ldc;             // row pitch of c (first_step_state)
     float* sk_scratch;       // [pair * 2 + rank][parity][4 chunks][128 rows][16] fp32
     unsigned int* sk_flags;  // [pair * 2 + rank] exchange epochs
     unsigned int* dep;       // [dir][m_tile][rank] finished epilogues
@@ -941,12 +940,19 @@ template <int KQ, int UC = 64, bool KMAJ = false>
 struct BwdPersistTraits : tc::TraitsBase, BwdEpi {
     static constexpr int BN = UC * KQ;  // pair tile width
     static constexpr int NCHK = UC / 16;  // 16-unit chunks per finalised block
+#ifdef ADPSGD_NO_TSTATE
+    static constexpr bool TSTATE_ = false;
+#else
+    static constexpr bool TSTATE_ = KQ == 2;
+#endif
 #ifdef ADPSGD_BWD_EPI_WARPS
     static constexpr int EPI_WARPS = ADPSGD_BWD_EPI_WARPS;  // A/B experiments
 #else
     static constexpr int EPI_WARPS = 8;
 #endif
-    static constexpr int EPI_SMEM = EPI_WARPS * 12 * 1024;  // BwdEpi::body_g<64, INPLACE, .., NBUF = 1>
+    // BwdEpi::body_g<64, INPLACE, .., NBUF = 1>: 12 KB per warp, or 8 KB (compact chunk buffer) when
+    // dc_rec / c live in TMEM from the first step on -- the saved 32 KB buy a 6th mainloop stage
+    static constexpr int EPI_SMEM = EPI_WARPS * (TSTATE_ ? 8 : 12) * 1024;
     static constexpr int ACC_STAGES = 2;
     static constexpr bool A_MN = false;
     static constexpr bool B_MN = UC == 64 && !KMAJ;  // KMAJ: K-major W_hh^T for the 64-unit tiles too
@@ -983,8 +989,12 @@ struct BwdPersistTraits : tc::TraitsBase, BwdEpi {
         r.cp = r.has_prev ? tnp * p.B : 0;
         r.dc = 0;
         if (TSTATE) {
-            r.dc_tmem = u.s > 0;  // the first step's dc_rec comes from the first cell backward (memory)
-            r.c_tmem = u.s > 0;   // c_t = the c_{t-1} this CTA loaded one step earlier
+            // dc_rec and c_t always from TMEM: the first step's (the first cell backward's dc_rec and
+            // c_{T-2} / c_1) are put there by first_step_state() before that step's cell backward;
+            // after it, c_t is the c_{t-1} this CTA loaded one step earlier
+            r.dc_tmem = true;
+            r.c_tmem = true;
+            r.compact = true;
             if (have_q) {         // tmem_q: TMEM base of this warp's lane quarter (epilogue only)
                 r.tstate = true;
                 r.tdc = tmem_q + 2 * BN + UC * u.d;
@@ -994,6 +1004,33 @@ struct BwdPersistTraits : tc::TraitsBase, BwdEpi {
             }
         }
         return r;
+    }
+    // First BPTT step of each direction: load this thread's row of dc_rec (the first cell backward's
+    // output) and of c at tn into the TMEM state columns, for the chunks this warp owns.
+    __device__ static void first_step_state(const BwdPParams& p, const U& u, int m0, int u0, int q, int lane, tc::EpiSlot sl,
+                                            const EpiRows& r) {
+        const BwdGroup& g = p.g[u.d];
+        const int64_t row = m0 + q * 32 + lane;
+        const float* dcrow = g.dc_rec + row * p.H;
+        const float* crow = g.c + (r.data + row) * p.ldc;
+#pragma unroll 1
+        for (int uc = 16 * sl.sub; uc < UC; uc += 16 * sl.n) {
+            uint32_t vdc[16], vc[16];
+            const float4* a = reinterpret_cast<const float4*>(dcrow + u0 + uc);
+            const float4* b = reinterpret_cast<const float4*>(crow + u0 + uc);
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const float4 x = __ldcg(a + v), y = __ldcg(b + v);
+                vdc[4 * v] = __float_as_uint(x.x); vdc[4 * v + 1] = __float_as_uint(x.y);
+                vdc[4 * v + 2] = __float_as_uint(x.z); vdc[4 * v + 3] = __float_as_uint(x.w);
+                vc[4 * v] = __float_as_uint(y.x); vc[4 * v + 1] = __float_as_uint(y.y);
+                vc[4 * v + 2] = __float_as_uint(y.z); vc[4 * v + 3] = __float_as_uint(y.w);
+            }
+            __syncwarp();
+            ptx::tmem_st_32x32b_x16(r.tdc + uc, vdc);
+            ptx::tmem_st_32x32b_x16(r.tc_ + uc, vc);
+        }
+        ptx::tmem_st_wait();
     }
     __device__ static int num_tiles(const BwdPParams& p) { return 2 * (p.T - 1); }
     __device__ static int kblocks(const BwdPParams& p, int) { return p.kbh; }
@@ -1116,9 +1153,12 @@ struct BwdPersistTraits : tc::TraitsBase, BwdEpi {
         for (int j = 0, n = 0; j < KQ; ++j)
             if (j != u.kh) pr[n++] = block(base + j * per, u.kh);
         auto rel = [&] { tc::release_acc_2sm(tempty_leader, lane); };
+        const EpiRows rr = rows(p, u, tbase - (tbase & 0xFFFFu) % (2 * BN), true);
+        if (TSTATE && u.s == 0)
+            first_step_state(p, u, u.mt * 2 * kBM + kBM * static_cast<int>(rank), u.nt * BN + UC * u.kh, q, lane, sl, rr);
         body_g<UC, true, decltype(rel), 1>(p.g[u.d], p.H, u.mt * 2 * kBM + kBM * static_cast<int>(rank),
                                           u.nt * BN + UC * u.kh, tbase + UC * u.kh, q, lane, rel, st, ebar, ephase, sl,
-                                          pr[0], true, rows(p, u, tbase - (tbase & 0xFFFFu) % (2 * BN), true), pr[1], pr[2]);
+                                          pr[0], true, rr, pr[1], pr[2]);
         }
         // 4) publish: this CTA's dz block of step tn is in memory (TMA stores complete)
 #ifdef ADPSGD_DBG_NOEPI
@@ -1508,9 +1548,12 @@ bool lstm_bwd_layer_persistent(const LstmBwdLayer& L, int ndirs, int B, int H, i
         g.m_cp = g.m_c;
         make_map_gen(&g.m_gates, L.gates + d * G4, false, G4, TB, L.ldg, 16, 32, CU_TENSOR_MAP_SWIZZLE_32B);
         make_map_gen(&g.m_dz, L.dZ + d * G4, false, G4, TB, L.ld_dz, 16, 32, CU_TENSOR_MAP_SWIZZLE_32B);
+        g.dc_rec = L.dc_rec[d];
+        g.c = L.c + d * H;
         g.kb = G4 / kBK;
     }
     p.B = B; p.H = H; p.T = T; p.m_tiles = m_tiles; p.n_tiles = n_tiles; p.units = units; p.kbh = G4 / kBK / kq;
+    p.ldc = L.ldc;
     p.sk_scratch = sk_scratch; p.sk_flags = sk_flags; p.dep = dep; p.exit_ctr = exit_ctr;
     p.epi_skip = knobs().export_dbg;
     p.trace = trace_take();
