@@ -30,6 +30,11 @@ constexpr int BM = 128, BK = 64;
 struct TcParams {
     CUtensorMap ta[2];
     CUtensorMap tb[2];
+    // MN-major operands as 3-D views {64, K, M/64 (or N/64)} (when the extent is a multiple of 64):
+    // a CTA's two 64-wide blocks of a k-block in ONE TMA op (see tma_load_3d_2sm)
+    CUtensorMap ta3[2];
+    CUtensorMap tb3[2];
+    int a3d, b3d;
     int kblocks[2];
     int nseg;
     int M, N;
@@ -207,11 +212,17 @@ struct GenTraits : tc::TraitsBase {
         const CUtensorMap* a[2];
         const CUtensorMap* b[2];
         int m0, nb, kbs;
+        bool a3, b3;  // MN-major A / B through the 3-D views (one op for the CTA's two 64-wide blocks)
     };
     __device__ static LoadCtx load_ctx(const TcParams& p, int tile, uint32_t rank) {
         constexpr int SUBN = BN > 256 ? 256 : BN;
         LoadCtx c;
-        for (int s = 0; s < 2; ++s) { c.a[s] = &p.ta[s]; c.b[s] = &p.tb[s]; }
+        c.a3 = AMN && p.a3d;
+        c.b3 = BMN && SUBN == 256 && p.b3d;
+        for (int s = 0; s < 2; ++s) {
+            c.a[s] = c.a3 ? &p.ta3[s] : &p.ta[s];
+            c.b[s] = c.b3 ? &p.tb3[s] : &p.tb[s];
+        }
         c.m0 = (tile % p.m_tiles) * 2 * BM + BM * static_cast<int>(rank);
         c.nb = (tile / p.m_tiles) * BN + (SUBN / 2) * static_cast<int>(rank);
         c.kbs = p.kblocks[0];
@@ -221,8 +232,12 @@ struct GenTraits : tc::TraitsBase {
         const int s = kb < c.kbs ? 0 : 1;
         const int k0 = (kb - s * c.kbs) * BK;
         if (AMN) {
+            if (c.a3) {
+                ptx::tma_load_3d_2sm(sA, c.a[s], bar, 0, k0, c.m0 / 64);
+            } else {
 #pragma unroll
-            for (int j = 0; j < BM / 64; ++j) ptx::tma_load_2d_2sm(sA + j * 64 * BK * 2, c.a[s], bar, c.m0 + 64 * j, k0);
+                for (int j = 0; j < BM / 64; ++j) ptx::tma_load_2d_2sm(sA + j * 64 * BK * 2, c.a[s], bar, c.m0 + 64 * j, k0);
+            }
         } else {
             ptx::tma_load_2d_2sm(sA, c.a[s], bar, k0, c.m0);
         }
@@ -232,8 +247,12 @@ struct GenTraits : tc::TraitsBase {
             const int n0 = c.nb + u * SUBN;
             uint8_t* dst = sB + u * (SUBN / 2) * BK * 2;
             if (BMN) {
+                if (c.b3) {
+                    ptx::tma_load_3d_2sm(dst, c.b[s], bar, 0, k0, n0 / 64);
+                } else {
 #pragma unroll
-                for (int j = 0; j < SUBN / 128; ++j) ptx::tma_load_2d_2sm(dst + j * 64 * BK * 2, c.b[s], bar, n0 + 64 * j, k0);
+                    for (int j = 0; j < SUBN / 128; ++j) ptx::tma_load_2d_2sm(dst + j * 64 * BK * 2, c.b[s], bar, n0 + 64 * j, k0);
+                }
             } else {
                 ptx::tma_load_2d_2sm(dst, c.b[s], bar, k0, n0);
             }
@@ -584,6 +603,20 @@ void make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, 
     AB_CHECK(r == CUDA_SUCCESS, ADPSGD_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
 }
 
+// MN-major bf16 operand [K rows x extent] (pitch ld) as a 3-D view {64, K, extent / 64}: block b of
+// row k at column 64 b; box {64, 64, 2} = a CTA's two 64-wide blocks of one k-block.
+void make_map3_mn(CUtensorMap* m, const void* base, uint64_t extent, uint64_t K, int64_t ld_elems) {
+    AB_CHECK((reinterpret_cast<uintptr_t>(base) & 15) == 0, ADPSGD_E_DIMENSION, "TMA base must be 16B aligned");
+    cuuint64_t dims[3] = {64, K, extent / 64};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld_elems) * 2, 128};
+    cuuint32_t box[3] = {64, 64, 2};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = get_encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    AB_CHECK(r == CUDA_SUCCESS, ADPSGD_E_CUDA, "cuTensorMapEncodeTiled (3-D MN) failed: " + std::to_string(r));
+}
+
 template <class Traits>
 void launch_single(const TcParams& p, cudaStream_t s) {
     auto k = tc::persistent_kernel<Traits, TcParams>;
@@ -799,7 +832,7 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
     }
     key.tail = xb ? g.b_tail : nullptr;
     key.M = g.M; key.N = g.N; key.nseg = g.nseg; key.bn = bn * (pair ? 2 : 1); key.amn = amn; key.bmn = bmn;
-    key.mode = (xtra ? 1 : 0) | (sk ? 2 : 0) | (xb ? 4 : 0);
+    key.mode = (xtra ? 1 : 0) | (sk ? 2 : 0) | (xb ? 4 : 0) | (knobs().no_tma3d ? 8 : 0);
 
     TcParams p;
     {
@@ -818,6 +851,15 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
                 if (bmn) make_map(&p.tb[i], sg.b.ptr, g.N, sg.K, sg.b.ld, BK);
                 else make_map(&p.tb[i], sg.b.ptr, sg.K, g.N, sg.b.ld, pair ? (bn > 256 ? 128 : bn / 2) : bn);
                 p.kblocks[i] = (sg.K + BK - 1) / BK;
+            }
+            // 3-D views of MN-major operands (CTA pairs; same extent as the 2-D maps, whole 64-wide
+            // blocks only, so both views read and zero-fill exactly the same elements)
+            p.a3d = amn && pair && g.M % 64 == 0 && !knobs().no_tma3d;
+            p.b3d = bmn && pair && bn >= 256 && g.N % 64 == 0 && !knobs().no_tma3d;
+            for (int i = 0; i < g.nseg; ++i) {
+                const GemmSeg& sg = g.seg[i];
+                if (p.a3d) make_map3_mn(&p.ta3[i], sg.a.ptr, g.M, sg.K, sg.a.ld);
+                if (p.b3d) make_map3_mn(&p.tb3[i], sg.b.ptr, g.N, sg.K, sg.b.ld);
             }
             if (xb) {
                 make_map(&p.tx, g.b_tail, g.seg[0].K, 16, g.ld_tail, 8);

@@ -32,6 +32,7 @@ Knobs load() {
     k.fwd_u32 = flag("ADPSGD_NO_FWD_U32", true, false);
     k.bwd_u32 = flag("ADPSGD_NO_BWD_U32", true, false);
     k.bwd_kmajor = flag("ADPSGD_BWD_KMAJOR", false, true);
+    k.no_tma3d = flag("ADPSGD_NO_TMA3D", false, true);
     k.unfused_ce = flag("ADPSGD_UNFUSED_CE", false, true);
     k.fused_update = flag("ADPSGD_FUSED_UPDATE", false, true);
     k.bwd_kq4 = flag("ADPSGD_BWD_KQ4", false, true);

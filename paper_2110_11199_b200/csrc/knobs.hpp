@@ -34,6 +34,7 @@ struct Knobs {
     int split_max = 4;         // ADPSGD_SPLIT_MAX=n: K slices of the one-wave split-K weight gradients (1: off)
     bool fwd_u32 = true;       // ADPSGD_NO_FWD_U32=1: persistent forward always in 64-unit tiles
     bool bwd_u32 = true;       // ADPSGD_NO_BWD_U32=1: persistent BPTT always with 64 units per CTA
+    bool no_tma3d = false;     // ADPSGD_NO_TMA3D=1: MN-major GEMM operands as two 2-D boxes per k-block (no 3-D views)
     bool bwd_kmajor = false;   // ADPSGD_BWD_KMAJOR=1: 64-unit persistent BPTT reads a K-major W_hh^T (else MN-major W_hh)
     int pitch_align = 64;      // ADPSGD_PITCH_ALIGN=n: activation row pitches (elements) rounded up to n (1: unpadded)
     bool fwd_l2win = false;    // ADPSGD_FWD_L2WIN=1: persisting L2 window over the persistent forward's weights
