@@ -1317,108 +1317,7 @@ void lstm_bwd_step(const LstmBwdDir* dirs, int ndirs, int B, int H, int lddh, in
 }
 
 #ifdef ADPSGD_DBG_PROBE
-// Timing experiments only: the persistent forward's TMA pipeline alone (no MMA, no epilogue, no
-// cross-CTA dependencies) on the layer's real tensor maps, with a minimal CTA pair: both CTAs'
-// loads complete on the leader's full barrier; the leader frees each stage in both CTAs.
-// flags: 1 = free stages by tcgen05.commit (TMEM allocated: 512 columns) instead of remote arrives
-__global__ void __launch_bounds__(192) fwd_probe_kernel(const __grid_constant__ FwdPParams p, int stages, int flags) {
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    __shared__ __align__(8) uint64_t full[8], empty[8];
-    __shared__ uint32_t tslot;
-    using T = FwdPersistT<64>;
-    constexpr int AB = tc::kBM * tc::kBK * 2, BB = 128 * tc::kBK * 2;
-    const uint32_t rank = ptx::cluster_ctarank();
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < stages; ++i) { ptx::mbar_init(&full[i], 1); ptx::mbar_init(&empty[i], 1); }
-        ptx::fence_barrier_init();
-    }
-    if ((flags & 1) && threadIdx.x >= 32 && threadIdx.x < 64) ptx::tmem_alloc_2sm(&tslot, 512);
-    ptx::tc_fence_before();
-    __syncthreads();
-    ptx::cluster_sync();
-    ptx::tc_fence_after();
-    const int nitems = 2 * p.T;
-    if (threadIdx.x == 0) {
-        int st = 0;
-        uint32_t ph = 0;
-        for (int it = 0; it < nitems; ++it) {
-            const T::LoadCtx c = T::load_ctx(p, it, rank);
-            for (int kb = 0; kb < T::kblocks(p, it); ++kb) {
-                ptx::mbar_wait(&empty[st], ph ^ 1);
-                const uint32_t bar0 = ptx::mapa(ptx::smem_u32(&full[st]), 0);
-                if (rank == 0) ptx::mbar_arrive_expect_tx(&full[st], 2 * (AB + BB));
-                T::load2c(c, kb, smem + st * AB, smem + stages * AB + st * BB, bar0);
-                if (++st == stages) { st = 0; ph ^= 1; }
-            }
-        }
-    } else if (threadIdx.x == 32 && rank == 0) {
-        int st = 0;
-        uint32_t ph = 0;
-        for (int it = 0; it < nitems; ++it)
-            for (int kb = 0; kb < T::kblocks(p, it); ++kb) {
-                ptx::mbar_wait(&full[st], ph);
-                if (flags & 1) {
-                    ptx::tc_fence_after();
-                    ptx::mma_commit_2sm(&empty[st], 3);
-                } else {
-                    for (uint32_t r = 0; r < 2; ++r) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&empty[st]), r));
-                }
-                if (++st == stages) { st = 0; ph ^= 1; }
-            }
-    }
-    ptx::tc_fence_before();
-    __syncthreads();
-    ptx::cluster_sync();
-    if ((flags & 1) && threadIdx.x >= 32 && threadIdx.x < 64) ptx::tmem_dealloc_2sm(tslot, 512);
-}
-// ADPSGD_DBG_PROBE_STAGES=n: variants (flags | threads | smem | PDL), each timed best-of-4
-void fwd_probe(const FwdPParams& p, int units, cudaStream_t s) {
-    const char* e = std::getenv("ADPSGD_DBG_PROBE_STAGES");
-    const int stages = e ? std::atoi(e) : 4;
-    constexpr int SB = tc::kBM * tc::kBK * 2 + 128 * tc::kBK * 2;
-    static bool attr = false;
-    if (!attr) {
-        AB_CUDA(cudaFuncSetAttribute(fwd_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-        attr = true;
-    }
-    struct V { int flags, threads, smem; bool pdl; const char* name; };
-    const V vs[] = {{0, 64, stages * SB + 1024, false, "base"},
-                    {1, 64, stages * SB + 1024, false, "commit+tmem512"},
-                    {1, 192, stages * SB + 1024, false, "+192 threads"},
-                    {1, 192, 220 * 1024, false, "+220KB smem"},
-                    {1, 192, 220 * 1024, true, "+PDL"}};
-    for (const V& v : vs) {
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(2 * units);
-        cfg.blockDim = dim3(v.threads);
-        cfg.dynamicSmemBytes = v.smem;
-        cfg.stream = s;
-        cudaLaunchAttribute a[2];
-        a[0].id = cudaLaunchAttributeClusterDimension;
-        a[0].val.clusterDim.x = 2; a[0].val.clusterDim.y = 1; a[0].val.clusterDim.z = 1;
-        a[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        a[1].val.programmaticStreamSerializationAllowed = 1;
-        cfg.attrs = a;
-        cfg.numAttrs = v.pdl ? 2 : 1;
-        cudaEvent_t e0, e1;
-        AB_CUDA(cudaEventCreate(&e0));
-        AB_CUDA(cudaEventCreate(&e1));
-        float best = 1e30f;
-        for (int rep = 0; rep < 5; ++rep) {
-            AB_CUDA(cudaEventRecord(e0, s));
-            AB_CUDA(cudaLaunchKernelEx(&cfg, fwd_probe_kernel, p, stages, v.flags));
-            AB_CUDA(cudaEventRecord(e1, s));
-            AB_CUDA(cudaEventSynchronize(e1));
-            float ms;
-            AB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-            if (rep > 0) best = ms < best ? ms : best;
-        }
-        std::fprintf(stderr, "[fwd_probe] K=%d stages=%d %-16s %.1f us per launch\n", p.kbx * 64, stages, v.name, best * 1e3);
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
-    }
-}
+#include "dbg_fwd_probe.inc"  // timing experiments only
 #endif
 
 bool lstm_fwd_layer_persistent(const LstmFwdLayer& L, int ndirs, int B, int H, int T, cudaStream_t s, unsigned int* dep,
