@@ -44,7 +44,10 @@ def _run(bf16, M, N, K, amn, bmn, c_bf16=False, accumulate=False, bias=False, al
 
 @pytest.mark.parametrize("amn,bmn", list(itertools.product([0, 1], [0, 1])))
 @pytest.mark.parametrize("shape", [(128, 256, 64), (256, 512, 320), (300, 200, 136), (1024, 4096, 1024),
-                                   (64, 1000, 264), (4096, 264, 2048)])
+                                   (64, 1000, 264), (4096, 264, 2048),
+                                   # MN-major operands through the 3-D tensor-map views (extent % 64 == 0) with a
+                                   # partial last n-tile and a ragged K (zero-filled blocks / rows)
+                                   (512, 320, 1000), (768, 576, 4160)])
 def test_tc_gemm_majorness_and_shapes(amn, bmn, shape):
     M, N, K = shape
     if (amn and M % 8) or (bmn and N % 8):
