@@ -21,6 +21,8 @@ cap dgrad "GenTraits<.int.512" 0
 cap update "sdpsgd_kernel" 0
 cap gather "gather_kernel" 1
 python bench.py > gpurun_out/${tag}_bench.log 2>&1
-python tools/ingress_probe.py > gpurun_out/${tag}_ingress.txt 2>&1
+python tools/ingress_probe.py > gpurun_out/${tag}_ingress.txt 2>&1  # (its A operand is DRAM-streamed: see DESIGN 6)
+[ -x tools/tma_mc_probe ] && timeout 120 tools/tma_mc_probe 32 40 > gpurun_out/${tag}_tma_probe.txt 2>&1
+[ -x tools/mma_rate ] && timeout 120 tools/mma_rate > gpurun_out/${tag}_mma_rate.txt 2>&1
 tail -1 gpurun_out/${tag}_bench.log > gpurun_out/${tag}_bench.json
 ls -la gpurun_out | grep $tag
