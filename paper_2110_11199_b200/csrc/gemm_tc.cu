@@ -812,8 +812,11 @@ void gemm_tc(const GemmArgs& g, cudaStream_t s) {
                wsp.flag_count >= static_cast<size_t>(npairs) * 2;
     };
     const bool wide_wgrad = knobs().wide_gemm && amn && bmn && !g.c_bf16 && !g.extra && gemm_wgrad_wide(g.M, g.N);
+    // 256 x 512 tiles have one accumulator stage (the epilogue is exposed once per tile): worth it
+    // from ~3 waves of tiles on (H = 1024 dgrads: 4.5 waves, -6 % vs 256-wide; H = 512: 2.3 waves,
+    // +6 %)
     const bool wide = (!xtra && wide_wgrad) || (!xtra && knobs().wide_gemm && bn0 == 256 && g.N >= 1024 && g.N % 512 == 0 &&
-                                     (m_tiles * (g.N / 512) >= npairs || knobs().force_ext) && sk_ok(512));
+                                     (m_tiles * (g.N / 512) >= 3 * npairs || knobs().force_ext) && sk_ok(512));
     const int bn = wide ? 512 : (xb ? 256 : bn0);
     const int tiles = m_tiles * ((n_eff + bn - 1) / bn);
     const bool sk = !wide_wgrad && sk_ok(bn);
