@@ -2,6 +2,8 @@
 // library shares whichever libnccl.so.2 the process already loaded (torch's).
 #include "comm.hpp"
 
+#include <cstdlib>
+
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -82,6 +84,11 @@ Comm::Comm(Ctx& c, int r, int w, const void* id128) : rank(r), world(w), D_(c.D)
         return;
     }
     forced = w == 1 && knobs().comm_force;
+    // The D1D weight allreduce runs concurrently with the persistent recurrent kernels, which need
+    // all their 2 x 64 CTAs co-resident (cross-CTA step counters) and leave 148 - 128 = 20 SMs free:
+    // cap NCCL's CTAs so its kernel fits beside them instead of holding SMs the forward is waiting
+    // for (16 CTAs move the 0.58 GB allreduce well inside the forward). A user setting wins.
+    if (!std::getenv("NCCL_MAX_CTAS")) setenv("NCCL_MAX_CTAS", "16", 0);
     ncclUniqueId id;
     std::memcpy(&id, id128, sizeof(id));
     ncclComm_t comm;
