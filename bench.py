@@ -463,7 +463,8 @@ def run_ours(a):
     cs = line["clocks"]
     if cs.get("energy_j"):  # board energy of the timed region (power-capped part: J per step sets the step time)
         line["energy"] = {"j_per_step": cs["energy_j"] / a.steps, "power_w_avg": cs["power_w_avg"],
-                          "frames_per_joule": a.batch * T_UNROLL * a.steps / cs["energy_j"], "source": "NVML total energy counter"}
+                          "frames_per_joule": a.batch * T_UNROLL * a.steps / cs["energy_j"],
+                          "source": "NVML total energy counter over the timed region (coarse for a sub-second region)"}
     print(json.dumps(line), flush=True)
     g.close()
 
