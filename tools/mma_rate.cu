@@ -67,7 +67,26 @@ __global__ void __launch_bounds__(128) mma_rate(int N, int b_mn, int iters, unsi
         const long long t1 = clock64();
         out[blockIdx.x / 2] = static_cast<unsigned long long>(t1 - t0);
     }
-    if (load && threadIdx.x == 64) {  // streaming loader (both CTAs) until the pair's MMAs are done
+    if (load == 2 && threadIdx.x >= 64) {  // LSU smem traffic (warps 2-3): 16-B stores + loads over 64 KB until done
+        const uint32_t base = ptx::smem_u32(sm + 32768);
+        uint32_t acc = 0, it = 0;
+        const long long t0 = clock64();
+        for (;; ++it) {
+            const uint32_t off = ((it * 64 + (threadIdx.x - 64)) * 16) & 0xFFFF;
+            ptx::st_shared_v4(base + off, it, acc, it, acc);
+            const float4 v = ptx::ld_shared_v4f(base + (off ^ 0x8000));
+            acc += __float_as_uint(v.x);
+            if ((it & 63) == 0) {
+                uint32_t fin;
+                asm volatile("{\n.reg .pred P;\nmbarrier.test_wait.parity.shared::cta.b64 P, [%1], 0;\nselp.u32 %0, 1, 0, P;\n}\n"
+                             : "=r"(fin) : "r"(ptx::smem_u32(&done)) : "memory");
+                if (fin) break;
+            }
+        }
+        const long long t1 = clock64();
+        if (threadIdx.x == 64) loaded[blockIdx.x] = static_cast<unsigned long long>(it + 1) * 64 * 32 * 1000 / static_cast<unsigned long long>(t1 - t0) + (acc == 12345u);
+    }
+    if (load == 1 && threadIdx.x == 64) {  // streaming loader (both CTAs) until the pair's MMAs are done
         uint8_t* ring = sm + 32768;
         unsigned long long n = 0;
         uint32_t ph[NSLOT] = {};
@@ -112,8 +131,8 @@ int main() {
     CK(cudaMemset(src, 0, 160ull * NSLOT * 16384));
     CK(cudaFuncSetAttribute(mma_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, (33 + 16 * NSLOT) * 1024));
     const int iters = 200000;
-    for (int rnd : {0, 1})
-    for (int load : {0})
+    for (int rnd : {1})
+    for (int load : {0, 2})
     for (int pairs : {1, 74})
         for (int b_mn : {0})
             for (int N : {128, 256}) {
