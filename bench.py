@@ -388,7 +388,7 @@ def run_ours(a):
             pick = lambda pat: next((v for k, v in kc.items() if pat in k), None)  # noqa: E731
             tensor_pipe = {"source": "profiles/tensor_counters.json (ncu sm__ops_path_tensor_op_utchmma_src_bf16_dst_fp32)",
                            "fwd_recurrent_pct": (pick("FwdPersistT<64>") or {}).get("dense_tensor_util_pct"),
-                           "bptt_recurrent_pct": (pick("BwdPersistTraits<2, 64>") or {}).get("dense_tensor_util_pct"),
+                           "bptt_recurrent_pct": (pick("BwdPersistTraits<2, 64") or {}).get("dense_tensor_util_pct"),
                            "wgrad_pct": (pick("GenTraits<256, 1, 1, 0, 0, 0, 0>") or {}).get("dense_tensor_util_pct"),
                            "dgrad_pct": (pick("GenTraits<512, 0, 1, 0, 0, 1, 0>") or {}).get("dense_tensor_util_pct"),
                            "target_pct": 50}
