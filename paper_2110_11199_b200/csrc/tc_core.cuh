@@ -27,7 +27,7 @@ __device__ __forceinline__ void trace(unsigned long long* buf, int ev) {
     }
 }
 
-// Per-item timeline (tools/trace_items.py), after the block above: [cta][item < 64][8 events]
+// Per-item timeline (tools/trace_items.py), after the block above: [cta][item < 64][12 slots]
 // 0 producer: first load issued, 1 producer: mid-item dependency passed, 2 producer: last load issued,
 // 3 MMA: first stage landed, 4 MMA: last MMA committed, 5 epilogue: accumulator full, 6 epilogue done,
 // 7 producer: item reached (before its cross-CTA dependency wait); durations (ns, summed over the
