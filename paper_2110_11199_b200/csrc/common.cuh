@@ -10,6 +10,11 @@
 
 #include "adpsgd_b200.h"
 
+// L2 sector promotion of every tcgen05 operand / epilogue tensor map (A/B builds may override)
+#ifndef ADPSGD_L2PROMO
+#define ADPSGD_L2PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+#endif
+
 namespace ab {
 
 // Status-carrying exception used inside the library; converted to adpsgd_status at the

@@ -36,7 +36,7 @@ void make_map_gen(CUtensorMap* m, const void* base, bool f32, uint64_t inner, ui
     cuuint32_t es[2] = {1, 1};
     CUresult r = get_encode_fn()(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
                                  const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
-                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                                 ADPSGD_L2PROMO, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     AB_CHECK(r == CUDA_SUCCESS, ADPSGD_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
 }
 
@@ -52,7 +52,7 @@ void make_map_3d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t oute
     cuuint32_t box[3] = {64, box1, box2};
     cuuint32_t es[3] = {1, 1, 1};
     CUresult r = get_encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
-                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, ADPSGD_L2PROMO,
                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     AB_CHECK(r == CUDA_SUCCESS, ADPSGD_E_CUDA, "cuTensorMapEncodeTiled (3-D) failed: " + std::to_string(r));
 }

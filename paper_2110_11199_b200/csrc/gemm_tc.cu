@@ -599,7 +599,7 @@ void make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, 
     cuuint32_t es[2] = {1, 1};
     CUresult r = get_encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                             ADPSGD_L2PROMO, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     AB_CHECK(r == CUDA_SUCCESS, ADPSGD_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
 }
 
@@ -613,7 +613,7 @@ void make_map3_mn(CUtensorMap* m, const void* base, uint64_t extent, uint64_t K,
     cuuint32_t es[3] = {1, 1, 1};
     CUresult r = get_encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
                                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                                 ADPSGD_L2PROMO, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     AB_CHECK(r == CUDA_SUCCESS, ADPSGD_E_CUDA, "cuTensorMapEncodeTiled (3-D MN) failed: " + std::to_string(r));
 }
 
